@@ -1,0 +1,543 @@
+"""Pin the CPU oracle (oracle/bm_oracle.cpp) to the reference's own known-answer
+tests, golden values and tolerances.  CPU only.
+
+Each test names the reference test it restates (paths relative to proj/).
+Independent checkers use scipy / numpy, never the oracle's own code path.
+"""
+import math
+
+import numpy as np
+import pytest
+from scipy import special
+
+from oracle import bmo
+
+PI = math.pi
+
+
+# ------------------------------------------------------------- philox (test_volio.cpp:34-59)
+def test_philox_known_answer_and_streams():
+    z = bmo.philox_round10([0, 0, 0, 0], [0, 0])
+    assert [int(x) for x in z] == [0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8]
+    a = bmo.philox_u32(42, 0, 100)
+    b = bmo.philox_u32(42, 0, 100)
+    c = bmo.philox_u32(42, 1, 100)
+    assert np.array_equal(a, b) and not np.array_equal(a, c)
+    g = bmo.philox_gaussian(7, 3, 200000)
+    assert abs(g.mean()) < 0.01
+    assert abs((g * g).mean() - 1.0) < 0.02
+
+
+# ------------------------------------------------------------- bessel (test_basis.cpp:34-95)
+def test_bessel_roots_closed_forms_and_bisection():
+    assert bmo.bessel_root(0, 1) == pytest.approx(PI, rel=1e-14)
+    assert bmo.bessel_root(0, 3) == pytest.approx(3 * PI, rel=1e-14)
+    lo, hi = PI, 2 * PI
+    for _ in range(200):
+        mid = 0.5 * (lo + hi)
+        if (special.spherical_jn(1, lo) > 0) == (special.spherical_jn(1, mid) > 0):
+            lo = mid
+        else:
+            hi = mid
+    assert bmo.bessel_root(1, 1) == pytest.approx(0.5 * (lo + hi), rel=1e-12)
+    assert bmo.bessel_root(1, 1) == pytest.approx(4.493409457909064, rel=1e-13)
+
+
+@pytest.mark.parametrize("l", [0, 1, 3, 10, 25, 42])
+def test_bessel_root_residuals(l):
+    prev = 0.0
+    for k in range(1, 6):
+        r = bmo.bessel_root(l, k)
+        assert abs(special.spherical_jn(l, r)) < 1e-12
+        assert r > prev
+        if k > 1:  # no interior sign change: r is the next root after prev
+            xs = np.linspace(prev + 1e-7, r - 1e-7, 3001)
+            s = np.sign(special.spherical_jn(l, xs))
+            assert np.all(s == s[0])
+        prev = r
+
+
+def test_radial_norm_closed_form_and_quadrature():
+    spec = bmo.Spec(2, 12.0)
+    assert spec.norm(0, 1) == pytest.approx(math.sqrt(2) * PI, rel=1e-12)
+    from scipy.integrate import quad
+    for l, k in [(0, 1), (1, 1), (2, 1)]:
+        lam = spec.root(l, k)
+        c = spec.norm(l, k)
+        val, _ = quad(lambda r: (c * special.spherical_jn(l, lam * r) * r) ** 2, 0, 1,
+                      epsabs=1e-13, epsrel=1e-12)
+        assert val == pytest.approx(1.0, rel=1e-8)
+
+
+def test_sph_jl_against_scipy():
+    for l in (0, 1, 2, 5, 16, 30, 42):
+        for x in (1e-7, 0.3, 2.0, 7.5, 20.0, 55.0, 130.0):
+            ref = special.spherical_jn(l, x)
+            assert abs(bmo.sph_jl(l, x) - ref) <= 1e-12 * max(1.0, abs(ref)) + 1e-300
+
+
+# ------------------------------------------------------------- harmonics (test_basis.cpp:97-137)
+def test_spherical_harmonics_pinned_and_conjugation():
+    y00 = bmo.spherical_harmonic(0, 0, 0.7, 1.3)
+    assert y00.real == pytest.approx(0.28209479177387814, rel=1e-14) and y00.imag == 0.0
+    assert bmo.spherical_harmonic(1, 0, 0.0, 0.0).real == pytest.approx(math.sqrt(3 / (4 * PI)),
+                                                                        rel=1e-14)
+    rng = np.random.default_rng(11)
+    for _ in range(20):
+        l = int(rng.integers(0, 9))
+        m = int(rng.integers(0, l + 1))
+        th, ph = rng.uniform(0, PI), rng.uniform(0, 2 * PI)
+        a = bmo.spherical_harmonic(l, -m, th, ph)
+        b = np.conj(bmo.spherical_harmonic(l, m, th, ph))
+        assert abs(a - (-b if m % 2 else b)) < 1e-13
+        # scipy's sph_harm_y(l, m, theta, phi) uses the same Condon-Shortley convention
+        ref = special.sph_harm_y(l, m, th, ph)
+        assert abs(bmo.spherical_harmonic(l, m, th, ph) - ref) < 1e-12
+
+
+def test_gauss_legendre_against_numpy():
+    for n in (1, 2, 7, 34, 50):
+        x, w = bmo.gauss_legendre(n)
+        xr, wr = np.polynomial.legendre.leggauss(n)
+        assert np.allclose(x, xr, atol=1e-14) and np.allclose(w, wr, atol=1e-14)
+
+
+# ------------------------------------------------------------- build_spec (test_basis.cpp:139-191)
+def test_build_spec_retention_rules():
+    s0 = bmo.Spec(0, 7.0)
+    assert s0.radial_count(0) == 2 and s0.coeff_count == 2
+    s1 = bmo.Spec(1, 4.0)
+    assert s1.radial_count(0) == 1 and s1.radial_count(1) == 0
+    with pytest.raises(ValueError):
+        bmo.Spec(1, 3.0)
+
+
+def _enumerate_roots(l, cut):
+    step = 0.25
+    xs = np.arange(0.5, cut + 2.0, step)  # (first root > pi; avoids scipy underflow sign noise)
+    f = special.spherical_jn(l, xs)
+    roots = []
+    for i in range(1, len(xs)):
+        if (f[i] > 0) != (f[i - 1] > 0):
+            lo, hi = xs[i - 1], xs[i]
+            flo = f[i - 1]
+            for _ in range(100):
+                mid = 0.5 * (lo + hi)
+                if (special.spherical_jn(l, mid) > 0) == (flo > 0):
+                    lo = mid
+                else:
+                    hi = mid
+            roots.append(0.5 * (lo + hi))
+    while roots and roots[-1] > cut + 1e-9:
+        roots.pop()
+    return roots
+
+
+def test_build_spec_brute_force_l42():
+    cut = 32 * PI
+    s = bmo.Spec(42, cut)
+    total = 0
+    for l in range(43):
+        ref = _enumerate_roots(l, cut)
+        assert s.radial_count(l) == len(ref)
+        for k in range(1, s.radial_count(l) + 1):
+            assert s.root(l, k) == pytest.approx(ref[k - 1], rel=1e-10)
+            assert s.norm(l, k) > 0
+        total += s.radial_count(l) * (2 * l + 1)
+    assert s.coeff_count == total
+
+
+@pytest.mark.parametrize("L,C", [(8, 408), (16, 3050), (20, 5886), (24, 10089)])
+def test_config_coefficient_counts(L, C):
+    """SURVEY §8 size table: lambda_cut = K*pi with K = L."""
+    assert bmo.Spec(L, L * PI).coeff_count == C
+
+
+def test_default_lambda_cut_caps_coefficients():
+    for n, L in ((32, 8), (48, 16), (64, 24)):
+        cut = bmo.default_lambda_cut(n, L)
+        assert cut <= PI * n / 2 + 1e-12
+        assert bmo.Spec(L, cut).coeff_count <= n ** 3 // 4
+
+
+# ------------------------------------------------------------- expand (test_basis.cpp:193-239)
+def smooth_blob_volume(n, seed):
+    """proj/tests/oracles.hpp:76-109 (LCG-seeded smooth blobs), restated."""
+    mask = (1 << 64) - 1
+    state = (seed * 6364136223846793005 + 1442695040888963407) & mask
+
+    def unit():
+        nonlocal state
+        state = (state * 6364136223846793005 + 1442695040888963407) & mask
+        return (state >> 11) * 2.0 ** -53
+
+    blobs = []
+    for _ in range(4):
+        r = 0.45 * np.cbrt(unit())
+        th = math.acos(2 * unit() - 1)
+        ph = 2 * PI * unit()
+        blobs.append((r * math.sin(th) * math.cos(ph), r * math.sin(th) * math.sin(ph),
+                      r * math.cos(th), 0.10 + 0.06 * unit(),
+                      (-1.0 if unit() < 0.5 else 1.0) * (0.5 + 0.5 * unit())))
+    c = (np.arange(n) - n // 2) * (2.0 / n)
+    z, y, x = np.meshgrid(c, c, c, indexing="ij")
+    v = np.zeros((n, n, n))
+    for bx, by, bz, s, a in blobs:
+        v += a * np.exp(-0.5 * ((x - bx) ** 2 + (y - by) ** 2 + (z - bz) ** 2) / (s * s))
+    return v
+
+
+def test_expand_zero_and_unit_mode_round_trip():
+    spec = bmo.Spec(4, 9.0)
+    assert np.all(bmo.expand(np.zeros((32, 32, 32)), spec) == 0)
+    for (k, l, m) in [(1, 0, 0), (1, 2, 1), (1, 3, -2)]:
+        unit = np.zeros(spec.coeff_count, dtype=complex)
+        unit[spec.index_of(k, l, m)] = 1.0
+        partner = -1.0 if m % 2 else 1.0
+        if m != 0:
+            unit[spec.index_of(k, l, -m)] = partner
+        v = bmo.synthesize(unit, spec, 160)
+        back = bmo.expand(v, spec)
+        for ll in range(spec.l_max + 1):
+            for kk in range(1, spec.radial_count(ll) + 1):
+                for mm in range(-ll, ll + 1):
+                    c = back[spec.index_of(kk, ll, mm)]
+                    if (kk, ll, mm) == (k, l, m):
+                        assert abs(c - 1) < 5e-3
+                    elif m != 0 and (kk, ll, mm) == (k, l, -m):
+                        assert abs(c - partner) < 5e-3
+                    else:
+                        assert abs(c) < 1e-4
+
+
+def test_expand_parseval():
+    n = 64
+    v = smooth_blob_volume(n, 7)
+    spec = bmo.Spec(24, bmo.default_lambda_cut(n, 24))
+    e = bmo.expand(v, spec)
+    c = (np.arange(n) - n // 2) * (2.0 / n)
+    z, y, x = np.meshgrid(c, c, c, indexing="ij")
+    inside = x * x + y * y + z * z < 1.0
+    grid_energy = float((v[inside] ** 2).sum() * (2.0 / n) ** 3)
+    assert float(np.sum(np.abs(e) ** 2)) == pytest.approx(grid_energy, rel=0.02)
+
+
+def test_expand_reality_symmetry():
+    spec = bmo.Spec(8, 8 * PI)
+    e = bmo.expand(smooth_blob_volume(32, 3), spec)
+    for l in range(spec.l_max + 1):
+        for k in range(1, spec.radial_count(l) + 1):
+            assert e[spec.index_of(k, l, 0)].imag == 0.0
+            for m in range(1, l + 1):
+                want = np.conj(e[spec.index_of(k, l, m)]) * (-1) ** m
+                assert abs(e[spec.index_of(k, l, -m)] - want) < 1e-15
+
+
+# ------------------------------------------------------------- little-d (test_steer.cpp:42-67)
+def wigner_d_sum(l, m, mp, beta):
+    c, s = math.cos(beta / 2), math.sin(beta / 2)
+    f = math.factorial
+    pref = math.sqrt(f(l + m) * f(l - m) * f(l + mp) * f(l - mp))
+    tot = 0.0
+    for k in range(max(0, m - mp), min(l + m, l - mp) + 1):
+        den = f(l + m - k) * f(k) * f(mp - m + k) * f(l - mp - k)
+        term = c ** (2 * l + m - mp - 2 * k) * s ** (mp - m + 2 * k) / den
+        tot += -term if k % 2 else term
+    return pref * tot
+
+
+def test_little_d_pinned_and_factorial_sum():
+    assert bmo.little_d(0, 1.234)[0][0] == pytest.approx(1.0)
+    d1 = bmo.little_d(1, PI / 3)[0]
+    assert bmo.xi_block(d1, 1)[1, 1] == pytest.approx(math.cos(PI / 3), rel=1e-14)  # (m, m') = (0, 0)
+    rng = np.random.default_rng(31)
+    for l in (2, 3, 5, 8, 10):
+        b = rng.uniform(0.05, PI - 0.05)
+        blk = bmo.xi_block(bmo.little_d(l, b)[0], l)
+        for m in range(-l, l + 1):
+            for mp in range(-l, l + 1):
+                assert blk[m + l, mp + l] == pytest.approx(wigner_d_sum(l, m, mp, b), rel=1e-10,
+                                                           abs=1e-14)
+
+
+@pytest.mark.parametrize("l", [15, 30, 42])
+def test_little_d_orthogonality(l):
+    blk = bmo.xi_block(bmo.little_d(l, 1.1)[0], l)
+    assert np.abs(blk @ blk.T - np.eye(2 * l + 1)).max() < 1e-10
+
+
+def test_little_d_derivatives_vs_finite_differences():
+    L, b, h = 12, 0.9, 1e-5
+    v, d1, d2 = bmo.little_d(L, b, 2)
+    vp, d1p = bmo.little_d(L, b + h, 1)
+    vm, d1m = bmo.little_d(L, b - h, 1)
+    assert np.abs(d1 - (vp - vm) / (2 * h)).max() < 1e-6
+    assert np.abs(d2 - (d1p - d1m) / (2 * h)).max() < 1e-5
+
+
+# ------------------------------------------------------------- wigner-D (test_steer.cpp:69-93)
+def test_wigner_D_identity_unitarity_homomorphism():
+    D = bmo.wigner_D(6, [1, 0, 0, 0])
+    for l in range(7):
+        assert np.abs(bmo.xi_block(D, l) - np.eye(2 * l + 1)).max() < 1e-12
+    L = 42
+    for t in range(3):
+        g = bmo.haar_rotation(32, t)
+        D = bmo.wigner_D(L, g)
+        for l in (1, 7, 20, 42):
+            blk = bmo.xi_block(D, l)
+            assert np.abs(blk @ blk.conj().T - np.eye(2 * l + 1)).max() < 1e-10
+    for t in range(3):
+        g1 = bmo.haar_rotation(33, t)
+        g2 = bmo.haar_rotation(34, t)
+        g12 = quat_mul(g1, g2)
+        a, b, c = bmo.wigner_D(L, g1), bmo.wigner_D(L, g2), bmo.wigner_D(L, g12)
+        for l in (1, 3, 13, 42):
+            assert np.abs(bmo.xi_block(a, l) @ bmo.xi_block(b, l) - bmo.xi_block(c, l)).max() < 1e-9
+
+
+def quat_mul(a, b):
+    w1, x1, y1, z1 = a
+    w2, x2, y2, z2 = b
+    return np.array([w1 * w2 - x1 * x2 - y1 * y2 - z1 * z2, w1 * x2 + x1 * w2 + y1 * z2 - z1 * y2,
+                     w1 * y2 - x1 * z2 + y1 * w2 + z1 * x2, w1 * z2 + x1 * y2 - y1 * x2 + z1 * w2])
+
+
+def test_rotation_euler_round_trip_and_geodesic():
+    rng = np.random.default_rng(5)
+    for t in range(50):
+        q = bmo.haar_rotation(77, t)
+        e = bmo.euler_zyz(q)
+        q2 = bmo.from_euler_zyz(*e)
+        assert bmo.geodesic_degrees(q, q2) < 1e-6
+        assert 0 <= e[1] <= PI
+    a = bmo.from_euler_zyz(0.1, 0.2, 0.3)
+    b = bmo.from_euler_zyz(0.1, 0.2, 0.3 + math.radians(10))
+    assert bmo.geodesic_degrees(a, b) == pytest.approx(10.0, rel=1e-9)
+
+
+# ------------------------------------------------------------- xi / correlation (test_xcorr.cpp)
+@pytest.fixture(scope="module")
+def xfix():
+    """test_xcorr.cpp:19-42 fixture: phantom -> expand -> xi (n=48, l_max=10)."""
+    n, L, seed = 48, 10, 1234
+    q = bmo.haar_rotation(seed, 17)
+    t, s, _, _ = bmo.make_phantom(n=n, blobs=4, seed=seed, quat=q, shift=(0, 0, 0))
+    spec = bmo.Spec(L, bmo.default_lambda_cut(n, L))
+    th = bmo.expand(t, spec)
+    fh = bmo.expand(s, spec)
+    xi = bmo.xi_coefficients(th, fh, spec)
+    return dict(spec=spec, th=th, fh=fh, xi=xi, L=L)
+
+
+def test_xi_self_correlation_and_zero(xfix):
+    spec, th = xfix["spec"], xfix["th"]
+    self_xi = bmo.xi_coefficients(th, th, spec)
+    val = bmo.correlation_derivatives(self_xi, spec.l_max, [0, 0, 0], spec.l_max, 0).value
+    assert val == pytest.approx(float(np.sum(np.abs(th) ** 2)), rel=1e-12)
+    z = bmo.xi_coefficients(np.zeros_like(th), xfix["fh"], spec)
+    assert np.all(z == 0)
+
+
+def test_xi_equals_steering_inner_product(xfix):
+    spec, th, fh, xi, L = xfix["spec"], xfix["th"], xfix["fh"], xfix["xi"], xfix["L"]
+    for t in range(10):
+        g = bmo.haar_rotation(9, t)
+        rf = bmo.rotate_expansion(fh, spec, g)
+        e = bmo.euler_zyz(g)
+        for l_cut in (0, 3, L):
+            sel = np.array([l <= l_cut for l in range(L + 1)
+                            for _ in range(spec.radial_count(l) * (2 * l + 1))])
+            direct = np.sum(np.conj(th[sel]) * rf[sel])
+            d = bmo.correlation_derivatives(xi, L, e, l_cut, 0)
+            via = complex(d.value, d.imag)
+            assert abs(via - direct) <= 1e-9 * max(1.0, abs(direct))
+
+
+def test_band_additivity_and_imag_diagnostic(xfix):
+    xi, L = xfix["xi"], xfix["L"]
+    g = bmo.haar_rotation(10, 5)
+    e = bmo.euler_zyz(g)
+    D = bmo.wigner_D(L, g)
+    for l in range(1, L + 1):
+        delta = (bmo.correlation_derivatives(xi, L, e, l, 0).value -
+                 bmo.correlation_derivatives(xi, L, e, l - 1, 0).value)
+        blk = np.sum(bmo.xi_block(xi, l) * bmo.xi_block(D, l)).real
+        assert delta == pytest.approx(blk, rel=1e-9, abs=1e-12)
+    full = bmo.correlation_derivatives(xi, L, e, L, 0)
+    assert abs(full.imag) < 1e-8 * max(1.0, abs(full.value))
+
+
+def test_gradient_hessian_vs_finite_differences(xfix):
+    xi, L = xfix["xi"], xfix["L"]
+    for t in range(10):
+        e = bmo.euler_zyz(bmo.haar_rotation(13, t))
+        e[1] = min(max(e[1], 0.2), PI - 0.2)
+        d = bmo.correlation_derivatives(xi, L, e, L, 2)
+        f = lambda a: bmo.correlation_derivatives(xi, L, a, L, 0).value
+        scale = max(1e-12, np.abs(d.grad).max())
+        for ax in range(3):
+            hp, hm = e.copy(), e.copy()
+            hp[ax] += 1e-5
+            hm[ax] -= 1e-5
+            fd = (f(hp) - f(hm)) / 2e-5
+            assert abs(d.grad[ax] - fd) / scale < 1e-5
+        assert np.abs(d.hess - d.hess.T).max() < 1e-8
+        hs = max(1e-12, np.abs(d.hess).max())
+        for ax in range(3):
+            for ax2 in range(3):
+                hp, hm = e.copy(), e.copy()
+                hp[ax2] += 1e-4
+                hm[ax2] -= 1e-4
+                fd = (bmo.correlation_derivatives(xi, L, hp, L, 1).grad[ax] -
+                      bmo.correlation_derivatives(xi, L, hm, L, 1).grad[ax]) / 2e-4
+                assert abs(d.hess[ax, ax2] - fd) / hs < 1e-4
+
+
+def test_xi_compose_right_identity(xfix):
+    xi, L = xfix["xi"], xfix["L"]
+    a = bmo.haar_rotation(3, 3)
+    comp = bmo.xi_compose_right(xi, L, a)
+    for t in range(5):
+        h = bmo.haar_rotation(4, t)
+        v1 = bmo.correlation_derivatives(comp, L, bmo.euler_zyz(h), L, 0).value
+        v2 = bmo.correlation_derivatives(xi, L, bmo.euler_zyz(quat_mul(h, a)), L, 0).value
+        assert v1 == pytest.approx(v2, rel=1e-9, abs=1e-12)
+
+
+# ------------------------------------------------------------- wedge (test_xcorr.cpp:250-429)
+def test_wedge_kept_fraction_and_profile():
+    assert bmo.wedge_kept_fraction(32, 90.0) == 1.0
+    n = 64
+    f = np.arange(-n // 2, n // 2)
+    fz, fy, fx = np.meshgrid(f, f, f, indexing="ij")
+    disc = fx * fx + fz * fz <= (n // 2) ** 2
+    keep = np.abs(fz) <= math.tan(math.radians(60)) * np.abs(fx)
+    assert keep[disc].mean() == pytest.approx(2 * 60 / 180, rel=0.02)
+    assert bmo.wedge_keep_profile(32, 60, [1, 0, 0]) == 1.0
+    assert bmo.wedge_keep_profile(32, 60, [0, 0, 1]) == 0.0
+    assert bmo.wedge_keep_profile(32, 60, [0, 0, 0]) == 1.0
+    prev = 1.0
+    for a in np.arange(50, 64.01, 0.5):
+        r = math.radians(a)
+        s = bmo.wedge_keep_profile(32, 60, [math.cos(r), 0, math.sin(r)])
+        assert s <= prev + 1e-12
+        prev = s
+
+
+def test_fft_r2c_matches_numpy():
+    rng = np.random.default_rng(0)
+    for n in (8, 12, 32, 48):
+        v = rng.standard_normal((n, n, n))
+        assert np.abs(bmo.fft_r2c_3d(v) - np.fft.rfftn(v)).max() < 1e-9 * n ** 1.5
+
+
+def test_apply_wedge_projector_properties():
+    t, _, _, _ = bmo.make_phantom(n=32, blobs=3, seed=2024, quat=[1, 0, 0, 0], shift=(0, 0, 0))
+    once = bmo.apply_wedge(t, 60.0)
+    twice = bmo.apply_wedge(once, 60.0)
+    assert np.abs(twice - once).max() < 1e-10
+    assert np.abs(bmo.apply_wedge(t, 90.0) - t).max() < 1e-10
+    # Parseval vs numpy's spectrum (independent DFT)
+    n = 32
+    spec = np.fft.fftn(t)
+    fr = np.fft.fftfreq(n, 1.0 / n)
+    fz, fy, fx = np.meshgrid(fr, fr, fr, indexing="ij")
+    keep = np.abs(fz) <= math.tan(math.radians(60)) * np.abs(fx)
+    keep[0, 0, 0] = True
+    kept = float(np.sum(np.abs(spec[keep]) ** 2)) / n ** 3
+    assert float(np.sum(once ** 2)) == pytest.approx(kept, rel=1e-8)
+    w, _, _, _ = bmo.make_phantom(n=32, blobs=3, seed=2025, quat=[1, 0, 0, 0], shift=(0, 0, 0))
+    assert float(np.sum(once * w)) == pytest.approx(float(np.sum(t * bmo.apply_wedge(w, 60.0))),
+                                                    rel=1e-8)
+    with pytest.raises(ValueError):
+        bmo.apply_wedge(np.zeros((16, 16, 16)), 0.0)
+
+
+def test_taper_zero_is_binary_and_energy_decreases():
+    t, _, _, _ = bmo.make_phantom(n=32, blobs=3, seed=91, quat=[1, 0, 0, 0], shift=(0, 0, 0))
+    sharp = bmo.apply_wedge(t, 60.0)
+    t0 = bmo.apply_wedge_taper(t, 60.0, 0.0)
+    assert np.abs(sharp - t0).max() < 1e-10
+    soft = bmo.apply_wedge_taper(t, 60.0, 6.0)
+    assert float(np.sum(soft ** 2)) <= float(np.sum(t ** 2))
+
+
+@pytest.mark.slow
+def test_wedge_power_kernel_tracks_voxel_oracle():
+    t, _, _, _ = bmo.make_phantom(n=48, blobs=4, seed=2718, quat=[1, 0, 0, 0], shift=(0, 0, 0))
+    wp = bmo.wedge_power_kernel(t, 60.0, 16)
+    for k in range(5):
+        g = bmo.haar_rotation(15, k)
+        rho = bmo.correlation_derivatives(wp, 16, bmo.euler_zyz(g), 16, 0).value
+        assert 0.0 < rho < 1.0
+        rot = bmo.rotate_volume_trilinear(t, g)
+        srot = bmo.apply_wedge_taper(rot, 60.0)
+        assert abs(rho - (1.0 - float(np.sum(srot * rot)) / float(np.sum(rot * rot)))) < 0.05
+    open_ = bmo.wedge_power_kernel(t, 90.0, 16)
+    assert np.all(open_ == 0)
+
+
+# ------------------------------------------------------------- optimizer (test_optimize.cpp)
+def test_euler_grid_count():
+    for step in (PI / 8, PI / 6, math.radians(5)):
+        na, nb, ng = bmo.euler_grid_shape(step)
+        assert na * nb * ng == math.ceil(2 * PI / step) ** 2 * (math.ceil(PI / step) + 1)
+
+
+@pytest.fixture(scope="module")
+def ofix():
+    """test_optimize.cpp:27-50: 48^3 phantom template, L=16 self-kernel."""
+    t, _, _, _ = bmo.make_phantom(n=48, blobs=4, seed=4711, quat=[1, 0, 0, 0], shift=(0, 0, 0))
+    spec = bmo.Spec(16, bmo.default_lambda_cut(48, 16))
+    th = bmo.expand(t, spec)
+    return dict(tmpl=t, spec=spec, th=th, self_xi=bmo.xi_coefficients(th, th, spec))
+
+
+def small_cfg(**kw):
+    base = dict(l_max=16, bands=(4, 8, 14), seed_grid_step=PI / 8, shift_radius=4, shift_step=2)
+    base.update(kw)
+    return bmo.make_config(**base)
+
+
+def test_seed_candidates_self_finds_identity(ofix):
+    q, s, idx = bmo.seed_candidates(ofix["self_xi"], 16, 4, PI / 8, 20)
+    assert 0 < len(q) <= 20
+    assert np.all(np.diff(s) <= 0)
+    assert bmo.geodesic_degrees(q[0], [1, 0, 0, 0]) < 1e-9
+
+
+def test_refine_converges_from_5_degrees_monotone(ofix):
+    cfg = small_cfg()
+    rng = np.random.default_rng(5150)
+    for _ in range(4):
+        axis = rng.standard_normal(3)
+        axis /= np.linalg.norm(axis)
+        h = math.radians(5) / 2
+        start = np.concatenate([[math.cos(h)], axis * math.sin(h)])
+        r = bmo.refine(ofix["self_xi"], 16, start, cfg)
+        assert r["converged"]
+        assert bmo.geodesic_degrees(r["quat"], [1, 0, 0, 0]) < 0.1
+        band, last = -1, -1e300
+        for row in r["trace"]:
+            if row[0] != band:
+                band, last = row[0], -1e300
+            assert row[5] >= last - 1e-9
+            last = row[5]
+
+
+def test_refine_stationary_start(ofix):
+    r = bmo.refine(ofix["self_xi"], 16, [1, 0, 0, 0], small_cfg())
+    assert r["converged"] and len(r["trace"]) <= 3
+    assert bmo.geodesic_degrees(r["quat"], [1, 0, 0, 0]) < 1e-6
+
+
+@pytest.mark.slow
+def test_align_recovers_known_rotation_and_shift_noiseless():
+    """test_optimize.cpp:199-221 (48^3 phantom, known rotation + shift)."""
+    q = bmo.from_euler_zyz(1.1, 1.3, -0.7)
+    t, s, q_true, sh = bmo.make_phantom(n=48, blobs=4, seed=4711, quat=q, shift=(1, -2, 1))
+    cfg = small_cfg(shift_radius=2, shift_step=2, max_candidates=10)
+    r = bmo.align(t, s, cfg)
+    assert r["shift"] == sh
+    assert bmo.geodesic_degrees(r["quat"], q_true) < 0.5
