@@ -48,6 +48,20 @@ def _declare(L: C.CDLL) -> None:
     L.bm_abi_version.restype = I
     L.bm_split3_gemm.argtypes = [I, I, I, P, P, P, P, P, LL, LL, LL, LL, I, I, P, P, P]
     L.bm_split3_gemm.restype = I
+    L.bm_context_create.argtypes = [I, I, I, D, C.POINTER(C.c_void_p)]
+    L.bm_context_create.restype = I
+    L.bm_context_destroy.argtypes = [P]
+    L.bm_context_destroy.restype = I
+    L.bm_context_info.argtypes = [P, P]
+    L.bm_context_info.restype = I
+    L.bm_context_lambda_cut.argtypes = [P]
+    L.bm_context_lambda_cut.restype = D
+    L.bm_context_roots.argtypes = [P, I, P, P]
+    L.bm_context_roots.restype = I
+    L.bm_default_lambda_cut.argtypes = [I, I]
+    L.bm_default_lambda_cut.restype = D
+    L.bm_expand.argtypes = [P, P, I, P, P, P]
+    L.bm_expand.restype = I
 
 
 def check(rc: int, what: str = "") -> None:

@@ -1,0 +1,105 @@
+// Context construction and the batched expansion driver.
+#include "context.hpp"
+
+#include <stdexcept>
+
+namespace bmb {
+
+#define BMB_CUDA(x)                                                                   \
+    do {                                                                              \
+        cudaError_t e_ = (x);                                                         \
+        if (e_ != cudaSuccess)                                                        \
+            throw std::runtime_error(std::string(#x) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+Context::Context(int dev, int n_, int l_max, double lambda_cut) : device(dev), n(n_) {
+    if (n_ < 8 || n_ % 2) throw std::invalid_argument("context: grid size must be even and >= 8");
+    BMB_CUDA(cudaSetDevice(device));
+    BMB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    basis = host::make_basis(l_max, lambda_cut);
+    host::Operator op = host::build_operator(basis, n);
+    voxels_host = op.voxels;
+
+    geo.n = n;
+    geo.l_max = l_max;
+    geo.coeffs = op.rows;
+    geo.support = op.support;
+    geo.m_pad = op.m_pad;
+    geo.k_pad = op.k_pad;
+
+    upload(E_hi, op.hi, stream);
+    upload(E_lo, op.lo, stream);
+    upload(row_scale, op.row_scale, stream);
+    upload(voxels, op.voxels, stream);
+    std::vector<int> rc(l_max + 1);
+    for (int l = 0; l <= l_max; ++l) rc[l] = basis.radial_count(l);
+    upload(block_off, basis.block_off, stream);
+    upload(radial_count, rc, stream);
+    std::vector<float> rw(op.rows);
+    std::vector<int4> lkm(op.rows);
+    for (int l = 0; l <= l_max; ++l)
+        for (int k = 1; k <= basis.radial_count(l); ++k)
+            for (int m = 0; m <= l; ++m)
+                for (int part = 0; part < (m ? 2 : 1); ++part) {
+                    const int r = basis.row(l, k, m, part);
+                    rw[r] = m ? 2.0f : 1.0f;
+                    lkm[r] = make_int4(l, k, m, part);
+                }
+    upload(row_weight, rw, stream);
+    upload(row_lkm, lkm, stream);
+    geo.block_off = block_off.as<int>();
+    geo.radial_count = radial_count.as<int>();
+    geo.row_weight = row_weight.as<float>();
+    geo.row_lkm = row_lkm.as<int4>();
+    BMB_CUDA(cudaStreamSynchronize(stream));
+}
+
+Context::~Context() {
+    cudaSetDevice(device);
+    if (stream) {
+        cudaStreamSynchronize(stream);
+        cudaStreamDestroy(stream);
+    }
+}
+
+void Context::expand_windows(const float* vols, long long vol_stride, int n_vol,
+                             const std::vector<int>& wvol, const std::vector<int>& wshift) {
+    const int nw = (int)wvol.size();
+    if (nw == 0) return;
+    const int bn = gemm_block_n;
+    const long long n_pad = (long long)(nw + bn - 1) / bn * bn;
+    vol_scale.reserve(sizeof(float) * n_vol);
+    launch_absmax_scale(vols, n_vol, vol_stride, vol_scale.as<float>(), stream);
+    upload(win_vol, wvol, stream);
+    upload(win_shift, wshift, stream);
+    B_hi.reserve(sizeof(__half) * n_pad * geo.k_pad);
+    B_lo.reserve(sizeof(__half) * n_pad * geo.k_pad);
+    col_scale.reserve(sizeof(float) * n_pad);
+    coef.reserve(sizeof(float) * (size_t)nw * geo.m_pad);
+    launch_gather_windows(vols, vol_stride, win_vol.as<int>(), win_shift.as<int>(), nw,
+                          vol_scale.as<float>(), voxels.as<int>(), geo.support, geo.k_pad, n,
+                          B_hi.as<__half>(), B_lo.as<__half>(), col_scale.as<float>(), stream);
+    SplitGemmArgs a;
+    a.fmt = 0;
+    a.block_n = bn;
+    a.kchunk = gemm_kchunk;
+    a.a_hi = E_hi.p;
+    a.a_lo = E_lo.p;
+    a.b_hi = B_hi.p;
+    a.b_lo = B_lo.p;
+    a.out = coef.as<float>();
+    a.ldo = geo.m_pad;
+    a.m_pad = geo.m_pad;
+    a.n_pad = n_pad;
+    a.k_pad = geo.k_pad;
+    a.m_valid = geo.coeffs;
+    a.n_valid = nw;
+    a.row_scale = row_scale.as<float>();
+    a.col_scale = col_scale.as<float>();
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    a.num_sms = sms;
+    if (launch_split3_gemm(a, stream) != BMB_OK) throw std::runtime_error("split3 gemm launch failed");
+}
+
+}  // namespace bmb

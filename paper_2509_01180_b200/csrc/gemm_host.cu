@@ -57,13 +57,9 @@ static int launch_impl(const SplitGemmArgs& a, cudaStream_t stream) {
     rc |= make_operand_tmap(&tb_lo, a.b_lo, FMT, a.n_pad, a.k_pad, BN);
     if (rc != BMB_OK) return BMB_ERR_CUDA;
     auto kern = split3_gemm_kernel<FMT, BN>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 Cfg::kSmemBytes) != cudaSuccess)
-            return BMB_ERR_CUDA;
-        attr_set = true;
-    }
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             Cfg::kSmemBytes) != cudaSuccess)
+        return BMB_ERR_CUDA;
     const int mt = (int)(a.m_pad / kGemmBlockM), nt = (int)(a.n_pad / BN);
     const int tiles = mt * nt;
     int grid = a.num_sms > 0 ? a.num_sms : 148;

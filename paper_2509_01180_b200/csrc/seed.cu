@@ -1,0 +1,184 @@
+// Seeding (kernel K6): band-L_low correlation on the uniform ZYZ Euler grid,
+// strict 26-neighbour local maxima, best-first top-N, initial candidate states.
+// Restates grid_scores + seed_candidates (src/optimize.cpp:48-97, 197-253) with
+// one CTA per shift window; FP64 throughout (the grid is small), the A(beta)
+// collapse and phase sweeps in the reference's summation order.
+#include <cfloat>
+
+#include "kernels.cuh"
+#include "rotation.cuh"
+#include "seed.cuh"
+
+namespace bmb {
+
+__global__ void __launch_bounds__(256) seed_kernel(SeedArgs a) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const int w = blockIdx.x;
+    const int L = a.L_low, wd = 2 * L + 1;
+    const int npt = a.na * a.nb * a.ng;
+    const int nrow = a.rows_low;  // real-packed rows of degrees <= L
+    double* f = reinterpret_cast<double*>(sm);
+    double* t = f + nrow;
+    double2* xi = reinterpret_cast<double2*>(t + nrow);           // N_xi(L)
+    double2* A = xi + a.nxi;                                        // nb x wd x wd
+    double* sc = reinterpret_cast<double*>(A + (size_t)a.nb * wd * wd);  // npt
+    int* maxima = reinterpret_cast<int*>(sc + npt);                 // npt
+    __shared__ int n_max;
+
+    const float* cw = a.coef + (long long)w * a.ldc;
+    for (int r = threadIdx.x; r < nrow; r += blockDim.x) {
+        f[r] = cw[r];
+        t[r] = a.t_hat[r];
+    }
+    if (threadIdx.x == 0) n_max = 0;
+    __syncthreads();
+
+    // xi_l[m,m'] = sum_k conj(f_klm) t_klm'  (xi_coefficients(f_hat, t_hat), xcorr.cpp:34-50)
+    for (int e = threadIdx.x; e < a.nxi; e += blockDim.x) {
+        int l = 0;
+        while ((l + 1) * (2 * l + 1) * (2 * l + 3) / 3 <= e) ++l;
+        const int o = e - l * (2 * l - 1) * (2 * l + 1) / 3;
+        const int m = o / (2 * l + 1) - l, mp = o % (2 * l + 1) - l;
+        const int nk = a.radial_count[l], base = a.block_off[l];
+        double re = 0.0, im = 0.0;
+        for (int k = 0; k < nk; ++k) {
+            const double* fr = f + base + k * (2 * l + 1);
+            const double* tr = t + base + k * (2 * l + 1);
+            const int am = abs(m), amp = abs(mp);
+            double fre = fr[am == 0 ? 0 : 2 * am - 1], fim = am == 0 ? 0.0 : fr[2 * am];
+            if (m < 0) {
+                const double s = (am & 1) ? -1.0 : 1.0;
+                fre *= s;
+                fim *= -s;
+            }
+            double tre = tr[amp == 0 ? 0 : 2 * amp - 1], tim = amp == 0 ? 0.0 : tr[2 * amp];
+            if (mp < 0) {
+                const double s = (amp & 1) ? -1.0 : 1.0;
+                tre *= s;
+                tim *= -s;
+            }
+            re += fre * tre + fim * tim;  // conj(f) * t
+            im += fre * tim - fim * tre;
+        }
+        xi[e] = make_double2(re, im);
+    }
+    __syncthreads();
+
+    // A_j[m][m'] = sum_l xi_l[m,m'] d^l_{m,m'}(beta_j)
+    for (int e = threadIdx.x; e < a.nb * wd * wd; e += blockDim.x) {
+        const int j = e / (wd * wd), m = (e / wd) % wd - L, mp = e % wd - L;
+        double re = 0.0, im = 0.0;
+        for (int l = max(abs(m), abs(mp)); l <= L; ++l) {
+            const int o = l * (2 * l - 1) * (2 * l + 1) / 3 + (m + l) * (2 * l + 1) + (mp + l);
+            const double d = a.dgrid[(size_t)j * a.nxi + o];
+            re += xi[o].x * d;
+            im += xi[o].y * d;
+        }
+        A[e] = make_double2(re, im);
+    }
+    __syncthreads();
+
+    // score(i,j,k) = Re sum_m ua_i[m] sum_m' A_j[m][m'] ug_k[m']
+    for (int idx = threadIdx.x; idx < npt; idx += blockDim.x) {
+        const int k = idx % a.ng, i = (idx / a.ng) % a.na, j = idx / (a.ng * a.na);
+        const double2* Aj = A + (size_t)j * wd * wd;
+        const double2* pg = a.ug + (size_t)k * wd;
+        const double2* pa = a.ua + (size_t)i * wd;
+        double acc = 0.0;
+        for (int m = 0; m < wd; ++m) {
+            double bre = 0.0, bim = 0.0;
+            for (int mp = 0; mp < wd; ++mp) {
+                const double2 x = Aj[m * wd + mp], y = pg[mp];
+                bre += x.x * y.x - x.y * y.y;
+                bim += x.x * y.y + x.y * y.x;
+            }
+            acc += pa[m].x * bre - pa[m].y * bim;
+        }
+        if (a.wedge_sqrt) acc /= a.wedge_sqrt[idx];
+        sc[idx] = acc;
+    }
+    __syncthreads();
+
+    // strict local maxima over the 26-neighbourhood (alpha/gamma wrap, beta clamps);
+    // a plateau keeps its lowest flat index
+    for (int idx = threadIdx.x; idx < npt; idx += blockDim.x) {
+        const int k = idx % a.ng, i = (idx / a.ng) % a.na, j = idx / (a.ng * a.na);
+        const double s = sc[idx];
+        bool is_max = true;
+        for (int dj = -1; dj <= 1 && is_max; ++dj) {
+            const int jj = j + dj;
+            if (jj < 0 || jj >= a.nb) continue;
+            for (int di = -1; di <= 1 && is_max; ++di) {
+                const int ii = (i + di + a.na) % a.na;
+                for (int dk = -1; dk <= 1; ++dk) {
+                    const int kk = (k + dk + a.ng) % a.ng;
+                    const int other = (jj * a.na + ii) * a.ng + kk;
+                    if (other == idx) continue;
+                    const double o = sc[other];
+                    if (o > s || (o == s && other < idx)) {
+                        is_max = false;
+                        break;
+                    }
+                }
+            }
+        }
+        if (is_max) maxima[atomicAdd(&n_max, 1)] = idx;
+    }
+    __syncthreads();
+
+    // rank by (score desc, flat index asc); keep the best max_cand
+    const int nm = n_max;
+    const int keep = min(nm, a.max_cand);
+    for (int q = threadIdx.x; q < nm; q += blockDim.x) {
+        const int idx = maxima[q];
+        const double s = sc[idx];
+        int rank = 0;
+        for (int o = 0; o < nm; ++o) {
+            const int jdx = maxima[o];
+            const double t2 = sc[jdx];
+            rank += (t2 > s || (t2 == s && jdx < idx)) ? 1 : 0;
+        }
+        if (rank < keep) {
+            const int k = idx % a.ng, i = (idx / a.ng) % a.na, j = idx / (a.ng * a.na);
+            const double alpha = 2.0 * 3.14159265358979323846 * i / a.na;
+            const double beta = a.nb > 1 ? 3.14159265358979323846 * j / (a.nb - 1) : 0.0;
+            const double gamma = 2.0 * 3.14159265358979323846 * k / a.ng;
+            const Quat q0 = q_from_euler(alpha, beta, gamma);
+            CandState& c = a.cand[(size_t)w * a.max_cand + rank];
+            c.g[0] = c.best_g[0] = q0.w;
+            c.g[1] = c.best_g[1] = q0.x;
+            c.g[2] = c.best_g[2] = q0.y;
+            c.g[3] = c.best_g[3] = q0.z;
+            c.anchor[0] = 1.0;
+            c.anchor[1] = c.anchor[2] = c.anchor[3] = 0.0;
+            c.best_score = -DBL_MAX * 2.0;  // -inf
+            c.score = 0.0;
+            c.anchored = 0;
+            c.anchor_limit = -1;
+            c.diverged = 0;
+            c.band_converged = 0;
+            c.evals = 0;
+            c.active = 1;
+            if (a.seed_score) a.seed_score[(size_t)w * a.max_cand + rank] = s;
+        }
+    }
+    if (threadIdx.x == 0) a.cand_count[w] = keep;
+}
+
+size_t seed_smem_bytes(const SeedArgs& a) {
+    const int wd = 2 * a.L_low + 1;
+    const int npt = a.na * a.nb * a.ng;
+    return sizeof(double) * 2 * a.rows_low + sizeof(double2) * a.nxi +
+           sizeof(double2) * (size_t)a.nb * wd * wd + sizeof(double) * npt + sizeof(int) * npt;
+}
+
+int launch_seed(const SeedArgs& a, int n_win, cudaStream_t s) {
+    if (n_win <= 0) return 0;
+    const size_t smem = seed_smem_bytes(a);
+    if (smem > 200 * 1024) return 1;
+    cudaFuncSetAttribute(seed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    seed_kernel<<<n_win, 256, smem, s>>>(a);
+    return cudaGetLastError() == cudaSuccess ? 0 : 2;
+}
+
+}  // namespace bmb

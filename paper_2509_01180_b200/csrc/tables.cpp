@@ -1,0 +1,182 @@
+// Host builders for the per-band device tables (see kernels.cuh BandTables).
+#include "tables.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <stdexcept>
+
+namespace bmb {
+
+namespace {
+
+double sqrt_binom(int n, int k) {  // sqrt(C(n, k)) (src/steer.cpp:34-39)
+    double r = 1.0;
+    for (int i = 1; i <= k; ++i) r *= (double)(n - k + i) / i;
+    return std::sqrt(r);
+}
+
+// closed-form border of the recursion at degree l0 = max(|m|,|m'|):
+// d^{l0}_{m,m'} = fac * cos(b/2)^a sin(b/2)^p  (src/steer.cpp:109-128)
+void border(int m, int mp, double& fac, int& a, int& p) {
+    const int l = std::max(std::abs(m), std::abs(mp));
+    if (l == 0) {
+        fac = 1.0;
+        a = p = 0;
+        return;
+    }
+    if (m == l) {  // top row
+        fac = (((l - mp) % 2) ? -1.0 : 1.0) * sqrt_binom(2 * l, l + mp);
+        a = l + mp;
+        p = l - mp;
+    } else if (m == -l) {  // bottom row
+        fac = sqrt_binom(2 * l, l + mp);
+        a = l - mp;
+        p = l + mp;
+    } else if (mp == l) {  // right column
+        fac = sqrt_binom(2 * l, l + m);
+        a = l + m;
+        p = l - m;
+    } else {  // left column, mp == -l
+        fac = (((l + m) % 2) ? -1.0 : 1.0) * sqrt_binom(2 * l, l + m);
+        a = l - m;
+        p = l + m;
+    }
+}
+
+}  // namespace
+
+BandTablesHost build_band_tables(int L) {
+    if (L < 0 || L > kMaxL) throw std::invalid_argument("band limit out of range");
+    BandTablesHost t;
+    t.L = L;
+    struct It {
+        int m, mp, l0;
+    };
+    std::vector<It> items;
+    for (int m = 0; m <= L; ++m)
+        for (int mp = (m == 0 ? 0 : -L); mp <= L; ++mp)
+            items.push_back({m, mp, std::max(std::abs(m), std::abs(mp))});
+    std::stable_sort(items.begin(), items.end(), [](const It& x, const It& y) {
+        if (x.l0 != y.l0) return x.l0 < y.l0;
+        if (x.m != y.m) return x.m < y.m;
+        return x.mp < y.mp;
+    });
+    t.n_items = (int)items.size();
+    t.n_groups = (t.n_items + 31) / 32;
+    const int slots = t.n_groups * 32;
+    t.item_mm.assign(slots, char2{0, 0});
+    t.item_len.assign(slots, 0);
+    t.bfac.assign(slots, 0.0f);
+    t.bexp.assign(slots, 0);
+    t.row_off.assign(t.n_groups + 1, 0);
+    for (int g = 0; g < t.n_groups; ++g) {
+        int glen = 0;
+        for (int j = 0; j < 32 && g * 32 + j < t.n_items; ++j)
+            glen = std::max(glen, L - items[g * 32 + j].l0 + 1);
+        t.row_off[g + 1] = t.row_off[g] + glen;
+    }
+    t.rows = t.row_off[t.n_groups];
+    t.P.assign((size_t)t.rows * 32, 0.0f);
+    t.Q.assign((size_t)t.rows * 32, 0.0f);
+    t.R.assign((size_t)t.rows * 32, 0.0f);
+    t.item_of.assign((size_t)(2 * L + 1) * (2 * L + 1), 0);
+    for (int i = 0; i < t.n_items; ++i) {
+        const It& it = items[i];
+        const int g = i / 32, j = i % 32;
+        t.item_mm[i] = char2{(signed char)it.m, (signed char)it.mp};
+        t.item_len[i] = L - it.l0 + 1;
+        double fac;
+        int a, p;
+        border(it.m, it.mp, fac, a, p);
+        t.bfac[i] = (float)fac;
+        t.bexp[i] = a | (p << 8);
+        t.item_of[(size_t)(it.m + L) * (2 * L + 1) + (it.mp + L)] = (int16_t)i;
+        if (it.m != 0 || it.mp != 0)
+            t.item_of[(size_t)(-it.m + L) * (2 * L + 1) + (-it.mp + L)] = (int16_t)(-(i + 1));
+        const double m = it.m, mp = it.mp;
+        for (int s = 1; s <= L - it.l0; ++s) {
+            const int l = it.l0 + s;
+            const size_t at = (size_t)(t.row_off[g] + s) * 32 + j;
+            if (it.l0 == 0 && l == 1) {  // d^1_00 = cos b (steer.cpp:130-133)
+                t.P[at] = 1.0f;
+                continue;
+            }
+            // steer.cpp:101-141: t1 = P cos b + Q, t2 = R
+            const double a2 = std::sqrt(((double)l * l - m * m) * ((double)l * l - mp * mp));
+            const bool has2 = std::abs(it.m) <= l - 2 && std::abs(it.mp) <= l - 2;
+            const double b2 = has2 ? std::sqrt(((double)(l - 1) * (l - 1) - m * m) *
+                                               ((double)(l - 1) * (l - 1) - mp * mp))
+                                   : 0.0;
+            t.P[at] = (float)((2.0 * l - 1.0) * l / a2);
+            t.Q[at] = (float)(-(2.0 * l - 1.0) * m * mp / ((l - 1.0) * a2));
+            t.R[at] = (float)(l * b2 / ((l - 1.0) * a2));
+        }
+    }
+    return t;
+}
+
+std::vector<float2> wedge_band_entries(const BandTablesHost& t,
+                                       const std::vector<std::complex<double>>& chi,
+                                       const std::vector<std::complex<double>>& q, double total) {
+    std::vector<float2> w((size_t)t.rows * 32, float2{0.0f, 0.0f});
+    auto coef = [](const std::vector<std::complex<double>>& hat, int l, int m) {
+        if (m >= 0) return hat[host::tri(l, m)];
+        const std::complex<double> c = std::conj(hat[host::tri(l, -m)]);
+        return ((-m) % 2) ? -c : c;
+    };
+    for (int i = 0; i < t.n_items; ++i) {
+        const int m = t.item_mm[i].x, mp = t.item_mm[i].y;
+        const int l0 = std::max(std::abs(m), std::abs(mp));
+        const int g = i / 32, j = i % 32;
+        for (int l = l0; l <= t.L; ++l) {
+            const std::complex<double> v = std::conj(coef(chi, l, m)) * coef(q, l, mp) / total;
+            w[(size_t)(t.row_off[g] + l - l0) * 32 + j] = float2{(float)v.real(), (float)v.imag()};
+        }
+    }
+    return w;
+}
+
+std::vector<double> little_d_full(int L, double beta) {
+    std::vector<size_t> off(L + 2, 0);
+    for (int l = 0; l <= L; ++l) off[l + 1] = off[l] + (size_t)(2 * l + 1) * (2 * l + 1);
+    std::vector<double> d(off[L + 1], 0.0);
+    const double cb = std::cos(beta), ch = std::cos(0.5 * beta), sh = std::sin(0.5 * beta);
+    auto at = [&](int l, int m, int mp) -> double& {
+        return d[off[l] + (size_t)(m + l) * (2 * l + 1) + (mp + l)];
+    };
+    auto ipow = [](double x, int e) {
+        double r = 1.0;
+        for (int i = 0; i < e; ++i) r *= x;
+        return r;
+    };
+    at(0, 0, 0) = 1.0;
+    for (int l = 1; l <= L; ++l) {
+        for (int m = -l; m <= l; ++m)
+            for (int mp = -l; mp <= l; ++mp) {
+                if (std::abs(m) != l && std::abs(mp) != l) continue;
+                double fac;
+                int a, p;
+                border(m, mp, fac, a, p);
+                at(l, m, mp) = fac * (ipow(ch, a) * ipow(sh, p));
+            }
+        if (l == 1) {
+            at(1, 0, 0) = cb;
+            continue;
+        }
+        for (int m = -(l - 1); m <= l - 1; ++m)
+            for (int mp = -(l - 1); mp <= l - 1; ++mp) {
+                const double a2 = std::sqrt(((double)l * l - (double)m * m) * ((double)l * l - (double)mp * mp));
+                const double den = (l - 1.0) * a2;
+                const double t1 = (2.0 * l - 1.0) * (l * (l - 1.0) * cb - (double)m * mp) / den;
+                const bool has2 = std::abs(m) <= l - 2 && std::abs(mp) <= l - 2;
+                const double b2 = has2 ? std::sqrt(((double)(l - 1) * (l - 1) - (double)m * m) *
+                                                   ((double)(l - 1) * (l - 1) - (double)mp * mp))
+                                       : 0.0;
+                const double t2 = l * b2 / den;
+                at(l, m, mp) = t1 * at(l - 1, m, mp) - (has2 ? t2 * at(l - 2, m, mp) : 0.0);
+            }
+    }
+    return d;
+}
+
+}  // namespace bmb
