@@ -66,6 +66,96 @@ double bm_default_lambda_cut(int n, int l_max);
 int bm_expand(bm_context* ctx, const float* vols, int count, const int* shifts, double* out,
               void* stream);
 
+/* ------------------------------------------------------------------ alignment
+ * Mirrors OptimizerConfig (include/ballmatch/optimize.hpp:15-32) with fixed
+ * bands; l_max and lambda_cut are the context's.  accept_tol is the relative
+ * slack of the Newton acceptance test (reference: 1e-12 with FP64 scores,
+ * src/optimize.cpp:332); the FP32 evaluation uses a wider default. */
+typedef struct bm_align_config {
+    int n_bands;
+    int bands[16];
+    double seed_grid_step;
+    int max_candidates;
+    int newton_max_iter;
+    double grad_tol;
+    double step_damping;
+    int shift_radius;
+    int shift_step;
+    double accept_tol;
+} bm_align_config;
+
+/* AlignmentResult (optimize.hpp:71-88): shift, rotation (template -> particle,
+ * quaternion w,x,y,z), score normalized by the expansion norms. */
+typedef struct bm_align_result {
+    int shift[3];
+    double quat[4];
+    double score;
+    int converged;
+    long long candidates;
+    long long evaluations;
+    double subtomo_norm;
+    int windows;
+} bm_align_result;
+
+/* One window outcome (search_one_shift, src/optimize.cpp:361-419). */
+typedef struct bm_window_result {
+    int volume;
+    int shift[3];
+    int valid;
+    int n_candidates;
+    int converged;
+    double raw_score;
+    double norm_score;
+    double subtomo_norm;
+    double quat[4];
+    long long evaluations;
+} bm_window_result;
+
+/* Template state of align() (src/optimize.cpp:438-454): expand the template
+ * (device float32 n^3), and for a wedge (theta in (0,90), tilt axis y) build
+ * the tapered filter and the wedge-power kernel.  theta <= 0: no wedge. */
+int bm_set_template(bm_context* ctx, const float* tmpl, double wedge_theta_deg, void* stream);
+/* template norm ||t_hat|| */
+double bm_template_norm(const bm_context* ctx);
+
+/* align() for `count` particles (device float32, count x n^3): wedge filter,
+ * coarse + fine shift windows, seeding, device Newton with frequency marching.
+ * Results to host memory; synchronizes the context stream. */
+int bm_align_batch(bm_context* ctx, const float* particles, int count, const bm_align_config* cfg,
+                   bm_align_result* out, void* stream);
+
+/* search_one_shift for explicit windows (volume index, shift) of device
+ * volumes (already wedge-filtered by the caller if needed); results to host. */
+int bm_search_windows(bm_context* ctx, const float* vols, int n_vol, const int* win_vol,
+                      const int* win_shift, int n_win, const bm_align_config* cfg,
+                      bm_window_result* out, void* stream);
+
+/* Batched rotate-score-gradient (correlation_derivatives order 0/1,
+ * src/xcorr.cpp:52-105) of xi_p = xi_coefficients(f_p, t) at band L = l_max:
+ * f: device complex128 (n_f x coeff_count, reference layout, real-volume
+ * symmetric), t: one device complex128 coefficient set, euler: device
+ * double (n_rot x 3).  out: device double (n_f x n_rot x 4):
+ * value, dC/dalpha, dC/dbeta, dC/dgamma. */
+int bm_eval_sweep(bm_context* ctx, const double* f, int n_f, const double* t, const double* euler,
+                  int n_rot, int order, double* out, void* stream);
+
+/* Tapered missing-wedge filter of the current template's context on device
+ * volumes (apply_wedge_taper, src/xcorr.cpp:210-232). */
+int bm_apply_wedge_taper(bm_context* ctx, const float* in, float* out, int count, void* stream);
+
+/* ------------------------------------------------------------------ synthetic inputs
+ * Seeded generator on the device (BASELINE.json configs; particle pipeline of
+ * make_phantom, src/volio.cpp:285-314).  Template: isotropic Gaussian blobs
+ * (Philox stream 0 of `seed`).  Particle p uses seed base_seed + p: Haar
+ * rotation (stream 1), shift in [-shift_max, shift_max]^3 (stream 2), rotate ->
+ * shift by -s -> binary wedge (wedge_deg in (0,90), else none) -> noise at
+ * `snr` inside the unit ball (stream 3; snr <= 0: none) -> float32.
+ * out: device float32; quats (4 per particle) / shifts (3): host, may be NULL. */
+int bm_make_template(int device, int n, int blobs, unsigned long long seed, float* out, void* stream);
+int bm_make_particles(int device, const float* tmpl, int n, int count, unsigned long long base_seed,
+                      int shift_max, double snr, double wedge_deg, float* out, double* quats,
+                      int* shifts, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

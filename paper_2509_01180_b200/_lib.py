@@ -43,6 +43,28 @@ LL = C.c_longlong
 D = C.c_double
 
 
+class AlignConfig(C.Structure):
+    """bm_align_config: OptimizerConfig (include/ballmatch/optimize.hpp:15-32), fixed bands."""
+    _fields_ = [("n_bands", C.c_int), ("bands", C.c_int * 16), ("seed_grid_step", C.c_double),
+                ("max_candidates", C.c_int), ("newton_max_iter", C.c_int),
+                ("grad_tol", C.c_double), ("step_damping", C.c_double),
+                ("shift_radius", C.c_int), ("shift_step", C.c_int), ("accept_tol", C.c_double)]
+
+
+class AlignResult(C.Structure):
+    _fields_ = [("shift", C.c_int * 3), ("quat", C.c_double * 4), ("score", C.c_double),
+                ("converged", C.c_int), ("candidates", C.c_longlong),
+                ("evaluations", C.c_longlong), ("subtomo_norm", C.c_double),
+                ("windows", C.c_int)]
+
+
+class WindowResult(C.Structure):
+    _fields_ = [("volume", C.c_int), ("shift", C.c_int * 3), ("valid", C.c_int),
+                ("n_candidates", C.c_int), ("converged", C.c_int), ("raw_score", C.c_double),
+                ("norm_score", C.c_double), ("subtomo_norm", C.c_double),
+                ("quat", C.c_double * 4), ("evaluations", C.c_longlong)]
+
+
 def _declare(L: C.CDLL) -> None:
     L.bm_last_error.restype = C.c_char_p
     L.bm_abi_version.restype = I
@@ -62,6 +84,23 @@ def _declare(L: C.CDLL) -> None:
     L.bm_default_lambda_cut.restype = D
     L.bm_expand.argtypes = [P, P, I, P, P, P]
     L.bm_expand.restype = I
+    L.bm_set_template.argtypes = [P, P, D, P]
+    L.bm_set_template.restype = I
+    L.bm_template_norm.argtypes = [P]
+    L.bm_template_norm.restype = D
+    L.bm_align_batch.argtypes = [P, P, I, C.POINTER(AlignConfig), C.POINTER(AlignResult), P]
+    L.bm_align_batch.restype = I
+    L.bm_search_windows.argtypes = [P, P, I, P, P, I, C.POINTER(AlignConfig),
+                                    C.POINTER(WindowResult), P]
+    L.bm_search_windows.restype = I
+    L.bm_eval_sweep.argtypes = [P, P, I, P, P, I, I, P, P]
+    L.bm_eval_sweep.restype = I
+    L.bm_apply_wedge_taper.argtypes = [P, P, P, I, P]
+    L.bm_apply_wedge_taper.restype = I
+    L.bm_make_template.argtypes = [I, I, I, C.c_ulonglong, P, P]
+    L.bm_make_template.restype = I
+    L.bm_make_particles.argtypes = [I, P, I, I, C.c_ulonglong, I, D, D, P, P, P, P]
+    L.bm_make_particles.restype = I
 
 
 def check(rc: int, what: str = "") -> None:

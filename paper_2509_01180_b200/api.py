@@ -27,9 +27,62 @@ def _torch():
     return torch
 
 
+# FP32 evaluation: acceptance slack of the Newton line test and gradient
+# tolerance floor (the reference's 1e-12 / 1e-7 assume FP64 scores)
+FP32_ACCEPT_TOL = 1e-6
+FP32_GRAD_TOL = 1e-5
+
+
+def make_config(bands=(7, 12, 33), seed_grid_step=np.pi / 8, max_candidates=20,
+                newton_max_iter=30, grad_tol=1e-7, step_damping=1e-3, shift_radius=4,
+                shift_step=2, accept_tol=None) -> _lib.AlignConfig:
+    """OptimizerConfig defaults (include/ballmatch/optimize.hpp:15-32); grad_tol is
+    floored at the FP32 evaluation's resolution unless accept_tol is given explicitly."""
+    c = _lib.AlignConfig()
+    c.n_bands = len(bands)
+    for i, b in enumerate(bands):
+        c.bands[i] = int(b)
+    c.seed_grid_step = seed_grid_step
+    c.max_candidates = max_candidates
+    c.newton_max_iter = newton_max_iter
+    c.grad_tol = max(grad_tol, FP32_GRAD_TOL) if accept_tol is None else grad_tol
+    c.step_damping = step_damping
+    c.shift_radius = shift_radius
+    c.shift_step = shift_step
+    c.accept_tol = FP32_ACCEPT_TOL if accept_tol is None else accept_tol
+    return c
+
+
 def default_lambda_cut(n: int, l_max: int) -> float:
     """default_lambda_cut (src/basis.cpp:117-138)."""
     return _lib.lib().bm_default_lambda_cut(n, l_max)
+
+
+def make_template(n: int, blobs: int, seed: int, device: int = 0):
+    """BASELINE template model on the device (float32 (n, n, n) tensor)."""
+    torch = _torch()
+    out = torch.empty((n, n, n), dtype=torch.float32, device=f"cuda:{device}")
+    stream = torch.cuda.current_stream(out.device).cuda_stream
+    _lib.check(_lib.lib().bm_make_template(device, n, blobs, seed, C.c_void_p(out.data_ptr()),
+                                           C.c_void_p(stream)), "make_template")
+    return out
+
+
+def make_particles(tmpl, count: int, base_seed: int, shift_max: int, snr=None, wedge_deg=None):
+    """Particles of a BASELINE config on the device: (count, n, n, n) float32 tensor plus
+    the ground truth (quaternions (count, 4), shifts (count, 3))."""
+    torch = _torch()
+    n = tmpl.shape[-1]
+    out = torch.empty((count, n, n, n), dtype=torch.float32, device=tmpl.device)
+    q = np.zeros((count, 4))
+    sh = np.zeros((count, 3), dtype=np.int32)
+    stream = torch.cuda.current_stream(out.device).cuda_stream
+    _lib.check(_lib.lib().bm_make_particles(
+        tmpl.device.index or 0, C.c_void_p(tmpl.contiguous().data_ptr()), n, count, base_seed,
+        shift_max, snr or 0.0, wedge_deg or 0.0, C.c_void_p(out.data_ptr()),
+        q.ctypes.data_as(C.c_void_p), sh.ctypes.data_as(C.c_void_p), C.c_void_p(stream)),
+        "make_particles")
+    return out, q, sh
 
 
 class Context:
@@ -94,3 +147,60 @@ class Context:
         _lib.check(_lib.lib().bm_expand(self._h, C.c_void_p(v.data_ptr()), count, sh,
                                         C.c_void_p(out.data_ptr()), C.c_void_p(stream)), "expand")
         return torch.view_as_complex(out)
+
+    # ------------------------------------------------------------------ align
+    def _dev(self, vols):
+        torch = _torch()
+        v = vols if isinstance(vols, torch.Tensor) else torch.as_tensor(np.asarray(vols))
+        if v.dim() == 3:
+            v = v.unsqueeze(0)
+        return v.to(device=f"cuda:{self.device}", dtype=torch.float32).contiguous()
+
+    def _stream(self, t):
+        return C.c_void_p(_torch().cuda.current_stream(t.device).cuda_stream)
+
+    def set_template(self, tmpl, wedge_theta_deg: float = 0.0):
+        """Template state of align() (src/optimize.cpp:438-454)."""
+        t = self._dev(tmpl)
+        _lib.check(_lib.lib().bm_set_template(self._h, C.c_void_p(t.data_ptr()), wedge_theta_deg,
+                                              self._stream(t)), "set_template")
+        self.template_norm = _lib.lib().bm_template_norm(self._h)
+        self.wedge_theta_deg = wedge_theta_deg
+
+    def align_batch(self, particles, cfg: _lib.AlignConfig):
+        """align() for every particle of the batch; list of dicts (AlignmentResult)."""
+        v = self._dev(particles)
+        count = v.shape[0]
+        out = (_lib.AlignResult * max(count, 1))()
+        _lib.check(_lib.lib().bm_align_batch(self._h, C.c_void_p(v.data_ptr()), count,
+                                             C.byref(cfg), out, self._stream(v)), "align")
+        return [dict(shift=tuple(r.shift), quat=np.array(r.quat[:]), score=r.score,
+                     converged=bool(r.converged), candidates=r.candidates,
+                     evaluations=r.evaluations, subtomo_norm=r.subtomo_norm, windows=r.windows)
+                for r in out[:count]]
+
+    def search_windows(self, vols, windows, cfg: _lib.AlignConfig):
+        """search_one_shift for explicit (volume index, (sx, sy, sz)) windows."""
+        v = self._dev(vols)
+        n_win = len(windows)
+        wv = np.ascontiguousarray([w[0] for w in windows], dtype=np.int32)
+        ws = np.ascontiguousarray([w[1] for w in windows], dtype=np.int32).reshape(-1)
+        out = (_lib.WindowResult * max(n_win, 1))()
+        _lib.check(_lib.lib().bm_search_windows(
+            self._h, C.c_void_p(v.data_ptr()), v.shape[0], wv.ctypes.data_as(C.c_void_p),
+            ws.ctypes.data_as(C.c_void_p), n_win, C.byref(cfg), out, self._stream(v)),
+            "search_windows")
+        return [dict(volume=r.volume, shift=tuple(r.shift), valid=bool(r.valid),
+                     candidates=r.n_candidates, converged=bool(r.converged),
+                     raw_score=r.raw_score, norm_score=r.norm_score,
+                     subtomo_norm=r.subtomo_norm, quat=np.array(r.quat[:]),
+                     evaluations=r.evaluations) for r in out[:n_win]]
+
+    def apply_wedge_taper(self, vols):
+        torch = _torch()
+        v = self._dev(vols)
+        out = torch.empty_like(v)
+        _lib.check(_lib.lib().bm_apply_wedge_taper(self._h, C.c_void_p(v.data_ptr()),
+                                                   C.c_void_p(out.data_ptr()), v.shape[0],
+                                                   self._stream(v)), "apply_wedge_taper")
+        return out

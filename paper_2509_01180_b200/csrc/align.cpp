@@ -1,0 +1,381 @@
+// Host alignment driver of the B200 path (kernel K7 orchestration + the
+// coarse-to-fine shift search of align(), src/optimize.cpp:423-521).
+//
+// Per stage (coarse shift grid, then the unit-step fine cube): all windows of
+// all particles in the batch are expanded by the tcgen05 GEMM, seeded on the
+// Euler grid, refined band by band (the host raises L between launches =
+// frequency marching), and reduced to one outcome per window on the device.
+// The host only picks the best window per particle (outcome_better) and builds
+// the fine window list.
+#include <algorithm>
+#include <array>
+#include <cfloat>
+#include <cmath>
+#include <stdexcept>
+
+#include "context.hpp"
+#include "refine.cuh"
+#include "rotation.cuh"
+#include "seed.cuh"
+#include "tables.hpp"
+#include "wedge.hpp"
+
+namespace bmb {
+
+namespace {
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+}  // namespace
+
+void AlignConfig::validate(int l_max) const {
+    if (bands.empty()) throw std::invalid_argument("config: need fixed bands or auto band selection");
+    for (size_t i = 0; i < bands.size(); ++i) {
+        if (bands[i] < 0 || bands[i] > l_max) throw std::invalid_argument("config: bands must lie in [0, l_max]");
+        if (i > 0 && bands[i] <= bands[i - 1]) throw std::invalid_argument("config: bands must be strictly increasing");
+    }
+    if (!(seed_grid_step > 0.0) || seed_grid_step > kPiH)
+        throw std::invalid_argument("config: seed grid step must be in (0, pi]");
+    if (max_candidates < 1 || newton_max_iter < 1) throw std::invalid_argument("config: counts must be positive");
+    if (!(grad_tol > 0.0) || !(step_damping > 0.0)) throw std::invalid_argument("config: tolerances must be positive");
+    if (shift_radius < 0 || shift_step < 1) throw std::invalid_argument("config: bad shift search parameters");
+}
+
+BandTables BandDev::view() const {
+    BandTables t;
+    t.L = L;
+    t.n_items = n_items;
+    t.n_groups = n_groups;
+    t.rows = rows;
+    t.row_off = row_off.as<int>();
+    t.item_mm = item_mm.as<char2>();
+    t.item_len = item_len.as<int>();
+    t.bfac = bfac.as<float>();
+    t.bexp = bexp.as<int>();
+    t.P = P.as<float>();
+    t.Q = Q.as<float>();
+    t.R = R.as<float>();
+    t.item_of = item_of.as<int16_t>();
+    t.wedge = has_wedge ? wedge.as<float2>() : nullptr;
+    return t;
+}
+
+BandDev& Context::band(int L) {
+    auto it = bands_.find(L);
+    if (it != bands_.end()) {
+        BandDev& b = *it->second;
+        if (wedge_active() && !b.has_wedge) {
+            BandTablesHost h = build_band_tables(L);
+            upload(b.wedge, wedge_band_entries(h, chi_hat, q_hat, wp_total), stream);
+            b.has_wedge = true;
+        }
+        return b;
+    }
+    auto b = std::make_unique<BandDev>();
+    BandTablesHost h = build_band_tables(L);
+    b->L = L;
+    b->n_items = h.n_items;
+    b->n_groups = h.n_groups;
+    b->rows = h.rows;
+    upload(b->row_off, h.row_off, stream);
+    upload(b->item_mm, h.item_mm, stream);
+    upload(b->item_len, h.item_len, stream);
+    upload(b->bfac, h.bfac, stream);
+    upload(b->bexp, h.bexp, stream);
+    upload(b->P, h.P, stream);
+    upload(b->Q, h.Q, stream);
+    upload(b->R, h.R, stream);
+    upload(b->item_of, h.item_of, stream);
+    std::vector<int> rg(h.rows);
+    for (int g = 0; g < h.n_groups; ++g)
+        for (int r = h.row_off[g]; r < h.row_off[g + 1]; ++r) rg[r] = g;
+    upload(b->row_group, rg, stream);
+    if (wedge_active()) {
+        upload(b->wedge, wedge_band_entries(h, chi_hat, q_hat, wp_total), stream);
+        b->has_wedge = true;
+    }
+    ck(cudaStreamSynchronize(stream), "band tables");
+    return *bands_.emplace(L, std::move(b)).first->second;
+}
+
+SeedDev& Context::seed_tables(int L, double step) {
+    const long long key_step = (long long)std::llround(step * 1e12);
+    auto key = std::make_pair(L, key_step);
+    auto it = seeds_.find(key);
+    if (it != seeds_.end() && it->second->has_wedge == wedge_active()) return *it->second;
+    auto s = std::make_unique<SeedDev>();
+    s->L_low = L;
+    s->step = step;
+    // EulerGrid::with_step (optimize.cpp:30-36)
+    s->na = s->ng = (int)std::ceil(2.0 * kPiH / step);
+    s->nb = (int)std::ceil(kPiH / step) + 1;
+    s->nxi = (L + 1) * (2 * L + 1) * (2 * L + 3) / 3;
+    const int wd = 2 * L + 1;
+    std::vector<double> dgrid;
+    std::vector<std::vector<double>> dj(s->nb);
+    for (int j = 0; j < s->nb; ++j) {
+        const double beta = s->nb > 1 ? kPiH * j / (s->nb - 1) : 0.0;
+        dj[j] = little_d_full(L, beta);
+        dgrid.insert(dgrid.end(), dj[j].begin(), dj[j].end());
+    }
+    std::vector<double2> ua((size_t)s->na * wd), ug((size_t)s->ng * wd);
+    for (int i = 0; i < s->na; ++i)
+        for (int m = -L; m <= L; ++m) {
+            const std::complex<double> z = std::polar(1.0, -m * (2.0 * kPiH * i / s->na));
+            ua[(size_t)i * wd + (m + L)] = double2{z.real(), z.imag()};
+        }
+    for (int k = 0; k < s->ng; ++k)
+        for (int m = -L; m <= L; ++m) {
+            const std::complex<double> z = std::polar(1.0, -m * (2.0 * kPiH * k / s->ng));
+            ug[(size_t)k * wd + (m + L)] = double2{z.real(), z.imag()};
+        }
+    upload(s->dgrid, dgrid, stream);
+    upload(s->ua, ua, stream);
+    upload(s->ug, ug, stream);
+    if (wedge_active()) {
+        // rho on the grid from the wedge-power kernel at min(L, l_max) (optimize.cpp:202-206)
+        const int Lw = std::min(L, basis.l_max);
+        auto coef = [](const std::vector<std::complex<double>>& hat, int l, int m) {
+            if (m >= 0) return hat[host::tri(l, m)];
+            const std::complex<double> c = std::conj(hat[host::tri(l, -m)]);
+            return ((-m) % 2) ? -c : c;
+        };
+        const int w2 = 2 * Lw + 1;
+        std::vector<double> sq((size_t)s->na * s->nb * s->ng);
+        for (int j = 0; j < s->nb; ++j) {
+            const std::vector<double>& d = dj[j];
+            std::vector<std::complex<double>> A((size_t)w2 * w2, {0.0, 0.0});
+            for (int l = 0; l <= Lw; ++l) {
+                const int wl = 2 * l + 1;
+                const size_t off = (size_t)l * (2 * l - 1) * (2 * l + 1) / 3;
+                for (int m = -l; m <= l; ++m)
+                    for (int mp = -l; mp <= l; ++mp)
+                        A[(size_t)(m + Lw) * w2 + (mp + Lw)] +=
+                            std::conj(coef(chi_hat, l, m)) * coef(q_hat, l, mp) / wp_total *
+                            d[off + (size_t)(m + l) * wl + (mp + l)];
+            }
+            for (int k = 0; k < s->ng; ++k)
+                for (int i = 0; i < s->na; ++i) {
+                    double acc = 0.0;
+                    for (int m = 0; m < w2; ++m) {
+                        std::complex<double> b{0.0, 0.0};
+                        for (int mp = 0; mp < w2; ++mp)
+                            b += A[(size_t)m * w2 + mp] * std::polar(1.0, -(mp - Lw) * (2.0 * kPiH * k / s->ng));
+                        const std::complex<double> pa = std::polar(1.0, -(m - Lw) * (2.0 * kPiH * i / s->na));
+                        acc += pa.real() * b.real() - pa.imag() * b.imag();
+                    }
+                    sq[((size_t)j * s->na + i) * s->ng + k] = std::sqrt(std::clamp(1.0 - acc, 0.02, 2.0));
+                }
+        }
+        upload(s->wedge_sqrt, sq, stream);
+        s->has_wedge = true;
+    }
+    ck(cudaStreamSynchronize(stream), "seed tables");
+    auto& ref = seeds_[key];
+    ref = std::move(s);
+    return *ref;
+}
+
+void Context::set_template(const float* tmpl, double wedge_theta) {
+    if (geo.support == 0) throw std::invalid_argument("set_template: context has no operator (n = 0)");
+    // template expansion through the same tensor-core path (align: t_hat = expand(tmpl))
+    std::vector<int> wv{0}, ws{0, 0, 0};
+    expand_windows(tmpl, (long long)n * n * n, 1, wv, ws);
+    t_hat.reserve(sizeof(float) * geo.m_pad);
+    ck(cudaMemcpyAsync(t_hat.p, coef.p, sizeof(float) * geo.m_pad, cudaMemcpyDeviceToDevice, stream), "t_hat");
+    norms.reserve(sizeof(double));
+    launch_window_norms(coef.as<float>(), 1, geo.m_pad, geo, norms.as<double>(), stream);
+    ck(cudaMemcpyAsync(&t_norm, norms.p, sizeof(double), cudaMemcpyDeviceToHost, stream), "t_norm");
+    ck(cudaStreamSynchronize(stream), "set_template");
+    if (!(t_norm > 0.0)) throw std::invalid_argument("align: template has no in-ball energy");
+    wedge_deg = wedge_theta;
+    wedge.reset();
+    chi_hat.clear();
+    q_hat.clear();
+    wp_total = 0.0;
+    if (wedge_theta > 0.0 && wedge_theta < 90.0) {
+        wedge = std::make_unique<WedgeFilter>(n, wedge_theta, kWedgeTaperDeg);
+        WedgePowerFactors f = wedge_power_factors(tmpl, n, basis.l_max, wedge_theta, kWedgeTaperDeg, stream);
+        chi_hat = std::move(f.chi_hat);
+        q_hat = std::move(f.q_hat);
+        wp_total = f.total;
+    }
+    // band tables carry the wedge entries of this template: rebuild lazily
+    bands_.clear();
+    seeds_.clear();
+    has_template = true;
+}
+
+std::vector<WindowOutcome> Context::run_windows(const float* vols, int n_vol, const std::vector<int>& wvol,
+                                                const std::vector<int>& wshift, const AlignConfig& cfg) {
+    if (!has_template) throw std::invalid_argument("align: set_template first");
+    cfg.validate(basis.l_max);
+    const int nw = (int)wvol.size();
+    std::vector<WindowOutcome> res(nw);
+    if (nw == 0) return res;
+    const long long vstride = (long long)n * n * n;
+    expand_windows(vols, vstride, n_vol, wvol, wshift);
+    sub_norm_.reserve(sizeof(double) * nw);
+    launch_window_norms(coef.as<float>(), nw, geo.m_pad, geo, sub_norm_.as<double>(), stream);
+
+    const int maxc = cfg.max_candidates;
+    cand_.reserve(sizeof(CandState) * (size_t)nw * maxc);
+    cand_count_.reserve(sizeof(int) * nw);
+    outcome_.reserve(sizeof(WindowOutcome) * nw);
+    win_counter_.reserve(sizeof(int));
+    SeedDev& sd = seed_tables(cfg.bands.front(), cfg.seed_grid_step);
+    SeedArgs sa;
+    sa.coef = coef.as<float>();
+    sa.ldc = geo.m_pad;
+    sa.t_hat = t_hat.as<float>();
+    sa.block_off = geo.block_off;
+    sa.radial_count = geo.radial_count;
+    sa.L_low = sd.L_low;
+    sa.rows_low = sd.L_low + 1 <= basis.l_max ? basis.block_off[sd.L_low + 1] : geo.coeffs;
+    sa.nxi = sd.nxi;
+    sa.na = sd.na;
+    sa.nb = sd.nb;
+    sa.ng = sd.ng;
+    sa.dgrid = sd.dgrid.as<double>();
+    sa.ua = sd.ua.as<double2>();
+    sa.ug = sd.ug.as<double2>();
+    sa.wedge_sqrt = sd.has_wedge ? sd.wedge_sqrt.as<double>() : nullptr;
+    sa.max_cand = maxc;
+    sa.cand = cand_.as<CandState>();
+    sa.cand_count = cand_count_.as<int>();
+    if (launch_seed(sa, nw, stream) != 0) throw std::runtime_error("seed kernel launch failed");
+
+    const Quat koff = q_from_euler(0.0, kPiH / 2.0, 0.0);
+    for (size_t bi = 0; bi < cfg.bands.size(); ++bi) {
+        const int L = cfg.bands[bi];
+        BandDev& bd = band(L);
+        RefineArgs ra;
+        ra.T = bd.view();
+        ra.row_group = bd.row_group.as<int>();
+        ra.coef = coef.as<float>();
+        ra.ldc = geo.m_pad;
+        ra.t_hat = t_hat.as<float>();
+        ra.block_off = geo.block_off;
+        ra.radial_count = geo.radial_count;
+        ra.rows_band = L + 1 <= basis.l_max ? basis.block_off[L + 1] : geo.coeffs;
+        ra.cand_count = cand_count_.as<int>();
+        ra.cand = cand_.as<CandState>();
+        ra.max_cand = maxc;
+        ra.n_win = nw;
+        ra.win_counter = win_counter_.as<int>();
+        const int blocks = std::min(nw, refine_resident_blocks(ra.T, ra.rows_band, maxc, device));
+        ra.scratch_per_warp = (refine_scratch_floats(ra.T) + 3) / 4 * 4;
+        scratch_.reserve(sizeof(float) * (size_t)blocks * 8 * ra.scratch_per_warp);
+        ra.scratch = scratch_.as<float>();
+        ra.prm.band = L;
+        ra.prm.newton_max_iter = cfg.newton_max_iter;
+        ra.prm.grad_tol = cfg.grad_tol;
+        ra.prm.accept_tol = cfg.accept_tol;
+        ra.prm.step_damping = cfg.step_damping;
+        ra.prm.koffset[0] = koff.w;
+        ra.prm.koffset[1] = koff.x;
+        ra.prm.koffset[2] = koff.y;
+        ra.prm.koffset[3] = koff.z;
+        ra.prm.max_cand = maxc;
+        ra.prm.has_wedge = wedge_active() ? 1 : 0;
+        ra.prm.first_band = bi == 0;
+        ra.last_band = bi + 1 == cfg.bands.size();
+        ra.sub_norm = sub_norm_.as<double>();
+        ra.t_norm = t_norm;
+        ra.win_particle = win_vol.as<int>();
+        ra.win_shift = win_shift.as<int>();
+        ra.grid_evals = (long long)sd.na * sd.nb * sd.ng;
+        ra.out = outcome_.as<WindowOutcome>();
+        ck(cudaMemsetAsync(win_counter_.p, 0, sizeof(int), stream), "counter");
+        if (launch_refine(ra, blocks, stream) != 0) throw std::runtime_error("refine kernel launch failed");
+    }
+    ck(cudaMemcpyAsync(res.data(), outcome_.p, sizeof(WindowOutcome) * nw, cudaMemcpyDeviceToHost, stream),
+       "outcomes");
+    ck(cudaStreamSynchronize(stream), "run_windows");
+    return res;
+}
+
+namespace {
+// outcome_better (optimize.cpp:144-149): score, then lexicographic shift, then angle
+bool better(const WindowOutcome& a, const WindowOutcome& b) {
+    if (a.norm_score != b.norm_score) return a.norm_score > b.norm_score;
+    for (int i = 0; i < 3; ++i)
+        if (a.shift[i] != b.shift[i]) return a.shift[i] < b.shift[i];
+    return q_angle(Quat{a.quat[0], a.quat[1], a.quat[2], a.quat[3]}) <
+           q_angle(Quat{b.quat[0], b.quat[1], b.quat[2], b.quat[3]});
+}
+}  // namespace
+
+std::vector<ParticleResult> Context::align_batch(const float* particles, int count, const AlignConfig& cfg) {
+    if (!has_template) throw std::invalid_argument("align: set_template first");
+    cfg.validate(basis.l_max);
+    std::vector<ParticleResult> out(count);
+    if (count == 0) return out;
+    const long long vstride = (long long)n * n * n;
+    const float* fw = particles;
+    if (wedge) {  // missing-wedge restriction before any window (optimize.cpp:445)
+        filtered.reserve(sizeof(float) * vstride * count);
+        wedge->apply(particles, filtered.as<float>(), count, stream);
+        fw = filtered.as<float>();
+    }
+    std::vector<std::array<int, 3>> coarse;
+    for (int z = -cfg.shift_radius; z <= cfg.shift_radius; z += cfg.shift_step)
+        for (int y = -cfg.shift_radius; y <= cfg.shift_radius; y += cfg.shift_step)
+            for (int x = -cfg.shift_radius; x <= cfg.shift_radius; x += cfg.shift_step) coarse.push_back({x, y, z});
+    std::vector<int> wv, ws;
+    for (int p = 0; p < count; ++p)
+        for (const auto& s : coarse) {
+            wv.push_back(p);
+            ws.insert(ws.end(), s.begin(), s.end());
+        }
+    std::vector<WindowOutcome> oc = run_windows(fw, count, wv, ws, cfg);
+    std::vector<int> best(count, -1);
+    std::vector<long long> cand(count, 0), evals(count, 0);
+    std::vector<int> nwin(count, 0);
+    for (size_t i = 0; i < oc.size(); ++i) {
+        const int p = oc[i].particle;
+        cand[p] += oc[i].n_cand;
+        evals[p] += oc[i].evals;
+        ++nwin[p];
+        if (oc[i].valid && (best[p] < 0 || better(oc[i], oc[best[p]]))) best[p] = (int)i;
+    }
+    for (int p = 0; p < count; ++p)
+        if (best[p] < 0) throw std::invalid_argument("align: no usable shift window (empty subtomogram)");
+    // fine pass: unit-step cube around the coarse winner, minus coarse points (optimize.cpp:490-501)
+    std::vector<int> fv, fs;
+    for (int p = 0; p < count; ++p) {
+        const int* b = oc[best[p]].shift;
+        for (int z = -cfg.shift_step; z <= cfg.shift_step; ++z)
+            for (int y = -cfg.shift_step; y <= cfg.shift_step; ++y)
+                for (int x = -cfg.shift_step; x <= cfg.shift_step; ++x) {
+                    const std::array<int, 3> s{b[0] + x, b[1] + y, b[2] + z};
+                    if (std::find(coarse.begin(), coarse.end(), s) != coarse.end()) continue;
+                    fv.push_back(p);
+                    fs.insert(fs.end(), s.begin(), s.end());
+                }
+    }
+    std::vector<WindowOutcome> fo = run_windows(fw, count, fv, fs, cfg);
+    std::vector<WindowOutcome> bestw(count);
+    for (int p = 0; p < count; ++p) bestw[p] = oc[best[p]];
+    for (const auto& o : fo) {
+        const int p = o.particle;
+        cand[p] += o.n_cand;
+        evals[p] += o.evals;
+        ++nwin[p];
+        if (o.valid && better(o, bestw[p])) bestw[p] = o;
+    }
+    for (int p = 0; p < count; ++p) {
+        ParticleResult& r = out[p];
+        for (int i = 0; i < 3; ++i) r.shift[i] = bestw[p].shift[i];
+        for (int i = 0; i < 4; ++i) r.quat[i] = bestw[p].quat[i];
+        r.score = bestw[p].norm_score;
+        r.converged = bestw[p].converged;
+        r.candidates = cand[p];
+        r.evaluations = evals[p];
+        r.subtomo_norm = bestw[p].sub_norm;
+        r.windows = nwin[p];
+    }
+    return out;
+}
+
+}  // namespace bmb

@@ -10,6 +10,9 @@
 #include "../../include/ballmatch_b200.h"
 #include "bmb_internal.hpp"
 #include "context.hpp"
+#include "generate.hpp"
+#include "refine.cuh"
+#include "wedge.hpp"
 
 struct bm_context {
     std::unique_ptr<bmb::Context> impl;
@@ -158,6 +161,172 @@ int bm_expand(bm_context* ctx, const float* vols, int count, const int* shifts, 
         c.expand_windows(vols, stride, count, wv, ws);
         bmb::launch_to_complex(c.coef.as<float>(), count, c.geo.m_pad, c.geo, out, c.stream);
         if (cudaGetLastError() != cudaSuccess) throw std::runtime_error("kernel launch failed");
+        return (int)BM_OK;
+    });
+}
+
+
+static bmb::AlignConfig cfg_of(const bm_align_config* c) {
+    if (!c) throw std::invalid_argument("null config");
+    if (c->n_bands < 1 || c->n_bands > 16) throw std::invalid_argument("config: need fixed bands or auto band selection");
+    bmb::AlignConfig a;
+    a.bands.assign(c->bands, c->bands + c->n_bands);
+    a.seed_grid_step = c->seed_grid_step;
+    a.max_candidates = c->max_candidates;
+    a.newton_max_iter = c->newton_max_iter;
+    a.grad_tol = c->grad_tol;
+    a.step_damping = c->step_damping;
+    a.shift_radius = c->shift_radius;
+    a.shift_step = c->shift_step;
+    a.accept_tol = c->accept_tol;
+    return a;
+}
+
+int bm_set_template(bm_context* ctx, const float* tmpl, double wedge_theta_deg, void* stream) {
+    return guarded("bm_set_template", [&] {
+        if (!ctx) return (int)BM_ERR_STATE;
+        if (!tmpl) throw std::invalid_argument("null template");
+        cudaSetDevice(ctx->impl->device);
+        StreamJoin join(ctx, stream);
+        ctx->impl->set_template(tmpl, wedge_theta_deg);
+        return (int)BM_OK;
+    });
+}
+
+double bm_template_norm(const bm_context* ctx) { return ctx ? ctx->impl->t_norm : 0.0; }
+
+int bm_align_batch(bm_context* ctx, const float* particles, int count, const bm_align_config* cfg,
+                   bm_align_result* out, void* stream) {
+    return guarded("bm_align_batch", [&] {
+        if (!ctx) return (int)BM_ERR_STATE;
+        if (count < 0 || (count > 0 && (!particles || !out))) throw std::invalid_argument("bad buffers");
+        cudaSetDevice(ctx->impl->device);
+        StreamJoin join(ctx, stream);
+        const auto res = ctx->impl->align_batch(particles, count, cfg_of(cfg));
+        for (int i = 0; i < count; ++i) {
+            const auto& r = res[i];
+            bm_align_result& o = out[i];
+            for (int j = 0; j < 3; ++j) o.shift[j] = r.shift[j];
+            for (int j = 0; j < 4; ++j) o.quat[j] = r.quat[j];
+            o.score = r.score;
+            o.converged = r.converged;
+            o.candidates = r.candidates;
+            o.evaluations = r.evaluations;
+            o.subtomo_norm = r.subtomo_norm;
+            o.windows = r.windows;
+        }
+        return (int)BM_OK;
+    });
+}
+
+int bm_search_windows(bm_context* ctx, const float* vols, int n_vol, const int* win_vol,
+                      const int* win_shift, int n_win, const bm_align_config* cfg,
+                      bm_window_result* out, void* stream) {
+    return guarded("bm_search_windows", [&] {
+        if (!ctx) return (int)BM_ERR_STATE;
+        if (n_win < 0 || (n_win > 0 && (!vols || !win_vol || !win_shift || !out)))
+            throw std::invalid_argument("bad buffers");
+        for (int i = 0; i < n_win; ++i)
+            if (win_vol[i] < 0 || win_vol[i] >= n_vol) throw std::invalid_argument("window volume index out of range");
+        cudaSetDevice(ctx->impl->device);
+        StreamJoin join(ctx, stream);
+        std::vector<int> wv(win_vol, win_vol + n_win), ws(win_shift, win_shift + 3 * n_win);
+        const auto res = ctx->impl->run_windows(vols, n_vol, wv, ws, cfg_of(cfg));
+        for (int i = 0; i < n_win; ++i) {
+            const auto& r = res[i];
+            bm_window_result& o = out[i];
+            o.volume = r.particle;
+            for (int j = 0; j < 3; ++j) o.shift[j] = r.shift[j];
+            o.valid = r.valid;
+            o.n_candidates = r.n_cand;
+            o.converged = r.converged;
+            o.raw_score = r.raw_score;
+            o.norm_score = r.norm_score;
+            o.subtomo_norm = r.sub_norm;
+            for (int j = 0; j < 4; ++j) o.quat[j] = r.quat[j];
+            o.evaluations = r.evals;
+        }
+        return (int)BM_OK;
+    });
+}
+
+int bm_eval_sweep(bm_context* ctx, const double* f, int n_f, const double* t, const double* euler,
+                  int n_rot, int order, double* out, void* stream) {
+    return guarded("bm_eval_sweep", [&] {
+        if (!ctx) return (int)BM_ERR_STATE;
+        if (n_f < 0 || n_rot < 0 || order < 0 || order > 1) throw std::invalid_argument("bad sizes/order");
+        if (n_f == 0 || n_rot == 0) return (int)BM_OK;
+        auto& c = *ctx->impl;
+        cudaSetDevice(c.device);
+        StreamJoin join(ctx, stream);
+        const int ld = c.geo.m_pad;
+        c.work_f.reserve(sizeof(float) * (size_t)(n_f + 1) * ld);
+        float* fr = c.work_f.as<float>();
+        float* tr = fr + (size_t)n_f * ld;
+        bmb::launch_from_complex(f, n_f, c.geo, fr, ld, c.stream);
+        bmb::launch_from_complex(t, 1, c.geo, tr, ld, c.stream);
+        bmb::BandDev& bd = c.band(c.basis.l_max);
+        bmb::XiArgs xa;
+        xa.T = bd.view();
+        xa.row_group = bd.row_group.as<int>();
+        xa.f = fr;
+        xa.ldf = ld;
+        xa.t = tr;
+        xa.ldt = 0;
+        xa.block_off = c.geo.block_off;
+        xa.radial_count = c.geo.radial_count;
+        xa.n = n_f;
+        c.work_xi.reserve(sizeof(float2) * (size_t)n_f * bd.rows * 32);
+        xa.out = c.work_xi.as<float2>();
+        if (bmb::launch_build_xi(xa, c.stream) != 0) throw std::runtime_error("build_xi launch failed");
+        bmb::EvalArgs ea;
+        ea.T = bd.view();
+        ea.xi = xa.out;
+        ea.euler = euler;
+        ea.n_xi = n_f;
+        ea.n_rot = n_rot;
+        ea.order = order;
+        ea.out = out;
+        if (bmb::launch_eval_sweep(ea, c.stream) != 0) throw std::runtime_error("eval sweep launch failed");
+        return (int)BM_OK;
+    });
+}
+
+int bm_apply_wedge_taper(bm_context* ctx, const float* in, float* out, int count, void* stream) {
+    return guarded("bm_apply_wedge_taper", [&] {
+        if (!ctx) return (int)BM_ERR_STATE;
+        auto& c = *ctx->impl;
+        if (!c.wedge) throw std::invalid_argument("no wedge configured (bm_set_template with theta in (0,90))");
+        cudaSetDevice(c.device);
+        StreamJoin join(ctx, stream);
+        c.wedge->apply(in, out, count, c.stream);
+        return (int)BM_OK;
+    });
+}
+
+
+int bm_make_template(int device, int n, int blobs, unsigned long long seed, float* out, void* stream) {
+    return guarded("bm_make_template", [&] {
+        if (n < 8 || n % 2 || blobs < 1 || !out) throw std::invalid_argument("bad template arguments");
+        if (cudaSetDevice(device) != cudaSuccess) throw std::runtime_error("no CUDA device");
+        bmb::make_template(n, blobs, seed, out, static_cast<cudaStream_t>(stream));
+        return (int)BM_OK;
+    });
+}
+
+int bm_make_particles(int device, const float* tmpl, int n, int count, unsigned long long base_seed,
+                      int shift_max, double snr, double wedge_deg, float* out, double* quats,
+                      int* shifts, void* stream) {
+    return guarded("bm_make_particles", [&] {
+        if (n < 8 || n % 2 || count < 0 || !tmpl || (count > 0 && !out) || shift_max < 0)
+            throw std::invalid_argument("bad particle arguments");
+        if (cudaSetDevice(device) != cudaSuccess) throw std::runtime_error("no CUDA device");
+        std::vector<double> q(4 * (size_t)count);
+        std::vector<int> sh(3 * (size_t)count);
+        bmb::make_particles(tmpl, n, count, base_seed, shift_max, snr, wedge_deg, out, q.data(), sh.data(),
+                            static_cast<cudaStream_t>(stream));
+        if (quats) std::memcpy(quats, q.data(), sizeof(double) * q.size());
+        if (shifts) std::memcpy(shifts, sh.data(), sizeof(int) * sh.size());
         return (int)BM_OK;
     });
 }

@@ -1,7 +1,10 @@
 // Context construction and the batched expansion driver.
 #include "context.hpp"
 
+#include <algorithm>
 #include <stdexcept>
+
+#include "wedge.hpp"
 
 namespace bmb {
 
@@ -13,11 +16,19 @@ namespace bmb {
     } while (0)
 
 Context::Context(int dev, int n_, int l_max, double lambda_cut) : device(dev), n(n_) {
-    if (n_ < 8 || n_ % 2) throw std::invalid_argument("context: grid size must be even and >= 8");
+    // n = 0: basis-only context (coefficient-space work, no expansion operator)
+    if (n_ != 0 && (n_ < 8 || n_ % 2)) throw std::invalid_argument("context: grid size must be even and >= 8");
+    if (l_max > kMaxL) throw std::invalid_argument("context: l_max exceeds the device tables (48)");
     BMB_CUDA(cudaSetDevice(device));
     BMB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     basis = host::make_basis(l_max, lambda_cut);
-    host::Operator op = host::build_operator(basis, n);
+    host::Operator op;
+    if (n_ > 0) {
+        op = host::build_operator(basis, n);
+    } else {
+        op.rows = basis.coeffs;
+        op.m_pad = (op.rows + 127) / 128 * 128;
+    }
     voxels_host = op.voxels;
 
     geo.n = n;
@@ -56,6 +67,7 @@ Context::Context(int dev, int n_, int l_max, double lambda_cut) : device(dev), n
 
 Context::~Context() {
     cudaSetDevice(device);
+    wedge.reset();
     if (stream) {
         cudaStreamSynchronize(stream);
         cudaStreamDestroy(stream);
@@ -66,8 +78,10 @@ void Context::expand_windows(const float* vols, long long vol_stride, int n_vol,
                              const std::vector<int>& wvol, const std::vector<int>& wshift) {
     const int nw = (int)wvol.size();
     if (nw == 0) return;
+    if (geo.support == 0) throw std::invalid_argument("expand: context has no operator (n = 0)");
     const int bn = gemm_block_n;
-    const long long n_pad = (long long)(nw + bn - 1) / bn * bn;
+    const long long chunk = std::min<long long>(nw, max_chunk_windows);
+    const long long n_pad = (chunk + bn - 1) / bn * bn;
     vol_scale.reserve(sizeof(float) * n_vol);
     launch_absmax_scale(vols, n_vol, vol_stride, vol_scale.as<float>(), stream);
     upload(win_vol, wvol, stream);
@@ -76,30 +90,33 @@ void Context::expand_windows(const float* vols, long long vol_stride, int n_vol,
     B_lo.reserve(sizeof(__half) * n_pad * geo.k_pad);
     col_scale.reserve(sizeof(float) * n_pad);
     coef.reserve(sizeof(float) * (size_t)nw * geo.m_pad);
-    launch_gather_windows(vols, vol_stride, win_vol.as<int>(), win_shift.as<int>(), nw,
-                          vol_scale.as<float>(), voxels.as<int>(), geo.support, geo.k_pad, n,
-                          B_hi.as<__half>(), B_lo.as<__half>(), col_scale.as<float>(), stream);
-    SplitGemmArgs a;
-    a.fmt = 0;
-    a.block_n = bn;
-    a.kchunk = gemm_kchunk;
-    a.a_hi = E_hi.p;
-    a.a_lo = E_lo.p;
-    a.b_hi = B_hi.p;
-    a.b_lo = B_lo.p;
-    a.out = coef.as<float>();
-    a.ldo = geo.m_pad;
-    a.m_pad = geo.m_pad;
-    a.n_pad = n_pad;
-    a.k_pad = geo.k_pad;
-    a.m_valid = geo.coeffs;
-    a.n_valid = nw;
-    a.row_scale = row_scale.as<float>();
-    a.col_scale = col_scale.as<float>();
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    a.num_sms = sms;
-    if (launch_split3_gemm(a, stream) != BMB_OK) throw std::runtime_error("split3 gemm launch failed");
+    for (long long w0 = 0; w0 < nw; w0 += chunk) {
+        const int cnt = (int)std::min<long long>(chunk, nw - w0);
+        launch_gather_windows(vols, vol_stride, win_vol.as<int>() + w0, win_shift.as<int>() + 3 * w0,
+                              cnt, vol_scale.as<float>(), voxels.as<int>(), geo.support, geo.k_pad,
+                              n, B_hi.as<__half>(), B_lo.as<__half>(), col_scale.as<float>(), stream);
+        SplitGemmArgs a;
+        a.fmt = 0;
+        a.block_n = bn;
+        a.kchunk = gemm_kchunk;
+        a.a_hi = E_hi.p;
+        a.a_lo = E_lo.p;
+        a.b_hi = B_hi.p;
+        a.b_lo = B_lo.p;
+        a.out = coef.as<float>() + (size_t)w0 * geo.m_pad;
+        a.ldo = geo.m_pad;
+        a.m_pad = geo.m_pad;
+        a.n_pad = (cnt + bn - 1) / bn * bn;
+        a.k_pad = geo.k_pad;
+        a.m_valid = geo.coeffs;
+        a.n_valid = cnt;
+        a.row_scale = row_scale.as<float>();
+        a.col_scale = col_scale.as<float>();
+        a.num_sms = sms;
+        if (launch_split3_gemm(a, stream) != BMB_OK) throw std::runtime_error("split3 gemm launch failed");
+    }
 }
 
 }  // namespace bmb

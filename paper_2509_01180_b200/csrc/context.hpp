@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 #include <cufft.h>
 
+#include <complex>
 #include <map>
 #include <memory>
 #include <string>
@@ -53,7 +54,24 @@ void upload(DevBuf& d, const std::vector<T>& h, cudaStream_t s) {
         cudaMemcpyAsync(d.p, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice, s);
 }
 
-struct BandTablesHost;  // owned device storage of one band's tables
+struct WedgeFilter;
+
+// device storage of one band's evaluation tables (+ the wedge entries)
+struct BandDev {
+    int L = 0;
+    int n_items = 0, n_groups = 0, rows = 0;
+    DevBuf row_off, item_mm, item_len, bfac, bexp, P, Q, R, item_of, row_group, wedge;
+    bool has_wedge = false;
+    BandTables view() const;
+};
+
+// seed-grid tables for one (L_low, grid step) and the current template
+struct SeedDev {
+    int L_low = 0, na = 0, nb = 0, ng = 0, nxi = 0;
+    double step = 0.0;
+    DevBuf dgrid, ua, ug, wedge_sqrt;
+    bool has_wedge = false;
+};
 
 struct AlignConfig {
     std::vector<int> bands;
@@ -64,6 +82,8 @@ struct AlignConfig {
     double step_damping;
     int shift_radius;
     int shift_step;
+    double accept_tol;
+    void validate(int l_max) const;  // OptimizerConfig::validate (optimize.cpp:153-177)
 };
 
 struct ParticleResult {
@@ -103,6 +123,35 @@ public:
 
     int gemm_block_n = 128;
     int gemm_kchunk = 4;
+    long long max_chunk_windows = 8192;  // windows expanded per GEMM chunk
+
+    // ---------------------------------------------------------- template
+    DevBuf t_hat;          // real-packed FP32 template coefficients
+    double t_norm = 0.0;
+    bool has_template = false;
+    double wedge_deg = 0.0;                // <= 0 or >= 90: no wedge
+    std::unique_ptr<WedgeFilter> wedge;    // tapered filter for the particles
+    std::vector<std::complex<double>> chi_hat, q_hat;  // wedge power factors
+    double wp_total = 0.0;
+    bool wedge_active() const { return wedge_deg > 0.0 && wedge_deg < 90.0 && wp_total > 0.0; }
+    void set_template(const float* tmpl, double wedge_deg);
+
+    BandDev& band(int L);
+    SeedDev& seed_tables(int L_low, double step);
+
+    // one window stage: search_one_shift for every (volume, shift) window
+    std::vector<WindowOutcome> run_windows(const float* vols, int n_vol, const std::vector<int>& wvol,
+                                           const std::vector<int>& wshift, const AlignConfig& cfg);
+    // align() for a batch of particles (coarse + fine shift stages)
+    std::vector<ParticleResult> align_batch(const float* particles, int count, const AlignConfig& cfg);
+
+    // rotate-score-gradient sweep (config 4): kernels from coefficient pairs
+    DevBuf work_f, work_xi, filtered;
+
+private:
+    std::map<int, std::unique_ptr<BandDev>> bands_;
+    std::map<std::pair<int, long long>, std::unique_ptr<SeedDev>> seeds_;
+    DevBuf cand_, cand_count_, outcome_, win_counter_, scratch_, sub_norm_;
 };
 
 }  // namespace bmb

@@ -134,4 +134,26 @@ void launch_to_complex(const float* coef, int n_win, int ldc, const Geometry& ge
                                            reinterpret_cast<double2*>(out));
 }
 
+// reference complex layout -> real-packed rows (Re of m >= 0, Im of m > 0)
+__global__ void from_complex_kernel(const double2* __restrict__ in, int rows,
+                                    const int4* __restrict__ lkm, const int* __restrict__ block_off,
+                                    float* __restrict__ out, int ldo) {
+    const double2* c = in + (long long)blockIdx.y * rows;
+    float* o = out + (long long)blockIdx.y * ldo;
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
+        const int4 q = lkm[r];
+        const int l = q.x, k = q.y, m = q.z;
+        const double2 v = c[block_off[l] + (k - 1) * (2 * l + 1) + l + m];
+        o[r] = (float)(q.w == 0 ? v.x : v.y);
+    }
+}
+
+void launch_from_complex(const double* in, int count, const Geometry& geo, float* out, int ldo,
+                         cudaStream_t s) {
+    if (count <= 0) return;
+    dim3 grid((geo.coeffs + 255) / 256, count);
+    from_complex_kernel<<<grid, 256, 0, s>>>(reinterpret_cast<const double2*>(in), geo.coeffs,
+                                             geo.row_lkm, geo.block_off, out, ldo);
+}
+
 }  // namespace bmb

@@ -96,6 +96,8 @@ void launch_absmax_scale(const float* vols, int count, long long stride, float* 
                          cudaStream_t s);
 void launch_window_norms(const float* coef, int n_win, int ldc, const Geometry& geo,
                          double* norm, cudaStream_t s);  // sqrt(sum |f_klm|^2) over all m
+void launch_from_complex(const double* in, int count, const Geometry& geo, float* out, int ldo,
+                         cudaStream_t s);
 void launch_to_complex(const float* coef, int n_win, int ldc, const Geometry& geo, double* out,
                        cudaStream_t s);
 

@@ -1,0 +1,79 @@
+"""Alignment parity (kernels K4-K7 + host driver) against the CPU oracle on
+identical float32 inputs.  Bars (BASELINE.json north_star): rotations within
+0.5 deg geodesic, shifts exact, scores within 1e-4 relative."""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import bmo
+from paper_2509_01180_b200 import api
+
+pytestmark = pytest.mark.gpu
+
+
+def _particles(n, blobs, seed, count, shift_max, snr, wedge):
+    tmpl = bmo.gaussian_blob_template(n, blobs, seed)
+    parts, truth = [], []
+    for p in range(count):
+        s, q, sh = bmo.make_particle(tmpl, seed * 1000 + p + 1, shift_max, snr, wedge)
+        parts.append(s)
+        truth.append((q, sh))
+    return tmpl, np.stack(parts), truth
+
+
+def test_single_window_cfg1_like(cuda_device):
+    """Config-1 slice: 32^3, L=8, single window s=0, 8 starts, one band."""
+    n, L = 32, 8
+    tmpl, parts, truth = _particles(n, 20, 11, 6, 0, 0.5, None)
+    ctx = api.Context(n, L, L * math.pi)
+    ctx.set_template(tmpl.astype(np.float32))
+    cfg = api.make_config(bands=(8,), max_candidates=8)
+    got = ctx.search_windows(parts.astype(np.float32), [(i, (0, 0, 0)) for i in range(len(parts))], cfg)
+    spec = bmo.Spec(L, L * math.pi)
+    ocfg = bmo.make_config(l_max=L, lambda_cut=L * math.pi, bands=(8,), max_candidates=8)
+    for i, g in enumerate(got):
+        ref = bmo.search_window(spec, tmpl, parts[i].astype(np.float32).astype(np.float64),
+                                (0, 0, 0), ocfg)
+        ang = bmo.geodesic_degrees(g["quat"], ref["quat"])
+        assert ang < 0.5, f"particle {i}: {ang:.3f} deg"
+        assert g["norm_score"] == pytest.approx(ref["norm_score"], rel=1e-4)
+        assert g["subtomo_norm"] == pytest.approx(ref["subtomo_norm"], rel=1e-5)
+
+
+def test_windows_with_shifts_and_wedge(cuda_device):
+    n, L = 32, 8
+    tmpl, parts, truth = _particles(n, 20, 12, 3, 2, 0.5, 60.0)
+    ctx = api.Context(n, L, L * math.pi)
+    ctx.set_template(tmpl.astype(np.float32), 60.0)
+    cfg = api.make_config(bands=(4, 8), max_candidates=8)
+    f32 = parts.astype(np.float32)
+    filt = ctx.apply_wedge_taper(f32).cpu().numpy()
+    wins = [(i, s) for i in range(len(parts)) for s in [(0, 0, 0), (1, -1, 2), (-2, 0, 1)]]
+    got = ctx.search_windows(filt, wins, cfg)
+    spec = bmo.Spec(L, L * math.pi)
+    ocfg = bmo.make_config(l_max=L, lambda_cut=L * math.pi, bands=(4, 8), max_candidates=8)
+    for (i, s), g in zip(wins, got):
+        ref = bmo.search_window(spec, tmpl, f32[i].astype(np.float64), s, ocfg, wedge_deg=60.0)
+        ang = bmo.geodesic_degrees(g["quat"], ref["quat"])
+        assert ang < 0.5, f"window {(i, s)}: {ang:.3f} deg"
+        assert g["norm_score"] == pytest.approx(ref["norm_score"], rel=1e-4)
+
+
+def test_align_batch_matches_oracle(cuda_device):
+    n, L = 32, 8
+    tmpl, parts, truth = _particles(n, 20, 13, 3, 2, 1.0, None)
+    ctx = api.Context(n, L, L * math.pi)
+    ctx.set_template(tmpl.astype(np.float32))
+    cfg = api.make_config(bands=(4, 8), max_candidates=8, shift_radius=2, shift_step=2)
+    got = ctx.align_batch(parts.astype(np.float32), cfg)
+    ocfg = bmo.make_config(l_max=L, lambda_cut=L * math.pi, bands=(4, 8), max_candidates=8,
+                           shift_radius=2, shift_step=2)
+    for i, g in enumerate(got):
+        ref = bmo.align(tmpl, parts[i].astype(np.float32).astype(np.float64), ocfg)
+        assert g["shift"] == ref["shift"]
+        assert bmo.geodesic_degrees(g["quat"], ref["quat"]) < 0.5
+        assert g["score"] == pytest.approx(ref["score"], rel=1e-4)
+        assert g["windows"] == ref["windows"]
+        # ground truth: shift recovered exactly, rotation close
+        assert g["shift"] == truth[i][1]
