@@ -1,0 +1,353 @@
+#!/usr/bin/env python3
+"""Benchmark: subtomograms aligned/s (64^3, L=16) — BASELINE.json config 2.
+
+One step = align() of every particle of this rank's batch (default 1024, the
+config's subtomogram count) through the C ABI: wedge filter, 125 coarse + ~100
+fine shift windows per particle (tcgen05 expansion GEMM), seeding, device
+Newton with frequency marching L = 4 -> 8 -> 16, then the coefficient-space
+average numerator of the batch and (N > 1) one NCCL allreduce of it.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl product|reference]
+
+Under torchrun each rank aligns its own seeded shard (weak scaling, no data-path
+collective except the final allreduce).  --impl reference times the CPU
+restatement of the reference (oracle/, the reference itself cannot be built
+here) on the host cores, rank 0 only.  Prints one JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np
+
+METRIC = "subtomograms aligned/s (64^3, L=16)"
+UNIT = "subtomograms/s"
+CFG = dict(n=64, l_max=16, lambda_cut=16 * math.pi, blobs=40, shift_max=3, snr=0.1, wedge=60.0,
+           bands=(4, 8, 16), max_candidates=24, shift_radius=4, shift_step=2,
+           template_seed=20250901, particles=1024)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="product", choices=["product", "reference"])
+    ap.add_argument("--particles", type=int, default=CFG["particles"], help="per rank per step")
+    ap.add_argument("--cpu-sample", type=int, default=1, help="particles in the CPU baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200", "-f", self.path],
+                stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": []}
+        try:
+            rows = [r.split(",") for r in Path(self.path).read_text().strip().splitlines() if r.strip()]
+        except Exception:
+            return out
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].strip().replace(".", "").isdigit()]
+        if sm:
+            loaded = [x for x in sm if x > 0.5 * max(sm)] or sm
+            out["sm_mhz"] = statistics.median(loaded)
+        if mx:
+            out["sm_max_mhz"] = max(mx)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in rows:
+            if len(r) < 9:
+                continue
+            for i, nm in enumerate(names):
+                if "Active" in r[5 + i] and "Not" not in r[5 + i]:
+                    reasons.add(nm)
+        out["reasons"] = sorted(reasons)
+        out["samples"] = len(rows)
+        return out
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def oracle_config():
+    from oracle import bmo
+    return bmo.make_config(l_max=CFG["l_max"], lambda_cut=CFG["lambda_cut"], bands=CFG["bands"],
+                           max_candidates=CFG["max_candidates"], shift_radius=CFG["shift_radius"],
+                           shift_step=CFG["shift_step"], threads=cpu_cores())
+
+
+def cpu_align_seconds(tmpl, parts):
+    """The CPU restatement of align() (oracle/) on host cores: seconds for `parts`."""
+    from oracle import bmo
+    cfg = oracle_config()
+    t0 = time.perf_counter()
+    for p in parts:
+        bmo.align(tmpl, p, cfg, wedge_deg=CFG["wedge"])
+    return time.perf_counter() - t0
+
+
+def run_reference(args):
+    """--impl reference: the CPU path on the host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import bmo
+    bmo.build()
+    tmpl = bmo.gaussian_blob_template(CFG["n"], CFG["blobs"], CFG["template_seed"])
+    parts = []
+    for i in range(max(1, args.cpu_sample) * (args.steps + args.warmup)):
+        s, _, _ = bmo.make_particle(tmpl, 1000 + i, CFG["shift_max"], CFG["snr"], CFG["wedge"])
+        parts.append(s)
+    k = max(1, args.cpu_sample)
+    for w in range(args.warmup):
+        cpu_align_seconds(tmpl, parts[w * k:(w + 1) * k])
+    t = 0.0
+    for s in range(args.steps):
+        off = (args.warmup + s) * k
+        t += cpu_align_seconds(tmpl, parts[off:off + k])
+    ms = 1000.0 * t / args.steps
+    value = k / (ms / 1000.0)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded Philox phantoms, BASELINE config 2)",
+        "config": config_block(k),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu_cores(), "kind": "port",
+                         "sample": f"{k} particle(s) of config 2 per step, align() with OpenMP "
+                                   f"over shift windows (oracle/ restatement; the reference "
+                                   f"needs Eigen3/FFTW3, absent)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_block(batch):
+    return {"workload": "config2: 64^3, L=K=16, bands 4-8-16, 24 starts, shifts +-3 "
+                        "(search radius 4 step 2 + fine), SNR 0.1, +-60 deg wedge about y",
+            "particles_per_rank_per_step": batch, "template_blobs": CFG["blobs"],
+            "lambda_cut": "16*pi", "l2": "inputs larger than L2 (1 GiB of particles per rank)"}
+
+
+def run_product(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2509_01180_b200 import api
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    P = args.particles
+
+    ctx = api.Context(CFG["n"], CFG["l_max"], CFG["lambda_cut"], device=local)
+    tmpl = api.make_template(CFG["n"], CFG["blobs"], CFG["template_seed"], device=local)
+    ctx.set_template(tmpl, CFG["wedge"])
+    parts, q_true, s_true = api.make_particles(tmpl, P, 1000 + rank * 10_000_000, CFG["shift_max"],
+                                               CFG["snr"], CFG["wedge"])
+    cfg = api.make_config(bands=CFG["bands"], max_candidates=CFG["max_candidates"],
+                          shift_radius=CFG["shift_radius"], shift_step=CFG["shift_step"])
+    avg = torch.zeros((ctx.coeff_count, 2), dtype=torch.float64, device=dev)
+
+    def step(vols):
+        res = ctx.align_batch(vols, cfg)
+        avg.zero_()
+        ctx.average_accumulate(vols, res, avg)
+        if world > 1:
+            dist.all_reduce(avg)  # one NCCL allreduce of the partial average
+        return res
+
+    for _ in range(args.warmup):
+        res = step(parts)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---------------- device-resident timed region
+    ctx.set_timing(True)
+    ctx.timings(reset=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        e0.record()
+        for _ in range(args.steps):
+            res = step(parts)
+        e1.record()
+        barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    kms, counts = ctx.timings(reset=True)
+    ctx.set_timing(False)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = P * world / (ms_max / 1000.0)
+
+    # ---------------- end to end through the C ABI with host buffers
+    host = parts.cpu().pin_memory()
+    dev_buf = torch.empty_like(parts)
+    barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record()
+    for _ in range(args.steps):
+        dev_buf.copy_(host, non_blocking=True)
+        res_e2e = step(dev_buf)  # results land in host memory (bm_align_result)
+        avg_host = avg.cpu()
+    f1.record()
+    barrier()
+    e2e_ms = f0.elapsed_time(f1) / args.steps
+    t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t.item())
+    h2d = host.numel() * 4
+    import ctypes
+    from paper_2509_01180_b200 import _lib
+    d2h = P * ctypes.sizeof(_lib.AlignResult) + avg.numel() * 8
+
+    # ---------------- accuracy vs ground truth (reported, not asserted)
+    def geod(a, b):
+        return math.degrees(2 * math.acos(min(1.0, abs(float(np.dot(a, b))))))
+    errs = [geod(r["quat"], q_true[i]) for i, r in enumerate(res)]
+    shift_ok = sum(tuple(r["shift"]) == tuple(int(x) for x in s_true[i]) for i, r in enumerate(res))
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    # ---------------- roofline of the dominant kernel (CUDA-event averages)
+    peaks, peak_kind = measured_peaks()
+    steps = args.steps
+    C, V = ctx.coeff_count, ctx.support
+    gemm_ms = kms["split_gemm"] / steps
+    refine_ms = kms["refine"] / steps
+    windows_per_step = counts["windows_expanded"] / steps
+    gemm_flops = 2.0 * C * V * windows_per_step  # algorithmic (FP32-equivalent) per step
+    gemm_launches = max(1, counts["gemm_launches"] // steps)
+    peak_fp32eq = peaks["bf16_tflops"] / 3.0      # FP16 three-pass split: 3 tensor passes
+    kernels = {k: round(v / steps, 3) for k, v in kms.items()}
+    evals_per_step = sum(r["evaluations"] for r in res)
+    roof_gemm = {"kernel": "split3_gemm_kernel (tcgen05 kind::f16, 3-pass FP32 emulation)",
+                 "bound": "tensor", "achieved": gemm_flops / (gemm_ms / 1000.0) / 1e12 if gemm_ms > 0 else None,
+                 "peak": peak_fp32eq, "unit": "TFLOP/s",
+                 "peak_note": f"{peak_kind} dense bf16 {peaks['bf16_tflops']} / 3 passes",
+                 "per_launch_flops": gemm_flops / gemm_launches,
+                 "algorithmic": "2*C*V per window, C=%d V=%d" % (C, V), "traffic": None}
+    roof_gemm["frac"] = roof_gemm["achieved"] / peak_fp32eq if roof_gemm["achieved"] else None
+    dominant = "refine" if refine_ms > gemm_ms else "split_gemm"
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded Philox phantoms generated on device, BASELINE config 2)",
+        "config": config_block(P),
+        "roofline": roof_gemm,
+        "dominant_kernel": dominant,
+        "kernel_ms_per_step": kernels,
+        "refine": {"ms_per_step": refine_ms, "evaluations_per_step": evals_per_step,
+                   "note": "FP32 SIMT register recursion; see DESIGN.md for its roofline"},
+        "e2e": {"value": P * world / (e2e_ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+        "gpu_launches": counts["launches"],
+        "clocks": clk.summary(),
+        "accuracy_vs_truth": {"shift_exact": f"{shift_ok}/{P}",
+                              "rot_err_deg_median": float(np.median(errs)),
+                              "rot_err_deg_p90": float(np.percentile(errs, 90))},
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            from oracle import bmo
+            bmo.build()
+            k = max(1, args.cpu_sample)
+            tmpl_h = tmpl.double().cpu().numpy()
+            sample = [p.double().cpu().numpy() for p in parts[:k]]
+            sec = cpu_align_seconds(tmpl_h, sample)
+            line["cpu_baseline"] = {"value": k / sec, "unit": UNIT, "cores": cpu_cores(),
+                                    "kind": "port",
+                                    "sample": f"first {k} particle(s) of the batch (identical "
+                                              f"float32 bytes), oracle align() with OpenMP over "
+                                              f"shift windows, {sec:.1f} s"}
+        except Exception as exc:  # reported, never fatal
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": cpu_cores(),
+                                    "kind": "port", "sample": f"failed: {exc}"}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_product(args)
+
+
+if __name__ == "__main__":
+    main()

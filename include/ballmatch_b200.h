@@ -143,6 +143,23 @@ int bm_eval_sweep(bm_context* ctx, const double* f, int n_f, const double* t, co
  * volumes (apply_wedge_taper, src/xcorr.cpp:210-232). */
 int bm_apply_wedge_taper(bm_context* ctx, const float* in, float* out, int count, void* stream);
 
+/* Subtomogram averaging (new; building blocks rotate_expansion,
+ * src/steer.cpp:208-223): sum (device complex128, coeff_count entries,
+ * reference layout) += sum_p rotate_expansion(expand(shift_volume(f_w,p, s_p)),
+ * g_p^-1) for the particles and their align results (host).  f_w is the
+ * wedge-filtered particle when the template state has a wedge.  Dividing by
+ * the particle count (after the cross-device allreduce) gives the average. */
+int bm_average_accumulate(bm_context* ctx, const float* particles, int count,
+                          const bm_align_result* results, double* sum, void* stream);
+
+/* Kernel timing evidence: with timing on, CUDA events on the context stream
+ * bracket every launch of this library.  out_ms[0..5]: gather, split GEMM,
+ * seed, refine, wedge filter, misc (milliseconds, accumulated since reset);
+ * out_counts[0..3]: kernels launched, windows expanded, GEMM launches,
+ * refine launches.  reset != 0 clears after reading. */
+int bm_context_set_timing(bm_context* ctx, int on);
+int bm_context_timings(bm_context* ctx, double* out_ms, long long* out_counts, int reset);
+
 /* ------------------------------------------------------------------ synthetic inputs
  * Seeded generator on the device (BASELINE.json configs; particle pipeline of
  * make_phantom, src/volio.cpp:285-314).  Template: isotropic Gaussian blobs

@@ -97,6 +97,12 @@ def _declare(L: C.CDLL) -> None:
     L.bm_eval_sweep.restype = I
     L.bm_apply_wedge_taper.argtypes = [P, P, P, I, P]
     L.bm_apply_wedge_taper.restype = I
+    L.bm_average_accumulate.argtypes = [P, P, I, P, P, P]
+    L.bm_average_accumulate.restype = I
+    L.bm_context_set_timing.argtypes = [P, I]
+    L.bm_context_set_timing.restype = I
+    L.bm_context_timings.argtypes = [P, P, P, I]
+    L.bm_context_timings.restype = I
     L.bm_make_template.argtypes = [I, I, I, C.c_ulonglong, P, P]
     L.bm_make_template.restype = I
     L.bm_make_particles.argtypes = [I, P, I, I, C.c_ulonglong, I, D, D, P, P, P, P]

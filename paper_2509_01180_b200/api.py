@@ -179,6 +179,25 @@ class Context:
                      evaluations=r.evaluations, subtomo_norm=r.subtomo_norm, windows=r.windows)
                 for r in out[:count]]
 
+    def average_accumulate(self, particles, results, out=None):
+        """Coefficient-space average numerator: out (complex128, coeff_count, device) +=
+        sum_p rotate_expansion(f_hat_{p,s_p}, g_p^-1)."""
+        torch = _torch()
+        v = self._dev(particles)
+        count = v.shape[0]
+        if out is None:
+            out = torch.zeros((self.coeff_count, 2), dtype=torch.float64, device=v.device)
+        res = (_lib.AlignResult * max(count, 1))()
+        for i, r in enumerate(results):
+            for j in range(3):
+                res[i].shift[j] = int(r["shift"][j])
+            for j in range(4):
+                res[i].quat[j] = float(r["quat"][j])
+        _lib.check(_lib.lib().bm_average_accumulate(self._h, C.c_void_p(v.data_ptr()), count, res,
+                                                    C.c_void_p(out.data_ptr()), self._stream(v)),
+                   "average")
+        return out
+
     def search_windows(self, vols, windows, cfg: _lib.AlignConfig):
         """search_one_shift for explicit (volume index, (sx, sy, sz)) windows."""
         v = self._dev(vols)
@@ -204,3 +223,16 @@ class Context:
                                                    C.c_void_p(out.data_ptr()), v.shape[0],
                                                    self._stream(v)), "apply_wedge_taper")
         return out
+
+    # ------------------------------------------------------------------ evidence
+    def set_timing(self, on: bool = True):
+        _lib.check(_lib.lib().bm_context_set_timing(self._h, 1 if on else 0), "set_timing")
+
+    def timings(self, reset: bool = False):
+        ms = (C.c_double * 6)()
+        cnt = (C.c_longlong * 4)()
+        _lib.check(_lib.lib().bm_context_timings(self._h, ms, cnt, 1 if reset else 0), "timings")
+        names = ("gather", "split_gemm", "seed", "refine", "wedge", "misc")
+        return (dict(zip(names, ms[:])),
+                dict(launches=cnt[0], windows_expanded=cnt[1], gemm_launches=cnt[2],
+                     refine_launches=cnt[3]))

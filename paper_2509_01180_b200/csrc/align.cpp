@@ -52,9 +52,7 @@ BandTables BandDev::view() const {
     t.item_len = item_len.as<int>();
     t.bfac = bfac.as<float>();
     t.bexp = bexp.as<int>();
-    t.P = P.as<float>();
-    t.Q = Q.as<float>();
-    t.R = R.as<float>();
+    t.PQR = PQR.as<float4>();
     t.item_of = item_of.as<int16_t>();
     t.wedge = has_wedge ? wedge.as<float2>() : nullptr;
     return t;
@@ -82,9 +80,9 @@ BandDev& Context::band(int L) {
     upload(b->item_len, h.item_len, stream);
     upload(b->bfac, h.bfac, stream);
     upload(b->bexp, h.bexp, stream);
-    upload(b->P, h.P, stream);
-    upload(b->Q, h.Q, stream);
-    upload(b->R, h.R, stream);
+    std::vector<float4> pqr(h.P.size());
+    for (size_t i = 0; i < pqr.size(); ++i) pqr[i] = make_float4(h.P[i], h.Q[i], h.R[i], 0.0f);
+    upload(b->PQR, pqr, stream);
     upload(b->item_of, h.item_of, stream);
     std::vector<int> rg(h.rows);
     for (int g = 0; g < h.n_groups; ++g)
@@ -216,7 +214,10 @@ std::vector<WindowOutcome> Context::run_windows(const float* vols, int n_vol, co
     const long long vstride = (long long)n * n * n;
     expand_windows(vols, vstride, n_vol, wvol, wshift);
     sub_norm_.reserve(sizeof(double) * nw);
+    cudaEvent_t t0 = timer.begin(stream);
     launch_window_norms(coef.as<float>(), nw, geo.m_pad, geo, sub_norm_.as<double>(), stream);
+    ++timer.launches;
+    timer.end(K_MISC, t0, stream);
 
     const int maxc = cfg.max_candidates;
     cand_.reserve(sizeof(CandState) * (size_t)nw * maxc);
@@ -243,7 +244,10 @@ std::vector<WindowOutcome> Context::run_windows(const float* vols, int n_vol, co
     sa.max_cand = maxc;
     sa.cand = cand_.as<CandState>();
     sa.cand_count = cand_count_.as<int>();
+    cudaEvent_t s0 = timer.begin(stream);
     if (launch_seed(sa, nw, stream) != 0) throw std::runtime_error("seed kernel launch failed");
+    ++timer.launches;
+    timer.end(K_SEED, s0, stream);
 
     const Quat koff = q_from_euler(0.0, kPiH / 2.0, 0.0);
     for (size_t bi = 0; bi < cfg.bands.size(); ++bi) {
@@ -287,11 +291,16 @@ std::vector<WindowOutcome> Context::run_windows(const float* vols, int n_vol, co
         ra.grid_evals = (long long)sd.na * sd.nb * sd.ng;
         ra.out = outcome_.as<WindowOutcome>();
         ck(cudaMemsetAsync(win_counter_.p, 0, sizeof(int), stream), "counter");
+        cudaEvent_t r0 = timer.begin(stream);
         if (launch_refine(ra, blocks, stream) != 0) throw std::runtime_error("refine kernel launch failed");
+        ++timer.launches;
+        ++timer.refine_launches;
+        timer.end(K_REFINE, r0, stream);
     }
     ck(cudaMemcpyAsync(res.data(), outcome_.p, sizeof(WindowOutcome) * nw, cudaMemcpyDeviceToHost, stream),
        "outcomes");
     ck(cudaStreamSynchronize(stream), "run_windows");
+    timer.collect();
     return res;
 }
 
@@ -315,7 +324,10 @@ std::vector<ParticleResult> Context::align_batch(const float* particles, int cou
     const float* fw = particles;
     if (wedge) {  // missing-wedge restriction before any window (optimize.cpp:445)
         filtered.reserve(sizeof(float) * vstride * count);
+        cudaEvent_t w0 = timer.begin(stream);
         wedge->apply(particles, filtered.as<float>(), count, stream);
+        ++timer.launches;  // the profile multiply (cuFFT kernels are library launches)
+        timer.end(K_WEDGE, w0, stream);
         fw = filtered.as<float>();
     }
     std::vector<std::array<int, 3>> coarse;

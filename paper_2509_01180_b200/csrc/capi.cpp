@@ -10,6 +10,7 @@
 #include "../../include/ballmatch_b200.h"
 #include "bmb_internal.hpp"
 #include "context.hpp"
+#include "average.hpp"
 #include "generate.hpp"
 #include "refine.cuh"
 #include "wedge.hpp"
@@ -304,6 +305,61 @@ int bm_apply_wedge_taper(bm_context* ctx, const float* in, float* out, int count
     });
 }
 
+
+int bm_average_accumulate(bm_context* ctx, const float* particles, int count,
+                          const bm_align_result* results, double* sum, void* stream) {
+    return guarded("bm_average_accumulate", [&] {
+        if (!ctx) return (int)BM_ERR_STATE;
+        if (count < 0 || (count > 0 && (!particles || !results || !sum))) throw std::invalid_argument("bad buffers");
+        if (count == 0) return (int)BM_OK;
+        auto& c = *ctx->impl;
+        cudaSetDevice(c.device);
+        StreamJoin join(ctx, stream);
+        const long long vstride = (long long)c.n * c.n * c.n;
+        const float* fw = particles;
+        if (c.wedge) {
+            c.filtered.reserve(sizeof(float) * vstride * count);
+            c.wedge->apply(particles, c.filtered.as<float>(), count, c.stream);
+            ++c.timer.launches;
+            fw = c.filtered.as<float>();
+        }
+        std::vector<int> wv(count), ws(3 * count);
+        std::vector<double> q(4 * (size_t)count);
+        for (int i = 0; i < count; ++i) {
+            wv[i] = i;
+            for (int j = 0; j < 3; ++j) ws[3 * i + j] = results[i].shift[j];
+            for (int j = 0; j < 4; ++j) q[4 * i + j] = results[i].quat[j];
+        }
+        c.expand_windows(fw, vstride, count, wv, ws);
+        bmb::upload(c.work_xi, q, c.stream);
+        bmb::launch_average(c.coef.as<float>(), c.geo.m_pad, c.work_xi.as<double>(), count, c.basis.l_max,
+                            c.geo.block_off, c.geo.radial_count, sum, c.stream);
+        ++c.timer.launches;
+        return (int)BM_OK;
+    });
+}
+
+int bm_context_set_timing(bm_context* ctx, int on) {
+    if (!ctx) return BM_ERR_STATE;
+    ctx->impl->timer.on = on != 0;
+    return BM_OK;
+}
+
+int bm_context_timings(bm_context* ctx, double* out_ms, long long* out_counts, int reset) {
+    if (!ctx) return BM_ERR_STATE;
+    auto& t = ctx->impl->timer;
+    t.collect();
+    if (out_ms)
+        for (int i = 0; i < bmb::K_COUNT; ++i) out_ms[i] = t.ms[i];
+    if (out_counts) {
+        out_counts[0] = t.launches;
+        out_counts[1] = t.windows_expanded;
+        out_counts[2] = t.gemm_launches;
+        out_counts[3] = t.refine_launches;
+    }
+    if (reset) t.reset();
+    return BM_OK;
+}
 
 int bm_make_template(int device, int n, int blobs, unsigned long long seed, float* out, void* stream) {
     return guarded("bm_make_template", [&] {

@@ -83,7 +83,10 @@ void Context::expand_windows(const float* vols, long long vol_stride, int n_vol,
     const long long chunk = std::min<long long>(nw, max_chunk_windows);
     const long long n_pad = (chunk + bn - 1) / bn * bn;
     vol_scale.reserve(sizeof(float) * n_vol);
+    cudaEvent_t t0 = timer.begin(stream);
     launch_absmax_scale(vols, n_vol, vol_stride, vol_scale.as<float>(), stream);
+    ++timer.launches;
+    timer.end(K_MISC, t0, stream);
     upload(win_vol, wvol, stream);
     upload(win_shift, wshift, stream);
     B_hi.reserve(sizeof(__half) * n_pad * geo.k_pad);
@@ -94,9 +97,12 @@ void Context::expand_windows(const float* vols, long long vol_stride, int n_vol,
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     for (long long w0 = 0; w0 < nw; w0 += chunk) {
         const int cnt = (int)std::min<long long>(chunk, nw - w0);
+        cudaEvent_t g0 = timer.begin(stream);
         launch_gather_windows(vols, vol_stride, win_vol.as<int>() + w0, win_shift.as<int>() + 3 * w0,
                               cnt, vol_scale.as<float>(), voxels.as<int>(), geo.support, geo.k_pad,
                               n, B_hi.as<__half>(), B_lo.as<__half>(), col_scale.as<float>(), stream);
+        ++timer.launches;
+        timer.end(K_GATHER, g0, stream);
         SplitGemmArgs a;
         a.fmt = 0;
         a.block_n = bn;
@@ -115,7 +121,12 @@ void Context::expand_windows(const float* vols, long long vol_stride, int n_vol,
         a.row_scale = row_scale.as<float>();
         a.col_scale = col_scale.as<float>();
         a.num_sms = sms;
+        cudaEvent_t m0 = timer.begin(stream);
         if (launch_split3_gemm(a, stream) != BMB_OK) throw std::runtime_error("split3 gemm launch failed");
+        ++timer.launches;
+        ++timer.gemm_launches;
+        timer.windows_expanded += cnt;
+        timer.end(K_GEMM, m0, stream);
     }
 }
 

@@ -60,7 +60,7 @@ struct WedgeFilter;
 struct BandDev {
     int L = 0;
     int n_items = 0, n_groups = 0, rows = 0;
-    DevBuf row_off, item_mm, item_len, bfac, bexp, P, Q, R, item_of, row_group, wedge;
+    DevBuf row_off, item_mm, item_len, bfac, bexp, PQR, item_of, row_group, wedge;
     bool has_wedge = false;
     BandTables view() const;
 };
@@ -97,8 +97,50 @@ struct ParticleResult {
     int windows;
 };
 
+// Per-kernel-class CUDA-event timing on the context stream (bench evidence).
+enum KClass { K_GATHER = 0, K_GEMM, K_SEED, K_REFINE, K_WEDGE, K_MISC, K_COUNT };
+struct KernelTimer {
+    bool on = false;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+    double ms[K_COUNT] = {0};
+    long long launches = 0;        // kernels of this library launched (always counted)
+    long long windows_expanded = 0;
+    long long gemm_launches = 0, refine_launches = 0;
+    cudaEvent_t begin(cudaStream_t s) {
+        if (!on) return nullptr;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, s);
+        return e;
+    }
+    void end(int cls, cudaEvent_t b, cudaStream_t s) {
+        if (!on || !b) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, s);
+        pending.push_back({cls, {b, e}});
+    }
+    void collect() {
+        for (auto& p : pending) {
+            float t = 0.f;
+            cudaEventSynchronize(p.second.second);
+            cudaEventElapsedTime(&t, p.second.first, p.second.second);
+            ms[p.first] += t;
+            cudaEventDestroy(p.second.first);
+            cudaEventDestroy(p.second.second);
+        }
+        pending.clear();
+    }
+    void reset() {
+        collect();
+        for (double& x : ms) x = 0.0;
+        launches = windows_expanded = gemm_launches = refine_launches = 0;
+    }
+};
+
 class Context {
 public:
+    KernelTimer timer;
     Context(int device, int n, int l_max, double lambda_cut);
     ~Context();
 

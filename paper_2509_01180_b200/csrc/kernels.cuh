@@ -25,9 +25,8 @@ struct BandTables {
     const int* item_len = nullptr;   // [n_groups*32] steps of the item (0 for padding)
     const float* bfac = nullptr;     // [n_groups*32] sign * sqrt_binom of the border closed form
     const int* bexp = nullptr;       // [n_groups*32] packed exponents: a | p << 8 (cos^a sin^p)
-    const float* P = nullptr;        // [rows*32] t1 = P cos b + Q, t1' = -P sin b, t1'' = -P cos b
-    const float* Q = nullptr;
-    const float* R = nullptr;        // t2
+    const float4* PQR = nullptr;     // [rows*32] (P, Q, R, 0): t1 = P cos b + Q,
+                                     // t1' = -P sin b, t1'' = -P cos b, t2 = R
     const int16_t* item_of = nullptr;  // [(2L+1)^2]: item index of (m,m') (>=0) or -(idx+1) for
                                        // the conjugate partner (-m,-m') of a half-plane item
     const float2* wedge = nullptr;     // [rows*32] wedge-power kernel entries (or null)

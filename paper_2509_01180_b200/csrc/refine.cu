@@ -57,7 +57,7 @@ __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
 // angles (alpha, beta, gamma), band T.L.  Warp-cooperative; all lanes return
 // the same (FP64) results.
 template <int ORDER, bool WEDGE>
-__device__ void warp_eval(const BandTables& T, const float2* xi, const float2* wx, double alpha,
+__device__ __noinline__ void warp_eval(const BandTables& T, const float2* xi, const float2* wx, double alpha,
                           double beta, double gamma, WarpScratch& ws, Derivs& c, Derivs& r) {
     const int lane = threadIdx.x & 31;
     const int L = T.L;
@@ -71,10 +71,14 @@ __device__ void warp_eval(const BandTables& T, const float2* xi, const float2* w
     }
     const double ch = cos(0.5 * beta), sh = sin(0.5 * beta);
     for (int j = lane; j <= 2 * L + 2; j += 32) {
-        double pc = 1.0, ps = 1.0;
-        for (int q = 0; q < j; ++q) {
-            pc *= ch;
-            ps *= sh;
+        double pc = 1.0, ps = 1.0, bc = ch, bs = sh;  // binary exponentiation
+        for (int e = j; e; e >>= 1) {
+            if (e & 1) {
+                pc *= bc;
+                ps *= bs;
+            }
+            bc *= bc;
+            bs *= bs;
         }
         ws.cp[j] = (float)pc;
         ws.sp[j] = (float)ps;
@@ -119,9 +123,11 @@ __device__ void warp_eval(const BandTables& T, const float2* xi, const float2* w
             W1 = make_float2(w0.x * dp, w0.y * dp);
             W2 = make_float2(w0.x * dpp, w0.y * dpp);
         }
+#pragma unroll 2
         for (int s = 1; s < glen; ++s) {
             const int at = (r0 + s) * 32 + lane;
-            const float P = __ldg(T.P + at), Q = __ldg(T.Q + at), R = __ldg(T.R + at);
+            const float4 pqr = __ldg(T.PQR + at);
+            const float P = pqr.x, Q = pqr.y, R = pqr.z;
             const float t1 = fmaf(P, cb, Q);
             const float dn = t1 * d - R * d1;
             float dpn = 0.0f, dppn = 0.0f;
@@ -497,7 +503,7 @@ __device__ float2 xi_entry(const BandTables& T, const int* row_group, const floa
     const int am = abs(m), amp = abs(mp);
     const float sm = (m < 0 && (am & 1)) ? -1.0f : 1.0f;
     const float smp = (mp < 0 && (amp & 1)) ? -1.0f : 1.0f;
-    double re = 0.0, im = 0.0;
+    float re = 0.0f, im = 0.0f;
     for (int k = 0; k < nk; ++k) {
         const float* fr = f + base + k * (2 * l + 1);
         const float* tr = t + base + k * (2 * l + 1);
@@ -505,13 +511,13 @@ __device__ float2 xi_entry(const BandTables& T, const int* row_group, const floa
         if (m < 0) fre *= sm, fim *= -sm;
         float tre = tr[amp == 0 ? 0 : 2 * amp - 1], tim = amp == 0 ? 0.0f : tr[2 * amp];
         if (mp < 0) tre *= smp, tim *= -smp;
-        re += (double)fre * tre + (double)fim * tim;
-        im += (double)fre * tim - (double)fim * tre;
+        re = fmaf(fre, tre, fmaf(fim, tim, re));  // conj(f) * t
+        im = fmaf(fre, tim, fmaf(-fim, tre, im));
     }
-    return make_float2((float)re, (float)im);
+    return make_float2(re, im);
 }
 
-__global__ void __launch_bounds__(kWarps * 32) refine_kernel(RefineArgs a) {
+__global__ void __launch_bounds__(kWarps * 32, 2) refine_kernel(RefineArgs a) {
     extern __shared__ __align__(16) unsigned char sm[];
     const BandTables& T = a.T;
     float2* xi = reinterpret_cast<float2*>(sm);                        // rows*32
