@@ -197,6 +197,14 @@ void Context::set_template(const float* tmpl, double wedge_theta) {
         chi_hat = std::move(f.chi_hat);
         q_hat = std::move(f.q_hat);
         wp_total = f.total;
+        std::vector<double2> cd(chi_hat.size()), qd(q_hat.size());
+        for (size_t i = 0; i < cd.size(); ++i) {
+            cd[i] = double2{chi_hat[i].real(), chi_hat[i].imag()};
+            qd[i] = double2{q_hat[i].real(), q_hat[i].imag()};
+        }
+        upload(chi_dev, cd, stream);
+        upload(q_dev, qd, stream);
+        ck(cudaStreamSynchronize(stream), "wedge factors");
     }
     // band tables carry the wedge entries of this template: rebuild lazily
     bands_.clear();
@@ -267,9 +275,11 @@ std::vector<WindowOutcome> Context::run_windows(const float* vols, int n_vol, co
         ra.max_cand = maxc;
         ra.n_win = nw;
         ra.win_counter = win_counter_.as<int>();
-        const int blocks = std::min(nw, refine_resident_blocks(ra.T, ra.rows_band, maxc, device));
+        ra.batch = refine_batch(ra.T, ra.rows_band);
+        const int blocks = std::min((nw + ra.batch - 1) / ra.batch,
+                                    refine_resident_blocks(ra.T, ra.rows_band, ra.batch, device));
         ra.scratch_per_warp = (refine_scratch_floats(ra.T) + 3) / 4 * 4;
-        scratch_.reserve(sizeof(float) * (size_t)blocks * 8 * ra.scratch_per_warp);
+        scratch_.reserve(sizeof(float) * (size_t)blocks * refine_warps() * ra.scratch_per_warp);
         ra.scratch = scratch_.as<float>();
         ra.prm.band = L;
         ra.prm.newton_max_iter = cfg.newton_max_iter;
@@ -290,6 +300,11 @@ std::vector<WindowOutcome> Context::run_windows(const float* vols, int n_vol, co
         ra.win_shift = win_shift.as<int>();
         ra.grid_evals = (long long)sd.na * sd.nb * sd.ng;
         ra.out = outcome_.as<WindowOutcome>();
+        if (wedge_active()) {
+            ra.chi_hat = chi_dev.as<double2>();
+            ra.q_hat = q_dev.as<double2>();
+            ra.wp_total = wp_total;
+        }
         ck(cudaMemsetAsync(win_counter_.p, 0, sizeof(int), stream), "counter");
         cudaEvent_t r0 = timer.begin(stream);
         if (launch_refine(ra, blocks, stream) != 0) throw std::runtime_error("refine kernel launch failed");

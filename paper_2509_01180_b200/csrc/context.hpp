@@ -175,6 +175,7 @@ public:
     std::unique_ptr<WedgeFilter> wedge;    // tapered filter for the particles
     std::vector<std::complex<double>> chi_hat, q_hat;  // wedge power factors
     double wp_total = 0.0;
+    DevBuf chi_dev, q_dev;  // device copies of chi_hat / q_hat
     bool wedge_active() const { return wedge_deg > 0.0 && wedge_deg < 90.0 && wp_total > 0.0; }
     void set_template(const float* tmpl, double wedge_deg);
 

@@ -280,111 +280,155 @@ __device__ void eval_objective(const BandTables& T, const float2* xi, const floa
 }
 
 // ---------------------------------------------------------------- anchoring
-__device__ double sqrt_binom_d(int n, int k) {
-    double r = 1.0;
-    for (int i = 1; i <= k; ++i) r *= (double)(n - k + i) / i;
-    return sqrt(r);
-}
-__device__ double ipow_d(double x, int e) {
-    double r = 1.0;
-    for (int i = 0; i < e; ++i) r *= x;
-    return r;
-}
 __host__ __device__ __forceinline__ int xi_off(int l) { return l * (2 * l - 1) * (2 * l + 1) / 3; }
 
-// value of a band-layout kernel at (l, m, n), any orders, via the item map and
-// the real-volume symmetry
-__device__ float2 band_at(const BandTables& T, const float2* src, int l, int m, int n) {
-    const int L = T.L;
-    const int v = T.item_of[(m + L) * (2 * L + 1) + (n + L)];
-    const int i = v >= 0 ? v : -v - 1;
-    const int l0 = max(abs(m), abs(n));
-    const float2 x = src[(T.row_off[i >> 5] + l - l0) * 32 + (i & 31)];
-    if (v >= 0) return x;
-    const float sg = ((m + n) & 1) ? -1.0f : 1.0f;
-    return make_float2(sg * x.x, -sg * x.y);
-}
-
-// xi~_l = xi_l D^l(a)^T  (xi_compose_right, src/xcorr.cpp:149-155) for the
-// correlation kernel and the wedge-power kernel, written in band layout.
-__device__ void compose_kernels(const BandTables& T, const float2* src, const float2* src_w,
-                                const Quat& anchor, float* dtab, float2* out, float2* out_w,
+// xi~_l = xi_l D^l(a)^T  (xi_compose_right, src/xcorr.cpp:149-155), with
+// D^l_{m'n}(a) = e^{-i m' a} d^l_{m'n}(b) e^{-i n g}:
+//   xi~_l[m,m'] = e^{-i m' a} sum_n (xi_l[m,n] e^{-i n g}) d^l_{m'n}(b).
+// The full-plane d^l(b) comes from the same band tables as the evaluation
+// (half-plane chains + d_{-m,-m'} = (-1)^{m-m'} d_{m,m'}); xi is unpacked into a
+// dense, phase-folded scratch so the n-sum runs over contiguous rows.  The
+// wedge-power kernel is rank one (conj(chi_lm) q_lm' / total), so its
+// composition only rotates q: q~_l = D^l(a) q_l  (O(l^2) per degree).
+__device__ void compose_kernels(const BandTables& T, const float2* src, const RefineArgs& a,
+                                const Quat& anchor, float* scratch, float2* out, float2* out_w,
                                 WarpScratch& ws) {
     const int lane = threadIdx.x & 31;
-    const int L = T.L, W = 2 * L + 1;
+    const int L = T.L;
+    const int nxi = xi_off(L + 1);
+    float* dtab = scratch;                                                  // nxi floats
+    float2* xd = reinterpret_cast<float2*>(scratch + ((nxi + 1) & ~1));    // nxi complex
+    float2* qt = xd + nxi;                                                  // (L+1)^2 complex
     const Euler3 e = q_euler(anchor);
-    const double cb = cos(e.b), ch = cos(0.5 * e.b), sh = sin(0.5 * e.b);
     __syncwarp();
-    // full-plane little-d^l(beta_a), FP64 chains (steer.cpp:43-144)
-    for (int idx = lane; idx < W * W; idx += 32) {
-        const int m = idx / W - L, n = idx % W - L;
-        const int l0 = max(abs(m), abs(n));
-        double fac;
-        int pa, pp;
-        if (l0 == 0) {
-            fac = 1.0, pa = pp = 0;
-        } else if (m == l0) {
-            fac = (((l0 - n) & 1) ? -1.0 : 1.0) * sqrt_binom_d(2 * l0, l0 + n), pa = l0 + n, pp = l0 - n;
-        } else if (m == -l0) {
-            fac = sqrt_binom_d(2 * l0, l0 + n), pa = l0 - n, pp = l0 + n;
-        } else if (n == l0) {
-            fac = sqrt_binom_d(2 * l0, l0 + m), pa = l0 + m, pp = l0 - m;
-        } else {
-            fac = (((l0 + m) & 1) ? -1.0 : 1.0) * sqrt_binom_d(2 * l0, l0 + m), pa = l0 - m, pp = l0 + m;
-        }
-        double dcur = fac * (ipow_d(ch, pa) * ipow_d(sh, pp)), dprev = 0.0;
-        dtab[xi_off(l0) + (m + l0) * (2 * l0 + 1) + (n + l0)] = (float)dcur;
-        for (int l = l0 + 1; l <= L; ++l) {
-            double dn;
-            if (l == 1) {
-                dn = cb;
-            } else {
-                const double a2 = sqrt(((double)l * l - (double)m * m) * ((double)l * l - (double)n * n));
-                const double den = (l - 1.0) * a2;
-                const double t1 = (2.0 * l - 1.0) * (l * (l - 1.0) * cb - (double)m * n) / den;
-                const bool has2 = abs(m) <= l - 2 && abs(n) <= l - 2;
-                const double b2 = has2 ? sqrt(((double)(l - 1) * (l - 1) - (double)m * m) *
-                                              ((double)(l - 1) * (l - 1) - (double)n * n))
-                                       : 0.0;
-                dn = t1 * dcur - (has2 ? l * b2 / den * dprev : 0.0);
-            }
-            dprev = dcur;
-            dcur = dn;
-            dtab[xi_off(l) + (m + l) * (2 * l + 1) + (n + l)] = (float)dcur;
-        }
-    }
     for (int m = lane; m <= L; m += 32) {
-        double s, co;
-        sincos(m * e.a, &s, &co);
-        ws.ua[m] = make_float2((float)co, (float)-s);
-        sincos(m * e.g, &s, &co);
-        ws.ug[m] = make_float2((float)co, (float)-s);
+        double sn, co;
+        sincos(m * e.a, &sn, &co);
+        ws.ua[m] = make_float2((float)co, (float)-sn);
+        sincos(m * e.g, &sn, &co);
+        ws.ug[m] = make_float2((float)co, (float)-sn);
+    }
+    const double ch = cos(0.5 * e.b), sh = sin(0.5 * e.b);
+    for (int j = lane; j <= 2 * L + 2; j += 32) {
+        double pc = 1.0, ps = 1.0, bc = ch, bs = sh;
+        for (int q = j; q; q >>= 1) {
+            if (q & 1) {
+                pc *= bc;
+                ps *= bs;
+            }
+            bc *= bc;
+            bs *= bs;
+        }
+        ws.cp[j] = (float)pc;
+        ws.sp[j] = (float)ps;
     }
     __syncwarp();
-    for (int item = lane; item < T.n_items; item += 32) {
+    const float cb = (float)cos(e.b);
+    // full-plane d^l_{m,m'}(b_a): half-plane chains + mirror
+    for (int g = 0; g < T.n_groups; ++g) {
+        const int item = g * 32 + lane;
+        const int len = T.item_len[item];
         const int m = T.item_mm[item].x, mp = T.item_mm[item].y;
         const int l0 = max(abs(m), abs(mp));
-        float2 em = ws.ua[abs(mp)];
-        if (mp < 0) em.y = -em.y;
-        const int base = T.row_off[item >> 5] * 32 + (item & 31);
-        for (int l = l0; l <= L; ++l) {
-            float2 acc = make_float2(0.f, 0.f), accw = make_float2(0.f, 0.f);
-            const float* drow = dtab + xi_off(l) + (mp + l) * (2 * l + 1) + l;  // d^l_{m',n}
-            for (int n = -l; n <= l; ++n) {
-                float2 eg = ws.ug[abs(n)];
-                if (n < 0) eg.y = -eg.y;
-                const float d = drow[n];
-                const float2 x = cmul(band_at(T, src, l, m, n), eg);
-                acc.x = fmaf(x.x, d, acc.x);
-                acc.y = fmaf(x.y, d, acc.y);
-                if (src_w) {
-                    const float2 y = cmul(band_at(T, src_w, l, m, n), eg);
-                    accw.x = fmaf(y.x, d, accw.x);
-                    accw.y = fmaf(y.y, d, accw.y);
-                }
+        const int be = T.bexp[item];
+        float d = T.bfac[item] * ws.cp[be & 0xff] * ws.sp[be >> 8], d1 = 0.0f;
+        const float mir = ((m - mp) & 1) ? -1.0f : 1.0f;
+        const int r0 = T.row_off[g];
+        for (int s = 0; s < len; ++s) {
+            if (s > 0) {
+                const float4 pqr = __ldg(T.PQR + (r0 + s) * 32 + lane);
+                const float dn = fmaf(pqr.x, cb, pqr.y) * d - pqr.z * d1;
+                d1 = d;
+                d = dn;
             }
-            out[base + (l - l0) * 32] = cmul(em, acc);
-            if (src_w) out_w[base + (l - l0) * 32] = cmul(em, accw);
+            const int l = l0 + s, w = 2 * l + 1, o = xi_off(l);
+            dtab[o + (m + l) * w + (mp + l)] = d;
+            dtab[o + (-m + l) * w + (-mp + l)] = mir * d;
+        }
+    }
+    // dense xi'_l[m,n] = xi_l[m,n] e^{-i n g} (both half-planes)
+    for (int at = lane; at < T.rows * 32; at += 32) {
+        const int row = at >> 5, j = at & 31;
+        const int g = a.row_group[row];
+        const int item = g * 32 + j;
+        const int s = row - T.row_off[g];
+        if (s >= T.item_len[item]) continue;
+        const int m = T.item_mm[item].x, mp = T.item_mm[item].y;
+        const int l = max(abs(m), abs(mp)) + s, w = 2 * l + 1, o = xi_off(l);
+        const float2 x = src[at];
+        float2 eg = ws.ug[abs(mp)];
+        if (mp < 0) eg.y = -eg.y;
+        xd[o + (m + l) * w + (mp + l)] = cmul(x, eg);
+        const float sg = ((m + mp) & 1) ? -1.0f : 1.0f;
+        const float2 xm = make_float2(sg * x.x, -sg * x.y);  // xi[-m,-m']
+        xd[o + (-m + l) * w + (-mp + l)] = cmul(xm, make_float2(eg.x, -eg.y));
+    }
+    // wedge: q~_l[m'] = e^{-i m' a} sum_n d_{m'n} e^{-i n g} q_ln
+    const bool wedge = out_w != nullptr;
+    if (wedge) {
+        for (int idx = lane; idx < (L + 1) * (L + 1); idx += 32) {
+            int l = 0;
+            while ((l + 1) * (l + 1) <= idx) ++l;
+            const int mp = idx - l * l - l;
+            const int w = 2 * l + 1, o = xi_off(l);
+            float re = 0.0f, im = 0.0f;
+            for (int n = -l; n <= l; ++n) {
+                const int an = abs(n);
+                double2 qv = a.q_hat[l * (l + 1) / 2 + an];
+                if (n < 0) {
+                    const double sgn = (an & 1) ? -1.0 : 1.0;
+                    qv = make_double2(sgn * qv.x, -sgn * qv.y);
+                }
+                float2 eg = ws.ug[an];
+                if (n < 0) eg.y = -eg.y;
+                const float2 t = cmul(make_float2((float)qv.x, (float)qv.y), eg);
+                const float dv = dtab[o + (mp + l) * w + (n + l)];
+                re = fmaf(dv, t.x, re);
+                im = fmaf(dv, t.y, im);
+            }
+            float2 ea = ws.ua[abs(mp)];
+            if (mp < 0) ea.y = -ea.y;
+            qt[idx] = cmul(ea, make_float2(re, im));
+        }
+    }
+    __syncwarp();
+    // xi~ in band layout
+    const float inv_total = (float)(1.0 / a.wp_total);
+    for (int at = lane; at < T.rows * 32; at += 32) {
+        const int row = at >> 5, j = at & 31;
+        const int g = a.row_group[row];
+        const int item = g * 32 + j;
+        const int s = row - T.row_off[g];
+        if (s >= T.item_len[item]) {
+            out[at] = make_float2(0.f, 0.f);
+            if (wedge) out_w[at] = make_float2(0.f, 0.f);
+            continue;
+        }
+        const int m = T.item_mm[item].x, mp = T.item_mm[item].y;
+        const int l = max(abs(m), abs(mp)) + s, w = 2 * l + 1, o = xi_off(l);
+        const float2* xr = xd + o + (m + l) * w;
+        const float* dr = dtab + o + (mp + l) * w;
+        float re = 0.0f, im = 0.0f;
+        for (int n = 0; n < w; ++n) {
+            const float2 x = xr[n];
+            const float dv = dr[n];
+            re = fmaf(x.x, dv, re);
+            im = fmaf(x.y, dv, im);
+        }
+        float2 ea = ws.ua[abs(mp)];
+        if (mp < 0) ea.y = -ea.y;
+        out[at] = cmul(ea, make_float2(re, im));
+        if (wedge) {
+            const int am = abs(m);
+            double2 c = a.chi_hat[l * (l + 1) / 2 + am];
+            if (m < 0) {
+                const double sgn = (am & 1) ? -1.0 : 1.0;
+                c = make_double2(sgn * c.x, -sgn * c.y);
+            }
+            const float2 qv = qt[l * l + (mp + l)];
+            // conj(chi_lm) q~_lm' / total
+            const float cr = (float)c.x, ci = (float)-c.y;
+            out_w[at] = make_float2((cr * qv.x - ci * qv.y) * inv_total, (cr * qv.y + ci * qv.x) * inv_total);
         }
     }
     __syncwarp();
@@ -398,8 +442,8 @@ __device__ void newton_band(const RefineArgs& a, const float2* xi_s, CandState& 
     const bool wedge = prm.has_wedge != 0;
     const int band = prm.band;
     const Quat koff{prm.koffset[0], prm.koffset[1], prm.koffset[2], prm.koffset[3]};
-    float* dtab = scratch;
-    float2* xi_t = reinterpret_cast<float2*>(scratch + ((xi_off(T.L + 1) + 1) & ~1));  // 8-byte aligned
+    const int nxi = xi_off(T.L + 1);
+    float2* xi_t = reinterpret_cast<float2*>(scratch + ((nxi + 1) & ~1)) + nxi + (T.L + 1) * (T.L + 1);
     float2* w_t = xi_t + (size_t)T.rows * 32;
     Quat g{st.g[0], st.g[1], st.g[2], st.g[3]};
     Quat anchor{st.anchor[0], st.anchor[1], st.anchor[2], st.anchor[3]};
@@ -409,7 +453,7 @@ __device__ void newton_band(const RefineArgs& a, const float2* xi_s, CandState& 
     auto reanchor = [&](const Quat& target) {
         anchor = q_mul(q_inv(koff), target);
         st.anchor_limit = band;
-        compose_kernels(T, xi_s, wedge ? T.wedge : nullptr, anchor, dtab, xi_t, w_t, ws);
+        compose_kernels(T, xi_s, a, anchor, scratch, xi_t, wedge ? w_t : nullptr, ws);
         st.anchored = 1;
     };
 
@@ -517,63 +561,88 @@ __device__ float2 xi_entry(const BandTables& T, const int* row_group, const floa
     return make_float2(re, im);
 }
 
-__global__ void __launch_bounds__(kWarps * 32, 2) refine_kernel(RefineArgs a) {
+constexpr int kRefineWarps = 16;
+constexpr int kMaxBatch = 8;
+
+// Persistent CTAs take batches of `a.batch` windows: their kernels are built in
+// shared memory, then the CTA's 16 warps pull (window, candidate) items from
+// one pooled queue, so the per-candidate Newton time imbalance averages over
+// the whole batch instead of stalling every window at a barrier.
+__global__ void __launch_bounds__(kRefineWarps * 32, 1) refine_kernel(RefineArgs a) {
     extern __shared__ __align__(16) unsigned char sm[];
     const BandTables& T = a.T;
-    float2* xi = reinterpret_cast<float2*>(sm);                        // rows*32
-    float* fbuf = reinterpret_cast<float*>(xi + (size_t)T.rows * 32);   // rows_band
-    float* tbuf = fbuf + a.rows_band;
+    const int xi_len = T.rows * 32;
+    float2* xib = reinterpret_cast<float2*>(sm);                               // batch * rows*32
+    float* tbuf = reinterpret_cast<float*>(xib + (size_t)a.batch * xi_len);    // rows_band
+    float* fbuf = tbuf + a.rows_band;                                          // rows_band
     WarpScratch* wsc = reinterpret_cast<WarpScratch*>(
-        (reinterpret_cast<uintptr_t>(tbuf + a.rows_band) + 15) & ~uintptr_t(15));
-    __shared__ int s_win, s_next;
+        (reinterpret_cast<uintptr_t>(fbuf + a.rows_band) + 15) & ~uintptr_t(15));
+    __shared__ int s_w0, s_next, s_nitems;
+    __shared__ int s_start[kMaxBatch + 1];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     WarpScratch& ws = wsc[warp];
-    float* scratch = a.scratch + (size_t)(blockIdx.x * kWarps + warp) * a.scratch_per_warp;
+    float* scratch = a.scratch + (size_t)(blockIdx.x * kRefineWarps + warp) * a.scratch_per_warp;
 
+    for (int r = threadIdx.x; r < a.rows_band; r += blockDim.x) tbuf[r] = a.t_hat[r];
     for (;;) {
         __syncthreads();
         if (threadIdx.x == 0) {
-            s_win = atomicAdd(a.win_counter, 1);
+            s_w0 = atomicAdd(a.win_counter, a.batch);
             s_next = 0;
+            int acc = 0;
+            for (int b = 0; b < a.batch; ++b) {
+                s_start[b] = acc;
+                const int w = s_w0 + b;
+                acc += w < a.n_win ? a.cand_count[w] : 0;
+            }
+            s_start[a.batch] = acc;
+            s_nitems = acc;
         }
         __syncthreads();
-        const int w = s_win;
-        if (w >= a.n_win) break;
-        const int nc = a.cand_count[w];
-        CandState* cs = a.cand + (size_t)w * a.max_cand;
-        if (nc > 0) {
-            const float* cw = a.coef + (long long)w * a.ldc;
-            for (int r = threadIdx.x; r < a.rows_band; r += blockDim.x) {
-                fbuf[r] = cw[r];
-                tbuf[r] = a.t_hat[r];
-            }
+        const int w0 = s_w0;
+        if (w0 >= a.n_win) break;
+        const int nb = min(a.batch, a.n_win - w0);
+        // build the batch's kernels (windows without candidates are skipped)
+        for (int b = 0; b < nb; ++b) {
+            if (s_start[b + 1] == s_start[b]) continue;
+            const float* cw = a.coef + (long long)(w0 + b) * a.ldc;
+            for (int r = threadIdx.x; r < a.rows_band; r += blockDim.x) fbuf[r] = cw[r];
             __syncthreads();
-            for (int e = threadIdx.x; e < T.rows * 32; e += blockDim.x)
-                xi[e] = xi_entry(T, a.row_group, fbuf, tbuf, a.block_off, a.radial_count, e >> 5,
-                                 e & 31);
-            __syncthreads();
-            for (;;) {
-                int c = 0;
-                if (lane == 0) c = atomicAdd(&s_next, 1);
-                c = __shfl_sync(0xffffffffu, c, 0);
-                if (c >= nc) break;
-                CandState st = cs[c];
-                if (!st.diverged) newton_band(a, xi, st, ws, scratch);
-                if (a.last_band) {
-                    // final unanchored score at the top band (optimize.cpp:349-352)
-                    const Quat rq = st.diverged ? Quat{st.best_g[0], st.best_g[1], st.best_g[2], st.best_g[3]}
-                                                : Quat{st.g[0], st.g[1], st.g[2], st.g[3]};
-                    Derivs f;
-                    eval_objective<0>(T, xi, T.wedge, a.prm.has_wedge != 0, q_euler(rq), ws, f);
-                    st.score = f.v;
-                    ++st.evals;
-                }
-                if (lane == 0) cs[c] = st;
-                __syncwarp();
-            }
+            float2* xi = xib + (size_t)b * xi_len;
+            for (int e = threadIdx.x; e < xi_len; e += blockDim.x)
+                xi[e] = xi_entry(T, a.row_group, fbuf, tbuf, a.block_off, a.radial_count, e >> 5, e & 31);
             __syncthreads();
         }
-        if (a.last_band && threadIdx.x == 0) {
+        const int nitems = s_nitems;
+        for (;;) {
+            int it = 0;
+            if (lane == 0) it = atomicAdd(&s_next, 1);
+            it = __shfl_sync(0xffffffffu, it, 0);
+            if (it >= nitems) break;
+            int b = 0;
+            while (it >= s_start[b + 1]) ++b;
+            const int c = it - s_start[b];
+            const float2* xi = xib + (size_t)b * xi_len;
+            CandState* cs = a.cand + (size_t)(w0 + b) * a.max_cand;
+            CandState st = cs[c];
+            if (!st.diverged) newton_band(a, xi, st, ws, scratch);
+            if (a.last_band) {
+                // final unanchored score at the top band (optimize.cpp:349-352)
+                const Quat rq = st.diverged ? Quat{st.best_g[0], st.best_g[1], st.best_g[2], st.best_g[3]}
+                                            : Quat{st.g[0], st.g[1], st.g[2], st.g[3]};
+                Derivs f;
+                eval_objective<0>(T, xi, T.wedge, a.prm.has_wedge != 0, q_euler(rq), ws, f);
+                st.score = f.v;
+                ++st.evals;
+            }
+            if (lane == 0) cs[c] = st;
+            __syncwarp();
+        }
+        __syncthreads();
+        if (a.last_band && threadIdx.x < nb) {
+            const int w = w0 + threadIdx.x;
+            const int nc = a.cand_count[w];
+            const CandState* cs = a.cand + (size_t)w * a.max_cand;
             WindowOutcome o;
             o.particle = a.win_particle[w];
             o.shift[0] = a.win_shift[3 * w];
@@ -650,31 +719,44 @@ __global__ void build_xi_kernel(XiArgs a) {
 
 }  // namespace
 
-size_t refine_smem_bytes(const BandTables& T, int rows_band, int max_cand) {
-    (void)max_cand;
-    return sizeof(float2) * (size_t)T.rows * 32 + sizeof(float) * 2 * rows_band + 16 +
-           sizeof(WarpScratch) * kWarps;
+static size_t refine_fixed_bytes(int rows_band) {
+    return sizeof(float) * 2 * rows_band + 16 + sizeof(WarpScratch) * kRefineWarps;
+}
+
+int refine_batch(const BandTables& T, int rows_band) {
+    const size_t budget = 200 * 1024;
+    const size_t fixed = refine_fixed_bytes(rows_band);
+    const size_t per = sizeof(float2) * (size_t)T.rows * 32;
+    int b = fixed + per <= budget ? (int)((budget - fixed) / per) : 1;
+    return b < 1 ? 1 : (b > kMaxBatch ? kMaxBatch : b);
+}
+
+size_t refine_smem_bytes(const BandTables& T, int rows_band, int batch) {
+    return sizeof(float2) * (size_t)T.rows * 32 * batch + refine_fixed_bytes(rows_band);
 }
 
 long long refine_scratch_floats(const BandTables& T) {
-    // dtab (N_xi(L) floats, +1 pad) + two band-layout complex kernels
-    return (long long)(xi_off(T.L + 1) + 2) + 4LL * T.rows * 32;
+    // dtab (N_xi floats) + dense xi' (N_xi complex) + q~ ((L+1)^2 complex) + two band-layout kernels
+    const long long nxi = xi_off(T.L + 1);
+    return (nxi + 2) + 2 * nxi + 2LL * (T.L + 1) * (T.L + 1) + 4LL * T.rows * 32;
 }
 
-int refine_resident_blocks(const BandTables& T, int rows_band, int max_cand, int device) {
-    const size_t smem = refine_smem_bytes(T, rows_band, max_cand);
+int refine_warps() { return kRefineWarps; }
+
+int refine_resident_blocks(const BandTables& T, int rows_band, int batch, int device) {
+    const size_t smem = refine_smem_bytes(T, rows_band, batch);
     cudaFuncSetAttribute(refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0, sms = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, refine_kernel, kWarps * 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, refine_kernel, kRefineWarps * 32, smem);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     return (per_sm > 0 ? per_sm : 1) * sms;
 }
 
 int launch_refine(const RefineArgs& a, int blocks, cudaStream_t s) {
     if (a.n_win <= 0) return 0;
-    const size_t smem = refine_smem_bytes(a.T, a.rows_band, a.max_cand);
+    const size_t smem = refine_smem_bytes(a.T, a.rows_band, a.batch);
     cudaFuncSetAttribute(refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    refine_kernel<<<blocks, kWarps * 32, smem, s>>>(a);
+    refine_kernel<<<blocks, kRefineWarps * 32, smem, s>>>(a);
     return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }
 

@@ -20,6 +20,7 @@ struct RefineArgs {
     CandState* cand = nullptr;
     int max_cand = 0;
     int n_win = 0;
+    int batch = 1;                  // windows per CTA batch (refine_batch)
     int* win_counter = nullptr;     // zeroed before launch
     float* scratch = nullptr;       // per resident warp: anchored-chart kernels
     long long scratch_per_warp = 0; // floats
@@ -32,11 +33,17 @@ struct RefineArgs {
     const int* win_shift = nullptr;
     long long grid_evals = 0;       // seed-grid evaluations per window
     WindowOutcome* out = nullptr;
+    // wedge-power factors (packed (l, m >= 0)) for the anchored-chart composition
+    const double2* chi_hat = nullptr;
+    const double2* q_hat = nullptr;
+    double wp_total = 1.0;
 };
 
-size_t refine_smem_bytes(const BandTables& T, int rows_band, int max_cand);
+int refine_batch(const BandTables& T, int rows_band);
+size_t refine_smem_bytes(const BandTables& T, int rows_band, int batch);
 long long refine_scratch_floats(const BandTables& T);
-int refine_resident_blocks(const BandTables& T, int rows_band, int max_cand, int device);
+int refine_warps();
+int refine_resident_blocks(const BandTables& T, int rows_band, int batch, int device);
 int launch_refine(const RefineArgs& a, int blocks, cudaStream_t s);
 
 // standalone batched evaluation (rotate-score-gradient sweep, config 4):
