@@ -153,8 +153,9 @@ int bm_average_accumulate(bm_context* ctx, const float* particles, int count,
                           const bm_align_result* results, double* sum, void* stream);
 
 /* Kernel timing evidence: with timing on, CUDA events on the context stream
- * bracket every launch of this library.  out_ms[0..5]: gather, split GEMM,
- * seed, refine, wedge filter, misc (milliseconds, accumulated since reset);
+ * bracket every launch of this library.  out_ms[0..9]: gather, split GEMM,
+ * seed, refine, wedge filter, misc, refine by band position 0, 1, 2, 3+
+ * (milliseconds, accumulated since reset);
  * out_counts[0..3]: kernels launched, windows expanded, GEMM launches,
  * refine launches.  reset != 0 clears after reading. */
 int bm_context_set_timing(bm_context* ctx, int on);

@@ -215,6 +215,24 @@ class Context:
                      subtomo_norm=r.subtomo_norm, quat=np.array(r.quat[:]),
                      evaluations=r.evaluations) for r in out[:n_win]]
 
+    def eval_sweep(self, f, t, euler, order: int = 1):
+        """Rotate-score-gradient sweep (config 4): value and Euler gradient of
+        C = Re sum xi D(g), xi = xi_coefficients(f_p, t), for every (p, g).
+        f: complex (n_f, coeff_count), t: complex (coeff_count,), euler: (n_rot, 3);
+        returns float64 (n_f, n_rot, 4) on the device."""
+        torch = _torch()
+        dev = torch.device(f"cuda:{self.device}")
+        fa = torch.view_as_real(torch.as_tensor(f, dtype=torch.complex128)).to(dev).contiguous()
+        ta = torch.view_as_real(torch.as_tensor(t, dtype=torch.complex128)).to(dev).contiguous()
+        ea = torch.as_tensor(euler, dtype=torch.float64).to(dev).contiguous()
+        n_f, n_rot = fa.shape[0], ea.shape[0]
+        out = torch.empty((n_f, n_rot, 4), dtype=torch.float64, device=dev)
+        _lib.check(_lib.lib().bm_eval_sweep(self._h, C.c_void_p(fa.data_ptr()), n_f,
+                                            C.c_void_p(ta.data_ptr()), C.c_void_p(ea.data_ptr()),
+                                            n_rot, order, C.c_void_p(out.data_ptr()),
+                                            self._stream(out)), "eval_sweep")
+        return out
+
     def apply_wedge_taper(self, vols):
         torch = _torch()
         v = self._dev(vols)
@@ -229,10 +247,11 @@ class Context:
         _lib.check(_lib.lib().bm_context_set_timing(self._h, 1 if on else 0), "set_timing")
 
     def timings(self, reset: bool = False):
-        ms = (C.c_double * 6)()
+        ms = (C.c_double * 10)()
         cnt = (C.c_longlong * 4)()
         _lib.check(_lib.lib().bm_context_timings(self._h, ms, cnt, 1 if reset else 0), "timings")
-        names = ("gather", "split_gemm", "seed", "refine", "wedge", "misc")
+        names = ("gather", "split_gemm", "seed", "refine", "wedge", "misc", "refine_band0",
+                 "refine_band1", "refine_band2", "refine_band3+")
         return (dict(zip(names, ms[:])),
                 dict(launches=cnt[0], windows_expanded=cnt[1], gemm_launches=cnt[2],
                      refine_launches=cnt[3]))

@@ -11,6 +11,8 @@
 #include <array>
 #include <cfloat>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <stdexcept>
 
 #include "context.hpp"
@@ -37,6 +39,7 @@ void AlignConfig::validate(int l_max) const {
     if (!(seed_grid_step > 0.0) || seed_grid_step > kPiH)
         throw std::invalid_argument("config: seed grid step must be in (0, pi]");
     if (max_candidates < 1 || newton_max_iter < 1) throw std::invalid_argument("config: counts must be positive");
+    if (max_candidates > 256) throw std::invalid_argument("config: max_candidates above 256 is not supported on the device path");
     if (!(grad_tol > 0.0) || !(step_damping > 0.0)) throw std::invalid_argument("config: tolerances must be positive");
     if (shift_radius < 0 || shift_step < 1) throw std::invalid_argument("config: bad shift search parameters");
 }
@@ -212,6 +215,170 @@ void Context::set_template(const float* tmpl, double wedge_theta) {
     has_template = true;
 }
 
+// Bulk-synchronous damped Newton over every candidate of every window
+// (refine(), src/optimize.cpp:255-357), band by band; windows are processed in
+// chunks so the anchored-chart kernel pool stays bounded.
+void Context::refine_windows(int nw, int maxc, const AlignConfig& cfg, const Quat& koff, long long grid_evals) {
+    work_.reserve(sizeof(CandWork) * (size_t)nw * maxc);
+    counters_.reserve(sizeof(int) * 8);
+    int* d_counts = counters_.as<int>();  // CNT_L2, CNT_COMP, CNT_T0, CNT_T1
+    int* d_pool = d_counts + 4;
+    int* d_over = d_counts + 5;
+    int* h_active = nullptr;
+    cudaMallocHost(&h_active, sizeof(int) * 4);
+    const bool wedge = wedge_active();
+    // window kernels of the largest band and the anchored pool share a budget
+    const int Lmax_band = cfg.bands.back();
+    BandDev& btop = band(Lmax_band);
+    const size_t kernel_bytes = sizeof(float2) * (size_t)btop.rows * 32;
+    const size_t per_window = kernel_bytes * (1 + (size_t)maxc * pool_fraction_ * (wedge ? 2 : 1));
+    long long chunk = std::max<long long>(64, (long long)(pool_budget_ / per_window));
+    chunk = std::min<long long>(chunk, nw);
+    for (long long w0 = 0; w0 < nw; w0 += chunk) {
+        const int cnt = (int)std::min<long long>(chunk, nw - w0);
+        double frac = pool_fraction_;
+        for (int attempt = 0; attempt < 2; ++attempt) {
+            if (attempt == 1) {  // pool overflow: rerun the chunk with a slot per candidate
+                frac = 1.0;
+                ck(cudaMemcpyAsync(cand_.as<CandState>() + (size_t)w0 * maxc, cand_backup_.p,
+                                   sizeof(CandState) * (size_t)cnt * maxc, cudaMemcpyDeviceToDevice, stream),
+                   "restore");
+            } else {
+                cand_backup_.reserve(sizeof(CandState) * (size_t)cnt * maxc);
+                ck(cudaMemcpyAsync(cand_backup_.p, cand_.as<CandState>() + (size_t)w0 * maxc,
+                                   sizeof(CandState) * (size_t)cnt * maxc, cudaMemcpyDeviceToDevice, stream),
+                   "backup");
+            }
+            ck(cudaMemsetAsync(d_over, 0, sizeof(int), stream), "overflow");
+            for (size_t bi = 0; bi < cfg.bands.size(); ++bi) {
+                const int L = cfg.bands[bi];
+                BandDev& bd = band(L);
+                const size_t len = (size_t)bd.rows * 32;
+                StageArgs a;
+                a.T = bd.view();
+                a.row_group = bd.row_group.as<int>();
+                // window kernels of this band
+                xi_win_.reserve(sizeof(float2) * len * cnt);
+                XiArgs xa;
+                xa.T = a.T;
+                xa.row_group = a.row_group;
+                xa.f = coef.as<float>() + (size_t)w0 * geo.m_pad;
+                xa.ldf = geo.m_pad;
+                xa.t = t_hat.as<float>();
+                xa.ldt = 0;
+                xa.block_off = geo.block_off;
+                xa.radial_count = geo.radial_count;
+                xa.n = cnt;
+                xa.out = xi_win_.as<float2>();
+                cudaEvent_t r0 = timer.begin(stream);
+                cudaEvent_t rb = timer.begin(stream);
+                if (launch_build_xi(xa, stream) != 0) throw std::runtime_error("build_xi launch failed");
+                ++timer.launches;
+                a.xi_win = xi_win_.as<float2>();
+                a.pool = std::max(1, (int)std::ceil(frac * cnt * maxc));
+                xi_pool_.reserve(sizeof(float2) * len * a.pool);
+                a.xi_pool = xi_pool_.as<float2>();
+                if (wedge) {
+                    w_pool_.reserve(sizeof(float2) * len * a.pool);
+                    a.w_pool = w_pool_.as<float2>();
+                    a.chi_hat = chi_dev.as<double2>();
+                    a.q_hat = q_dev.as<double2>();
+                    a.wp_total = wp_total;
+                }
+                a.pool_counter = d_pool;
+                a.overflow = d_over;
+                a.cand = cand_.as<CandState>() + (size_t)w0 * maxc;
+                a.work = work_.as<CandWork>() + (size_t)w0 * maxc;
+                a.cand_count = cand_count_.as<int>() + w0;
+                a.max_cand = maxc;
+                a.n_win = cnt;
+                a.prm.band = L;
+                a.prm.newton_max_iter = cfg.newton_max_iter;
+                a.prm.grad_tol = cfg.grad_tol;
+                a.prm.accept_tol = cfg.accept_tol;
+                a.prm.step_damping = cfg.step_damping;
+                a.prm.koffset[0] = koff.w;
+                a.prm.koffset[1] = koff.x;
+                a.prm.koffset[2] = koff.y;
+                a.prm.koffset[3] = koff.z;
+                a.prm.max_cand = maxc;
+                a.prm.has_wedge = wedge ? 1 : 0;
+                a.compose_smem = compose_smem_bytes(L) <= 200 * 1024 ? 1 : 0;
+                a.scratch_per_warp = compose_scratch_floats(L);
+                const long long slots = (long long)cnt * maxc;
+                lists_.reserve(sizeof(int) * 4 * (size_t)slots);
+                a.list2 = lists_.as<int>();
+                a.listc = a.list2 + slots;
+                int* lt0 = a.listc + slots;
+                int* lt1 = lt0 + slots;
+                a.counts = d_counts;
+                ck(cudaMemsetAsync(d_pool, 0, sizeof(int), stream), "pool");
+                launch_band_begin(a, stream);
+                ++timer.launches;
+                for (int it = 0; it < cfg.newton_max_iter; ++it) {
+                    ck(cudaMemsetAsync(d_counts, 0, sizeof(int) * 4, stream), "counts");
+                    launch_iter_begin(a, stream);
+                    ++timer.launches;
+                    ck(cudaMemcpyAsync(h_active, d_counts, sizeof(int) * 2, cudaMemcpyDeviceToHost, stream),
+                       "active");
+                    ck(cudaStreamSynchronize(stream), "iteration");
+                    const int n2 = h_active[0], nc = h_active[1];
+                    if (debug_iters_) fprintf(stderr, "[refine] band %d iter %d active %d compose %d\n", L, it, n2, nc);
+                    if (n2 == 0) break;
+                    if (nc > 0) {
+                        if (!a.compose_smem)
+                            scratch_.reserve(sizeof(float) * (size_t)std::min(nc, 4096) * a.scratch_per_warp);
+                        a.scratch = scratch_.as<float>();
+                        launch_compose(a, a.compose_smem ? nc : std::min(nc, 4096), stream);
+                        ++timer.launches;
+                    }
+                    launch_eval(a, 2, a.list2, d_counts + CNT_L2, n2, stream);
+                    launch_step(a, lt0, d_counts + CNT_T0, n2, stream);
+                    timer.launches += 2;
+                    for (int r = 0; r < 3; ++r) {
+                        int* src = (r & 1) ? lt1 : lt0;
+                        int* dst = (r & 1) ? lt0 : lt1;
+                        int* csrc = d_counts + ((r & 1) ? CNT_T1 : CNT_T0);
+                        int* cdst = d_counts + ((r & 1) ? CNT_T0 : CNT_T1);
+                        launch_eval(a, 0, src, csrc, n2, stream);
+                        ck(cudaMemsetAsync(cdst, 0, sizeof(int), stream), "retry count");
+                        launch_accept(a, src, csrc, dst, cdst, n2, stream);
+                        timer.launches += 2;
+                    }
+                }
+                if (bi + 1 == cfg.bands.size()) {
+                    // final unanchored score at the top band (optimize.cpp:349-352)
+                    ck(cudaMemsetAsync(d_counts, 0, sizeof(int), stream), "final count");
+                    launch_final_prep(a, stream);
+                    launch_eval(a, 0, a.list2, d_counts + CNT_L2, (int)slots, stream);
+                    launch_final_score(a, (int)slots, stream);
+                    timer.launches += 3;
+                }
+                ++timer.refine_launches;
+                timer.end(K_REFINE, r0, stream);
+                timer.end(K_REFINE_B0 + (int)std::min<size_t>(bi, 3), rb, stream);
+            }
+            ck(cudaMemcpyAsync(h_active + 1, d_over, sizeof(int), cudaMemcpyDeviceToHost, stream), "overflow");
+            ck(cudaStreamSynchronize(stream), "chunk");
+            if (h_active[1] == 0) break;
+        }
+        ReduceArgs ra;
+        ra.cand = cand_.as<CandState>() + (size_t)w0 * maxc;
+        ra.cand_count = cand_count_.as<int>() + w0;
+        ra.max_cand = maxc;
+        ra.n_win = cnt;
+        ra.sub_norm = sub_norm_.as<double>() + w0;
+        ra.t_norm = t_norm;
+        ra.win_particle = win_vol.as<int>() + w0;
+        ra.win_shift = win_shift.as<int>() + 3 * w0;
+        ra.grid_evals = grid_evals;
+        ra.out = outcome_.as<WindowOutcome>() + w0;
+        launch_window_reduce(ra, stream);
+        ++timer.launches;
+    }
+    cudaFreeHost(h_active);
+}
+
 std::vector<WindowOutcome> Context::run_windows(const float* vols, int n_vol, const std::vector<int>& wvol,
                                                 const std::vector<int>& wshift, const AlignConfig& cfg) {
     if (!has_template) throw std::invalid_argument("align: set_template first");
@@ -258,60 +425,7 @@ std::vector<WindowOutcome> Context::run_windows(const float* vols, int n_vol, co
     timer.end(K_SEED, s0, stream);
 
     const Quat koff = q_from_euler(0.0, kPiH / 2.0, 0.0);
-    for (size_t bi = 0; bi < cfg.bands.size(); ++bi) {
-        const int L = cfg.bands[bi];
-        BandDev& bd = band(L);
-        RefineArgs ra;
-        ra.T = bd.view();
-        ra.row_group = bd.row_group.as<int>();
-        ra.coef = coef.as<float>();
-        ra.ldc = geo.m_pad;
-        ra.t_hat = t_hat.as<float>();
-        ra.block_off = geo.block_off;
-        ra.radial_count = geo.radial_count;
-        ra.rows_band = L + 1 <= basis.l_max ? basis.block_off[L + 1] : geo.coeffs;
-        ra.cand_count = cand_count_.as<int>();
-        ra.cand = cand_.as<CandState>();
-        ra.max_cand = maxc;
-        ra.n_win = nw;
-        ra.win_counter = win_counter_.as<int>();
-        ra.batch = refine_batch(ra.T, ra.rows_band);
-        const int blocks = std::min((nw + ra.batch - 1) / ra.batch,
-                                    refine_resident_blocks(ra.T, ra.rows_band, ra.batch, device));
-        ra.scratch_per_warp = (refine_scratch_floats(ra.T) + 3) / 4 * 4;
-        scratch_.reserve(sizeof(float) * (size_t)blocks * refine_warps() * ra.scratch_per_warp);
-        ra.scratch = scratch_.as<float>();
-        ra.prm.band = L;
-        ra.prm.newton_max_iter = cfg.newton_max_iter;
-        ra.prm.grad_tol = cfg.grad_tol;
-        ra.prm.accept_tol = cfg.accept_tol;
-        ra.prm.step_damping = cfg.step_damping;
-        ra.prm.koffset[0] = koff.w;
-        ra.prm.koffset[1] = koff.x;
-        ra.prm.koffset[2] = koff.y;
-        ra.prm.koffset[3] = koff.z;
-        ra.prm.max_cand = maxc;
-        ra.prm.has_wedge = wedge_active() ? 1 : 0;
-        ra.prm.first_band = bi == 0;
-        ra.last_band = bi + 1 == cfg.bands.size();
-        ra.sub_norm = sub_norm_.as<double>();
-        ra.t_norm = t_norm;
-        ra.win_particle = win_vol.as<int>();
-        ra.win_shift = win_shift.as<int>();
-        ra.grid_evals = (long long)sd.na * sd.nb * sd.ng;
-        ra.out = outcome_.as<WindowOutcome>();
-        if (wedge_active()) {
-            ra.chi_hat = chi_dev.as<double2>();
-            ra.q_hat = q_dev.as<double2>();
-            ra.wp_total = wp_total;
-        }
-        ck(cudaMemsetAsync(win_counter_.p, 0, sizeof(int), stream), "counter");
-        cudaEvent_t r0 = timer.begin(stream);
-        if (launch_refine(ra, blocks, stream) != 0) throw std::runtime_error("refine kernel launch failed");
-        ++timer.launches;
-        ++timer.refine_launches;
-        timer.end(K_REFINE, r0, stream);
-    }
+    refine_windows(nw, maxc, cfg, koff, (long long)sd.na * sd.nb * sd.ng);
     ck(cudaMemcpyAsync(res.data(), outcome_.p, sizeof(WindowOutcome) * nw, cudaMemcpyDeviceToHost, stream),
        "outcomes");
     ck(cudaStreamSynchronize(stream), "run_windows");

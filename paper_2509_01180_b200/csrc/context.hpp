@@ -9,6 +9,7 @@
 #include <cufft.h>
 
 #include <complex>
+#include <cstdlib>
 #include <map>
 #include <memory>
 #include <string>
@@ -17,6 +18,7 @@
 #include "basis_host.hpp"
 #include "bmb_internal.hpp"
 #include "kernels.cuh"
+#include "rotation.cuh"
 
 namespace bmb {
 
@@ -98,7 +100,7 @@ struct ParticleResult {
 };
 
 // Per-kernel-class CUDA-event timing on the context stream (bench evidence).
-enum KClass { K_GATHER = 0, K_GEMM, K_SEED, K_REFINE, K_WEDGE, K_MISC, K_COUNT };
+enum KClass { K_GATHER = 0, K_GEMM, K_SEED, K_REFINE, K_WEDGE, K_MISC, K_REFINE_B0, K_REFINE_B1, K_REFINE_B2, K_REFINE_B3, K_COUNT };
 struct KernelTimer {
     bool on = false;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
@@ -191,7 +193,13 @@ public:
     // rotate-score-gradient sweep (config 4): kernels from coefficient pairs
     DevBuf work_f, work_xi, filtered;
 
+    bool debug_iters_ = std::getenv("BMB_DEBUG_ITERS") != nullptr;
+    double pool_fraction_ = 0.5;           // anchored-chart pool slots per candidate
+    size_t pool_budget_ = 8ull << 30;       // bytes for window kernels + pool per chunk
+
 private:
+    void refine_windows(int nw, int maxc, const AlignConfig& cfg, const Quat& koff, long long grid_evals);
+    DevBuf work_, counters_, xi_win_, xi_pool_, w_pool_, cand_backup_, lists_;
     std::map<int, std::unique_ptr<BandDev>> bands_;
     std::map<std::pair<int, long long>, std::unique_ptr<SeedDev>> seeds_;
     DevBuf cand_, cand_count_, outcome_, win_counter_, scratch_, sub_norm_;

@@ -1,6 +1,7 @@
-// Rotate-score-gradient evaluation and the device Newton state machine.
+// Rotate-score-gradient evaluation and the bulk-synchronous damped Newton
+// refinement (kernels K4, K5, K7).
 //
-// Kernel K4+K5 (warp_eval): C(g) = Re sum_l sum_{m,m'} xi_l[m,m'] e^{-i m a}
+// K4+K5 (warp_eval): C(g) = Re sum_l sum_{m,m'} xi_l[m,m'] e^{-i m a}
 // d^l_{m,m'}(b) e^{-i m' g} with its Euler gradient and Hessian
 // (correlation_derivatives, src/xcorr.cpp:52-105).  One warp per evaluation;
 // each lane owns half-plane (m,m') chains and marches the three-term Wigner-d
@@ -9,15 +10,20 @@
 // angles and band, Objective::eval, src/optimize.cpp:106-130) and never stored.
 // The (-m,-m') half follows from the real-volume symmetry
 // xi_{-m,-m'} D_{-m,-m'} = conj(xi_{m,m'} D_{m,m'}).  FP32 recursion and lane
-// accumulation, FP64 phases / cross-lane reduction / Newton algebra.
+// accumulation, FP64 phases / cross-lane reduction.
 //
-// Kernel K7 (refine_kernel): one CTA per shift window (persistent), xi of the
-// window built in shared memory in the band layout, one warp per candidate
-// running the damped-Newton iteration of refine() (src/optimize.cpp:255-357):
-// Levenberg lambda, <= 3 retries x10, one-radian trust cap, FullPivLU
-// semantics, re-anchoring near the gimbal poles with the composed kernel
-// xi~ = xi D(a)^T (xcorr.cpp:149-155) in per-warp scratch, final unanchored
-// score at the top band, best-candidate selection per window.
+// K7 (refine()): the damped-Newton iteration of src/optimize.cpp:255-357
+// (Levenberg lambda, <= 3 retries x10, one-radian trust cap, FullPivLU
+// semantics, re-anchoring within 0.05 of the gimbal poles through the composed
+// kernel xi~ = xi D(a)^T, xcorr.cpp:149-155) run bulk-synchronously over every
+// candidate of every window: per iteration, small kernels for the chart /
+// re-anchor decision (thread per candidate), the chart-kernel composition
+// (warp per re-anchored candidate), the order-2 evaluation (warp per candidate,
+// CTA per window), the FP64 Newton step (thread per candidate: objective
+// quotient, 3x3 full-pivot LU, trial rotation) and up to three order-0 trial
+// evaluations with their acceptance tests.  The host raises L between bands
+// (frequency marching) and relaunches the iteration until no candidate is
+// active.
 #include <cfloat>
 
 #include "refine.cuh"
@@ -35,41 +41,65 @@ struct WarpScratch {
     float2 ug[kMaxL + 1];
     float cp[2 * kMaxL + 3];
     float sp[2 * kMaxL + 3];
+    double res[20];     // reduced (value, grad[3], hess aa ab ag bb bg gg) x (corr, wedge)
+    double cs_half[8];  // cos, sin of beta/2, beta, alpha, gamma
 };
 
-struct Derivs {
-    double v;
-    double g[3];
-    double h[9];
-};
-
-__device__ __forceinline__ double warp_sum(double x) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-    return x;
-}
+// single out-of-line copies of the FP64 math-library routines
+__device__ __noinline__ void sincos_d(double x, double* s, double* c) { sincos(x, s, c); }
 
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
     return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
 
-// Evaluate the correlation (and the wedge-power kernel when WEDGE) at ZYZ
-// angles (alpha, beta, gamma), band T.L.  Warp-cooperative; all lanes return
-// the same (FP64) results.
-template <int ORDER, bool WEDGE>
-__device__ __noinline__ void warp_eval(const BandTables& T, const float2* xi, const float2* wx, double alpha,
-                          double beta, double gamma, WarpScratch& ws, Derivs& c, Derivs& r) {
+__host__ __device__ __forceinline__ int xi_off(int l) { return l * (2 * l - 1) * (2 * l + 1) / 3; }
+
+// Evaluate the correlation (and the wedge-power kernel when wx != null) at ZYZ
+// angles (alpha, beta, gamma), band T.L.  Warp-cooperative; results in ws.res.
+template <int ORDER>
+__device__ __noinline__ void warp_eval(const BandTables& T, const float2* xi, const float2* wx,
+                                       double alpha, double beta, double gamma, WarpScratch& ws) {
+    const bool WEDGE = wx != nullptr;
     const int lane = threadIdx.x & 31;
     const int L = T.L;
     __syncwarp();
-    for (int m = lane; m <= L; m += 32) {
-        double s, co;
-        sincos(m * alpha, &s, &co);
-        ws.ua[m] = make_float2((float)co, (float)-s);
-        sincos(m * gamma, &s, &co);
-        ws.ug[m] = make_float2((float)co, (float)-s);
+    // four FP64 sincos on lanes 0..3 (beta/2, beta, alpha, gamma); the phases
+    // e^{-i m alpha}, e^{-i m gamma} are then binary powers of the bases
+    if (lane < 4) {
+        const double ang = lane == 0 ? 0.5 * beta : (lane == 1 ? beta : (lane == 2 ? alpha : gamma));
+        double sn, co;
+        sincos_d(ang, &sn, &co);
+        ws.cs_half[2 * lane] = co;
+        ws.cs_half[2 * lane + 1] = sn;
     }
-    const double ch = cos(0.5 * beta), sh = sin(0.5 * beta);
+    __syncwarp();
+    {
+        const double car = ws.cs_half[4], cai = -ws.cs_half[5];  // e^{-i alpha}
+        const double cgr = ws.cs_half[6], cgi = -ws.cs_half[7];  // e^{-i gamma}
+        for (int m = lane; m <= L; m += 32) {
+            double ar = 1.0, ai = 0.0, gr = 1.0, gi = 0.0;
+            double br_ = car, bi_ = cai, hr = cgr, hi = cgi;
+            for (int e = m; e; e >>= 1) {
+                if (e & 1) {
+                    const double t = ar * br_ - ai * bi_;
+                    ai = ar * bi_ + ai * br_;
+                    ar = t;
+                    const double u = gr * hr - gi * hi;
+                    gi = gr * hi + gi * hr;
+                    gr = u;
+                }
+                const double t2 = br_ * br_ - bi_ * bi_;
+                bi_ = 2.0 * br_ * bi_;
+                br_ = t2;
+                const double u2 = hr * hr - hi * hi;
+                hi = 2.0 * hr * hi;
+                hr = u2;
+            }
+            ws.ua[m] = make_float2((float)ar, (float)ai);
+            ws.ug[m] = make_float2((float)gr, (float)gi);
+        }
+    }
+    const double ch = ws.cs_half[0], sh = ws.cs_half[1];
     for (int j = lane; j <= 2 * L + 2; j += 32) {
         double pc = 1.0, ps = 1.0, bc = ch, bs = sh;  // binary exponentiation
         for (int e = j; e; e >>= 1) {
@@ -84,7 +114,7 @@ __device__ __noinline__ void warp_eval(const BandTables& T, const float2* xi, co
         ws.sp[j] = (float)ps;
     }
     __syncwarp();
-    const float cb = (float)cos(beta), sb = (float)sin(beta);
+    const float cb = (float)ws.cs_half[2], sb = (float)ws.cs_half[3];
 
     float acc[10], accw[10];
 #pragma unroll
@@ -220,68 +250,31 @@ __device__ __noinline__ void warp_eval(const BandTables& T, const float2* xi, co
             }
         }
     }
-    // cross-lane reduction in FP64; hess index map: aa ab ag / ab bb bg / ag bg gg
-    c.v = warp_sum(acc[0]);
-    if (WEDGE) r.v = warp_sum(accw[0]);
-    if (ORDER >= 1) {
-        for (int i = 0; i < 3; ++i) c.g[i] = warp_sum(acc[1 + i]);
-        if (WEDGE)
-            for (int i = 0; i < 3; ++i) r.g[i] = warp_sum(accw[1 + i]);
+    // cross-lane reduction in FP64 (one interleaved butterfly for all values),
+    // published through shared memory
+    constexpr int NV = ORDER == 0 ? 1 : (ORDER == 1 ? 4 : 10);
+    constexpr int NT = 2 * NV;
+    double v[NT];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        v[i] = acc[i];
+        v[NV + i] = accw[i];
     }
-    if (ORDER >= 2) {
-        double h[6], hw[6];
-        for (int i = 0; i < 6; ++i) h[i] = warp_sum(acc[4 + i]);
-        // acc order: aa, ab, ag, bb, bg, gg
-        c.h[0] = h[0], c.h[1] = h[1], c.h[2] = h[2];
-        c.h[3] = h[1], c.h[4] = h[3], c.h[5] = h[4];
-        c.h[6] = h[2], c.h[7] = h[4], c.h[8] = h[5];
-        if (WEDGE) {
-            for (int i = 0; i < 6; ++i) hw[i] = warp_sum(accw[4 + i]);
-            r.h[0] = hw[0], r.h[1] = hw[1], r.h[2] = hw[2];
-            r.h[3] = hw[1], r.h[4] = hw[3], r.h[5] = hw[4];
-            r.h[6] = hw[2], r.h[7] = hw[4], r.h[8] = hw[5];
+#pragma unroll
+    for (int o = 16; o; o >>= 1)
+#pragma unroll
+        for (int i = 0; i < NT; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
+    if (lane == 0) {
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            ws.res[i] = v[i];
+            if (WEDGE) ws.res[10 + i] = v[NV + i];
         }
     }
+    __syncwarp();
 }
 
-// Objective::eval (src/optimize.cpp:106-130): C / sqrt(clamp(1 - rho, 0.02, 2))
-__device__ void objective(const Derivs& c, const Derivs& r, bool wedge, int order, Derivs& f) {
-    if (!wedge) {
-        f = c;
-        return;
-    }
-    const double v = fmin(fmax(1.0 - r.v, 0.02), 2.0);
-    const double s = 1.0 / sqrt(v);
-    f.v = c.v * s;
-    if (order >= 1) {
-        const double dv[3] = {-r.g[0], -r.g[1], -r.g[2]};
-        const double v32 = s / v;
-        for (int i = 0; i < 3; ++i) f.g[i] = c.g[i] * s - 0.5 * c.v * v32 * dv[i];
-        if (order >= 2) {
-            const double v52 = v32 / v;
-            for (int i = 0; i < 3; ++i)
-                for (int j = 0; j < 3; ++j) {
-                    const double hv = -r.h[i * 3 + j];
-                    f.h[i * 3 + j] = c.h[i * 3 + j] * s -
-                                     0.5 * v32 * (c.g[i] * dv[j] + dv[i] * c.g[j] + c.v * hv) +
-                                     0.75 * c.v * v52 * dv[i] * dv[j];
-                }
-        }
-    }
-}
-
-template <int ORDER>
-__device__ void eval_objective(const BandTables& T, const float2* xi, const float2* wx,
-                               bool wedge, const Euler3& e, WarpScratch& ws, Derivs& f) {
-    Derivs c, r;
-    if (wedge) warp_eval<ORDER, true>(T, xi, wx, e.a, e.b, e.g, ws, c, r);
-    else warp_eval<ORDER, false>(T, xi, wx, e.a, e.b, e.g, ws, c, r);
-    objective(c, r, wedge, ORDER, f);
-}
-
-// ---------------------------------------------------------------- anchoring
-__host__ __device__ __forceinline__ int xi_off(int l) { return l * (2 * l - 1) * (2 * l + 1) / 3; }
-
+// ---------------------------------------------------------------- composition
 // xi~_l = xi_l D^l(a)^T  (xi_compose_right, src/xcorr.cpp:149-155), with
 // D^l_{m'n}(a) = e^{-i m' a} d^l_{m'n}(b) e^{-i n g}:
 //   xi~_l[m,m'] = e^{-i m' a} sum_n (xi_l[m,n] e^{-i n g}) d^l_{m'n}(b).
@@ -290,26 +283,39 @@ __host__ __device__ __forceinline__ int xi_off(int l) { return l * (2 * l - 1) *
 // dense, phase-folded scratch so the n-sum runs over contiguous rows.  The
 // wedge-power kernel is rank one (conj(chi_lm) q_lm' / total), so its
 // composition only rotates q: q~_l = D^l(a) q_l  (O(l^2) per degree).
-__device__ void compose_kernels(const BandTables& T, const float2* src, const RefineArgs& a,
-                                const Quat& anchor, float* scratch, float2* out, float2* out_w,
-                                WarpScratch& ws) {
-    const int lane = threadIdx.x & 31;
+struct ComposeScratch {
+    double eul[3];
+    float2 ua[kMaxL + 1];
+    float2 ug[kMaxL + 1];
+    float cp[2 * kMaxL + 3];
+    float sp[2 * kMaxL + 3];
+};
+
+// Block-cooperative composition of one candidate's chart kernels; dtab / xd /
+// qt live in shared memory when they fit (else in global scratch).
+__device__ void compose_block(const BandTables& T, const float2* src, const StageArgs& a, const Quat& anchor,
+                              float* dtab, float2* xd, float2* qt, float2* out, float2* out_w,
+                              ComposeScratch& cs) {
+    const int tid = threadIdx.x, nt = blockDim.x;
     const int L = T.L;
-    const int nxi = xi_off(L + 1);
-    float* dtab = scratch;                                                  // nxi floats
-    float2* xd = reinterpret_cast<float2*>(scratch + ((nxi + 1) & ~1));    // nxi complex
-    float2* qt = xd + nxi;                                                  // (L+1)^2 complex
-    const Euler3 e = q_euler(anchor);
-    __syncwarp();
-    for (int m = lane; m <= L; m += 32) {
-        double sn, co;
-        sincos(m * e.a, &sn, &co);
-        ws.ua[m] = make_float2((float)co, (float)-sn);
-        sincos(m * e.g, &sn, &co);
-        ws.ug[m] = make_float2((float)co, (float)-sn);
+    if (tid == 0) {
+        const Euler3 e = q_euler(anchor);
+        cs.eul[0] = e.a;
+        cs.eul[1] = e.b;
+        cs.eul[2] = e.g;
     }
-    const double ch = cos(0.5 * e.b), sh = sin(0.5 * e.b);
-    for (int j = lane; j <= 2 * L + 2; j += 32) {
+    __syncthreads();
+    const double ea = cs.eul[0], eb = cs.eul[1], eg = cs.eul[2];
+    for (int m = tid; m <= L; m += nt) {
+        double sn, co;
+        sincos_d(m * ea, &sn, &co);
+        cs.ua[m] = make_float2((float)co, (float)-sn);
+        sincos_d(m * eg, &sn, &co);
+        cs.ug[m] = make_float2((float)co, (float)-sn);
+    }
+    double ch, sh;
+    sincos_d(0.5 * eb, &sh, &ch);
+    for (int j = tid; j <= 2 * L + 2; j += nt) {
         double pc = 1.0, ps = 1.0, bc = ch, bs = sh;
         for (int q = j; q; q >>= 1) {
             if (q & 1) {
@@ -319,54 +325,53 @@ __device__ void compose_kernels(const BandTables& T, const float2* src, const Re
             bc *= bc;
             bs *= bs;
         }
-        ws.cp[j] = (float)pc;
-        ws.sp[j] = (float)ps;
+        cs.cp[j] = (float)pc;
+        cs.sp[j] = (float)ps;
     }
-    __syncwarp();
-    const float cb = (float)cos(e.b);
+    __syncthreads();
+    const float cb = (float)cos(eb);
     // full-plane d^l_{m,m'}(b_a): half-plane chains + mirror
-    for (int g = 0; g < T.n_groups; ++g) {
-        const int item = g * 32 + lane;
+    for (int item = tid; item < T.n_groups * 32; item += nt) {
         const int len = T.item_len[item];
         const int m = T.item_mm[item].x, mp = T.item_mm[item].y;
         const int l0 = max(abs(m), abs(mp));
         const int be = T.bexp[item];
-        float d = T.bfac[item] * ws.cp[be & 0xff] * ws.sp[be >> 8], d1 = 0.0f;
+        float d = T.bfac[item] * cs.cp[be & 0xff] * cs.sp[be >> 8], d1 = 0.0f;
         const float mir = ((m - mp) & 1) ? -1.0f : 1.0f;
-        const int r0 = T.row_off[g];
-        for (int s = 0; s < len; ++s) {
-            if (s > 0) {
-                const float4 pqr = __ldg(T.PQR + (r0 + s) * 32 + lane);
+        const int r0 = T.row_off[item >> 5], lane = item & 31;
+        for (int st = 0; st < len; ++st) {
+            if (st > 0) {
+                const float4 pqr = __ldg(T.PQR + (r0 + st) * 32 + lane);
                 const float dn = fmaf(pqr.x, cb, pqr.y) * d - pqr.z * d1;
                 d1 = d;
                 d = dn;
             }
-            const int l = l0 + s, w = 2 * l + 1, o = xi_off(l);
+            const int l = l0 + st, w = 2 * l + 1, o = xi_off(l);
             dtab[o + (m + l) * w + (mp + l)] = d;
             dtab[o + (-m + l) * w + (-mp + l)] = mir * d;
         }
     }
     // dense xi'_l[m,n] = xi_l[m,n] e^{-i n g} (both half-planes)
-    for (int at = lane; at < T.rows * 32; at += 32) {
+    for (int at = tid; at < T.rows * 32; at += nt) {
         const int row = at >> 5, j = at & 31;
         const int g = a.row_group[row];
         const int item = g * 32 + j;
-        const int s = row - T.row_off[g];
-        if (s >= T.item_len[item]) continue;
+        const int st = row - T.row_off[g];
+        if (st >= T.item_len[item]) continue;
         const int m = T.item_mm[item].x, mp = T.item_mm[item].y;
-        const int l = max(abs(m), abs(mp)) + s, w = 2 * l + 1, o = xi_off(l);
+        const int l = max(abs(m), abs(mp)) + st, w = 2 * l + 1, o = xi_off(l);
         const float2 x = src[at];
-        float2 eg = ws.ug[abs(mp)];
-        if (mp < 0) eg.y = -eg.y;
-        xd[o + (m + l) * w + (mp + l)] = cmul(x, eg);
+        float2 egp = cs.ug[abs(mp)];
+        if (mp < 0) egp.y = -egp.y;
+        xd[o + (m + l) * w + (mp + l)] = cmul(x, egp);
         const float sg = ((m + mp) & 1) ? -1.0f : 1.0f;
         const float2 xm = make_float2(sg * x.x, -sg * x.y);  // xi[-m,-m']
-        xd[o + (-m + l) * w + (-mp + l)] = cmul(xm, make_float2(eg.x, -eg.y));
+        xd[o + (-m + l) * w + (-mp + l)] = cmul(xm, make_float2(egp.x, -egp.y));
     }
-    // wedge: q~_l[m'] = e^{-i m' a} sum_n d_{m'n} e^{-i n g} q_ln
+    __syncthreads();
     const bool wedge = out_w != nullptr;
-    if (wedge) {
-        for (int idx = lane; idx < (L + 1) * (L + 1); idx += 32) {
+    if (wedge) {  // q~_l[m'] = e^{-i m' a} sum_n d_{m'n} e^{-i n g} q_ln
+        for (int idx = tid; idx < (L + 1) * (L + 1); idx += nt) {
             int l = 0;
             while ((l + 1) * (l + 1) <= idx) ++l;
             const int mp = idx - l * l - l;
@@ -379,33 +384,32 @@ __device__ void compose_kernels(const BandTables& T, const float2* src, const Re
                     const double sgn = (an & 1) ? -1.0 : 1.0;
                     qv = make_double2(sgn * qv.x, -sgn * qv.y);
                 }
-                float2 eg = ws.ug[an];
-                if (n < 0) eg.y = -eg.y;
-                const float2 t = cmul(make_float2((float)qv.x, (float)qv.y), eg);
+                float2 egn = cs.ug[an];
+                if (n < 0) egn.y = -egn.y;
+                const float2 t = cmul(make_float2((float)qv.x, (float)qv.y), egn);
                 const float dv = dtab[o + (mp + l) * w + (n + l)];
                 re = fmaf(dv, t.x, re);
                 im = fmaf(dv, t.y, im);
             }
-            float2 ea = ws.ua[abs(mp)];
-            if (mp < 0) ea.y = -ea.y;
-            qt[idx] = cmul(ea, make_float2(re, im));
+            float2 eam = cs.ua[abs(mp)];
+            if (mp < 0) eam.y = -eam.y;
+            qt[idx] = cmul(eam, make_float2(re, im));
         }
+        __syncthreads();
     }
-    __syncwarp();
-    // xi~ in band layout
     const float inv_total = (float)(1.0 / a.wp_total);
-    for (int at = lane; at < T.rows * 32; at += 32) {
+    for (int at = tid; at < T.rows * 32; at += nt) {
         const int row = at >> 5, j = at & 31;
         const int g = a.row_group[row];
         const int item = g * 32 + j;
-        const int s = row - T.row_off[g];
-        if (s >= T.item_len[item]) {
+        const int st = row - T.row_off[g];
+        if (st >= T.item_len[item]) {
             out[at] = make_float2(0.f, 0.f);
             if (wedge) out_w[at] = make_float2(0.f, 0.f);
             continue;
         }
         const int m = T.item_mm[item].x, mp = T.item_mm[item].y;
-        const int l = max(abs(m), abs(mp)) + s, w = 2 * l + 1, o = xi_off(l);
+        const int l = max(abs(m), abs(mp)) + st, w = 2 * l + 1, o = xi_off(l);
         const float2* xr = xd + o + (m + l) * w;
         const float* dr = dtab + o + (mp + l) * w;
         float re = 0.0f, im = 0.0f;
@@ -415,9 +419,9 @@ __device__ void compose_kernels(const BandTables& T, const float2* src, const Re
             re = fmaf(x.x, dv, re);
             im = fmaf(x.y, dv, im);
         }
-        float2 ea = ws.ua[abs(mp)];
-        if (mp < 0) ea.y = -ea.y;
-        out[at] = cmul(ea, make_float2(re, im));
+        float2 eam = cs.ua[abs(mp)];
+        if (mp < 0) eam.y = -eam.y;
+        out[at] = cmul(eam, make_float2(re, im));
         if (wedge) {
             const int am = abs(m);
             double2 c = a.chi_hat[l * (l + 1) / 2 + am];
@@ -426,111 +430,11 @@ __device__ void compose_kernels(const BandTables& T, const float2* src, const Re
                 c = make_double2(sgn * c.x, -sgn * c.y);
             }
             const float2 qv = qt[l * l + (mp + l)];
-            // conj(chi_lm) q~_lm' / total
-            const float cr = (float)c.x, ci = (float)-c.y;
+            const float cr = (float)c.x, ci = (float)-c.y;  // conj(chi_lm)
             out_w[at] = make_float2((cr * qv.x - ci * qv.y) * inv_total, (cr * qv.y + ci * qv.x) * inv_total);
         }
     }
-    __syncwarp();
-}
-
-// Damped-Newton band of one candidate (warp-redundant scalar state).
-__device__ void newton_band(const RefineArgs& a, const float2* xi_s, CandState& st,
-                            WarpScratch& ws, float* scratch) {
-    const BandTables& T = a.T;
-    const RefineParams& prm = a.prm;
-    const bool wedge = prm.has_wedge != 0;
-    const int band = prm.band;
-    const Quat koff{prm.koffset[0], prm.koffset[1], prm.koffset[2], prm.koffset[3]};
-    const int nxi = xi_off(T.L + 1);
-    float2* xi_t = reinterpret_cast<float2*>(scratch + ((nxi + 1) & ~1)) + nxi + (T.L + 1) * (T.L + 1);
-    float2* w_t = xi_t + (size_t)T.rows * 32;
-    Quat g{st.g[0], st.g[1], st.g[2], st.g[3]};
-    Quat anchor{st.anchor[0], st.anchor[1], st.anchor[2], st.anchor[3]};
-    Quat best_g{st.best_g[0], st.best_g[1], st.best_g[2], st.best_g[3]};
-    double best = st.best_score;
-
-    auto reanchor = [&](const Quat& target) {
-        anchor = q_mul(q_inv(koff), target);
-        st.anchor_limit = band;
-        compose_kernels(T, xi_s, a, anchor, scratch, xi_t, wedge ? w_t : nullptr, ws);
-        st.anchored = 1;
-    };
-
-    double lambda = prm.step_damping;
-    st.band_converged = 0;
-    if (st.anchored && band > st.anchor_limit) reanchor(g);
-    for (int iter = 0; iter < prm.newton_max_iter; ++iter) {
-        Quat h = q_mul(g, q_inv(anchor));
-        Euler3 e = q_euler(h);
-        if (e.b < 0.05 || e.b > kPiD - 0.05) {
-            reanchor(g);
-            h = koff;
-            e = q_euler(h);
-        }
-        const float2* xs = st.anchored ? xi_t : xi_s;
-        const float2* wsrc = st.anchored ? w_t : T.wedge;
-        Derivs d;
-        eval_objective<2>(T, xs, wsrc, wedge, e, ws, d);
-        ++st.evals;
-        const double scale = fmax(fabs(d.v), 1e-300);
-        const double gnorm = sqrt(d.g[0] * d.g[0] + d.g[1] * d.g[1] + d.g[2] * d.g[2]);
-        if (d.v > best) {
-            best = d.v;
-            best_g = g;
-        }
-        if (gnorm <= prm.grad_tol * scale) {
-            st.band_converged = 1;
-            break;
-        }
-        bool accepted = false;
-        double lam = lambda;
-        for (int retry = 0; retry < 3 && !accepted; ++retry, lam *= 10.0) {
-            double mtx[9];
-            for (int i = 0; i < 9; ++i) mtx[i] = d.h[i];
-            mtx[0] -= lam;
-            mtx[4] -= lam;
-            mtx[8] -= lam;
-            LU3 lu;
-            lu.factor(mtx);
-            double p[3];
-            if (lu.invertible()) {
-                double x[3];
-                lu.solve(d.g, x);
-                p[0] = -x[0], p[1] = -x[1], p[2] = -x[2];
-            } else {
-                p[0] = d.g[0] / lam, p[1] = d.g[1] / lam, p[2] = d.g[2] / lam;
-            }
-            const double pn = sqrt(p[0] * p[0] + p[1] * p[1] + p[2] * p[2]);
-            if (pn > 1.0) {
-                const double sc = 1.0 / pn;
-                p[0] *= sc, p[1] *= sc, p[2] *= sc;
-            }
-            const Quat h_try = q_from_euler(e.a + p[0], e.b + p[1], e.g + p[2]);
-            Derivs tr;
-            eval_objective<0>(T, xs, wsrc, wedge, q_euler(h_try), ws, tr);
-            ++st.evals;
-            if (tr.v > d.v - prm.accept_tol * scale) {
-                g = q_mul(h_try, anchor);
-                lambda = fmax(lam / 10.0, 1e-12);
-                accepted = true;
-                if (tr.v > best) {
-                    best = tr.v;
-                    best_g = g;
-                }
-            }
-        }
-        if (!accepted) {
-            st.diverged = 1;
-            break;
-        }
-    }
-    st.g[0] = g.w, st.g[1] = g.x, st.g[2] = g.y, st.g[3] = g.z;
-    st.anchor[0] = anchor.w, st.anchor[1] = anchor.x, st.anchor[2] = anchor.y,
-    st.anchor[3] = anchor.z;
-    st.best_g[0] = best_g.w, st.best_g[1] = best_g.x, st.best_g[2] = best_g.y,
-    st.best_g[3] = best_g.z;
-    st.best_score = best;
+    __syncthreads();
 }
 
 // xi_l[m,m'] for the table entry (row, lane) from real-packed f and t
@@ -561,129 +465,368 @@ __device__ float2 xi_entry(const BandTables& T, const int* row_group, const floa
     return make_float2(re, im);
 }
 
-constexpr int kRefineWarps = 16;
-constexpr int kMaxBatch = 8;
 
-// Persistent CTAs take batches of `a.batch` windows: their kernels are built in
-// shared memory, then the CTA's 16 warps pull (window, candidate) items from
-// one pooled queue, so the per-candidate Newton time imbalance averages over
-// the whole batch instead of stalling every window at a barrier.
-__global__ void __launch_bounds__(kRefineWarps * 32, 1) refine_kernel(RefineArgs a) {
-    extern __shared__ __align__(16) unsigned char sm[];
-    const BandTables& T = a.T;
-    const int xi_len = T.rows * 32;
-    float2* xib = reinterpret_cast<float2*>(sm);                               // batch * rows*32
-    float* tbuf = reinterpret_cast<float*>(xib + (size_t)a.batch * xi_len);    // rows_band
-    float* fbuf = tbuf + a.rows_band;                                          // rows_band
-    WarpScratch* wsc = reinterpret_cast<WarpScratch*>(
-        (reinterpret_cast<uintptr_t>(fbuf + a.rows_band) + 15) & ~uintptr_t(15));
-    __shared__ int s_w0, s_next, s_nitems;
-    __shared__ int s_start[kMaxBatch + 1];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    WarpScratch& ws = wsc[warp];
-    float* scratch = a.scratch + (size_t)(blockIdx.x * kRefineWarps + warp) * a.scratch_per_warp;
+// ---------------------------------------------------------------- scalar Newton
+struct Derivs {
+    double v;
+    double g[3];
+    double h[9];
+};
 
-    for (int r = threadIdx.x; r < a.rows_band; r += blockDim.x) tbuf[r] = a.t_hat[r];
-    for (;;) {
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            s_w0 = atomicAdd(a.win_counter, a.batch);
-            s_next = 0;
-            int acc = 0;
-            for (int b = 0; b < a.batch; ++b) {
-                s_start[b] = acc;
-                const int w = s_w0 + b;
-                acc += w < a.n_win ? a.cand_count[w] : 0;
-            }
-            s_start[a.batch] = acc;
-            s_nitems = acc;
-        }
-        __syncthreads();
-        const int w0 = s_w0;
-        if (w0 >= a.n_win) break;
-        const int nb = min(a.batch, a.n_win - w0);
-        // build the batch's kernels (windows without candidates are skipped)
-        for (int b = 0; b < nb; ++b) {
-            if (s_start[b + 1] == s_start[b]) continue;
-            const float* cw = a.coef + (long long)(w0 + b) * a.ldc;
-            for (int r = threadIdx.x; r < a.rows_band; r += blockDim.x) fbuf[r] = cw[r];
-            __syncthreads();
-            float2* xi = xib + (size_t)b * xi_len;
-            for (int e = threadIdx.x; e < xi_len; e += blockDim.x)
-                xi[e] = xi_entry(T, a.row_group, fbuf, tbuf, a.block_off, a.radial_count, e >> 5, e & 31);
-            __syncthreads();
-        }
-        const int nitems = s_nitems;
-        for (;;) {
-            int it = 0;
-            if (lane == 0) it = atomicAdd(&s_next, 1);
-            it = __shfl_sync(0xffffffffu, it, 0);
-            if (it >= nitems) break;
-            int b = 0;
-            while (it >= s_start[b + 1]) ++b;
-            const int c = it - s_start[b];
-            const float2* xi = xib + (size_t)b * xi_len;
-            CandState* cs = a.cand + (size_t)(w0 + b) * a.max_cand;
-            CandState st = cs[c];
-            if (!st.diverged) newton_band(a, xi, st, ws, scratch);
-            if (a.last_band) {
-                // final unanchored score at the top band (optimize.cpp:349-352)
-                const Quat rq = st.diverged ? Quat{st.best_g[0], st.best_g[1], st.best_g[2], st.best_g[3]}
-                                            : Quat{st.g[0], st.g[1], st.g[2], st.g[3]};
-                Derivs f;
-                eval_objective<0>(T, xi, T.wedge, a.prm.has_wedge != 0, q_euler(rq), ws, f);
-                st.score = f.v;
-                ++st.evals;
-            }
-            if (lane == 0) cs[c] = st;
-            __syncwarp();
-        }
-        __syncthreads();
-        if (a.last_band && threadIdx.x < nb) {
-            const int w = w0 + threadIdx.x;
-            const int nc = a.cand_count[w];
-            const CandState* cs = a.cand + (size_t)w * a.max_cand;
-            WindowOutcome o;
-            o.particle = a.win_particle[w];
-            o.shift[0] = a.win_shift[3 * w];
-            o.shift[1] = a.win_shift[3 * w + 1];
-            o.shift[2] = a.win_shift[3 * w + 2];
-            o.n_cand = nc;
-            o.sub_norm = a.sub_norm[w];
-            o.valid = (nc > 0 && o.sub_norm > 0.0) ? 1 : 0;
-            o.evals = a.grid_evals;
-            int best = -1;
-            double bs = 0.0, ba = 0.0;
-            for (int c = 0; c < nc; ++c) {
-                const CandState& st = cs[c];
-                o.evals += st.evals;
-                const Quat rq = st.diverged ? Quat{st.best_g[0], st.best_g[1], st.best_g[2], st.best_g[3]}
-                                            : Quat{st.g[0], st.g[1], st.g[2], st.g[3]};
-                const double ang = q_angle(rq);
-                // search_one_shift tie rule (optimize.cpp:405-412)
-                if (best < 0 || st.score > bs || (st.score == bs && ang < ba)) {
-                    best = c;
-                    bs = st.score;
-                    ba = ang;
+__device__ void unpack(const double* res, int order, Derivs& c) {
+    c.v = res[0];
+    if (order >= 1) c.g[0] = res[1], c.g[1] = res[2], c.g[2] = res[3];
+    if (order >= 2) {  // res: aa ab ag bb bg gg
+        c.h[0] = res[4], c.h[1] = res[5], c.h[2] = res[6];
+        c.h[3] = res[5], c.h[4] = res[7], c.h[5] = res[8];
+        c.h[6] = res[6], c.h[7] = res[8], c.h[8] = res[9];
+    }
+}
+
+// Objective::eval (src/optimize.cpp:106-130): C / sqrt(clamp(1 - rho, 0.02, 2))
+__device__ void objective(const double* cr, const double* rr, bool wedge, int order, Derivs& f) {
+    Derivs c, r;
+    unpack(cr, order, c);
+    if (!wedge) {
+        f = c;
+        return;
+    }
+    unpack(rr, order, r);
+    const double v = fmin(fmax(1.0 - r.v, 0.02), 2.0);
+    const double s = 1.0 / sqrt(v);
+    f.v = c.v * s;
+    if (order >= 1) {
+        const double dv[3] = {-r.g[0], -r.g[1], -r.g[2]};
+        const double v32 = s / v;
+        for (int i = 0; i < 3; ++i) f.g[i] = c.g[i] * s - 0.5 * c.v * v32 * dv[i];
+        if (order >= 2) {
+            const double v52 = v32 / v;
+            for (int i = 0; i < 3; ++i)
+                for (int j = 0; j < 3; ++j) {
+                    const double hv = -r.h[i * 3 + j];
+                    f.h[i * 3 + j] = c.h[i * 3 + j] * s -
+                                     0.5 * v32 * (c.g[i] * dv[j] + dv[i] * c.g[j] + c.v * hv) +
+                                     0.75 * c.v * v52 * dv[i] * dv[j];
                 }
-            }
-            o.best_cand = best;
-            if (best >= 0) {
-                const CandState& st = cs[best];
-                const double* q = st.diverged ? st.best_g : st.g;
-                for (int i = 0; i < 4; ++i) o.quat[i] = q[i];
-                o.raw_score = st.score;
-                o.converged = (!st.diverged && st.band_converged) ? 1 : 0;
-                o.norm_score = o.valid ? st.score / (a.t_norm * o.sub_norm) : -DBL_MAX;
-            } else {
-                o.quat[0] = 1.0, o.quat[1] = o.quat[2] = o.quat[3] = 0.0;
-                o.raw_score = 0.0;
-                o.converged = 0;
-                o.norm_score = -DBL_MAX;
-            }
-            a.out[w] = o;
         }
     }
+}
+
+// damped step from wk.f with wk.lam, trial chart rotation (optimize.cpp:313-328)
+__device__ void make_trial(CandWork& wk) {
+    double m[9];
+    for (int i = 0; i < 9; ++i) m[i] = wk.f[4 + i];
+    m[0] -= wk.lam;
+    m[4] -= wk.lam;
+    m[8] -= wk.lam;
+    const double g[3] = {wk.f[1], wk.f[2], wk.f[3]};
+    double p[3];
+    LU3 lu;
+    lu.factor(m);
+    if (lu.invertible()) {
+        double x[3];
+        lu.solve(g, x);
+        p[0] = -x[0], p[1] = -x[1], p[2] = -x[2];
+    } else {
+        p[0] = g[0] / wk.lam, p[1] = g[1] / wk.lam, p[2] = g[2] / wk.lam;
+    }
+    const double pn = sqrt(p[0] * p[0] + p[1] * p[1] + p[2] * p[2]);
+    if (pn > 1.0) {
+        const double sc = 1.0 / pn;
+        p[0] *= sc, p[1] *= sc, p[2] *= sc;
+    }
+    const Quat h = q_from_euler(wk.e[0] + p[0], wk.e[1] + p[1], wk.e[2] + p[2]);
+    wk.gt[0] = h.w, wk.gt[1] = h.x, wk.gt[2] = h.y, wk.gt[3] = h.z;
+    const Euler3 et = q_euler(h);
+    wk.et[0] = et.a, wk.et[1] = et.b, wk.et[2] = et.g;
+}
+
+__device__ __forceinline__ Quat qload(const double* q) { return Quat{q[0], q[1], q[2], q[3]}; }
+__device__ __forceinline__ void qstore(double* d, const Quat& q) {
+    d[0] = q.w, d[1] = q.x, d[2] = q.y, d[3] = q.z;
+}
+
+__device__ __forceinline__ bool slot_of(const StageArgs& a, long long idx) {
+    const int w = (int)(idx / a.max_cand), c = (int)(idx % a.max_cand);
+    return w < a.n_win && c < a.cand_count[w];
+}
+
+__global__ void band_begin_kernel(StageArgs a) {
+    const long long n = (long long)a.n_win * a.max_cand;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        CandWork& wk = a.work[i];
+        wk.slot = -1;
+        wk.compose = 0;
+        wk.iter = 0;
+        wk.retry = 0;
+        wk.status = ST_DONE;
+        if (!slot_of(a, i)) continue;
+        CandState& st = a.cand[i];
+        if (!st.active || st.diverged) continue;
+        wk.lambda = a.prm.step_damping;
+        st.band_converged = 0;
+        if (st.anchored && a.prm.band > st.anchor_limit) {  // widen the chart kernel
+            const Quat koff{a.prm.koffset[0], a.prm.koffset[1], a.prm.koffset[2], a.prm.koffset[3]};
+            qstore(st.anchor, q_mul(q_inv(koff), qload(st.g)));
+            st.anchor_limit = a.prm.band;
+            wk.compose = 1;
+        }
+        wk.status = ST_START;
+    }
+}
+
+// chart / re-anchor decision of every candidate still iterating; appends to
+// the order-2 list and the composition list
+__global__ void iter_begin_kernel(StageArgs a) {
+    const long long n = (long long)a.n_win * a.max_cand;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        CandWork& wk = a.work[i];
+        if (wk.status != ST_START) continue;
+        if (wk.iter >= a.prm.newton_max_iter) {
+            wk.status = ST_DONE;
+            continue;
+        }
+        CandState& st = a.cand[i];
+        const Quat g = qload(st.g);
+        Euler3 e = q_euler(q_mul(g, q_inv(qload(st.anchor))));
+        if (e.b < 0.05 || e.b > kPiD - 0.05) {
+            const Quat koff{a.prm.koffset[0], a.prm.koffset[1], a.prm.koffset[2], a.prm.koffset[3]};
+            qstore(st.anchor, q_mul(q_inv(koff), g));
+            st.anchor_limit = a.prm.band;
+            st.anchored = 1;
+            wk.compose = 1;
+            e = q_euler(koff);
+        }
+        wk.e[0] = e.a, wk.e[1] = e.b, wk.e[2] = e.g;
+        wk.status = ST_EVAL2;
+        ++wk.iter;
+        a.list2[atomicAdd(a.counts + CNT_L2, 1)] = (int)i;
+        if (wk.compose) a.listc[atomicAdd(a.counts + CNT_COMP, 1)] = (int)i;
+    }
+}
+
+// one CTA per candidate of the composition list
+__global__ void __launch_bounds__(256) compose_kernel(StageArgs a) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    __shared__ ComposeScratch cs;
+    __shared__ int s_slot;
+    const int n = a.counts[CNT_COMP];
+    const int L = a.T.L;
+    const int nxi = xi_off(L + 1);
+    const int len = a.T.rows * 32;
+    const bool wedge = a.prm.has_wedge != 0;
+    float* dtab;
+    float2 *xd, *qt;
+    if (a.compose_smem) {
+        dtab = reinterpret_cast<float*>(sm);
+        xd = reinterpret_cast<float2*>(dtab + ((nxi + 1) & ~1));
+        qt = xd + nxi;
+    } else {
+        float* base = a.scratch + (size_t)blockIdx.x * a.scratch_per_warp;
+        dtab = base;
+        xd = reinterpret_cast<float2*>(dtab + ((nxi + 1) & ~1));
+        qt = xd + nxi;
+    }
+    for (int q = blockIdx.x; q < n; q += gridDim.x) {
+        const int i = a.listc[q];
+        CandWork& wk = a.work[i];
+        if (threadIdx.x == 0) {
+            int slot = wk.slot;
+            if (slot < 0) {
+                slot = atomicAdd(a.pool_counter, 1);
+                if (slot >= a.pool) {  // pool exhausted: the host reruns this chunk
+                    *a.overflow = 1;
+                    wk.status = ST_DONE;
+                    slot = -1;
+                }
+            }
+            s_slot = slot;
+        }
+        __syncthreads();
+        const int slot = s_slot;
+        if (slot >= 0) {
+            const int w = i / a.max_cand;
+            compose_block(a.T, a.xi_win + (size_t)w * len, a, qload(a.cand[i].anchor), dtab, xd, qt,
+                          a.xi_pool + (size_t)slot * len, wedge ? a.w_pool + (size_t)slot * len : nullptr, cs);
+        }
+        if (threadIdx.x == 0) {
+            wk.slot = slot;
+            wk.compose = 0;
+        }
+        __syncthreads();
+    }
+}
+
+// warp per listed candidate
+template <int ORDER>
+__global__ void __launch_bounds__(kWarps * 32) eval_kernel(StageArgs a, const int* list, const int* count) {
+    __shared__ WarpScratch wsc[kWarps];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n = *count;
+    const int len = a.T.rows * 32;
+    const bool wedge = a.prm.has_wedge != 0;
+    for (int q = blockIdx.x * kWarps + warp; q < n; q += gridDim.x * kWarps) {
+        const int i = list[q];
+        CandWork& wk = a.work[i];
+        const int w = i / a.max_cand;
+        const bool fin = wk.status == ST_FINAL;
+        const bool chart = !fin && a.cand[i].anchored;
+        const float2* xi = chart ? a.xi_pool + (size_t)wk.slot * len : a.xi_win + (size_t)w * len;
+        const float2* wx = !wedge ? nullptr : (chart ? a.w_pool + (size_t)wk.slot * len : a.T.wedge);
+        const double* e = wk.status == ST_EVAL2 ? wk.e : wk.et;
+        warp_eval<ORDER>(a.T, xi, wx, e[0], e[1], e[2], wsc[warp]);
+        constexpr int NV = ORDER == 0 ? 1 : 10;
+        if (lane < NV) {
+            wk.c[lane] = wsc[warp].res[lane];
+            wk.r[lane] = wsc[warp].res[10 + lane];
+        }
+        __syncwarp();
+    }
+}
+
+// Newton step of every order-2 evaluated candidate; appends trials to list_out
+__global__ void step_kernel(StageArgs a, int* list_out, int* count_out) {
+    const int n = a.counts[CNT_L2];
+    const bool wedge = a.prm.has_wedge != 0;
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+        const int i = a.list2[q];
+        CandWork& wk = a.work[i];
+        CandState& st = a.cand[i];
+        Derivs f;
+        objective(wk.c, wk.r, wedge, 2, f);
+        ++st.evals;
+        wk.f[0] = f.v;
+        for (int k = 0; k < 3; ++k) wk.f[1 + k] = f.g[k];
+        for (int k = 0; k < 9; ++k) wk.f[4 + k] = f.h[k];
+        const double scale = fmax(fabs(f.v), 1e-300);
+        const double gnorm = sqrt(f.g[0] * f.g[0] + f.g[1] * f.g[1] + f.g[2] * f.g[2]);
+        if (f.v > st.best_score) {
+            st.best_score = f.v;
+            for (int k = 0; k < 4; ++k) st.best_g[k] = st.g[k];
+        }
+        if (gnorm <= a.prm.grad_tol * scale) {
+            st.band_converged = 1;
+            wk.status = ST_DONE;
+            continue;
+        }
+        wk.lam = wk.lambda;
+        wk.retry = 0;
+        make_trial(wk);
+        wk.status = ST_EVAL0;
+        list_out[atomicAdd(count_out, 1)] = i;
+    }
+}
+
+// acceptance test of every trial in list_in; failed trials with retries left
+// are re-queued in list_out
+__global__ void accept_kernel(StageArgs a, const int* list_in, const int* count_in, int* list_out,
+                              int* count_out) {
+    const int n = *count_in;
+    const bool wedge = a.prm.has_wedge != 0;
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+        const int i = list_in[q];
+        CandWork& wk = a.work[i];
+        CandState& st = a.cand[i];
+        Derivs t;
+        objective(wk.c, wk.r, wedge, 0, t);
+        ++st.evals;
+        const double scale = fmax(fabs(wk.f[0]), 1e-300);
+        // tolerant acceptance (optimize.cpp:330-341)
+        if (t.v > wk.f[0] - a.prm.accept_tol * scale) {
+            qstore(st.g, q_mul(qload(wk.gt), qload(st.anchor)));
+            wk.lambda = fmax(wk.lam / 10.0, 1e-12);
+            if (t.v > st.best_score) {
+                st.best_score = t.v;
+                for (int k = 0; k < 4; ++k) st.best_g[k] = st.g[k];
+            }
+            wk.status = ST_START;
+        } else {
+            ++wk.retry;
+            wk.lam *= 10.0;
+            if (wk.retry == 3) {  // three damped retries failed to ascend
+                st.diverged = 1;
+                wk.status = ST_DONE;
+            } else {
+                make_trial(wk);
+                list_out[atomicAdd(count_out, 1)] = i;
+            }
+        }
+    }
+}
+
+__global__ void final_prep_kernel(StageArgs a) {
+    const long long n = (long long)a.n_win * a.max_cand;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        CandWork& wk = a.work[i];
+        wk.status = ST_DONE;
+        if (!slot_of(a, i) || !a.cand[i].active) continue;
+        const CandState& st = a.cand[i];
+        const Euler3 e = q_euler(qload(st.diverged ? st.best_g : st.g));
+        wk.et[0] = e.a, wk.et[1] = e.b, wk.et[2] = e.g;
+        wk.status = ST_FINAL;
+        a.list2[atomicAdd(a.counts + CNT_L2, 1)] = (int)i;
+    }
+}
+
+__global__ void final_score_kernel(StageArgs a) {
+    const int n = a.counts[CNT_L2];
+    const bool wedge = a.prm.has_wedge != 0;
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+        const int i = a.list2[q];
+        CandWork& wk = a.work[i];
+        Derivs t;
+        objective(wk.c, wk.r, wedge, 0, t);
+        a.cand[i].score = t.v;
+        ++a.cand[i].evals;
+        wk.status = ST_DONE;
+    }
+}
+
+__global__ void window_reduce_kernel(ReduceArgs a) {
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= a.n_win) return;
+    const int nc = a.cand_count[w];
+    const CandState* cs = a.cand + (size_t)w * a.max_cand;
+    WindowOutcome o;
+    o.particle = a.win_particle[w];
+    o.shift[0] = a.win_shift[3 * w];
+    o.shift[1] = a.win_shift[3 * w + 1];
+    o.shift[2] = a.win_shift[3 * w + 2];
+    o.n_cand = nc;
+    o.sub_norm = a.sub_norm[w];
+    o.valid = (nc > 0 && o.sub_norm > 0.0) ? 1 : 0;
+    o.evals = a.grid_evals;
+    int best = -1;
+    double bs = 0.0, ba = 0.0;
+    for (int c = 0; c < nc; ++c) {
+        const CandState& st = cs[c];
+        o.evals += st.evals;
+        const double ang = q_angle(qload(st.diverged ? st.best_g : st.g));
+        // search_one_shift tie rule (optimize.cpp:405-412)
+        if (best < 0 || st.score > bs || (st.score == bs && ang < ba)) {
+            best = c;
+            bs = st.score;
+            ba = ang;
+        }
+    }
+    o.best_cand = best;
+    if (best >= 0) {
+        const CandState& st = cs[best];
+        const double* q = st.diverged ? st.best_g : st.g;
+        for (int i = 0; i < 4; ++i) o.quat[i] = q[i];
+        o.raw_score = st.score;
+        o.converged = (!st.diverged && st.band_converged) ? 1 : 0;
+        o.norm_score = o.valid ? st.score / (a.t_norm * o.sub_norm) : -DBL_MAX;
+    } else {
+        o.quat[0] = 1.0, o.quat[1] = o.quat[2] = o.quat[3] = 0.0;
+        o.raw_score = 0.0;
+        o.converged = 0;
+        o.norm_score = -DBL_MAX;
+    }
+    a.out[w] = o;
 }
 
 // ---------------------------------------------------------------- sweep
@@ -695,17 +838,18 @@ __global__ void __launch_bounds__(kWarps * 32) eval_sweep_kernel(EvalArgs a) {
          u += (long long)gridDim.x * kWarps) {
         const int p = (int)(u / a.n_rot), gi = (int)(u % a.n_rot);
         const float2* xi = a.xi + (size_t)p * a.T.rows * 32;
-        Derivs c, r;
         const double* e = a.euler + 3 * gi;
-        if (a.order >= 1) warp_eval<1, false>(a.T, xi, nullptr, e[0], e[1], e[2], wsc[warp], c, r);
-        else warp_eval<0, false>(a.T, xi, nullptr, e[0], e[1], e[2], wsc[warp], c, r);
+        if (a.order >= 1) warp_eval<1>(a.T, xi, nullptr, e[0], e[1], e[2], wsc[warp]);
+        else warp_eval<0>(a.T, xi, nullptr, e[0], e[1], e[2], wsc[warp]);
         if (lane == 0) {
+            const double* r = wsc[warp].res;
             double* o = a.out + 4 * u;
-            o[0] = c.v;
-            o[1] = a.order >= 1 ? c.g[0] : 0.0;
-            o[2] = a.order >= 1 ? c.g[1] : 0.0;
-            o[3] = a.order >= 1 ? c.g[2] : 0.0;
+            o[0] = r[0];
+            o[1] = a.order >= 1 ? r[1] : 0.0;
+            o[2] = a.order >= 1 ? r[2] : 0.0;
+            o[3] = a.order >= 1 ? r[3] : 0.0;
         }
+        __syncwarp();
     }
 }
 
@@ -719,45 +863,52 @@ __global__ void build_xi_kernel(XiArgs a) {
 
 }  // namespace
 
-static size_t refine_fixed_bytes(int rows_band) {
-    return sizeof(float) * 2 * rows_band + 16 + sizeof(WarpScratch) * kRefineWarps;
+long long compose_scratch_floats(int L) {
+    // dtab (N_xi floats) + dense xi' (N_xi complex) + q~ ((L+1)^2 complex)
+    const long long nxi = xi_off(L + 1);
+    return ((nxi + 2) + 2 * nxi + 2LL * (L + 1) * (L + 1) + 3) / 4 * 4;
 }
 
-int refine_batch(const BandTables& T, int rows_band) {
-    const size_t budget = 200 * 1024;
-    const size_t fixed = refine_fixed_bytes(rows_band);
-    const size_t per = sizeof(float2) * (size_t)T.rows * 32;
-    int b = fixed + per <= budget ? (int)((budget - fixed) / per) : 1;
-    return b < 1 ? 1 : (b > kMaxBatch ? kMaxBatch : b);
+size_t compose_smem_bytes(int L) { return sizeof(float) * (size_t)compose_scratch_floats(L); }
+
+static int thread_grid(long long n) {
+    long long b = (n + 255) / 256;
+    return (int)(b < 1 ? 1 : (b > 4096 ? 4096 : b));
 }
 
-size_t refine_smem_bytes(const BandTables& T, int rows_band, int batch) {
-    return sizeof(float2) * (size_t)T.rows * 32 * batch + refine_fixed_bytes(rows_band);
+void launch_band_begin(const StageArgs& a, cudaStream_t s) {
+    band_begin_kernel<<<thread_grid((long long)a.n_win * a.max_cand), 256, 0, s>>>(a);
 }
-
-long long refine_scratch_floats(const BandTables& T) {
-    // dtab (N_xi floats) + dense xi' (N_xi complex) + q~ ((L+1)^2 complex) + two band-layout kernels
-    const long long nxi = xi_off(T.L + 1);
-    return (nxi + 2) + 2 * nxi + 2LL * (T.L + 1) * (T.L + 1) + 4LL * T.rows * 32;
+void launch_iter_begin(const StageArgs& a, cudaStream_t s) {
+    iter_begin_kernel<<<thread_grid((long long)a.n_win * a.max_cand), 256, 0, s>>>(a);
 }
-
-int refine_warps() { return kRefineWarps; }
-
-int refine_resident_blocks(const BandTables& T, int rows_band, int batch, int device) {
-    const size_t smem = refine_smem_bytes(T, rows_band, batch);
-    cudaFuncSetAttribute(refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int per_sm = 0, sms = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, refine_kernel, kRefineWarps * 32, smem);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    return (per_sm > 0 ? per_sm : 1) * sms;
+void launch_compose(const StageArgs& a, int n, cudaStream_t s) {
+    if (n <= 0) return;
+    const size_t smem = a.compose_smem ? compose_smem_bytes(a.T.L) : 0;
+    if (smem) cudaFuncSetAttribute(compose_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    compose_kernel<<<n, 256, smem, s>>>(a);
 }
-
-int launch_refine(const RefineArgs& a, int blocks, cudaStream_t s) {
-    if (a.n_win <= 0) return 0;
-    const size_t smem = refine_smem_bytes(a.T, a.rows_band, a.batch);
-    cudaFuncSetAttribute(refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    refine_kernel<<<blocks, kRefineWarps * 32, smem, s>>>(a);
-    return cudaGetLastError() == cudaSuccess ? 0 : 2;
+void launch_eval(const StageArgs& a, int order, const int* list, const int* count, int max_n, cudaStream_t s) {
+    if (max_n <= 0) return;
+    const int grid = (max_n + kWarps - 1) / kWarps;
+    if (order == 2) eval_kernel<2><<<grid, kWarps * 32, 0, s>>>(a, list, count);
+    else eval_kernel<0><<<grid, kWarps * 32, 0, s>>>(a, list, count);
+}
+void launch_step(const StageArgs& a, int* list_out, int* count_out, int max_n, cudaStream_t s) {
+    step_kernel<<<thread_grid(max_n), 256, 0, s>>>(a, list_out, count_out);
+}
+void launch_accept(const StageArgs& a, const int* list_in, const int* count_in, int* list_out, int* count_out,
+                   int max_n, cudaStream_t s) {
+    accept_kernel<<<thread_grid(max_n), 256, 0, s>>>(a, list_in, count_in, list_out, count_out);
+}
+void launch_final_prep(const StageArgs& a, cudaStream_t s) {
+    final_prep_kernel<<<thread_grid((long long)a.n_win * a.max_cand), 256, 0, s>>>(a);
+}
+void launch_final_score(const StageArgs& a, int max_n, cudaStream_t s) {
+    final_score_kernel<<<thread_grid(max_n), 256, 0, s>>>(a);
+}
+void launch_window_reduce(const ReduceArgs& a, cudaStream_t s) {
+    window_reduce_kernel<<<(a.n_win + 127) / 128, 128, 0, s>>>(a);
 }
 
 int launch_eval_sweep(const EvalArgs& a, cudaStream_t s) {

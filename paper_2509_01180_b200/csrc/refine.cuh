@@ -1,4 +1,4 @@
-// Refinement kernel interface (kernels K4/K5/K7).
+// Refinement interface (kernels K4/K5/K7): bulk-synchronous damped Newton.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -7,44 +7,79 @@
 
 namespace bmb {
 
-struct RefineArgs {
-    BandTables T;                   // tables of this band
-    const int* row_group = nullptr;  // [T.rows] group of each table row
-    const float* coef = nullptr;    // [n_win][ldc] real-packed window coefficients
-    int ldc = 0;
-    const float* t_hat = nullptr;
-    const int* block_off = nullptr;
-    const int* radial_count = nullptr;
-    int rows_band = 0;              // real-packed rows of degrees <= band
-    const int* cand_count = nullptr;
+// Per-candidate working state of the bulk-synchronous Newton iteration.
+enum CandStatus : int { ST_DONE = 0, ST_START = 1, ST_EVAL2 = 2, ST_EVAL0 = 3, ST_FINAL = 4 };
+
+struct CandWork {
+    double e[3];    // chart Euler angles of the current iterate
+    double et[3];   // chart Euler angles of the trial iterate
+    double gt[4];   // trial chart rotation h_try
+    double c[10];   // raw correlation derivatives (value, grad, hess aa ab ag bb bg gg)
+    double r[10];   // raw wedge-power derivatives
+    double f[13];   // objective at e: value, grad[3], hess[9]
+    double lambda;  // Levenberg parameter of the iteration
+    double lam;     // damping of the current retry
+    int status;
+    int retry;
+    int iter;
+    int compose;    // 1: the chart kernel must be (re)built
+    int slot;       // pool slot of the anchored-chart kernels (-1: none this band)
+    int pad;
+};
+
+struct StageArgs {
+    BandTables T;
+    const int* row_group = nullptr;
+    const float2* xi_win = nullptr;  // [n_win][T.rows*32] window kernels
+    float2* xi_pool = nullptr;       // [pool][T.rows*32] anchored correlation kernels
+    float2* w_pool = nullptr;        // [pool][T.rows*32] anchored wedge kernels
+    int pool = 0;
+    int* pool_counter = nullptr;     // slot allocator (reset per band)
+    int* overflow = nullptr;         // set when the pool is exhausted
     CandState* cand = nullptr;
+    CandWork* work = nullptr;
+    const int* cand_count = nullptr;
     int max_cand = 0;
     int n_win = 0;
-    int batch = 1;                  // windows per CTA batch (refine_batch)
-    int* win_counter = nullptr;     // zeroed before launch
-    float* scratch = nullptr;       // per resident warp: anchored-chart kernels
-    long long scratch_per_warp = 0; // floats
     RefineParams prm;
-    int last_band = 0;
-    // outcome (last band only)
+    const double2* chi_hat = nullptr;
+    const double2* q_hat = nullptr;
+    double wp_total = 1.0;
+    float* scratch = nullptr;        // compose temporaries per CTA (when not in shared memory)
+    long long scratch_per_warp = 0;  // floats per composing CTA
+    int compose_smem = 0;            // compose temporaries in shared memory
+    int* counts = nullptr;           // [CNT_*] list lengths
+    int* list2 = nullptr;            // candidates awaiting the order-2 evaluation (or final)
+    int* listc = nullptr;            // candidates whose chart kernel must be (re)built
+};
+enum { CNT_L2 = 0, CNT_COMP = 1, CNT_T0 = 2, CNT_T1 = 3 };
+
+// one window outcome per window (last band)
+struct ReduceArgs {
+    const CandState* cand = nullptr;
+    const int* cand_count = nullptr;
+    int max_cand = 0;
+    int n_win = 0;
     const double* sub_norm = nullptr;
     double t_norm = 0.0;
     const int* win_particle = nullptr;
     const int* win_shift = nullptr;
-    long long grid_evals = 0;       // seed-grid evaluations per window
+    long long grid_evals = 0;
     WindowOutcome* out = nullptr;
-    // wedge-power factors (packed (l, m >= 0)) for the anchored-chart composition
-    const double2* chi_hat = nullptr;
-    const double2* q_hat = nullptr;
-    double wp_total = 1.0;
 };
 
-int refine_batch(const BandTables& T, int rows_band);
-size_t refine_smem_bytes(const BandTables& T, int rows_band, int batch);
-long long refine_scratch_floats(const BandTables& T);
-int refine_warps();
-int refine_resident_blocks(const BandTables& T, int rows_band, int batch, int device);
-int launch_refine(const RefineArgs& a, int blocks, cudaStream_t s);
+long long compose_scratch_floats(int L);
+size_t compose_smem_bytes(int L);
+void launch_band_begin(const StageArgs& a, cudaStream_t s);
+void launch_iter_begin(const StageArgs& a, cudaStream_t s);
+void launch_compose(const StageArgs& a, int n, cudaStream_t s);
+void launch_eval(const StageArgs& a, int order, const int* list, const int* count, int max_n, cudaStream_t s);
+void launch_step(const StageArgs& a, int* list_out, int* count_out, int max_n, cudaStream_t s);
+void launch_accept(const StageArgs& a, const int* list_in, const int* count_in, int* list_out, int* count_out,
+                   int max_n, cudaStream_t s);
+void launch_final_prep(const StageArgs& a, cudaStream_t s);
+void launch_final_score(const StageArgs& a, int max_n, cudaStream_t s);
+void launch_window_reduce(const ReduceArgs& a, cudaStream_t s);
 
 // standalone batched evaluation (rotate-score-gradient sweep, config 4):
 // value + gradient of C(g) = Re sum xi D(g) for n_xi kernels x n_rot angle
