@@ -48,7 +48,19 @@ def parse():
     ap.add_argument("--particles", type=int, default=CFG["particles"], help="per rank per step")
     ap.add_argument("--cpu-sample", type=int, default=4, help="particles in the CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--expand", default="factored", choices=["factored", "gemm"],
+                    help="expansion algorithm (K2f factored, or the dense operator on tcgen05)")
     return ap.parse_args()
+
+
+def fp32_simt_peak():
+    """FP32 FMA throughput: profiles/fp32_peak.json (tools/probe_fp32_peak.cu measured on
+    this pool's B200), else the nominal 148 SM x 128 lanes x 2 x 1.965 GHz."""
+    p = ROOT / "profiles" / "fp32_peak.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["fp32_fma_tflops"]), "measured (tools/probe_fp32_peak.cu, profiles/fp32_peak.json)"
+    return 148 * 128 * 2 * 1.965e9 / 1e12, "nominal (148 SM x 128 FMA/clk x 1.965 GHz); not measured"
 
 
 def measured_peaks():
@@ -201,6 +213,7 @@ def run_product(args):
     P = args.particles
 
     ctx = api.Context(CFG["n"], CFG["l_max"], CFG["lambda_cut"], device=local)
+    ctx.set_expand_mode(args.expand)
     tmpl = api.make_template(CFG["n"], CFG["blobs"], CFG["template_seed"], device=local)
     ctx.set_template(tmpl, CFG["wedge"])
     parts, q_true, s_true = api.make_particles(tmpl, P, 1000 + rank * 10_000_000, CFG["shift_max"],
@@ -268,9 +281,11 @@ def run_product(args):
     # context stream (kernel shares for the roofline), outside the timed regions
     ctx.set_timing(True)
     ctx.timings(reset=True)
+    ctx.eval_stats(reset=True)
     step(parts)
     torch.cuda.synchronize()
     kms, counts = ctx.timings(reset=True)
+    ev2, ev0, ev_flops = ctx.eval_stats(reset=True)
     ctx.set_timing(False)
     import ctypes
     from paper_2509_01180_b200 import _lib
@@ -292,34 +307,62 @@ def run_product(args):
     peaks, peak_kind = measured_peaks()
     steps = 1  # the instrumented step
     C, V = ctx.coeff_count, ctx.support
-    gemm_ms = kms["split_gemm"] / steps
+    gemm_ms = kms["expand"] / steps
     refine_ms = kms["refine"] / steps
     windows_per_step = counts["windows_expanded"] / steps
-    gemm_flops = 2.0 * C * V * windows_per_step  # algorithmic (FP32-equivalent) per step
     gemm_launches = max(1, counts["gemm_launches"] // steps)
-    peak_fp32eq = peaks["bf16_tflops"] / 3.0      # FP16 three-pass split: 3 tensor passes
     kernels = {k: round(v / steps, 3) for k, v in kms.items()}
     evals_per_step = sum(r["evaluations"] for r in res)
-    roof_gemm = {"kernel": "split3_gemm_kernel (tcgen05 kind::f16, 3-pass FP32 emulation)",
-                 "bound": "tensor", "achieved": gemm_flops / (gemm_ms / 1000.0) / 1e12 if gemm_ms > 0 else None,
-                 "peak": peak_fp32eq, "unit": "TFLOP/s",
-                 "peak_note": f"{peak_kind} dense bf16 {peaks['bf16_tflops']} / 3 passes",
-                 "per_launch_flops": gemm_flops / gemm_launches,
-                 "algorithmic": "2*C*V per window, C=%d V=%d" % (C, V), "traffic": None}
-    roof_gemm["frac"] = roof_gemm["achieved"] / peak_fp32eq if roof_gemm["achieved"] else None
-    dominant = "refine" if refine_ms > gemm_ms else "split_gemm"
+    fp32_peak, fp32_kind = fp32_simt_peak()
+    if args.expand == "gemm":
+        gemm_flops = 2.0 * C * V * windows_per_step  # algorithmic (FP32-equivalent) per step
+        peak_x = peaks["bf16_tflops"] / 3.0          # FP16 three-pass split: 3 tensor passes
+        roof_gemm = {"kernel": "split3_gemm_kernel (tcgen05 kind::f16, 3-pass FP32 emulation) + gather",
+                     "bound": "tensor", "peak": peak_x,
+                     "peak_note": f"{peak_kind} dense bf16 {peaks['bf16_tflops']} / 3 passes",
+                     "algorithmic": "2*C*V per window, C=%d V=%d" % (C, V)}
+    else:
+        S = ctx.n_r * ctx.n_theta * ctx.n_phi
+        ntri = (CFG["l_max"] + 1) * (CFG["l_max"] + 2) // 2
+        per_win = (16.0 * S + 4.0 * ctx.n_phi * ctx.n_r * ctx.n_theta * (CFG["l_max"] + 1)
+                   + 4.0 * ctx.n_r * ntri * ctx.n_theta + 2.0 * ctx.n_r * C)
+        gemm_flops = per_win * windows_per_step
+        peak_x = fp32_peak
+        roof_gemm = {"kernel": "expand_factored_kernel (trilinear samples, phi-DFT, theta + radial contractions)",
+                     "bound": "fp32_simt", "peak": peak_x, "peak_note": fp32_kind,
+                     "algorithmic": "per window 16 S taps + 4 n_phi n_r n_theta (L+1) + 4 n_r tri(L) n_theta + "
+                                    "2 n_r C, S=%d C=%d (%.2f MFLOP)" % (S, C, per_win / 1e6)}
+    roof_gemm.update({"achieved": gemm_flops / (gemm_ms / 1000.0) / 1e12 if gemm_ms > 0 else None,
+                      "unit": "TFLOP/s", "per_launch_flops": gemm_flops / gemm_launches, "traffic": None})
+    roof_gemm["frac"] = roof_gemm["achieved"] / peak_x if roof_gemm["achieved"] else None
+    # rotate-score-gradient evaluation kernels (FP32 SIMT register recursion)
+    eval_ms = kms["eval_order2"] + kms["eval_order0"]
+    roof_eval = {"kernel": "eval_kernel<2>+eval_kernel<0> (warp Wigner-d recursion, K jobs per warp)",
+                 "bound": "fp32_simt",
+                 "achieved": ev_flops / (eval_ms / 1000.0) / 1e12 if eval_ms > 0 else None,
+                 "peak": fp32_peak, "unit": "TFLOP/s", "peak_note": fp32_kind,
+                 "evaluations": {"order2": ev2, "order0": ev0},
+                 "per_launch_flops": None,
+                 "algorithmic": "per evaluation at band L: 6(o+1)N_xi recursion + (4(o+1)N_xi + "
+                                "6*nv*(2L+1)^2) per kernel (x2 with the wedge), N_xi=(L+1)(2L+1)(2L+3)/3",
+                 "traffic": None}
+    roof_eval["frac"] = roof_eval["achieved"] / fp32_peak if roof_eval["achieved"] else None
+    dominant = "refine" if refine_ms > gemm_ms else "expand"
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded Philox phantoms generated on device, BASELINE config 2)",
-        "config": config_block(P),
-        "roofline": roof_gemm,
+        "config": dict(config_block(P), expansion=args.expand),
+        "roofline": roof_eval if dominant == "refine" else roof_gemm,
+        "roofline_expansion": roof_gemm,
+        "roofline_refine_eval": roof_eval,
         "dominant_kernel": dominant,
         "kernel_ms_per_step": kernels,
         "kernel_ms_note": "CUDA events on the context stream, one instrumented step outside the timed region",
-        "refine": {"ms_per_step": refine_ms, "evaluations_per_step": evals_per_step,
-                   "note": "FP32 SIMT register recursion; see DESIGN.md for its roofline"},
+        "refine": {"ms_per_step": refine_ms, "eval_kernels_ms_per_step": eval_ms,
+                   "evaluations_per_step": evals_per_step,
+                   "note": "evaluations_per_step counts the seed grid too (align() counters)"},
         "e2e": {"value": P * world / (e2e_ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
         "gpu_launches": counts_timed["launches"],

@@ -50,6 +50,11 @@ int bm_context_create(int device, int n, int l_max, double lambda_cut, bm_contex
 int bm_context_destroy(bm_context* ctx);
 /* info[0..9]: n, l_max, coeff_count, support_voxels, m_pad, k_pad, n_r, n_theta, n_phi, pair_count */
 int bm_context_info(const bm_context* ctx, long long* info);
+/* Expansion algorithm of the context: 0 = factored (trilinear samples, phi-DFT,
+ * theta and radial contractions per window; default), 1 = dense pulled-back
+ * operator on the tensor cores (gather + bm_split3_gemm; the operator is built
+ * on first use).  Both follow expand() (src/basis.cpp:254-328). */
+int bm_context_set_expand_mode(bm_context* ctx, int mode);
 /* lambda_cut actually used by the context */
 double bm_context_lambda_cut(const bm_context* ctx);
 /* radial roots / norms of degree l (BasisSpec::root/norm, basis.hpp:40-41); returns count k_l */
@@ -153,13 +158,18 @@ int bm_average_accumulate(bm_context* ctx, const float* particles, int count,
                           const bm_align_result* results, double* sum, void* stream);
 
 /* Kernel timing evidence: with timing on, CUDA events on the context stream
- * bracket every launch of this library.  out_ms[0..9]: gather, split GEMM,
- * seed, refine, wedge filter, misc, refine by band position 0, 1, 2, 3+
- * (milliseconds, accumulated since reset);
+ * bracket every launch of this library.  out_ms[0..11]: gather, split GEMM,
+ * seed, refine, wedge filter, misc, refine by band position 0, 1, 2, 3+, the
+ * order-2 and order-0 evaluation launches inside refine (milliseconds,
+ * accumulated since reset);
  * out_counts[0..3]: kernels launched, windows expanded, GEMM launches,
  * refine launches.  reset != 0 clears after reading. */
 int bm_context_set_timing(bm_context* ctx, int on);
 int bm_context_timings(bm_context* ctx, double* out_ms, long long* out_counts, int reset);
+/* Rotate-score-gradient evaluations run by the refinement since the last reset:
+ * evals[0] order 2 (value, gradient, Hessian), evals[1] order 0 (value), and
+ * their algorithmic FLOPs (DESIGN.md §3 K5 accounting).  Always counted. */
+int bm_context_eval_stats(bm_context* ctx, long long* evals, double* flops, int reset);
 
 /* ------------------------------------------------------------------ synthetic inputs
  * Seeded generator on the device (BASELINE.json configs; particle pipeline of

@@ -103,6 +103,10 @@ def _declare(L: C.CDLL) -> None:
     L.bm_context_set_timing.restype = I
     L.bm_context_timings.argtypes = [P, P, P, I]
     L.bm_context_timings.restype = I
+    L.bm_context_set_expand_mode.argtypes = [P, I]
+    L.bm_context_set_expand_mode.restype = I
+    L.bm_context_eval_stats.argtypes = [P, P, P, I]
+    L.bm_context_eval_stats.restype = I
     L.bm_make_template.argtypes = [I, I, I, C.c_ulonglong, P, P]
     L.bm_make_template.restype = I
     L.bm_make_particles.argtypes = [I, P, I, I, C.c_ulonglong, I, D, D, P, P, P, P]

@@ -94,11 +94,14 @@ class Context:
         _lib.check(L.bm_context_create(device, n, l_max, lambda_cut, C.byref(h)), "build_spec")
         self._h = h
         self.device = device
+        self._refresh_info()
+        self.lambda_cut = L.bm_context_lambda_cut(self._h)
+
+    def _refresh_info(self):
         info = (C.c_longlong * 10)()
-        L.bm_context_info(self._h, info)
+        _lib.lib().bm_context_info(self._h, info)
         (self.n, self.l_max, self.coeff_count, self.support, self.m_pad, self.k_pad, self.n_r,
          self.n_theta, self.n_phi, self.pair_count) = (int(v) for v in info)
-        self.lambda_cut = L.bm_context_lambda_cut(self._h)
 
     def close(self):
         if getattr(self, "_h", None):
@@ -246,12 +249,25 @@ class Context:
     def set_timing(self, on: bool = True):
         _lib.check(_lib.lib().bm_context_set_timing(self._h, 1 if on else 0), "set_timing")
 
+    def set_expand_mode(self, mode: str):
+        """'factored' (default) or 'gemm' (dense operator on the tensor cores)."""
+        _lib.check(_lib.lib().bm_context_set_expand_mode(self._h, {"factored": 0, "gemm": 1}[mode]),
+                   "set_expand_mode")
+        self._refresh_info()
+
+    def eval_stats(self, reset: bool = False):
+        """(order-2 evaluations, order-0 evaluations, algorithmic FLOPs) of the refinement."""
+        ev = (C.c_longlong * 2)()
+        fl = C.c_double()
+        _lib.check(_lib.lib().bm_context_eval_stats(self._h, ev, C.byref(fl), 1 if reset else 0), "eval_stats")
+        return ev[0], ev[1], fl.value
+
     def timings(self, reset: bool = False):
-        ms = (C.c_double * 10)()
+        ms = (C.c_double * 12)()
         cnt = (C.c_longlong * 4)()
         _lib.check(_lib.lib().bm_context_timings(self._h, ms, cnt, 1 if reset else 0), "timings")
-        names = ("gather", "split_gemm", "seed", "refine", "wedge", "misc", "refine_band0",
-                 "refine_band1", "refine_band2", "refine_band3+")
+        names = ("gather", "expand", "seed", "refine", "wedge", "misc", "refine_band0",
+                 "refine_band1", "refine_band2", "refine_band3+", "eval_order2", "eval_order0")
         return (dict(zip(names, ms[:])),
                 dict(launches=cnt[0], windows_expanded=cnt[1], gemm_launches=cnt[2],
                      refine_launches=cnt[3]))

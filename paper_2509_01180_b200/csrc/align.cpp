@@ -312,6 +312,7 @@ void Context::refine_windows(int nw, int maxc, const AlignConfig& cfg, const Qua
                 int* lt0 = a.listc + slots;
                 int* lt1 = lt0 + slots;
                 a.counts = d_counts;
+                a.eval_stats = eval_stats();
                 ck(cudaMemsetAsync(d_pool, 0, sizeof(int), stream), "pool");
                 launch_band_begin(a, stream);
                 ++timer.launches;
@@ -332,7 +333,9 @@ void Context::refine_windows(int nw, int maxc, const AlignConfig& cfg, const Qua
                         launch_compose(a, a.compose_smem ? nc : std::min(nc, 4096), stream);
                         ++timer.launches;
                     }
+                    cudaEvent_t e2 = timer.begin(stream);
                     launch_eval(a, 2, a.list2, d_counts + CNT_L2, n2, stream);
+                    timer.end(K_EVAL2, e2, stream);
                     launch_step(a, lt0, d_counts + CNT_T0, n2, stream);
                     timer.launches += 2;
                     for (int r = 0; r < 3; ++r) {
@@ -340,7 +343,9 @@ void Context::refine_windows(int nw, int maxc, const AlignConfig& cfg, const Qua
                         int* dst = (r & 1) ? lt0 : lt1;
                         int* csrc = d_counts + ((r & 1) ? CNT_T1 : CNT_T0);
                         int* cdst = d_counts + ((r & 1) ? CNT_T0 : CNT_T1);
+                        cudaEvent_t e0 = timer.begin(stream);
                         launch_eval(a, 0, src, csrc, n2, stream);
+                        timer.end(K_EVAL0, e0, stream);
                         ck(cudaMemsetAsync(cdst, 0, sizeof(int), stream), "retry count");
                         launch_accept(a, src, csrc, dst, cdst, n2, stream);
                         timer.launches += 2;
@@ -350,7 +355,9 @@ void Context::refine_windows(int nw, int maxc, const AlignConfig& cfg, const Qua
                     // final unanchored score at the top band (optimize.cpp:349-352)
                     ck(cudaMemsetAsync(d_counts, 0, sizeof(int), stream), "final count");
                     launch_final_prep(a, stream);
+                    cudaEvent_t ef = timer.begin(stream);
                     launch_eval(a, 0, a.list2, d_counts + CNT_L2, (int)slots, stream);
+                    timer.end(K_EVAL0, ef, stream);
                     launch_final_score(a, (int)slots, stream);
                     timer.launches += 3;
                 }
@@ -419,6 +426,11 @@ std::vector<WindowOutcome> Context::run_windows(const float* vols, int n_vol, co
     sa.max_cand = maxc;
     sa.cand = cand_.as<CandState>();
     sa.cand_count = cand_count_.as<int>();
+    if (seed_needs_scratch(sa)) {
+        sa.scratch_windows = 4096;
+        seed_scratch_.reserve(sizeof(double2) * (size_t)sa.scratch_windows * sa.nxi);
+        sa.xi_scratch = seed_scratch_.as<double2>();
+    }
     cudaEvent_t s0 = timer.begin(stream);
     if (launch_seed(sa, nw, stream) != 0) throw std::runtime_error("seed kernel launch failed");
     ++timer.launches;
@@ -517,6 +529,26 @@ std::vector<ParticleResult> Context::align_batch(const float* particles, int cou
         r.windows = nwin[p];
     }
     return out;
+}
+
+void Context::read_eval_stats(long long* evals, double* flops, bool reset) {
+    std::vector<unsigned long long> h(kEvalStats, 0ull);
+    ck(cudaMemcpyAsync(h.data(), eval_stats(), sizeof(unsigned long long) * kEvalStats, cudaMemcpyDeviceToHost,
+                       stream),
+       "eval stats");
+    ck(cudaStreamSynchronize(stream), "eval stats");
+    long long e2 = 0, e0 = 0;
+    double fl = 0.0;
+    for (int L = 0; L <= kMaxL; ++L)
+        for (int o = 0; o < 2; ++o)
+            for (int w = 0; w < 2; ++w) {
+                const unsigned long long c = h[((size_t)L * 2 + o) * 2 + w];
+                (o ? e2 : e0) += (long long)c;
+                fl += (double)c * eval_flops(L, o ? 2 : 0, w != 0);
+            }
+    if (evals) evals[0] = e2, evals[1] = e0;
+    if (flops) *flops = fl;
+    if (reset) ck(cudaMemsetAsync(eval_stats(), 0, sizeof(unsigned long long) * kEvalStats, stream), "eval stats");
 }
 
 }  // namespace bmb

@@ -270,25 +270,10 @@ Operator build_operator(const Basis& b, int n) {
     op.support = (int)op.voxels.size();
 
     // 2. separable factor tables
-    const double wphi = 2.0 * kPi / np;
-    std::vector<std::vector<double>> radial(L + 1);  // [l][(k-1)*nr + i]
-    for (int l = 0; l <= L; ++l)
-        for (int k = 0; k < b.radial_count(l); ++k)
-            for (int i = 0; i < nr; ++i)
-                radial[l].push_back(b.norms[l][k] * sph_jl(l, b.roots[l][k] * b.r[i]) * b.r[i] *
-                                    b.r[i] * b.wr[i] * wphi);
-    std::vector<double> ptab(tri_count(L) * nt), tab(tri_count(L));
-    for (int t = 0; t < nt; ++t) {
-        legendre(L, b.u[t], tab.data());
-        for (size_t q = 0; q < tab.size(); ++q) ptab[q * nt + t] = tab[q] * b.wu[t];
-    }
-    std::vector<double> cs((size_t)(L + 1) * np), sn((size_t)(L + 1) * np);
-    for (int m = 0; m <= L; ++m)
-        for (int p = 0; p < np; ++p) {
-            const long long a = ((long long)m * p) % np;  // exact argument reduction
-            cs[(size_t)m * np + p] = std::cos(2.0 * kPi * a / np);
-            sn[(size_t)m * np + p] = -std::sin(2.0 * kPi * a / np);
-        }
+    const FactorTables ft = build_factor_tables(b);
+    const std::vector<double>& ptab = ft.ptab;
+    const std::vector<double>& cs = ft.cs;
+    const std::vector<double>& sn = ft.sn;
 
     // 3. columns of E, 32 voxels per task; pass 0 finds the row maxima (power-of-two
     //    row scales), pass 1 recomputes and writes the FP16 hi/lo split
@@ -314,7 +299,7 @@ Operator build_operator(const Basis& b, int n) {
                     const double re = pt * cs[(size_t)m * np + p];
                     const double im = pt * sn[(size_t)m * np + p];
                     for (int k = 1; k <= nk; ++k) {
-                        const double rad = radial[l][(size_t)(k - 1) * nr + i];
+                        const double rad = ft.radial[(size_t)(ft.pair_off[l] + k - 1) * nr + i];
                         col[b.row(l, k, m, 0)] += rad * re;
                         if (m > 0) col[b.row(l, k, m, 1)] += rad * im;
                     }
@@ -357,6 +342,70 @@ Operator build_operator(const Basis& b, int n) {
                 op.row_scale[r] = rmax[r] > 0.0 ? (float)std::ldexp(1.0, (int)std::ceil(std::log2(rmax[r]))) : 1.0f;
     }
     return op;
+}
+
+FactorTables build_factor_tables(const Basis& b) {
+    const int L = b.l_max, nr = b.n_r, nt = b.n_theta, np = b.n_phi;
+    FactorTables f;
+    f.pair_off.resize(L + 1);
+    for (int l = 0; l <= L; ++l) {
+        f.pair_off[l] = f.pairs;
+        f.pairs += b.radial_count(l);
+    }
+    const double wphi = 2.0 * kPi / np;
+    f.radial.resize((size_t)f.pairs * nr);
+    for (int l = 0; l <= L; ++l)
+        for (int k = 0; k < b.radial_count(l); ++k)
+            for (int i = 0; i < nr; ++i)
+                f.radial[(size_t)(f.pair_off[l] + k) * nr + i] =
+                    b.norms[l][k] * sph_jl(l, b.roots[l][k] * b.r[i]) * b.r[i] * b.r[i] * b.wr[i] * wphi;
+    f.ptab.resize(tri_count(L) * nt);
+    std::vector<double> tab(tri_count(L));
+    for (int t = 0; t < nt; ++t) {
+        legendre(L, b.u[t], tab.data());
+        for (size_t q = 0; q < tab.size(); ++q) f.ptab[q * nt + t] = tab[q] * b.wu[t];
+    }
+    f.cs.resize((size_t)(L + 1) * np);
+    f.sn.resize((size_t)(L + 1) * np);
+    for (int m = 0; m <= L; ++m)
+        for (int p = 0; p < np; ++p) {
+            const long long a = ((long long)m * p) % np;  // exact argument reduction
+            f.cs[(size_t)m * np + p] = std::cos(2.0 * kPi * a / np);
+            f.sn[(size_t)m * np + p] = -std::sin(2.0 * kPi * a / np);
+        }
+    return f;
+}
+
+int support_count(const Basis& b, int n) {
+    std::vector<char> hit((size_t)n * n * n, 0);
+    for (int i = 0; i < b.n_r; ++i)
+        for (int t = 0; t < b.n_theta; ++t) {
+            const double st = std::sqrt(std::max(0.0, 1.0 - b.u[t] * b.u[t]));
+            const double rs = b.r[i] * st, z = b.r[i] * b.u[t];
+            for (int p = 0; p < b.n_phi; ++p) {
+                const double phi = 2.0 * kPi * p / b.n_phi;
+                const double g[3] = {rs * std::cos(phi) * (n / 2.0) + n / 2.0, rs * std::sin(phi) * (n / 2.0) + n / 2.0,
+                                     z * (n / 2.0) + n / 2.0};
+                int c0[3];
+                double fr[3];
+                for (int a = 0; a < 3; ++a) {
+                    c0[a] = (int)std::floor(g[a]);
+                    fr[a] = g[a] - c0[a];
+                }
+                for (int dz = 0; dz < 2; ++dz)
+                    for (int dy = 0; dy < 2; ++dy)
+                        for (int dx = 0; dx < 2; ++dx) {
+                            const int xx = c0[0] + dx, yy = c0[1] + dy, zz = c0[2] + dz;
+                            if (xx < 0 || xx >= n || yy < 0 || yy >= n || zz < 0 || zz >= n) continue;
+                            const double w = (dx ? fr[0] : 1.0 - fr[0]) * (dy ? fr[1] : 1.0 - fr[1]) *
+                                             (dz ? fr[2] : 1.0 - fr[2]);
+                            if (w != 0.0) hit[((size_t)zz * n + yy) * n + xx] = 1;
+                        }
+            }
+        }
+    int c = 0;
+    for (char h : hit) c += h;
+    return c;
 }
 
 uint16_t half_bits(double x) {

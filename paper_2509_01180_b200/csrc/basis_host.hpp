@@ -56,6 +56,19 @@ struct Operator {
     std::vector<uint16_t> hi, lo;  // m_pad x k_pad, __half bit patterns
 };
 Operator build_operator(const Basis& b, int n);
+
+// Separable factors of expand() stages 2-4 (src/basis.cpp:254-328), FP64:
+//   radial[(pair_off[l] + k-1) * n_r + i] = c_lk j_l(lambda_lk r_i) r_i^2 w_i 2pi/n_phi
+//   ptab[tri(l,m) * n_theta + t]        = Pbar_l^m(u_t) w_t
+//   cs/sn[m * n_phi + p]                 = cos / -sin(2 pi (m p mod n_phi) / n_phi)
+struct FactorTables {
+    std::vector<double> radial, ptab, cs, sn;
+    std::vector<int> pair_off;  // [l_max + 1]
+    int pairs = 0;
+};
+FactorTables build_factor_tables(const Basis& b);
+// voxels whose trilinear footprint reaches a quadrature sample (the support V)
+int support_count(const Basis& b, int n);
 uint16_t half_bits(double x);      // round-to-nearest-even, subnormals kept
 double half_value(uint16_t h);
 

@@ -361,6 +361,27 @@ int bm_context_timings(bm_context* ctx, double* out_ms, long long* out_counts, i
     return BM_OK;
 }
 
+int bm_context_set_expand_mode(bm_context* ctx, int mode) {
+    return guarded("bm_context_set_expand_mode", [&] {
+        if (!ctx) return (int)BM_ERR_STATE;
+        if (mode != 0 && mode != 1) throw std::invalid_argument("expand mode must be 0 (factored) or 1 (gemm)");
+        auto& c = *ctx->impl;
+        cudaSetDevice(c.device);
+        c.expand_mode = mode;
+        if (mode == 1) c.ensure_operator();
+        return (int)BM_OK;
+    });
+}
+
+int bm_context_eval_stats(bm_context* ctx, long long* evals, double* flops, int reset) {
+    return guarded("bm_context_eval_stats", [&] {
+        if (!ctx) return (int)BM_ERR_STATE;
+        cudaSetDevice(ctx->impl->device);
+        ctx->impl->read_eval_stats(evals, flops, reset != 0);
+        return (int)BM_OK;
+    });
+}
+
 int bm_make_template(int device, int n, int blobs, unsigned long long seed, float* out, void* stream) {
     return guarded("bm_make_template", [&] {
         if (n < 8 || n % 2 || blobs < 1 || !out) throw std::invalid_argument("bad template arguments");

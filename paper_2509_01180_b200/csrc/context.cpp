@@ -22,32 +22,23 @@ Context::Context(int dev, int n_, int l_max, double lambda_cut) : device(dev), n
     BMB_CUDA(cudaSetDevice(device));
     BMB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     basis = host::make_basis(l_max, lambda_cut);
-    host::Operator op;
-    if (n_ > 0) {
-        op = host::build_operator(basis, n);
-    } else {
-        op.rows = basis.coeffs;
-        op.m_pad = (op.rows + 127) / 128 * 128;
-    }
-    voxels_host = op.voxels;
-
+    if (const char* e = std::getenv("BMB_EXPAND")) expand_mode = std::string(e) == "gemm" ? 1 : 0;
     geo.n = n;
     geo.l_max = l_max;
-    geo.coeffs = op.rows;
-    geo.support = op.support;
-    geo.m_pad = op.m_pad;
-    geo.k_pad = op.k_pad;
-
-    upload(E_hi, op.hi, stream);
-    upload(E_lo, op.lo, stream);
-    upload(row_scale, op.row_scale, stream);
-    upload(voxels, op.voxels, stream);
+    geo.coeffs = basis.coeffs;
+    geo.m_pad = (basis.coeffs + 127) / 128 * 128;
+    geo.support = n_ > 0 ? host::support_count(basis, n) : 0;
+    geo.k_pad = 0;
+    if (n_ > 0) {
+        build_factored_tables();
+        if (expand_mode == 1) ensure_operator();
+    }
     std::vector<int> rc(l_max + 1);
     for (int l = 0; l <= l_max; ++l) rc[l] = basis.radial_count(l);
     upload(block_off, basis.block_off, stream);
     upload(radial_count, rc, stream);
-    std::vector<float> rw(op.rows);
-    std::vector<int4> lkm(op.rows);
+    std::vector<float> rw(geo.coeffs);
+    std::vector<int4> lkm(geo.coeffs);
     for (int l = 0; l <= l_max; ++l)
         for (int k = 1; k <= basis.radial_count(l); ++k)
             for (int m = 0; m <= l; ++m)
@@ -65,6 +56,78 @@ Context::Context(int dev, int n_, int l_max, double lambda_cut) : device(dev), n
     BMB_CUDA(cudaStreamSynchronize(stream));
 }
 
+// dense pulled-back operator of the GEMM expansion path (built on first use)
+void Context::ensure_operator() {
+    if (operator_ready || n == 0) return;
+    host::Operator op = host::build_operator(basis, n);
+    if (op.m_pad != geo.m_pad || op.rows != geo.coeffs) throw std::logic_error("operator layout mismatch");
+    voxels_host = op.voxels;
+    geo.support = op.support;
+    geo.k_pad = op.k_pad;
+    upload(E_hi, op.hi, stream);
+    upload(E_lo, op.lo, stream);
+    upload(row_scale, op.row_scale, stream);
+    upload(voxels, op.voxels, stream);
+    BMB_CUDA(cudaStreamSynchronize(stream));
+    operator_ready = true;
+}
+
+void Context::build_factored_tables() {
+    const host::FactorTables ft = host::build_factor_tables(basis);
+    const int L = basis.l_max, nr = basis.n_r, nt = basis.n_theta, np = basis.n_phi;
+    std::vector<double> st(nt), cphi(np), sphi(np);
+    for (int t = 0; t < nt; ++t) st[t] = std::sqrt(std::max(0.0, 1.0 - basis.u[t] * basis.u[t]));
+    for (int p = 0; p < np; ++p) {
+        const double phi = 2.0 * host::kPi * p / np;  // build_operator / expand sample points
+        cphi[p] = std::cos(phi);
+        sphi[p] = std::sin(phi);
+    }
+    const int half = np / 2;
+    std::vector<float2> tw((size_t)(half + 1) * (L + 1));
+    for (int p = 0; p <= half; ++p)
+        for (int m = 0; m <= L; ++m)
+            tw[(size_t)p * (L + 1) + m] = make_float2((float)ft.cs[(size_t)m * np + p], (float)ft.sn[(size_t)m * np + p]);
+    const int ntri = (int)host::tri_count(L);
+    std::vector<float> ptab(ft.ptab.begin(), ft.ptab.end());
+    std::vector<int2> tlm(ntri);
+    for (int l = 0; l <= L; ++l)
+        for (int m = 0; m <= l; ++m) tlm[host::tri(l, m)] = make_int2(l, m);
+    std::vector<float> radial(ft.radial.begin(), ft.radial.end());
+    std::vector<int4> rowmap(geo.coeffs);
+    for (int l = 0; l <= L; ++l)
+        for (int k = 1; k <= basis.radial_count(l); ++k)
+            for (int m = 0; m <= l; ++m)
+                for (int part = 0; part < (m ? 2 : 1); ++part)
+                    rowmap[basis.row(l, k, m, part)] = make_int4((int)host::tri(l, m), part, ft.pair_off[l] + k - 1, 0);
+    upload(fx_r, basis.r, stream);
+    upload(fx_st, st, stream);
+    upload(fx_u, basis.u, stream);
+    upload(fx_cphi, cphi, stream);
+    upload(fx_sphi, sphi, stream);
+    upload(fx_tw, tw, stream);
+    upload(fx_ptab, ptab, stream);
+    upload(fx_trilm, tlm, stream);
+    upload(fx_radial, radial, stream);
+    upload(fx_rowmap, rowmap, stream);
+    fx.n = n;
+    fx.L = L;
+    fx.nr = nr;
+    fx.nt = nt;
+    fx.np = np;
+    fx.coeffs = geo.coeffs;
+    fx.ntri = ntri;
+    fx.r = fx_r.as<double>();
+    fx.st = fx_st.as<double>();
+    fx.u = fx_u.as<double>();
+    fx.cphi = fx_cphi.as<double>();
+    fx.sphi = fx_sphi.as<double>();
+    fx.tw = fx_tw.as<float2>();
+    fx.ptab = fx_ptab.as<float>();
+    fx.tri_lm = fx_trilm.as<int2>();
+    fx.radial = fx_radial.as<float>();
+    fx.rowmap = fx_rowmap.as<int4>();
+}
+
 Context::~Context() {
     cudaSetDevice(device);
     wedge.reset();
@@ -78,7 +141,22 @@ void Context::expand_windows(const float* vols, long long vol_stride, int n_vol,
                              const std::vector<int>& wvol, const std::vector<int>& wshift) {
     const int nw = (int)wvol.size();
     if (nw == 0) return;
-    if (geo.support == 0) throw std::invalid_argument("expand: context has no operator (n = 0)");
+    if (n == 0) throw std::invalid_argument("expand: context has no operator (n = 0)");
+    if (expand_mode == 0) {
+        upload(win_vol, wvol, stream);
+        upload(win_shift, wshift, stream);
+        coef.reserve(sizeof(float) * (size_t)nw * geo.m_pad);
+        cudaEvent_t f0 = timer.begin(stream);
+        if (launch_expand_factored(fx, vols, vol_stride, win_vol.as<int>(), win_shift.as<int>(), nw, coef.as<float>(),
+                                   geo.m_pad, stream) != 0)
+            throw std::runtime_error("factored expansion launch failed");
+        ++timer.launches;
+        ++timer.gemm_launches;
+        timer.windows_expanded += nw;
+        timer.end(K_GEMM, f0, stream);
+        return;
+    }
+    ensure_operator();
     const int bn = gemm_block_n;
     const long long chunk = std::min<long long>(nw, max_chunk_windows);
     const long long n_pad = (chunk + bn - 1) / bn * bn;

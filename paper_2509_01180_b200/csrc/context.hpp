@@ -17,6 +17,7 @@
 
 #include "basis_host.hpp"
 #include "bmb_internal.hpp"
+#include "expand_factored.hpp"
 #include "kernels.cuh"
 #include "rotation.cuh"
 
@@ -100,7 +101,7 @@ struct ParticleResult {
 };
 
 // Per-kernel-class CUDA-event timing on the context stream (bench evidence).
-enum KClass { K_GATHER = 0, K_GEMM, K_SEED, K_REFINE, K_WEDGE, K_MISC, K_REFINE_B0, K_REFINE_B1, K_REFINE_B2, K_REFINE_B3, K_COUNT };
+enum KClass { K_GATHER = 0, K_GEMM, K_SEED, K_REFINE, K_WEDGE, K_MISC, K_REFINE_B0, K_REFINE_B1, K_REFINE_B2, K_REFINE_B3, K_EVAL2, K_EVAL0, K_COUNT };
 struct KernelTimer {
     bool on = false;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
@@ -165,6 +166,12 @@ public:
     void expand_windows(const float* vols, long long vol_stride, int n_vol,
                         const std::vector<int>& wvol, const std::vector<int>& wshift);
 
+    int expand_mode = 0;          // 0: factored expansion (K2f), 1: dense operator GEMM (K1 + K2)
+    bool operator_ready = false;
+    void ensure_operator();
+    void build_factored_tables();
+    FactoredTables fx;
+    DevBuf fx_r, fx_st, fx_u, fx_cphi, fx_sphi, fx_tw, fx_ptab, fx_trilm, fx_radial, fx_rowmap;
     int gemm_block_n = 128;
     int gemm_kchunk = 4;
     long long max_chunk_windows = 8192;  // windows expanded per GEMM chunk
@@ -194,6 +201,18 @@ public:
     DevBuf work_f, work_xi, filtered;
 
     bool debug_iters_ = std::getenv("BMB_DEBUG_ITERS") != nullptr;
+    DevBuf seed_scratch_;                   // seed xi when it does not fit in shared memory
+    DevBuf eval_stats_;                     // [kMaxL+1][order 0/2][wedge 0/1] evaluation counts
+    static constexpr size_t kEvalStats = (size_t)(kMaxL + 1) * 4;
+    unsigned long long* eval_stats() {
+        if (!eval_stats_.p) {
+            eval_stats_.reserve(sizeof(unsigned long long) * kEvalStats);
+            cudaMemsetAsync(eval_stats_.p, 0, sizeof(unsigned long long) * kEvalStats, stream);
+        }
+        return eval_stats_.as<unsigned long long>();
+    }
+    // evaluations (order 2, order 0) and their algorithmic FLOPs since the last reset
+    void read_eval_stats(long long* evals, double* flops, bool reset);
     double pool_fraction_ = 0.5;           // anchored-chart pool slots per candidate
     size_t pool_budget_ = 8ull << 30;       // bytes for window kernels + pool per chunk
 

@@ -1,0 +1,179 @@
+// Factored ball-harmonic expansion (kernel K2f): the four
+// stages of expand() (src/basis.cpp:254-328) run per shift window on the
+// device, radius by radius, instead of the dense pulled-back operator:
+//   1. trilinear samples f(r_i, theta_t, phi_p) of the shifted window
+//      (sample_trilinear + shift_volume, src/volume.cpp:19-67), FP64 taps;
+//   2. unnormalized phi-DFT of every theta ring (dft_r2c_rows,
+//      src/detail/fftw_util.cpp:16-28), folded over p <-> n_phi - p;
+//   3. theta contraction with Pbar_l^m(u_t) w_t, folded over the GL symmetry
+//      u_{n-1-t} = -u_t (Pbar_l^m(-u) = (-1)^(l+m) Pbar_l^m(u));
+//   4. radial contraction c_lk j_l(lambda r_i) r_i^2 w_i 2pi/n_phi accumulated
+//      into the real-packed coefficient rows.
+// One CTA per window; stages 2-4 use FP32 tables with FP32 accumulation.
+// Algorithmic work per window (DESIGN.md §3 K2f): 8 n_r n_theta n_phi taps +
+// ~2 n_r n_theta (L+1) n_phi + 2 n_r tri(L) n_theta + n_r C FLOP — about
+// 100x fewer than the dense 2 C V of the pulled-back operator.
+#include "expand_factored.hpp"
+
+namespace bmb {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+struct Smem {
+    size_t cphi, sphi, st, u, tw, samp, F, G, acc, total;
+};
+
+__host__ __device__ inline size_t al16(size_t x) { return (x + 15) / 16 * 16; }
+
+__host__ __device__ inline Smem smem_plan(const FactoredTables& T) {
+    Smem s;
+    const int L = T.L, half = T.np / 2;
+    size_t o = 0;
+    s.cphi = o;
+    o = al16(o + sizeof(double) * T.np);
+    s.sphi = o;
+    o = al16(o + sizeof(double) * T.np);
+    s.st = o;
+    o = al16(o + sizeof(double) * T.nt);
+    s.u = o;
+    o = al16(o + sizeof(double) * T.nt);
+    s.tw = o;
+    o = al16(o + sizeof(float2) * (size_t)(half + 1) * (L + 1));
+    s.samp = o;
+    o = al16(o + sizeof(float) * (size_t)T.nt * T.np);
+    s.F = o;
+    o = al16(o + sizeof(float2) * (size_t)T.nt * (L + 1));
+    s.G = o;
+    o = al16(o + sizeof(float2) * (size_t)T.ntri);
+    s.acc = o;
+    o = al16(o + sizeof(float) * (size_t)T.coeffs);
+    s.total = o;
+    return s;
+}
+
+__global__ void __launch_bounds__(kThreads) expand_factored_kernel(FactoredTables T, const float* __restrict__ vols,
+                                                                    long long vol_stride, const int* __restrict__ win_vol,
+                                                                    const int* __restrict__ win_shift, float* __restrict__ out,
+                                                                    int ldo) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const Smem P = smem_plan(T);
+    double* cphi = reinterpret_cast<double*>(sm + P.cphi);
+    double* sphi = reinterpret_cast<double*>(sm + P.sphi);
+    double* st = reinterpret_cast<double*>(sm + P.st);
+    double* uu = reinterpret_cast<double*>(sm + P.u);
+    float2* tw = reinterpret_cast<float2*>(sm + P.tw);
+    float* samp = reinterpret_cast<float*>(sm + P.samp);
+    float2* F = reinterpret_cast<float2*>(sm + P.F);
+    float2* G = reinterpret_cast<float2*>(sm + P.G);
+    float* acc = reinterpret_cast<float*>(sm + P.acc);
+
+    const int w = blockIdx.x, tid = threadIdx.x;
+    const int n = T.n, L = T.L, nt = T.nt, np = T.np, half = np / 2, nl = L + 1;
+    const float* __restrict__ v = vols + (long long)win_vol[w] * vol_stride;
+    const int sx = win_shift[3 * w], sy = win_shift[3 * w + 1], sz = win_shift[3 * w + 2];
+    for (int i = tid; i < np; i += kThreads) {
+        cphi[i] = T.cphi[i];
+        sphi[i] = T.sphi[i];
+    }
+    for (int i = tid; i < nt; i += kThreads) {
+        st[i] = T.st[i];
+        uu[i] = T.u[i];
+    }
+    for (int i = tid; i < (half + 1) * nl; i += kThreads) tw[i] = T.tw[i];
+    for (int i = tid; i < T.coeffs; i += kThreads) acc[i] = 0.0f;
+    const double h = 0.5 * n;
+    __syncthreads();
+
+    for (int ir = 0; ir < T.nr; ++ir) {
+        const double r = T.r[ir];
+        // 1. trilinear samples of the shifted window (zero outside the grid and
+        //    where the shifted source leaves it)
+        for (int s = tid; s < nt * np; s += kThreads) {
+            const int t = s / np, p = s - t * np;
+            const double rs = r * st[t];
+            const double gx = rs * cphi[p] * h + h, gy = rs * sphi[p] * h + h, gz = r * uu[t] * h + h;
+            const double fx0 = floor(gx), fy0 = floor(gy), fz0 = floor(gz);
+            const int x0 = (int)fx0, y0 = (int)fy0, z0 = (int)fz0;
+            const double fx = gx - fx0, fy = gy - fy0, fz = gz - fz0;
+            double val = 0.0;
+#pragma unroll
+            for (int dz = 0; dz < 2; ++dz) {
+                const int zz = z0 + dz, zs = zz + sz;
+                if ((unsigned)zz >= (unsigned)n || (unsigned)zs >= (unsigned)n) continue;
+                const double wz = dz ? fz : 1.0 - fz;
+#pragma unroll
+                for (int dy = 0; dy < 2; ++dy) {
+                    const int yy = y0 + dy, ys = yy + sy;
+                    if ((unsigned)yy >= (unsigned)n || (unsigned)ys >= (unsigned)n) continue;
+                    const double wy = dy ? fy : 1.0 - fy;
+                    const float* row = v + ((long long)zs * n + ys) * n;
+#pragma unroll
+                    for (int dx = 0; dx < 2; ++dx) {
+                        const int xx = x0 + dx, xs = xx + sx;
+                        if ((unsigned)xx >= (unsigned)n || (unsigned)xs >= (unsigned)n) continue;
+                        val += (dx ? fx : 1.0 - fx) * wy * wz * (double)__ldg(row + xs);
+                    }
+                }
+            }
+            samp[s] = (float)val;
+        }
+        __syncthreads();
+        // 2. phi-DFT: F[t][m] = sum_p f[t][p] e^{-2 pi i m p / n_phi}, folded
+        for (int o = tid; o < nt * nl; o += kThreads) {
+            const int t = o / nl, m = o - t * nl;
+            const float* f = samp + t * np;
+            float re = f[0] + ((m & 1) ? -f[half] : f[half]);
+            float im = 0.0f;
+            for (int p = 1; p < half; ++p) {
+                const float2 c = tw[p * nl + m];  // (cos, -sin)
+                re = fmaf(f[p] + f[np - p], c.x, re);
+                im = fmaf(f[p] - f[np - p], c.y, im);
+            }
+            F[o] = make_float2(re, im);
+        }
+        __syncthreads();
+        // 3. theta: G[l,m] = sum_t Pbar_l^m(u_t) w_t F[t][m], folded over t <-> nt-1-t
+        for (int q = tid; q < T.ntri; q += kThreads) {
+            const int2 lm = T.tri_lm[q];
+            const float sgn = ((lm.x + lm.y) & 1) ? -1.0f : 1.0f;
+            const float* pt = T.ptab + (size_t)q * nt;
+            float re = 0.0f, im = 0.0f;
+            for (int t = 0; t < nt / 2; ++t) {
+                const float2 a = F[t * nl + lm.y], b = F[(nt - 1 - t) * nl + lm.y];
+                const float wgt = __ldg(pt + t);
+                re = fmaf(wgt, fmaf(sgn, b.x, a.x), re);
+                im = fmaf(wgt, fmaf(sgn, b.y, a.y), im);
+            }
+            G[q] = make_float2(re, im);
+        }
+        __syncthreads();
+        // 4. radial: row (l,k,m,part) += radial[(l,k)][i] * G[l,m].part
+        for (int row = tid; row < T.coeffs; row += kThreads) {
+            const int4 rm = T.rowmap[row];
+            const float g = rm.y ? G[rm.x].y : G[rm.x].x;
+            acc[row] = fmaf(__ldg(T.radial + (size_t)rm.z * T.nr + ir), g, acc[row]);
+        }
+        // (the next radius only rewrites samp / F / G after further barriers)
+    }
+    __syncthreads();
+    float* o = out + (long long)w * ldo;
+    for (int row = tid; row < T.coeffs; row += kThreads) o[row] = acc[row];
+}
+
+}  // namespace
+
+size_t factored_smem_bytes(const FactoredTables& T) { return smem_plan(T).total; }
+
+int launch_expand_factored(const FactoredTables& T, const float* vols, long long vol_stride, const int* win_vol,
+                           const int* win_shift, int n_win, float* out, int ldo, cudaStream_t s) {
+    if (n_win <= 0) return 0;
+    const size_t smem = factored_smem_bytes(T);
+    if (smem > 220 * 1024) return 1;
+    cudaFuncSetAttribute(expand_factored_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    expand_factored_kernel<<<n_win, kThreads, smem, s>>>(T, vols, vol_stride, win_vol, win_shift, out, ldo);
+    return cudaGetLastError() == cudaSuccess ? 0 : 2;
+}
+
+}  // namespace bmb

@@ -25,6 +25,7 @@
 // (frequency marching) and relaunches the iteration until no candidate is
 // active.
 #include <cfloat>
+#include <cstdlib>
 
 #include "refine.cuh"
 #include "rotation.cuh"
@@ -33,7 +34,6 @@ namespace bmb {
 
 namespace {
 
-constexpr int kWarps = 8;
 constexpr double kPiD = 3.14159265358979323846;
 
 struct WarpScratch {
@@ -54,28 +54,51 @@ __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
 
 __host__ __device__ __forceinline__ int xi_off(int l) { return l * (2 * l - 1) * (2 * l + 1) / 3; }
 
-// Evaluate the correlation (and the wedge-power kernel when wx != null) at ZYZ
-// angles (alpha, beta, gamma), band T.L.  Warp-cooperative; results in ws.res.
-template <int ORDER>
-__device__ __noinline__ void warp_eval(const BandTables& T, const float2* xi, const float2* wx,
-                                       double alpha, double beta, double gamma, WarpScratch& ws) {
+// One evaluation job: correlation kernel, wedge-power kernel (null: no wedge)
+// and the ZYZ angles.
+struct EvalJob {
+    const float2* xi;
+    const float2* wx;
+    double a, b, g;
+};
+
+// products with explicit rounding so that every evaluation runs the identical
+// FP32 sequence whichever slot k of a K-way warp it occupies
+__device__ __forceinline__ float2 cmul_x(float2 a, float2 b) {
+    return make_float2(fmaf(a.x, b.x, -__fmul_rn(a.y, b.y)), fmaf(a.x, b.y, __fmul_rn(a.y, b.x)));
+}
+
+// Evaluate K jobs at band T.L that share their kernels (job[k].xi == job[0].xi,
+// job[k].wx == job[0].wx: rotations of one window, or of one particle in the
+// sweep) — the correlation and, when wx != null, the wedge-power kernel at the
+// same angles.  Warp-cooperative; results in ws[k].res.  Each table load (the
+// recursion coefficients and both kernels) feeds K recursion chains per lane.
+template <int ORDER, int K>
+__device__ __forceinline__ void warp_eval_k(const BandTables& T, const EvalJob (&job)[K], WarpScratch* ws) {
+    const float2* __restrict__ xi = job[0].xi;
+    const float2* __restrict__ wx = job[0].wx;
     const bool WEDGE = wx != nullptr;
     const int lane = threadIdx.x & 31;
     const int L = T.L;
     __syncwarp();
-    // four FP64 sincos on lanes 0..3 (beta/2, beta, alpha, gamma); the phases
-    // e^{-i m alpha}, e^{-i m gamma} are then binary powers of the bases
-    if (lane < 4) {
-        const double ang = lane == 0 ? 0.5 * beta : (lane == 1 ? beta : (lane == 2 ? alpha : gamma));
+    // four FP64 sincos per job on lanes 4k..4k+3 (beta/2, beta, alpha, gamma);
+    // the phases e^{-i m alpha}, e^{-i m gamma} are binary powers of the bases
+    if (lane < 4 * K) {
+        const int c = lane & 3;
+        double ang = 0.0;
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+            if ((lane >> 2) == k) ang = c == 0 ? 0.5 * job[k].b : (c == 1 ? job[k].b : (c == 2 ? job[k].a : job[k].g));
         double sn, co;
         sincos_d(ang, &sn, &co);
-        ws.cs_half[2 * lane] = co;
-        ws.cs_half[2 * lane + 1] = sn;
+        ws[lane >> 2].cs_half[2 * c] = co;
+        ws[lane >> 2].cs_half[2 * c + 1] = sn;
     }
     __syncwarp();
-    {
-        const double car = ws.cs_half[4], cai = -ws.cs_half[5];  // e^{-i alpha}
-        const double cgr = ws.cs_half[6], cgi = -ws.cs_half[7];  // e^{-i gamma}
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const double car = ws[k].cs_half[4], cai = -ws[k].cs_half[5];  // e^{-i alpha}
+        const double cgr = ws[k].cs_half[6], cgi = -ws[k].cs_half[7];  // e^{-i gamma}
         for (int m = lane; m <= L; m += 32) {
             double ar = 1.0, ai = 0.0, gr = 1.0, gi = 0.0;
             double br_ = car, bi_ = cai, hr = cgr, hi = cgi;
@@ -95,30 +118,38 @@ __device__ __noinline__ void warp_eval(const BandTables& T, const float2* xi, co
                 hi = 2.0 * hr * hi;
                 hr = u2;
             }
-            ws.ua[m] = make_float2((float)ar, (float)ai);
-            ws.ug[m] = make_float2((float)gr, (float)gi);
+            ws[k].ua[m] = make_float2((float)ar, (float)ai);
+            ws[k].ug[m] = make_float2((float)gr, (float)gi);
         }
-    }
-    const double ch = ws.cs_half[0], sh = ws.cs_half[1];
-    for (int j = lane; j <= 2 * L + 2; j += 32) {
-        double pc = 1.0, ps = 1.0, bc = ch, bs = sh;  // binary exponentiation
-        for (int e = j; e; e >>= 1) {
-            if (e & 1) {
-                pc *= bc;
-                ps *= bs;
+        const double ch = ws[k].cs_half[0], sh = ws[k].cs_half[1];
+        for (int j = lane; j <= 2 * L + 2; j += 32) {
+            double pc = 1.0, ps = 1.0, bc = ch, bs = sh;
+            for (int e = j; e; e >>= 1) {
+                if (e & 1) {
+                    pc *= bc;
+                    ps *= bs;
+                }
+                bc *= bc;
+                bs *= bs;
             }
-            bc *= bc;
-            bs *= bs;
+            ws[k].cp[j] = (float)pc;
+            ws[k].sp[j] = (float)ps;
         }
-        ws.cp[j] = (float)pc;
-        ws.sp[j] = (float)ps;
     }
     __syncwarp();
-    const float cb = (float)ws.cs_half[2], sb = (float)ws.cs_half[3];
-
-    float acc[10], accw[10];
+    float cb[K], sb[K];
 #pragma unroll
-    for (int i = 0; i < 10; ++i) acc[i] = accw[i] = 0.0f;
+    for (int k = 0; k < K; ++k) {
+        cb[k] = (float)ws[k].cs_half[2];
+        sb[k] = (float)ws[k].cs_half[3];
+    }
+
+    constexpr int NV = ORDER == 0 ? 1 : (ORDER == 1 ? 4 : 10);
+    float acc[K][NV], accw[K][NV];
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+        for (int i = 0; i < NV; ++i) acc[k][i] = accw[k][i] = 0.0f;
 
     for (int g = 0; g < T.n_groups; ++g) {
         const int item = g * 32 + lane;
@@ -129,147 +160,147 @@ __device__ __noinline__ void warp_eval(const BandTables& T, const float2* xi, co
         const int be = T.bexp[item];
         const int ea = be & 0xff, ep = be >> 8;
         const float bf = T.bfac[item];
-        // closed-form border at l0 (cs_power, steer.cpp:19-31)
-        float d = bf * ws.cp[ea] * ws.sp[ep];
-        float dp = 0.0f, dpp = 0.0f;
-        if (ORDER >= 1) {
-            const float tb = ep ? ep * ws.cp[ea + 1] * ws.sp[ep - 1] : 0.0f;
-            const float ta = ea ? ea * ws.cp[ea - 1] * ws.sp[ep + 1] : 0.0f;
-            dp = 0.5f * bf * (tb - ta);
-        }
-        if (ORDER >= 2) {
-            const float t2b = ep > 1 ? ep * (ep - 1.0f) * ws.cp[ea + 2] * ws.sp[ep - 2] : 0.0f;
-            const float t2a = ea > 1 ? ea * (ea - 1.0f) * ws.cp[ea - 2] * ws.sp[ep + 2] : 0.0f;
-            dpp = 0.25f * bf * (t2b + t2a - (2.0f * ea * ep + ea + ep) * ws.cp[ea] * ws.sp[ep]);
-        }
-        float d1 = 0.0f, dp1 = 0.0f, dpp1 = 0.0f;  // degree l-1 (none at the border)
+        float d[K], dp[K], dpp[K], d1[K], dp1[K], dpp1[K];
+        float2 A0[K], A1[K], A2[K], W0[K], W1[K], W2[K];
         const float2 x0 = xi[r0 * 32 + lane];
-        float2 A0 = make_float2(x0.x * d, x0.y * d), A1 = make_float2(x0.x * dp, x0.y * dp),
-               A2 = make_float2(x0.x * dpp, x0.y * dpp);
-        float2 W0 = make_float2(0.f, 0.f), W1 = W0, W2 = W0;
-        if (WEDGE) {
-            const float2 w0 = wx[r0 * 32 + lane];
-            W0 = make_float2(w0.x * d, w0.y * d);
-            W1 = make_float2(w0.x * dp, w0.y * dp);
-            W2 = make_float2(w0.x * dpp, w0.y * dpp);
+        const float2 w0 = WEDGE ? wx[r0 * 32 + lane] : make_float2(0.f, 0.f);
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            // closed-form border at l0 (cs_power, steer.cpp:19-31)
+            const float* cp = ws[k].cp;
+            const float* sp = ws[k].sp;
+            d[k] = __fmul_rn(__fmul_rn(bf, cp[ea]), sp[ep]);
+            dp[k] = dpp[k] = d1[k] = dp1[k] = dpp1[k] = 0.0f;
+            if (ORDER >= 1) {
+                const float tb = ep ? __fmul_rn(__fmul_rn((float)ep, cp[ea + 1]), sp[ep - 1]) : 0.0f;
+                const float ta = ea ? __fmul_rn(__fmul_rn((float)ea, cp[ea - 1]), sp[ep + 1]) : 0.0f;
+                dp[k] = __fmul_rn(__fmul_rn(0.5f, bf), __fsub_rn(tb, ta));
+            }
+            if (ORDER >= 2) {
+                const float t2b = ep > 1 ? __fmul_rn(__fmul_rn(ep * (ep - 1.0f), cp[ea + 2]), sp[ep - 2]) : 0.0f;
+                const float t2a = ea > 1 ? __fmul_rn(__fmul_rn(ea * (ea - 1.0f), cp[ea - 2]), sp[ep + 2]) : 0.0f;
+                const float mid = __fmul_rn(__fmul_rn(2.0f * ea * ep + ea + ep, cp[ea]), sp[ep]);
+                dpp[k] = __fmul_rn(__fmul_rn(0.25f, bf), __fsub_rn(__fadd_rn(t2b, t2a), mid));
+            }
+            A0[k] = make_float2(__fmul_rn(x0.x, d[k]), __fmul_rn(x0.y, d[k]));
+            A1[k] = make_float2(__fmul_rn(x0.x, dp[k]), __fmul_rn(x0.y, dp[k]));
+            A2[k] = make_float2(__fmul_rn(x0.x, dpp[k]), __fmul_rn(x0.y, dpp[k]));
+            W0[k] = make_float2(__fmul_rn(w0.x, d[k]), __fmul_rn(w0.y, d[k]));
+            W1[k] = make_float2(__fmul_rn(w0.x, dp[k]), __fmul_rn(w0.y, dp[k]));
+            W2[k] = make_float2(__fmul_rn(w0.x, dpp[k]), __fmul_rn(w0.y, dpp[k]));
         }
 #pragma unroll 2
         for (int s = 1; s < glen; ++s) {
             const int at = (r0 + s) * 32 + lane;
             const float4 pqr = __ldg(T.PQR + at);
             const float P = pqr.x, Q = pqr.y, R = pqr.z;
-            const float t1 = fmaf(P, cb, Q);
-            const float dn = t1 * d - R * d1;
-            float dpn = 0.0f, dppn = 0.0f;
-            if (ORDER >= 1) {
-                const float t1p = -P * sb;
-                dpn = t1p * d + t1 * dp - R * dp1;
-                if (ORDER >= 2) {
-                    const float t1pp = -P * cb;
-                    dppn = t1pp * d + 2.0f * t1p * dp + t1 * dpp - R * dpp1;
-                }
-            }
-            d1 = d;
-            d = dn;
-            if (ORDER >= 1) {
-                dp1 = dp;
-                dp = dpn;
-            }
-            if (ORDER >= 2) {
-                dpp1 = dpp;
-                dpp = dppn;
-            }
             const float2 x = xi[at];
-            A0.x = fmaf(x.x, d, A0.x);
-            A0.y = fmaf(x.y, d, A0.y);
-            if (ORDER >= 1) {
-                A1.x = fmaf(x.x, dp, A1.x);
-                A1.y = fmaf(x.y, dp, A1.y);
-            }
-            if (ORDER >= 2) {
-                A2.x = fmaf(x.x, dpp, A2.x);
-                A2.y = fmaf(x.y, dpp, A2.y);
-            }
-            if (WEDGE) {
-                const float2 w = wx[at];
-                W0.x = fmaf(w.x, d, W0.x);
-                W0.y = fmaf(w.y, d, W0.y);
+            const float2 w = WEDGE ? wx[at] : make_float2(0.f, 0.f);
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                // three-term recursion (steer.cpp:101-141): t1 = P cos b + Q, t2 = R
+                const float t1 = fmaf(P, cb[k], Q);
+                const float dn = fmaf(t1, d[k], -__fmul_rn(R, d1[k]));
+                float dpn = 0.0f, dppn = 0.0f;
                 if (ORDER >= 1) {
-                    W1.x = fmaf(w.x, dp, W1.x);
-                    W1.y = fmaf(w.y, dp, W1.y);
+                    const float t1p = __fmul_rn(-P, sb[k]);
+                    dpn = fmaf(t1p, d[k], fmaf(t1, dp[k], -__fmul_rn(R, dp1[k])));
+                    if (ORDER >= 2) {
+                        const float t1pp = __fmul_rn(-P, cb[k]);
+                        dppn = fmaf(t1pp, d[k], fmaf(2.0f * t1p, dp[k], fmaf(t1, dpp[k], -__fmul_rn(R, dpp1[k]))));
+                    }
+                }
+                d1[k] = d[k];
+                d[k] = dn;
+                if (ORDER >= 1) {
+                    dp1[k] = dp[k];
+                    dp[k] = dpn;
                 }
                 if (ORDER >= 2) {
-                    W2.x = fmaf(w.x, dpp, W2.x);
-                    W2.y = fmaf(w.y, dpp, W2.y);
+                    dpp1[k] = dpp[k];
+                    dpp[k] = dppn;
+                }
+                A0[k].x = fmaf(x.x, d[k], A0[k].x);
+                A0[k].y = fmaf(x.y, d[k], A0[k].y);
+                if (ORDER >= 1) {
+                    A1[k].x = fmaf(x.x, dp[k], A1[k].x);
+                    A1[k].y = fmaf(x.y, dp[k], A1[k].y);
+                }
+                if (ORDER >= 2) {
+                    A2[k].x = fmaf(x.x, dpp[k], A2[k].x);
+                    A2[k].y = fmaf(x.y, dpp[k], A2[k].y);
+                }
+                if (WEDGE) {
+                    W0[k].x = fmaf(w.x, d[k], W0[k].x);
+                    W0[k].y = fmaf(w.y, d[k], W0[k].y);
+                    if (ORDER >= 1) {
+                        W1[k].x = fmaf(w.x, dp[k], W1[k].x);
+                        W1[k].y = fmaf(w.y, dp[k], W1[k].y);
+                    }
+                    if (ORDER >= 2) {
+                        W2[k].x = fmaf(w.x, dpp[k], W2[k].x);
+                        W2[k].y = fmaf(w.y, dpp[k], W2[k].y);
+                    }
                 }
             }
         }
-        // phases e^{-i m a} e^{-i m' g}; conj for negative orders
-        float2 pa = ws.ua[abs(m)], pg = ws.ug[abs(mp)];
-        if (m < 0) pa.y = -pa.y;
-        if (mp < 0) pg.y = -pg.y;
-        const float2 z = cmul(pa, pg);
         const float wgt = (m == 0 && mp == 0) ? 1.0f : 2.0f;  // half-plane symmetry
         const float fm = (float)m, fmp = (float)mp;
-        {
-            const float2 v0 = cmul(z, A0);
-            acc[0] += wgt * v0.x;
-            if (ORDER >= 1) {
-                const float2 v1 = cmul(z, A1);
-                acc[1] += wgt * fm * v0.y;
-                acc[2] += wgt * v1.x;
-                acc[3] += wgt * fmp * v0.y;
-                if (ORDER >= 2) {
-                    const float2 v2 = cmul(z, A2);
-                    acc[4] -= wgt * fm * fm * v0.x;
-                    acc[5] += wgt * fm * v1.y;
-                    acc[6] -= wgt * fm * fmp * v0.x;
-                    acc[7] += wgt * v2.x;
-                    acc[8] += wgt * fmp * v1.y;
-                    acc[9] -= wgt * fmp * fmp * v0.x;
-                }
-            }
-        }
-        if (WEDGE) {
-            const float2 v0 = cmul(z, W0);
-            accw[0] += wgt * v0.x;
-            if (ORDER >= 1) {
-                const float2 v1 = cmul(z, W1);
-                accw[1] += wgt * fm * v0.y;
-                accw[2] += wgt * v1.x;
-                accw[3] += wgt * fmp * v0.y;
-                if (ORDER >= 2) {
-                    const float2 v2 = cmul(z, W2);
-                    accw[4] -= wgt * fm * fm * v0.x;
-                    accw[5] += wgt * fm * v1.y;
-                    accw[6] -= wgt * fm * fmp * v0.x;
-                    accw[7] += wgt * v2.x;
-                    accw[8] += wgt * fmp * v1.y;
-                    accw[9] -= wgt * fmp * fmp * v0.x;
+        const float wm = wgt * fm, wmp = wgt * fmp;  // exact (wgt is 1 or 2)
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            // phases e^{-i m a} e^{-i m' g}; conj for negative orders
+            float2 pa = ws[k].ua[abs(m)], pg = ws[k].ug[abs(mp)];
+            if (m < 0) pa.y = -pa.y;
+            if (mp < 0) pg.y = -pg.y;
+            const float2 z = cmul_x(pa, pg);
+#pragma unroll
+            for (int part = 0; part < 2; ++part) {
+                if (part == 1 && !WEDGE) break;
+                float* ac = part ? accw[k] : acc[k];
+                const float2 v0 = cmul_x(z, part ? W0[k] : A0[k]);
+                ac[0] = fmaf(wgt, v0.x, ac[0]);
+                if (ORDER >= 1) {
+                    const float2 v1 = cmul_x(z, part ? W1[k] : A1[k]);
+                    ac[NV > 1 ? 1 : 0] = fmaf(wm, v0.y, ac[NV > 1 ? 1 : 0]);
+                    ac[NV > 2 ? 2 : 0] = fmaf(wgt, v1.x, ac[NV > 2 ? 2 : 0]);
+                    ac[NV > 3 ? 3 : 0] = fmaf(wmp, v0.y, ac[NV > 3 ? 3 : 0]);
+                    if (ORDER >= 2) {
+                        const float2 v2 = cmul_x(z, part ? W2[k] : A2[k]);
+                        ac[NV > 4 ? 4 : 0] = fmaf(-__fmul_rn(wm, fm), v0.x, ac[NV > 4 ? 4 : 0]);
+                        ac[NV > 5 ? 5 : 0] = fmaf(wm, v1.y, ac[NV > 5 ? 5 : 0]);
+                        ac[NV > 6 ? 6 : 0] = fmaf(-__fmul_rn(wm, fmp), v0.x, ac[NV > 6 ? 6 : 0]);
+                        ac[NV > 7 ? 7 : 0] = fmaf(wgt, v2.x, ac[NV > 7 ? 7 : 0]);
+                        ac[NV > 8 ? 8 : 0] = fmaf(wmp, v1.y, ac[NV > 8 ? 8 : 0]);
+                        ac[NV > 9 ? 9 : 0] = fmaf(-__fmul_rn(wmp, fmp), v0.x, ac[NV > 9 ? 9 : 0]);
+                    }
                 }
             }
         }
     }
     // cross-lane reduction in FP64 (one interleaved butterfly for all values),
     // published through shared memory
-    constexpr int NV = ORDER == 0 ? 1 : (ORDER == 1 ? 4 : 10);
-    constexpr int NT = 2 * NV;
+    constexpr int NT = 2 * NV * K;
     double v[NT];
 #pragma unroll
-    for (int i = 0; i < NV; ++i) {
-        v[i] = acc[i];
-        v[NV + i] = accw[i];
-    }
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            v[2 * NV * k + i] = acc[k][i];
+            v[2 * NV * k + NV + i] = accw[k][i];
+        }
 #pragma unroll
     for (int o = 16; o; o >>= 1)
 #pragma unroll
         for (int i = 0; i < NT; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
     if (lane == 0) {
 #pragma unroll
-        for (int i = 0; i < NV; ++i) {
-            ws.res[i] = v[i];
-            if (WEDGE) ws.res[10 + i] = v[NV + i];
-        }
+        for (int k = 0; k < K; ++k)
+#pragma unroll
+            for (int i = 0; i < NV; ++i) {
+                ws[k].res[i] = v[2 * NV * k + i];
+                ws[k].res[10 + i] = WEDGE ? v[2 * NV * k + NV + i] : 0.0;
+            }
     }
     __syncwarp();
 }
@@ -659,31 +690,70 @@ __global__ void __launch_bounds__(256) compose_kernel(StageArgs a) {
     }
 }
 
-// warp per listed candidate
-template <int ORDER>
-__global__ void __launch_bounds__(kWarps * 32) eval_kernel(StageArgs a, const int* list, const int* count) {
-    __shared__ WarpScratch wsc[kWarps];
+// warps per CTA of the evaluation kernels (K scratch sets per warp in static smem)
+template <int K>
+struct EvalShape {
+    static constexpr int WARPS = K >= 4 ? 4 : 8;
+};
+
+// K jobs of one warp: one K-way evaluation when they share their kernels,
+// else one after the other
+template <int ORDER, int K>
+__device__ __forceinline__ void eval_group(const BandTables& T, const EvalJob (&job)[K], WarpScratch* ws) {
+    bool same = true;
+#pragma unroll
+    for (int k = 1; k < K; ++k) same &= job[k].xi == job[0].xi && job[k].wx == job[0].wx;
+    if (K == 1 || same) {
+        warp_eval_k<ORDER, K>(T, job, ws);
+    } else {
+#pragma unroll 1
+        for (int k = 0; k < K; ++k) {
+            const EvalJob one[1] = {job[k]};
+            warp_eval_k<ORDER, 1>(T, one, ws + k);
+        }
+    }
+}
+
+// K listed candidates per warp
+template <int ORDER, int K>
+__global__ void __launch_bounds__(EvalShape<K>::WARPS * 32) eval_kernel(StageArgs a, const int* list,
+                                                                        const int* count) {
+    constexpr int WARPS = EvalShape<K>::WARPS;
+    __shared__ WarpScratch wsc[WARPS * K];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n = *count;
     const int len = a.T.rows * 32;
     const bool wedge = a.prm.has_wedge != 0;
-    for (int q = blockIdx.x * kWarps + warp; q < n; q += gridDim.x * kWarps) {
+    if (a.eval_stats && blockIdx.x == 0 && threadIdx.x == 0)
+        atomicAdd(a.eval_stats + ((size_t)a.T.L * 2 + (ORDER == 2)) * 2 + (wedge ? 1 : 0), (unsigned long long)n);
+    const int q0 = (blockIdx.x * WARPS + warp) * K;
+    if (q0 >= n) return;
+    EvalJob job[K];
+    int idx[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const int q = q0 + k < n ? q0 + k : q0;  // tail: repeat the first job, results dropped
         const int i = list[q];
-        CandWork& wk = a.work[i];
+        idx[k] = q0 + k < n ? i : -1;
+        const CandWork& wk = a.work[i];
         const int w = i / a.max_cand;
         const bool fin = wk.status == ST_FINAL;
         const bool chart = !fin && a.cand[i].anchored;
-        const float2* xi = chart ? a.xi_pool + (size_t)wk.slot * len : a.xi_win + (size_t)w * len;
-        const float2* wx = !wedge ? nullptr : (chart ? a.w_pool + (size_t)wk.slot * len : a.T.wedge);
+        job[k].xi = chart ? a.xi_pool + (size_t)wk.slot * len : a.xi_win + (size_t)w * len;
+        job[k].wx = !wedge ? nullptr : (chart ? a.w_pool + (size_t)wk.slot * len : a.T.wedge);
         const double* e = wk.status == ST_EVAL2 ? wk.e : wk.et;
-        warp_eval<ORDER>(a.T, xi, wx, e[0], e[1], e[2], wsc[warp]);
-        constexpr int NV = ORDER == 0 ? 1 : 10;
-        if (lane < NV) {
-            wk.c[lane] = wsc[warp].res[lane];
-            wk.r[lane] = wsc[warp].res[10 + lane];
-        }
-        __syncwarp();
+        job[k].a = e[0], job[k].b = e[1], job[k].g = e[2];
     }
+    WarpScratch* ws = wsc + warp * K;
+    eval_group<ORDER, K>(a.T, job, ws);
+    constexpr int NV = ORDER == 0 ? 1 : 10;
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+        if (idx[k] >= 0 && lane < NV) {
+            CandWork& wk = a.work[idx[k]];
+            wk.c[lane] = ws[k].res[lane];
+            wk.r[lane] = ws[k].res[10 + lane];
+        }
 }
 
 // Newton step of every order-2 evaluated candidate; appends trials to list_out
@@ -830,24 +900,33 @@ __global__ void window_reduce_kernel(ReduceArgs a) {
 }
 
 // ---------------------------------------------------------------- sweep
-__global__ void __launch_bounds__(kWarps * 32) eval_sweep_kernel(EvalArgs a) {
-    __shared__ WarpScratch wsc[kWarps];
+template <int ORDER, int K>
+__global__ void __launch_bounds__(EvalShape<K>::WARPS * 32) eval_sweep_kernel(EvalArgs a) {
+    constexpr int WARPS = EvalShape<K>::WARPS;
+    __shared__ WarpScratch wsc[WARPS * K];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    WarpScratch* ws = wsc + warp * K;
     const long long total = (long long)a.n_xi * a.n_rot;
-    for (long long u = (long long)blockIdx.x * kWarps + warp; u < total;
-         u += (long long)gridDim.x * kWarps) {
-        const int p = (int)(u / a.n_rot), gi = (int)(u % a.n_rot);
-        const float2* xi = a.xi + (size_t)p * a.T.rows * 32;
-        const double* e = a.euler + 3 * gi;
-        if (a.order >= 1) warp_eval<1>(a.T, xi, nullptr, e[0], e[1], e[2], wsc[warp]);
-        else warp_eval<0>(a.T, xi, nullptr, e[0], e[1], e[2], wsc[warp]);
-        if (lane == 0) {
-            const double* r = wsc[warp].res;
-            double* o = a.out + 4 * u;
+    for (long long u0 = ((long long)blockIdx.x * WARPS + warp) * K; u0 < total;
+         u0 += (long long)gridDim.x * WARPS * K) {
+        EvalJob job[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const long long u = u0 + k < total ? u0 + k : u0;
+            const int p = (int)(u / a.n_rot), gi = (int)(u % a.n_rot);
+            job[k].xi = a.xi + (size_t)p * a.T.rows * 32;
+            job[k].wx = nullptr;
+            const double* e = a.euler + 3 * gi;
+            job[k].a = e[0], job[k].b = e[1], job[k].g = e[2];
+        }
+        eval_group<ORDER, K>(a.T, job, ws);
+        if (lane < K && u0 + lane < total) {
+            const double* r = ws[lane].res;
+            double* o = a.out + 4 * (u0 + lane);
             o[0] = r[0];
-            o[1] = a.order >= 1 ? r[1] : 0.0;
-            o[2] = a.order >= 1 ? r[2] : 0.0;
-            o[3] = a.order >= 1 ? r[3] : 0.0;
+            o[1] = ORDER >= 1 ? r[1] : 0.0;
+            o[2] = ORDER >= 1 ? r[2] : 0.0;
+            o[3] = ORDER >= 1 ? r[3] : 0.0;
         }
         __syncwarp();
     }
@@ -871,6 +950,15 @@ long long compose_scratch_floats(int L) {
 
 size_t compose_smem_bytes(int L) { return sizeof(float) * (size_t)compose_scratch_floats(L); }
 
+double eval_flops(int L, int order, bool wedge) {
+    const double nxi = (L + 1.0) * (2.0 * L + 1.0) * (2.0 * L + 3.0) / 3.0;
+    const double plane = (2.0 * L + 1.0) * (2.0 * L + 1.0);
+    const int nd = order + 1;                                  // d, d', d''
+    const int nv = order == 0 ? 1 : (order == 1 ? 4 : 10);     // reduced values
+    const double per_kernel = 4.0 * nd * nxi + 6.0 * nv * plane;
+    return 6.0 * nd * nxi + per_kernel * (wedge ? 2.0 : 1.0);
+}
+
 static int thread_grid(long long n) {
     long long b = (n + 255) / 256;
     return (int)(b < 1 ? 1 : (b > 4096 ? 4096 : b));
@@ -888,11 +976,35 @@ void launch_compose(const StageArgs& a, int n, cudaStream_t s) {
     if (smem) cudaFuncSetAttribute(compose_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     compose_kernel<<<n, 256, smem, s>>>(a);
 }
+// jobs per warp in the refinement: 1 (measured fastest: refinement lists mix
+// windows, and one job per warp keeps the most warps in flight); BMB_EVAL_K=2/4
+// selects K-way warps for experiments
+static int eval_k_for(int order, int /*max_n*/) {
+    static const int forced = [] {
+        const char* e = std::getenv("BMB_EVAL_K");
+        return e ? std::atoi(e) : 1;
+    }();
+    if (forced == 2 || forced == 4) return order == 2 ? 2 : forced;
+    return 1;
+}
+
+template <int ORDER, int K>
+static void launch_eval_k(const StageArgs& a, const int* list, const int* count, int max_n, cudaStream_t s) {
+    constexpr int per = K * EvalShape<K>::WARPS;
+    eval_kernel<ORDER, K><<<(max_n + per - 1) / per, EvalShape<K>::WARPS * 32, 0, s>>>(a, list, count);
+}
+
 void launch_eval(const StageArgs& a, int order, const int* list, const int* count, int max_n, cudaStream_t s) {
     if (max_n <= 0) return;
-    const int grid = (max_n + kWarps - 1) / kWarps;
-    if (order == 2) eval_kernel<2><<<grid, kWarps * 32, 0, s>>>(a, list, count);
-    else eval_kernel<0><<<grid, kWarps * 32, 0, s>>>(a, list, count);
+    const int k = eval_k_for(order, max_n);
+    if (order == 2) {
+        if (k >= 2) launch_eval_k<2, 2>(a, list, count, max_n, s);
+        else launch_eval_k<2, 1>(a, list, count, max_n, s);
+    } else {
+        if (k == 4) launch_eval_k<0, 4>(a, list, count, max_n, s);
+        else if (k == 2) launch_eval_k<0, 2>(a, list, count, max_n, s);
+        else launch_eval_k<0, 1>(a, list, count, max_n, s);
+    }
 }
 void launch_step(const StageArgs& a, int* list_out, int* count_out, int max_n, cudaStream_t s) {
     step_kernel<<<thread_grid(max_n), 256, 0, s>>>(a, list_out, count_out);
@@ -915,7 +1027,18 @@ int launch_eval_sweep(const EvalArgs& a, cudaStream_t s) {
     int sms = 0, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    eval_sweep_kernel<<<sms * 4, kWarps * 32, 0, s>>>(a);
+    const char* e = std::getenv("BMB_SWEEP_K");
+    const int k = e ? std::atoi(e) : 4;
+    const int grid = sms * 8;
+    if (a.order >= 1) {
+        if (k == 1) eval_sweep_kernel<1, 1><<<grid, EvalShape<1>::WARPS * 32, 0, s>>>(a);
+        else if (k == 2) eval_sweep_kernel<1, 2><<<grid, EvalShape<2>::WARPS * 32, 0, s>>>(a);
+        else eval_sweep_kernel<1, 4><<<grid, EvalShape<4>::WARPS * 32, 0, s>>>(a);
+    } else {
+        if (k == 1) eval_sweep_kernel<0, 1><<<grid, EvalShape<1>::WARPS * 32, 0, s>>>(a);
+        else if (k == 2) eval_sweep_kernel<0, 2><<<grid, EvalShape<2>::WARPS * 32, 0, s>>>(a);
+        else eval_sweep_kernel<0, 4><<<grid, EvalShape<4>::WARPS * 32, 0, s>>>(a);
+    }
     return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }
 

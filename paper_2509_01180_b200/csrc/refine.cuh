@@ -51,6 +51,7 @@ struct StageArgs {
     int* counts = nullptr;           // [CNT_*] list lengths
     int* list2 = nullptr;            // candidates awaiting the order-2 evaluation (or final)
     int* listc = nullptr;            // candidates whose chart kernel must be (re)built
+    unsigned long long* eval_stats = nullptr;  // [kMaxL+1][2][2] evaluations by (L, order, wedge)
 };
 enum { CNT_L2 = 0, CNT_COMP = 1, CNT_T0 = 2, CNT_T1 = 3 };
 
@@ -93,6 +94,11 @@ struct EvalArgs {
     double* out = nullptr;
 };
 int launch_eval_sweep(const EvalArgs& a, cudaStream_t s);
+
+// algorithmic FLOPs of one evaluation (SURVEY.md §8(d) accounting, full (m,m') plane):
+// recursion 6 N_xi per derivative order, contraction 4 N_xi and phases 6 (2L+1)^2 per
+// reduced value and kernel (correlation, + wedge-power kernel)
+double eval_flops(int L, int order, bool wedge);
 
 // build band-layout kernels xi_l[m,m'] = sum_k conj(f_klm) t_klm' for many
 // coefficient pairs (f from real-packed rows)

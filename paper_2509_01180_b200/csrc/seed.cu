@@ -11,18 +11,43 @@
 
 namespace bmb {
 
+// shared-memory plan: [f | t] (later reused for one beta slice A_j), xi (or
+// the global scratch when it does not fit), scores, maxima
+struct SeedSmem {
+    size_t region0, xi, sc, maxima, total;
+    bool xi_in_smem;
+};
+__host__ __device__ inline SeedSmem seed_smem_plan(int rows_low, int L, int nxi, int npt) {
+    const int wd = 2 * L + 1;
+    SeedSmem p;
+    const size_t ft = sizeof(double) * 2 * (size_t)rows_low;
+    const size_t aj = sizeof(double2) * (size_t)wd * wd;
+    p.region0 = (ft > aj ? ft : aj + 0);
+    p.region0 = (p.region0 + 15) / 16 * 16;
+    const size_t xib = sizeof(double2) * (size_t)nxi;
+    const size_t rest = sizeof(double) * npt + sizeof(int) * npt;
+    p.xi_in_smem = p.region0 + xib + rest <= 200 * 1024;
+    p.xi = p.region0;
+    p.sc = p.xi + (p.xi_in_smem ? xib : 0);
+    p.maxima = p.sc + sizeof(double) * npt;
+    p.total = p.maxima + sizeof(int) * npt;
+    return p;
+}
+
 __global__ void __launch_bounds__(256) seed_kernel(SeedArgs a) {
     extern __shared__ __align__(16) unsigned char sm[];
     const int w = blockIdx.x;
     const int L = a.L_low, wd = 2 * L + 1;
     const int npt = a.na * a.nb * a.ng;
     const int nrow = a.rows_low;  // real-packed rows of degrees <= L
+    const SeedSmem plan = seed_smem_plan(nrow, L, a.nxi, npt);
     double* f = reinterpret_cast<double*>(sm);
     double* t = f + nrow;
-    double2* xi = reinterpret_cast<double2*>(t + nrow);           // N_xi(L)
-    double2* A = xi + a.nxi;                                        // nb x wd x wd
-    double* sc = reinterpret_cast<double*>(A + (size_t)a.nb * wd * wd);  // npt
-    int* maxima = reinterpret_cast<int*>(sc + npt);                 // npt
+    double2* Aj = reinterpret_cast<double2*>(sm);  // overlays f, t once xi is built
+    double2* xi = plan.xi_in_smem ? reinterpret_cast<double2*>(sm + plan.xi)
+                                  : a.xi_scratch + (size_t)w * a.nxi;
+    double* sc = reinterpret_cast<double*>(sm + plan.sc);
+    int* maxima = reinterpret_cast<int*>(sm + plan.maxima);
     __shared__ int n_max;
 
     const float* cw = a.coef + (long long)w * a.ldc;
@@ -64,40 +89,41 @@ __global__ void __launch_bounds__(256) seed_kernel(SeedArgs a) {
     }
     __syncthreads();
 
-    // A_j[m][m'] = sum_l xi_l[m,m'] d^l_{m,m'}(beta_j)
-    for (int e = threadIdx.x; e < a.nb * wd * wd; e += blockDim.x) {
-        const int j = e / (wd * wd), m = (e / wd) % wd - L, mp = e % wd - L;
-        double re = 0.0, im = 0.0;
-        for (int l = max(abs(m), abs(mp)); l <= L; ++l) {
-            const int o = l * (2 * l - 1) * (2 * l + 1) / 3 + (m + l) * (2 * l + 1) + (mp + l);
-            const double d = a.dgrid[(size_t)j * a.nxi + o];
-            re += xi[o].x * d;
-            im += xi[o].y * d;
-        }
-        A[e] = make_double2(re, im);
-    }
-    __syncthreads();
-
+    // per beta slice j: A_j[m][m'] = sum_l xi_l[m,m'] d^l_{m,m'}(beta_j), then
     // score(i,j,k) = Re sum_m ua_i[m] sum_m' A_j[m][m'] ug_k[m']
-    for (int idx = threadIdx.x; idx < npt; idx += blockDim.x) {
-        const int k = idx % a.ng, i = (idx / a.ng) % a.na, j = idx / (a.ng * a.na);
-        const double2* Aj = A + (size_t)j * wd * wd;
-        const double2* pg = a.ug + (size_t)k * wd;
-        const double2* pa = a.ua + (size_t)i * wd;
-        double acc = 0.0;
-        for (int m = 0; m < wd; ++m) {
-            double bre = 0.0, bim = 0.0;
-            for (int mp = 0; mp < wd; ++mp) {
-                const double2 x = Aj[m * wd + mp], y = pg[mp];
-                bre += x.x * y.x - x.y * y.y;
-                bim += x.x * y.y + x.y * y.x;
+    for (int j = 0; j < a.nb; ++j) {
+        for (int e = threadIdx.x; e < wd * wd; e += blockDim.x) {
+            const int m = e / wd - L, mp = e % wd - L;
+            double re = 0.0, im = 0.0;
+            for (int l = max(abs(m), abs(mp)); l <= L; ++l) {
+                const int o = l * (2 * l - 1) * (2 * l + 1) / 3 + (m + l) * (2 * l + 1) + (mp + l);
+                const double d = a.dgrid[(size_t)j * a.nxi + o];
+                re += xi[o].x * d;
+                im += xi[o].y * d;
             }
-            acc += pa[m].x * bre - pa[m].y * bim;
+            Aj[e] = make_double2(re, im);
         }
-        if (a.wedge_sqrt) acc /= a.wedge_sqrt[idx];
-        sc[idx] = acc;
+        __syncthreads();
+        for (int q = threadIdx.x; q < a.na * a.ng; q += blockDim.x) {
+            const int k = q % a.ng, i = q / a.ng;
+            const int idx = (j * a.na + i) * a.ng + k;
+            const double2* pg = a.ug + (size_t)k * wd;
+            const double2* pa = a.ua + (size_t)i * wd;
+            double acc = 0.0;
+            for (int m = 0; m < wd; ++m) {
+                double bre = 0.0, bim = 0.0;
+                for (int mp = 0; mp < wd; ++mp) {
+                    const double2 x = Aj[m * wd + mp], y = pg[mp];
+                    bre += x.x * y.x - x.y * y.y;
+                    bim += x.x * y.y + x.y * y.x;
+                }
+                acc += pa[m].x * bre - pa[m].y * bim;
+            }
+            if (a.wedge_sqrt) acc /= a.wedge_sqrt[idx];
+            sc[idx] = acc;
+        }
+        __syncthreads();
     }
-    __syncthreads();
 
     // strict local maxima over the 26-neighbourhood (alpha/gamma wrap, beta clamps);
     // a plateau keeps its lowest flat index
@@ -166,10 +192,10 @@ __global__ void __launch_bounds__(256) seed_kernel(SeedArgs a) {
 }
 
 size_t seed_smem_bytes(const SeedArgs& a) {
-    const int wd = 2 * a.L_low + 1;
-    const int npt = a.na * a.nb * a.ng;
-    return sizeof(double) * 2 * a.rows_low + sizeof(double2) * a.nxi +
-           sizeof(double2) * (size_t)a.nb * wd * wd + sizeof(double) * npt + sizeof(int) * npt;
+    return seed_smem_plan(a.rows_low, a.L_low, a.nxi, a.na * a.nb * a.ng).total;
+}
+bool seed_needs_scratch(const SeedArgs& a) {
+    return !seed_smem_plan(a.rows_low, a.L_low, a.nxi, a.na * a.nb * a.ng).xi_in_smem;
 }
 
 int launch_seed(const SeedArgs& a, int n_win, cudaStream_t s) {
@@ -177,7 +203,19 @@ int launch_seed(const SeedArgs& a, int n_win, cudaStream_t s) {
     const size_t smem = seed_smem_bytes(a);
     if (smem > 200 * 1024) return 1;
     cudaFuncSetAttribute(seed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    seed_kernel<<<n_win, 256, smem, s>>>(a);
+    if (!seed_needs_scratch(a)) {
+        seed_kernel<<<n_win, 256, smem, s>>>(a);
+    } else {  // xi in global scratch: a.scratch_windows windows per launch
+        if (!a.xi_scratch || a.scratch_windows < 1) return 1;
+        for (int w0 = 0; w0 < n_win; w0 += a.scratch_windows) {
+            SeedArgs c = a;
+            c.coef = a.coef + (long long)w0 * a.ldc;
+            c.cand = a.cand + (size_t)w0 * a.max_cand;
+            c.cand_count = a.cand_count + w0;
+            if (a.seed_score) c.seed_score = a.seed_score + (size_t)w0 * a.max_cand;
+            seed_kernel<<<min(a.scratch_windows, n_win - w0), 256, smem, s>>>(c);
+        }
+    }
     return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }
 

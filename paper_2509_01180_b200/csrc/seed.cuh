@@ -25,8 +25,11 @@ struct SeedArgs {
     CandState* cand = nullptr;     // [n_win][max_cand]
     int* cand_count = nullptr;     // [n_win]
     double* seed_score = nullptr;  // [n_win][max_cand] or null
+    double2* xi_scratch = nullptr; // [scratch_windows][nxi] when xi does not fit in shared memory
+    int scratch_windows = 0;
 };
 
 int launch_seed(const SeedArgs& a, int n_win, cudaStream_t s);
+bool seed_needs_scratch(const SeedArgs& a);
 
 }  // namespace bmb

@@ -1,6 +1,7 @@
-"""Expansion parity (kernel K2, tcgen05 FP16 3-pass): GPU vs the CPU oracle's
-expand(shift_volume(v, s)) on identical float32 inputs; bar: 1e-5 relative L2
-(BASELINE.json north_star)."""
+"""Expansion parity, both device algorithms (K2f factored: trilinear samples +
+phi-DFT + theta/radial contractions; K1+K2 dense operator on tcgen05 FP16
+3-pass): GPU vs the CPU oracle's expand(shift_volume(v, s)) on identical
+float32 inputs; bar: 1e-5 relative L2 (BASELINE.json north_star)."""
 import math
 
 import numpy as np
@@ -16,9 +17,13 @@ def _rel_l2(a, b):
     return float(np.linalg.norm(a - b) / np.linalg.norm(b))
 
 
-@pytest.mark.parametrize("n,L,seed", [(32, 8, 1), (64, 16, 2), (48, 8, 3)])
-def test_expand_matches_oracle(cuda_device, n, L, seed):
+@pytest.mark.parametrize("mode", ["factored", "gemm"])
+@pytest.mark.parametrize("n,L,seed", [(32, 8, 1), (64, 16, 2), (48, 8, 3), (48, 24, 4)])
+def test_expand_matches_oracle(cuda_device, n, L, seed, mode):
+    if mode == "gemm" and L == 24:
+        pytest.skip("dense operator at L=24 takes minutes to build on the host")
     ctx = api.Context(n, L, L * math.pi)
+    ctx.set_expand_mode(mode)
     spec = bmo.Spec(L, L * math.pi)
     assert ctx.coeff_count == spec.coeff_count
     for l in range(L + 1):
@@ -42,8 +47,10 @@ def test_expand_matches_oracle(cuda_device, n, L, seed):
         assert err < 1e-5, f"window {i} shift {s}: rel L2 {err:.2e}"
 
 
-def test_expand_zero_volume_and_batch_consistency(cuda_device):
+@pytest.mark.parametrize("mode", ["factored", "gemm"])
+def test_expand_zero_volume_and_batch_consistency(cuda_device, mode):
     ctx = api.Context(32, 8, 8 * math.pi)
+    ctx.set_expand_mode(mode)
     z = np.zeros((1, 32, 32, 32), np.float32)
     assert np.all(ctx.expand(z).cpu().numpy() == 0)
     t = bmo.gaussian_blob_template(32, 20, 9).astype(np.float32)
