@@ -227,28 +227,37 @@ void Context::refine_windows(int nw, int maxc, const AlignConfig& cfg, const Qua
     int* h_active = nullptr;
     cudaMallocHost(&h_active, sizeof(int) * 4);
     const bool wedge = wedge_active();
-    // window kernels of the largest band and the anchored pool share a budget
+    // window kernels of the largest band plus one anchored-chart slot per seeded
+    // candidate (correlation + wedge kernel) share a memory budget; chunk
+    // boundaries follow the actual per-window candidate counts
     const int Lmax_band = cfg.bands.back();
     BandDev& btop = band(Lmax_band);
     const size_t kernel_bytes = sizeof(float2) * (size_t)btop.rows * 32;
-    const size_t per_window = kernel_bytes * (1 + (size_t)maxc * pool_fraction_ * (wedge ? 2 : 1));
-    long long chunk = std::max<long long>(64, (long long)(pool_budget_ / per_window));
-    chunk = std::min<long long>(chunk, nw);
-    for (long long w0 = 0; w0 < nw; w0 += chunk) {
-        const int cnt = (int)std::min<long long>(chunk, nw - w0);
-        double frac = pool_fraction_;
-        for (int attempt = 0; attempt < 2; ++attempt) {
-            if (attempt == 1) {  // pool overflow: rerun the chunk with a slot per candidate
-                frac = 1.0;
-                ck(cudaMemcpyAsync(cand_.as<CandState>() + (size_t)w0 * maxc, cand_backup_.p,
-                                   sizeof(CandState) * (size_t)cnt * maxc, cudaMemcpyDeviceToDevice, stream),
-                   "restore");
-            } else {
-                cand_backup_.reserve(sizeof(CandState) * (size_t)cnt * maxc);
-                ck(cudaMemcpyAsync(cand_backup_.p, cand_.as<CandState>() + (size_t)w0 * maxc,
-                                   sizeof(CandState) * (size_t)cnt * maxc, cudaMemcpyDeviceToDevice, stream),
-                   "backup");
+    const size_t slot_bytes = kernel_bytes * (wedge ? 2 : 1);
+    std::vector<int> ncand(nw);
+    ck(cudaMemcpyAsync(ncand.data(), cand_count_.p, sizeof(int) * nw, cudaMemcpyDeviceToHost, stream), "cand counts");
+    ck(cudaStreamSynchronize(stream), "cand counts");
+    std::vector<std::pair<int, int>> chunks;  // (first window, windows)
+    {
+        int w0 = 0;
+        size_t bytes = 0;
+        for (int w = 0; w < nw; ++w) {
+            const size_t need = kernel_bytes + slot_bytes * (size_t)ncand[w];
+            if (w > w0 && bytes + need > pool_budget_) {
+                chunks.push_back({w0, w - w0});
+                w0 = w;
+                bytes = 0;
             }
+            bytes += need;
+        }
+        if (nw > w0) chunks.push_back({w0, nw - w0});
+    }
+    for (const auto& ch : chunks) {
+        const long long w0 = ch.first;
+        const int cnt = ch.second;
+        long long chunk_cands = 0;
+        for (int w = 0; w < cnt; ++w) chunk_cands += ncand[w0 + w];
+        {
             ck(cudaMemsetAsync(d_over, 0, sizeof(int), stream), "overflow");
             for (size_t bi = 0; bi < cfg.bands.size(); ++bi) {
                 const int L = cfg.bands[bi];
@@ -275,7 +284,7 @@ void Context::refine_windows(int nw, int maxc, const AlignConfig& cfg, const Qua
                 if (launch_build_xi(xa, stream) != 0) throw std::runtime_error("build_xi launch failed");
                 ++timer.launches;
                 a.xi_win = xi_win_.as<float2>();
-                a.pool = std::max(1, (int)std::ceil(frac * cnt * maxc));
+                a.pool = (int)std::max<long long>(1, chunk_cands);  // a slot for every candidate: no overflow
                 xi_pool_.reserve(sizeof(float2) * len * a.pool);
                 a.xi_pool = xi_pool_.as<float2>();
                 if (wedge) {
@@ -367,7 +376,7 @@ void Context::refine_windows(int nw, int maxc, const AlignConfig& cfg, const Qua
             }
             ck(cudaMemcpyAsync(h_active + 1, d_over, sizeof(int), cudaMemcpyDeviceToHost, stream), "overflow");
             ck(cudaStreamSynchronize(stream), "chunk");
-            if (h_active[1] == 0) break;
+            if (h_active[1] != 0) throw std::logic_error("refine: anchored-chart pool overflow");
         }
         ReduceArgs ra;
         ra.cand = cand_.as<CandState>() + (size_t)w0 * maxc;

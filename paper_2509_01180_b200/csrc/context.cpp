@@ -23,6 +23,7 @@ Context::Context(int dev, int n_, int l_max, double lambda_cut) : device(dev), n
     BMB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     basis = host::make_basis(l_max, lambda_cut);
     if (const char* e = std::getenv("BMB_EXPAND")) expand_mode = std::string(e) == "gemm" ? 1 : 0;
+    if (const char* e = std::getenv("BMB_BRICKS")) use_bricks = std::atoi(e) != 0;
     geo.n = n;
     geo.l_max = l_max;
     geo.coeffs = basis.coeffs;
@@ -147,8 +148,18 @@ void Context::expand_windows(const float* vols, long long vol_stride, int n_vol,
         upload(win_shift, wshift, stream);
         coef.reserve(sizeof(float) * (size_t)nw * geo.m_pad);
         cudaEvent_t f0 = timer.begin(stream);
-        if (launch_expand_factored(fx, vols, vol_stride, win_vol.as<int>(), win_shift.as<int>(), nw, coef.as<float>(),
-                                   geo.m_pad, stream) != 0)
+        const float* src = vols;
+        long long stride = vol_stride;
+        const bool bricked = use_bricks && n % 4 == 0;
+        if (bricked) {  // 4x4x4-brick copy of the volumes (gather locality of the trilinear taps)
+            bricks_.reserve(sizeof(float) * (size_t)n_vol * n * n * n);
+            launch_to_bricks(vols, vol_stride, n_vol, bricks_.as<float>(), n, stream);
+            ++timer.launches;
+            src = bricks_.as<float>();
+            stride = (long long)n * n * n;
+        }
+        if (launch_expand_factored(fx, src, stride, bricked, win_vol.as<int>(), win_shift.as<int>(), nw,
+                                   coef.as<float>(), geo.m_pad, stream) != 0)
             throw std::runtime_error("factored expansion launch failed");
         ++timer.launches;
         ++timer.gemm_launches;

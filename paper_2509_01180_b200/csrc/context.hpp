@@ -168,6 +168,8 @@ public:
 
     int expand_mode = 0;          // 0: factored expansion (K2f), 1: dense operator GEMM (K1 + K2)
     bool operator_ready = false;
+    bool use_bricks = true;       // factored expansion reads a 4x4x4-brick copy of the volumes
+    DevBuf bricks_;
     void ensure_operator();
     void build_factored_tables();
     FactoredTables fx;
@@ -213,12 +215,11 @@ public:
     }
     // evaluations (order 2, order 0) and their algorithmic FLOPs since the last reset
     void read_eval_stats(long long* evals, double* flops, bool reset);
-    double pool_fraction_ = 0.5;           // anchored-chart pool slots per candidate
-    size_t pool_budget_ = 8ull << 30;       // bytes for window kernels + pool per chunk
+    size_t pool_budget_ = 24ull << 30;      // bytes for window kernels + anchored-chart pool per chunk
 
 private:
     void refine_windows(int nw, int maxc, const AlignConfig& cfg, const Quat& koff, long long grid_evals);
-    DevBuf work_, counters_, xi_win_, xi_pool_, w_pool_, cand_backup_, lists_;
+    DevBuf work_, counters_, xi_win_, xi_pool_, w_pool_, lists_;
     std::map<int, std::unique_ptr<BandDev>> bands_;
     std::map<std::pair<int, long long>, std::unique_ptr<SeedDev>> seeds_;
     DevBuf cand_, cand_count_, outcome_, win_counter_, scratch_, sub_norm_;

@@ -2,7 +2,8 @@
 // stages of expand() (src/basis.cpp:254-328) run per shift window on the
 // device, radius by radius, instead of the dense pulled-back operator:
 //   1. trilinear samples f(r_i, theta_t, phi_p) of the shifted window
-//      (sample_trilinear + shift_volume, src/volume.cpp:19-67), FP64 taps;
+//      (sample_trilinear + shift_volume, src/volume.cpp:19-67): FP64 sample
+//      coordinates, FP32 tap weights, volumes read from a 4x4x4-brick copy;
 //   2. unnormalized phi-DFT of every theta ring (dft_r2c_rows,
 //      src/detail/fftw_util.cpp:16-28), folded over p <-> n_phi - p;
 //   3. theta contraction with Pbar_l^m(u_t) w_t, folded over the GL symmetry
@@ -53,6 +54,23 @@ __host__ __device__ inline Smem smem_plan(const FactoredTables& T) {
     return s;
 }
 
+// 4x4x4 bricks (256 B): the 2x2x2 trilinear footprint of a sample then touches
+// ~1.5 cache lines instead of 4 rows of the raster layout
+__host__ __device__ inline long long brick_offset(int x, int y, int z, int nb) {
+    return ((((long long)(z >> 2) * nb + (y >> 2)) * nb + (x >> 2)) << 6) + ((z & 3) << 4) + ((y & 3) << 2) + (x & 3);
+}
+
+__global__ void to_bricks_kernel(const float* __restrict__ in, long long in_stride, float* __restrict__ out, int n) {
+    const float* v = in + (long long)blockIdx.y * in_stride;
+    float* o = out + (long long)blockIdx.y * n * n * n;
+    const int nb = n >> 2;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n * n * n; i += gridDim.x * blockDim.x) {
+        const int x = i % n, y = (i / n) % n, z = i / (n * n);
+        o[brick_offset(x, y, z, nb)] = v[i];
+    }
+}
+
+template <bool BRICK>
 __global__ void __launch_bounds__(kThreads) expand_factored_kernel(FactoredTables T, const float* __restrict__ vols,
                                                                     long long vol_stride, const int* __restrict__ win_vol,
                                                                     const int* __restrict__ win_shift, float* __restrict__ out,
@@ -96,28 +114,41 @@ __global__ void __launch_bounds__(kThreads) expand_factored_kernel(FactoredTable
             const double gx = rs * cphi[p] * h + h, gy = rs * sphi[p] * h + h, gz = r * uu[t] * h + h;
             const double fx0 = floor(gx), fy0 = floor(gy), fz0 = floor(gz);
             const int x0 = (int)fx0, y0 = (int)fy0, z0 = (int)fz0;
-            const double fx = gx - fx0, fy = gy - fy0, fz = gz - fz0;
-            double val = 0.0;
-#pragma unroll
-            for (int dz = 0; dz < 2; ++dz) {
-                const int zz = z0 + dz, zs = zz + sz;
-                if ((unsigned)zz >= (unsigned)n || (unsigned)zs >= (unsigned)n) continue;
-                const double wz = dz ? fz : 1.0 - fz;
-#pragma unroll
-                for (int dy = 0; dy < 2; ++dy) {
-                    const int yy = y0 + dy, ys = yy + sy;
-                    if ((unsigned)yy >= (unsigned)n || (unsigned)ys >= (unsigned)n) continue;
-                    const double wy = dy ? fy : 1.0 - fy;
-                    const float* row = v + ((long long)zs * n + ys) * n;
-#pragma unroll
-                    for (int dx = 0; dx < 2; ++dx) {
-                        const int xx = x0 + dx, xs = xx + sx;
-                        if ((unsigned)xx >= (unsigned)n || (unsigned)xs >= (unsigned)n) continue;
-                        val += (dx ? fx : 1.0 - fx) * wy * wz * (double)__ldg(row + xs);
-                    }
-                }
+            const float fx = (float)(gx - fx0), fy = (float)(gy - fy0), fz = (float)(gz - fz0);
+            // source voxel of the base tap and the +1 steps along each axis
+            const int xs0 = x0 + sx, ys0 = y0 + sy, zs0 = z0 + sz;
+            long long o0;
+            int dx, dy, dz;
+            if (BRICK) {
+                o0 = brick_offset(xs0, ys0, zs0, n >> 2);
+                dx = (xs0 & 3) != 3 ? 1 : 61;
+                dy = (ys0 & 3) != 3 ? 4 : (n >> 2) * 64 - 12;
+                dz = (zs0 & 3) != 3 ? 16 : (n >> 2) * (n >> 2) * 64 - 48;
+            } else {
+                o0 = ((long long)zs0 * n + ys0) * n + xs0;
+                dx = 1;
+                dy = n;
+                dz = n * n;
             }
-            samp[s] = (float)val;
+            // a tap contributes when it lies in the window grid and its source in the volume
+            const bool vx0 = (unsigned)x0 < (unsigned)n && (unsigned)xs0 < (unsigned)n;
+            const bool vx1 = (unsigned)(x0 + 1) < (unsigned)n && (unsigned)(xs0 + 1) < (unsigned)n;
+            const bool vy0 = (unsigned)y0 < (unsigned)n && (unsigned)ys0 < (unsigned)n;
+            const bool vy1 = (unsigned)(y0 + 1) < (unsigned)n && (unsigned)(ys0 + 1) < (unsigned)n;
+            const bool vz0 = (unsigned)z0 < (unsigned)n && (unsigned)zs0 < (unsigned)n;
+            const bool vz1 = (unsigned)(z0 + 1) < (unsigned)n && (unsigned)(zs0 + 1) < (unsigned)n;
+            float val = 0.0f;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {  // (y, z) rows of the footprint
+                const int b = c & 1, a = c >> 1;
+                if (!(b ? vy1 : vy0) || !(a ? vz1 : vz0)) continue;
+                const long long orow = o0 + (b ? dy : 0) + (a ? dz : 0);
+                const float v0 = vx0 ? __ldg(v + orow) : 0.0f;
+                const float v1 = vx1 ? __ldg(v + orow + dx) : 0.0f;
+                const float wyz = (b ? fy : 1.0f - fy) * (a ? fz : 1.0f - fz);
+                val = fmaf(wyz, fmaf(fx, v1 - v0, v0), val);
+            }
+            samp[s] = val;
         }
         __syncthreads();
         // 2. phi-DFT: F[t][m] = sum_p f[t][p] e^{-2 pi i m p / n_phi}, folded
@@ -166,13 +197,24 @@ __global__ void __launch_bounds__(kThreads) expand_factored_kernel(FactoredTable
 
 size_t factored_smem_bytes(const FactoredTables& T) { return smem_plan(T).total; }
 
-int launch_expand_factored(const FactoredTables& T, const float* vols, long long vol_stride, const int* win_vol,
-                           const int* win_shift, int n_win, float* out, int ldo, cudaStream_t s) {
+void launch_to_bricks(const float* in, long long in_stride, int count, float* out, int n, cudaStream_t s) {
+    if (count <= 0) return;
+    dim3 grid((n * n * n + 1023) / 1024, count);
+    to_bricks_kernel<<<grid, 256, 0, s>>>(in, in_stride, out, n);
+}
+
+int launch_expand_factored(const FactoredTables& T, const float* vols, long long vol_stride, bool bricked,
+                           const int* win_vol, const int* win_shift, int n_win, float* out, int ldo, cudaStream_t s) {
     if (n_win <= 0) return 0;
     const size_t smem = factored_smem_bytes(T);
     if (smem > 220 * 1024) return 1;
-    cudaFuncSetAttribute(expand_factored_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    expand_factored_kernel<<<n_win, kThreads, smem, s>>>(T, vols, vol_stride, win_vol, win_shift, out, ldo);
+    if (bricked) {
+        cudaFuncSetAttribute(expand_factored_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        expand_factored_kernel<true><<<n_win, kThreads, smem, s>>>(T, vols, vol_stride, win_vol, win_shift, out, ldo);
+    } else {
+        cudaFuncSetAttribute(expand_factored_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        expand_factored_kernel<false><<<n_win, kThreads, smem, s>>>(T, vols, vol_stride, win_vol, win_shift, out, ldo);
+    }
     return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }
 

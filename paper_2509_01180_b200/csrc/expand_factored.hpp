@@ -23,7 +23,10 @@ struct FactoredTables {
 size_t factored_smem_bytes(const FactoredTables& T);
 // coefficients of windows (volume win_vol[w] shifted by win_shift[3w..3w+2]) into
 // out[w * ldo + row], real-packed FP32 rows
-int launch_expand_factored(const FactoredTables& T, const float* vols, long long vol_stride, const int* win_vol,
-                           const int* win_shift, int n_win, float* out, int ldo, cudaStream_t s);
+// vols: raster (x fastest) or, bricked = true, the 4x4x4-brick layout of launch_to_bricks
+int launch_expand_factored(const FactoredTables& T, const float* vols, long long vol_stride, bool bricked,
+                           const int* win_vol, const int* win_shift, int n_win, float* out, int ldo, cudaStream_t s);
+// raster volumes (in_stride apart) -> 4x4x4 bricks (n % 4 == 0), n^3 apart
+void launch_to_bricks(const float* in, long long in_stride, int count, float* out, int n, cudaStream_t s);
 
 }  // namespace bmb

@@ -42,6 +42,7 @@ struct WarpScratch {
     float cp[2 * kMaxL + 3];
     float sp[2 * kMaxL + 3];
     double res[20];     // reduced (value, grad[3], hess aa ab ag bb bg gg) x (corr, wedge)
+    double red[32];     // reduce-scatter staging (first scratch set of a warp)
     double cs_half[8];  // cos, sin of beta/2, beta, alpha, gamma
 };
 
@@ -53,6 +54,39 @@ __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
 }
 
 __host__ __device__ __forceinline__ int xi_off(int l) { return l * (2 * l - 1) * (2 * l + 1) / 3; }
+
+// Sum NT per-lane values over the warp and publish sum i to out[i] (shared
+// memory): recursive-halving reduce-scatter (P - 1 FP64 shuffles for P = next
+// power of two >= NT, then plain butterfly rounds) instead of NT butterflies.
+template <int NT>
+__device__ __forceinline__ void warp_reduce_publish(double (&v)[NT], double* out) {
+    constexpr int P = NT <= 1 ? 1 : NT <= 2 ? 2 : NT <= 4 ? 4 : NT <= 8 ? 8 : NT <= 16 ? 16 : 32;
+    static_assert(NT <= 32, "reduce-scatter over at most 32 values");
+    constexpr int LOGP = P == 1 ? 0 : P == 2 ? 1 : P == 4 ? 2 : P == 8 ? 3 : P == 16 ? 4 : 5;
+    const int lane = threadIdx.x & 31;
+    double w[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) w[i] = i < NT ? v[i] : 0.0;
+#pragma unroll
+    for (int r = 0; r < LOGP; ++r) {
+        const int off = 16 >> r;
+        const int half = P >> (r + 1);
+        const bool low = (lane & off) == 0;
+#pragma unroll
+        for (int j = 0; j < half; ++j) {
+            const double mine = low ? w[j] : w[j + half];
+            const double send = low ? w[j + half] : w[j];
+            w[j] = mine + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+    }
+#pragma unroll
+    for (int r = LOGP; r < 5; ++r) w[0] += __shfl_xor_sync(0xffffffffu, w[0], 16 >> r);
+    // lanes whose top LOGP bits equal i hold sum i
+    int idx = 0;
+#pragma unroll
+    for (int r = 0; r < LOGP; ++r) idx = (idx << 1) | ((lane >> (4 - r)) & 1);
+    if ((lane & ((32 >> LOGP) - 1)) == 0 && idx < NT) out[idx] = w[0];
+}
 
 // One evaluation job: correlation kernel, wedge-power kernel (null: no wedge)
 // and the ZYZ angles.
@@ -73,11 +107,10 @@ __device__ __forceinline__ float2 cmul_x(float2 a, float2 b) {
 // sweep) — the correlation and, when wx != null, the wedge-power kernel at the
 // same angles.  Warp-cooperative; results in ws[k].res.  Each table load (the
 // recursion coefficients and both kernels) feeds K recursion chains per lane.
-template <int ORDER, int K>
+template <int ORDER, int K, bool WEDGE>
 __device__ __forceinline__ void warp_eval_k(const BandTables& T, const EvalJob (&job)[K], WarpScratch* ws) {
     const float2* __restrict__ xi = job[0].xi;
     const float2* __restrict__ wx = job[0].wx;
-    const bool WEDGE = wx != nullptr;
     const int lane = threadIdx.x & 31;
     const int L = T.L;
     __syncwarp();
@@ -162,8 +195,11 @@ __device__ __forceinline__ void warp_eval_k(const BandTables& T, const EvalJob (
         const float bf = T.bfac[item];
         float d[K], dp[K], dpp[K], d1[K], dp1[K], dpp1[K];
         float2 A0[K], A1[K], A2[K], W0[K], W1[K], W2[K];
-        const float2 x0 = xi[r0 * 32 + lane];
-        const float2 w0 = WEDGE ? wx[r0 * 32 + lane] : make_float2(0.f, 0.f);
+        const float4* __restrict__ pq = T.PQR + r0 * 32 + lane;
+        const float2* __restrict__ xr = xi + r0 * 32 + lane;
+        const float2* __restrict__ wr = WEDGE ? wx + r0 * 32 + lane : nullptr;
+        const float2 x0 = xr[0];
+        const float2 w0 = WEDGE ? wr[0] : make_float2(0.f, 0.f);
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             // closed-form border at l0 (cs_power, steer.cpp:19-31)
@@ -191,11 +227,10 @@ __device__ __forceinline__ void warp_eval_k(const BandTables& T, const EvalJob (
         }
 #pragma unroll 2
         for (int s = 1; s < glen; ++s) {
-            const int at = (r0 + s) * 32 + lane;
-            const float4 pqr = __ldg(T.PQR + at);
+            const float4 pqr = __ldg(pq + s * 32);
             const float P = pqr.x, Q = pqr.y, R = pqr.z;
-            const float2 x = xi[at];
-            const float2 w = WEDGE ? wx[at] : make_float2(0.f, 0.f);
+            const float2 x = xr[s * 32];
+            const float2 w = WEDGE ? wr[s * 32] : make_float2(0.f, 0.f);
 #pragma unroll
             for (int k = 0; k < K; ++k) {
                 // three-term recursion (steer.cpp:101-141): t1 = P cos b + Q, t2 = R
@@ -280,27 +315,45 @@ __device__ __forceinline__ void warp_eval_k(const BandTables& T, const EvalJob (
     }
     // cross-lane reduction in FP64 (one interleaved butterfly for all values),
     // published through shared memory
-    constexpr int NT = 2 * NV * K;
+    constexpr int NW = WEDGE ? 2 : 1;
+    constexpr int NT = NW * NV * K;
     double v[NT];
 #pragma unroll
     for (int k = 0; k < K; ++k)
 #pragma unroll
         for (int i = 0; i < NV; ++i) {
-            v[2 * NV * k + i] = acc[k][i];
-            v[2 * NV * k + NV + i] = accw[k][i];
+            v[NW * NV * k + i] = acc[k][i];
+            if (WEDGE) v[NW * NV * k + (NW - 1) * NV + i] = accw[k][i];
         }
+    if constexpr (NT <= 32) {
+        double* red = ws[0].red;  // reduced sums, then scattered to the per-job results
+        warp_reduce_publish<NT>(v, red);
+        __syncwarp();
+        if (lane < K * NV) {
+            const int k = lane / NV, i = lane % NV;
+            const double c = red[NW * NV * k + i];
+            const double wv = WEDGE ? red[NW * NV * k + (NW - 1) * NV + i] : 0.0;
 #pragma unroll
-    for (int o = 16; o; o >>= 1)
+            for (int kk = 0; kk < K; ++kk)
+                if (kk == k) {
+                    ws[kk].res[i] = c;
+                    ws[kk].res[10 + i] = wv;
+                }
+        }
+    } else {
 #pragma unroll
-        for (int i = 0; i < NT; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
-    if (lane == 0) {
+        for (int o = 16; o; o >>= 1)
 #pragma unroll
-        for (int k = 0; k < K; ++k)
+            for (int i = 0; i < NT; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
+        if (lane == 0) {
 #pragma unroll
-            for (int i = 0; i < NV; ++i) {
-                ws[k].res[i] = v[2 * NV * k + i];
-                ws[k].res[10 + i] = WEDGE ? v[2 * NV * k + NV + i] : 0.0;
-            }
+            for (int k = 0; k < K; ++k)
+#pragma unroll
+                for (int i = 0; i < NV; ++i) {
+                    ws[k].res[i] = v[NW * NV * k + i];
+                    ws[k].res[10 + i] = WEDGE ? v[NW * NV * k + (NW - 1) * NV + i] : 0.0;
+                }
+        }
     }
     __syncwarp();
 }
@@ -698,18 +751,18 @@ struct EvalShape {
 
 // K jobs of one warp: one K-way evaluation when they share their kernels,
 // else one after the other
-template <int ORDER, int K>
+template <int ORDER, int K, bool WEDGE>
 __device__ __forceinline__ void eval_group(const BandTables& T, const EvalJob (&job)[K], WarpScratch* ws) {
     bool same = true;
 #pragma unroll
     for (int k = 1; k < K; ++k) same &= job[k].xi == job[0].xi && job[k].wx == job[0].wx;
     if (K == 1 || same) {
-        warp_eval_k<ORDER, K>(T, job, ws);
+        warp_eval_k<ORDER, K, WEDGE>(T, job, ws);
     } else {
 #pragma unroll 1
         for (int k = 0; k < K; ++k) {
             const EvalJob one[1] = {job[k]};
-            warp_eval_k<ORDER, 1>(T, one, ws + k);
+            warp_eval_k<ORDER, 1, WEDGE>(T, one, ws + k);
         }
     }
 }
@@ -745,7 +798,8 @@ __global__ void __launch_bounds__(EvalShape<K>::WARPS * 32) eval_kernel(StageArg
         job[k].a = e[0], job[k].b = e[1], job[k].g = e[2];
     }
     WarpScratch* ws = wsc + warp * K;
-    eval_group<ORDER, K>(a.T, job, ws);
+    if (wedge) eval_group<ORDER, K, true>(a.T, job, ws);
+    else eval_group<ORDER, K, false>(a.T, job, ws);
     constexpr int NV = ORDER == 0 ? 1 : 10;
 #pragma unroll
     for (int k = 0; k < K; ++k)
@@ -919,7 +973,7 @@ __global__ void __launch_bounds__(EvalShape<K>::WARPS * 32) eval_sweep_kernel(Ev
             const double* e = a.euler + 3 * gi;
             job[k].a = e[0], job[k].b = e[1], job[k].g = e[2];
         }
-        eval_group<ORDER, K>(a.T, job, ws);
+        eval_group<ORDER, K, false>(a.T, job, ws);
         if (lane < K && u0 + lane < total) {
             const double* r = ws[lane].res;
             double* o = a.out + 4 * (u0 + lane);
