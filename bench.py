@@ -72,60 +72,59 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled through NVML (in-process thread, every
+    200 ms) during the timed region; nvidia-smi in a loop was intrusive there."""
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4}
 
     def __init__(self, device):
         self.device = device
-        self.proc = None
-        self.path = None
+        self.samples = []
+        self.stop = None
+        self.thread = None
 
     def __enter__(self):
+        import threading
         try:
-            fd, self.path = tempfile.mkstemp(suffix=".csv")
-            os.close(fd)
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200", "-f", self.path],
-                stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+            import pynvml
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[self.device]) if vis else self.device
+            h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
         except Exception:
-            self.proc = None
+            return self
+        self.stop = threading.Event()
+
+        def run():
+            while not self.stop.is_set():
+                try:
+                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.samples.append((sm, rs))
+                except Exception:
+                    pass
+                self.stop.wait(0.2)
+
+        self.thread = threading.Thread(target=run, daemon=True)
+        self.thread.start()
         return self
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        if self.thread:
+            self.stop.set()
+            self.thread.join(timeout=2)
 
     def summary(self):
-        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": []}
-        try:
-            rows = [r.split(",") for r in Path(self.path).read_text().strip().splitlines() if r.strip()]
-        except Exception:
+        out = {"sm_mhz": None, "sm_max_mhz": getattr(self, "max_mhz", None), "reasons": [],
+               "samples": len(self.samples), "source": "nvml"}
+        if not self.samples:
             return out
-        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].strip().replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].strip().replace(".", "").isdigit()]
-        if sm:
-            loaded = [x for x in sm if x > 0.5 * max(sm)] or sm
-            out["sm_mhz"] = statistics.median(loaded)
-        if mx:
-            out["sm_max_mhz"] = max(mx)
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        for r in rows:
-            if len(r) < 9:
-                continue
-            for i, nm in enumerate(names):
-                if "Active" in r[5 + i] and "Not" not in r[5 + i]:
-                    reasons.add(nm)
-        out["reasons"] = sorted(reasons)
-        out["samples"] = len(rows)
+        sm = [x for x, _ in self.samples]
+        loaded = [x for x in sm if x > 0.5 * max(sm)] or sm
+        out["sm_mhz"] = statistics.median(loaded)
+        out["reasons"] = sorted(nm for nm, bit in self.REASONS.items() if any(r & bit for _, r in self.samples))
         return out
 
 
@@ -243,14 +242,21 @@ def run_product(args):
     ctx.set_timing(False)
     ctx.timings(reset=True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    host_ms = []
     with ClockSampler(local) as clk:
         barrier()
         e0.record()
-        for _ in range(args.steps):
+        marks[0].record()
+        for i in range(args.steps):
+            h0 = time.perf_counter()
             res = step(parts)
+            marks[i + 1].record()
+            host_ms.append((time.perf_counter() - h0) * 1e3)
         e1.record()
         barrier()
     ms = e0.elapsed_time(e1) / args.steps
+    step_ms = [marks[i].elapsed_time(marks[i + 1]) for i in range(args.steps)]
     _, counts_timed = ctx.timings(reset=True)  # launch counts of the timed region
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -366,6 +372,7 @@ def run_product(args):
         "e2e": {"value": P * world / (e2e_ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
         "gpu_launches": counts_timed["launches"],
+        "step_ms": [round(x, 1) for x in step_ms], "host_step_ms": [round(x, 1) for x in host_ms],
         "clocks": clk.summary(),
         "accuracy_vs_truth": {"shift_exact": f"{shift_ok}/{P}",
                               "rot_err_deg_median": float(np.median(errs)),

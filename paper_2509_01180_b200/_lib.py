@@ -6,11 +6,13 @@ CUDA device is absent, calls raise instead of degrading silently.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import re
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "libballmatch_b200.so"
+# BMB_LIB: alternative build of the same library (variant experiments, tools/build_variant.py)
+LIB_PATH = Path(os.environ["BMB_LIB"]) if os.environ.get("BMB_LIB") else PKG / "libballmatch_b200.so"
 HEADER = PKG.parent / "include" / "ballmatch_b200.h"
 
 _lib = None

@@ -224,8 +224,7 @@ void Context::refine_windows(int nw, int maxc, const AlignConfig& cfg, const Qua
     int* d_counts = counters_.as<int>();  // CNT_L2, CNT_COMP, CNT_T0, CNT_T1
     int* d_pool = d_counts + 4;
     int* d_over = d_counts + 5;
-    int* h_active = nullptr;
-    cudaMallocHost(&h_active, sizeof(int) * 4);
+    int* h_active = pinned_counts();
     const bool wedge = wedge_active();
     // window kernels of the largest band plus one anchored-chart slot per seeded
     // candidate (correlation + wedge kernel) share a memory budget; chunk
@@ -392,7 +391,6 @@ void Context::refine_windows(int nw, int maxc, const AlignConfig& cfg, const Qua
         launch_window_reduce(ra, stream);
         ++timer.launches;
     }
-    cudaFreeHost(h_active);
 }
 
 std::vector<WindowOutcome> Context::run_windows(const float* vols, int n_vol, const std::vector<int>& wvol,

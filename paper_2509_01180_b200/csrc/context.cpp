@@ -132,6 +132,7 @@ void Context::build_factored_tables() {
 Context::~Context() {
     cudaSetDevice(device);
     wedge.reset();
+    if (pinned_) cudaFreeHost(pinned_);
     if (stream) {
         cudaStreamSynchronize(stream);
         cudaStreamDestroy(stream);

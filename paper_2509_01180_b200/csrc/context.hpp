@@ -203,6 +203,13 @@ public:
     DevBuf work_f, work_xi, filtered;
 
     bool debug_iters_ = std::getenv("BMB_DEBUG_ITERS") != nullptr;
+    // pinned host words for the per-iteration list counts (allocated once:
+    // cudaMallocHost / cudaFreeHost per call stall the host unpredictably)
+    int* pinned_ = nullptr;
+    int* pinned_counts() {
+        if (!pinned_ && cudaMallocHost(&pinned_, sizeof(int) * 16) != cudaSuccess) throw std::bad_alloc();
+        return pinned_;
+    }
     DevBuf seed_scratch_;                   // seed xi when it does not fit in shared memory
     DevBuf eval_stats_;                     // [kMaxL+1][order 0/2][wedge 0/1] evaluation counts
     static constexpr size_t kEvalStats = (size_t)(kMaxL + 1) * 4;

@@ -96,6 +96,33 @@ struct EvalJob {
     double a, b, g;
 };
 
+// load-latency options of the evaluation (bit 0: refinement order 0, bit 1:
+// refinement order 2, bit 2: sweep): L1 prefetch of the next group's kernel
+// rows, and loads software-pipelined one chain step ahead
+#ifndef BMB_PF_MASK
+#define BMB_PF_MASK 3
+#endif
+#ifndef BMB_PIPE_MASK
+#define BMB_PIPE_MASK 2
+#endif
+template <int ORDER, bool SWEEP>
+struct EvalOpts {
+    static constexpr int bit = SWEEP ? 4 : (ORDER == 2 ? 2 : 1);
+    static constexpr bool PF = (BMB_PF_MASK & bit) != 0;
+    static constexpr bool PIPE = (BMB_PIPE_MASK & bit) != 0;
+};
+
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+// warp-cooperative L1 prefetch of the contiguous rows [r0, r1) of a band-layout
+// kernel (256 B per row): one 128-byte line per lane and pass
+__device__ __forceinline__ void prefetch_rows(const float2* k, int r0, int r1, int lane) {
+    const char* base = reinterpret_cast<const char*>(k + (size_t)r0 * 32);
+    const int bytes = (r1 - r0) * 256;
+    for (int off = lane * 128; off < bytes; off += 32 * 128) prefetch_l1(base + off);
+}
+
 // products with explicit rounding so that every evaluation runs the identical
 // FP32 sequence whichever slot k of a K-way warp it occupies
 __device__ __forceinline__ float2 cmul_x(float2 a, float2 b) {
@@ -107,12 +134,18 @@ __device__ __forceinline__ float2 cmul_x(float2 a, float2 b) {
 // sweep) — the correlation and, when wx != null, the wedge-power kernel at the
 // same angles.  Warp-cooperative; results in ws[k].res.  Each table load (the
 // recursion coefficients and both kernels) feeds K recursion chains per lane.
-template <int ORDER, int K, bool WEDGE>
+template <int ORDER, int K, bool WEDGE, bool PF = false, bool PIPE = false>
 __device__ __forceinline__ void warp_eval_k(const BandTables& T, const EvalJob (&job)[K], WarpScratch* ws) {
     const float2* __restrict__ xi = job[0].xi;
     const float2* __restrict__ wx = job[0].wx;
     const int lane = threadIdx.x & 31;
     const int L = T.L;
+    // the kernels are streamed once per evaluation: group g+1's rows are pulled
+    // into L1 while group g runs (L2 latency off the recursion's critical path)
+    if (PF && T.n_groups > 0) {
+        prefetch_rows(xi, T.row_off[0], T.row_off[1], lane);
+        if (WEDGE) prefetch_rows(wx, T.row_off[0], T.row_off[1], lane);
+    }
     __syncwarp();
     // four FP64 sincos per job on lanes 4k..4k+3 (beta/2, beta, alpha, gamma);
     // the phases e^{-i m alpha}, e^{-i m gamma} are binary powers of the bases
@@ -190,6 +223,11 @@ __device__ __forceinline__ void warp_eval_k(const BandTables& T, const EvalJob (
         const int m = mm.x, mp = mm.y;
         const int r0 = T.row_off[g];
         const int glen = T.row_off[g + 1] - r0;
+        if (PF && g + 1 < T.n_groups) {
+            const int n0 = T.row_off[g + 1], n1 = T.row_off[g + 2];
+            prefetch_rows(xi, n0, n1, lane);
+            if (WEDGE) prefetch_rows(wx, n0, n1, lane);
+        }
         const int be = T.bexp[item];
         const int ea = be & 0xff, ep = be >> 8;
         const float bf = T.bfac[item];
@@ -225,12 +263,29 @@ __device__ __forceinline__ void warp_eval_k(const BandTables& T, const EvalJob (
             W1[k] = make_float2(__fmul_rn(w0.x, dp[k]), __fmul_rn(w0.y, dp[k]));
             W2[k] = make_float2(__fmul_rn(w0.x, dpp[k]), __fmul_rn(w0.y, dpp[k]));
         }
+        // optionally software-pipelined one step ahead
+        float4 pqn = (PIPE && glen > 1) ? __ldg(pq + 32) : make_float4(0.f, 0.f, 0.f, 0.f);
+        float2 xn = (PIPE && glen > 1) ? xr[32] : make_float2(0.f, 0.f);
+        float2 wn = (PIPE && WEDGE && glen > 1) ? wr[32] : make_float2(0.f, 0.f);
 #pragma unroll 2
         for (int s = 1; s < glen; ++s) {
-            const float4 pqr = __ldg(pq + s * 32);
+            float4 pqr;
+            float2 x, w;
+            if (PIPE) {
+                pqr = pqn;
+                x = xn;
+                w = wn;
+                if (s + 1 < glen) {
+                    pqn = __ldg(pq + (s + 1) * 32);
+                    xn = xr[(s + 1) * 32];
+                    if (WEDGE) wn = wr[(s + 1) * 32];
+                }
+            } else {
+                pqr = __ldg(pq + s * 32);
+                x = xr[s * 32];
+                w = WEDGE ? wr[s * 32] : make_float2(0.f, 0.f);
+            }
             const float P = pqr.x, Q = pqr.y, R = pqr.z;
-            const float2 x = xr[s * 32];
-            const float2 w = WEDGE ? wr[s * 32] : make_float2(0.f, 0.f);
 #pragma unroll
             for (int k = 0; k < K; ++k) {
                 // three-term recursion (steer.cpp:101-141): t1 = P cos b + Q, t2 = R
@@ -751,18 +806,19 @@ struct EvalShape {
 
 // K jobs of one warp: one K-way evaluation when they share their kernels,
 // else one after the other
-template <int ORDER, int K, bool WEDGE>
+template <int ORDER, int K, bool WEDGE, bool SWEEP>
 __device__ __forceinline__ void eval_group(const BandTables& T, const EvalJob (&job)[K], WarpScratch* ws) {
+    using O = EvalOpts<ORDER, SWEEP>;
     bool same = true;
 #pragma unroll
     for (int k = 1; k < K; ++k) same &= job[k].xi == job[0].xi && job[k].wx == job[0].wx;
     if (K == 1 || same) {
-        warp_eval_k<ORDER, K, WEDGE>(T, job, ws);
+        warp_eval_k<ORDER, K, WEDGE, O::PF, O::PIPE>(T, job, ws);
     } else {
 #pragma unroll 1
         for (int k = 0; k < K; ++k) {
             const EvalJob one[1] = {job[k]};
-            warp_eval_k<ORDER, 1, WEDGE>(T, one, ws + k);
+            warp_eval_k<ORDER, 1, WEDGE, O::PF, O::PIPE>(T, one, ws + k);
         }
     }
 }
@@ -798,8 +854,8 @@ __global__ void __launch_bounds__(EvalShape<K>::WARPS * 32) eval_kernel(StageArg
         job[k].a = e[0], job[k].b = e[1], job[k].g = e[2];
     }
     WarpScratch* ws = wsc + warp * K;
-    if (wedge) eval_group<ORDER, K, true>(a.T, job, ws);
-    else eval_group<ORDER, K, false>(a.T, job, ws);
+    if (wedge) eval_group<ORDER, K, true, false>(a.T, job, ws);
+    else eval_group<ORDER, K, false, false>(a.T, job, ws);
     constexpr int NV = ORDER == 0 ? 1 : 10;
 #pragma unroll
     for (int k = 0; k < K; ++k)
@@ -973,7 +1029,7 @@ __global__ void __launch_bounds__(EvalShape<K>::WARPS * 32) eval_sweep_kernel(Ev
             const double* e = a.euler + 3 * gi;
             job[k].a = e[0], job[k].b = e[1], job[k].g = e[2];
         }
-        eval_group<ORDER, K, false>(a.T, job, ws);
+        eval_group<ORDER, K, false, true>(a.T, job, ws);
         if (lane < K && u0 + lane < total) {
             const double* r = ws[lane].res;
             double* o = a.out + 4 * (u0 + lane);
