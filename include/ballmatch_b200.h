@@ -158,10 +158,11 @@ int bm_average_accumulate(bm_context* ctx, const float* particles, int count,
                           const bm_align_result* results, double* sum, void* stream);
 
 /* Kernel timing evidence: with timing on, CUDA events on the context stream
- * bracket every launch of this library.  out_ms[0..11]: gather, split GEMM,
- * seed, refine, wedge filter, misc, refine by band position 0, 1, 2, 3+, the
- * order-2 and order-0 evaluation launches inside refine (milliseconds,
- * accumulated since reset);
+ * bracket every launch of this library.  out_ms[0..14]: gather, expansion,
+ * seed, refine, wedge filter, misc, refine by band position 0, 1, 2, 3+, and
+ * inside refine: order-2 evaluations, order-0 evaluations, chart-kernel
+ * composition, Newton bookkeeping (iteration start, step, acceptance), window
+ * kernel build (milliseconds, accumulated since reset);
  * out_counts[0..3]: kernels launched, windows expanded, GEMM launches,
  * refine launches.  reset != 0 clears after reading. */
 int bm_context_set_timing(bm_context* ctx, int on);

@@ -263,11 +263,12 @@ class Context:
         return ev[0], ev[1], fl.value
 
     def timings(self, reset: bool = False):
-        ms = (C.c_double * 12)()
+        ms = (C.c_double * 15)()
         cnt = (C.c_longlong * 4)()
         _lib.check(_lib.lib().bm_context_timings(self._h, ms, cnt, 1 if reset else 0), "timings")
         names = ("gather", "expand", "seed", "refine", "wedge", "misc", "refine_band0",
-                 "refine_band1", "refine_band2", "refine_band3+", "eval_order2", "eval_order0")
+                 "refine_band1", "refine_band2", "refine_band3+", "eval_order2", "eval_order0",
+                 "compose", "newton", "xi_build")
         return (dict(zip(names, ms[:])),
                 dict(launches=cnt[0], windows_expanded=cnt[1], gemm_launches=cnt[2],
                      refine_launches=cnt[3]))

@@ -280,7 +280,9 @@ void Context::refine_windows(int nw, int maxc, const AlignConfig& cfg, const Qua
                 xa.out = xi_win_.as<float2>();
                 cudaEvent_t r0 = timer.begin(stream);
                 cudaEvent_t rb = timer.begin(stream);
+                cudaEvent_t x0 = timer.begin(stream);
                 if (launch_build_xi(xa, stream) != 0) throw std::runtime_error("build_xi launch failed");
+                timer.end(K_XI, x0, stream);
                 ++timer.launches;
                 a.xi_win = xi_win_.as<float2>();
                 a.pool = (int)std::max<long long>(1, chunk_cands);  // a slot for every candidate: no overflow
@@ -326,7 +328,9 @@ void Context::refine_windows(int nw, int maxc, const AlignConfig& cfg, const Qua
                 ++timer.launches;
                 for (int it = 0; it < cfg.newton_max_iter; ++it) {
                     ck(cudaMemsetAsync(d_counts, 0, sizeof(int) * 4, stream), "counts");
+                    cudaEvent_t n2e = timer.begin(stream);
                     launch_iter_begin(a, stream);
+                    timer.end(K_NEWTON, n2e, stream);
                     ++timer.launches;
                     ck(cudaMemcpyAsync(h_active, d_counts, sizeof(int) * 2, cudaMemcpyDeviceToHost, stream),
                        "active");
@@ -338,13 +342,17 @@ void Context::refine_windows(int nw, int maxc, const AlignConfig& cfg, const Qua
                         if (!a.compose_smem)
                             scratch_.reserve(sizeof(float) * (size_t)std::min(nc, 4096) * a.scratch_per_warp);
                         a.scratch = scratch_.as<float>();
+                        cudaEvent_t c0 = timer.begin(stream);
                         launch_compose(a, a.compose_smem ? nc : std::min(nc, 4096), stream);
+                        timer.end(K_COMPOSE, c0, stream);
                         ++timer.launches;
                     }
                     cudaEvent_t e2 = timer.begin(stream);
                     launch_eval(a, 2, a.list2, d_counts + CNT_L2, n2, stream);
                     timer.end(K_EVAL2, e2, stream);
+                    cudaEvent_t n0 = timer.begin(stream);
                     launch_step(a, lt0, d_counts + CNT_T0, n2, stream);
+                    timer.end(K_NEWTON, n0, stream);
                     timer.launches += 2;
                     for (int r = 0; r < 3; ++r) {
                         int* src = (r & 1) ? lt1 : lt0;
@@ -355,7 +363,9 @@ void Context::refine_windows(int nw, int maxc, const AlignConfig& cfg, const Qua
                         launch_eval(a, 0, src, csrc, n2, stream);
                         timer.end(K_EVAL0, e0, stream);
                         ck(cudaMemsetAsync(cdst, 0, sizeof(int), stream), "retry count");
+                        cudaEvent_t n1 = timer.begin(stream);
                         launch_accept(a, src, csrc, dst, cdst, n2, stream);
+                        timer.end(K_NEWTON, n1, stream);
                         timer.launches += 2;
                     }
                 }

@@ -23,7 +23,6 @@ Context::Context(int dev, int n_, int l_max, double lambda_cut) : device(dev), n
     BMB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     basis = host::make_basis(l_max, lambda_cut);
     if (const char* e = std::getenv("BMB_EXPAND")) expand_mode = std::string(e) == "gemm" ? 1 : 0;
-    if (const char* e = std::getenv("BMB_BRICKS")) use_bricks = std::atoi(e) != 0;
     geo.n = n;
     geo.l_max = l_max;
     geo.coeffs = basis.coeffs;
@@ -76,12 +75,17 @@ void Context::ensure_operator() {
 void Context::build_factored_tables() {
     const host::FactorTables ft = host::build_factor_tables(basis);
     const int L = basis.l_max, nr = basis.n_r, nt = basis.n_theta, np = basis.n_phi;
-    std::vector<double> st(nt), cphi(np), sphi(np);
-    for (int t = 0; t < nt; ++t) st[t] = std::sqrt(std::max(0.0, 1.0 - basis.u[t] * basis.u[t]));
-    for (int p = 0; p < np; ++p) {
-        const double phi = 2.0 * host::kPi * p / np;  // build_operator / expand sample points
-        cphi[p] = std::cos(phi);
-        sphi[p] = std::sin(phi);
+    const double h = 0.5 * n;
+    std::vector<double> dirh((size_t)3 * nt * np);
+    for (int t = 0; t < nt; ++t) {
+        const double st = std::sqrt(std::max(0.0, 1.0 - basis.u[t] * basis.u[t]));
+        for (int p = 0; p < np; ++p) {
+            const double phi = 2.0 * host::kPi * p / np;  // the sample points of expand()
+            double* d = dirh.data() + 3 * ((size_t)t * np + p);
+            d[0] = h * st * std::cos(phi);
+            d[1] = h * st * std::sin(phi);
+            d[2] = h * basis.u[t];
+        }
     }
     const int half = np / 2;
     std::vector<float2> tw((size_t)(half + 1) * (L + 1));
@@ -93,23 +97,25 @@ void Context::build_factored_tables() {
     std::vector<int2> tlm(ntri);
     for (int l = 0; l <= L; ++l)
         for (int m = 0; m <= l; ++m) tlm[host::tri(l, m)] = make_int2(l, m);
-    std::vector<float> radial(ft.radial.begin(), ft.radial.end());
-    std::vector<int4> rowmap(geo.coeffs);
+    std::vector<float> radial_t((size_t)nr * ft.pairs);
+    for (int pr = 0; pr < ft.pairs; ++pr)
+        for (int i = 0; i < nr; ++i) radial_t[(size_t)i * ft.pairs + pr] = (float)ft.radial[(size_t)pr * nr + i];
+    if (ft.pairs >= 32768 || (L + 1) * (L + 1) >= 65536) throw std::invalid_argument("basis too large for the factored tables");
+    std::vector<int> rowpack(geo.coeffs);
     for (int l = 0; l <= L; ++l)
         for (int k = 1; k <= basis.radial_count(l); ++k)
             for (int m = 0; m <= l; ++m)
-                for (int part = 0; part < (m ? 2 : 1); ++part)
-                    rowmap[basis.row(l, k, m, part)] = make_int4((int)host::tri(l, m), part, ft.pair_off[l] + k - 1, 0);
+                for (int part = 0; part < (m ? 2 : 1); ++part) {
+                    const int j = m == 0 ? 0 : 2 * m - 1 + part;
+                    rowpack[basis.row(l, k, m, part)] = ((ft.pair_off[l] + k - 1) << 16) | (l * l + j);
+                }
     upload(fx_r, basis.r, stream);
-    upload(fx_st, st, stream);
-    upload(fx_u, basis.u, stream);
-    upload(fx_cphi, cphi, stream);
-    upload(fx_sphi, sphi, stream);
+    upload(fx_dirh, dirh, stream);
     upload(fx_tw, tw, stream);
     upload(fx_ptab, ptab, stream);
     upload(fx_trilm, tlm, stream);
-    upload(fx_radial, radial, stream);
-    upload(fx_rowmap, rowmap, stream);
+    upload(fx_radial, radial_t, stream);
+    upload(fx_rowmap, rowpack, stream);
     fx.n = n;
     fx.L = L;
     fx.nr = nr;
@@ -117,16 +123,14 @@ void Context::build_factored_tables() {
     fx.np = np;
     fx.coeffs = geo.coeffs;
     fx.ntri = ntri;
+    fx.pairs = ft.pairs;
     fx.r = fx_r.as<double>();
-    fx.st = fx_st.as<double>();
-    fx.u = fx_u.as<double>();
-    fx.cphi = fx_cphi.as<double>();
-    fx.sphi = fx_sphi.as<double>();
+    fx.dirh = fx_dirh.as<double>();
     fx.tw = fx_tw.as<float2>();
     fx.ptab = fx_ptab.as<float>();
     fx.tri_lm = fx_trilm.as<int2>();
-    fx.radial = fx_radial.as<float>();
-    fx.rowmap = fx_rowmap.as<int4>();
+    fx.radial_t = fx_radial.as<float>();
+    fx.rowpack = fx_rowmap.as<int>();
 }
 
 Context::~Context() {
@@ -149,18 +153,8 @@ void Context::expand_windows(const float* vols, long long vol_stride, int n_vol,
         upload(win_shift, wshift, stream);
         coef.reserve(sizeof(float) * (size_t)nw * geo.m_pad);
         cudaEvent_t f0 = timer.begin(stream);
-        const float* src = vols;
-        long long stride = vol_stride;
-        const bool bricked = use_bricks && n % 4 == 0;
-        if (bricked) {  // 4x4x4-brick copy of the volumes (gather locality of the trilinear taps)
-            bricks_.reserve(sizeof(float) * (size_t)n_vol * n * n * n);
-            launch_to_bricks(vols, vol_stride, n_vol, bricks_.as<float>(), n, stream);
-            ++timer.launches;
-            src = bricks_.as<float>();
-            stride = (long long)n * n * n;
-        }
-        if (launch_expand_factored(fx, src, stride, bricked, win_vol.as<int>(), win_shift.as<int>(), nw,
-                                   coef.as<float>(), geo.m_pad, stream) != 0)
+        if (launch_expand_factored(fx, vols, vol_stride, win_vol.as<int>(), win_shift.as<int>(), nw, coef.as<float>(),
+                                   geo.m_pad, stream) != 0)
             throw std::runtime_error("factored expansion launch failed");
         ++timer.launches;
         ++timer.gemm_launches;

@@ -101,7 +101,7 @@ struct ParticleResult {
 };
 
 // Per-kernel-class CUDA-event timing on the context stream (bench evidence).
-enum KClass { K_GATHER = 0, K_GEMM, K_SEED, K_REFINE, K_WEDGE, K_MISC, K_REFINE_B0, K_REFINE_B1, K_REFINE_B2, K_REFINE_B3, K_EVAL2, K_EVAL0, K_COUNT };
+enum KClass { K_GATHER = 0, K_GEMM, K_SEED, K_REFINE, K_WEDGE, K_MISC, K_REFINE_B0, K_REFINE_B1, K_REFINE_B2, K_REFINE_B3, K_EVAL2, K_EVAL0, K_COMPOSE, K_NEWTON, K_XI, K_COUNT };
 struct KernelTimer {
     bool on = false;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
@@ -168,12 +168,10 @@ public:
 
     int expand_mode = 0;          // 0: factored expansion (K2f), 1: dense operator GEMM (K1 + K2)
     bool operator_ready = false;
-    bool use_bricks = true;       // factored expansion reads a 4x4x4-brick copy of the volumes
-    DevBuf bricks_;
     void ensure_operator();
     void build_factored_tables();
     FactoredTables fx;
-    DevBuf fx_r, fx_st, fx_u, fx_cphi, fx_sphi, fx_tw, fx_ptab, fx_trilm, fx_radial, fx_rowmap;
+    DevBuf fx_r, fx_dirh, fx_tw, fx_ptab, fx_trilm, fx_radial, fx_rowmap;
     int gemm_block_n = 128;
     int gemm_kchunk = 4;
     long long max_chunk_windows = 8192;  // windows expanded per GEMM chunk

@@ -746,7 +746,9 @@ __global__ void iter_begin_kernel(StageArgs a) {
     }
 }
 
-// one CTA per candidate of the composition list
+// one CTA per candidate of the composition list; SMEM: the temporaries live in
+// shared memory (known address space -> LDS/STS), else in global scratch
+template <bool SMEM>
 __global__ void __launch_bounds__(256) compose_kernel(StageArgs a) {
     extern __shared__ __align__(16) unsigned char sm[];
     __shared__ ComposeScratch cs;
@@ -758,7 +760,7 @@ __global__ void __launch_bounds__(256) compose_kernel(StageArgs a) {
     const bool wedge = a.prm.has_wedge != 0;
     float* dtab;
     float2 *xd, *qt;
-    if (a.compose_smem) {
+    if (SMEM) {
         dtab = reinterpret_cast<float*>(sm);
         xd = reinterpret_cast<float2*>(dtab + ((nxi + 1) & ~1));
         qt = xd + nxi;
@@ -1083,8 +1085,12 @@ void launch_iter_begin(const StageArgs& a, cudaStream_t s) {
 void launch_compose(const StageArgs& a, int n, cudaStream_t s) {
     if (n <= 0) return;
     const size_t smem = a.compose_smem ? compose_smem_bytes(a.T.L) : 0;
-    if (smem) cudaFuncSetAttribute(compose_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    compose_kernel<<<n, 256, smem, s>>>(a);
+    if (smem) {
+        cudaFuncSetAttribute(compose_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        compose_kernel<true><<<n, 256, smem, s>>>(a);
+    } else {
+        compose_kernel<false><<<n, 256, 0, s>>>(a);
+    }
 }
 // jobs per warp in the refinement: 1 (measured fastest: refinement lists mix
 // windows, and one job per warp keeps the most warps in flight); BMB_EVAL_K=2/4

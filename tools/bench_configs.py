@@ -28,14 +28,14 @@ def timed(fn, reps=1):
     return e0.elapsed_time(e1) / reps, out
 
 
-def cfg3(batch=8192):
-    for n in (48, 64):
+def cfg3(batch=8192, ns=(48, 64), Ls=(8, 16, 24)):
+    for n in ns:
         g = torch.Generator(device="cuda").manual_seed(3)
         vols = torch.randn((batch, n, n, n), device="cuda", generator=g)
         c = (torch.arange(n, device="cuda") - n // 2) * (2.0 / n)
         r2 = c[None, None, :] ** 2 + c[None, :, None] ** 2 + c[:, None, None] ** 2
         vols *= (r2 < 1.0).float()
-        for L in (8, 16, 24):
+        for L in Ls:
             ctx = api.Context(n, L, L * math.pi)
             ms, _ = timed(lambda: ctx.expand(vols))
             S = ctx.n_r * ctx.n_theta * ctx.n_phi
@@ -112,6 +112,8 @@ if __name__ == "__main__":
     which = sys.argv[1:] or ["3", "4", "5"]
     if "3" in which:
         cfg3()
+    if "3x" in which:  # one case: 64^3, L = 16 (profiling)
+        cfg3(ns=(64,), Ls=(16,))
     if "4" in which:
         cfg4()
     if "5" in which:

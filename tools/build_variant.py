@@ -10,6 +10,9 @@ sys.path.insert(0, str(ROOT))
 from paper_2509_01180_b200 import build as B  # noqa: E402
 
 
+VARIANT_SOURCES = ("refine.cu", "expand_factored.cu")
+
+
 def main():
     name, defs = sys.argv[1], sys.argv[2:]
     out_dir = ROOT / "build" / "variants"
@@ -19,8 +22,8 @@ def main():
     objs = []
     for src in B.sources():
         obj = B.OBJ / (src.name + ".o")
-        if src.name == "refine.cu":
-            obj = obj_dir / "refine.cu.o"
+        if src.name in VARIANT_SOURCES:
+            obj = obj_dir / (src.name + ".o")
             cmd = [B.NVCC, *B.ARCH, *B.CFLAGS, *defs, "-c", str(src), "-o", str(obj)]
             subprocess.run(cmd, check=True)
         objs.append(str(obj))

@@ -1,0 +1,2 @@
+mkdir -p gpurun_out
+python bench.py --no-cpu-baseline --steps 5 > gpurun_out/bench_r1.json 2> gpurun_out/bench_r1.err
