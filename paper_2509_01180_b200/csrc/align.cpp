@@ -52,12 +52,14 @@ BandTables BandDev::view() const {
     t.rows = rows;
     t.row_off = row_off.as<int>();
     t.item_mm = item_mm.as<char2>();
+    t.item_pm = item_pm.as<char2>();
+    t.item_w = item_w.as<float2>();
     t.item_len = item_len.as<int>();
     t.bfac = bfac.as<float>();
     t.bexp = bexp.as<int>();
     t.PQR = PQR.as<float4>();
-    t.item_of = item_of.as<int16_t>();
-    t.wedge = has_wedge ? wedge.as<float2>() : nullptr;
+    t.item_of = item_of.as<int>();
+    t.wedge = has_wedge ? wedge.as<float4>() : nullptr;
     return t;
 }
 
@@ -80,6 +82,8 @@ BandDev& Context::band(int L) {
     b->rows = h.rows;
     upload(b->row_off, h.row_off, stream);
     upload(b->item_mm, h.item_mm, stream);
+    upload(b->item_pm, h.item_pm, stream);
+    upload(b->item_w, h.item_w, stream);
     upload(b->item_len, h.item_len, stream);
     upload(b->bfac, h.bfac, stream);
     upload(b->bexp, h.bexp, stream);
@@ -231,7 +235,7 @@ void Context::refine_windows(int nw, int maxc, const AlignConfig& cfg, const Qua
     // boundaries follow the actual per-window candidate counts
     const int Lmax_band = cfg.bands.back();
     BandDev& btop = band(Lmax_band);
-    const size_t kernel_bytes = sizeof(float2) * (size_t)btop.rows * 32;
+    const size_t kernel_bytes = sizeof(float4) * (size_t)btop.rows * 32;
     const size_t slot_bytes = kernel_bytes * (wedge ? 2 : 1);
     std::vector<int> ncand(nw);
     ck(cudaMemcpyAsync(ncand.data(), cand_count_.p, sizeof(int) * nw, cudaMemcpyDeviceToHost, stream), "cand counts");
@@ -266,7 +270,7 @@ void Context::refine_windows(int nw, int maxc, const AlignConfig& cfg, const Qua
                 a.T = bd.view();
                 a.row_group = bd.row_group.as<int>();
                 // window kernels of this band
-                xi_win_.reserve(sizeof(float2) * len * cnt);
+                xi_win_.reserve(sizeof(float4) * len * cnt);
                 XiArgs xa;
                 xa.T = a.T;
                 xa.row_group = a.row_group;
@@ -277,20 +281,20 @@ void Context::refine_windows(int nw, int maxc, const AlignConfig& cfg, const Qua
                 xa.block_off = geo.block_off;
                 xa.radial_count = geo.radial_count;
                 xa.n = cnt;
-                xa.out = xi_win_.as<float2>();
+                xa.out = xi_win_.as<float4>();
                 cudaEvent_t r0 = timer.begin(stream);
                 cudaEvent_t rb = timer.begin(stream);
                 cudaEvent_t x0 = timer.begin(stream);
                 if (launch_build_xi(xa, stream) != 0) throw std::runtime_error("build_xi launch failed");
                 timer.end(K_XI, x0, stream);
                 ++timer.launches;
-                a.xi_win = xi_win_.as<float2>();
+                a.xi_win = xi_win_.as<float4>();
                 a.pool = (int)std::max<long long>(1, chunk_cands);  // a slot for every candidate: no overflow
-                xi_pool_.reserve(sizeof(float2) * len * a.pool);
-                a.xi_pool = xi_pool_.as<float2>();
+                xi_pool_.reserve(sizeof(float4) * len * a.pool);
+                a.xi_pool = xi_pool_.as<float4>();
                 if (wedge) {
-                    w_pool_.reserve(sizeof(float2) * len * a.pool);
-                    a.w_pool = w_pool_.as<float2>();
+                    w_pool_.reserve(sizeof(float4) * len * a.pool);
+                    a.w_pool = w_pool_.as<float4>();
                     a.chi_hat = chi_dev.as<double2>();
                     a.q_hat = q_dev.as<double2>();
                     a.wp_total = wp_total;

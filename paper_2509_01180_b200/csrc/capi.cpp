@@ -277,8 +277,8 @@ int bm_eval_sweep(bm_context* ctx, const double* f, int n_f, const double* t, co
         xa.block_off = c.geo.block_off;
         xa.radial_count = c.geo.radial_count;
         xa.n = n_f;
-        c.work_xi.reserve(sizeof(float2) * (size_t)n_f * bd.rows * 32);
-        xa.out = c.work_xi.as<float2>();
+        c.work_xi.reserve(sizeof(float4) * (size_t)n_f * bd.rows * 32);
+        xa.out = c.work_xi.as<float4>();
         if (bmb::launch_build_xi(xa, c.stream) != 0) throw std::runtime_error("build_xi launch failed");
         bmb::EvalArgs ea;
         ea.T = bd.view();

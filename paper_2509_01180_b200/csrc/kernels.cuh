@@ -21,15 +21,16 @@ struct BandTables {
     int n_groups = 0;
     int rows = 0;                    // sum of group lengths
     const int* row_off = nullptr;    // [n_groups + 1]
-    const char2* item_mm = nullptr;  // [n_groups*32] (m, m'); padded lanes (0, 0) with len 0
+    const char2* item_mm = nullptr;  // [n_groups*32] (m, m'), m >= |m'|; padded lanes (0, 0) with len 0
+    const char2* item_pm = nullptr;  // [n_groups*32] half-plane partner (m', m) or (-m', -m)
+    const float2* item_w = nullptr;  // [n_groups*32] (weight of A, sign * weight of B; 0 if self-paired)
     const int* item_len = nullptr;   // [n_groups*32] steps of the item (0 for padding)
     const float* bfac = nullptr;     // [n_groups*32] sign * sqrt_binom of the border closed form
     const int* bexp = nullptr;       // [n_groups*32] packed exponents: a | p << 8 (cos^a sin^p)
     const float4* PQR = nullptr;     // [rows*32] (P, Q, R, 0): t1 = P cos b + Q,
                                      // t1' = -P sin b, t1'' = -P cos b, t2 = R
-    const int16_t* item_of = nullptr;  // [(2L+1)^2]: item index of (m,m') (>=0) or -(idx+1) for
-                                       // the conjugate partner (-m,-m') of a half-plane item
-    const float2* wedge = nullptr;     // [rows*32] wedge-power kernel entries (or null)
+    const int* item_of = nullptr;    // [(2L+1)^2] 2 item + slot of each half-plane entry (m, m'), else -1
+    const float4* wedge = nullptr;   // [rows*32] wedge-power kernel entries (A, B) (or null)
 };
 
 // Per-context constants used by the kernels.

@@ -55,6 +55,101 @@ __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
 
 __host__ __device__ __forceinline__ int xi_off(int l) { return l * (2 * l - 1) * (2 * l + 1) / 3; }
 
+// One evaluation job: correlation kernel, wedge-power kernel (null: no wedge)
+// and the ZYZ angles.
+struct EvalJob {
+    const float4* xi;
+    const float4* wx;
+    double a, b, g;
+};
+
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+// warp-cooperative L1 prefetch of the contiguous rows [r0, r1) of a band-layout
+// kernel (512 B per row): one 128-byte line per lane and pass
+__device__ __forceinline__ void prefetch_rows(const float4* k, int r0, int r1, int lane) {
+    const char* base = reinterpret_cast<const char*>(k + (size_t)r0 * 32);
+    const int bytes = (r1 - r0) * 512;
+    for (int off = lane * 128; off < bytes; off += 32 * 128) prefetch_l1(base + off);
+}
+
+// products with explicit rounding so that every evaluation runs the identical
+// FP32 sequence whichever slot k of a K-way warp it occupies
+__device__ __forceinline__ float2 cmul_x(float2 a, float2 b) {
+    return make_float2(fmaf(a.x, b.x, -__fmul_rn(a.y, b.y)), fmaf(a.x, b.y, __fmul_rn(a.y, b.x)));
+}
+
+// order-dependent accumulators of one (kernel, entry) of a chain
+template <int ORDER>
+struct Chain3 {
+    float2 v0, v1, v2;
+    __device__ __forceinline__ void init(float2 x, float d, float dp, float dpp) {
+        v0 = make_float2(__fmul_rn(x.x, d), __fmul_rn(x.y, d));
+        v1 = make_float2(__fmul_rn(x.x, dp), __fmul_rn(x.y, dp));
+        v2 = make_float2(__fmul_rn(x.x, dpp), __fmul_rn(x.y, dpp));
+    }
+    __device__ __forceinline__ void step(float2 x, float d, float dp, float dpp) {
+        v0.x = fmaf(x.x, d, v0.x);
+        v0.y = fmaf(x.y, d, v0.y);
+        if (ORDER >= 1) {
+            v1.x = fmaf(x.x, dp, v1.x);
+            v1.y = fmaf(x.y, dp, v1.y);
+        }
+        if (ORDER >= 2) {
+            v2.x = fmaf(x.x, dpp, v2.x);
+            v2.y = fmaf(x.y, dpp, v2.y);
+        }
+    }
+};
+
+// C += wgt Re(z(m,m') ch) and its derivatives (alpha: -i m, gamma: -i m', beta: d', d'')
+template <int ORDER, int NV>
+__device__ __forceinline__ void phase_acc(float* ac, const Chain3<ORDER>& ch, float2 z, float wgt, int m, int mp) {
+    const float fm = (float)m, fmp = (float)mp;
+    const float wm = wgt * fm, wmp = wgt * fmp;
+    const float2 v0 = cmul_x(z, ch.v0);
+    ac[0] = fmaf(wgt, v0.x, ac[0]);
+    if (ORDER >= 1) {
+        const float2 v1 = cmul_x(z, ch.v1);
+        ac[NV > 1 ? 1 : 0] = fmaf(wm, v0.y, ac[NV > 1 ? 1 : 0]);
+        ac[NV > 2 ? 2 : 0] = fmaf(wgt, v1.x, ac[NV > 2 ? 2 : 0]);
+        ac[NV > 3 ? 3 : 0] = fmaf(wmp, v0.y, ac[NV > 3 ? 3 : 0]);
+        if (ORDER >= 2) {
+            const float2 v2 = cmul_x(z, ch.v2);
+            ac[NV > 4 ? 4 : 0] = fmaf(-__fmul_rn(wm, fm), v0.x, ac[NV > 4 ? 4 : 0]);
+            ac[NV > 5 ? 5 : 0] = fmaf(wm, v1.y, ac[NV > 5 ? 5 : 0]);
+            ac[NV > 6 ? 6 : 0] = fmaf(-__fmul_rn(wm, fmp), v0.x, ac[NV > 6 ? 6 : 0]);
+            ac[NV > 7 ? 7 : 0] = fmaf(wgt, v2.x, ac[NV > 7 ? 7 : 0]);
+            ac[NV > 8 ? 8 : 0] = fmaf(wmp, v1.y, ac[NV > 8 ? 8 : 0]);
+            ac[NV > 9 ? 9 : 0] = fmaf(-__fmul_rn(wmp, fmp), v0.x, ac[NV > 9 ? 9 : 0]);
+        }
+    }
+}
+
+__device__ __forceinline__ float2 phase_of(const WarpScratch& w, int m, int mp) {
+    float2 pa = w.ua[abs(m)], pg = w.ug[abs(mp)];
+    if (m < 0) pa.y = -pa.y;
+    if (mp < 0) pg.y = -pg.y;
+    return cmul_x(pa, pg);
+}
+
+// load-latency options of the evaluation (bit 0: refinement order 0, bit 1:
+// refinement order 2, bit 2: sweep): L1 prefetch of the next group's kernel
+// rows, and loads software-pipelined one chain step ahead
+#ifndef BMB_PF_MASK
+#define BMB_PF_MASK 3
+#endif
+#ifndef BMB_PIPE_MASK
+#define BMB_PIPE_MASK 0
+#endif
+template <int ORDER, bool SWEEP>
+struct EvalOpts {
+    static constexpr int bit = SWEEP ? 4 : (ORDER == 2 ? 2 : 1);
+    static constexpr bool PF = (BMB_PF_MASK & bit) != 0;
+    static constexpr bool PIPE = (BMB_PIPE_MASK & bit) != 0;
+};
+
 // Sum NT per-lane values over the warp and publish sum i to out[i] (shared
 // memory): recursive-halving reduce-scatter (P - 1 FP64 shuffles for P = next
 // power of two >= NT, then plain butterfly rounds) instead of NT butterflies.
@@ -88,56 +183,17 @@ __device__ __forceinline__ void warp_reduce_publish(double (&v)[NT], double* out
     if ((lane & ((32 >> LOGP) - 1)) == 0 && idx < NT) out[idx] = w[0];
 }
 
-// One evaluation job: correlation kernel, wedge-power kernel (null: no wedge)
-// and the ZYZ angles.
-struct EvalJob {
-    const float2* xi;
-    const float2* wx;
-    double a, b, g;
-};
-
-// load-latency options of the evaluation (bit 0: refinement order 0, bit 1:
-// refinement order 2, bit 2: sweep): L1 prefetch of the next group's kernel
-// rows, and loads software-pipelined one chain step ahead
-#ifndef BMB_PF_MASK
-#define BMB_PF_MASK 3
-#endif
-#ifndef BMB_PIPE_MASK
-#define BMB_PIPE_MASK 2
-#endif
-template <int ORDER, bool SWEEP>
-struct EvalOpts {
-    static constexpr int bit = SWEEP ? 4 : (ORDER == 2 ? 2 : 1);
-    static constexpr bool PF = (BMB_PF_MASK & bit) != 0;
-    static constexpr bool PIPE = (BMB_PIPE_MASK & bit) != 0;
-};
-
-__device__ __forceinline__ void prefetch_l1(const void* p) {
-    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
-}
-// warp-cooperative L1 prefetch of the contiguous rows [r0, r1) of a band-layout
-// kernel (256 B per row): one 128-byte line per lane and pass
-__device__ __forceinline__ void prefetch_rows(const float2* k, int r0, int r1, int lane) {
-    const char* base = reinterpret_cast<const char*>(k + (size_t)r0 * 32);
-    const int bytes = (r1 - r0) * 256;
-    for (int off = lane * 128; off < bytes; off += 32 * 128) prefetch_l1(base + off);
-}
-
-// products with explicit rounding so that every evaluation runs the identical
-// FP32 sequence whichever slot k of a K-way warp it occupies
-__device__ __forceinline__ float2 cmul_x(float2 a, float2 b) {
-    return make_float2(fmaf(a.x, b.x, -__fmul_rn(a.y, b.y)), fmaf(a.x, b.y, __fmul_rn(a.y, b.x)));
-}
-
 // Evaluate K jobs at band T.L that share their kernels (job[k].xi == job[0].xi,
 // job[k].wx == job[0].wx: rotations of one window, or of one particle in the
-// sweep) — the correlation and, when wx != null, the wedge-power kernel at the
-// same angles.  Warp-cooperative; results in ws[k].res.  Each table load (the
-// recursion coefficients and both kernels) feeds K recursion chains per lane.
+// sweep) — the correlation and, when WEDGE, the wedge-power kernel at the same
+// angles.  Warp-cooperative; results in ws[k].res.  Each lane runs the
+// Wigner-d recursion of its items (m, m'), m >= |m'|; one chain feeds both
+// half-plane entries of an item (A and its partner B), and each table load
+// feeds K chains.
 template <int ORDER, int K, bool WEDGE, bool PF = false, bool PIPE = false>
 __device__ __forceinline__ void warp_eval_k(const BandTables& T, const EvalJob (&job)[K], WarpScratch* ws) {
-    const float2* __restrict__ xi = job[0].xi;
-    const float2* __restrict__ wx = job[0].wx;
+    const float4* __restrict__ xi = job[0].xi;
+    const float4* __restrict__ wx = job[0].wx;
     const int lane = threadIdx.x & 31;
     const int L = T.L;
     // the kernels are streamed once per evaluation: group g+1's rows are pulled
@@ -219,8 +275,6 @@ __device__ __forceinline__ void warp_eval_k(const BandTables& T, const EvalJob (
 
     for (int g = 0; g < T.n_groups; ++g) {
         const int item = g * 32 + lane;
-        const char2 mm = T.item_mm[item];
-        const int m = mm.x, mp = mm.y;
         const int r0 = T.row_off[g];
         const int glen = T.row_off[g + 1] - r0;
         if (PF && g + 1 < T.n_groups) {
@@ -232,15 +286,15 @@ __device__ __forceinline__ void warp_eval_k(const BandTables& T, const EvalJob (
         const int ea = be & 0xff, ep = be >> 8;
         const float bf = T.bfac[item];
         float d[K], dp[K], dpp[K], d1[K], dp1[K], dpp1[K];
-        float2 A0[K], A1[K], A2[K], W0[K], W1[K], W2[K];
+        Chain3<ORDER> CA[K], CB[K], WA[K], WB[K];
         const float4* __restrict__ pq = T.PQR + r0 * 32 + lane;
-        const float2* __restrict__ xr = xi + r0 * 32 + lane;
-        const float2* __restrict__ wr = WEDGE ? wx + r0 * 32 + lane : nullptr;
-        const float2 x0 = xr[0];
-        const float2 w0 = WEDGE ? wr[0] : make_float2(0.f, 0.f);
+        const float4* __restrict__ xr = xi + r0 * 32 + lane;
+        const float4* __restrict__ wr = WEDGE ? wx + r0 * 32 + lane : nullptr;
+        const float4 x0 = xr[0];
+        const float4 w0 = WEDGE ? wr[0] : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-            // closed-form border at l0 (cs_power, steer.cpp:19-31)
+            // closed-form border at l0 = m (cs_power, steer.cpp:19-31)
             const float* cp = ws[k].cp;
             const float* sp = ws[k].sp;
             d[k] = __fmul_rn(__fmul_rn(bf, cp[ea]), sp[ep]);
@@ -256,21 +310,20 @@ __device__ __forceinline__ void warp_eval_k(const BandTables& T, const EvalJob (
                 const float mid = __fmul_rn(__fmul_rn(2.0f * ea * ep + ea + ep, cp[ea]), sp[ep]);
                 dpp[k] = __fmul_rn(__fmul_rn(0.25f, bf), __fsub_rn(__fadd_rn(t2b, t2a), mid));
             }
-            A0[k] = make_float2(__fmul_rn(x0.x, d[k]), __fmul_rn(x0.y, d[k]));
-            A1[k] = make_float2(__fmul_rn(x0.x, dp[k]), __fmul_rn(x0.y, dp[k]));
-            A2[k] = make_float2(__fmul_rn(x0.x, dpp[k]), __fmul_rn(x0.y, dpp[k]));
-            W0[k] = make_float2(__fmul_rn(w0.x, d[k]), __fmul_rn(w0.y, d[k]));
-            W1[k] = make_float2(__fmul_rn(w0.x, dp[k]), __fmul_rn(w0.y, dp[k]));
-            W2[k] = make_float2(__fmul_rn(w0.x, dpp[k]), __fmul_rn(w0.y, dpp[k]));
+            CA[k].init(make_float2(x0.x, x0.y), d[k], dp[k], dpp[k]);
+            CB[k].init(make_float2(x0.z, x0.w), d[k], dp[k], dpp[k]);
+            if (WEDGE) {
+                WA[k].init(make_float2(w0.x, w0.y), d[k], dp[k], dpp[k]);
+                WB[k].init(make_float2(w0.z, w0.w), d[k], dp[k], dpp[k]);
+            }
         }
         // optionally software-pipelined one step ahead
         float4 pqn = (PIPE && glen > 1) ? __ldg(pq + 32) : make_float4(0.f, 0.f, 0.f, 0.f);
-        float2 xn = (PIPE && glen > 1) ? xr[32] : make_float2(0.f, 0.f);
-        float2 wn = (PIPE && WEDGE && glen > 1) ? wr[32] : make_float2(0.f, 0.f);
+        float4 xn = (PIPE && glen > 1) ? xr[32] : make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 wn = (PIPE && WEDGE && glen > 1) ? wr[32] : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 2
         for (int s = 1; s < glen; ++s) {
-            float4 pqr;
-            float2 x, w;
+            float4 pqr, x, w;
             if (PIPE) {
                 pqr = pqn;
                 x = xn;
@@ -283,7 +336,7 @@ __device__ __forceinline__ void warp_eval_k(const BandTables& T, const EvalJob (
             } else {
                 pqr = __ldg(pq + s * 32);
                 x = xr[s * 32];
-                w = WEDGE ? wr[s * 32] : make_float2(0.f, 0.f);
+                w = WEDGE ? wr[s * 32] : make_float4(0.f, 0.f, 0.f, 0.f);
             }
             const float P = pqr.x, Q = pqr.y, R = pqr.z;
 #pragma unroll
@@ -310,66 +363,29 @@ __device__ __forceinline__ void warp_eval_k(const BandTables& T, const EvalJob (
                     dpp1[k] = dpp[k];
                     dpp[k] = dppn;
                 }
-                A0[k].x = fmaf(x.x, d[k], A0[k].x);
-                A0[k].y = fmaf(x.y, d[k], A0[k].y);
-                if (ORDER >= 1) {
-                    A1[k].x = fmaf(x.x, dp[k], A1[k].x);
-                    A1[k].y = fmaf(x.y, dp[k], A1[k].y);
-                }
-                if (ORDER >= 2) {
-                    A2[k].x = fmaf(x.x, dpp[k], A2[k].x);
-                    A2[k].y = fmaf(x.y, dpp[k], A2[k].y);
-                }
+                CA[k].step(make_float2(x.x, x.y), d[k], dp[k], dpp[k]);
+                CB[k].step(make_float2(x.z, x.w), d[k], dp[k], dpp[k]);
                 if (WEDGE) {
-                    W0[k].x = fmaf(w.x, d[k], W0[k].x);
-                    W0[k].y = fmaf(w.y, d[k], W0[k].y);
-                    if (ORDER >= 1) {
-                        W1[k].x = fmaf(w.x, dp[k], W1[k].x);
-                        W1[k].y = fmaf(w.y, dp[k], W1[k].y);
-                    }
-                    if (ORDER >= 2) {
-                        W2[k].x = fmaf(w.x, dpp[k], W2[k].x);
-                        W2[k].y = fmaf(w.y, dpp[k], W2[k].y);
-                    }
+                    WA[k].step(make_float2(w.x, w.y), d[k], dp[k], dpp[k]);
+                    WB[k].step(make_float2(w.z, w.w), d[k], dp[k], dpp[k]);
                 }
             }
         }
-        const float wgt = (m == 0 && mp == 0) ? 1.0f : 2.0f;  // half-plane symmetry
-        const float fm = (float)m, fmp = (float)mp;
-        const float wm = wgt * fm, wmp = wgt * fmp;  // exact (wgt is 1 or 2)
+        const char2 mm = T.item_mm[item], pm = T.item_pm[item];
+        const float2 iw = T.item_w[item];  // (weight A, sign * weight B)
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             // phases e^{-i m a} e^{-i m' g}; conj for negative orders
-            float2 pa = ws[k].ua[abs(m)], pg = ws[k].ug[abs(mp)];
-            if (m < 0) pa.y = -pa.y;
-            if (mp < 0) pg.y = -pg.y;
-            const float2 z = cmul_x(pa, pg);
-#pragma unroll
-            for (int part = 0; part < 2; ++part) {
-                if (part == 1 && !WEDGE) break;
-                float* ac = part ? accw[k] : acc[k];
-                const float2 v0 = cmul_x(z, part ? W0[k] : A0[k]);
-                ac[0] = fmaf(wgt, v0.x, ac[0]);
-                if (ORDER >= 1) {
-                    const float2 v1 = cmul_x(z, part ? W1[k] : A1[k]);
-                    ac[NV > 1 ? 1 : 0] = fmaf(wm, v0.y, ac[NV > 1 ? 1 : 0]);
-                    ac[NV > 2 ? 2 : 0] = fmaf(wgt, v1.x, ac[NV > 2 ? 2 : 0]);
-                    ac[NV > 3 ? 3 : 0] = fmaf(wmp, v0.y, ac[NV > 3 ? 3 : 0]);
-                    if (ORDER >= 2) {
-                        const float2 v2 = cmul_x(z, part ? W2[k] : A2[k]);
-                        ac[NV > 4 ? 4 : 0] = fmaf(-__fmul_rn(wm, fm), v0.x, ac[NV > 4 ? 4 : 0]);
-                        ac[NV > 5 ? 5 : 0] = fmaf(wm, v1.y, ac[NV > 5 ? 5 : 0]);
-                        ac[NV > 6 ? 6 : 0] = fmaf(-__fmul_rn(wm, fmp), v0.x, ac[NV > 6 ? 6 : 0]);
-                        ac[NV > 7 ? 7 : 0] = fmaf(wgt, v2.x, ac[NV > 7 ? 7 : 0]);
-                        ac[NV > 8 ? 8 : 0] = fmaf(wmp, v1.y, ac[NV > 8 ? 8 : 0]);
-                        ac[NV > 9 ? 9 : 0] = fmaf(-__fmul_rn(wmp, fmp), v0.x, ac[NV > 9 ? 9 : 0]);
-                    }
-                }
+            const float2 za = phase_of(ws[k], mm.x, mm.y), zb = phase_of(ws[k], pm.x, pm.y);
+            phase_acc<ORDER, NV>(acc[k], CA[k], za, iw.x, mm.x, mm.y);
+            phase_acc<ORDER, NV>(acc[k], CB[k], zb, iw.y, pm.x, pm.y);
+            if (WEDGE) {
+                phase_acc<ORDER, NV>(accw[k], WA[k], za, iw.x, mm.x, mm.y);
+                phase_acc<ORDER, NV>(accw[k], WB[k], zb, iw.y, pm.x, pm.y);
             }
         }
     }
-    // cross-lane reduction in FP64 (one interleaved butterfly for all values),
-    // published through shared memory
+    // cross-lane reduction in FP64, published through shared memory
     constexpr int NW = WEDGE ? 2 : 1;
     constexpr int NT = NW * NV * K;
     double v[NT];
@@ -432,8 +448,8 @@ struct ComposeScratch {
 
 // Block-cooperative composition of one candidate's chart kernels; dtab / xd /
 // qt live in shared memory when they fit (else in global scratch).
-__device__ void compose_block(const BandTables& T, const float2* src, const StageArgs& a, const Quat& anchor,
-                              float* dtab, float2* xd, float2* qt, float2* out, float2* out_w,
+__device__ void compose_block(const BandTables& T, const float4* src, const StageArgs& a, const Quat& anchor,
+                              float* dtab, float2* xd, float2* qt, float4* out, float4* out_w,
                               ComposeScratch& cs) {
     const int tid = threadIdx.x, nt = blockDim.x;
     const int L = T.L;
@@ -469,14 +485,19 @@ __device__ void compose_block(const BandTables& T, const float2* src, const Stag
     }
     __syncthreads();
     const float cb = (float)cos(eb);
-    // full-plane d^l_{m,m'}(b_a): half-plane chains + mirror
+    // full-plane d^l_{m,m'}(b_a): item chains, their partners, and the mirrors
+    // d_{-m,-m'} = (-1)^(m-m') d_{m,m'}
     for (int item = tid; item < T.n_groups * 32; item += nt) {
         const int len = T.item_len[item];
         const int m = T.item_mm[item].x, mp = T.item_mm[item].y;
-        const int l0 = max(abs(m), abs(mp));
+        const int pa = T.item_pm[item].x, pb = T.item_pm[item].y;
+        const float wb = T.item_w[item].y;
+        const float sg = wb < 0.0f ? -1.0f : 1.0f;
+        const bool pair = wb != 0.0f;
         const int be = T.bexp[item];
         float d = T.bfac[item] * cs.cp[be & 0xff] * cs.sp[be >> 8], d1 = 0.0f;
         const float mir = ((m - mp) & 1) ? -1.0f : 1.0f;
+        const float mirp = ((pa - pb) & 1) ? -1.0f : 1.0f;
         const int r0 = T.row_off[item >> 5], lane = item & 31;
         for (int st = 0; st < len; ++st) {
             if (st > 0) {
@@ -485,27 +506,39 @@ __device__ void compose_block(const BandTables& T, const float2* src, const Stag
                 d1 = d;
                 d = dn;
             }
-            const int l = l0 + st, w = 2 * l + 1, o = xi_off(l);
+            const int l = m + st, w = 2 * l + 1, o = xi_off(l);
             dtab[o + (m + l) * w + (mp + l)] = d;
             dtab[o + (-m + l) * w + (-mp + l)] = mir * d;
+            if (pair) {
+                dtab[o + (pa + l) * w + (pb + l)] = sg * d;
+                dtab[o + (-pa + l) * w + (-pb + l)] = mirp * sg * d;
+            }
         }
     }
-    // dense xi'_l[m,n] = xi_l[m,n] e^{-i n g} (both half-planes)
+    // dense xi'_l[m,n] = xi_l[m,n] e^{-i n g} over the full plane: the A and B
+    // entries of every (row, lane) and their conjugate mirrors
+    // xi_{-m,-n} = (-1)^(m+n) conj(xi_{m,n})
     for (int at = tid; at < T.rows * 32; at += nt) {
         const int row = at >> 5, j = at & 31;
         const int g = a.row_group[row];
         const int item = g * 32 + j;
         const int st = row - T.row_off[g];
         if (st >= T.item_len[item]) continue;
-        const int m = T.item_mm[item].x, mp = T.item_mm[item].y;
-        const int l = max(abs(m), abs(mp)) + st, w = 2 * l + 1, o = xi_off(l);
-        const float2 x = src[at];
-        float2 egp = cs.ug[abs(mp)];
-        if (mp < 0) egp.y = -egp.y;
-        xd[o + (m + l) * w + (mp + l)] = cmul(x, egp);
-        const float sg = ((m + mp) & 1) ? -1.0f : 1.0f;
-        const float2 xm = make_float2(sg * x.x, -sg * x.y);  // xi[-m,-m']
-        xd[o + (-m + l) * w + (-mp + l)] = cmul(xm, make_float2(egp.x, -egp.y));
+        const float4 x4 = src[at];
+        const int l = T.item_mm[item].x + st, w = 2 * l + 1, o = xi_off(l);
+#pragma unroll
+        for (int slot = 0; slot < 2; ++slot) {
+            if (slot == 1 && T.item_w[item].y == 0.0f) break;
+            const char2 e = slot ? T.item_pm[item] : T.item_mm[item];
+            const int m = e.x, mp = e.y;
+            const float2 x = slot ? make_float2(x4.z, x4.w) : make_float2(x4.x, x4.y);
+            float2 egp = cs.ug[abs(mp)];
+            if (mp < 0) egp.y = -egp.y;
+            xd[o + (m + l) * w + (mp + l)] = cmul(x, egp);
+            const float sgn = ((m + mp) & 1) ? -1.0f : 1.0f;
+            const float2 xm = make_float2(sgn * x.x, -sgn * x.y);  // xi[-m,-m']
+            xd[o + (-m + l) * w + (-mp + l)] = cmul(xm, make_float2(egp.x, -egp.y));
+        }
     }
     __syncthreads();
     const bool wedge = out_w != nullptr;
@@ -543,49 +576,46 @@ __device__ void compose_block(const BandTables& T, const float2* src, const Stag
         const int item = g * 32 + j;
         const int st = row - T.row_off[g];
         if (st >= T.item_len[item]) {
-            out[at] = make_float2(0.f, 0.f);
-            if (wedge) out_w[at] = make_float2(0.f, 0.f);
+            out[at] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (wedge) out_w[at] = make_float4(0.f, 0.f, 0.f, 0.f);
             continue;
         }
-        const int m = T.item_mm[item].x, mp = T.item_mm[item].y;
-        const int l = max(abs(m), abs(mp)) + st, w = 2 * l + 1, o = xi_off(l);
-        const float2* xr = xd + o + (m + l) * w;
-        const float* dr = dtab + o + (mp + l) * w;
-        float re = 0.0f, im = 0.0f;
-        for (int n = 0; n < w; ++n) {
-            const float2 x = xr[n];
-            const float dv = dr[n];
-            re = fmaf(x.x, dv, re);
-            im = fmaf(x.y, dv, im);
-        }
-        float2 eam = cs.ua[abs(mp)];
-        if (mp < 0) eam.y = -eam.y;
-        out[at] = cmul(eam, make_float2(re, im));
-        if (wedge) {
-            const int am = abs(m);
-            double2 c = a.chi_hat[l * (l + 1) / 2 + am];
-            if (m < 0) {
-                const double sgn = (am & 1) ? -1.0 : 1.0;
-                c = make_double2(sgn * c.x, -sgn * c.y);
+        const int l = T.item_mm[item].x + st, w = 2 * l + 1, o = xi_off(l);
+        float2 r[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        float2 rw[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+        for (int slot = 0; slot < 2; ++slot) {
+            if (slot == 1 && T.item_w[item].y == 0.0f) break;
+            const char2 e = slot ? T.item_pm[item] : T.item_mm[item];
+            const int m = e.x, mp = e.y;  // m >= 0 (half plane)
+            const float2* xrow = xd + o + (m + l) * w;
+            const float* drow = dtab + o + (mp + l) * w;
+            float re = 0.0f, im = 0.0f;
+            for (int n = 0; n < w; ++n) {
+                const float2 x = xrow[n];
+                const float dv = drow[n];
+                re = fmaf(x.x, dv, re);
+                im = fmaf(x.y, dv, im);
             }
-            const float2 qv = qt[l * l + (mp + l)];
-            const float cr = (float)c.x, ci = (float)-c.y;  // conj(chi_lm)
-            out_w[at] = make_float2((cr * qv.x - ci * qv.y) * inv_total, (cr * qv.y + ci * qv.x) * inv_total);
+            float2 eam = cs.ua[abs(mp)];
+            if (mp < 0) eam.y = -eam.y;
+            r[slot] = cmul(eam, make_float2(re, im));
+            if (wedge) {
+                const double2 c = a.chi_hat[l * (l + 1) / 2 + m];
+                const float2 qv = qt[l * l + (mp + l)];
+                const float cr = (float)c.x, ci = (float)-c.y;  // conj(chi_lm)
+                rw[slot] = make_float2((cr * qv.x - ci * qv.y) * inv_total, (cr * qv.y + ci * qv.x) * inv_total);
+            }
         }
+        out[at] = make_float4(r[0].x, r[0].y, r[1].x, r[1].y);
+        if (wedge) out_w[at] = make_float4(rw[0].x, rw[0].y, rw[1].x, rw[1].y);
     }
     __syncthreads();
 }
 
-// xi_l[m,m'] for the table entry (row, lane) from real-packed f and t
-__device__ float2 xi_entry(const BandTables& T, const int* row_group, const float* f,
-                           const float* t, const int* block_off, const int* radial_count,
-                           int row, int lane) {
-    const int g = row_group[row];
-    const int item = g * 32 + lane;
-    const int s = row - T.row_off[g];
-    if (s >= T.item_len[item]) return make_float2(0.f, 0.f);
-    const int m = T.item_mm[item].x, mp = T.item_mm[item].y;
-    const int l = max(abs(m), abs(mp)) + s;
+// xi_l[m,m'] = sum_k conj(f_klm) t_klm' from real-packed f and t
+__device__ float2 xi_value(int l, int m, int mp, const float* f, const float* t, const int* block_off,
+                           const int* radial_count) {
     const int nk = radial_count[l], base = block_off[l];
     const int am = abs(m), amp = abs(mp);
     const float sm = (m < 0 && (am & 1)) ? -1.0f : 1.0f;
@@ -602,6 +632,21 @@ __device__ float2 xi_entry(const BandTables& T, const int* row_group, const floa
         im = fmaf(fre, tim, fmaf(-fim, tre, im));
     }
     return make_float2(re, im);
+}
+
+// band-layout entry (row, lane): (xi_l[A], xi_l[B]) of the lane's item
+__device__ float4 xi_entry(const BandTables& T, const int* row_group, const float* f, const float* t,
+                           const int* block_off, const int* radial_count, int row, int lane) {
+    const int g = row_group[row];
+    const int item = g * 32 + lane;
+    const int s = row - T.row_off[g];
+    if (s >= T.item_len[item]) return make_float4(0.f, 0.f, 0.f, 0.f);
+    const char2 mm = T.item_mm[item], pm = T.item_pm[item];
+    const int l = mm.x + s;
+    const float2 xa = xi_value(l, mm.x, mm.y, f, t, block_off, radial_count);
+    const float2 xb = T.item_w[item].y == 0.0f ? make_float2(0.f, 0.f)
+                                               : xi_value(l, pm.x, pm.y, f, t, block_off, radial_count);
+    return make_float4(xa.x, xa.y, xb.x, xb.y);
 }
 
 
@@ -826,9 +871,12 @@ __device__ __forceinline__ void eval_group(const BandTables& T, const EvalJob (&
 }
 
 // K listed candidates per warp
+#ifndef BMB_EVAL_MINB
+#define BMB_EVAL_MINB 1
+#endif
 template <int ORDER, int K>
-__global__ void __launch_bounds__(EvalShape<K>::WARPS * 32) eval_kernel(StageArgs a, const int* list,
-                                                                        const int* count) {
+__global__ void __launch_bounds__(EvalShape<K>::WARPS * 32, BMB_EVAL_MINB) eval_kernel(StageArgs a, const int* list,
+                                                                                       const int* count) {
     constexpr int WARPS = EvalShape<K>::WARPS;
     __shared__ WarpScratch wsc[WARPS * K];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1047,7 +1095,7 @@ __global__ void __launch_bounds__(EvalShape<K>::WARPS * 32) eval_sweep_kernel(Ev
 __global__ void build_xi_kernel(XiArgs a) {
     const float* f = a.f + (long long)blockIdx.y * a.ldf;
     const float* t = a.t + (long long)blockIdx.y * a.ldt;
-    float2* out = a.out + (size_t)blockIdx.y * a.T.rows * 32;
+    float4* out = a.out + (size_t)blockIdx.y * a.T.rows * 32;
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < a.T.rows * 32; e += gridDim.x * blockDim.x)
         out[e] = xi_entry(a.T, a.row_group, f, t, a.block_off, a.radial_count, e >> 5, e & 31);
 }

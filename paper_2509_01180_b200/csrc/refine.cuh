@@ -30,9 +30,9 @@ struct CandWork {
 struct StageArgs {
     BandTables T;
     const int* row_group = nullptr;
-    const float2* xi_win = nullptr;  // [n_win][T.rows*32] window kernels
-    float2* xi_pool = nullptr;       // [pool][T.rows*32] anchored correlation kernels
-    float2* w_pool = nullptr;        // [pool][T.rows*32] anchored wedge kernels
+    const float4* xi_win = nullptr;  // [n_win][T.rows*32] window kernels (A, B entries)
+    float4* xi_pool = nullptr;       // [pool][T.rows*32] anchored correlation kernels
+    float4* w_pool = nullptr;        // [pool][T.rows*32] anchored wedge kernels
     int pool = 0;
     int* pool_counter = nullptr;     // slot allocator (reset per band)
     int* overflow = nullptr;         // set when the pool is exhausted
@@ -87,7 +87,7 @@ void launch_window_reduce(const ReduceArgs& a, cudaStream_t s);
 // triples; out[(p*n_rot + g)*4 + {0..3}] = value, dC/dalpha, dC/dbeta, dC/dgamma.
 struct EvalArgs {
     BandTables T;
-    const float2* xi = nullptr;     // [n_xi][T.rows*32] kernels in band layout
+    const float4* xi = nullptr;     // [n_xi][T.rows*32] kernels in band layout
     const double* euler = nullptr;  // [n_rot][3]
     int n_xi = 0, n_rot = 0;
     int order = 1;
@@ -112,7 +112,7 @@ struct XiArgs {
     const int* block_off = nullptr;
     const int* radial_count = nullptr;
     int n = 0;
-    float2* out = nullptr;      // [n][T.rows*32]
+    float4* out = nullptr;      // [n][T.rows*32]
 };
 int launch_build_xi(const XiArgs& a, cudaStream_t s);
 

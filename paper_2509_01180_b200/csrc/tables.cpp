@@ -50,75 +50,78 @@ BandTablesHost build_band_tables(int L) {
     BandTablesHost t;
     t.L = L;
     struct It {
-        int m, mp, l0;
+        int m, mp;
     };
-    std::vector<It> items;
+    std::vector<It> items;  // sorted by l0 = m, then m'
     for (int m = 0; m <= L; ++m)
-        for (int mp = (m == 0 ? 0 : -L); mp <= L; ++mp)
-            items.push_back({m, mp, std::max(std::abs(m), std::abs(mp))});
-    std::stable_sort(items.begin(), items.end(), [](const It& x, const It& y) {
-        if (x.l0 != y.l0) return x.l0 < y.l0;
-        if (x.m != y.m) return x.m < y.m;
-        return x.mp < y.mp;
-    });
+        for (int mp = -m; mp <= m; ++mp) items.push_back({m, mp});
     t.n_items = (int)items.size();
     t.n_groups = (t.n_items + 31) / 32;
     const int slots = t.n_groups * 32;
     t.item_mm.assign(slots, char2{0, 0});
+    t.item_pm.assign(slots, char2{0, 0});
+    t.item_w.assign(slots, float2{0.0f, 0.0f});
     t.item_len.assign(slots, 0);
     t.bfac.assign(slots, 0.0f);
     t.bexp.assign(slots, 0);
     t.row_off.assign(t.n_groups + 1, 0);
     for (int g = 0; g < t.n_groups; ++g) {
         int glen = 0;
-        for (int j = 0; j < 32 && g * 32 + j < t.n_items; ++j)
-            glen = std::max(glen, L - items[g * 32 + j].l0 + 1);
+        for (int j = 0; j < 32 && g * 32 + j < t.n_items; ++j) glen = std::max(glen, L - items[g * 32 + j].m + 1);
         t.row_off[g + 1] = t.row_off[g] + glen;
     }
     t.rows = t.row_off[t.n_groups];
     t.P.assign((size_t)t.rows * 32, 0.0f);
     t.Q.assign((size_t)t.rows * 32, 0.0f);
     t.R.assign((size_t)t.rows * 32, 0.0f);
-    t.item_of.assign((size_t)(2 * L + 1) * (2 * L + 1), 0);
+    t.item_of.assign((size_t)(2 * L + 1) * (2 * L + 1), -1);
     for (int i = 0; i < t.n_items; ++i) {
         const It& it = items[i];
         const int g = i / 32, j = i % 32;
-        t.item_mm[i] = char2{(signed char)it.m, (signed char)it.mp};
-        t.item_len[i] = L - it.l0 + 1;
+        const int m = it.m, mp = it.mp;
+        // partner in the half plane: swap (m', m) with sign (-1)^(m-m') for m' >= 0,
+        // anti-swap (-m', -m) with sign +1 for m' < 0 (d^l_{m'm} = (-1)^(m-m') d^l_{mm'},
+        // d^l_{-m',-m} = d^l_{mm'}, src/steer.cpp:43-144)
+        const int pa = mp >= 0 ? mp : -mp, pb = mp >= 0 ? m : -m;
+        const double sg = mp >= 0 ? (((m - mp) & 1) ? -1.0 : 1.0) : 1.0;
+        const bool self = pa == m && pb == mp;
+        t.item_mm[i] = char2{(signed char)m, (signed char)mp};
+        t.item_pm[i] = char2{(signed char)pa, (signed char)pb};
+        t.item_w[i] = float2{(m == 0 && mp == 0) ? 1.0f : 2.0f, self ? 0.0f : (float)(2.0 * sg)};
+        t.item_len[i] = L - m + 1;
         double fac;
         int a, p;
-        border(it.m, it.mp, fac, a, p);
+        border(m, mp, fac, a, p);
         t.bfac[i] = (float)fac;
         t.bexp[i] = a | (p << 8);
-        t.item_of[(size_t)(it.m + L) * (2 * L + 1) + (it.mp + L)] = (int16_t)i;
-        if (it.m != 0 || it.mp != 0)
-            t.item_of[(size_t)(-it.m + L) * (2 * L + 1) + (-it.mp + L)] = (int16_t)(-(i + 1));
-        const double m = it.m, mp = it.mp;
-        for (int s = 1; s <= L - it.l0; ++s) {
-            const int l = it.l0 + s;
+        t.item_of[(size_t)(m + L) * (2 * L + 1) + (mp + L)] = 2 * i;
+        if (!self) t.item_of[(size_t)(pa + L) * (2 * L + 1) + (pb + L)] = 2 * i + 1;
+        for (int s = 1; s <= L - m; ++s) {
+            const int l = m + s;
             const size_t at = (size_t)(t.row_off[g] + s) * 32 + j;
-            if (it.l0 == 0 && l == 1) {  // d^1_00 = cos b (steer.cpp:130-133)
+            if (m == 0 && l == 1) {  // d^1_00 = cos b (steer.cpp:130-133)
                 t.P[at] = 1.0f;
                 continue;
             }
-            // steer.cpp:101-141: t1 = P cos b + Q, t2 = R
-            const double a2 = std::sqrt(((double)l * l - m * m) * ((double)l * l - mp * mp));
-            const bool has2 = std::abs(it.m) <= l - 2 && std::abs(it.mp) <= l - 2;
-            const double b2 = has2 ? std::sqrt(((double)(l - 1) * (l - 1) - m * m) *
-                                               ((double)(l - 1) * (l - 1) - mp * mp))
+            // steer.cpp:101-141: t1 = P cos b + Q, t2 = R (symmetric in m <-> m' and under m,m' -> -m',-m)
+            const double dm = m, dmp = mp;
+            const double a2 = std::sqrt(((double)l * l - dm * dm) * ((double)l * l - dmp * dmp));
+            const bool has2 = std::abs(m) <= l - 2 && std::abs(mp) <= l - 2;
+            const double b2 = has2 ? std::sqrt(((double)(l - 1) * (l - 1) - dm * dm) *
+                                               ((double)(l - 1) * (l - 1) - dmp * dmp))
                                    : 0.0;
             t.P[at] = (float)((2.0 * l - 1.0) * l / a2);
-            t.Q[at] = (float)(-(2.0 * l - 1.0) * m * mp / ((l - 1.0) * a2));
+            t.Q[at] = (float)(-(2.0 * l - 1.0) * dm * dmp / ((l - 1.0) * a2));
             t.R[at] = (float)(l * b2 / ((l - 1.0) * a2));
         }
     }
     return t;
 }
 
-std::vector<float2> wedge_band_entries(const BandTablesHost& t,
+std::vector<float4> wedge_band_entries(const BandTablesHost& t,
                                        const std::vector<std::complex<double>>& chi,
                                        const std::vector<std::complex<double>>& q, double total) {
-    std::vector<float2> w((size_t)t.rows * 32, float2{0.0f, 0.0f});
+    std::vector<float4> w((size_t)t.rows * 32, float4{0.0f, 0.0f, 0.0f, 0.0f});
     auto coef = [](const std::vector<std::complex<double>>& hat, int l, int m) {
         if (m >= 0) return hat[host::tri(l, m)];
         const std::complex<double> c = std::conj(hat[host::tri(l, -m)]);
@@ -126,11 +129,15 @@ std::vector<float2> wedge_band_entries(const BandTablesHost& t,
     };
     for (int i = 0; i < t.n_items; ++i) {
         const int m = t.item_mm[i].x, mp = t.item_mm[i].y;
-        const int l0 = std::max(std::abs(m), std::abs(mp));
+        const int pa = t.item_pm[i].x, pb = t.item_pm[i].y;
+        const bool self = t.item_w[i].y == 0.0f;
         const int g = i / 32, j = i % 32;
-        for (int l = l0; l <= t.L; ++l) {
-            const std::complex<double> v = std::conj(coef(chi, l, m)) * coef(q, l, mp) / total;
-            w[(size_t)(t.row_off[g] + l - l0) * 32 + j] = float2{(float)v.real(), (float)v.imag()};
+        for (int l = m; l <= t.L; ++l) {
+            const std::complex<double> va = std::conj(coef(chi, l, m)) * coef(q, l, mp) / total;
+            const std::complex<double> vb =
+                self ? std::complex<double>(0.0, 0.0) : std::conj(coef(chi, l, pa)) * coef(q, l, pb) / total;
+            w[(size_t)(t.row_off[g] + l - m) * 32 + j] =
+                float4{(float)va.real(), (float)va.imag(), (float)vb.real(), (float)vb.imag()};
         }
     }
     return w;

@@ -9,22 +9,29 @@
 
 namespace bmb {
 
+// Recursion items (m, m') with m >= |m'| (the (m,m') <-> (m',m) and
+// (m,m') <-> (-m',-m) symmetries of d^l): one chain serves the half-plane entry
+// A = (m, m') and its partner B = (m', m) (sign (-1)^(m-m')) or (-m', -m) (sign +1);
+// items with m' = +-m are their own partner (B weight 0).  Kernel entries per
+// (row, lane) are float4 (A.re, A.im, B.re, B.im).
 struct BandTablesHost {
     int L = 0;
     int n_items = 0, n_groups = 0, rows = 0;
     std::vector<int> row_off;
-    std::vector<char2> item_mm;
+    std::vector<char2> item_mm;   // (m, m')
+    std::vector<char2> item_pm;   // partner (pa, pb) in the half plane
+    std::vector<float2> item_w;   // (weight of A, sign * weight of B)
     std::vector<int> item_len;
     std::vector<float> bfac;
     std::vector<int> bexp;
     std::vector<float> P, Q, R;
-    std::vector<int16_t> item_of;
+    std::vector<int> item_of;     // [(m+L)(2L+1) + m'+L]: 2 item + slot of half-plane entries, else -1
 };
 BandTablesHost build_band_tables(int L);
 
 // wedge-power kernel entries in the band layout:
 // W_l[m,m'] = conj(chi_hat_lm) q_hat_lm' / total  (src/xcorr.cpp:344-355)
-std::vector<float2> wedge_band_entries(const BandTablesHost& t,
+std::vector<float4> wedge_band_entries(const BandTablesHost& t,
                                        const std::vector<std::complex<double>>& chi_hat,
                                        const std::vector<std::complex<double>>& q_hat,
                                        double total);
