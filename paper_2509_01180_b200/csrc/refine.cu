@@ -1119,16 +1119,22 @@ double eval_flops(int L, int order, bool wedge) {
     return 6.0 * nd * nxi + per_kernel * (wedge ? 2.0 : 1.0);
 }
 
+// thread-per-candidate bookkeeping kernels: small CTAs so that a few thousand
+// candidates still spread over every SM (these kernels are latency-bound)
+#ifndef BMB_NEWTON_BLOCK
+#define BMB_NEWTON_BLOCK 32
+#endif
+constexpr int kNB = BMB_NEWTON_BLOCK;
 static int thread_grid(long long n) {
-    long long b = (n + 255) / 256;
-    return (int)(b < 1 ? 1 : (b > 4096 ? 4096 : b));
+    long long b = (n + kNB - 1) / kNB;
+    return (int)(b < 1 ? 1 : (b > 16384 ? 16384 : b));
 }
 
 void launch_band_begin(const StageArgs& a, cudaStream_t s) {
-    band_begin_kernel<<<thread_grid((long long)a.n_win * a.max_cand), 256, 0, s>>>(a);
+    band_begin_kernel<<<thread_grid((long long)a.n_win * a.max_cand), kNB, 0, s>>>(a);
 }
 void launch_iter_begin(const StageArgs& a, cudaStream_t s) {
-    iter_begin_kernel<<<thread_grid((long long)a.n_win * a.max_cand), 256, 0, s>>>(a);
+    iter_begin_kernel<<<thread_grid((long long)a.n_win * a.max_cand), kNB, 0, s>>>(a);
 }
 void launch_compose(const StageArgs& a, int n, cudaStream_t s) {
     if (n <= 0) return;
@@ -1171,17 +1177,17 @@ void launch_eval(const StageArgs& a, int order, const int* list, const int* coun
     }
 }
 void launch_step(const StageArgs& a, int* list_out, int* count_out, int max_n, cudaStream_t s) {
-    step_kernel<<<thread_grid(max_n), 256, 0, s>>>(a, list_out, count_out);
+    step_kernel<<<thread_grid(max_n), kNB, 0, s>>>(a, list_out, count_out);
 }
 void launch_accept(const StageArgs& a, const int* list_in, const int* count_in, int* list_out, int* count_out,
                    int max_n, cudaStream_t s) {
-    accept_kernel<<<thread_grid(max_n), 256, 0, s>>>(a, list_in, count_in, list_out, count_out);
+    accept_kernel<<<thread_grid(max_n), kNB, 0, s>>>(a, list_in, count_in, list_out, count_out);
 }
 void launch_final_prep(const StageArgs& a, cudaStream_t s) {
-    final_prep_kernel<<<thread_grid((long long)a.n_win * a.max_cand), 256, 0, s>>>(a);
+    final_prep_kernel<<<thread_grid((long long)a.n_win * a.max_cand), kNB, 0, s>>>(a);
 }
 void launch_final_score(const StageArgs& a, int max_n, cudaStream_t s) {
-    final_score_kernel<<<thread_grid(max_n), 256, 0, s>>>(a);
+    final_score_kernel<<<thread_grid(max_n), kNB, 0, s>>>(a);
 }
 void launch_window_reduce(const ReduceArgs& a, cudaStream_t s) {
     window_reduce_kernel<<<(a.n_win + 127) / 128, 128, 0, s>>>(a);
