@@ -14,7 +14,7 @@ namespace bmb {
 // shared-memory plan: [f | t] (later reused for one beta slice A_j), xi (or
 // the global scratch when it does not fit), scores, maxima
 struct SeedSmem {
-    size_t region0, xi, sc, maxima, total;
+    size_t region0, xi, sc, maxima, bk, total;
     bool xi_in_smem;
 };
 __host__ __device__ inline SeedSmem seed_smem_plan(int rows_low, int L, int nxi, int npt) {
@@ -25,12 +25,14 @@ __host__ __device__ inline SeedSmem seed_smem_plan(int rows_low, int L, int nxi,
     p.region0 = (ft > aj ? ft : aj + 0);
     p.region0 = (p.region0 + 15) / 16 * 16;
     const size_t xib = sizeof(double2) * (size_t)nxi;
-    const size_t rest = sizeof(double) * npt + sizeof(int) * npt;
+    const size_t bkb = sizeof(double2) * (size_t)wd * 64;  // b[k][m] for up to 64 gamma points
+    const size_t rest = sizeof(double) * npt + sizeof(int) * npt + bkb;
     p.xi_in_smem = p.region0 + xib + rest <= 200 * 1024;
     p.xi = p.region0;
     p.sc = p.xi + (p.xi_in_smem ? xib : 0);
     p.maxima = p.sc + sizeof(double) * npt;
-    p.total = p.maxima + sizeof(int) * npt;
+    p.bk = (p.maxima + sizeof(int) * npt + 15) / 16 * 16;
+    p.total = p.bk + bkb;
     return p;
 }
 
@@ -47,6 +49,7 @@ __global__ void __launch_bounds__(256) seed_kernel(SeedArgs a) {
     double2* xi = plan.xi_in_smem ? reinterpret_cast<double2*>(sm + plan.xi)
                                   : a.xi_scratch + (size_t)w * a.nxi;
     double* sc = reinterpret_cast<double*>(sm + plan.sc);
+    double2* Bk = reinterpret_cast<double2*>(sm + plan.bk);
     int* maxima = reinterpret_cast<int*>(sm + plan.maxima);
     __shared__ int n_max;
 
@@ -104,21 +107,27 @@ __global__ void __launch_bounds__(256) seed_kernel(SeedArgs a) {
             Aj[e] = make_double2(re, im);
         }
         __syncthreads();
+        // b[k][m] = sum_m' A_j[m][m'] ug_k[m'], then score = Re sum_m ua_i[m] b[k][m]
+        // (the reference's collapse and sweep order, optimize.cpp:79-93)
+        for (int q = threadIdx.x; q < a.ng * wd; q += blockDim.x) {
+            const int k = q / wd, m = q % wd;
+            const double2* pg = a.ug + (size_t)k * wd;
+            double bre = 0.0, bim = 0.0;
+            for (int mp = 0; mp < wd; ++mp) {
+                const double2 x = Aj[m * wd + mp], y = pg[mp];
+                bre += x.x * y.x - x.y * y.y;
+                bim += x.x * y.y + x.y * y.x;
+            }
+            Bk[q] = make_double2(bre, bim);
+        }
+        __syncthreads();
         for (int q = threadIdx.x; q < a.na * a.ng; q += blockDim.x) {
             const int k = q % a.ng, i = q / a.ng;
             const int idx = (j * a.na + i) * a.ng + k;
-            const double2* pg = a.ug + (size_t)k * wd;
             const double2* pa = a.ua + (size_t)i * wd;
+            const double2* bk = Bk + (size_t)k * wd;
             double acc = 0.0;
-            for (int m = 0; m < wd; ++m) {
-                double bre = 0.0, bim = 0.0;
-                for (int mp = 0; mp < wd; ++mp) {
-                    const double2 x = Aj[m * wd + mp], y = pg[mp];
-                    bre += x.x * y.x - x.y * y.y;
-                    bim += x.x * y.y + x.y * y.x;
-                }
-                acc += pa[m].x * bre - pa[m].y * bim;
-            }
+            for (int m = 0; m < wd; ++m) acc += pa[m].x * bk[m].x - pa[m].y * bk[m].y;
             if (a.wedge_sqrt) acc /= a.wedge_sqrt[idx];
             sc[idx] = acc;
         }
@@ -200,6 +209,7 @@ bool seed_needs_scratch(const SeedArgs& a) {
 
 int launch_seed(const SeedArgs& a, int n_win, cudaStream_t s) {
     if (n_win <= 0) return 0;
+    if (a.ng > 64) return 1;  // b[k][m] staging holds up to 64 gamma points
     const size_t smem = seed_smem_bytes(a);
     if (smem > 200 * 1024) return 1;
     cudaFuncSetAttribute(seed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
