@@ -77,3 +77,37 @@ def test_align_batch_matches_oracle(cuda_device):
         assert g["windows"] == ref["windows"]
         # ground truth: shift recovered exactly, rotation close
         assert g["shift"] == truth[i][1]
+
+
+def test_config1_all_particles_match_oracle(cuda_device):
+    """BASELINE config 1 in full: 32^3, L=8, 20-blob template, 128 particles (Haar
+    rotations, SNR 0.5, no wedge, no shift), one window s = 0, band {8}, 8 starts —
+    every particle's rotation within 0.5 deg and score within 1e-4 of the oracle's
+    search_one_shift (src/optimize.cpp:361-419) on the same float32 bytes."""
+    import math
+
+    import numpy as np
+
+    from oracle import bmo
+    from paper_2509_01180_b200 import api
+
+    n, L, P = 32, 8, 128
+    cut = L * math.pi
+    tmpl_d = api.make_template(n, 20, 1)
+    parts, q_true, _ = api.make_particles(tmpl_d, P, 100, 0, 0.5, None)
+    ctx = api.Context(n, L, cut)
+    ctx.set_template(tmpl_d)
+    cfg = api.make_config(bands=(8,), max_candidates=8)
+    got = ctx.search_windows(parts, [(p, (0, 0, 0)) for p in range(P)], cfg)
+    spec = bmo.Spec(L, cut)
+    ocfg = bmo.make_config(l_max=L, lambda_cut=cut, bands=(8,), max_candidates=8)
+    tmpl = tmpl_d.cpu().numpy().astype(np.float64)
+    host = parts.cpu().numpy().astype(np.float64)
+    worst_ang, worst_score = 0.0, 0.0
+    for p in range(P):
+        ref = bmo.search_window(spec, tmpl, host[p], (0, 0, 0), ocfg)
+        ang = bmo.geodesic_degrees(got[p]["quat"], ref["quat"])
+        rel = abs(got[p]["norm_score"] - ref["norm_score"]) / abs(ref["norm_score"])
+        worst_ang, worst_score = max(worst_ang, ang), max(worst_score, rel)
+    assert worst_ang < 0.5, worst_ang
+    assert worst_score < 1e-4, worst_score
