@@ -570,45 +570,66 @@ __device__ void compose_block(const BandTables& T, const float4* src, const Stag
         __syncthreads();
     }
     const float inv_total = (float)(1.0 / a.wp_total);
+    // zero the layout (padding lanes, steps past an item's chain, B of self-paired items)
     for (int at = tid; at < T.rows * 32; at += nt) {
-        const int row = at >> 5, j = at & 31;
-        const int g = a.row_group[row];
-        const int item = g * 32 + j;
-        const int st = row - T.row_off[g];
-        if (st >= T.item_len[item]) {
-            out[at] = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (wedge) out_w[at] = make_float4(0.f, 0.f, 0.f, 0.f);
-            continue;
+        out[at] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (wedge) out_w[at] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    __syncthreads();
+    // xi~_l[m,m'] = e^{-i m' a} sum_n X_l[m,n] d^l_{m'n} over the half plane m >= 0,
+    // one task per (l, m, quad of 4 consecutive m'): the X row is loaded once per n
+    // for 4 outputs; results scatter to their (item, slot) of the band layout
+    float2* outp = reinterpret_cast<float2*>(out);
+    float2* outwp = reinterpret_cast<float2*>(out_w);
+    int total = 0;
+    for (int l = 0; l <= L; ++l) total += (l + 1) * ((2 * l + 4) / 4);
+    for (int wi = tid; wi < total; wi += nt) {
+        int l = 0, base = 0;
+        for (;; ++l) {
+            const int nb = (l + 1) * ((2 * l + 4) / 4);
+            if (wi < base + nb) break;
+            base += nb;
         }
-        const int l = T.item_mm[item].x + st, w = 2 * l + 1, o = xi_off(l);
-        float2 r[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-        float2 rw[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        const int nq = (2 * l + 4) / 4;
+        const int m = (wi - base) / nq, q0 = -l + 4 * ((wi - base) % nq);
+        const int w = 2 * l + 1, o = xi_off(l);
+        const float2* xrow = xd + o + (m + l) * w;
+        const float* drow[4];
 #pragma unroll
-        for (int slot = 0; slot < 2; ++slot) {
-            if (slot == 1 && T.item_w[item].y == 0.0f) break;
-            const char2 e = slot ? T.item_pm[item] : T.item_mm[item];
-            const int m = e.x, mp = e.y;  // m >= 0 (half plane)
-            const float2* xrow = xd + o + (m + l) * w;
-            const float* drow = dtab + o + (mp + l) * w;
-            float re = 0.0f, im = 0.0f;
-            for (int n = 0; n < w; ++n) {
-                const float2 x = xrow[n];
-                const float dv = drow[n];
-                re = fmaf(x.x, dv, re);
-                im = fmaf(x.y, dv, im);
+        for (int j = 0; j < 4; ++j) drow[j] = dtab + o + (min(q0 + j, l) + l) * w;
+        float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                         make_float2(0.f, 0.f)};
+        for (int n = 0; n < w; ++n) {
+            const float2 x = xrow[n];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float dv = drow[j][n];
+                acc[j].x = fmaf(x.x, dv, acc[j].x);
+                acc[j].y = fmaf(x.y, dv, acc[j].y);
             }
+        }
+        float cr = 0.0f, ci = 0.0f;  // conj(chi_lm), m >= 0 (wedge only)
+        if (wedge) {
+            const double2 c = a.chi_hat[l * (l + 1) / 2 + m];
+            cr = (float)c.x;
+            ci = (float)-c.y;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int mp = q0 + j;
+            if (mp > l || (m == 0 && mp < 0)) continue;
+            const int code = T.item_of[(m + L) * (2 * L + 1) + (mp + L)];
+            const int item = code >> 1, slot = code & 1;
+            const int at = (T.row_off[item >> 5] + (l - T.item_mm[item].x)) * 32 + (item & 31);
             float2 eam = cs.ua[abs(mp)];
             if (mp < 0) eam.y = -eam.y;
-            r[slot] = cmul(eam, make_float2(re, im));
+            outp[2 * at + slot] = cmul(eam, acc[j]);
             if (wedge) {
-                const double2 c = a.chi_hat[l * (l + 1) / 2 + m];
                 const float2 qv = qt[l * l + (mp + l)];
-                const float cr = (float)c.x, ci = (float)-c.y;  // conj(chi_lm)
-                rw[slot] = make_float2((cr * qv.x - ci * qv.y) * inv_total, (cr * qv.y + ci * qv.x) * inv_total);
+                outwp[2 * at + slot] =
+                    make_float2((cr * qv.x - ci * qv.y) * inv_total, (cr * qv.y + ci * qv.x) * inv_total);
             }
         }
-        out[at] = make_float4(r[0].x, r[0].y, r[1].x, r[1].y);
-        if (wedge) out_w[at] = make_float4(rw[0].x, rw[0].y, rw[1].x, rw[1].y);
     }
     __syncthreads();
 }
