@@ -157,6 +157,13 @@ int bm_apply_wedge_taper(bm_context* ctx, const float* in, float* out, int count
 int bm_average_accumulate(bm_context* ctx, const float* particles, int count,
                           const bm_align_result* results, double* sum, void* stream);
 
+/* Voxel synthesis of a coefficient set (synthesize, src/basis.cpp:332-419,
+ * with its Catmull-Rom radial table, basis.cpp:221-245): coeffs device
+ * complex128 (coeff_count, reference layout), real_volume != 0 when the set has
+ * the real-volume symmetry (e.g. an average of expansions); out device double
+ * n^3 (x fastest), zero outside the unit ball.  FP64. */
+int bm_synthesize(bm_context* ctx, const double* coeffs, int real_volume, int n, double* out, void* stream);
+
 /* Kernel timing evidence: with timing on, CUDA events on the context stream
  * bracket every launch of this library.  out_ms[0..14]: gather, expansion,
  * seed, refine, wedge filter, misc, refine by band position 0, 1, 2, 3+, and

@@ -369,6 +369,22 @@ inline BallExpansion expand(const Volume& v, const BasisSpec& spec) {
     return e;
 }
 
+// synthesize (basis.hpp:99, basis.cpp:332-419): voxel map of a coefficient set,
+// zero outside the unit ball; FP64 on the device
+inline Volume synthesize(const BallExpansion& e, int n, double voxel_size = 1.0) {
+    if (n < 8) throw std::invalid_argument("synthesize: grid size must be >= 8");
+    const BasisSpec& spec = e.spec();
+    bm_context* ctx = spec.plan(0);
+    detail::DeviceBuffer<double> d_c(2 * spec.coeff_count()), d_out(static_cast<size_t>(n) * n * n);
+    detail::cuda(cudaMemcpy(d_c.get(), e.coeffs().data(), spec.coeff_count() * sizeof(cdouble), cudaMemcpyHostToDevice),
+                 "synthesize H2D");
+    detail::check(bm_synthesize(ctx, d_c.get(), e.real_volume() ? 1 : 0, n, d_out.get(), nullptr), "synthesize");
+    Volume v(n, voxel_size);
+    detail::cuda(cudaMemcpy(v.data.data(), d_out.get(), v.data.size() * sizeof(double), cudaMemcpyDeviceToHost),
+                 "synthesize D2H");
+    return v;
+}
+
 // ------------------------------------------------------------------ wedge (xcorr.hpp:82-125)
 struct WedgeMask {
     int n = 0;

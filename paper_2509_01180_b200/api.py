@@ -249,6 +249,22 @@ class Context:
     def set_timing(self, on: bool = True):
         _lib.check(_lib.lib().bm_context_set_timing(self._h, 1 if on else 0), "set_timing")
 
+    def synthesize(self, coeffs, n: int, real_volume: bool = True):
+        """synthesize (src/basis.cpp:332-419): coefficients (complex128 (coeff_count,) or
+        float64 (coeff_count, 2), device or host) -> float64 (n, n, n) voxel map on the device."""
+        torch = _torch()
+        dev = torch.device(f"cuda:{self.device}")
+        c = torch.as_tensor(coeffs)
+        if c.is_complex():
+            c = torch.view_as_real(c.to(torch.complex128))
+        c = c.to(device=dev, dtype=torch.float64).contiguous()
+        if c.numel() != 2 * self.coeff_count:
+            raise ValueError("synthesize: coefficient count does not match the basis")
+        out = torch.empty((n, n, n), dtype=torch.float64, device=dev)
+        _lib.check(_lib.lib().bm_synthesize(self._h, C.c_void_p(c.data_ptr()), 1 if real_volume else 0, n,
+                                            C.c_void_p(out.data_ptr()), self._stream(out)), "synthesize")
+        return out
+
     def set_expand_mode(self, mode: str):
         """'factored' (default) or 'gemm' (dense operator on the tensor cores)."""
         _lib.check(_lib.lib().bm_context_set_expand_mode(self._h, {"factored": 0, "gemm": 1}[mode]),

@@ -339,6 +339,18 @@ int bm_average_accumulate(bm_context* ctx, const float* particles, int count,
     });
 }
 
+int bm_synthesize(bm_context* ctx, const double* coeffs, int real_volume, int n, double* out, void* stream) {
+    return guarded("bm_synthesize", [&] {
+        if (!ctx) return (int)BM_ERR_STATE;
+        if (!coeffs || !out) throw std::invalid_argument("bad buffers");
+        auto& c = *ctx->impl;
+        cudaSetDevice(c.device);
+        StreamJoin join(ctx, stream);
+        c.synthesize(coeffs, real_volume != 0, n, out);
+        return (int)BM_OK;
+    });
+}
+
 int bm_context_set_timing(bm_context* ctx, int on) {
     if (!ctx) return BM_ERR_STATE;
     ctx->impl->timer.on = on != 0;

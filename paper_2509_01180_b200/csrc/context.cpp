@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <stdexcept>
 
+#include "synth.hpp"
 #include "wedge.hpp"
 
 namespace bmb {
@@ -131,6 +132,44 @@ void Context::build_factored_tables() {
     fx.tri_lm = fx_trilm.as<int2>();
     fx.radial_t = fx_radial.as<float>();
     fx.rowpack = fx_rowmap.as<int>();
+}
+
+void Context::synthesize(const double* coef, bool real_volume, int n_out, double* out) {
+    if (n_out < 8) throw std::invalid_argument("synthesize: grid size must be >= 8");
+    const int L = basis.l_max;
+    const int n_fine = 2048, row_len = n_fine + 3;
+    std::vector<int> pair_off(L + 1);
+    int pairs = 0;
+    for (int l = 0; l <= L; ++l) {
+        pair_off[l] = pairs;
+        pairs += basis.radial_count(l);
+    }
+    if (!synth_table_.p) {
+        std::vector<double> rows((size_t)pairs * row_len, 0.0);
+        const double h = 1.0 / n_fine;
+        for (int l = 0; l <= L; ++l)
+            for (int k = 0; k < basis.radial_count(l); ++k) {
+                double* row = rows.data() + (size_t)(pair_off[l] + k) * row_len;
+                for (int j = 1; j < row_len; ++j) row[j] = basis.norms[l][k] * host::sph_jl(l, basis.roots[l][k] * (j - 1) * h);
+                row[0] = (l % 2 ? -1.0 : 1.0) * row[2];  // ghost node at -h by parity
+            }
+        upload(synth_table_, rows, stream);
+        upload(synth_pair_off_, pair_off, stream);
+    }
+    SynthArgs a;
+    a.coef = reinterpret_cast<const double2*>(coef);
+    a.real_volume = real_volume;
+    a.n = n_out;
+    a.L = L;
+    a.block_off = geo.block_off;
+    a.radial_count = geo.radial_count;
+    a.pair_off = synth_pair_off_.as<int>();
+    a.table = synth_table_.as<double>();
+    a.n_fine = n_fine;
+    a.row_len = row_len;
+    a.out = out;
+    if (launch_synthesize(a, stream) != 0) throw std::runtime_error("synthesize launch failed");
+    ++timer.launches;
 }
 
 Context::~Context() {

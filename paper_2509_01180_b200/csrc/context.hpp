@@ -208,6 +208,9 @@ public:
         if (!pinned_ && cudaMallocHost(&pinned_, sizeof(int) * 16) != cudaSuccess) throw std::bad_alloc();
         return pinned_;
     }
+    // synthesize() radial table (basis.cpp:221-245), built on first use
+    DevBuf synth_table_, synth_pair_off_;
+    void synthesize(const double* coef, bool real_volume, int n_out, double* out);
     DevBuf seed_scratch_;                   // seed xi when it does not fit in shared memory
     DevBuf eval_stats_;                     // [kMaxL+1][order 0/2][wedge 0/1] evaluation counts
     static constexpr size_t kEvalStats = (size_t)(kMaxL + 1) * 4;

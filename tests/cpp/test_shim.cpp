@@ -199,6 +199,28 @@ static void average_matches_oracle() {
     CHECK(dot.real() / (t_hat.norm() * avg.norm()) > 0.5);
 }
 
+// synthesize (basis.cpp:332-419) of the average against the oracle's, FP64 both sides
+static void synthesize_matches_oracle() {
+    const auto tmpl = rounded(bmo::gaussian_blob_template(32, 20, 5));
+    const double cut = 8 * std::numbers::pi;
+    const auto s = bm::build_spec(8, cut);
+    const auto o = bmo::build_spec(8, cut);
+    const auto e = bm::expand(to_product(tmpl), s);
+    const auto v = bm::synthesize(e, 32);
+    bmo::Expansion oe;
+    oe.spec = &o;
+    oe.c = e.coeffs();
+    oe.real = true;
+    const auto ov = bmo::synthesize(oe, 32);
+    double num = 0.0, den = 0.0;
+    for (size_t i = 0; i < v.data.size(); ++i) {
+        num += (v.data[i] - ov.d[i]) * (v.data[i] - ov.d[i]);
+        den += ov.d[i] * ov.d[i];
+    }
+    std::printf("  synthesize rel L2 %.2e\n", std::sqrt(num / den));
+    CHECK(std::sqrt(num / den) < 1e-10);
+}
+
 // error behaviour mirrors the reference (optimize.cpp:153-177, 423-449)
 static void errors_match_reference() {
     const auto tmpl = to_product(rounded(bmo::gaussian_blob_template(32, 20, 1)));
@@ -235,6 +257,7 @@ int main() {
         {"expand_matches_oracle", expand_matches_oracle},
         {"align_matches_oracle", align_matches_oracle},
         {"average_matches_oracle", average_matches_oracle},
+        {"synthesize_matches_oracle", synthesize_matches_oracle},
         {"errors_match_reference", errors_match_reference},
     };
     for (const auto& [name, fn] : tests) {
