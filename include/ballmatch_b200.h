@@ -13,7 +13,7 @@
 extern "C" {
 #endif
 
-#define BM_ABI_VERSION 1
+#define BM_ABI_VERSION 2
 
 enum bm_status {
     BM_OK = 0,
@@ -72,10 +72,14 @@ int bm_expand(bm_context* ctx, const float* vols, int count, const int* shifts, 
               void* stream);
 
 /* ------------------------------------------------------------------ alignment
- * Mirrors OptimizerConfig (include/ballmatch/optimize.hpp:15-32) with fixed
- * bands; l_max and lambda_cut are the context's.  accept_tol is the relative
- * slack of the Newton acceptance test (reference: 1e-12 with FP64 scores,
- * src/optimize.cpp:332); the FP32 evaluation uses a wider default. */
+ * Mirrors OptimizerConfig (include/ballmatch/optimize.hpp:15-32); l_max and
+ * lambda_cut are the context's.  accept_tol is the relative slack of the Newton
+ * acceptance test (reference: 1e-12 with FP64 scores, src/optimize.cpp:332);
+ * the FP32 evaluation uses a wider default.  auto_bands != 0 selects
+ * each particle's bands from its zero-shift kernel (select_bands with the
+ * thresholds, optimize.cpp:179-195, 455-460; n_thresholds 0: 0.5, 0.25, 0.05);
+ * prune_after_band != 0 keeps only each window's best candidate after the
+ * first band (optimize.cpp:391-403). */
 typedef struct bm_align_config {
     int n_bands;
     int bands[16];
@@ -87,6 +91,10 @@ typedef struct bm_align_config {
     int shift_radius;
     int shift_step;
     double accept_tol;
+    int auto_bands;
+    int prune_after_band;
+    int n_thresholds;
+    double thresholds[8];
 } bm_align_config;
 
 /* AlignmentResult (optimize.hpp:71-88): shift, rotation (template -> particle,
@@ -100,6 +108,8 @@ typedef struct bm_align_result {
     long long evaluations;
     double subtomo_norm;
     int windows;
+    int n_bands;   /* the band schedule used (auto_bands: per particle) */
+    int bands[16];
 } bm_align_result;
 
 /* One window outcome (search_one_shift, src/optimize.cpp:361-419). */

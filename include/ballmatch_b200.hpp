@@ -403,7 +403,7 @@ struct OptimizerConfig {
     double lambda_cut = 0.0;  // 0 = default for the grid size
     std::vector<double> band_thresholds{0.5, 0.25, 0.05};
     std::vector<int> fixed_bands{7, 12, 33};
-    bool auto_bands = false;  // not supported on the device path yet: throws
+    bool auto_bands = false;  // per-particle bands from the zero-shift kernel (select_bands)
     double seed_grid_step = std::numbers::pi / 8;
     int max_candidates = 20;
     int newton_max_iter = 30;
@@ -411,7 +411,7 @@ struct OptimizerConfig {
     double step_damping = 1e-3;
     int shift_radius = 4;
     int shift_step = 2;
-    bool prune_after_band = false;  // not supported on the device path yet: throws
+    bool prune_after_band = false;  // keep each window's first-band winner for the rest
     int threads = 0;                // host threads: unused (the device does the work)
     // device path only
     int device = -1;          // -1: current device
@@ -420,10 +420,14 @@ struct OptimizerConfig {
     // optimize.cpp:153-177
     void validate() const {
         if (l_max < 0) throw std::invalid_argument("config: l_max must be >= 0");
-        if (auto_bands) throw std::invalid_argument("config: auto_bands is not supported by the B200 path");
-        if (prune_after_band)
-            throw std::invalid_argument("config: prune_after_band is not supported by the B200 path");
-        if (fixed_bands.empty()) throw std::invalid_argument("config: need fixed bands or auto band selection");
+        for (size_t i = 1; i < band_thresholds.size(); ++i)
+            if (!(band_thresholds[i - 1] >= band_thresholds[i]))
+                throw std::invalid_argument("config: band thresholds must be strictly decreasing");
+        for (double t : band_thresholds)
+            if (!(t > 0.0 && t < 1.0)) throw std::invalid_argument("config: band thresholds must lie in (0,1)");
+        if (band_thresholds.size() > 8) throw std::invalid_argument("config: at most 8 band thresholds");
+        if (fixed_bands.empty() && !auto_bands)
+            throw std::invalid_argument("config: need fixed bands or auto band selection");
         if (fixed_bands.size() > 16) throw std::invalid_argument("config: at most 16 bands");
         for (size_t i = 0; i < fixed_bands.size(); ++i) {
             if (fixed_bands[i] < 0 || fixed_bands[i] > l_max)
@@ -450,6 +454,10 @@ struct OptimizerConfig {
         c.shift_radius = shift_radius;
         c.shift_step = shift_step;
         c.accept_tol = accept_tol > 0.0 ? accept_tol : kFp32AcceptTol;
+        c.auto_bands = auto_bands ? 1 : 0;
+        c.prune_after_band = prune_after_band ? 1 : 0;
+        c.n_thresholds = static_cast<int>(band_thresholds.size());
+        for (size_t i = 0; i < band_thresholds.size(); ++i) c.thresholds[i] = band_thresholds[i];
         return c;
     }
 };
@@ -513,7 +521,7 @@ public:
             o.converged = r.converged != 0;
             o.candidates_evaluated = static_cast<long>(r.candidates);
             o.evaluations = static_cast<long>(r.evaluations);
-            o.bands = cfg_.fixed_bands;
+            o.bands.assign(r.bands, r.bands + r.n_bands);
             o.template_norm = template_norm();
             o.subtomo_norm = r.subtomo_norm;
             o.wall_time_s = wall;

@@ -883,6 +883,32 @@ double Xi::total_energy() const {
         for (const auto& x : blk) e += std::norm(x);
     return e;
 }
+// src/xcorr.cpp:129-137
+double energy_ratio(const Xi& xi, int l_cut) {
+    if (l_cut > xi.l_max) throw std::invalid_argument("energy_ratio: l_cut exceeds band limit");
+    const double total = xi.total_energy();
+    if (!(total > 0.0)) throw std::domain_error("energy_ratio: zero kernel energy");
+    double high = 0.0;
+    for (int l = l_cut + 1; l <= xi.l_max; ++l)
+        for (const auto& x : xi.b[l]) high += std::norm(x);
+    return high / total;
+}
+// optimize.cpp:179-195: per threshold, the lowest band whose energy above it is small enough
+std::vector<int> select_bands(const Xi& xi, const std::vector<double>& thresholds) {
+    std::vector<double> ratio(xi.l_max + 1);
+    for (int l = 0; l <= xi.l_max; ++l) ratio[l] = energy_ratio(xi, l);
+    std::vector<int> bands;
+    for (double tau : thresholds)
+        for (int l = 0; l <= xi.l_max; ++l)
+            if (ratio[l] <= tau) {
+                bands.push_back(l);
+                break;
+            }
+    std::sort(bands.begin(), bands.end());
+    bands.erase(std::unique(bands.begin(), bands.end()), bands.end());
+    return bands;
+}
+
 // src/xcorr.cpp:34-50: xi_l = T_l^H F_l, i.e. xi[m,m'] = sum_k conj(t[k,m]) f[k,m']
 Xi xi_coefficients(const Expansion& t, const Expansion& f, std::array<int, 3> shift) {
     const Spec& spec = *t.spec;
@@ -1330,9 +1356,15 @@ std::vector<double> grid_scores(const Xi& xi, int l_cut, double step) {
     return grid_scores_impl(xi, l_cut, EulerGrid::with_step(step));
 }
 
-void Config::validate() const {  // optimize.cpp:153-177 (fixed-band mode)
+void Config::validate() const {  // optimize.cpp:153-177
     if (l_max < 0) throw std::invalid_argument("config: l_max must be >= 0");
-    if (fixed_bands.empty()) throw std::invalid_argument("config: need fixed bands or auto band selection");
+    for (size_t i = 1; i < band_thresholds.size(); ++i)
+        if (!(band_thresholds[i - 1] >= band_thresholds[i]))
+            throw std::invalid_argument("config: band thresholds must be strictly decreasing");
+    for (double t : band_thresholds)
+        if (!(t > 0.0 && t < 1.0)) throw std::invalid_argument("config: band thresholds must lie in (0,1)");
+    if (fixed_bands.empty() && !auto_bands)
+        throw std::invalid_argument("config: need fixed bands or auto band selection");
     for (size_t i = 0; i < fixed_bands.size(); ++i) {
         if (fixed_bands[i] < 0 || fixed_bands[i] > l_max)
             throw std::invalid_argument("config: bands must lie in [0, l_max]");
@@ -1511,15 +1543,34 @@ ShiftOutcome search_one_shift(const Volume& subtomo, const std::array<int, 3>& s
     const EulerGrid grid = EulerGrid::with_step(cfg.seed_grid_step);
     oc.evals[bands.front()] += grid.size();
     if (cands.empty()) return oc;
-    RefineResult best;
-    bool have = false;
-    for (const auto& c : cands) {
-        RefineResult r = refine(xi, c.rotation, bands, cfg, wedge_power);
+    auto run = [&](const Rot& start, const std::vector<int>& schedule) {
+        RefineResult r = refine(xi, start, schedule, cfg, wedge_power);
         for (const auto& [band, n] : r.evals) oc.evals[band] += n;
         ++oc.candidates;
-        if (!have || r.score > best.score || (r.score == best.score && r.rotation.angle() < best.rotation.angle())) {
-            best = std::move(r);
-            have = true;
+        return r;
+    };
+    RefineResult best;
+    bool have = false;
+    if (cfg.prune_after_band && bands.size() > 1) {  // optimize.cpp:391-403
+        RefineResult low_best;
+        bool low_have = false;
+        for (const auto& c : cands) {
+            RefineResult r = run(c.rotation, {bands.front()});
+            if (!low_have || r.score > low_best.score) {
+                low_best = std::move(r);
+                low_have = true;
+            }
+        }
+        best = run(low_best.rotation, std::vector<int>(bands.begin() + 1, bands.end()));
+        have = true;
+    } else {
+        for (const auto& c : cands) {
+            RefineResult r = run(c.rotation, bands);
+            if (!have || r.score > best.score ||
+                (r.score == best.score && r.rotation.angle() < best.rotation.angle())) {
+                best = std::move(r);
+                have = true;
+            }
         }
     }
     oc.refined = std::move(best);
@@ -1546,7 +1597,12 @@ AlignResult align(const Volume& tmpl, const Volume& subtomo, const Config& cfg,
     std::optional<Xi> wp;
     if (wedge && wedge->theta_max_deg < 90.0) wp = wedge_power_kernel(tmpl, *wedge, cfg.l_max);
     const Xi* wp_ptr = wp ? &*wp : nullptr;
-    const std::vector<int> bands = cfg.fixed_bands;
+    std::vector<int> bands = cfg.fixed_bands;
+    if (cfg.auto_bands) {  // optimize.cpp:455-460: the zero-shift kernel's energy ratios
+        const Expansion f0 = expand(f_w, spec);
+        bands = select_bands(xi_coefficients(f0, t_hat, {0, 0, 0}), cfg.band_thresholds);
+    }
+    out.bands = bands;
 #ifdef _OPENMP
     const int n_threads = cfg.threads > 0 ? cfg.threads : omp_get_max_threads();
 #endif

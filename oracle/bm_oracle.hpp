@@ -160,6 +160,8 @@ struct Xi {
     double total_energy() const;
 };
 Xi xi_coefficients(const Expansion& t, const Expansion& f, std::array<int, 3> shift = {0, 0, 0});
+double energy_ratio(const Xi& xi, int l_cut);
+std::vector<int> select_bands(const Xi& xi, const std::vector<double>& thresholds);
 struct Deriv {
     double value = 0, imag = 0;
     Vec3 grad{0, 0, 0};
@@ -208,6 +210,9 @@ struct Config {
     int shift_radius = 4;
     int shift_step = 2;
     int threads = 0;
+    std::vector<double> band_thresholds{0.5, 0.25, 0.05};
+    bool auto_bands = false;        // bands from the zero-shift kernel's energy ratios
+    bool prune_after_band = false;  // keep only the lowest band's winner for the rest
     void validate() const;
 };
 struct TraceRow {
@@ -252,6 +257,7 @@ struct AlignResult {
     std::map<int, long> evals;
     double template_norm = 0, subtomo_norm = 0;
     int windows = 0;
+    std::vector<int> bands;
 };
 AlignResult align(const Volume& tmpl, const Volume& sub, const Config& cfg,
                   const std::optional<WedgeMask>& wedge = std::nullopt);

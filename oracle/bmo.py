@@ -39,18 +39,20 @@ class Config(C.Structure):
     _fields_ = [("l_max", I), ("lambda_cut", D), ("n_bands", I), ("bands", I * 16),
                 ("seed_grid_step", D), ("max_candidates", I), ("newton_max_iter", I),
                 ("grad_tol", D), ("step_damping", D), ("shift_radius", I), ("shift_step", I),
-                ("threads", I)]
+                ("threads", I), ("auto_bands", I), ("prune_after_band", I), ("n_thresholds", I),
+                ("thresholds", D * 8)]
 
 
 class AlignOut(C.Structure):
     _fields_ = [("shift", I * 3), ("quat", D * 4), ("score", D), ("converged", I),
                 ("candidates_evaluated", LL), ("evaluations", LL), ("template_norm", D),
-                ("subtomo_norm", D), ("windows", I)]
+                ("subtomo_norm", D), ("windows", I), ("n_bands", I), ("bands", I * 16)]
 
 
 def make_config(l_max=42, lambda_cut=0.0, bands=(7, 12, 33), seed_grid_step=np.pi / 8,
                 max_candidates=20, newton_max_iter=30, grad_tol=1e-7, step_damping=1e-3,
-                shift_radius=4, shift_step=2, threads=0) -> Config:
+                shift_radius=4, shift_step=2, threads=0, auto_bands=False, prune_after_band=False,
+                band_thresholds=(0.5, 0.25, 0.05)) -> Config:
     c = Config()
     c.l_max = l_max
     c.lambda_cut = lambda_cut
@@ -65,6 +67,11 @@ def make_config(l_max=42, lambda_cut=0.0, bands=(7, 12, 33), seed_grid_step=np.p
     c.shift_radius = shift_radius
     c.shift_step = shift_step
     c.threads = threads
+    c.auto_bands = 1 if auto_bands else 0
+    c.prune_after_band = 1 if prune_after_band else 0
+    c.n_thresholds = len(band_thresholds)
+    for i, t in enumerate(band_thresholds):
+        c.thresholds[i] = t
     return c
 
 
@@ -105,6 +112,8 @@ def lib():
             "bmo_grid_scores": ([I, P, I, D, P], None),
             "bmo_seed_candidates": ([I, P, I, D, I, I, P, P, P, P], I),
             "bmo_refine": ([I, P, P, C.POINTER(Config), I, P, P, P, P, P, I, P, P], I),
+            "bmo_energy_ratio": ([I, P, I, P], I),
+            "bmo_select_bands": ([I, P, P, I, P], I),
             "bmo_align": ([I, P, P, C.POINTER(Config), D, C.POINTER(AlignOut)], I),
             "bmo_search_window": ([P, I, P, P, P, C.POINTER(Config), D, P, P, P, P, P], I),
             "bmo_apply_wedge": ([I, P, D, P], I),
@@ -366,6 +375,28 @@ def seed_candidates(xi, L, l_low, step, max_candidates, wp=None, L_wp=0):
     return q[:n], s[:n], idx[:n]
 
 
+def energy_ratio(xi, L, l_cut):
+    """energy_ratio (src/xcorr.cpp:129-137); ArithmeticError for a zero kernel."""
+    x = np.ascontiguousarray(xi, dtype=np.complex128)
+    out = np.zeros(1)
+    rc = lib().bmo_energy_ratio(L, _p(x), l_cut, _p(out))
+    if rc == 3:
+        raise ArithmeticError(lib().bmo_last_error().decode())
+    _chk(rc, "energy_ratio")
+    return float(out[0])
+
+
+def select_bands(xi, L, thresholds):
+    """select_bands (src/optimize.cpp:179-195)."""
+    x = np.ascontiguousarray(xi, dtype=np.complex128)
+    t = np.ascontiguousarray(thresholds, dtype=np.float64)
+    out = np.zeros(L + 1, dtype=np.int32)
+    n = lib().bmo_select_bands(L, _p(x), _p(t), len(t), _p(out))
+    if n < 0:
+        raise ValueError(lib().bmo_last_error().decode())
+    return [int(b) for b in out[:n]]
+
+
 def refine(xi, L, start, cfg: Config, wp=None, L_wp=0, max_trace=4096):
     x = np.ascontiguousarray(xi, dtype=np.complex128)
     st = np.asarray(start, dtype=np.float64)
@@ -391,7 +422,8 @@ def align(tmpl, sub, cfg: Config, wedge_deg=0.0):
     return dict(shift=tuple(out.shift), quat=np.array(out.quat[:]), score=out.score,
                 converged=bool(out.converged), candidates=out.candidates_evaluated,
                 evaluations=out.evaluations, template_norm=out.template_norm,
-                subtomo_norm=out.subtomo_norm, windows=out.windows)
+                subtomo_norm=out.subtomo_norm, windows=out.windows,
+                bands=[int(b) for b in out.bands[:out.n_bands]])
 
 
 def search_window(spec: Spec, tmpl, sub, shift, cfg: Config, wedge_deg=0.0):

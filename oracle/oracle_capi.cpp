@@ -81,6 +81,10 @@ struct bmo_config {
     int shift_radius;
     int shift_step;
     int threads;
+    int auto_bands;
+    int prune_after_band;
+    int n_thresholds;
+    double thresholds[8];
 };
 struct bmo_align_out {
     int shift[3];
@@ -92,6 +96,8 @@ struct bmo_align_out {
     double template_norm;
     double subtomo_norm;
     int windows;
+    int n_bands;
+    int bands[16];
 };
 
 static Config cfg_of(const bmo_config* c) {
@@ -107,6 +113,9 @@ static Config cfg_of(const bmo_config* c) {
     cfg.shift_radius = c->shift_radius;
     cfg.shift_step = c->shift_step;
     cfg.threads = c->threads;
+    cfg.auto_bands = c->auto_bands != 0;
+    cfg.prune_after_band = c->prune_after_band != 0;
+    if (c->n_thresholds > 0) cfg.band_thresholds.assign(c->thresholds, c->thresholds + c->n_thresholds);
     return cfg;
 }
 
@@ -285,6 +294,30 @@ int bmo_seed_candidates(int L, const double* xi, int l_low, double step, int max
     }
 }
 // out_trace: rows of [band, iter, alpha, beta, gamma, score, gnorm] (max_trace rows)
+// energy_ratio / select_bands (xcorr.cpp:129-137, optimize.cpp:179-195)
+int bmo_energy_ratio(int L, const double* xi, int l_cut, double* out) {
+    try {
+        *out = energy_ratio(unpack_xi(L, xi), l_cut);
+        return 0;
+    } catch (const std::domain_error& e) {
+        g_err = e.what();
+        return 3;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+int bmo_select_bands(int L, const double* xi, const double* thresholds, int n_thr, int* out_bands) {
+    try {
+        const auto b = select_bands(unpack_xi(L, xi), std::vector<double>(thresholds, thresholds + n_thr));
+        for (size_t i = 0; i < b.size(); ++i) out_bands[i] = b[i];
+        return (int)b.size();
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
 int bmo_refine(int L, const double* xi, const double* start, const bmo_config* c, int L_wp,
                const double* wp, double* out_quat, double* out_score, int* out_converged,
                double* out_trace, int max_trace, int* n_trace, long long* n_evals) {
@@ -337,6 +370,8 @@ int bmo_align(int n, const double* tmpl, const double* sub, const bmo_config* c,
         out->template_norm = r.template_norm;
         out->subtomo_norm = r.subtomo_norm;
         out->windows = r.windows;
+        out->n_bands = (int)std::min<size_t>(r.bands.size(), 16);
+        for (int b = 0; b < out->n_bands; ++b) out->bands[b] = r.bands[b];
         return 0;
     } catch (const std::exception& e) {
         return fail(e, 1);

@@ -46,18 +46,20 @@ D = C.c_double
 
 
 class AlignConfig(C.Structure):
-    """bm_align_config: OptimizerConfig (include/ballmatch/optimize.hpp:15-32), fixed bands."""
+    """bm_align_config: OptimizerConfig (include/ballmatch/optimize.hpp:15-32)."""
     _fields_ = [("n_bands", C.c_int), ("bands", C.c_int * 16), ("seed_grid_step", C.c_double),
                 ("max_candidates", C.c_int), ("newton_max_iter", C.c_int),
                 ("grad_tol", C.c_double), ("step_damping", C.c_double),
-                ("shift_radius", C.c_int), ("shift_step", C.c_int), ("accept_tol", C.c_double)]
+                ("shift_radius", C.c_int), ("shift_step", C.c_int), ("accept_tol", C.c_double),
+                ("auto_bands", C.c_int), ("prune_after_band", C.c_int), ("n_thresholds", C.c_int),
+                ("thresholds", C.c_double * 8)]
 
 
 class AlignResult(C.Structure):
     _fields_ = [("shift", C.c_int * 3), ("quat", C.c_double * 4), ("score", C.c_double),
                 ("converged", C.c_int), ("candidates", C.c_longlong),
                 ("evaluations", C.c_longlong), ("subtomo_norm", C.c_double),
-                ("windows", C.c_int)]
+                ("windows", C.c_int), ("n_bands", C.c_int), ("bands", C.c_int * 16)]
 
 
 class WindowResult(C.Structure):

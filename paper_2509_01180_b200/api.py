@@ -35,10 +35,16 @@ FP32_GRAD_TOL = 1e-5
 
 def make_config(bands=(7, 12, 33), seed_grid_step=np.pi / 8, max_candidates=20,
                 newton_max_iter=30, grad_tol=1e-7, step_damping=1e-3, shift_radius=4,
-                shift_step=2, accept_tol=None) -> _lib.AlignConfig:
+                shift_step=2, accept_tol=None, auto_bands=False, prune_after_band=False,
+                band_thresholds=(0.5, 0.25, 0.05)) -> _lib.AlignConfig:
     """OptimizerConfig defaults (include/ballmatch/optimize.hpp:15-32); grad_tol is
     floored at the FP32 evaluation's resolution unless accept_tol is given explicitly."""
     c = _lib.AlignConfig()
+    c.auto_bands = 1 if auto_bands else 0
+    c.prune_after_band = 1 if prune_after_band else 0
+    c.n_thresholds = len(band_thresholds)
+    for i, t in enumerate(band_thresholds):
+        c.thresholds[i] = float(t)
     c.n_bands = len(bands)
     for i, b in enumerate(bands):
         c.bands[i] = int(b)
@@ -179,7 +185,8 @@ class Context:
                                              C.byref(cfg), out, self._stream(v)), "align")
         return [dict(shift=tuple(r.shift), quat=np.array(r.quat[:]), score=r.score,
                      converged=bool(r.converged), candidates=r.candidates,
-                     evaluations=r.evaluations, subtomo_norm=r.subtomo_norm, windows=r.windows)
+                     evaluations=r.evaluations, subtomo_norm=r.subtomo_norm, windows=r.windows,
+                     bands=[int(b) for b in r.bands[:r.n_bands]])
                 for r in out[:count]]
 
     def average_accumulate(self, particles, results, out=None):

@@ -11,8 +11,10 @@
 #include <array>
 #include <cfloat>
 #include <cmath>
+#include <complex>
 #include <cstdio>
 #include <cstdlib>
+#include <map>
 #include <stdexcept>
 
 #include "context.hpp"
@@ -31,7 +33,12 @@ void ck(cudaError_t e, const char* what) {
 }  // namespace
 
 void AlignConfig::validate(int l_max) const {
-    if (bands.empty()) throw std::invalid_argument("config: need fixed bands or auto band selection");
+    for (size_t i = 1; i < band_thresholds.size(); ++i)
+        if (!(band_thresholds[i - 1] >= band_thresholds[i]))
+            throw std::invalid_argument("config: band thresholds must be strictly decreasing");
+    for (double t : band_thresholds)
+        if (!(t > 0.0 && t < 1.0)) throw std::invalid_argument("config: band thresholds must lie in (0,1)");
+    if (bands.empty() && !auto_bands) throw std::invalid_argument("config: need fixed bands or auto band selection");
     for (size_t i = 0; i < bands.size(); ++i) {
         if (bands[i] < 0 || bands[i] > l_max) throw std::invalid_argument("config: bands must lie in [0, l_max]");
         if (i > 0 && bands[i] <= bands[i - 1]) throw std::invalid_argument("config: bands must be strictly increasing");
@@ -373,8 +380,10 @@ void Context::refine_windows(int nw, int maxc, const AlignConfig& cfg, const Qua
                         timer.launches += 2;
                     }
                 }
-                if (bi + 1 == cfg.bands.size()) {
-                    // final unanchored score at the top band (optimize.cpp:349-352)
+                const bool prune_now = cfg.prune_after_band && cfg.bands.size() > 1 && bi == 0;
+                if (bi + 1 == cfg.bands.size() || prune_now) {
+                    // final unanchored score at the top band (optimize.cpp:349-352), or at
+                    // the first band before prune_after_band keeps each window's winner
                     ck(cudaMemsetAsync(d_counts, 0, sizeof(int), stream), "final count");
                     launch_final_prep(a, stream);
                     cudaEvent_t ef = timer.begin(stream);
@@ -382,6 +391,10 @@ void Context::refine_windows(int nw, int maxc, const AlignConfig& cfg, const Qua
                     timer.end(K_EVAL0, ef, stream);
                     launch_final_score(a, (int)slots, stream);
                     timer.launches += 3;
+                    if (prune_now) {
+                        launch_prune(a, stream);
+                        ++timer.launches;
+                    }
                 }
                 ++timer.refine_launches;
                 timer.end(K_REFINE, r0, stream);
@@ -401,6 +414,7 @@ void Context::refine_windows(int nw, int maxc, const AlignConfig& cfg, const Qua
         ra.win_particle = win_vol.as<int>() + w0;
         ra.win_shift = win_shift.as<int>() + 3 * w0;
         ra.grid_evals = grid_evals;
+        ra.extra_candidates = (cfg.prune_after_band && cfg.bands.size() > 1) ? 1 : 0;
         ra.out = outcome_.as<WindowOutcome>() + w0;
         launch_window_reduce(ra, stream);
         ++timer.launches;
@@ -492,20 +506,119 @@ std::vector<ParticleResult> Context::align_batch(const float* particles, int cou
         timer.end(K_WEDGE, w0, stream);
         fw = filtered.as<float>();
     }
+    if (!cfg.auto_bands) {
+        std::vector<int> all(count);
+        for (int p = 0; p < count; ++p) all[p] = p;
+        align_group(fw, count, all, cfg, out);
+        return out;
+    }
+    // auto_bands (optimize.cpp:455-460): each particle's schedule from its zero-shift
+    // kernel; particles sharing a schedule are aligned together
+    const std::vector<std::vector<int>> sched = auto_band_schedules(fw, count, cfg.band_thresholds);
+    std::map<std::vector<int>, std::vector<int>> groups;
+    for (int p = 0; p < count; ++p) groups[sched[p]].push_back(p);
+    for (const auto& [bands, members] : groups) {
+        AlignConfig c = cfg;
+        c.auto_bands = false;
+        c.bands = bands;
+        c.validate(basis.l_max);
+        align_group(fw, count, members, c, out);
+    }
+    return out;
+}
+
+// select_bands (optimize.cpp:179-195) of xi_coefficients(expand(f_w), t_hat) for every
+// particle: band energies ||xi_l||^2 in FP64 on the host from the FP32 expansions
+std::vector<std::vector<int>> Context::auto_band_schedules(const float* fw, int count,
+                                                           const std::vector<double>& thresholds) {
+    const long long vstride = (long long)n * n * n;
+    std::vector<int> wv(count), ws(3 * (size_t)count, 0);
+    for (int p = 0; p < count; ++p) wv[p] = p;
+    expand_windows(fw, vstride, count, wv, ws);
+    const int ld = geo.m_pad, C = geo.coeffs, L = basis.l_max;
+    std::vector<float> f((size_t)count * ld), t(ld);
+    ck(cudaMemcpyAsync(f.data(), coef.p, sizeof(float) * f.size(), cudaMemcpyDeviceToHost, stream), "auto bands f");
+    ck(cudaMemcpyAsync(t.data(), t_hat.p, sizeof(float) * ld, cudaMemcpyDeviceToHost, stream), "auto bands t");
+    ck(cudaStreamSynchronize(stream), "auto bands");
+    (void)C;
+    std::vector<std::vector<int>> out(count);
+    int zero_energy = 0;
+#pragma omp parallel for schedule(dynamic) reduction(| : zero_energy)
+    for (int p = 0; p < count; ++p) {
+        const float* fp = f.data() + (size_t)p * ld;
+        std::vector<double> energy(L + 1, 0.0);
+        std::vector<std::complex<double>> Fm, Tm;
+        for (int l = 0; l <= L; ++l) {
+            const int nk = basis.radial_count(l), w = 2 * l + 1;
+            Fm.assign((size_t)nk * w, 0.0);
+            Tm.assign((size_t)nk * w, 0.0);
+            for (int k = 0; k < nk; ++k)
+                for (int m = -l; m <= l; ++m) {
+                    const int am = m < 0 ? -m : m;
+                    auto val = [&](const float* src) {
+                        const float* row = src + basis.block_off[l] + k * w;
+                        std::complex<double> z = am == 0 ? std::complex<double>(row[0], 0.0)
+                                                         : std::complex<double>(row[2 * am - 1], row[2 * am]);
+                        if (m < 0) z = ((am & 1) ? -1.0 : 1.0) * std::conj(z);  // real-volume symmetry
+                        return z;
+                    };
+                    Fm[(size_t)k * w + (m + l)] = val(fp);
+                    Tm[(size_t)k * w + (m + l)] = val(t.data());
+                }
+            double e = 0.0;
+            for (int m = 0; m < w; ++m)
+                for (int mp = 0; mp < w; ++mp) {
+                    std::complex<double> x = 0.0;
+                    for (int k = 0; k < nk; ++k) x += std::conj(Fm[(size_t)k * w + m]) * Tm[(size_t)k * w + mp];
+                    e += std::norm(x);
+                }
+            energy[l] = e;
+        }
+        double total = 0.0;
+        for (double e : energy) total += e;
+        if (!(total > 0.0)) {
+            zero_energy = 1;
+            continue;
+        }
+        std::vector<double> ratio(L + 1, 0.0);
+        for (int l = 0; l <= L; ++l) {
+            double high = 0.0;
+            for (int j = l + 1; j <= L; ++j) high += energy[j];
+            ratio[l] = high / total;
+        }
+        std::vector<int> bands;
+        for (double tau : thresholds)
+            for (int l = 0; l <= L; ++l)
+                if (ratio[l] <= tau) {
+                    bands.push_back(l);
+                    break;
+                }
+        std::sort(bands.begin(), bands.end());
+        bands.erase(std::unique(bands.begin(), bands.end()), bands.end());
+        out[p] = bands;
+    }
+    if (zero_energy) throw std::domain_error("energy_ratio: zero kernel energy");
+    return out;
+}
+
+// coarse + fine shift stages of align() (optimize.cpp:463-521) for the listed
+// particles (indices into the n_vol volumes at fw), all with cfg.bands
+void Context::align_group(const float* fw, int n_vol, const std::vector<int>& parts, const AlignConfig& cfg,
+                          std::vector<ParticleResult>& out) {
     std::vector<std::array<int, 3>> coarse;
     for (int z = -cfg.shift_radius; z <= cfg.shift_radius; z += cfg.shift_step)
         for (int y = -cfg.shift_radius; y <= cfg.shift_radius; y += cfg.shift_step)
             for (int x = -cfg.shift_radius; x <= cfg.shift_radius; x += cfg.shift_step) coarse.push_back({x, y, z});
     std::vector<int> wv, ws;
-    for (int p = 0; p < count; ++p)
+    for (int p : parts)
         for (const auto& s : coarse) {
             wv.push_back(p);
             ws.insert(ws.end(), s.begin(), s.end());
         }
-    std::vector<WindowOutcome> oc = run_windows(fw, count, wv, ws, cfg);
-    std::vector<int> best(count, -1);
-    std::vector<long long> cand(count, 0), evals(count, 0);
-    std::vector<int> nwin(count, 0);
+    std::vector<WindowOutcome> oc = run_windows(fw, n_vol, wv, ws, cfg);
+    std::vector<int> best(n_vol, -1);
+    std::vector<long long> cand(n_vol, 0), evals(n_vol, 0);
+    std::vector<int> nwin(n_vol, 0);
     for (size_t i = 0; i < oc.size(); ++i) {
         const int p = oc[i].particle;
         cand[p] += oc[i].n_cand;
@@ -513,11 +626,11 @@ std::vector<ParticleResult> Context::align_batch(const float* particles, int cou
         ++nwin[p];
         if (oc[i].valid && (best[p] < 0 || better(oc[i], oc[best[p]]))) best[p] = (int)i;
     }
-    for (int p = 0; p < count; ++p)
+    for (int p : parts)
         if (best[p] < 0) throw std::invalid_argument("align: no usable shift window (empty subtomogram)");
     // fine pass: unit-step cube around the coarse winner, minus coarse points (optimize.cpp:490-501)
     std::vector<int> fv, fs;
-    for (int p = 0; p < count; ++p) {
+    for (int p : parts) {
         const int* b = oc[best[p]].shift;
         for (int z = -cfg.shift_step; z <= cfg.shift_step; ++z)
             for (int y = -cfg.shift_step; y <= cfg.shift_step; ++y)
@@ -528,9 +641,9 @@ std::vector<ParticleResult> Context::align_batch(const float* particles, int cou
                     fs.insert(fs.end(), s.begin(), s.end());
                 }
     }
-    std::vector<WindowOutcome> fo = run_windows(fw, count, fv, fs, cfg);
-    std::vector<WindowOutcome> bestw(count);
-    for (int p = 0; p < count; ++p) bestw[p] = oc[best[p]];
+    std::vector<WindowOutcome> fo = run_windows(fw, n_vol, fv, fs, cfg);
+    std::vector<WindowOutcome> bestw(n_vol);
+    for (int p : parts) bestw[p] = oc[best[p]];
     for (const auto& o : fo) {
         const int p = o.particle;
         cand[p] += o.n_cand;
@@ -538,7 +651,7 @@ std::vector<ParticleResult> Context::align_batch(const float* particles, int cou
         ++nwin[p];
         if (o.valid && better(o, bestw[p])) bestw[p] = o;
     }
-    for (int p = 0; p < count; ++p) {
+    for (int p : parts) {
         ParticleResult& r = out[p];
         for (int i = 0; i < 3; ++i) r.shift[i] = bestw[p].shift[i];
         for (int i = 0; i < 4; ++i) r.quat[i] = bestw[p].quat[i];
@@ -548,8 +661,8 @@ std::vector<ParticleResult> Context::align_batch(const float* particles, int cou
         r.evaluations = evals[p];
         r.subtomo_norm = bestw[p].sub_norm;
         r.windows = nwin[p];
+        r.bands = cfg.bands;
     }
-    return out;
 }
 
 void Context::read_eval_stats(long long* evals, double* flops, bool reset) {

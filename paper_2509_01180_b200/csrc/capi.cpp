@@ -1,6 +1,7 @@
 // extern "C" boundary of libballmatch_b200 (declared in include/ballmatch_b200.h).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -169,9 +170,13 @@ int bm_expand(bm_context* ctx, const float* vols, int count, const int* shifts, 
 
 static bmb::AlignConfig cfg_of(const bm_align_config* c) {
     if (!c) throw std::invalid_argument("null config");
-    if (c->n_bands < 1 || c->n_bands > 16) throw std::invalid_argument("config: need fixed bands or auto band selection");
+    if (c->n_bands < 0 || c->n_bands > 16) throw std::invalid_argument("config: at most 16 bands");
+    if (c->n_thresholds < 0 || c->n_thresholds > 8) throw std::invalid_argument("config: at most 8 band thresholds");
     bmb::AlignConfig a;
     a.bands.assign(c->bands, c->bands + c->n_bands);
+    a.auto_bands = c->auto_bands != 0;
+    a.prune_after_band = c->prune_after_band != 0;
+    if (c->n_thresholds > 0) a.band_thresholds.assign(c->thresholds, c->thresholds + c->n_thresholds);
     a.seed_grid_step = c->seed_grid_step;
     a.max_candidates = c->max_candidates;
     a.newton_max_iter = c->newton_max_iter;
@@ -215,6 +220,8 @@ int bm_align_batch(bm_context* ctx, const float* particles, int count, const bm_
             o.evaluations = r.evaluations;
             o.subtomo_norm = r.subtomo_norm;
             o.windows = r.windows;
+            o.n_bands = (int)std::min<size_t>(r.bands.size(), 16);
+            for (int j = 0; j < o.n_bands; ++j) o.bands[j] = r.bands[j];
         }
         return (int)BM_OK;
     });

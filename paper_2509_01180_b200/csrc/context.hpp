@@ -86,6 +86,9 @@ struct AlignConfig {
     int shift_radius;
     int shift_step;
     double accept_tol;
+    bool auto_bands = false;
+    bool prune_after_band = false;
+    std::vector<double> band_thresholds{0.5, 0.25, 0.05};
     void validate(int l_max) const;  // OptimizerConfig::validate (optimize.cpp:153-177)
 };
 
@@ -98,6 +101,7 @@ struct ParticleResult {
     long long evaluations;
     double subtomo_norm;
     int windows;
+    std::vector<int> bands;
 };
 
 // Per-kernel-class CUDA-event timing on the context stream (bench evidence).
@@ -196,6 +200,9 @@ public:
                                            const std::vector<int>& wshift, const AlignConfig& cfg);
     // align() for a batch of particles (coarse + fine shift stages)
     std::vector<ParticleResult> align_batch(const float* particles, int count, const AlignConfig& cfg);
+    void align_group(const float* fw, int n_vol, const std::vector<int>& parts, const AlignConfig& cfg,
+                     std::vector<ParticleResult>& out);
+    std::vector<std::vector<int>> auto_band_schedules(const float* fw, int count, const std::vector<double>& thresholds);
 
     // rotate-score-gradient sweep (config 4): kernels from coefficient pairs
     DevBuf work_f, work_xi, filtered;

@@ -1036,6 +1036,36 @@ __global__ void final_score_kernel(StageArgs a) {
     }
 }
 
+// prune_after_band (optimize.cpp:391-403): after the first band every candidate
+// has its unanchored band-0 score; each window keeps its best (first on ties) and
+// restarts it as a fresh refine() from that result for the remaining bands
+__global__ void prune_kernel(StageArgs a) {
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= a.n_win) return;
+    const int nc = a.cand_count[w];
+    CandState* cs = a.cand + (size_t)w * a.max_cand;
+    int best = -1;
+    for (int c = 0; c < nc; ++c)
+        if (cs[c].active && (best < 0 || cs[c].score > cs[best].score)) best = c;
+    for (int c = 0; c < nc; ++c)
+        if (c != best) cs[c].active = 0;
+    if (best < 0) return;
+    CandState& st = cs[best];
+    const double* q = st.diverged ? st.best_g : st.g;
+    const double g0 = q[0], g1 = q[1], g2 = q[2], g3 = q[3];
+    st.g[0] = st.best_g[0] = g0;
+    st.g[1] = st.best_g[1] = g1;
+    st.g[2] = st.best_g[2] = g2;
+    st.g[3] = st.best_g[3] = g3;
+    st.anchor[0] = 1.0;
+    st.anchor[1] = st.anchor[2] = st.anchor[3] = 0.0;
+    st.anchored = 0;
+    st.anchor_limit = -1;
+    st.diverged = 0;
+    st.band_converged = 0;
+    st.best_score = -DBL_MAX * 2.0;  // -inf
+}
+
 __global__ void window_reduce_kernel(ReduceArgs a) {
     const int w = blockIdx.x * blockDim.x + threadIdx.x;
     if (w >= a.n_win) return;
@@ -1046,7 +1076,7 @@ __global__ void window_reduce_kernel(ReduceArgs a) {
     o.shift[0] = a.win_shift[3 * w];
     o.shift[1] = a.win_shift[3 * w + 1];
     o.shift[2] = a.win_shift[3 * w + 2];
-    o.n_cand = nc;
+    o.n_cand = nc + (nc > 0 ? a.extra_candidates : 0);
     o.sub_norm = a.sub_norm[w];
     o.valid = (nc > 0 && o.sub_norm > 0.0) ? 1 : 0;
     o.evals = a.grid_evals;
@@ -1055,6 +1085,7 @@ __global__ void window_reduce_kernel(ReduceArgs a) {
     for (int c = 0; c < nc; ++c) {
         const CandState& st = cs[c];
         o.evals += st.evals;
+        if (!st.active) continue;  // pruned after the first band
         const double ang = q_angle(qload(st.diverged ? st.best_g : st.g));
         // search_one_shift tie rule (optimize.cpp:405-412)
         if (best < 0 || st.score > bs || (st.score == bs && ang < ba)) {
@@ -1209,6 +1240,9 @@ void launch_final_prep(const StageArgs& a, cudaStream_t s) {
 }
 void launch_final_score(const StageArgs& a, int max_n, cudaStream_t s) {
     final_score_kernel<<<thread_grid(max_n), kNB, 0, s>>>(a);
+}
+void launch_prune(const StageArgs& a, cudaStream_t s) {
+    prune_kernel<<<(a.n_win + 127) / 128, 128, 0, s>>>(a);
 }
 void launch_window_reduce(const ReduceArgs& a, cudaStream_t s) {
     window_reduce_kernel<<<(a.n_win + 127) / 128, 128, 0, s>>>(a);

@@ -66,6 +66,7 @@ struct ReduceArgs {
     const int* win_particle = nullptr;
     const int* win_shift = nullptr;
     long long grid_evals = 0;
+    int extra_candidates = 0;   // prune_after_band: the winner's second refine() run
     WindowOutcome* out = nullptr;
 };
 
@@ -81,6 +82,7 @@ void launch_accept(const StageArgs& a, const int* list_in, const int* count_in, 
 void launch_final_prep(const StageArgs& a, cudaStream_t s);
 void launch_final_score(const StageArgs& a, int max_n, cudaStream_t s);
 void launch_window_reduce(const ReduceArgs& a, cudaStream_t s);
+void launch_prune(const StageArgs& a, cudaStream_t s);
 
 // standalone batched evaluation (rotate-score-gradient sweep, config 4):
 // value + gradient of C(g) = Re sum xi D(g) for n_xi kernels x n_rot angle

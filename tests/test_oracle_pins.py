@@ -541,3 +541,69 @@ def test_align_recovers_known_rotation_and_shift_noiseless():
     r = bmo.align(t, s, cfg)
     assert r["shift"] == sh
     assert bmo.geodesic_degrees(r["quat"], q_true) < 0.5
+
+
+def test_energy_ratio_formula_monotonicity_errors(xfix):
+    """test_xcorr.cpp:206-236: energy_ratio vs a two-pass oracle, non-increasing in
+    l_cut, zero at l_max, domain error for an all-zero kernel."""
+    L, xi = xfix["L"], xfix["xi"]
+    assert bmo.energy_ratio(xi, L, L) == 0.0
+    for l_cut in (0, 2, 5, L):
+        high = total = 0.0
+        for l in range(L + 1):
+            e = float(np.sum(np.abs(bmo.xi_block(xi, l)) ** 2))
+            total += e
+            high += e if l > l_cut else 0.0
+        assert bmo.energy_ratio(xi, L, l_cut) == pytest.approx(high / total, rel=1e-12)
+    prev = 1.1
+    for l in range(L + 1):
+        r = bmo.energy_ratio(xi, L, l)
+        assert 0.0 <= r <= prev + 1e-15
+        prev = r
+    with pytest.raises(ArithmeticError):
+        bmo.energy_ratio(np.zeros(bmo.xi_count(3), dtype=np.complex128), 3, 1)
+
+
+def test_select_bands_degenerate_and_minimal(ofix):
+    """test_optimize.cpp:67-100: a DC-only kernel selects {0}; on the self kernel every
+    selected band is the linear-scan minimum for some threshold."""
+    dc = np.zeros(bmo.xi_count(8), dtype=np.complex128)
+    dc[0] = 3.0
+    assert bmo.select_bands(dc, 8, [0.5, 0.25, 0.05]) == [0]
+    L, xi = 16, ofix["self_xi"]
+    th = [0.5, 0.25, 0.05]
+    bands = bmo.select_bands(xi, L, th)
+    assert bands and bands == sorted(bands) and bands[-1] <= L
+    ratio = [bmo.energy_ratio(xi, L, l) for l in range(L + 1)]
+    for tau in th:
+        expect = next(l for l in range(L + 1) if ratio[l] <= tau)
+        assert expect in bands
+    for b in bands:
+        assert ratio[b] <= th[0] + 1e-15
+        if b > 0:
+            assert any(ratio[b] <= tau < ratio[b - 1] for tau in th)
+
+
+def test_align_auto_bands_and_prune_after_band():
+    """OptimizerConfig.auto_bands (optimize.cpp:455-460): the schedule is the
+    zero-shift kernel's select_bands; prune_after_band (optimize.cpp:391-403) on a
+    noiseless phantom recovers the truth (< 0.5 deg, exact shift)."""
+    n, L = 32, 8
+    tmpl = bmo.gaussian_blob_template(n, 20, 3)
+    sub, q, sh = bmo.make_particle(tmpl, 11, 2, None, None)
+    spec = bmo.Spec(L, L * PI)
+    cfg = bmo.make_config(l_max=L, lambda_cut=L * PI, bands=(), auto_bands=True, max_candidates=8,
+                          shift_radius=2, shift_step=2)
+    r = bmo.align(tmpl, sub, cfg)
+    f0 = bmo.expand(sub, spec)
+    assert r["bands"] == bmo.select_bands(bmo.xi_coefficients(f0, bmo.expand(tmpl, spec), spec), L,
+                                          [0.5, 0.25, 0.05])
+    # (the selected schedule, e.g. [0, 1] for this smooth template, is too coarse to
+    # recover the rotation: auto selection is a reference option, not an accuracy claim)
+    assert r["windows"] > 0 and np.isfinite(r["score"])
+    cfg = bmo.make_config(l_max=L, lambda_cut=L * PI, bands=(4, 8), prune_after_band=True, max_candidates=8,
+                          shift_radius=2, shift_step=2)
+    r = bmo.align(tmpl, sub, cfg)
+    assert tuple(r["shift"]) == sh and bmo.geodesic_degrees(r["quat"], q) < 0.5
+    with pytest.raises(ValueError):
+        bmo.align(tmpl, sub, bmo.make_config(l_max=L, bands=(), auto_bands=False))
