@@ -52,6 +52,29 @@ def _compile(src: Path, verbose: bool) -> Path:
     return obj
 
 
+CLI_SRC = PKG / "cli" / "ballmatch_b200_cli.cpp"
+CLI_BIN = PKG / "bin" / "ballmatch-b200"
+CUDA_HOME = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
+
+
+def build_cli(verbose: bool = False, force: bool = False) -> Path:
+    """The ballmatch-b200 command-line front end (host C++ over the C ABI)."""
+    CLI_BIN.parent.mkdir(parents=True, exist_ok=True)
+    deps = [CLI_SRC, LIB, *(ROOT / "include").glob("*.h*")]
+    if not force and CLI_BIN.exists() and all(d.stat().st_mtime <= CLI_BIN.stat().st_mtime for d in deps):
+        return CLI_BIN
+    cxx = "/usr/bin/g++" if Path("/usr/bin/g++").exists() else "g++"
+    cmd = [cxx, "-O2", "-std=c++20", "-Wall", "-I", str(ROOT / "include"), "-I", str(CUDA_HOME / "include"),
+           str(CLI_SRC), "-o", str(CLI_BIN), "-L", str(PKG), "-lballmatch_b200", "-L", str(CUDA_HOME / "lib64"),
+           "-lcudart", "-Wl,-rpath,$ORIGIN/..", "-Wl,-rpath," + str(CUDA_HOME / "lib64")]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"cli build failed:\n{r.stdout}\n{r.stderr}")
+    return CLI_BIN
+
+
 def build(verbose: bool = False, force: bool = False) -> Path:
     OBJ.mkdir(parents=True, exist_ok=True)
     if force:
@@ -67,6 +90,7 @@ def build(verbose: bool = False, force: bool = False) -> Path:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    build_cli(verbose, force)
     return LIB
 
 
