@@ -55,6 +55,11 @@ int bm_context_info(const bm_context* ctx, long long* info);
  * operator on the tensor cores (gather + bm_split3_gemm; the operator is built
  * on first use).  Both follow expand() (src/basis.cpp:254-328). */
 int bm_context_set_expand_mode(bm_context* ctx, int mode);
+/* Concurrent lanes of bm_align_batch: a batch of at least lanes * min_per_lane
+ * particles is split into `lanes` slices aligned concurrently, each on its own
+ * stream with its own buffers and host thread (default 3 lanes, 64 particles per
+ * lane).  Results do not depend on the lane count. */
+int bm_context_set_lanes(bm_context* ctx, int lanes, int min_per_lane);
 /* lambda_cut actually used by the context */
 double bm_context_lambda_cut(const bm_context* ctx);
 /* radial roots / norms of degree l (BasisSpec::root/norm, basis.hpp:40-41); returns count k_l */

@@ -272,6 +272,10 @@ class Context:
                                             C.c_void_p(out.data_ptr()), self._stream(out)), "synthesize")
         return out
 
+    def set_lanes(self, lanes: int, min_per_lane: int = 64):
+        """Concurrent lanes of align_batch (default 3 lanes of >= 64 particles)."""
+        _lib.check(_lib.lib().bm_context_set_lanes(self._h, lanes, min_per_lane), "set_lanes")
+
     def set_expand_mode(self, mode: str):
         """'factored' (default) or 'gemm' (dense operator on the tensor cores)."""
         _lib.check(_lib.lib().bm_context_set_expand_mode(self._h, {"factored": 0, "gemm": 1}[mode]),

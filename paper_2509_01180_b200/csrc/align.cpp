@@ -16,6 +16,7 @@
 #include <cstdlib>
 #include <map>
 #include <stdexcept>
+#include <thread>
 
 #include "context.hpp"
 #include "refine.cuh"
@@ -224,6 +225,12 @@ void Context::set_template(const float* tmpl, double wedge_theta) {
     bands_.clear();
     seeds_.clear();
     has_template = true;
+    // the lanes re-adopt the template on their next use
+    tmpl_copy_.reserve(sizeof(float) * (size_t)n * n * n);
+    ck(cudaMemcpyAsync(tmpl_copy_.p, tmpl, sizeof(float) * (size_t)n * n * n, cudaMemcpyDeviceToDevice, stream),
+       "template copy");
+    ck(cudaStreamSynchronize(stream), "template copy");
+    lanes_stale_ = true;
 }
 
 // Bulk-synchronous damped Newton over every candidate of every window
@@ -494,6 +501,95 @@ bool better(const WindowOutcome& a, const WindowOutcome& b) {
 std::vector<ParticleResult> Context::align_batch(const float* particles, int count, const AlignConfig& cfg) {
     if (!has_template) throw std::invalid_argument("align: set_template first");
     cfg.validate(basis.l_max);
+    const int k = std::max(1, std::min(lanes, count / std::max(1, lane_min_particles)));
+    if (k <= 1) return align_batch_lane(particles, count, cfg);
+    ensure_lanes();
+    // the lanes start after the work already queued on this context's stream
+    cudaEvent_t ready;
+    ck(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming), "lane event");
+    ck(cudaEventRecord(ready, stream), "lane event");
+    const long long vstride = (long long)n * n * n;
+    std::vector<int> off(k + 1, 0);
+    for (int i = 0; i < k; ++i) off[i + 1] = off[i] + count / k + (i < count % k ? 1 : 0);
+    std::vector<std::vector<ParticleResult>> part(k);
+    std::vector<std::exception_ptr> err(k);
+    std::vector<std::thread> threads;
+    for (int i = 1; i < k; ++i)
+        threads.emplace_back([&, i] {
+            try {
+                Context& c = *lane_ctx_[i - 1];
+                ck(cudaSetDevice(device), "lane device");
+                ck(cudaStreamWaitEvent(c.stream, ready, 0), "lane wait");
+                c.timer.on = timer.on;
+                part[i] = c.align_batch_lane(particles + off[i] * vstride, off[i + 1] - off[i], cfg);
+            } catch (...) {
+                err[i] = std::current_exception();
+            }
+        });
+    try {
+        part[0] = align_batch_lane(particles, off[1], cfg);
+    } catch (...) {
+        err[0] = std::current_exception();
+    }
+    for (auto& t : threads) t.join();
+    cudaEventDestroy(ready);
+    for (auto& e : err)
+        if (e) std::rethrow_exception(e);
+    std::vector<ParticleResult> out;
+    out.reserve(count);
+    for (int i = 0; i < k; ++i) {
+        out.insert(out.end(), part[i].begin(), part[i].end());
+        if (i > 0) timer.absorb(lane_ctx_[i - 1]->timer);
+    }
+    return out;
+}
+
+void Context::ensure_lanes() {
+    while ((int)lane_ctx_.size() < lanes - 1) {
+        auto c = std::make_unique<Context>(device, n, basis.l_max, basis.lambda_cut);
+        c->lanes = 1;
+        lane_ctx_.push_back(std::move(c));
+    }
+    for (auto& c : lane_ctx_) {
+        c->expand_mode = expand_mode;
+        c->pool_budget_ = pool_budget_;  // each lane allocates only what its slice needs
+    }
+    if (lanes_stale_) {
+        for (auto& c : lane_ctx_) c->adopt_template(*this);
+        lanes_stale_ = false;
+    }
+}
+
+// a lane's template state: its own expansion of the template and wedge filter,
+// the wedge-power factors copied from the main context
+void Context::adopt_template(const Context& src) {
+    std::vector<int> wv{0}, ws{0, 0, 0};
+    expand_windows(src.tmpl_copy_.as<float>(), (long long)n * n * n, 1, wv, ws);
+    t_hat.reserve(sizeof(float) * geo.m_pad);
+    ck(cudaMemcpyAsync(t_hat.p, coef.p, sizeof(float) * geo.m_pad, cudaMemcpyDeviceToDevice, stream), "t_hat");
+    t_norm = src.t_norm;
+    wedge_deg = src.wedge_deg;
+    wedge.reset();
+    chi_hat = src.chi_hat;
+    q_hat = src.q_hat;
+    wp_total = src.wp_total;
+    if (src.wedge) {
+        wedge = std::make_unique<WedgeFilter>(n, wedge_deg, kWedgeTaperDeg);
+        std::vector<double2> cd(chi_hat.size()), qd(q_hat.size());
+        for (size_t i = 0; i < cd.size(); ++i) {
+            cd[i] = double2{chi_hat[i].real(), chi_hat[i].imag()};
+            qd[i] = double2{q_hat[i].real(), q_hat[i].imag()};
+        }
+        upload(chi_dev, cd, stream);
+        upload(q_dev, qd, stream);
+    }
+    ck(cudaStreamSynchronize(stream), "adopt template");
+    bands_.clear();
+    seeds_.clear();
+    has_template = true;
+}
+
+std::vector<ParticleResult> Context::align_batch_lane(const float* particles, int count, const AlignConfig& cfg) {
     std::vector<ParticleResult> out(count);
     if (count == 0) return out;
     const long long vstride = (long long)n * n * n;
@@ -680,6 +776,14 @@ void Context::read_eval_stats(long long* evals, double* flops, bool reset) {
                 (o ? e2 : e0) += (long long)c;
                 fl += (double)c * eval_flops(L, o ? 2 : 0, w != 0);
             }
+    for (auto& c : lane_ctx_) {
+        long long le[2] = {0, 0};
+        double lf = 0.0;
+        c->read_eval_stats(le, &lf, reset);
+        e2 += le[0];
+        e0 += le[1];
+        fl += lf;
+    }
     if (evals) evals[0] = e2, evals[1] = e0;
     if (flops) *flops = fl;
     if (reset) ck(cudaMemsetAsync(eval_stats(), 0, sizeof(unsigned long long) * kEvalStats, stream), "eval stats");

@@ -380,6 +380,16 @@ int bm_context_timings(bm_context* ctx, double* out_ms, long long* out_counts, i
     return BM_OK;
 }
 
+int bm_context_set_lanes(bm_context* ctx, int lanes, int min_per_lane) {
+    return guarded("bm_context_set_lanes", [&] {
+        if (!ctx) return (int)BM_ERR_STATE;
+        if (lanes < 1 || lanes > 8 || min_per_lane < 1) throw std::invalid_argument("lanes must be 1..8, min_per_lane >= 1");
+        ctx->impl->lanes = lanes;
+        ctx->impl->lane_min_particles = min_per_lane;
+        return (int)BM_OK;
+    });
+}
+
 int bm_context_set_expand_mode(bm_context* ctx, int mode) {
     return guarded("bm_context_set_expand_mode", [&] {
         if (!ctx) return (int)BM_ERR_STATE;

@@ -143,6 +143,16 @@ struct KernelTimer {
         for (double& x : ms) x = 0.0;
         launches = windows_expanded = gemm_launches = refine_launches = 0;
     }
+    // add another timer's totals (a lane's) and clear it
+    void absorb(KernelTimer& o) {
+        o.collect();
+        for (int i = 0; i < K_COUNT; ++i) ms[i] += o.ms[i];
+        launches += o.launches;
+        windows_expanded += o.windows_expanded;
+        gemm_launches += o.gemm_launches;
+        refine_launches += o.refine_launches;
+        o.reset();
+    }
 };
 
 class Context {
@@ -200,6 +210,17 @@ public:
                                            const std::vector<int>& wshift, const AlignConfig& cfg);
     // align() for a batch of particles (coarse + fine shift stages)
     std::vector<ParticleResult> align_batch(const float* particles, int count, const AlignConfig& cfg);
+    std::vector<ParticleResult> align_batch_lane(const float* particles, int count, const AlignConfig& cfg);
+    // concurrent lanes: sub-contexts with their own stream and buffers that align
+    // slices of a large batch from their own host threads (overlapping the
+    // low-occupancy tails of each lane's Newton loop)
+    int lanes = 3;
+    int lane_min_particles = 64;  // per lane
+    std::vector<std::unique_ptr<Context>> lane_ctx_;
+    DevBuf tmpl_copy_;
+    bool lanes_stale_ = true;
+    void ensure_lanes();
+    void adopt_template(const Context& src);
     void align_group(const float* fw, int n_vol, const std::vector<int>& parts, const AlignConfig& cfg,
                      std::vector<ParticleResult>& out);
     std::vector<std::vector<int>> auto_band_schedules(const float* fw, int count, const std::vector<double>& thresholds);

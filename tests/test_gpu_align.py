@@ -150,3 +150,27 @@ def test_prune_after_band_and_auto_bands_match_oracle(cuda_device, mode):
         assert got[p]["score"] == pytest.approx(ref["score"], rel=1e-4)
         # (candidate counters are not compared: a near-tied seed-grid maximum can add or
         # drop a candidate in a few windows, FP64 seed scores from FP32 vs FP64 expansions)
+
+
+def test_lanes_give_identical_results(cuda_device):
+    """bm_context_set_lanes: the batch split across concurrent lanes (own streams,
+    buffers and host threads) gives bit-identical results to one lane."""
+    import math
+
+    from paper_2509_01180_b200 import api
+
+    n, L = 32, 8
+    tmpl = api.make_template(n, 20, 5)
+    parts, _, _ = api.make_particles(tmpl, 12, 800, 2, 0.5, 60.0)
+    cfg = api.make_config(bands=(4, 8), max_candidates=8, shift_radius=2, shift_step=2)
+    out = {}
+    for lanes in (1, 3):
+        ctx = api.Context(n, L, L * math.pi)
+        ctx.set_template(tmpl, 60.0)
+        ctx.set_lanes(lanes, 2)
+        out[lanes] = ctx.align_batch(parts, cfg)
+    for a, b in zip(out[1], out[3]):
+        assert a["shift"] == b["shift"]
+        assert list(a["quat"]) == list(b["quat"])
+        assert a["score"] == b["score"]
+        assert a["evaluations"] == b["evaluations"]
