@@ -285,6 +285,8 @@ def run_product(args):
 
     # ---------------- one instrumented step: CUDA events around every launch on the
     # context stream (kernel shares for the roofline), outside the timed regions
+    # (one lane: concurrent lanes would overlap the kernels being timed)
+    ctx.set_lanes(1)
     ctx.set_timing(True)
     ctx.timings(reset=True)
     ctx.eval_stats(reset=True)
@@ -293,6 +295,7 @@ def run_product(args):
     kms, counts = ctx.timings(reset=True)
     ev2, ev0, ev_flops = ctx.eval_stats(reset=True)
     ctx.set_timing(False)
+    ctx.set_lanes(3)
     import ctypes
     from paper_2509_01180_b200 import _lib
     d2h = P * ctypes.sizeof(_lib.AlignResult) + avg.numel() * 8
@@ -365,7 +368,8 @@ def run_product(args):
         "roofline_refine_eval": roof_eval,
         "dominant_kernel": dominant,
         "kernel_ms_per_step": kernels,
-        "kernel_ms_note": "CUDA events on the context stream, one instrumented step outside the timed region",
+        "kernel_ms_note": "CUDA events on the context stream, one instrumented single-lane step outside the "
+                          "timed region (the timed region runs 3 concurrent lanes)",
         "refine": {"ms_per_step": refine_ms, "eval_kernels_ms_per_step": eval_ms,
                    "evaluations_per_step": evals_per_step,
                    "note": "evaluations_per_step counts the seed grid too (align() counters)"},
