@@ -16,6 +16,7 @@
 // (DESIGN.md §3 K2f): 16 S + 4 n_phi n_r n_theta (L+1) + 4 n_r tri(L) n_theta +
 // 2 n_r C FLOP, S = n_r n_theta n_phi — 4.47 MFLOP at config 2, about 120x fewer
 // than the dense 2 C V of the pulled-back operator.
+#include "smem_attr.hpp"
 #include "expand_factored.hpp"
 
 namespace bmb {
@@ -192,7 +193,7 @@ __global__ void __launch_bounds__(kThreads, BMB_EXPAND_MINB) expand_factored_ker
 template <int HALF, int RPT>
 int launch_t(const FactoredTables& T, size_t smem, const float* vols, long long vol_stride, const int* win_vol,
              const int* win_shift, int n_win, float* out, int ldo, cudaStream_t s) {
-    cudaFuncSetAttribute(expand_factored_kernel<HALF, RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    ensure_dynamic_smem(expand_factored_kernel<HALF, RPT>, (int)smem);
     expand_factored_kernel<HALF, RPT><<<n_win, kThreads, smem, s>>>(T, vols, vol_stride, win_vol, win_shift, out, ldo);
     return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }

@@ -27,6 +27,7 @@
 #include <cfloat>
 #include <cstdlib>
 
+#include "smem_attr.hpp"
 #include "refine.cuh"
 #include "rotation.cuh"
 
@@ -1192,7 +1193,7 @@ void launch_compose(const StageArgs& a, int n, cudaStream_t s) {
     if (n <= 0) return;
     const size_t smem = a.compose_smem ? compose_smem_bytes(a.T.L) : 0;
     if (smem) {
-        cudaFuncSetAttribute(compose_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        ensure_dynamic_smem(compose_kernel<true>, (int)smem);
         compose_kernel<true><<<n, 256, smem, s>>>(a);
     } else {
         compose_kernel<false><<<n, 256, 0, s>>>(a);
