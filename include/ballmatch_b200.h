@@ -60,6 +60,13 @@ int bm_context_set_expand_mode(bm_context* ctx, int mode);
  * stream with its own buffers and host thread (default 3 lanes, 64 particles per
  * lane).  Results do not depend on the lane count. */
 int bm_context_set_lanes(bm_context* ctx, int lanes, int min_per_lane);
+/* Refinement schedule of bm_align_batch (refine(), src/optimize.cpp:255-357):
+ * 0 = list-driven kernels (default: every phase of a Newton iteration is one
+ * launch over all candidates of all windows of the stage), 1 = fused per-window
+ * kernel (one persistent launch per stage: window kernels in shared memory, each
+ * warp iterating its own candidates; measured 4x slower).  Both
+ * run the same per-candidate arithmetic; outcomes are bit-identical. */
+int bm_context_set_refine_mode(bm_context* ctx, int mode);
 /* lambda_cut actually used by the context */
 double bm_context_lambda_cut(const bm_context* ctx);
 /* radial roots / norms of degree l (BasisSpec::root/norm, basis.hpp:40-41); returns count k_l */

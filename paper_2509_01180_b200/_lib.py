@@ -111,6 +111,8 @@ def _declare(L: C.CDLL) -> None:
     L.bm_synthesize.restype = I
     L.bm_context_set_lanes.argtypes = [P, I, I]
     L.bm_context_set_lanes.restype = I
+    L.bm_context_set_refine_mode.argtypes = [P, I]
+    L.bm_context_set_refine_mode.restype = I
     L.bm_context_set_expand_mode.argtypes = [P, I]
     L.bm_context_set_expand_mode.restype = I
     L.bm_context_eval_stats.argtypes = [P, P, P, I]

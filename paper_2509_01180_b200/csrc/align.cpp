@@ -428,6 +428,90 @@ void Context::refine_windows(int nw, int maxc, const AlignConfig& cfg, const Qua
     }
 }
 
+// Fused refinement (refine_fused_kernel): one launch per stage, persistent CTAs
+// pulling windows from a counter; false if the configuration does not fit it.
+bool Context::refine_windows_fused(int nw, int maxc, const AlignConfig& cfg, const Quat& koff, long long grid_evals) {
+    const bool wedge = wedge_active();
+    FusedArgs fa;
+    if ((int)cfg.bands.size() > kFusedMaxBands || maxc > kFusedMaxCand) return false;
+    fa.n_bands = (int)cfg.bands.size();
+    fa.prune_band0 = (cfg.prune_after_band && cfg.bands.size() > 1) ? 1 : 0;
+    int rows_max = 0;
+    work_.reserve(sizeof(CandWork) * (size_t)nw * maxc);
+    for (int bi = 0; bi < fa.n_bands; ++bi) {
+        const int L = cfg.bands[bi];
+        BandDev& bd = band(L);
+        rows_max = std::max(rows_max, bd.rows);
+        StageArgs& a = fa.st[bi];
+        a.T = bd.view();
+        a.row_group = bd.row_group.as<int>();
+        if (wedge) {
+            a.chi_hat = chi_dev.as<double2>();
+            a.q_hat = q_dev.as<double2>();
+            a.wp_total = wp_total;
+        }
+        a.cand = cand_.as<CandState>();
+        a.work = work_.as<CandWork>();
+        a.cand_count = cand_count_.as<int>();
+        a.max_cand = maxc;
+        a.n_win = nw;
+        a.prm.band = L;
+        a.prm.newton_max_iter = cfg.newton_max_iter;
+        a.prm.grad_tol = cfg.grad_tol;
+        a.prm.accept_tol = cfg.accept_tol;
+        a.prm.step_damping = cfg.step_damping;
+        a.prm.koffset[0] = koff.w;
+        a.prm.koffset[1] = koff.x;
+        a.prm.koffset[2] = koff.y;
+        a.prm.koffset[3] = koff.z;
+        a.prm.max_cand = maxc;
+        a.prm.has_wedge = wedge ? 1 : 0;
+        a.eval_stats = eval_stats();
+    }
+    fa.coef = coef.as<float>();
+    fa.ldf = geo.m_pad;
+    fa.t_hat = t_hat.as<float>();
+    fa.block_off = geo.block_off;
+    fa.radial_count = geo.radial_count;
+    fa.slot_len = (long long)rows_max * 32;
+    fa.smem_len = rows_max * 32;
+    fa.scratch_floats = compose_scratch_floats(cfg.bands.back());
+    const int grid = fused_refine_grid(fa, wedge);
+    if (grid <= 0) return false;
+    const size_t slots = (size_t)grid * maxc;
+    xi_pool_.reserve(sizeof(float4) * slots * fa.slot_len);
+    fa.xi_pool = xi_pool_.as<float4>();
+    if (wedge) {
+        w_pool_.reserve(sizeof(float4) * slots * fa.slot_len);
+        fa.w_pool = w_pool_.as<float4>();
+    }
+    scratch_.reserve(sizeof(float) * (size_t)grid * 4 * fa.scratch_floats);  // per warp
+    fa.scratch = scratch_.as<float>();
+    win_counter_.reserve(sizeof(int));
+    fa.win_counter = win_counter_.as<int>();
+    ck(cudaMemsetAsync(fa.win_counter, 0, sizeof(int), stream), "window counter");
+    cudaEvent_t r0 = timer.begin(stream);
+    if (launch_refine_fused(fa, grid, wedge, stream) != 0) throw std::runtime_error("fused refine launch failed");
+    timer.end(K_REFINE, r0, stream);
+    ++timer.launches;
+    ++timer.refine_launches;
+    ReduceArgs ra;
+    ra.cand = cand_.as<CandState>();
+    ra.cand_count = cand_count_.as<int>();
+    ra.max_cand = maxc;
+    ra.n_win = nw;
+    ra.sub_norm = sub_norm_.as<double>();
+    ra.t_norm = t_norm;
+    ra.win_particle = win_vol.as<int>();
+    ra.win_shift = win_shift.as<int>();
+    ra.grid_evals = grid_evals;
+    ra.extra_candidates = fa.prune_band0;
+    ra.out = outcome_.as<WindowOutcome>();
+    launch_window_reduce(ra, stream);
+    ++timer.launches;
+    return true;
+}
+
 std::vector<WindowOutcome> Context::run_windows(const float* vols, int n_vol, const std::vector<int>& wvol,
                                                 const std::vector<int>& wshift, const AlignConfig& cfg) {
     if (!has_template) throw std::invalid_argument("align: set_template first");
@@ -479,7 +563,9 @@ std::vector<WindowOutcome> Context::run_windows(const float* vols, int n_vol, co
     timer.end(K_SEED, s0, stream);
 
     const Quat koff = q_from_euler(0.0, kPiH / 2.0, 0.0);
-    refine_windows(nw, maxc, cfg, koff, (long long)sd.na * sd.nb * sd.ng);
+    const long long grid_evals = (long long)sd.na * sd.nb * sd.ng;
+    if (refine_mode != 1 || !refine_windows_fused(nw, maxc, cfg, koff, grid_evals))
+        refine_windows(nw, maxc, cfg, koff, grid_evals);
     ck(cudaMemcpyAsync(res.data(), outcome_.p, sizeof(WindowOutcome) * nw, cudaMemcpyDeviceToHost, stream),
        "outcomes");
     ck(cudaStreamSynchronize(stream), "run_windows");
@@ -552,6 +638,7 @@ void Context::ensure_lanes() {
     }
     for (auto& c : lane_ctx_) {
         c->expand_mode = expand_mode;
+        c->refine_mode = refine_mode;
         c->pool_budget_ = pool_budget_;  // each lane allocates only what its slice needs
     }
     if (lanes_stale_) {

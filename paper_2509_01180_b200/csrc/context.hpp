@@ -181,6 +181,7 @@ public:
                         const std::vector<int>& wvol, const std::vector<int>& wshift);
 
     int expand_mode = 0;          // 0: factored expansion (K2f), 1: dense operator GEMM (K1 + K2)
+    int refine_mode = 0;          // 0: list-driven kernels, 1: fused per-window refinement kernel
     bool operator_ready = false;
     void ensure_operator();
     void build_factored_tables();
@@ -255,6 +256,7 @@ public:
 
 private:
     void refine_windows(int nw, int maxc, const AlignConfig& cfg, const Quat& koff, long long grid_evals);
+    bool refine_windows_fused(int nw, int maxc, const AlignConfig& cfg, const Quat& koff, long long grid_evals);
     DevBuf work_, counters_, xi_win_, xi_pool_, w_pool_, lists_;
     std::map<int, std::unique_ptr<BandDev>> bands_;
     std::map<std::pair<int, long long>, std::unique_ptr<SeedDev>> seeds_;

@@ -199,9 +199,12 @@ __device__ __forceinline__ void warp_eval_k(const BandTables& T, const EvalJob (
     const int L = T.L;
     // the kernels are streamed once per evaluation: group g+1's rows are pulled
     // into L1 while group g runs (L2 latency off the recursion's critical path)
-    if (PF && T.n_groups > 0) {
-        prefetch_rows(xi, T.row_off[0], T.row_off[1], lane);
-        if (WEDGE) prefetch_rows(wx, T.row_off[0], T.row_off[1], lane);
+    // (kernels staged in shared memory by the fused refinement are not prefetched)
+    const bool pf_x = PF && __isGlobal(xi);
+    const bool pf_w = PF && WEDGE && __isGlobal(wx);
+    if (T.n_groups > 0) {
+        if (pf_x) prefetch_rows(xi, T.row_off[0], T.row_off[1], lane);
+        if (pf_w) prefetch_rows(wx, T.row_off[0], T.row_off[1], lane);
     }
     __syncwarp();
     // four FP64 sincos per job on lanes 4k..4k+3 (beta/2, beta, alpha, gamma);
@@ -278,10 +281,10 @@ __device__ __forceinline__ void warp_eval_k(const BandTables& T, const EvalJob (
         const int item = g * 32 + lane;
         const int r0 = T.row_off[g];
         const int glen = T.row_off[g + 1] - r0;
-        if (PF && g + 1 < T.n_groups) {
+        if ((pf_x || pf_w) && g + 1 < T.n_groups) {
             const int n0 = T.row_off[g + 1], n1 = T.row_off[g + 2];
-            prefetch_rows(xi, n0, n1, lane);
-            if (WEDGE) prefetch_rows(wx, n0, n1, lane);
+            if (pf_x) prefetch_rows(xi, n0, n1, lane);
+            if (pf_w) prefetch_rows(wx, n0, n1, lane);
         }
         const int be = T.bexp[item];
         const int ea = be & 0xff, ep = be >> 8;
@@ -449,10 +452,18 @@ struct ComposeScratch {
 
 // Block-cooperative composition of one candidate's chart kernels; dtab / xd /
 // qt live in shared memory when they fit (else in global scratch).
+template <bool WARP>
+__device__ __forceinline__ void group_sync() {
+    if (WARP) __syncwarp();
+    else __syncthreads();
+}
+
+// WARP: one warp composes (the fused refinement), else the whole CTA.
+template <bool WARP = false>
 __device__ void compose_block(const BandTables& T, const float4* src, const StageArgs& a, const Quat& anchor,
                               float* dtab, float2* xd, float2* qt, float4* out, float4* out_w,
                               ComposeScratch& cs) {
-    const int tid = threadIdx.x, nt = blockDim.x;
+    const int tid = WARP ? (threadIdx.x & 31) : threadIdx.x, nt = WARP ? 32 : blockDim.x;
     const int L = T.L;
     if (tid == 0) {
         const Euler3 e = q_euler(anchor);
@@ -460,7 +471,7 @@ __device__ void compose_block(const BandTables& T, const float4* src, const Stag
         cs.eul[1] = e.b;
         cs.eul[2] = e.g;
     }
-    __syncthreads();
+    group_sync<WARP>();
     const double ea = cs.eul[0], eb = cs.eul[1], eg = cs.eul[2];
     for (int m = tid; m <= L; m += nt) {
         double sn, co;
@@ -484,7 +495,7 @@ __device__ void compose_block(const BandTables& T, const float4* src, const Stag
         cs.cp[j] = (float)pc;
         cs.sp[j] = (float)ps;
     }
-    __syncthreads();
+    group_sync<WARP>();
     const float cb = (float)cos(eb);
     // full-plane d^l_{m,m'}(b_a): item chains, their partners, and the mirrors
     // d_{-m,-m'} = (-1)^(m-m') d_{m,m'}
@@ -541,7 +552,7 @@ __device__ void compose_block(const BandTables& T, const float4* src, const Stag
             xd[o + (-m + l) * w + (-mp + l)] = cmul(xm, make_float2(egp.x, -egp.y));
         }
     }
-    __syncthreads();
+    group_sync<WARP>();
     const bool wedge = out_w != nullptr;
     if (wedge) {  // q~_l[m'] = e^{-i m' a} sum_n d_{m'n} e^{-i n g} q_ln
         for (int idx = tid; idx < (L + 1) * (L + 1); idx += nt) {
@@ -568,7 +579,7 @@ __device__ void compose_block(const BandTables& T, const float4* src, const Stag
             if (mp < 0) eam.y = -eam.y;
             qt[idx] = cmul(eam, make_float2(re, im));
         }
-        __syncthreads();
+        group_sync<WARP>();
     }
     const float inv_total = (float)(1.0 / a.wp_total);
     // zero the layout (padding lanes, steps past an item's chain, B of self-paired items)
@@ -576,7 +587,7 @@ __device__ void compose_block(const BandTables& T, const float4* src, const Stag
         out[at] = make_float4(0.f, 0.f, 0.f, 0.f);
         if (wedge) out_w[at] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    __syncthreads();
+    group_sync<WARP>();
     // xi~_l[m,m'] = e^{-i m' a} sum_n X_l[m,n] d^l_{m'n} over the half plane m >= 0,
     // one task per (l, m, quad of 4 consecutive m'): the X row is loaded once per n
     // for 4 outputs; results scatter to their (item, slot) of the band layout
@@ -632,7 +643,7 @@ __device__ void compose_block(const BandTables& T, const float4* src, const Stag
             }
         }
     }
-    __syncthreads();
+    group_sync<WARP>();
 }
 
 // xi_l[m,m'] = sum_k conj(f_klm) t_klm' from real-packed f and t
@@ -757,59 +768,79 @@ __device__ __forceinline__ bool slot_of(const StageArgs& a, long long idx) {
     return w < a.n_win && c < a.cand_count[w];
 }
 
+// band start of candidate i (slot_of(a, i) holds)
+__device__ __forceinline__ void band_begin_one(const StageArgs& a, long long i) {
+    CandWork& wk = a.work[i];
+    wk.slot = -1;
+    wk.compose = 0;
+    wk.iter = 0;
+    wk.retry = 0;
+    wk.status = ST_DONE;
+    CandState& st = a.cand[i];
+    if (!st.active || st.diverged) return;
+    wk.lambda = a.prm.step_damping;
+    st.band_converged = 0;
+    if (st.anchored && a.prm.band > st.anchor_limit) {  // widen the chart kernel
+        const Quat koff{a.prm.koffset[0], a.prm.koffset[1], a.prm.koffset[2], a.prm.koffset[3]};
+        qstore(st.anchor, q_mul(q_inv(koff), qload(st.g)));
+        st.anchor_limit = a.prm.band;
+        wk.compose = 1;
+    }
+    wk.status = ST_START;
+}
+
 __global__ void band_begin_kernel(StageArgs a) {
     const long long n = (long long)a.n_win * a.max_cand;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
-        CandWork& wk = a.work[i];
-        wk.slot = -1;
-        wk.compose = 0;
-        wk.iter = 0;
-        wk.retry = 0;
-        wk.status = ST_DONE;
-        if (!slot_of(a, i)) continue;
-        CandState& st = a.cand[i];
-        if (!st.active || st.diverged) continue;
-        wk.lambda = a.prm.step_damping;
-        st.band_converged = 0;
-        if (st.anchored && a.prm.band > st.anchor_limit) {  // widen the chart kernel
-            const Quat koff{a.prm.koffset[0], a.prm.koffset[1], a.prm.koffset[2], a.prm.koffset[3]};
-            qstore(st.anchor, q_mul(q_inv(koff), qload(st.g)));
-            st.anchor_limit = a.prm.band;
-            wk.compose = 1;
+        if (!slot_of(a, i)) {
+            CandWork& wk = a.work[i];
+            wk.slot = -1;
+            wk.compose = 0;
+            wk.iter = 0;
+            wk.retry = 0;
+            wk.status = ST_DONE;
+            continue;
         }
-        wk.status = ST_START;
+        band_begin_one(a, i);
     }
 }
 
 // chart / re-anchor decision of every candidate still iterating; appends to
 // the order-2 list and the composition list
+// iteration start of candidate i: bit 0 = evaluate at order 2, bit 1 = (re)build
+// the chart kernel first
+__device__ __forceinline__ int iter_begin_one(const StageArgs& a, long long i) {
+    CandWork& wk = a.work[i];
+    if (wk.status != ST_START) return 0;
+    if (wk.iter >= a.prm.newton_max_iter) {
+        wk.status = ST_DONE;
+        return 0;
+    }
+    CandState& st = a.cand[i];
+    const Quat g = qload(st.g);
+    Euler3 e = q_euler(q_mul(g, q_inv(qload(st.anchor))));
+    if (e.b < 0.05 || e.b > kPiD - 0.05) {
+        const Quat koff{a.prm.koffset[0], a.prm.koffset[1], a.prm.koffset[2], a.prm.koffset[3]};
+        qstore(st.anchor, q_mul(q_inv(koff), g));
+        st.anchor_limit = a.prm.band;
+        st.anchored = 1;
+        wk.compose = 1;
+        e = q_euler(koff);
+    }
+    wk.e[0] = e.a, wk.e[1] = e.b, wk.e[2] = e.g;
+    wk.status = ST_EVAL2;
+    ++wk.iter;
+    return 1 | (wk.compose ? 2 : 0);
+}
+
 __global__ void iter_begin_kernel(StageArgs a) {
     const long long n = (long long)a.n_win * a.max_cand;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
-        CandWork& wk = a.work[i];
-        if (wk.status != ST_START) continue;
-        if (wk.iter >= a.prm.newton_max_iter) {
-            wk.status = ST_DONE;
-            continue;
-        }
-        CandState& st = a.cand[i];
-        const Quat g = qload(st.g);
-        Euler3 e = q_euler(q_mul(g, q_inv(qload(st.anchor))));
-        if (e.b < 0.05 || e.b > kPiD - 0.05) {
-            const Quat koff{a.prm.koffset[0], a.prm.koffset[1], a.prm.koffset[2], a.prm.koffset[3]};
-            qstore(st.anchor, q_mul(q_inv(koff), g));
-            st.anchor_limit = a.prm.band;
-            st.anchored = 1;
-            wk.compose = 1;
-            e = q_euler(koff);
-        }
-        wk.e[0] = e.a, wk.e[1] = e.b, wk.e[2] = e.g;
-        wk.status = ST_EVAL2;
-        ++wk.iter;
-        a.list2[atomicAdd(a.counts + CNT_L2, 1)] = (int)i;
-        if (wk.compose) a.listc[atomicAdd(a.counts + CNT_COMP, 1)] = (int)i;
+        const int f = iter_begin_one(a, i);
+        if (f & 1) a.list2[atomicAdd(a.counts + CNT_L2, 1)] = (int)i;
+        if (f & 2) a.listc[atomicAdd(a.counts + CNT_COMP, 1)] = (int)i;
     }
 }
 
@@ -938,37 +969,71 @@ __global__ void __launch_bounds__(EvalShape<K>::WARPS * 32, BMB_EVAL_MINB) eval_
         }
 }
 
+// Newton step of an order-2 evaluated candidate; true: a trial was made
+__device__ __forceinline__ bool step_one(const StageArgs& a, long long i) {
+    CandWork& wk = a.work[i];
+    CandState& st = a.cand[i];
+    Derivs f;
+    objective(wk.c, wk.r, a.prm.has_wedge != 0, 2, f);
+    ++st.evals;
+    wk.f[0] = f.v;
+    for (int k = 0; k < 3; ++k) wk.f[1 + k] = f.g[k];
+    for (int k = 0; k < 9; ++k) wk.f[4 + k] = f.h[k];
+    const double scale = fmax(fabs(f.v), 1e-300);
+    const double gnorm = sqrt(f.g[0] * f.g[0] + f.g[1] * f.g[1] + f.g[2] * f.g[2]);
+    if (f.v > st.best_score) {
+        st.best_score = f.v;
+        for (int k = 0; k < 4; ++k) st.best_g[k] = st.g[k];
+    }
+    if (gnorm <= a.prm.grad_tol * scale) {
+        st.band_converged = 1;
+        wk.status = ST_DONE;
+        return false;
+    }
+    wk.lam = wk.lambda;
+    wk.retry = 0;
+    make_trial(wk);
+    wk.status = ST_EVAL0;
+    return true;
+}
+
 // Newton step of every order-2 evaluated candidate; appends trials to list_out
 __global__ void step_kernel(StageArgs a, int* list_out, int* count_out) {
     const int n = a.counts[CNT_L2];
-    const bool wedge = a.prm.has_wedge != 0;
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
         const int i = a.list2[q];
-        CandWork& wk = a.work[i];
-        CandState& st = a.cand[i];
-        Derivs f;
-        objective(wk.c, wk.r, wedge, 2, f);
-        ++st.evals;
-        wk.f[0] = f.v;
-        for (int k = 0; k < 3; ++k) wk.f[1 + k] = f.g[k];
-        for (int k = 0; k < 9; ++k) wk.f[4 + k] = f.h[k];
-        const double scale = fmax(fabs(f.v), 1e-300);
-        const double gnorm = sqrt(f.g[0] * f.g[0] + f.g[1] * f.g[1] + f.g[2] * f.g[2]);
-        if (f.v > st.best_score) {
-            st.best_score = f.v;
+        if (step_one(a, i)) list_out[atomicAdd(count_out, 1)] = i;
+    }
+}
+
+// acceptance test of a trial; true: it failed with retries left (re-queue)
+__device__ __forceinline__ bool accept_one(const StageArgs& a, long long i) {
+    CandWork& wk = a.work[i];
+    CandState& st = a.cand[i];
+    Derivs t;
+    objective(wk.c, wk.r, a.prm.has_wedge != 0, 0, t);
+    ++st.evals;
+    const double scale = fmax(fabs(wk.f[0]), 1e-300);
+    // tolerant acceptance (optimize.cpp:330-341)
+    if (t.v > wk.f[0] - a.prm.accept_tol * scale) {
+        qstore(st.g, q_mul(qload(wk.gt), qload(st.anchor)));
+        wk.lambda = fmax(wk.lam / 10.0, 1e-12);
+        if (t.v > st.best_score) {
+            st.best_score = t.v;
             for (int k = 0; k < 4; ++k) st.best_g[k] = st.g[k];
         }
-        if (gnorm <= a.prm.grad_tol * scale) {
-            st.band_converged = 1;
-            wk.status = ST_DONE;
-            continue;
-        }
-        wk.lam = wk.lambda;
-        wk.retry = 0;
-        make_trial(wk);
-        wk.status = ST_EVAL0;
-        list_out[atomicAdd(count_out, 1)] = i;
+        wk.status = ST_START;
+        return false;
     }
+    ++wk.retry;
+    wk.lam *= 10.0;
+    if (wk.retry == 3) {  // three damped retries failed to ascend
+        st.diverged = 1;
+        wk.status = ST_DONE;
+        return false;
+    }
+    make_trial(wk);
+    return true;
 }
 
 // acceptance test of every trial in list_in; failed trials with retries left
@@ -976,73 +1041,55 @@ __global__ void step_kernel(StageArgs a, int* list_out, int* count_out) {
 __global__ void accept_kernel(StageArgs a, const int* list_in, const int* count_in, int* list_out,
                               int* count_out) {
     const int n = *count_in;
-    const bool wedge = a.prm.has_wedge != 0;
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
         const int i = list_in[q];
-        CandWork& wk = a.work[i];
-        CandState& st = a.cand[i];
-        Derivs t;
-        objective(wk.c, wk.r, wedge, 0, t);
-        ++st.evals;
-        const double scale = fmax(fabs(wk.f[0]), 1e-300);
-        // tolerant acceptance (optimize.cpp:330-341)
-        if (t.v > wk.f[0] - a.prm.accept_tol * scale) {
-            qstore(st.g, q_mul(qload(wk.gt), qload(st.anchor)));
-            wk.lambda = fmax(wk.lam / 10.0, 1e-12);
-            if (t.v > st.best_score) {
-                st.best_score = t.v;
-                for (int k = 0; k < 4; ++k) st.best_g[k] = st.g[k];
-            }
-            wk.status = ST_START;
-        } else {
-            ++wk.retry;
-            wk.lam *= 10.0;
-            if (wk.retry == 3) {  // three damped retries failed to ascend
-                st.diverged = 1;
-                wk.status = ST_DONE;
-            } else {
-                make_trial(wk);
-                list_out[atomicAdd(count_out, 1)] = i;
-            }
-        }
+        if (accept_one(a, i)) list_out[atomicAdd(count_out, 1)] = i;
     }
+}
+
+// final unanchored score of candidate i at the top band: true if it is scored
+__device__ __forceinline__ bool final_prep_one(const StageArgs& a, long long i) {
+    CandWork& wk = a.work[i];
+    wk.status = ST_DONE;
+    if (!a.cand[i].active) return false;
+    const CandState& st = a.cand[i];
+    const Euler3 e = q_euler(qload(st.diverged ? st.best_g : st.g));
+    wk.et[0] = e.a, wk.et[1] = e.b, wk.et[2] = e.g;
+    wk.status = ST_FINAL;
+    return true;
+}
+
+__device__ __forceinline__ void final_score_one(const StageArgs& a, long long i) {
+    CandWork& wk = a.work[i];
+    Derivs t;
+    objective(wk.c, wk.r, a.prm.has_wedge != 0, 0, t);
+    a.cand[i].score = t.v;
+    ++a.cand[i].evals;
+    wk.status = ST_DONE;
 }
 
 __global__ void final_prep_kernel(StageArgs a) {
     const long long n = (long long)a.n_win * a.max_cand;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
-        CandWork& wk = a.work[i];
-        wk.status = ST_DONE;
-        if (!slot_of(a, i) || !a.cand[i].active) continue;
-        const CandState& st = a.cand[i];
-        const Euler3 e = q_euler(qload(st.diverged ? st.best_g : st.g));
-        wk.et[0] = e.a, wk.et[1] = e.b, wk.et[2] = e.g;
-        wk.status = ST_FINAL;
-        a.list2[atomicAdd(a.counts + CNT_L2, 1)] = (int)i;
+        if (!slot_of(a, i)) {
+            a.work[i].status = ST_DONE;
+            continue;
+        }
+        if (final_prep_one(a, i)) a.list2[atomicAdd(a.counts + CNT_L2, 1)] = (int)i;
     }
 }
 
 __global__ void final_score_kernel(StageArgs a) {
     const int n = a.counts[CNT_L2];
-    const bool wedge = a.prm.has_wedge != 0;
-    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
-        const int i = a.list2[q];
-        CandWork& wk = a.work[i];
-        Derivs t;
-        objective(wk.c, wk.r, wedge, 0, t);
-        a.cand[i].score = t.v;
-        ++a.cand[i].evals;
-        wk.status = ST_DONE;
-    }
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x)
+        final_score_one(a, a.list2[q]);
 }
 
 // prune_after_band (optimize.cpp:391-403): after the first band every candidate
 // has its unanchored band-0 score; each window keeps its best (first on ties) and
 // restarts it as a fresh refine() from that result for the remaining bands
-__global__ void prune_kernel(StageArgs a) {
-    const int w = blockIdx.x * blockDim.x + threadIdx.x;
-    if (w >= a.n_win) return;
+__device__ void prune_window(const StageArgs& a, int w) {
     const int nc = a.cand_count[w];
     CandState* cs = a.cand + (size_t)w * a.max_cand;
     int best = -1;
@@ -1065,6 +1112,11 @@ __global__ void prune_kernel(StageArgs a) {
     st.diverged = 0;
     st.band_converged = 0;
     st.best_score = -DBL_MAX * 2.0;  // -inf
+}
+
+__global__ void prune_kernel(StageArgs a) {
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w < a.n_win) prune_window(a, w);
 }
 
 __global__ void window_reduce_kernel(ReduceArgs a) {
@@ -1110,6 +1162,221 @@ __global__ void window_reduce_kernel(ReduceArgs a) {
         o.norm_score = -DBL_MAX;
     }
     a.out[w] = o;
+}
+
+// ---------------------------------------------------------------- fused refinement
+// One persistent CTA of kFW warps per window at a time.  The window kernel of
+// the band is built once into shared memory; the window's candidates are dealt
+// to the warps (candidate c to warp c mod kFW) and every warp then runs its own
+// candidates' damped-Newton loop independently — warp-level lists, K-way
+// evaluations on the shared window kernel (every table and kernel load feeds
+// K rotation chains), chart kernels composed by the warp into its pool slots,
+// thread-per-candidate Newton steps — so a warp in a latency-bound FP64 phase
+// never holds the others.  Block barriers only at band boundaries.
+constexpr int kFW = 4;
+constexpr int kFT = kFW * 32;
+constexpr int kWarpCand = kFusedMaxCand / kFW;  // candidates per warp (<= 32 lanes)
+static_assert(kWarpCand <= 32, "one lane per candidate of a warp");
+
+struct WarpLists {
+    int u[kWarpCand];   // jobs on the window kernel
+    int a[kWarpCand];   // chart jobs
+    int c[kWarpCand];   // compositions
+};
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// warp-level append of the predicated lanes' candidate c; returns the new length
+__device__ __forceinline__ int wpush(bool pred, int* list, int n, int c) {
+    const unsigned m = __ballot_sync(0xffffffffu, pred);
+    if (pred) list[n + __popc(m & lanemask_lt())] = c;
+    return n + __popc(m);
+}
+
+// evaluation job of local candidate c of window w
+template <bool WEDGE>
+__device__ __forceinline__ EvalJob fused_job(const StageArgs& a, const FusedArgs& fa, const float4* sxi, int w, int c) {
+    const long long i = (long long)w * a.max_cand + c;
+    const CandWork& wk = a.work[i];
+    const bool chart = wk.status != ST_FINAL && a.cand[i].anchored;
+    const size_t slot = (size_t)blockIdx.x * a.max_cand + c;
+    EvalJob j;
+    j.xi = chart ? fa.xi_pool + slot * fa.slot_len : sxi;
+    j.wx = !WEDGE ? nullptr : (chart ? fa.w_pool + slot * fa.slot_len : a.T.wedge);
+    const double* e = wk.status == ST_EVAL2 ? wk.e : wk.et;
+    j.a = e[0], j.b = e[1], j.g = e[2];
+    return j;
+}
+
+template <int ORDER, int K, bool WEDGE>
+__device__ __forceinline__ void fused_eval_group(const StageArgs& a, const FusedArgs& fa, const float4* sxi, int w,
+                                                 const int* cl, WarpScratch* ws) {
+    using O = EvalOpts<ORDER, false>;
+    EvalJob job[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) job[k] = fused_job<WEDGE>(a, fa, sxi, w, cl[k]);
+    warp_eval_k<ORDER, K, WEDGE, O::PF, O::PIPE>(a.T, job, ws);
+    constexpr int NV = ORDER == 0 ? 1 : 10;
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+        if (lane < NV) {
+            CandWork& wk = a.work[(long long)w * a.max_cand + cl[k]];
+            wk.c[lane] = ws[k].res[lane];
+            wk.r[lane] = ws[k].res[10 + lane];
+        }
+    __syncwarp();
+}
+
+// one warp evaluates its listed candidates of window w: window-kernel jobs in
+// groups of KG (remainder in groups of 2 and 1), then the chart jobs
+template <int ORDER, bool WEDGE>
+__device__ void fused_eval(const StageArgs& a, const FusedArgs& fa, const float4* sxi, int w, const int* lu, int nu,
+                           const int* la, int na, WarpScratch* ws) {
+    constexpr int KG = ORDER == 2 ? 2 : 4;
+    int q = 0;
+    for (; q + KG <= nu; q += KG) fused_eval_group<ORDER, KG, WEDGE>(a, fa, sxi, w, lu + q, ws);
+    if (KG == 4 && q + 2 <= nu) {
+        fused_eval_group<ORDER, 2, WEDGE>(a, fa, sxi, w, lu + q, ws);
+        q += 2;
+    }
+    if (q < nu) fused_eval_group<ORDER, 1, WEDGE>(a, fa, sxi, w, lu + q, ws);
+    for (int j = 0; j < na; ++j) fused_eval_group<ORDER, 1, WEDGE>(a, fa, sxi, w, la + j, ws);
+}
+
+#ifdef BMB_FUSED_PROF
+// per-phase SM cycles of the fused kernel (warp lane 0, summed), debug builds only
+__device__ unsigned long long g_fprof[16];
+#define FP_T0() long long fp_t = clock64()
+#define FP_MARK(k)                                                              \
+    do {                                                                        \
+        __syncwarp();                                                           \
+        const long long fp_n = clock64();                                       \
+        if ((threadIdx.x & 31) == 0) atomicAdd(&g_fprof[k], (unsigned long long)(fp_n - fp_t)); \
+        fp_t = fp_n;                                                            \
+    } while (0)
+#define FP_COUNT(k, v) \
+    do { if ((threadIdx.x & 31) == 0) atomicAdd(&g_fprof[k], (unsigned long long)(v)); } while (0)
+#else
+#define FP_T0() (void)0
+#define FP_MARK(k) (void)0
+#define FP_COUNT(k, v) (void)0
+#endif
+
+template <bool WEDGE>
+__global__ void __launch_bounds__(kFT, 3) refine_fused_kernel(FusedArgs fa) {
+    extern __shared__ __align__(16) unsigned char fsm[];
+    float4* sxi = reinterpret_cast<float4*>(fsm);
+    __shared__ WarpScratch wsc[kFW * 4];
+    __shared__ ComposeScratch csc[kFW];
+    __shared__ WarpLists wl[kFW];
+    __shared__ int s_w;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int maxc = fa.st[0].max_cand;
+    const int n_win = fa.st[0].n_win;
+    WarpScratch* ws = wsc + warp * 4;
+    WarpLists& L_ = wl[warp];
+    float* scr = fa.scratch + ((size_t)blockIdx.x * kFW + warp) * fa.scratch_floats;
+    unsigned long long n_eval[kFusedMaxBands][2];
+    for (int b = 0; b < kFusedMaxBands; ++b) n_eval[b][0] = n_eval[b][1] = 0;
+    FP_T0();
+    for (;;) {
+        if (tid == 0) s_w = atomicAdd(fa.win_counter, 1);
+        __syncthreads();
+        const int w = s_w;
+        if (w >= n_win) break;
+        FP_COUNT(10, 1);
+        const int nc = fa.st[0].cand_count[w];
+        const long long base = (long long)w * maxc;
+        // this lane's candidate (warp-strided deal)
+        const int c = warp + kFW * lane;
+        const bool mine = lane < kWarpCand && c < nc;
+        for (int bi = 0; nc > 0 && bi < fa.n_bands; ++bi) {
+            const StageArgs& a = fa.st[bi];
+            const int len = a.T.rows * 32;
+            // window kernel of this band (build_xi, xi_coefficients) into shared memory
+            const float* f = fa.coef + (size_t)w * fa.ldf;
+            for (int e = tid; e < len; e += kFT)
+                sxi[e] = xi_entry(a.T, a.row_group, f, fa.t_hat, fa.block_off, fa.radial_count, e >> 5, e & 31);
+            if (mine) band_begin_one(a, base + c);
+            FP_MARK(0);
+            __syncthreads();
+            FP_MARK(7);
+            const int nxi = xi_off(a.T.L + 1);
+            float* dtab = scr;
+            float2* xd = reinterpret_cast<float2*>(dtab + ((nxi + 1) & ~1));
+            float2* qt = xd + nxi;
+            for (;;) {
+                const int fl = mine ? iter_begin_one(a, base + c) : 0;
+                const bool anch = (fl & 1) && a.cand[base + c].anchored;
+                const int n2u = wpush((fl & 1) && !anch, L_.u, 0, c);
+                const int n2a = wpush(anch, L_.a, 0, c);
+                const int ncomp = wpush((fl & 2) != 0, L_.c, 0, c);
+                FP_MARK(8);
+                if (n2u + n2a == 0) break;
+                FP_COUNT(11, 1);
+                FP_COUNT(9, ncomp);
+                // chart kernels xi~ = xi D(a)^T of the (re-)anchored candidates
+                for (int q = 0; q < ncomp; ++q) {
+                    const int cc = L_.c[q];
+                    const size_t slot = (size_t)blockIdx.x * maxc + cc;
+                    compose_block<true>(a.T, sxi, a, qload(a.cand[base + cc].anchor), dtab, xd, qt,
+                                        fa.xi_pool + slot * fa.slot_len,
+                                        WEDGE ? fa.w_pool + slot * fa.slot_len : nullptr, csc[warp]);
+                    if (lane == 0) {
+                        a.work[base + cc].slot = (int)slot;
+                        a.work[base + cc].compose = 0;
+                    }
+                }
+                FP_MARK(1);
+                fused_eval<2, WEDGE>(a, fa, sxi, w, L_.u, n2u, L_.a, n2a, ws);
+                n_eval[bi][1] += n2u + n2a;
+                FP_MARK(2);
+                bool tri = (fl & 1) && step_one(a, base + c);
+                FP_MARK(3);
+                for (int r = 0; r < 3; ++r) {
+                    const bool ta = tri && a.cand[base + c].anchored;
+                    const int ntu = wpush(tri && !ta, L_.u, 0, c);
+                    const int nta = wpush(ta, L_.a, 0, c);
+                    __syncwarp();
+                    if (ntu + nta == 0) break;
+                    fused_eval<0, WEDGE>(a, fa, sxi, w, L_.u, ntu, L_.a, nta, ws);
+                    n_eval[bi][0] += ntu + nta;
+                    FP_MARK(4);
+                    tri = tri && accept_one(a, base + c);
+                    FP_MARK(5);
+                }
+                __syncwarp();
+            }
+            const bool prune_now = fa.prune_band0 && bi == 0;
+            if (bi + 1 == fa.n_bands || prune_now) {
+                // final unanchored score (optimize.cpp:349-352) on the window kernel
+                const bool fin = mine && final_prep_one(a, base + c);
+                const int nf = wpush(fin, L_.u, 0, c);
+                __syncwarp();
+                fused_eval<0, WEDGE>(a, fa, sxi, w, L_.u, nf, L_.a, 0, ws);
+                n_eval[bi][0] += nf;
+                if (fin) final_score_one(a, base + c);
+                if (prune_now) {
+                    __syncthreads();
+                    if (tid == 0) prune_window(a, w);
+                }
+                FP_MARK(6);
+            }
+            __syncthreads();  // the next band rebuilds sxi; candidate state settled
+            FP_MARK(7);
+        }
+    }
+    // evaluation counters (one atomic per band and order per warp)
+    if (lane == 0 && fa.st[0].eval_stats)
+        for (int b = 0; b < fa.n_bands; ++b)
+            for (int o = 0; o < 2; ++o)
+                if (n_eval[b][o])
+                    atomicAdd(fa.st[0].eval_stats + ((size_t)fa.st[b].T.L * 2 + o) * 2 + (WEDGE ? 1 : 0), n_eval[b][o]);
 }
 
 // ---------------------------------------------------------------- sweep
@@ -1248,6 +1515,41 @@ void launch_prune(const StageArgs& a, cudaStream_t s) {
 void launch_window_reduce(const ReduceArgs& a, cudaStream_t s) {
     window_reduce_kernel<<<(a.n_win + 127) / 128, 128, 0, s>>>(a);
 }
+
+int fused_refine_grid(const FusedArgs& a, bool wedge) {
+    if (a.n_bands < 1 || a.n_bands > kFusedMaxBands || a.st[0].max_cand > kFusedMaxCand) return 0;
+    const int smem = (int)(sizeof(float4) * (size_t)a.smem_len);
+    if (smem > 160 * 1024) return 0;
+    if (a.st[0].max_cand > kFW * kWarpCand) return 0;
+    const void* fn = wedge ? reinterpret_cast<const void*>(refine_fused_kernel<true>)
+                           : reinterpret_cast<const void*>(refine_fused_kernel<false>);
+    if (ensure_dynamic_smem(fn, smem) != cudaSuccess) return 0;
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kFT, smem) != cudaSuccess || per_sm < 1) return 0;
+    return sms * per_sm;
+}
+
+int launch_refine_fused(const FusedArgs& a, int grid, bool wedge, cudaStream_t s) {
+    if (grid <= 0) return 2;
+    const size_t smem = sizeof(float4) * (size_t)a.smem_len;
+    if (wedge) refine_fused_kernel<true><<<grid, kFT, smem, s>>>(a);
+    else refine_fused_kernel<false><<<grid, kFT, smem, s>>>(a);
+    return cudaGetLastError() == cudaSuccess ? 0 : 2;
+}
+
+#ifdef BMB_FUSED_PROF
+extern "C" int bmb_fused_profile(unsigned long long* out, int reset) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, g_fprof, sizeof(unsigned long long) * 16);
+    if (reset) {
+        unsigned long long z[16] = {0};
+        cudaMemcpyToSymbol(g_fprof, z, sizeof(z));
+    }
+    return 0;
+}
+#endif
 
 int launch_eval_sweep(const EvalArgs& a, cudaStream_t s) {
     int sms = 0, dev = 0;

@@ -84,6 +84,36 @@ void launch_final_score(const StageArgs& a, int max_n, cudaStream_t s);
 void launch_window_reduce(const ReduceArgs& a, cudaStream_t s);
 void launch_prune(const StageArgs& a, cudaStream_t s);
 
+// Fused per-window refinement: one persistent CTA takes a window at a time
+// (atomic window counter) and runs every band of refine() for all of the
+// window's candidates — window kernel built into shared memory, chart kernels
+// composed into the CTA's own pool slots, evaluations, Newton steps and
+// acceptance — with no host round trip.  Same per-candidate arithmetic as the
+// list-driven kernels above, so the outcomes are bit-identical.
+constexpr int kFusedMaxBands = 8;
+constexpr int kFusedMaxCand = 64;
+struct FusedArgs {
+    StageArgs st[kFusedMaxBands];  // per band: tables, parameters (pool/scratch fields unused)
+    int n_bands = 0;
+    int prune_band0 = 0;           // prune_after_band: keep each window's winner after band 0
+    const float* coef = nullptr;   // [n_win][ldf] real-packed window coefficients
+    int ldf = 0;
+    const float* t_hat = nullptr;  // real-packed template coefficients
+    const int* block_off = nullptr;
+    const int* radial_count = nullptr;
+    int* win_counter = nullptr;    // zeroed before the launch
+    float4* xi_pool = nullptr;     // [grid][max_cand][slot_len] chart kernels
+    float4* w_pool = nullptr;      // same, wedge kernels
+    long long slot_len = 0;        // float4 per pool slot (largest band)
+    float* scratch = nullptr;      // [grid][scratch_floats] composition temporaries
+    long long scratch_floats = 0;
+    int smem_len = 0;              // float4 of the shared-memory window kernel (largest band)
+};
+// grid the fused kernel runs with (persistent: resident CTAs on every SM); 0 if
+// the configuration is not supported (too many candidates / bands, kernel too large)
+int fused_refine_grid(const FusedArgs& a, bool wedge);
+int launch_refine_fused(const FusedArgs& a, int grid, bool wedge, cudaStream_t s);
+
 // standalone batched evaluation (rotate-score-gradient sweep, config 4):
 // value + gradient of C(g) = Re sum xi D(g) for n_xi kernels x n_rot angle
 // triples; out[(p*n_rot + g)*4 + {0..3}] = value, dC/dalpha, dC/dbeta, dC/dgamma.
