@@ -195,6 +195,11 @@ int bm_synthesize(bm_context* ctx, const double* coeffs, int real_volume, int n,
  * out_counts[0..3]: kernels launched, windows expanded, GEMM launches,
  * refine launches.  reset != 0 clears after reading. */
 int bm_context_set_timing(bm_context* ctx, int on);
+/* Per-band split of the refinement timers (timing on): ms[b * 15 + k] for band
+ * index b = 0, 1, 2, 3+ and the timer classes k of bm_context_timings. */
+int bm_context_band_timings(bm_context* ctx, double* ms);
+/* Evaluations at band L since the last eval-stats reset: out[0] order 2, out[1] order 0. */
+int bm_context_eval_counts(bm_context* ctx, int L, long long* out);
 int bm_context_timings(bm_context* ctx, double* out_ms, long long* out_counts, int reset);
 /* Rotate-score-gradient evaluations run by the refinement since the last reset:
  * evals[0] order 2 (value, gradient, Hessian), evals[1] order 0 (value), and

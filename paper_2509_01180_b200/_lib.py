@@ -111,6 +111,10 @@ def _declare(L: C.CDLL) -> None:
     L.bm_synthesize.restype = I
     L.bm_context_set_lanes.argtypes = [P, I, I]
     L.bm_context_set_lanes.restype = I
+    L.bm_context_eval_counts.argtypes = [P, I, P]
+    L.bm_context_eval_counts.restype = I
+    L.bm_context_band_timings.argtypes = [P, P]
+    L.bm_context_band_timings.restype = I
     L.bm_context_set_refine_mode.argtypes = [P, I]
     L.bm_context_set_refine_mode.restype = I
     L.bm_context_set_expand_mode.argtypes = [P, I]

@@ -272,6 +272,21 @@ class Context:
                                             C.c_void_p(out.data_ptr()), self._stream(out)), "synthesize")
         return out
 
+    def eval_counts(self, L: int):
+        """(order-2, order-0) evaluations at band L since the last eval_stats(reset=True)."""
+        out = (C.c_longlong * 2)()
+        _lib.check(_lib.lib().bm_context_eval_counts(self._h, L, out), "eval_counts")
+        return out[0], out[1]
+
+    def band_timings(self):
+        """Per-band split of the refinement timers: {band index: {class: ms}} (timing on)."""
+        ms = (C.c_double * 60)()
+        _lib.check(_lib.lib().bm_context_band_timings(self._h, ms), "band_timings")
+        names = ("gather", "expand", "seed", "refine", "wedge", "misc", "refine_band0",
+                 "refine_band1", "refine_band2", "refine_band3+", "eval_order2", "eval_order0",
+                 "compose", "newton", "xi_build")
+        return {b: {n: ms[b * 15 + k] for k, n in enumerate(names) if ms[b * 15 + k] > 0} for b in range(4)}
+
     def set_lanes(self, lanes: int, min_per_lane: int = 64):
         """Concurrent lanes of align_batch (default 3 lanes of >= 64 particles)."""
         _lib.check(_lib.lib().bm_context_set_lanes(self._h, lanes, min_per_lane), "set_lanes")

@@ -298,6 +298,7 @@ void Context::refine_windows(int nw, int maxc, const AlignConfig& cfg, const Qua
                 xa.out = xi_win_.as<float4>();
                 cudaEvent_t r0 = timer.begin(stream);
                 cudaEvent_t rb = timer.begin(stream);
+                timer.band = (int)bi;
                 cudaEvent_t x0 = timer.begin(stream);
                 if (launch_build_xi(xa, stream) != 0) throw std::runtime_error("build_xi launch failed");
                 timer.end(K_XI, x0, stream);
@@ -404,6 +405,7 @@ void Context::refine_windows(int nw, int maxc, const AlignConfig& cfg, const Qua
                     }
                 }
                 ++timer.refine_launches;
+                timer.band = -1;
                 timer.end(K_REFINE, r0, stream);
                 timer.end(K_REFINE_B0 + (int)std::min<size_t>(bi, 3), rb, stream);
             }
@@ -874,6 +876,21 @@ void Context::read_eval_stats(long long* evals, double* flops, bool reset) {
     if (evals) evals[0] = e2, evals[1] = e0;
     if (flops) *flops = fl;
     if (reset) ck(cudaMemsetAsync(eval_stats(), 0, sizeof(unsigned long long) * kEvalStats, stream), "eval stats");
+}
+
+void Context::eval_counts(int L, long long* out) {
+    std::vector<unsigned long long> h(kEvalStats);
+    ck(cudaMemcpyAsync(h.data(), eval_stats(), sizeof(unsigned long long) * kEvalStats, cudaMemcpyDeviceToHost,
+                       stream), "eval counts");
+    ck(cudaStreamSynchronize(stream), "eval counts");
+    out[0] = (long long)(h[((size_t)L * 2 + 1) * 2] + h[((size_t)L * 2 + 1) * 2 + 1]);
+    out[1] = (long long)(h[((size_t)L * 2) * 2] + h[((size_t)L * 2) * 2 + 1]);
+    for (auto& c : lane_ctx_) {
+        long long o[2];
+        c->eval_counts(L, o);
+        out[0] += o[0];
+        out[1] += o[1];
+    }
 }
 
 }  // namespace bmb

@@ -380,6 +380,27 @@ int bm_context_timings(bm_context* ctx, double* out_ms, long long* out_counts, i
     return BM_OK;
 }
 
+int bm_context_eval_counts(bm_context* ctx, int L, long long* out) {
+    return guarded("bm_context_eval_counts", [&] {
+        if (!ctx) return (int)BM_ERR_STATE;
+        if (L < 0 || L > bmb::kMaxL) throw std::invalid_argument("band out of range");
+        cudaSetDevice(ctx->impl->device);
+        ctx->impl->eval_counts(L, out);
+        return (int)BM_OK;
+    });
+}
+
+int bm_context_band_timings(bm_context* ctx, double* ms) {
+    return guarded("bm_context_band_timings", [&] {
+        if (!ctx) return (int)BM_ERR_STATE;
+        auto& c = *ctx->impl;
+        c.timer.collect();
+        for (int b = 0; b < 4; ++b)
+            for (int k = 0; k < bmb::K_COUNT; ++k) ms[b * bmb::K_COUNT + k] = c.timer.band_ms[b][k];
+        return (int)BM_OK;
+    });
+}
+
 int bm_context_set_lanes(bm_context* ctx, int lanes, int min_per_lane) {
     return guarded("bm_context_set_lanes", [&] {
         if (!ctx) return (int)BM_ERR_STATE;

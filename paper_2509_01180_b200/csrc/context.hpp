@@ -110,6 +110,8 @@ struct KernelTimer {
     bool on = false;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
     double ms[K_COUNT] = {0};
+    double band_ms[4][K_COUNT] = {{0}};  // per band index (refinement classes; last slot: bands >= 3)
+    int band = -1;                        // band index of the launches being timed (-1: none)
     long long launches = 0;        // kernels of this library launched (always counted)
     long long windows_expanded = 0;
     long long gemm_launches = 0, refine_launches = 0;
@@ -125,14 +127,16 @@ struct KernelTimer {
         cudaEvent_t e;
         cudaEventCreate(&e);
         cudaEventRecord(e, s);
-        pending.push_back({cls, {b, e}});
+        pending.push_back({cls + (band >= 0 ? K_COUNT * (1 + (band < 3 ? band : 3)) : 0), {b, e}});
     }
     void collect() {
         for (auto& p : pending) {
             float t = 0.f;
             cudaEventSynchronize(p.second.second);
             cudaEventElapsedTime(&t, p.second.first, p.second.second);
-            ms[p.first] += t;
+            const int cls = p.first % K_COUNT, bi = p.first / K_COUNT - 1;
+            ms[cls] += t;
+            if (bi >= 0) band_ms[bi][cls] += t;
             cudaEventDestroy(p.second.first);
             cudaEventDestroy(p.second.second);
         }
@@ -141,12 +145,16 @@ struct KernelTimer {
     void reset() {
         collect();
         for (double& x : ms) x = 0.0;
+        for (auto& r : band_ms)
+            for (double& x : r) x = 0.0;
         launches = windows_expanded = gemm_launches = refine_launches = 0;
     }
     // add another timer's totals (a lane's) and clear it
     void absorb(KernelTimer& o) {
         o.collect();
         for (int i = 0; i < K_COUNT; ++i) ms[i] += o.ms[i];
+        for (int b = 0; b < 4; ++b)
+            for (int i = 0; i < K_COUNT; ++i) band_ms[b][i] += o.band_ms[b][i];
         launches += o.launches;
         windows_expanded += o.windows_expanded;
         gemm_launches += o.gemm_launches;
@@ -252,6 +260,7 @@ public:
     }
     // evaluations (order 2, order 0) and their algorithmic FLOPs since the last reset
     void read_eval_stats(long long* evals, double* flops, bool reset);
+    void eval_counts(int L, long long* out);  // (order 2, order 0) evaluations at band L
     size_t pool_budget_ = 24ull << 30;      // bytes for window kernels + anchored-chart pool per chunk
 
 private:

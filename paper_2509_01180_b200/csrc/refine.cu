@@ -433,6 +433,25 @@ __device__ __forceinline__ void warp_eval_k(const BandTables& T, const EvalJob (
     __syncwarp();
 }
 
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// warp-aggregated ordered append: the predicated lanes append v in lane order
+// (lists keep the candidate order of their producers, so the candidates of a
+// window stay adjacent and can evaluate K-way)
+__device__ __forceinline__ void wappend(bool pred, int v, int* list, int* count) {
+    const unsigned m = __ballot_sync(0xffffffffu, pred);
+    if (!m) return;
+    const int leader = __ffs(m) - 1;
+    int base = 0;
+    if ((threadIdx.x & 31) == leader) base = atomicAdd(count, __popc(m));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (pred) list[base + __popc(m & lanemask_lt())] = v;
+}
+
 // ---------------------------------------------------------------- composition
 // xi~_l = xi_l D^l(a)^T  (xi_compose_right, src/xcorr.cpp:149-155), with
 // D^l_{m'n}(a) = e^{-i m' a} d^l_{m'n}(b) e^{-i n g}:
@@ -836,11 +855,12 @@ __device__ __forceinline__ int iter_begin_one(const StageArgs& a, long long i) {
 
 __global__ void iter_begin_kernel(StageArgs a) {
     const long long n = (long long)a.n_win * a.max_cand;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+    const long long n_pad = (n + 31) & ~31LL;  // whole warps (ballots)
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n_pad;
          i += (long long)gridDim.x * blockDim.x) {
-        const int f = iter_begin_one(a, i);
-        if (f & 1) a.list2[atomicAdd(a.counts + CNT_L2, 1)] = (int)i;
-        if (f & 2) a.listc[atomicAdd(a.counts + CNT_COMP, 1)] = (int)i;
+        const int f = i < n ? iter_begin_one(a, i) : 0;
+        wappend(f & 1, (int)i, a.list2, a.counts + CNT_L2);
+        wappend((f & 2) != 0, (int)i, a.listc, a.counts + CNT_COMP);
     }
 }
 
@@ -904,21 +924,37 @@ struct EvalShape {
     static constexpr int WARPS = K >= 4 ? 4 : 8;
 };
 
-// K jobs of one warp: one K-way evaluation when they share their kernels,
-// else one after the other
+// K jobs of one warp, evaluated as runs of jobs that share their kernels
+// (K-way when all K share, else pairs, else one at a time)
 template <int ORDER, int K, bool WEDGE, bool SWEEP>
 __device__ __forceinline__ void eval_group(const BandTables& T, const EvalJob (&job)[K], WarpScratch* ws) {
     using O = EvalOpts<ORDER, SWEEP>;
-    bool same = true;
-#pragma unroll
-    for (int k = 1; k < K; ++k) same &= job[k].xi == job[0].xi && job[k].wx == job[0].wx;
-    if (K == 1 || same) {
-        warp_eval_k<ORDER, K, WEDGE, O::PF, O::PIPE>(T, job, ws);
+    if constexpr (K == 1) {
+        warp_eval_k<ORDER, 1, WEDGE, O::PF, O::PIPE>(T, job, ws);
     } else {
+        bool same[K];
+        same[0] = false;
+        bool all = true;
+#pragma unroll
+        for (int k = 1; k < K; ++k) {
+            same[k] = job[k].xi == job[k - 1].xi && job[k].wx == job[k - 1].wx;
+            all &= same[k];
+        }
+        if (all) {
+            warp_eval_k<ORDER, K, WEDGE, O::PF, O::PIPE>(T, job, ws);
+            return;
+        }
 #pragma unroll 1
-        for (int k = 0; k < K; ++k) {
-            const EvalJob one[1] = {job[k]};
-            warp_eval_k<ORDER, 1, WEDGE, O::PF, O::PIPE>(T, one, ws + k);
+        for (int k = 0; k < K;) {
+            if (K > 2 && k + 1 < K && same[k + 1]) {
+                const EvalJob two[2] = {job[k], job[k + 1]};
+                warp_eval_k<ORDER, 2, WEDGE, O::PF, O::PIPE>(T, two, ws + k);
+                k += 2;
+            } else {
+                const EvalJob one[1] = {job[k]};
+                warp_eval_k<ORDER, 1, WEDGE, O::PF, O::PIPE>(T, one, ws + k);
+                k += 1;
+            }
         }
     }
 }
@@ -1000,9 +1036,11 @@ __device__ __forceinline__ bool step_one(const StageArgs& a, long long i) {
 // Newton step of every order-2 evaluated candidate; appends trials to list_out
 __global__ void step_kernel(StageArgs a, int* list_out, int* count_out) {
     const int n = a.counts[CNT_L2];
-    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
-        const int i = a.list2[q];
-        if (step_one(a, i)) list_out[atomicAdd(count_out, 1)] = i;
+    const int n_pad = (n + 31) & ~31;
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_pad; q += gridDim.x * blockDim.x) {
+        const int i = q < n ? a.list2[q] : -1;
+        const bool t = i >= 0 && step_one(a, i);
+        wappend(t, i, list_out, count_out);
     }
 }
 
@@ -1041,9 +1079,11 @@ __device__ __forceinline__ bool accept_one(const StageArgs& a, long long i) {
 __global__ void accept_kernel(StageArgs a, const int* list_in, const int* count_in, int* list_out,
                               int* count_out) {
     const int n = *count_in;
-    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
-        const int i = list_in[q];
-        if (accept_one(a, i)) list_out[atomicAdd(count_out, 1)] = i;
+    const int n_pad = (n + 31) & ~31;
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_pad; q += gridDim.x * blockDim.x) {
+        const int i = q < n ? list_in[q] : -1;
+        const bool rq = i >= 0 && accept_one(a, i);
+        wappend(rq, i, list_out, count_out);
     }
 }
 
@@ -1070,13 +1110,15 @@ __device__ __forceinline__ void final_score_one(const StageArgs& a, long long i)
 
 __global__ void final_prep_kernel(StageArgs a) {
     const long long n = (long long)a.n_win * a.max_cand;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+    const long long n_pad = (n + 31) & ~31LL;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n_pad;
          i += (long long)gridDim.x * blockDim.x) {
-        if (!slot_of(a, i)) {
-            a.work[i].status = ST_DONE;
-            continue;
+        bool f = false;
+        if (i < n) {
+            if (!slot_of(a, i)) a.work[i].status = ST_DONE;
+            else f = final_prep_one(a, i);
         }
-        if (final_prep_one(a, i)) a.list2[atomicAdd(a.counts + CNT_L2, 1)] = (int)i;
+        wappend(f, (int)i, a.list2, a.counts + CNT_L2);
     }
 }
 
@@ -1183,12 +1225,6 @@ struct WarpLists {
     int a[kWarpCand];   // chart jobs
     int c[kWarpCand];   // compositions
 };
-
-__device__ __forceinline__ unsigned lanemask_lt() {
-    unsigned m;
-    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-    return m;
-}
 
 // warp-level append of the predicated lanes' candidate c; returns the new length
 __device__ __forceinline__ int wpush(bool pred, int* list, int n, int c) {
@@ -1466,16 +1502,19 @@ void launch_compose(const StageArgs& a, int n, cudaStream_t s) {
         compose_kernel<false><<<n, 256, 0, s>>>(a);
     }
 }
-// jobs per warp in the refinement: 1 (measured fastest: refinement lists mix
-// windows, and one job per warp keeps the most warps in flight); BMB_EVAL_K=2/4
-// selects K-way warps for experiments
+// jobs per warp in the refinement: 1 (measured fastest; K-way over runs of
+// same-window candidates in the ordered lists is slower at every order):
+// BMB_EVAL_K0 / BMB_EVAL_K2 (1, 2, 4) for A/B runs
 static int eval_k_for(int order, int /*max_n*/) {
-    static const int forced = [] {
-        const char* e = std::getenv("BMB_EVAL_K");
+    static const int k0 = [] {
+        const char* e = std::getenv("BMB_EVAL_K0");
         return e ? std::atoi(e) : 1;
     }();
-    if (forced == 2 || forced == 4) return order == 2 ? 2 : forced;
-    return 1;
+    static const int k2 = [] {
+        const char* e = std::getenv("BMB_EVAL_K2");
+        return e ? std::atoi(e) : 1;
+    }();
+    return order == 2 ? k2 : k0;
 }
 
 template <int ORDER, int K>
