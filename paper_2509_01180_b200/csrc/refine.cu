@@ -457,67 +457,108 @@ __device__ __forceinline__ void wappend(bool pred, int v, int* list, int* count)
 // D^l_{m'n}(a) = e^{-i m' a} d^l_{m'n}(b) e^{-i n g}:
 //   xi~_l[m,m'] = e^{-i m' a} sum_n (xi_l[m,n] e^{-i n g}) d^l_{m'n}(b).
 // The full-plane d^l(b) comes from the same band tables as the evaluation
-// (half-plane chains + d_{-m,-m'} = (-1)^{m-m'} d_{m,m'}); xi is unpacked into a
-// dense, phase-folded scratch so the n-sum runs over contiguous rows.  The
-// wedge-power kernel is rank one (conj(chi_lm) q_lm' / total), so its
-// composition only rotates q: q~_l = D^l(a) q_l  (O(l^2) per degree).
+// (half-plane chains + d_{-m,-m'} = (-1)^{m-m'} d_{m,m'}); the rows m >= 0 of xi
+// (all the product needs) are unpacked into a dense, phase-folded scratch so
+// the n-sum runs over contiguous rows.  The wedge-power kernel is rank one
+// (conj(chi_lm) q_lm' / total), so its composition only rotates q:
+// q~_l = D^l(a) q_l  (O(l^2) per degree).
 struct ComposeScratch {
-    double eul[3];
     float2 ua[kMaxL + 1];
     float2 ug[kMaxL + 1];
     float cp[2 * kMaxL + 3];
     float sp[2 * kMaxL + 3];
+    double eul[3];
 };
 
-// Block-cooperative composition of one candidate's chart kernels; dtab / xd /
-// qt live in shared memory when they fit (else in global scratch).
 template <bool WARP>
 __device__ __forceinline__ void group_sync() {
     if (WARP) __syncwarp();
     else __syncthreads();
 }
 
-// WARP: one warp composes (the fused refinement), else the whole CTA.
+// scratch layout of one composition (floats): full-plane d table, the m >= 0
+// rows of the phase-folded xi, q~, and the staged FP64 wedge factors
+struct ComposeLayout {
+    int dtab, xd, qt, qh, ch, total;
+};
+// offset of degree l in the m >= 0 half rows: sum_{j<l} (j+1)(2j+1)
+__host__ __device__ __forceinline__ int xh_off(int l) { return l * (l - 1) * (2 * l - 1) / 3 + 3 * l * (l - 1) / 2 + l; }
+__host__ __device__ inline ComposeLayout compose_layout(int L) {
+    ComposeLayout c;
+    const int nxi = xi_off(L + 1), ntri = (L + 1) * (L + 2) / 2;
+    int o = 0;
+    c.dtab = o;
+    o += (nxi + 3) & ~3;
+    c.xd = o;
+    o += (2 * xh_off(L + 1) + 3) & ~3;
+    c.qt = o;
+    o += (2 * (L + 1) * (L + 1) + 3) & ~3;
+    c.qh = o;
+    o += 4 * ntri;
+    c.ch = o;
+    o += 4 * ntri;
+    c.total = o;
+    return c;
+}
+
+// Cooperative composition of one candidate's chart kernels (WARP: one warp,
+// the fused refinement; else the whole CTA).  scr: compose_layout(T.L) floats
+// (shared memory when it fits).  Four phases: angles and phase tables (warp 0;
+// the other warps stage the wedge factors), d chains + xi unpack, the product
+// and q~, then the wedge kernel written whole (coalesced).
 template <bool WARP = false>
 __device__ void compose_block(const BandTables& T, const float4* src, const StageArgs& a, const Quat& anchor,
-                              float* dtab, float2* xd, float2* qt, float4* out, float4* out_w,
-                              ComposeScratch& cs) {
+                              float* scr, float4* out, float4* out_w, ComposeScratch& cs) {
     const int tid = WARP ? (threadIdx.x & 31) : threadIdx.x, nt = WARP ? 32 : blockDim.x;
     const int L = T.L;
-    if (tid == 0) {
+    const ComposeLayout lay = compose_layout(L);
+    float* dtab = scr + lay.dtab;
+    float2* xd = reinterpret_cast<float2*>(scr + lay.xd);
+    float2* qt = reinterpret_cast<float2*>(scr + lay.qt);
+    double2* qh = reinterpret_cast<double2*>(scr + lay.qh);
+    double2* chh = reinterpret_cast<double2*>(scr + lay.ch);
+    const bool wedge = out_w != nullptr;
+    const int ntri = (L + 1) * (L + 2) / 2;
+    if (tid < 32) {
+        // every lane of warp 0 converts the anchor (no serial section)
         const Euler3 e = q_euler(anchor);
-        cs.eul[0] = e.a;
-        cs.eul[1] = e.b;
-        cs.eul[2] = e.g;
-    }
-    group_sync<WARP>();
-    const double ea = cs.eul[0], eb = cs.eul[1], eg = cs.eul[2];
-    for (int m = tid; m <= L; m += nt) {
-        double sn, co;
-        sincos_d(m * ea, &sn, &co);
-        cs.ua[m] = make_float2((float)co, (float)-sn);
-        sincos_d(m * eg, &sn, &co);
-        cs.ug[m] = make_float2((float)co, (float)-sn);
-    }
-    double ch, sh;
-    sincos_d(0.5 * eb, &sh, &ch);
-    for (int j = tid; j <= 2 * L + 2; j += nt) {
-        double pc = 1.0, ps = 1.0, bc = ch, bs = sh;
-        for (int q = j; q; q >>= 1) {
-            if (q & 1) {
-                pc *= bc;
-                ps *= bs;
-            }
-            bc *= bc;
-            bs *= bs;
+        if (tid == 0) {
+            cs.eul[0] = e.a;
+            cs.eul[1] = e.b;
+            cs.eul[2] = e.g;
         }
-        cs.cp[j] = (float)pc;
-        cs.sp[j] = (float)ps;
+        for (int m = tid; m <= L; m += 32) {
+            double sn, co;
+            sincos_d(m * e.a, &sn, &co);
+            cs.ua[m] = make_float2((float)co, (float)-sn);
+            sincos_d(m * e.g, &sn, &co);
+            cs.ug[m] = make_float2((float)co, (float)-sn);
+        }
+        double ch, sh;
+        sincos_d(0.5 * e.b, &sh, &ch);
+        for (int j = tid; j <= 2 * L + 2; j += 32) {
+            double pc = 1.0, ps = 1.0, bc = ch, bs = sh;
+            for (int q = j; q; q >>= 1) {
+                if (q & 1) {
+                    pc *= bc;
+                    ps *= bs;
+                }
+                bc *= bc;
+                bs *= bs;
+            }
+            cs.cp[j] = (float)pc;
+            cs.sp[j] = (float)ps;
+        }
     }
+    if (wedge)
+        for (int i = (WARP ? tid : tid - 32); i >= 0 && i < ntri; i += (WARP ? 32 : nt - 32)) {
+            qh[i] = a.q_hat[i];
+            chh[i] = a.chi_hat[i];
+        }
     group_sync<WARP>();
-    const float cb = (float)cos(eb);
+    const float cb = (float)cos(cs.eul[1]);
     // full-plane d^l_{m,m'}(b_a): item chains, their partners, and the mirrors
-    // d_{-m,-m'} = (-1)^(m-m') d_{m,m'}
+    // d_{-m,-m'} = (-1)^(m-m') d_{m,m'}; recursion loads issued 4 steps at a time
     for (int item = tid; item < T.n_groups * 32; item += nt) {
         const int len = T.item_len[item];
         const int m = T.item_mm[item].x, mp = T.item_mm[item].y;
@@ -530,25 +571,35 @@ __device__ void compose_block(const BandTables& T, const float4* src, const Stag
         const float mir = ((m - mp) & 1) ? -1.0f : 1.0f;
         const float mirp = ((pa - pb) & 1) ? -1.0f : 1.0f;
         const int r0 = T.row_off[item >> 5], lane = item & 31;
-        for (int st = 0; st < len; ++st) {
-            if (st > 0) {
-                const float4 pqr = __ldg(T.PQR + (r0 + st) * 32 + lane);
-                const float dn = fmaf(pqr.x, cb, pqr.y) * d - pqr.z * d1;
-                d1 = d;
-                d = dn;
-            }
-            const int l = m + st, w = 2 * l + 1, o = xi_off(l);
-            dtab[o + (m + l) * w + (mp + l)] = d;
-            dtab[o + (-m + l) * w + (-mp + l)] = mir * d;
-            if (pair) {
-                dtab[o + (pa + l) * w + (pb + l)] = sg * d;
-                dtab[o + (-pa + l) * w + (-pb + l)] = mirp * sg * d;
+        for (int s0 = 0; s0 < len; s0 += 4) {
+            float4 pq[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                pq[u] = (s0 + u > 0 && s0 + u < len) ? __ldg(T.PQR + (r0 + s0 + u) * 32 + lane)
+                                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int st = s0 + u;
+                if (st >= len) break;
+                if (st > 0) {
+                    const float4 pqr = pq[u];
+                    const float dn = fmaf(pqr.x, cb, pqr.y) * d - pqr.z * d1;
+                    d1 = d;
+                    d = dn;
+                }
+                const int l = m + st, w = 2 * l + 1, o = xi_off(l);
+                dtab[o + (m + l) * w + (mp + l)] = d;
+                dtab[o + (-m + l) * w + (-mp + l)] = mir * d;
+                if (pair) {
+                    dtab[o + (pa + l) * w + (pb + l)] = sg * d;
+                    dtab[o + (-pa + l) * w + (-pb + l)] = mirp * sg * d;
+                }
             }
         }
     }
-    // dense xi'_l[m,n] = xi_l[m,n] e^{-i n g} over the full plane: the A and B
-    // entries of every (row, lane) and their conjugate mirrors
-    // xi_{-m,-n} = (-1)^(m+n) conj(xi_{m,n})
+    // rows m >= 0 of xi'_l[m,n] = xi_l[m,n] e^{-i n g}: the A and B entries of
+    // every (row, lane) (first index >= 0), and for m = 0 the conjugate mirror
+    // xi_{0,-n} = (-1)^n conj(xi_{0,n})
     for (int at = tid; at < T.rows * 32; at += nt) {
         const int row = at >> 5, j = at & 31;
         const int g = a.row_group[row];
@@ -556,7 +607,7 @@ __device__ void compose_block(const BandTables& T, const float4* src, const Stag
         const int st = row - T.row_off[g];
         if (st >= T.item_len[item]) continue;
         const float4 x4 = src[at];
-        const int l = T.item_mm[item].x + st, w = 2 * l + 1, o = xi_off(l);
+        const int l = T.item_mm[item].x + st, w = 2 * l + 1, o = xh_off(l);
 #pragma unroll
         for (int slot = 0; slot < 2; ++slot) {
             if (slot == 1 && T.item_w[item].y == 0.0f) break;
@@ -565,15 +616,17 @@ __device__ void compose_block(const BandTables& T, const float4* src, const Stag
             const float2 x = slot ? make_float2(x4.z, x4.w) : make_float2(x4.x, x4.y);
             float2 egp = cs.ug[abs(mp)];
             if (mp < 0) egp.y = -egp.y;
-            xd[o + (m + l) * w + (mp + l)] = cmul(x, egp);
-            const float sgn = ((m + mp) & 1) ? -1.0f : 1.0f;
-            const float2 xm = make_float2(sgn * x.x, -sgn * x.y);  // xi[-m,-m']
-            xd[o + (-m + l) * w + (-mp + l)] = cmul(xm, make_float2(egp.x, -egp.y));
+            xd[o + m * w + (mp + l)] = cmul(x, egp);
+            if (m == 0) {
+                const float sgn = (mp & 1) ? -1.0f : 1.0f;
+                const float2 xm = make_float2(sgn * x.x, -sgn * x.y);  // xi[0,-m']
+                xd[o + (-mp + l)] = cmul(xm, make_float2(egp.x, -egp.y));
+            }
         }
     }
     group_sync<WARP>();
-    const bool wedge = out_w != nullptr;
-    if (wedge) {  // q~_l[m'] = e^{-i m' a} sum_n d_{m'n} e^{-i n g} q_ln
+    // q~_l[m'] = e^{-i m' a} sum_n d_{m'n} e^{-i n g} q_ln (rank-one wedge factor)
+    if (wedge) {
         for (int idx = tid; idx < (L + 1) * (L + 1); idx += nt) {
             int l = 0;
             while ((l + 1) * (l + 1) <= idx) ++l;
@@ -582,7 +635,7 @@ __device__ void compose_block(const BandTables& T, const float4* src, const Stag
             float re = 0.0f, im = 0.0f;
             for (int n = -l; n <= l; ++n) {
                 const int an = abs(n);
-                double2 qv = a.q_hat[l * (l + 1) / 2 + an];
+                double2 qv = qh[l * (l + 1) / 2 + an];
                 if (n < 0) {
                     const double sgn = (an & 1) ? -1.0 : 1.0;
                     qv = make_double2(sgn * qv.x, -sgn * qv.y);
@@ -598,20 +651,19 @@ __device__ void compose_block(const BandTables& T, const float4* src, const Stag
             if (mp < 0) eam.y = -eam.y;
             qt[idx] = cmul(eam, make_float2(re, im));
         }
-        group_sync<WARP>();
     }
-    const float inv_total = (float)(1.0 / a.wp_total);
-    // zero the layout (padding lanes, steps past an item's chain, B of self-paired items)
+    // zero the layout positions no half-plane entry maps to (padding lanes, steps
+    // past an item's chain, B of self-paired items); the product writes the rest
     for (int at = tid; at < T.rows * 32; at += nt) {
-        out[at] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (wedge) out_w[at] = make_float4(0.f, 0.f, 0.f, 0.f);
+        const int row = at >> 5, item = a.row_group[row] * 32 + (at & 31);
+        const int st = row - T.row_off[item >> 5];
+        if (st >= T.item_len[item]) out[at] = make_float4(0.f, 0.f, 0.f, 0.f);
+        else if (T.item_w[item].y == 0.0f) reinterpret_cast<float2*>(out)[2 * at + 1] = make_float2(0.f, 0.f);
     }
-    group_sync<WARP>();
     // xi~_l[m,m'] = e^{-i m' a} sum_n X_l[m,n] d^l_{m'n} over the half plane m >= 0,
     // one task per (l, m, quad of 4 consecutive m'): the X row is loaded once per n
     // for 4 outputs; results scatter to their (item, slot) of the band layout
     float2* outp = reinterpret_cast<float2*>(out);
-    float2* outwp = reinterpret_cast<float2*>(out_w);
     int total = 0;
     for (int l = 0; l <= L; ++l) total += (l + 1) * ((2 * l + 4) / 4);
     for (int wi = tid; wi < total; wi += nt) {
@@ -624,7 +676,7 @@ __device__ void compose_block(const BandTables& T, const float4* src, const Stag
         const int nq = (2 * l + 4) / 4;
         const int m = (wi - base) / nq, q0 = -l + 4 * ((wi - base) % nq);
         const int w = 2 * l + 1, o = xi_off(l);
-        const float2* xrow = xd + o + (m + l) * w;
+        const float2* xrow = xd + xh_off(l) + m * w;
         const float* drow[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) drow[j] = dtab + o + (min(q0 + j, l) + l) * w;
@@ -639,12 +691,6 @@ __device__ void compose_block(const BandTables& T, const float4* src, const Stag
                 acc[j].y = fmaf(x.y, dv, acc[j].y);
             }
         }
-        float cr = 0.0f, ci = 0.0f;  // conj(chi_lm), m >= 0 (wedge only)
-        if (wedge) {
-            const double2 c = a.chi_hat[l * (l + 1) / 2 + m];
-            cr = (float)c.x;
-            ci = (float)-c.y;
-        }
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const int mp = q0 + j;
@@ -655,11 +701,32 @@ __device__ void compose_block(const BandTables& T, const float4* src, const Stag
             float2 eam = cs.ua[abs(mp)];
             if (mp < 0) eam.y = -eam.y;
             outp[2 * at + slot] = cmul(eam, acc[j]);
-            if (wedge) {
-                const float2 qv = qt[l * l + (mp + l)];
-                outwp[2 * at + slot] =
-                    make_float2((cr * qv.x - ci * qv.y) * inv_total, (cr * qv.y + ci * qv.x) * inv_total);
+        }
+    }
+    if (wedge) {
+        group_sync<WARP>();
+        // wedge kernel conj(chi_lm) q~_lm' / total, every layout position (A, B)
+        const float inv_total = (float)(1.0 / a.wp_total);
+        for (int at = tid; at < T.rows * 32; at += nt) {
+            const int row = at >> 5, item = a.row_group[row] * 32 + (at & 31);
+            const int st = row - T.row_off[item >> 5];
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (st < T.item_len[item]) {
+                const int l = T.item_mm[item].x + st;
+#pragma unroll
+                for (int slot = 0; slot < 2; ++slot) {
+                    if (slot == 1 && T.item_w[item].y == 0.0f) break;
+                    const char2 e = slot ? T.item_pm[item] : T.item_mm[item];
+                    const double2 c = chh[l * (l + 1) / 2 + e.x];
+                    const float cr = (float)c.x, ci = (float)-c.y;
+                    const float2 qv = qt[l * l + (e.y + l)];
+                    const float2 wv =
+                        make_float2((cr * qv.x - ci * qv.y) * inv_total, (cr * qv.y + ci * qv.x) * inv_total);
+                    if (slot) v.z = wv.x, v.w = wv.y;
+                    else v.x = wv.x, v.y = wv.y;
+                }
             }
+            out_w[at] = v;
         }
     }
     group_sync<WARP>();
@@ -872,22 +939,9 @@ __global__ void __launch_bounds__(256) compose_kernel(StageArgs a) {
     __shared__ ComposeScratch cs;
     __shared__ int s_slot;
     const int n = a.counts[CNT_COMP];
-    const int L = a.T.L;
-    const int nxi = xi_off(L + 1);
     const int len = a.T.rows * 32;
     const bool wedge = a.prm.has_wedge != 0;
-    float* dtab;
-    float2 *xd, *qt;
-    if (SMEM) {
-        dtab = reinterpret_cast<float*>(sm);
-        xd = reinterpret_cast<float2*>(dtab + ((nxi + 1) & ~1));
-        qt = xd + nxi;
-    } else {
-        float* base = a.scratch + (size_t)blockIdx.x * a.scratch_per_warp;
-        dtab = base;
-        xd = reinterpret_cast<float2*>(dtab + ((nxi + 1) & ~1));
-        qt = xd + nxi;
-    }
+    float* scr = SMEM ? reinterpret_cast<float*>(sm) : a.scratch + (size_t)blockIdx.x * a.scratch_per_warp;
     for (int q = blockIdx.x; q < n; q += gridDim.x) {
         const int i = a.listc[q];
         CandWork& wk = a.work[i];
@@ -907,7 +961,7 @@ __global__ void __launch_bounds__(256) compose_kernel(StageArgs a) {
         const int slot = s_slot;
         if (slot >= 0) {
             const int w = i / a.max_cand;
-            compose_block(a.T, a.xi_win + (size_t)w * len, a, qload(a.cand[i].anchor), dtab, xd, qt,
+            compose_block(a.T, a.xi_win + (size_t)w * len, a, qload(a.cand[i].anchor), scr,
                           a.xi_pool + (size_t)slot * len, wedge ? a.w_pool + (size_t)slot * len : nullptr, cs);
         }
         if (threadIdx.x == 0) {
@@ -1342,10 +1396,6 @@ __global__ void __launch_bounds__(kFT, 3) refine_fused_kernel(FusedArgs fa) {
             FP_MARK(0);
             __syncthreads();
             FP_MARK(7);
-            const int nxi = xi_off(a.T.L + 1);
-            float* dtab = scr;
-            float2* xd = reinterpret_cast<float2*>(dtab + ((nxi + 1) & ~1));
-            float2* qt = xd + nxi;
             for (;;) {
                 const int fl = mine ? iter_begin_one(a, base + c) : 0;
                 const bool anch = (fl & 1) && a.cand[base + c].anchored;
@@ -1360,7 +1410,7 @@ __global__ void __launch_bounds__(kFT, 3) refine_fused_kernel(FusedArgs fa) {
                 for (int q = 0; q < ncomp; ++q) {
                     const int cc = L_.c[q];
                     const size_t slot = (size_t)blockIdx.x * maxc + cc;
-                    compose_block<true>(a.T, sxi, a, qload(a.cand[base + cc].anchor), dtab, xd, qt,
+                    compose_block<true>(a.T, sxi, a, qload(a.cand[base + cc].anchor), scr,
                                         fa.xi_pool + slot * fa.slot_len,
                                         WEDGE ? fa.w_pool + slot * fa.slot_len : nullptr, csc[warp]);
                     if (lane == 0) {
@@ -1458,11 +1508,7 @@ __global__ void build_xi_kernel(XiArgs a) {
 
 }  // namespace
 
-long long compose_scratch_floats(int L) {
-    // dtab (N_xi floats) + dense xi' (N_xi complex) + q~ ((L+1)^2 complex)
-    const long long nxi = xi_off(L + 1);
-    return ((nxi + 2) + 2 * nxi + 2LL * (L + 1) * (L + 1) + 3) / 4 * 4;
-}
+long long compose_scratch_floats(int L) { return compose_layout(L).total; }
 
 size_t compose_smem_bytes(int L) { return sizeof(float) * (size_t)compose_scratch_floats(L); }
 
