@@ -1,4 +1,5 @@
 // Context construction and the batched expansion driver.
+#include <cstring>
 #include "context.hpp"
 
 #include <algorithm>
@@ -110,8 +111,28 @@ void Context::build_factored_tables() {
                     const int j = m == 0 ? 0 : 2 * m - 1 + part;
                     rowpack[basis.row(l, k, m, part)] = ((ft.pair_off[l] + k - 1) << 16) | (l * l + j);
                 }
+    // trilinear footprint of every quadrature sample (sample_trilinear,
+    // src/volume.cpp:19-48): g = r * (h d_tp) + h in FP64 exactly as the device
+    // formerly computed it, base voxel packed 10 bits per axis, FP32 fractions;
+    // indexed [ray][radius] (a warp's lanes walk along rays)
+    if (n > 1023) throw std::invalid_argument("factored expansion: grid edge above 1023");
+    std::vector<int4> samp((size_t)nt * np * nr);
+    for (int s = 0; s < nt * np; ++s)
+        for (int i = 0; i < nr; ++i) {
+            const double r = basis.r[i];
+            const double* d = dirh.data() + 3 * (size_t)s;
+            const double gx = std::fma(r, d[0], h), gy = std::fma(r, d[1], h), gz = std::fma(r, d[2], h);
+            const int x0 = (int)gx, y0 = (int)gy, z0 = (int)gz;
+            const float fx = (float)(gx - (double)x0), fy = (float)(gy - (double)y0), fz = (float)(gz - (double)z0);
+            int4 e;
+            e.x = (x0 & 1023) | ((y0 & 1023) << 10) | ((z0 & 1023) << 20);
+            std::memcpy(&e.y, &fx, 4);
+            std::memcpy(&e.z, &fy, 4);
+            std::memcpy(&e.w, &fz, 4);
+            samp[(size_t)s * nr + i] = e;
+        }
     upload(fx_r, basis.r, stream);
-    upload(fx_dirh, dirh, stream);
+    upload(fx_samp, samp, stream);
     upload(fx_tw, tw, stream);
     upload(fx_ptab, ptab, stream);
     upload(fx_trilm, tlm, stream);
@@ -126,7 +147,7 @@ void Context::build_factored_tables() {
     fx.ntri = ntri;
     fx.pairs = ft.pairs;
     fx.r = fx_r.as<double>();
-    fx.dirh = fx_dirh.as<double>();
+    fx.samp = fx_samp.as<int4>();
     fx.tw = fx_tw.as<float2>();
     fx.ptab = fx_ptab.as<float>();
     fx.tri_lm = fx_trilm.as<int2>();

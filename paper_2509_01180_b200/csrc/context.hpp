@@ -194,7 +194,7 @@ public:
     void ensure_operator();
     void build_factored_tables();
     FactoredTables fx;
-    DevBuf fx_r, fx_dirh, fx_tw, fx_ptab, fx_trilm, fx_radial, fx_rowmap;
+    DevBuf fx_r, fx_samp, fx_tw, fx_ptab, fx_trilm, fx_radial, fx_rowmap;
     int gemm_block_n = 128;
     int gemm_kchunk = 4;
     long long max_chunk_windows = 8192;  // windows expanded per GEMM chunk

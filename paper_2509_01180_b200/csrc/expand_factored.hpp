@@ -9,7 +9,7 @@ struct FactoredTables {
     int n = 0, L = 0, nr = 0, nt = 0, np = 0;
     int coeffs = 0, ntri = 0, pairs = 0;
     const double* r = nullptr;        // [nr] GL radii on [0, 1]
-    const double* dirh = nullptr;     // [nt * np][3] (n/2) * ray direction (sin t cos p, sin t sin p, cos t)
+    const int4* samp = nullptr;       // [nt * np][nr] trilinear footprint: x0 | y0 << 10 | z0 << 20, fx, fy, fz (FP32 bits)
     const float2* tw = nullptr;       // [np/2 + 1][L + 1] (cos, -sin)(2 pi m p / np)
     const float* ptab = nullptr;      // [ntri][nt] Pbar_l^m(u_t) w_t
     const int2* tri_lm = nullptr;     // [ntri] (l, m)

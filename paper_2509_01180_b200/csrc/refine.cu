@@ -1014,11 +1014,13 @@ __device__ __forceinline__ void eval_group(const BandTables& T, const EvalJob (&
 }
 
 // K listed candidates per warp
+// resident CTAs per SM the evaluation kernels are compiled for (register cap):
+// measured best 4 at order 2 (80 registers, small spills) and 3 at order 0
 #ifndef BMB_EVAL_MINB
-#define BMB_EVAL_MINB 1
+#define BMB_EVAL_MINB(order) ((order) == 2 ? 4 : 3)
 #endif
 template <int ORDER, int K>
-__global__ void __launch_bounds__(EvalShape<K>::WARPS * 32, BMB_EVAL_MINB) eval_kernel(StageArgs a, const int* list,
+__global__ void __launch_bounds__(EvalShape<K>::WARPS * 32, BMB_EVAL_MINB(ORDER)) eval_kernel(StageArgs a, const int* list,
                                                                                        const int* count) {
     constexpr int WARPS = EvalShape<K>::WARPS;
     __shared__ WarpScratch wsc[WARPS * K];
