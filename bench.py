@@ -195,6 +195,50 @@ def config_block(batch):
             "lambda_cut": "16*pi", "l2": "inputs larger than L2 (1 GiB of particles per rank)"}
 
 
+# kernel classes of the CUPTI breakdown (name prefix -> class)
+KCLASS = (("expand_factored", "expand"), ("split3_gemm", "expand"), ("gather_windows", "expand"),
+          ("eval_kernel<2", "eval_order2"), ("eval_kernel<0", "eval_order0"), ("compose_kernel", "compose"),
+          ("iter_begin", "newton"), ("step_kernel", "newton"), ("accept_kernel", "newton"),
+          ("band_begin", "newton"), ("final_", "newton"), ("prune", "newton"), ("seed_kernel", "seed"),
+          ("build_xi", "xi_build"), ("window_reduce", "misc"), ("window_norms", "misc"),
+          ("average", "average"), ("fft", "wedge"), ("scale_spectrum", "wedge"))
+
+
+def cupti_step(fn):
+    """Run fn under torch.profiler (CUPTI); per-class device ms, GPU busy ms (union of
+    kernel intervals) and per-class launch counts."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        fn()
+        torch.cuda.synchronize()
+    ms, n, iv = {}, {}, []
+    for e in prof.events():
+        if e.device_type != torch.autograd.DeviceType.CUDA:
+            continue
+        name = e.name.replace("(anonymous namespace)::", "").replace("void ", "").replace("bmb::", "")
+        if name.startswith("Memcpy") or name.startswith("Memset"):
+            continue
+        cls = next((c for k, c in KCLASS if name.startswith(k) or k in name.split("(")[0]), "other")
+        d = (e.time_range.end - e.time_range.start) / 1e3
+        ms[cls] = ms.get(cls, 0.0) + d
+        n[cls] = n.get(cls, 0) + 1
+        iv.append((e.time_range.start, e.time_range.end))
+    iv.sort()
+    busy, cs, ce = 0.0, None, None
+    for a, b in iv:
+        if ce is None or a > ce:
+            if ce is not None:
+                busy += ce - cs
+            cs, ce = a, b
+        else:
+            ce = max(ce, b)
+    if ce is not None:
+        busy += ce - cs
+    ms["refine"] = sum(ms.get(k, 0.0) for k in ("eval_order2", "eval_order0", "compose", "newton", "xi_build"))
+    return ms, busy / 1e3, n
+
+
 def run_product(args):
     import torch
     import torch.distributed as dist
@@ -283,16 +327,15 @@ def run_product(args):
     e2e_ms = float(t.item())
     h2d = host.numel() * 4
 
-    # ---------------- one instrumented step: CUDA events around every launch on the
-    # context stream (kernel shares for the roofline), outside the timed regions
-    # (one lane: concurrent lanes would overlap the kernels being timed)
+    # ---------------- one instrumented step, outside the timed regions: per-launch
+    # device durations from CUPTI activity records (torch.profiler; no replay, warm
+    # caches, no host enqueue gaps), one lane so that no two kernels overlap
     ctx.set_lanes(1)
-    ctx.set_timing(True)
+    ctx.set_timing(True)  # launch / window counters
     ctx.timings(reset=True)
     ctx.eval_stats(reset=True)
-    step(parts)
-    torch.cuda.synchronize()
-    kms, counts = ctx.timings(reset=True)
+    kms, busy_ms, launch_ms = cupti_step(lambda: step(parts))
+    _, counts = ctx.timings(reset=True)
     ev2, ev0, ev_flops = ctx.eval_stats(reset=True)
     ctx.set_timing(False)
     ctx.set_lanes(3)
@@ -316,11 +359,11 @@ def run_product(args):
     peaks, peak_kind = measured_peaks()
     steps = 1  # the instrumented step
     C, V = ctx.coeff_count, ctx.support
-    gemm_ms = kms["expand"] / steps
+    gemm_ms = kms.get("expand", 0.0) / steps
     refine_ms = kms["refine"] / steps
     windows_per_step = counts["windows_expanded"] / steps
     gemm_launches = max(1, counts["gemm_launches"] // steps)
-    kernels = {k: round(v / steps, 3) for k, v in kms.items()}
+    kernels = {k: round(v / steps, 3) for k, v in sorted(kms.items(), key=lambda x: -x[1])}
     evals_per_step = sum(r["evaluations"] for r in res)
     fp32_peak, fp32_kind = fp32_simt_peak()
     if args.expand == "gemm":
@@ -345,7 +388,7 @@ def run_product(args):
                       "unit": "TFLOP/s", "per_launch_flops": gemm_flops / gemm_launches, "traffic": None})
     roof_gemm["frac"] = roof_gemm["achieved"] / peak_x if roof_gemm["achieved"] else None
     # rotate-score-gradient evaluation kernels (FP32 SIMT register recursion)
-    eval_ms = kms["eval_order2"] + kms["eval_order0"]
+    eval_ms = kms.get("eval_order2", 0.0) + kms.get("eval_order0", 0.0)
     roof_eval = {"kernel": "eval_kernel<2>+eval_kernel<0> (warp Wigner-d recursion, K jobs per warp)",
                  "bound": "fp32_simt",
                  "achieved": ev_flops / (eval_ms / 1000.0) / 1e12 if eval_ms > 0 else None,
@@ -368,8 +411,10 @@ def run_product(args):
         "roofline_refine_eval": roof_eval,
         "dominant_kernel": dominant,
         "kernel_ms_per_step": kernels,
-        "kernel_ms_note": "CUDA events on the context stream, one instrumented single-lane step outside the "
-                          "timed region (the timed region runs 3 concurrent lanes)",
+        "kernel_ms_note": "CUPTI device durations (torch.profiler) of one instrumented single-lane step outside "
+                          "the timed region (the timed region runs 3 concurrent lanes); GPU busy %.1f ms of "
+                          "that step" % busy_ms,
+        "kernel_launches": launch_ms,
         "refine": {"ms_per_step": refine_ms, "eval_kernels_ms_per_step": eval_ms,
                    "evaluations_per_step": evals_per_step,
                    "note": "evaluations_per_step counts the seed grid too (align() counters)"},

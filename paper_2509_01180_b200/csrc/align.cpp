@@ -335,20 +335,26 @@ void Context::refine_windows(int nw, int maxc, const AlignConfig& cfg, const Qua
                 a.compose_smem = compose_smem_bytes(L) <= 200 * 1024 ? 1 : 0;
                 a.scratch_per_warp = compose_scratch_floats(L);
                 const long long slots = (long long)cnt * maxc;
-                lists_.reserve(sizeof(int) * 4 * (size_t)slots);
+                lists_.reserve(sizeof(int) * 6 * (size_t)slots);
                 a.list2 = lists_.as<int>();
                 a.listc = a.list2 + slots;
                 int* lt0 = a.listc + slots;
                 int* lt1 = lt0 + slots;
+                int* ls[2] = {lt1 + slots, lt1 + 2 * slots};  // start lists (this / next iteration)
+                int* d_start = d_counts + 6;                    // their counts
                 a.counts = d_counts;
                 a.eval_stats = eval_stats();
                 ck(cudaMemsetAsync(d_pool, 0, sizeof(int), stream), "pool");
-                launch_band_begin(a, stream);
+                ck(cudaMemsetAsync(d_start, 0, sizeof(int) * 2, stream), "start counts");
+                launch_band_begin(a, ls[0], d_start, stream);
+                int cur = 0;
+                long long start_max = slots;
                 ++timer.launches;
                 for (int it = 0; it < cfg.newton_max_iter; ++it) {
                     ck(cudaMemsetAsync(d_counts, 0, sizeof(int) * 4, stream), "counts");
                     cudaEvent_t n2e = timer.begin(stream);
-                    launch_iter_begin(a, stream);
+                    ck(cudaMemsetAsync(d_start + (cur ^ 1), 0, sizeof(int), stream), "next start count");
+                    launch_iter_begin(a, ls[cur], d_start + cur, (int)std::max<long long>(1, start_max), stream);
                     timer.end(K_NEWTON, n2e, stream);
                     ++timer.launches;
                     ck(cudaMemcpyAsync(h_active, d_counts, sizeof(int) * 2, cudaMemcpyDeviceToHost, stream),
@@ -383,10 +389,12 @@ void Context::refine_windows(int nw, int maxc, const AlignConfig& cfg, const Qua
                         timer.end(K_EVAL0, e0, stream);
                         ck(cudaMemsetAsync(cdst, 0, sizeof(int), stream), "retry count");
                         cudaEvent_t n1 = timer.begin(stream);
-                        launch_accept(a, src, csrc, dst, cdst, n2, stream);
+                        launch_accept(a, src, csrc, dst, cdst, ls[cur ^ 1], d_start + (cur ^ 1), n2, stream);
                         timer.end(K_NEWTON, n1, stream);
                         timer.launches += 2;
                     }
+                    cur ^= 1;
+                    start_max = n2;  // accepted trials <= evaluated candidates
                 }
                 const bool prune_now = cfg.prune_after_band && cfg.bands.size() > 1 && bi == 0;
                 if (bi + 1 == cfg.bands.size() || prune_now) {

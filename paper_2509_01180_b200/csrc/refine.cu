@@ -875,20 +875,28 @@ __device__ __forceinline__ void band_begin_one(const StageArgs& a, long long i) 
     wk.status = ST_START;
 }
 
-__global__ void band_begin_kernel(StageArgs a) {
+// band start of every candidate slot; the started candidates form the first
+// iteration's start list (ordered appends, whole warps)
+__global__ void band_begin_kernel(StageArgs a, int* start, int* start_count) {
     const long long n = (long long)a.n_win * a.max_cand;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+    const long long n_pad = (n + 31) & ~31LL;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n_pad;
          i += (long long)gridDim.x * blockDim.x) {
-        if (!slot_of(a, i)) {
-            CandWork& wk = a.work[i];
-            wk.slot = -1;
-            wk.compose = 0;
-            wk.iter = 0;
-            wk.retry = 0;
-            wk.status = ST_DONE;
-            continue;
+        bool st = false;
+        if (i < n) {
+            if (!slot_of(a, i)) {
+                CandWork& wk = a.work[i];
+                wk.slot = -1;
+                wk.compose = 0;
+                wk.iter = 0;
+                wk.retry = 0;
+                wk.status = ST_DONE;
+            } else {
+                band_begin_one(a, i);
+                st = a.work[i].status == ST_START;
+            }
         }
-        band_begin_one(a, i);
+        wappend(st, (int)i, start, start_count);
     }
 }
 
@@ -920,14 +928,16 @@ __device__ __forceinline__ int iter_begin_one(const StageArgs& a, long long i) {
     return 1 | (wk.compose ? 2 : 0);
 }
 
-__global__ void iter_begin_kernel(StageArgs a) {
-    const long long n = (long long)a.n_win * a.max_cand;
-    const long long n_pad = (n + 31) & ~31LL;  // whole warps (ballots)
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n_pad;
-         i += (long long)gridDim.x * blockDim.x) {
-        const int f = i < n ? iter_begin_one(a, i) : 0;
-        wappend(f & 1, (int)i, a.list2, a.counts + CNT_L2);
-        wappend((f & 2) != 0, (int)i, a.listc, a.counts + CNT_COMP);
+// iteration start of the candidates on the start list (band start, or accepted
+// trials of the previous iteration); appends to the order-2 and composition lists
+__global__ void iter_begin_kernel(StageArgs a, const int* start, const int* start_count) {
+    const int n = *start_count;
+    const int n_pad = (n + 31) & ~31;
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_pad; q += gridDim.x * blockDim.x) {
+        const int i = q < n ? start[q] : -1;
+        const int f = i >= 0 ? iter_begin_one(a, i) : 0;
+        wappend(f & 1, i, a.list2, a.counts + CNT_L2);
+        wappend((f & 2) != 0, i, a.listc, a.counts + CNT_COMP);
     }
 }
 
@@ -1132,14 +1142,17 @@ __device__ __forceinline__ bool accept_one(const StageArgs& a, long long i) {
 
 // acceptance test of every trial in list_in; failed trials with retries left
 // are re-queued in list_out
+// acceptance test of every trial in list_in; failed trials with retries left
+// are re-queued in list_out, accepted ones join the next iteration's start list
 __global__ void accept_kernel(StageArgs a, const int* list_in, const int* count_in, int* list_out,
-                              int* count_out) {
+                              int* count_out, int* start_out, int* start_count) {
     const int n = *count_in;
     const int n_pad = (n + 31) & ~31;
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_pad; q += gridDim.x * blockDim.x) {
         const int i = q < n ? list_in[q] : -1;
         const bool rq = i >= 0 && accept_one(a, i);
         wappend(rq, i, list_out, count_out);
+        wappend(i >= 0 && !rq && a.work[i].status == ST_START, i, start_out, start_count);
     }
 }
 
@@ -1534,11 +1547,11 @@ static int thread_grid(long long n) {
     return (int)(b < 1 ? 1 : (b > 16384 ? 16384 : b));
 }
 
-void launch_band_begin(const StageArgs& a, cudaStream_t s) {
-    band_begin_kernel<<<thread_grid((long long)a.n_win * a.max_cand), kNB, 0, s>>>(a);
+void launch_band_begin(const StageArgs& a, int* start, int* start_count, cudaStream_t s) {
+    band_begin_kernel<<<thread_grid((long long)a.n_win * a.max_cand), kNB, 0, s>>>(a, start, start_count);
 }
-void launch_iter_begin(const StageArgs& a, cudaStream_t s) {
-    iter_begin_kernel<<<thread_grid((long long)a.n_win * a.max_cand), kNB, 0, s>>>(a);
+void launch_iter_begin(const StageArgs& a, const int* start, const int* start_count, int max_n, cudaStream_t s) {
+    iter_begin_kernel<<<thread_grid(max_n), kNB, 0, s>>>(a, start, start_count);
 }
 void launch_compose(const StageArgs& a, int n, cudaStream_t s) {
     if (n <= 0) return;
@@ -1587,8 +1600,9 @@ void launch_step(const StageArgs& a, int* list_out, int* count_out, int max_n, c
     step_kernel<<<thread_grid(max_n), kNB, 0, s>>>(a, list_out, count_out);
 }
 void launch_accept(const StageArgs& a, const int* list_in, const int* count_in, int* list_out, int* count_out,
-                   int max_n, cudaStream_t s) {
-    accept_kernel<<<thread_grid(max_n), kNB, 0, s>>>(a, list_in, count_in, list_out, count_out);
+                   int* start_out, int* start_count, int max_n, cudaStream_t s) {
+    accept_kernel<<<thread_grid(max_n), kNB, 0, s>>>(a, list_in, count_in, list_out, count_out, start_out,
+                                                     start_count);
 }
 void launch_final_prep(const StageArgs& a, cudaStream_t s) {
     final_prep_kernel<<<thread_grid((long long)a.n_win * a.max_cand), kNB, 0, s>>>(a);

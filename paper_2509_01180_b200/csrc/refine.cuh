@@ -72,13 +72,15 @@ struct ReduceArgs {
 
 long long compose_scratch_floats(int L);
 size_t compose_smem_bytes(int L);
-void launch_band_begin(const StageArgs& a, cudaStream_t s);
-void launch_iter_begin(const StageArgs& a, cudaStream_t s);
+// band start of every candidate; the started ones are appended to start
+void launch_band_begin(const StageArgs& a, int* start, int* start_count, cudaStream_t s);
+// iteration start of the candidates on a start list (max_n bounds its length)
+void launch_iter_begin(const StageArgs& a, const int* start, const int* start_count, int max_n, cudaStream_t s);
 void launch_compose(const StageArgs& a, int n, cudaStream_t s);
 void launch_eval(const StageArgs& a, int order, const int* list, const int* count, int max_n, cudaStream_t s);
 void launch_step(const StageArgs& a, int* list_out, int* count_out, int max_n, cudaStream_t s);
 void launch_accept(const StageArgs& a, const int* list_in, const int* count_in, int* list_out, int* count_out,
-                   int max_n, cudaStream_t s);
+                   int* start_out, int* start_count, int max_n, cudaStream_t s);
 void launch_final_prep(const StageArgs& a, cudaStream_t s);
 void launch_final_score(const StageArgs& a, int max_n, cudaStream_t s);
 void launch_window_reduce(const ReduceArgs& a, cudaStream_t s);
