@@ -45,12 +45,12 @@ __host__ __device__ inline Smem smem_plan(const FactoredTables& T) {
     size_t o = 0;
     s.samp = o;
     o = al16(o + sizeof(float) * (size_t)kRC * T.nt * T.np);
-    s.F = o;  // per radius of the pass
-    o = al16(o + sizeof(float2) * (size_t)kRC * T.nt * (T.L + 1));
+    s.F = o;
+    o = al16(o + sizeof(float2) * (size_t)T.nt * (T.L + 1));
     s.G = o;
-    o = al16(o + sizeof(float) * (size_t)kRC * (T.L + 1) * (T.L + 1));
+    o = al16(o + sizeof(float) * (size_t)(T.L + 1) * (T.L + 1));
     s.rad = o;
-    o = al16(o + sizeof(float) * (size_t)kRC * T.pairs);
+    o = al16(o + sizeof(float) * (size_t)T.pairs);
     s.rowpack = o;
     o = al16(o + sizeof(int) * (size_t)T.coeffs);
     s.total = o;
@@ -92,14 +92,13 @@ __global__ void __launch_bounds__(kThreads, BMB_EXPAND_MINB) expand_factored_ker
     for (int q = 0; q < RPT; ++q) acc[q] = 0.0f;
     __syncthreads();
 
-    // passes of kRC radii: sample, DFT, theta and radial stages each run over
-    // all radii of the pass between barriers (radial sums stay in radius order)
-    for (int ir = 0; ir < T.nr; ir += kRC) {
-        const int nrc = min(kRC, T.nr - ir);
-        {
+    for (int ir = 0; ir < T.nr; ++ir) {
+        const int rc = ir % kRC;
+        if (rc == 0) {
             // 1. trilinear samples of the shifted window for radii ir .. ir+kRC-1
             //    (zero outside the grid and where the shifted source leaves it);
             //    0 < g < n, so truncation = floor.  Item = (ray, radius), radius fastest.
+            const int nrc = min(kRC, T.nr - ir);
             const int items = nsamp * kRC;
             for (int it0 = tid; it0 < items; it0 += kU * kThreads) {
                 float val[kU];
@@ -155,13 +154,13 @@ __global__ void __launch_bounds__(kThreads, BMB_EXPAND_MINB) expand_factored_ker
                 }
             }
         }
-        // radial slices of the pass's radii
-        for (int i = tid; i < nrc * T.pairs; i += kThreads) rad[i] = T.radial_t[(size_t)ir * T.pairs + i];
+        // radial slice of this radius (read after the barriers below)
+        for (int i = tid; i < T.pairs; i += kThreads) rad[i] = T.radial_t[(size_t)ir * T.pairs + i];
         __syncthreads();
-        // 2. phi-DFT: F[j][t][m] = sum_p f[j][t][p] e^{-2 pi i m p / n_phi}, folded
+        // 2. phi-DFT: F[t][m] = sum_p f[t][p] e^{-2 pi i m p / n_phi}, folded
         if (dtg < TG) {
-            for (int jt = dtg; jt < nrc * nt; jt += TG) {
-                const float* f = samp + jt * np;  // samp[j * nsamp + t * np] = samp[(j nt + t) np]
+            for (int t = dtg; t < nt; t += TG) {
+                const float* f = samp + rc * nsamp + t * np;
                 float re = f[0] + ((dm & 1) ? -f[half] : f[half]);
                 float im = 0.0f;
 #pragma unroll
@@ -172,45 +171,41 @@ __global__ void __launch_bounds__(kThreads, BMB_EXPAND_MINB) expand_factored_ker
                         im = fmaf(a - b, tw[p].y, im);
                     }
                 }
-                F[jt * nl + dm] = make_float2(re, im);
+                F[t * nl + dm] = make_float2(re, im);
             }
         }
         __syncthreads();
-        // 3. theta: G[j][l,m] = sum_t Pbar_l^m(u_t) w_t F[j][t][m], folded over t <-> nt-1-t
-        for (int jq = tid; jq < nrc * T.ntri; jq += kThreads) {
-            const int j = jq / T.ntri, q = jq - j * T.ntri;
+        // 3. theta: G[l,m] = sum_t Pbar_l^m(u_t) w_t F[t][m], folded over t <-> nt-1-t
+        for (int q = tid; q < T.ntri; q += kThreads) {
             const int2 lm = T.tri_lm[q];
             const float sgn = ((lm.x + lm.y) & 1) ? -1.0f : 1.0f;
             const float* pt = T.ptab + (size_t)q * nt;
-            const float2* Fj = F + (size_t)j * nt * nl;
             float re = 0.0f, im = 0.0f;
             for (int t = 0; t < nt / 2; ++t) {
-                const float2 a = Fj[t * nl + lm.y], b = Fj[(nt - 1 - t) * nl + lm.y];
+                const float2 a = F[t * nl + lm.y], b = F[(nt - 1 - t) * nl + lm.y];
                 const float wgt = __ldg(pt + t);
                 re = fmaf(wgt, fmaf(sgn, b.x, a.x), re);
                 im = fmaf(wgt, fmaf(sgn, b.y, a.y), im);
             }
-            float* Gj = Gp + j * nl * nl;
             const int base = lm.x * lm.x;
             if (lm.y == 0) {
-                Gj[base] = re;
+                Gp[base] = re;
             } else {
-                Gj[base + 2 * lm.y - 1] = re;
-                Gj[base + 2 * lm.y] = im;
+                Gp[base + 2 * lm.y - 1] = re;
+                Gp[base + 2 * lm.y] = im;
             }
         }
         __syncthreads();
-        // 4. radial: row (l, k, j) += radial[(l,k)][i] * Gp[l^2 + j], radius by radius
+        // 4. radial: row (l, k, j) += radial[(l,k)][i] * Gp[l^2 + j]
 #pragma unroll
         for (int q = 0; q < RPT; ++q) {
             const int row = tid + q * kThreads;
             if (row < T.coeffs) {
                 const int rp = rowpack[row];
-                for (int j = 0; j < nrc; ++j)
-                    acc[q] = fmaf(rad[j * T.pairs + (rp >> 16)], Gp[j * nl * nl + (rp & 0xffff)], acc[q]);
+                acc[q] = fmaf(rad[rp >> 16], Gp[rp & 0xffff], acc[q]);
             }
         }
-        // samp, rad, F and G are rewritten by the next pass
+        // rad (and samp at the next chunk) are rewritten: all threads must be done here
         __syncthreads();
     }
     float* o = out + (long long)w * ldo;
