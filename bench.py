@@ -338,7 +338,7 @@ def run_product(args):
     _, counts = ctx.timings(reset=True)
     ev2, ev0, ev_flops = ctx.eval_stats(reset=True)
     ctx.set_timing(False)
-    ctx.set_lanes(3)
+    ctx.set_lanes(4)
     import ctypes
     from paper_2509_01180_b200 import _lib
     d2h = P * ctypes.sizeof(_lib.AlignResult) + avg.numel() * 8
@@ -412,7 +412,7 @@ def run_product(args):
         "dominant_kernel": dominant,
         "kernel_ms_per_step": kernels,
         "kernel_ms_note": "CUPTI device durations (torch.profiler) of one instrumented single-lane step outside "
-                          "the timed region (the timed region runs 3 concurrent lanes); GPU busy %.1f ms of "
+                          "the timed region (the timed region runs 4 concurrent lanes); GPU busy %.1f ms of "
                           "that step" % busy_ms,
         "kernel_launches": launch_ms,
         "refine": {"ms_per_step": refine_ms, "eval_kernels_ms_per_step": eval_ms,

@@ -57,7 +57,7 @@ int bm_context_info(const bm_context* ctx, long long* info);
 int bm_context_set_expand_mode(bm_context* ctx, int mode);
 /* Concurrent lanes of bm_align_batch: a batch of at least lanes * min_per_lane
  * particles is split into `lanes` slices aligned concurrently, each on its own
- * stream with its own buffers and host thread (default 3 lanes, 64 particles per
+ * stream with its own buffers and host thread (default 4 lanes, 64 particles per
  * lane).  Results do not depend on the lane count. */
 int bm_context_set_lanes(bm_context* ctx, int lanes, int min_per_lane);
 /* Refinement schedule of bm_align_batch (refine(), src/optimize.cpp:255-357):

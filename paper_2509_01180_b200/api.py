@@ -288,7 +288,7 @@ class Context:
         return {b: {n: ms[b * 15 + k] for k, n in enumerate(names) if ms[b * 15 + k] > 0} for b in range(4)}
 
     def set_lanes(self, lanes: int, min_per_lane: int = 64):
-        """Concurrent lanes of align_batch (default 3 lanes of >= 64 particles)."""
+        """Concurrent lanes of align_batch (default 4 lanes of >= 64 particles)."""
         _lib.check(_lib.lib().bm_context_set_lanes(self._h, lanes, min_per_lane), "set_lanes")
 
     def set_refine_mode(self, mode: str):

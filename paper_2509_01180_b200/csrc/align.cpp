@@ -651,10 +651,10 @@ void Context::ensure_lanes() {
         c->refine_mode = refine_mode;
         c->pool_budget_ = pool_budget_;  // each lane allocates only what its slice needs
     }
-    if (lanes_stale_) {
-        for (auto& c : lane_ctx_) c->adopt_template(*this);
-        lanes_stale_ = false;
-    }
+    // lanes created after set_template (a larger set_lanes) adopt it too
+    for (auto& c : lane_ctx_)
+        if (lanes_stale_ || !c->has_template) c->adopt_template(*this);
+    lanes_stale_ = false;
 }
 
 // a lane's template state: its own expansion of the template and wedge filter,

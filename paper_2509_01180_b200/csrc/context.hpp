@@ -223,7 +223,7 @@ public:
     // concurrent lanes: sub-contexts with their own stream and buffers that align
     // slices of a large batch from their own host threads (overlapping the
     // low-occupancy tails of each lane's Newton loop)
-    int lanes = 3;
+    int lanes = 4;
     int lane_min_particles = 64;  // per lane
     std::vector<std::unique_ptr<Context>> lane_ctx_;
     DevBuf tmpl_copy_;

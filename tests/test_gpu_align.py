@@ -202,3 +202,22 @@ def test_fused_refine_matches_list_driven(cuda_device, prune):
         assert list(a["quat"]) == list(b["quat"])
         assert a["score"] == b["score"]
         assert a["evaluations"] == b["evaluations"]
+
+
+def test_lanes_raised_after_set_template(cuda_device):
+    """set_lanes to more lanes after set_template: the new lanes adopt the
+    template (regression: they used to raise 'set_template first')."""
+    import math
+
+    n, L = 32, 8
+    tmpl = api.make_template(n, 20, 5)
+    parts, _, _ = api.make_particles(tmpl, 8, 700, 2, 0.5, 60.0)
+    cfg = api.make_config(bands=(4, 8), max_candidates=8, shift_radius=2, shift_step=2)
+    ctx = api.Context(n, L, L * math.pi)
+    ctx.set_template(tmpl, 60.0)
+    ctx.set_lanes(2, 2)
+    a = ctx.align_batch(parts, cfg)
+    ctx.set_lanes(4, 2)
+    b = ctx.align_batch(parts, cfg)
+    for x, y in zip(a, b):
+        assert x["shift"] == y["shift"] and list(x["quat"]) == list(y["quat"]) and x["score"] == y["score"]
