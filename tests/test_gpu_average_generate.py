@@ -89,3 +89,44 @@ def test_synthesize_matches_oracle(cuda_device, n, L, m_out):
     assert np.linalg.norm(got_c - ref) <= 1e-10 * np.linalg.norm(ref)
     # the averaged map of an identity alignment reproduces the template's band-limited map
     assert np.linalg.norm(got - tmpl) <= 0.5 * np.linalg.norm(tmpl) if m_out == n else True
+
+
+def test_config5_sized_alignment_parity(cuda_device):
+    """Config-5 shape: 64^3, L=20, four marching bands 4-8-16-20, 24 starts, 60-blob
+    template, SNR 0.05, shifts +-4, wedge 60; one particle, GPU vs oracle align()."""
+    n, L = 64, 20
+    tmpl_d = api.make_template(n, 60, 20250905)
+    parts, q, sh = api.make_particles(tmpl_d, 1, 5000, 4, 0.05, 60.0)
+    ctx = api.Context(n, L, L * math.pi)
+    ctx.set_template(tmpl_d, 60.0)
+    cfg = api.make_config(bands=(4, 8, 16, 20), max_candidates=24, shift_radius=4, shift_step=2)
+    got = ctx.align_batch(parts, cfg)
+    ocfg = bmo.make_config(l_max=L, lambda_cut=L * math.pi, bands=(4, 8, 16, 20), max_candidates=24,
+                           shift_radius=4, shift_step=2)
+    tmpl = tmpl_d.cpu().numpy().astype(np.float64)
+    ref = bmo.align(tmpl, parts[0].cpu().numpy().astype(np.float64), ocfg, wedge_deg=60.0)
+    assert got[0]["shift"] == ref["shift"]
+    assert bmo.geodesic_degrees(got[0]["quat"], ref["quat"]) < 0.5
+    assert got[0]["score"] == pytest.approx(ref["score"], rel=1e-4)
+    assert got[0]["bands"] == [4, 8, 16, 20]
+
+
+def test_align_batch_edge_counts(cuda_device):
+    """An empty batch returns nothing; batches smaller than the lane split (1, 3
+    particles with 4 lanes) give the same results as one lane."""
+    n, L = 32, 8
+    tmpl = api.make_template(n, 20, 9)
+    parts, _, _ = api.make_particles(tmpl, 3, 4242, 2, 0.5, 60.0)
+    cfg = api.make_config(bands=(4, 8), max_candidates=8, shift_radius=2, shift_step=2)
+    ctx = api.Context(n, L, L * math.pi)
+    ctx.set_template(tmpl, 60.0)
+    assert ctx.align_batch(parts[:0], cfg) == []
+    ctx.set_lanes(4, 1)
+    many = ctx.align_batch(parts, cfg)
+    one = ctx.align_batch(parts[:1], cfg)
+    ctx.set_lanes(1)
+    ref = ctx.align_batch(parts, cfg)
+    assert len(many) == 3 and len(one) == 1
+    for a, b in zip(many, ref):
+        assert a["shift"] == b["shift"] and list(a["quat"]) == list(b["quat"]) and a["score"] == b["score"]
+    assert one[0]["shift"] == ref[0]["shift"] and one[0]["score"] == ref[0]["score"]
