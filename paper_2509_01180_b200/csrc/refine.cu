@@ -816,7 +816,12 @@ __device__ void objective(const double* cr, const double* rr, bool wedge, int or
 }
 
 // damped step from wk.f with wk.lam, trial chart rotation (optimize.cpp:313-328)
-__device__ void make_trial(CandWork& wk) {
+// The trial's order-0 evaluation needs only the objective VALUE, which is smooth
+// through the gimbal pole: an anchored candidate is evaluated at the global trial
+// rotation h_try * a on the window kernel (C~(h) = C(h a), xcorr.cpp:149-155)
+// instead of streaming its private chart kernels; et holds those angles.
+__device__ __forceinline__ Quat qload(const double* q);
+__device__ void make_trial(CandWork& wk, const CandState& st) {
     double m[9];
     for (int i = 0; i < 9; ++i) m[i] = wk.f[4 + i];
     m[0] -= wk.lam;
@@ -840,7 +845,7 @@ __device__ void make_trial(CandWork& wk) {
     }
     const Quat h = q_from_euler(wk.e[0] + p[0], wk.e[1] + p[1], wk.e[2] + p[2]);
     wk.gt[0] = h.w, wk.gt[1] = h.x, wk.gt[2] = h.y, wk.gt[3] = h.z;
-    const Euler3 et = q_euler(h);
+    const Euler3 et = q_euler(st.anchored ? q_mul(h, qload(st.anchor)) : h);
     wk.et[0] = et.a, wk.et[1] = et.b, wk.et[2] = et.g;
 }
 
@@ -1051,8 +1056,7 @@ __global__ void __launch_bounds__(EvalShape<K>::WARPS * 32, BMB_EVAL_MINB(ORDER)
         idx[k] = q0 + k < n ? i : -1;
         const CandWork& wk = a.work[i];
         const int w = i / a.max_cand;
-        const bool fin = wk.status == ST_FINAL;
-        const bool chart = !fin && a.cand[i].anchored;
+        const bool chart = wk.status == ST_EVAL2 && a.cand[i].anchored;  // order 0: global angles
         job[k].xi = chart ? a.xi_pool + (size_t)wk.slot * len : a.xi_win + (size_t)w * len;
         job[k].wx = !wedge ? nullptr : (chart ? a.w_pool + (size_t)wk.slot * len : a.T.wedge);
         const double* e = wk.status == ST_EVAL2 ? wk.e : wk.et;
@@ -1094,7 +1098,7 @@ __device__ __forceinline__ bool step_one(const StageArgs& a, long long i) {
     }
     wk.lam = wk.lambda;
     wk.retry = 0;
-    make_trial(wk);
+    make_trial(wk, st);
     wk.status = ST_EVAL0;
     return true;
 }
@@ -1136,7 +1140,7 @@ __device__ __forceinline__ bool accept_one(const StageArgs& a, long long i) {
         wk.status = ST_DONE;
         return false;
     }
-    make_trial(wk);
+    make_trial(wk, st);
     return true;
 }
 
@@ -1307,7 +1311,7 @@ template <bool WEDGE>
 __device__ __forceinline__ EvalJob fused_job(const StageArgs& a, const FusedArgs& fa, const float4* sxi, int w, int c) {
     const long long i = (long long)w * a.max_cand + c;
     const CandWork& wk = a.work[i];
-    const bool chart = wk.status != ST_FINAL && a.cand[i].anchored;
+    const bool chart = wk.status == ST_EVAL2 && a.cand[i].anchored;  // order 0: global angles
     const size_t slot = (size_t)blockIdx.x * a.max_cand + c;
     EvalJob j;
     j.xi = chart ? fa.xi_pool + slot * fa.slot_len : sxi;
