@@ -949,7 +949,10 @@ __global__ void iter_begin_kernel(StageArgs a, const int* start, const int* star
 // one CTA per candidate of the composition list; SMEM: the temporaries live in
 // shared memory (known address space -> LDS/STS), else in global scratch
 template <bool SMEM>
-__global__ void __launch_bounds__(256) compose_kernel(StageArgs a) {
+#ifndef BMB_COMPOSE_THREADS
+#define BMB_COMPOSE_THREADS 256
+#endif
+__global__ void __launch_bounds__(BMB_COMPOSE_THREADS) compose_kernel(StageArgs a) {
     extern __shared__ __align__(16) unsigned char sm[];
     __shared__ ComposeScratch cs;
     __shared__ int s_slot;
@@ -1562,9 +1565,9 @@ void launch_compose(const StageArgs& a, int n, cudaStream_t s) {
     const size_t smem = a.compose_smem ? compose_smem_bytes(a.T.L) : 0;
     if (smem) {
         ensure_dynamic_smem(compose_kernel<true>, (int)smem);
-        compose_kernel<true><<<n, 256, smem, s>>>(a);
+        compose_kernel<true><<<n, BMB_COMPOSE_THREADS, smem, s>>>(a);
     } else {
-        compose_kernel<false><<<n, 256, 0, s>>>(a);
+        compose_kernel<false><<<n, BMB_COMPOSE_THREADS, 0, s>>>(a);
     }
 }
 // jobs per warp in the refinement: 1 (measured fastest; K-way over runs of
