@@ -145,9 +145,12 @@ int bm_set_template(bm_context* ctx, const float* tmpl, double wedge_theta_deg, 
 /* template norm ||t_hat|| */
 double bm_template_norm(const bm_context* ctx);
 
-/* align() for `count` particles (device float32, count x n^3): wedge filter,
- * coarse + fine shift windows, seeding, device Newton with frequency marching.
- * Results to host memory; synchronizes the context stream. */
+/* align() for `count` particles (float32, count x n^3, device OR host memory):
+ * wedge filter, coarse + fine shift windows, seeding, device Newton with
+ * frequency marching.  Host particles (pinned for overlap) are staged by each
+ * concurrent lane on its own stream right before it aligns its slice; the
+ * staged copy also serves a following bm_average_accumulate of the same host
+ * buffer.  Results to host memory; synchronizes the context stream. */
 int bm_align_batch(bm_context* ctx, const float* particles, int count, const bm_align_config* cfg,
                    bm_align_result* out, void* stream);
 
@@ -178,6 +181,7 @@ int bm_apply_wedge_taper(bm_context* ctx, const float* in, float* out, int count
  * the particle count (after the cross-device allreduce) gives the average. */
 int bm_average_accumulate(bm_context* ctx, const float* particles, int count,
                           const bm_align_result* results, double* sum, void* stream);
+/* (particles: device or host memory, as for bm_align_batch) */
 
 /* Voxel synthesis of a coefficient set (synthesize, src/basis.cpp:332-419,
  * with its Catmull-Rom radial table, basis.cpp:221-245): coeffs device

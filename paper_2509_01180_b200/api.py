@@ -166,7 +166,20 @@ class Context:
         return v.to(device=f"cuda:{self.device}", dtype=torch.float32).contiguous()
 
     def _stream(self, t):
-        return C.c_void_p(_torch().cuda.current_stream(t.device).cuda_stream)
+        dev = t.device if t.device.type == "cuda" else _torch().device(f"cuda:{self.device}")
+        return C.c_void_p(_torch().cuda.current_stream(dev).cuda_stream)
+
+    def _particles(self, vols):
+        """float32 particle batch for bm_align_batch / bm_average_accumulate: CPU
+        tensors (pinned for overlap) and arrays stay in host memory, the library
+        stages them per lane; anything else goes to the context's device."""
+        torch = _torch()
+        v = vols if isinstance(vols, torch.Tensor) else torch.as_tensor(np.asarray(vols))
+        if v.dim() == 3:
+            v = v.unsqueeze(0)
+        if v.device.type == "cpu":
+            return v.to(dtype=torch.float32).contiguous()
+        return v.to(device=f"cuda:{self.device}", dtype=torch.float32).contiguous()
 
     def set_template(self, tmpl, wedge_theta_deg: float = 0.0):
         """Template state of align() (src/optimize.cpp:438-454)."""
@@ -177,8 +190,9 @@ class Context:
         self.wedge_theta_deg = wedge_theta_deg
 
     def align_batch(self, particles, cfg: _lib.AlignConfig):
-        """align() for every particle of the batch; list of dicts (AlignmentResult)."""
-        v = self._dev(particles)
+        """align() for every particle of the batch (device or host tensor); list of
+        dicts (AlignmentResult)."""
+        v = self._particles(particles)
         count = v.shape[0]
         out = (_lib.AlignResult * max(count, 1))()
         _lib.check(_lib.lib().bm_align_batch(self._h, C.c_void_p(v.data_ptr()), count,
@@ -193,10 +207,10 @@ class Context:
         """Coefficient-space average numerator: out (complex128, coeff_count, device) +=
         sum_p rotate_expansion(f_hat_{p,s_p}, g_p^-1)."""
         torch = _torch()
-        v = self._dev(particles)
+        v = self._particles(particles)
         count = v.shape[0]
         if out is None:
-            out = torch.zeros((self.coeff_count, 2), dtype=torch.float64, device=v.device)
+            out = torch.zeros((self.coeff_count, 2), dtype=torch.float64, device=f"cuda:{self.device}")
         res = (_lib.AlignResult * max(count, 1))()
         for i, r in enumerate(results):
             for j in range(3):

@@ -594,11 +594,50 @@ bool better(const WindowOutcome& a, const WindowOutcome& b) {
 }
 }  // namespace
 
+namespace {
+bool host_pointer(const void* p) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();  // unregistered host memory on older drivers
+        return true;
+    }
+    return at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeUnregistered;
+}
+}  // namespace
+
+const float* Context::device_particles(const float* particles, int count) {
+    if (count <= 0 || !host_pointer(particles)) return particles;
+    const size_t bytes = sizeof(float) * (size_t)n * n * n * count;
+    if (particles != staged_src_ || count != staged_count_) {
+        staged_.reserve(bytes);
+        ck(cudaMemcpyAsync(staged_.p, particles, bytes, cudaMemcpyHostToDevice, stream), "stage particles");
+        staged_src_ = particles;
+        staged_count_ = count;
+    }
+    return staged_.as<float>();
+}
+
 std::vector<ParticleResult> Context::align_batch(const float* particles, int count, const AlignConfig& cfg) {
     if (!has_template) throw std::invalid_argument("align: set_template first");
     cfg.validate(basis.l_max);
     const int k = std::max(1, std::min(lanes, count / std::max(1, lane_min_particles)));
-    if (k <= 1) return align_batch_lane(particles, count, cfg);
+    const bool host = count > 0 && host_pointer(particles);
+    float* stage = nullptr;
+    if (host) {
+        staged_.reserve(sizeof(float) * (size_t)n * n * n * count);
+        stage = staged_.as<float>();
+        staged_src_ = particles;
+        staged_count_ = count;
+    }
+    // slice [o, o + c) of the batch on the device: staged on stream s when host-resident
+    auto slice = [&](int o, int c, cudaStream_t s) -> const float* {
+        const long long vs = (long long)n * n * n;
+        if (!host) return particles + o * vs;
+        ck(cudaMemcpyAsync(stage + o * vs, particles + o * vs, sizeof(float) * vs * c, cudaMemcpyHostToDevice, s),
+           "stage particles");
+        return stage + o * vs;
+    };
+    if (k <= 1) return align_batch_lane(slice(0, count, stream), count, cfg);
     ensure_lanes();
     // the lanes start after the work already queued on this context's stream
     cudaEvent_t ready;
@@ -610,6 +649,24 @@ std::vector<ParticleResult> Context::align_batch(const float* particles, int cou
     std::vector<std::vector<ParticleResult>> part(k);
     std::vector<std::exception_ptr> err(k);
     std::vector<std::thread> threads;
+    // host particles: stage the slices in lane order, each copy after the previous
+    // one, so lane 0 starts computing after its own slice instead of after all
+    std::vector<const float*> dev_slice(k);
+    if (host) {
+        cudaEvent_t prev = ready;
+        std::vector<cudaEvent_t> done(k);
+        for (int i = 0; i < k; ++i) {
+            cudaStream_t s = i == 0 ? stream : lane_ctx_[i - 1]->stream;
+            ck(cudaStreamWaitEvent(s, prev, 0), "stage order");
+            dev_slice[i] = slice(off[i], off[i + 1] - off[i], s);
+            ck(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming), "stage event");
+            ck(cudaEventRecord(done[i], s), "stage event");
+            prev = done[i];
+        }
+        for (auto& e : done) cudaEventDestroy(e);  // released once their work completes
+    } else {
+        for (int i = 0; i < k; ++i) dev_slice[i] = particles + off[i] * vstride;
+    }
     for (int i = 1; i < k; ++i)
         threads.emplace_back([&, i] {
             try {
@@ -617,13 +674,13 @@ std::vector<ParticleResult> Context::align_batch(const float* particles, int cou
                 ck(cudaSetDevice(device), "lane device");
                 ck(cudaStreamWaitEvent(c.stream, ready, 0), "lane wait");
                 c.timer.on = timer.on;
-                part[i] = c.align_batch_lane(particles + off[i] * vstride, off[i + 1] - off[i], cfg);
+                part[i] = c.align_batch_lane(dev_slice[i], off[i + 1] - off[i], cfg);
             } catch (...) {
                 err[i] = std::current_exception();
             }
         });
     try {
-        part[0] = align_batch_lane(particles, off[1], cfg);
+        part[0] = align_batch_lane(dev_slice[0], off[1], cfg);
     } catch (...) {
         err[0] = std::current_exception();
     }

@@ -323,6 +323,7 @@ int bm_average_accumulate(bm_context* ctx, const float* particles, int count,
         cudaSetDevice(c.device);
         StreamJoin join(ctx, stream);
         const long long vstride = (long long)c.n * c.n * c.n;
+        particles = c.device_particles(particles, count);  // host buffers: the staged copy
         const float* fw = particles;
         if (c.wedge) {
             c.filtered.reserve(sizeof(float) * vstride * count);

@@ -218,7 +218,14 @@ public:
     std::vector<WindowOutcome> run_windows(const float* vols, int n_vol, const std::vector<int>& wvol,
                                            const std::vector<int>& wshift, const AlignConfig& cfg);
     // align() for a batch of particles (coarse + fine shift stages)
+    // particles: device or host memory (host: each lane stages its own slice on
+    // its stream right before aligning it, so the copies overlap other lanes'
+    // work; the staged copy serves a following average of the same buffer)
     std::vector<ParticleResult> align_batch(const float* particles, int count, const AlignConfig& cfg);
+    const float* device_particles(const float* particles, int count);  // staged copy of host particles
+    DevBuf staged_;
+    const float* staged_src_ = nullptr;
+    int staged_count_ = 0;
     std::vector<ParticleResult> align_batch_lane(const float* particles, int count, const AlignConfig& cfg);
     // concurrent lanes: sub-contexts with their own stream and buffers that align
     // slices of a large batch from their own host threads (overlapping the
