@@ -139,7 +139,7 @@ __device__ __forceinline__ float2 phase_of(const WarpScratch& w, int m, int mp) 
 // refinement order 2, bit 2: sweep): L1 prefetch of the next group's kernel
 // rows, and loads software-pipelined one chain step ahead
 #ifndef BMB_PF_MASK
-#define BMB_PF_MASK 3
+#define BMB_PF_MASK 2
 #endif
 #ifndef BMB_PIPE_MASK
 #define BMB_PIPE_MASK 0
@@ -1034,9 +1034,13 @@ __device__ __forceinline__ void eval_group(const BandTables& T, const EvalJob (&
 // K listed candidates per warp
 // resident CTAs per SM the evaluation kernels are compiled for (register cap):
 // measured best 4 at order 2 (80 registers, small spills) and 3 at order 0
-#ifndef BMB_EVAL_MINB
-#define BMB_EVAL_MINB(order) ((order) == 2 ? 4 : 3)
+#ifndef BMB_EVAL_MINB0
+#define BMB_EVAL_MINB0 3
 #endif
+#ifndef BMB_EVAL_MINB2
+#define BMB_EVAL_MINB2 4
+#endif
+#define BMB_EVAL_MINB(order) ((order) == 2 ? BMB_EVAL_MINB2 : BMB_EVAL_MINB0)
 template <int ORDER, int K>
 __global__ void __launch_bounds__(EvalShape<K>::WARPS * 32, BMB_EVAL_MINB(ORDER)) eval_kernel(StageArgs a, const int* list,
                                                                                        const int* count) {
