@@ -991,9 +991,12 @@ __global__ void __launch_bounds__(BMB_COMPOSE_THREADS) compose_kernel(StageArgs 
 }
 
 // warps per CTA of the evaluation kernels (K scratch sets per warp in static smem)
+#ifndef BMB_EVAL_WARPS1
+#define BMB_EVAL_WARPS1 8
+#endif
 template <int K>
 struct EvalShape {
-    static constexpr int WARPS = K >= 4 ? 4 : 8;
+    static constexpr int WARPS = K >= 4 ? 4 : (K == 1 ? BMB_EVAL_WARPS1 : 8);
 };
 
 // K jobs of one warp, evaluated as runs of jobs that share their kernels
