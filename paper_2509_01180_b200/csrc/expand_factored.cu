@@ -4,7 +4,7 @@
 //   1. trilinear samples f(r_i, theta_t, phi_p) of the shifted window
 //      (sample_trilinear + shift_volume, src/volume.cpp:19-67): base voxel and
 //      FP32 weights from a per-sample table (FP64 coordinates r * (h d_tp) + h,
-//      computed once on the host), FP32 taps, two samples' taps in flight per thread;
+//      computed once on the host), FP32 taps;
 //   2. unnormalized phi-DFT of every theta ring (dft_r2c_rows,
 //      src/detail/fftw_util.cpp:16-28), folded over p <-> n_phi - p, with each
 //      thread's order m fixed so its twiddle row lives in registers;
@@ -29,10 +29,6 @@ constexpr int kThreads = 256;
 #define BMB_EXPAND_RC 4
 #endif
 constexpr int kRC = BMB_EXPAND_RC;  // radii sampled per pass (lanes run along the ray: adjacent radii share cache lines)
-#ifndef BMB_EXPAND_U
-#define BMB_EXPAND_U 1
-#endif
-constexpr int kU = BMB_EXPAND_U;    // samples whose taps are in flight per thread
 
 struct Smem {
     size_t samp, F, G, rad, rowpack, total;
@@ -100,58 +96,32 @@ __global__ void __launch_bounds__(kThreads, BMB_EXPAND_MINB) expand_factored_ker
             //    0 < g < n, so truncation = floor.  Item = (ray, radius), radius fastest.
             const int nrc = min(kRC, T.nr - ir);
             const int items = nsamp * kRC;
-            for (int it0 = tid; it0 < items; it0 += kU * kThreads) {
-                float val[kU];
-                float4 tap[kU][2];  // (v0, v1) of the 4 (y, z) rows of each sample
-                float wx[kU], wy[kU], wz[kU];
-                int dst[kU];
+            for (int it = tid; it < items; it += kThreads) {
+                const int s = it / kRC, j = it - s * kRC;
+                if (j >= nrc) continue;
+                const int4 e = __ldg(T.samp + (size_t)s * T.nr + ir + j);
+                const int x0 = e.x & 1023, y0 = (e.x >> 10) & 1023, z0 = (e.x >> 20) & 1023;
+                const float fx = __int_as_float(e.y), fy = __int_as_float(e.z), fz = __int_as_float(e.w);
+                const int xs0 = x0 + sx, ys0 = y0 + sy, zs0 = z0 + sz;
+                const bool vx0 = (unsigned)x0 < (unsigned)n && (unsigned)xs0 < (unsigned)n;
+                const bool vx1 = (unsigned)(x0 + 1) < (unsigned)n && (unsigned)(xs0 + 1) < (unsigned)n;
+                const bool vy0 = (unsigned)y0 < (unsigned)n && (unsigned)ys0 < (unsigned)n;
+                const bool vy1 = (unsigned)(y0 + 1) < (unsigned)n && (unsigned)(ys0 + 1) < (unsigned)n;
+                const bool vz0 = (unsigned)z0 < (unsigned)n && (unsigned)zs0 < (unsigned)n;
+                const bool vz1 = (unsigned)(z0 + 1) < (unsigned)n && (unsigned)(zs0 + 1) < (unsigned)n;
+                const long long o0 = ((long long)zs0 * n + ys0) * n + xs0;
+                float val = 0.0f;
 #pragma unroll
-                for (int u = 0; u < kU; ++u) {
-                    val[u] = 0.0f;
-                    const int it = it0 + u * kThreads;
-                    const int s = it / kRC, j = it - s * kRC;
-                    dst[u] = (it < items && j < nrc) ? j * nsamp + s : -1;
-                    tap[u][0] = tap[u][1] = make_float4(0.f, 0.f, 0.f, 0.f);
-                    wx[u] = wy[u] = wz[u] = 0.0f;
-                    if (dst[u] < 0) continue;
-                    const int4 e = __ldg(T.samp + (size_t)s * T.nr + ir + j);
-                    const int x0 = e.x & 1023, y0 = (e.x >> 10) & 1023, z0 = (e.x >> 20) & 1023;
-                    wx[u] = __int_as_float(e.y), wy[u] = __int_as_float(e.z), wz[u] = __int_as_float(e.w);
-                    const int xs0 = x0 + sx, ys0 = y0 + sy, zs0 = z0 + sz;
-                    const bool vx0 = (unsigned)x0 < (unsigned)n && (unsigned)xs0 < (unsigned)n;
-                    const bool vx1 = (unsigned)(x0 + 1) < (unsigned)n && (unsigned)(xs0 + 1) < (unsigned)n;
-                    const bool vy0 = (unsigned)y0 < (unsigned)n && (unsigned)ys0 < (unsigned)n;
-                    const bool vy1 = (unsigned)(y0 + 1) < (unsigned)n && (unsigned)(ys0 + 1) < (unsigned)n;
-                    const bool vz0 = (unsigned)z0 < (unsigned)n && (unsigned)zs0 < (unsigned)n;
-                    const bool vz1 = (unsigned)(z0 + 1) < (unsigned)n && (unsigned)(zs0 + 1) < (unsigned)n;
-                    const long long o0 = ((long long)zs0 * n + ys0) * n + xs0;
-                    float t8[8];
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) {  // (y, z) rows of the footprint
-                        const int b = c & 1, a = c >> 1;
-                        const bool vr = (b ? vy1 : vy0) && (a ? vz1 : vz0);
-                        const float* row = v + o0 + (b ? n : 0) + (a ? (long long)n * n : 0);
-                        t8[2 * c] = (vr && vx0) ? __ldg(row) : 0.0f;
-                        t8[2 * c + 1] = (vr && vx1) ? __ldg(row + 1) : 0.0f;
-                    }
-                    tap[u][0] = make_float4(t8[0], t8[1], t8[2], t8[3]);
-                    tap[u][1] = make_float4(t8[4], t8[5], t8[6], t8[7]);
+                for (int c = 0; c < 4; ++c) {  // (y, z) rows of the footprint
+                    const int bb = c & 1, aa = c >> 1;
+                    const bool vr = (bb ? vy1 : vy0) && (aa ? vz1 : vz0);
+                    const float* row = v + o0 + (bb ? n : 0) + (aa ? (long long)n * n : 0);
+                    const float v0 = (vr && vx0) ? __ldg(row) : 0.0f;
+                    const float v1 = (vr && vx1) ? __ldg(row + 1) : 0.0f;
+                    const float wyz = (bb ? fy : 1.0f - fy) * (aa ? fz : 1.0f - fz);
+                    val = fmaf(wyz, fmaf(fx, v1 - v0, v0), val);
                 }
-#pragma unroll
-                for (int u = 0; u < kU; ++u) {
-                    if (dst[u] < 0) continue;
-                    const float t8[8] = {tap[u][0].x, tap[u][0].y, tap[u][0].z, tap[u][0].w,
-                                         tap[u][1].x, tap[u][1].y, tap[u][1].z, tap[u][1].w};
-                    const float fx = wx[u], fy = wy[u], fz = wz[u];
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        const int b = c & 1, a = c >> 1;
-                        const float v0 = t8[2 * c], v1 = t8[2 * c + 1];
-                        const float wyz = (b ? fy : 1.0f - fy) * (a ? fz : 1.0f - fz);
-                        val[u] = fmaf(wyz, fmaf(fx, v1 - v0, v0), val[u]);
-                    }
-                    samp[dst[u]] = val[u];
-                }
+                samp[j * nsamp + s] = val;
             }
         }
         // radial slice of this radius (read after the barriers below)
