@@ -268,7 +268,11 @@ public:
     // evaluations (order 2, order 0) and their algorithmic FLOPs since the last reset
     void read_eval_stats(long long* evals, double* flops, bool reset);
     void eval_counts(int L, long long* out);  // (order 2, order 0) evaluations at band L
-    size_t pool_budget_ = 24ull << 30;      // bytes for window kernels + anchored-chart pool per chunk
+    // bytes for window kernels + anchored-chart pool per chunk (BMB_POOL_GB overrides)
+    size_t pool_budget_ = [] {
+        const char* e = std::getenv("BMB_POOL_GB");
+        return (e && std::atoi(e) > 0) ? (size_t)std::atoi(e) << 30 : 24ull << 30;
+    }();
 
 private:
     void refine_windows(int nw, int maxc, const AlignConfig& cfg, const Quat& koff, long long grid_evals);
