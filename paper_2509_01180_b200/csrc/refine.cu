@@ -1535,6 +1535,24 @@ __global__ void build_xi_kernel(XiArgs a) {
         out[e] = xi_entry(a.T, a.row_group, f, t, a.block_off, a.radial_count, e >> 5, e & 31);
 }
 
+// one CTA per coefficient set: its rows (and the template's) staged in shared
+// memory, entries computed from there
+__global__ void __launch_bounds__(256) build_xi_staged_kernel(XiArgs a) {
+    extern __shared__ __align__(16) float xs[];
+    float* fs = xs;
+    float* ts = xs + ((a.nf + 3) & ~3);
+    const float* f = a.f + (long long)blockIdx.x * a.ldf;
+    const float* t = a.t + (long long)blockIdx.x * a.ldt;
+    for (int i = threadIdx.x; i < a.nf; i += blockDim.x) {
+        fs[i] = f[i];
+        ts[i] = t[i];
+    }
+    __syncthreads();
+    float4* out = a.out + (size_t)blockIdx.x * a.T.rows * 32;
+    for (int e = threadIdx.x; e < a.T.rows * 32; e += blockDim.x)
+        out[e] = xi_entry(a.T, a.row_group, fs, ts, a.block_off, a.radial_count, e >> 5, e & 31);
+}
+
 }  // namespace
 
 long long compose_scratch_floats(int L) { return compose_layout(L).total; }
@@ -1687,6 +1705,12 @@ int launch_eval_sweep(const EvalArgs& a, cudaStream_t s) {
 
 int launch_build_xi(const XiArgs& a, cudaStream_t s) {
     if (a.n <= 0) return 0;
+    const size_t smem = sizeof(float) * 2 * (size_t)((a.nf + 3) & ~3);
+    if (a.nf > 0 && smem <= 200 * 1024) {
+        ensure_dynamic_smem(build_xi_staged_kernel, (int)smem);
+        build_xi_staged_kernel<<<a.n, 256, smem, s>>>(a);
+        return cudaGetLastError() == cudaSuccess ? 0 : 2;
+    }
     dim3 grid((a.T.rows * 32 + 255) / 256, a.n);
     build_xi_kernel<<<grid, 256, 0, s>>>(a);
     return cudaGetLastError() == cudaSuccess ? 0 : 2;

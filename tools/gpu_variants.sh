@@ -9,5 +9,5 @@ for n in ${VARIANTS:-base}; do
     env:*) pre="${n#env:}" ;;
     *) pre="BMB_LIB=build/variants/$n.so" ;;
   esac
-  env $pre timeout 300 python tools/profile_kernels.py 512 1 2>&1 | grep -v arn | head -7 >> gpurun_out/variants.log
+  env $pre timeout 300 python tools/profile_kernels.py 512 1 2>&1 | grep -v arn | head -12 >> gpurun_out/variants.log
 done
