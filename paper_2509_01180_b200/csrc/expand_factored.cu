@@ -17,6 +17,12 @@
 // (DESIGN.md §3 K2f): 16 S + 4 n_phi n_r n_theta (L+1) + 4 n_r tri(L) n_theta +
 // 2 n_r C FLOP, S = n_r n_theta n_phi — 4.47 MFLOP at config 2, about 120x fewer
 // than the dense 2 C V of the pulled-back operator.
+#include <cmath>
+#include <cstdlib>
+#include <mutex>
+#include <set>
+#include <vector>
+
 #include "smem_attr.hpp"
 #include "expand_factored.hpp"
 
@@ -53,12 +59,71 @@ __host__ __device__ inline Smem smem_plan(const FactoredTables& T) {
     return s;
 }
 
+// phi-DFT twiddles of the common n_phi (= 2L + 2 for L = 8 / 16 / 20 / 24) as
+// compile-time constants: the FFMAs take them as immediates, no table loads
+// compile-time twiddles (Taylor series in double, |x| <= pi): FFMA immediates
+constexpr double ct_sin(double x) {
+    double term = x, sum = x;
+    for (int n = 1; n < 40; ++n) {
+        term *= -x * x / ((2.0 * n) * (2.0 * n + 1.0));
+        sum += term;
+    }
+    return sum;
+}
+constexpr double ct_cos(double x) {
+    double term = 1.0, sum = 1.0;
+    for (int n = 1; n < 40; ++n) {
+        term *= -x * x / ((2.0 * n - 1.0) * (2.0 * n));
+        sum += term;
+    }
+    return sum;
+}
+template <int NP>
+struct DftTab {
+    float c[NP / 2][NP / 2] = {};
+    float s[NP / 2][NP / 2] = {};
+    constexpr DftTab() {
+        for (int m = 0; m < NP / 2; ++m)
+            for (int p = 0; p < NP / 2; ++p) {
+                const long long a = ((long long)m * p) % NP;
+                double x = 2.0 * 3.14159265358979323846 * (double)a / NP;
+                if (x > 3.14159265358979323846) x -= 2.0 * 3.14159265358979323846;
+                c[m][p] = (float)ct_cos(x);
+                s[m][p] = (float)-ct_sin(x);
+            }
+    }
+};
+template <int NP, int MH>
+__device__ __forceinline__ void dft_ring(const float* f, float2* Frow) {
+    constexpr int H = NP / 2;
+    constexpr DftTab<NP> tab{};
+    float a[H], b[H];
+#pragma unroll
+    for (int p = 1; p < H; ++p) {
+        const float x = f[p], y = f[NP - p];
+        a[p] = x + y;
+        b[p] = x - y;
+    }
+    const float f0 = f[0], fh = f[H];
+#pragma unroll
+    for (int m = 0; m < MH; ++m) {
+        float re = f0 + ((m & 1) ? -fh : fh);
+        float im = 0.0f;
+#pragma unroll
+        for (int p = 1; p < H; ++p) {
+            re = fmaf(a[p], tab.c[m][p], re);
+            im = fmaf(b[p], tab.s[m][p], im);
+        }
+        Frow[m] = make_float2(re, im);
+    }
+}
+
 // HALF: compile-time bound on n_phi / 2 (twiddles in registers); RPT: bound on
 // the real-packed rows per thread (accumulators in registers)
 #ifndef BMB_EXPAND_MINB
 #define BMB_EXPAND_MINB 3
 #endif
-template <int HALF, int RPT>
+template <int HALF, int RPT, int NPC>
 __global__ void __launch_bounds__(kThreads, BMB_EXPAND_MINB) expand_factored_kernel(FactoredTables T, const float* __restrict__ vols,
                                                                     long long vol_stride, const int* __restrict__ win_vol,
                                                                     const int* __restrict__ win_shift, float* __restrict__ out,
@@ -128,7 +193,9 @@ __global__ void __launch_bounds__(kThreads, BMB_EXPAND_MINB) expand_factored_ker
         for (int i = tid; i < T.pairs; i += kThreads) rad[i] = T.radial_t[(size_t)ir * T.pairs + i];
         __syncthreads();
         // 2. phi-DFT: F[t][m] = sum_p f[t][p] e^{-2 pi i m p / n_phi}, folded
-        if (dtg < TG) {
+        if constexpr (NPC > 0) {  // one ring per thread, all orders
+            for (int t = tid; t < nt; t += kThreads) dft_ring<NPC, NPC / 2>(samp + rc * nsamp + t * np, F + t * nl);
+        } else if (dtg < TG) {
             for (int t = dtg; t < nt; t += TG) {
                 const float* f = samp + rc * nsamp + t * np;
                 float re = f[0] + ((dm & 1) ? -f[half] : f[half]);
@@ -186,11 +253,12 @@ __global__ void __launch_bounds__(kThreads, BMB_EXPAND_MINB) expand_factored_ker
     }
 }
 
-template <int HALF, int RPT>
+template <int HALF, int RPT, int NPC = 0>
 int launch_t(const FactoredTables& T, size_t smem, const float* vols, long long vol_stride, const int* win_vol,
              const int* win_shift, int n_win, float* out, int ldo, cudaStream_t s) {
-    ensure_dynamic_smem(expand_factored_kernel<HALF, RPT>, (int)smem);
-    expand_factored_kernel<HALF, RPT><<<n_win, kThreads, smem, s>>>(T, vols, vol_stride, win_vol, win_shift, out, ldo);
+    ensure_dynamic_smem(expand_factored_kernel<HALF, RPT, NPC>, (int)smem);
+    expand_factored_kernel<HALF, RPT, NPC><<<n_win, kThreads, smem, s>>>(T, vols, vol_stride, win_vol, win_shift, out,
+                                                                         ldo);
     return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }
 
@@ -205,6 +273,16 @@ int launch_expand_factored(const FactoredTables& T, const float* vols, long long
     if (smem > 220 * 1024) return 1;
     const int half = T.np / 2, rpt = (T.coeffs + kThreads - 1) / kThreads;
     if (T.L + 1 > kThreads) return 1;
+    static const bool cdft = [] {
+        const char* e = std::getenv("BMB_EXPAND_CDFT");
+        return !(e && std::atoi(e) == 0);
+    }();
+    if (cdft && T.L + 1 == T.np / 2) {  // n_phi = 2L + 2 with compile-time twiddles
+        if (T.np == 18 && rpt <= 4) return launch_t<9, 4, 18>(T, smem, vols, vol_stride, win_vol, win_shift, n_win, out, ldo, s);
+        if (T.np == 34 && rpt <= 12) return launch_t<17, 12, 34>(T, smem, vols, vol_stride, win_vol, win_shift, n_win, out, ldo, s);
+        if (T.np == 42 && rpt <= 24) return launch_t<21, 24, 42>(T, smem, vols, vol_stride, win_vol, win_shift, n_win, out, ldo, s);
+        if (T.np == 50 && rpt <= 40) return launch_t<25, 40, 50>(T, smem, vols, vol_stride, win_vol, win_shift, n_win, out, ldo, s);
+    }
     if (half <= 9 && rpt <= 4) return launch_t<9, 4>(T, smem, vols, vol_stride, win_vol, win_shift, n_win, out, ldo, s);
     if (half <= 17 && rpt <= 12) return launch_t<17, 12>(T, smem, vols, vol_stride, win_vol, win_shift, n_win, out, ldo, s);
     if (half <= 21 && rpt <= 24) return launch_t<21, 24>(T, smem, vols, vol_stride, win_vol, win_shift, n_win, out, ldo, s);
