@@ -121,7 +121,7 @@ __device__ __forceinline__ void dft_ring(const float* f, float2* Frow) {
 // HALF: compile-time bound on n_phi / 2 (twiddles in registers); RPT: bound on
 // the real-packed rows per thread (accumulators in registers)
 #ifndef BMB_EXPAND_MINB
-#define BMB_EXPAND_MINB 3
+#define BMB_EXPAND_MINB 4
 #endif
 template <int HALF, int RPT, int NPC>
 __global__ void __launch_bounds__(kThreads, BMB_EXPAND_MINB) expand_factored_kernel(FactoredTables T, const float* __restrict__ vols,
