@@ -67,6 +67,7 @@ BandTables BandDev::view() const {
     t.bexp = bexp.as<int>();
     t.PQR = PQR.as<float4>();
     t.item_of = item_of.as<int>();
+    t.out_pos = out_pos.as<int>();
     t.wedge = has_wedge ? wedge.as<float4>() : nullptr;
     return t;
 }
@@ -99,6 +100,7 @@ BandDev& Context::band(int L) {
     for (size_t i = 0; i < pqr.size(); ++i) pqr[i] = make_float4(h.P[i], h.Q[i], h.R[i], 0.0f);
     upload(b->PQR, pqr, stream);
     upload(b->item_of, h.item_of, stream);
+    upload(b->out_pos, h.out_pos, stream);
     std::vector<int> rg(h.rows);
     for (int g = 0; g < h.n_groups; ++g)
         for (int r = h.row_off[g]; r < h.row_off[g + 1]; ++r) rg[r] = g;

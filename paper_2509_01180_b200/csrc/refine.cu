@@ -600,12 +600,18 @@ __device__ void compose_block(const BandTables& T, const float4* src, const Stag
     // rows m >= 0 of xi'_l[m,n] = xi_l[m,n] e^{-i n g}: the A and B entries of
     // every (row, lane) (first index >= 0), and for m = 0 the conjugate mirror
     // xi_{0,-n} = (-1)^n conj(xi_{0,n})
+    // (the same pass zeroes the output positions no half-plane entry maps to:
+    // padding lanes, steps past an item's chain, B of self-paired items)
     for (int at = tid; at < T.rows * 32; at += nt) {
         const int row = at >> 5, j = at & 31;
         const int g = a.row_group[row];
         const int item = g * 32 + j;
         const int st = row - T.row_off[g];
-        if (st >= T.item_len[item]) continue;
+        if (st >= T.item_len[item]) {
+            out[at] = make_float4(0.f, 0.f, 0.f, 0.f);
+            continue;
+        }
+        if (T.item_w[item].y == 0.0f) reinterpret_cast<float2*>(out)[2 * at + 1] = make_float2(0.f, 0.f);
         const float4 x4 = src[at];
         const int l = T.item_mm[item].x + st, w = 2 * l + 1, o = xh_off(l);
 #pragma unroll
@@ -627,8 +633,8 @@ __device__ void compose_block(const BandTables& T, const float4* src, const Stag
     group_sync<WARP>();
     // q~_l[m'] = e^{-i m' a} sum_n d_{m'n} e^{-i n g} q_ln (rank-one wedge factor)
     if (wedge) {
+        int l = 0;  // idx increases: resume the degree scan
         for (int idx = tid; idx < (L + 1) * (L + 1); idx += nt) {
-            int l = 0;
             while ((l + 1) * (l + 1) <= idx) ++l;
             const int mp = idx - l * l - l;
             const int w = 2 * l + 1, o = xi_off(l);
@@ -652,22 +658,14 @@ __device__ void compose_block(const BandTables& T, const float4* src, const Stag
             qt[idx] = cmul(eam, make_float2(re, im));
         }
     }
-    // zero the layout positions no half-plane entry maps to (padding lanes, steps
-    // past an item's chain, B of self-paired items); the product writes the rest
-    for (int at = tid; at < T.rows * 32; at += nt) {
-        const int row = at >> 5, item = a.row_group[row] * 32 + (at & 31);
-        const int st = row - T.row_off[item >> 5];
-        if (st >= T.item_len[item]) out[at] = make_float4(0.f, 0.f, 0.f, 0.f);
-        else if (T.item_w[item].y == 0.0f) reinterpret_cast<float2*>(out)[2 * at + 1] = make_float2(0.f, 0.f);
-    }
     // xi~_l[m,m'] = e^{-i m' a} sum_n X_l[m,n] d^l_{m'n} over the half plane m >= 0,
     // one task per (l, m, quad of 4 consecutive m'): the X row is loaded once per n
     // for 4 outputs; results scatter to their (item, slot) of the band layout
     float2* outp = reinterpret_cast<float2*>(out);
     int total = 0;
     for (int l = 0; l <= L; ++l) total += (l + 1) * ((2 * l + 4) / 4);
+    int l = 0, base = 0;  // a thread's tasks increase: resume the degree scan
     for (int wi = tid; wi < total; wi += nt) {
-        int l = 0, base = 0;
         for (;; ++l) {
             const int nb = (l + 1) * ((2 * l + 4) / 4);
             if (wi < base + nb) break;
@@ -695,12 +693,9 @@ __device__ void compose_block(const BandTables& T, const float4* src, const Stag
         for (int j = 0; j < 4; ++j) {
             const int mp = q0 + j;
             if (mp > l || (m == 0 && mp < 0)) continue;
-            const int code = T.item_of[(m + L) * (2 * L + 1) + (mp + L)];
-            const int item = code >> 1, slot = code & 1;
-            const int at = (T.row_off[item >> 5] + (l - T.item_mm[item].x)) * 32 + (item & 31);
             float2 eam = cs.ua[abs(mp)];
             if (mp < 0) eam.y = -eam.y;
-            outp[2 * at + slot] = cmul(eam, acc[j]);
+            outp[T.out_pos[(m + L) * (2 * L + 1) + (mp + L)] + 64 * l] = cmul(eam, acc[j]);
         }
     }
     if (wedge) {

@@ -75,6 +75,7 @@ BandTablesHost build_band_tables(int L) {
     t.Q.assign((size_t)t.rows * 32, 0.0f);
     t.R.assign((size_t)t.rows * 32, 0.0f);
     t.item_of.assign((size_t)(2 * L + 1) * (2 * L + 1), -1);
+    t.out_pos.assign((size_t)(2 * L + 1) * (2 * L + 1), 0);
     for (int i = 0; i < t.n_items; ++i) {
         const It& it = items[i];
         const int g = i / 32, j = i % 32;
@@ -96,6 +97,11 @@ BandTablesHost build_band_tables(int L) {
         t.bexp[i] = a | (p << 8);
         t.item_of[(size_t)(m + L) * (2 * L + 1) + (mp + L)] = 2 * i;
         if (!self) t.item_of[(size_t)(pa + L) * (2 * L + 1) + (pb + L)] = 2 * i + 1;
+        {
+            const int p0 = 2 * ((t.row_off[g] - m) * 32 + j);
+            t.out_pos[(size_t)(m + L) * (2 * L + 1) + (mp + L)] = p0;
+            if (!self) t.out_pos[(size_t)(pa + L) * (2 * L + 1) + (pb + L)] = p0 + 1;
+        }
         for (int s = 1; s <= L - m; ++s) {
             const int l = m + s;
             const size_t at = (size_t)(t.row_off[g] + s) * 32 + j;

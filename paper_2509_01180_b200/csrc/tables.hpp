@@ -26,6 +26,7 @@ struct BandTablesHost {
     std::vector<int> bexp;
     std::vector<float> P, Q, R;
     std::vector<int> item_of;     // [(m+L)(2L+1) + m'+L]: 2 item + slot of half-plane entries, else -1
+    std::vector<int> out_pos;     // [(m+L)(2L+1) + m'+L]: 2 ((row_off[g] - m_item) 32 + lane) + slot; +64 l gives 2 at + slot
 };
 BandTablesHost build_band_tables(int L);
 
