@@ -68,6 +68,7 @@ BandTables BandDev::view() const {
     t.PQR = PQR.as<float4>();
     t.item_of = item_of.as<int>();
     t.out_pos = out_pos.as<int>();
+    t.at_desc = at_desc.as<int2>();
     t.wedge = has_wedge ? wedge.as<float4>() : nullptr;
     return t;
 }
@@ -101,6 +102,7 @@ BandDev& Context::band(int L) {
     upload(b->PQR, pqr, stream);
     upload(b->item_of, h.item_of, stream);
     upload(b->out_pos, h.out_pos, stream);
+    upload(b->at_desc, h.at_desc, stream);
     std::vector<int> rg(h.rows);
     for (int g = 0; g < h.n_groups; ++g)
         for (int r = h.row_off[g]; r < h.row_off[g + 1]; ++r) rg[r] = g;

@@ -63,7 +63,7 @@ struct WedgeFilter;
 struct BandDev {
     int L = 0;
     int n_items = 0, n_groups = 0, rows = 0;
-    DevBuf row_off, item_mm, item_pm, item_w, item_len, bfac, bexp, PQR, item_of, out_pos, row_group, wedge;
+    DevBuf row_off, item_mm, item_pm, item_w, item_len, bfac, bexp, PQR, item_of, out_pos, at_desc, row_group, wedge;
     bool has_wedge = false;
     BandTables view() const;
 };

@@ -30,6 +30,7 @@ struct BandTables {
     const float4* PQR = nullptr;     // [rows*32] (P, Q, R, 0): t1 = P cos b + Q,
                                      // t1' = -P sin b, t1'' = -P cos b, t2 = R
     const int* item_of = nullptr;    // [(2L+1)^2] 2 item + slot of each half-plane entry (m, m'), else -1
+    const int2* at_desc = nullptr;   // [rows*32] layout position descriptors (tables.hpp)
     const int* out_pos = nullptr;    // [(2L+1)^2] 2 ((row_off[g] - m_item) 32 + lane) + slot: + 64 l = 2 at + slot
     const float4* wedge = nullptr;   // [rows*32] wedge-power kernel entries (A, B) (or null)
 };

@@ -603,22 +603,20 @@ __device__ void compose_block(const BandTables& T, const float4* src, const Stag
     // (the same pass zeroes the output positions no half-plane entry maps to:
     // padding lanes, steps past an item's chain, B of self-paired items)
     for (int at = tid; at < T.rows * 32; at += nt) {
-        const int row = at >> 5, j = at & 31;
-        const int g = a.row_group[row];
-        const int item = g * 32 + j;
-        const int st = row - T.row_off[g];
-        if (st >= T.item_len[item]) {
+        const int2 dsc = T.at_desc[at];
+        if (!(dsc.x & 1)) {
             out[at] = make_float4(0.f, 0.f, 0.f, 0.f);
             continue;
         }
-        if (T.item_w[item].y == 0.0f) reinterpret_cast<float2*>(out)[2 * at + 1] = make_float2(0.f, 0.f);
+        const bool hasB = (dsc.x & 2) != 0;
+        if (!hasB) reinterpret_cast<float2*>(out)[2 * at + 1] = make_float2(0.f, 0.f);
         const float4 x4 = src[at];
-        const int l = T.item_mm[item].x + st, w = 2 * l + 1, o = xh_off(l);
+        const int l = (dsc.x >> 2) & 63, w = 2 * l + 1, o = xh_off(l);
 #pragma unroll
         for (int slot = 0; slot < 2; ++slot) {
-            if (slot == 1 && T.item_w[item].y == 0.0f) break;
-            const char2 e = slot ? T.item_pm[item] : T.item_mm[item];
-            const int m = e.x, mp = e.y;
+            if (slot == 1 && !hasB) break;
+            const int m = slot ? (dsc.y & 255) - 64 : ((dsc.x >> 8) & 255) - 64;
+            const int mp = slot ? ((dsc.y >> 8) & 255) - 64 : ((dsc.x >> 16) & 255) - 64;
             const float2 x = slot ? make_float2(x4.z, x4.w) : make_float2(x4.x, x4.y);
             float2 egp = cs.ug[abs(mp)];
             if (mp < 0) egp.y = -egp.y;
@@ -703,18 +701,18 @@ __device__ void compose_block(const BandTables& T, const float4* src, const Stag
         // wedge kernel conj(chi_lm) q~_lm' / total, every layout position (A, B)
         const float inv_total = (float)(1.0 / a.wp_total);
         for (int at = tid; at < T.rows * 32; at += nt) {
-            const int row = at >> 5, item = a.row_group[row] * 32 + (at & 31);
-            const int st = row - T.row_off[item >> 5];
+            const int2 dsc = T.at_desc[at];
             float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (st < T.item_len[item]) {
-                const int l = T.item_mm[item].x + st;
+            if (dsc.x & 1) {
+                const int l = (dsc.x >> 2) & 63;
 #pragma unroll
                 for (int slot = 0; slot < 2; ++slot) {
-                    if (slot == 1 && T.item_w[item].y == 0.0f) break;
-                    const char2 e = slot ? T.item_pm[item] : T.item_mm[item];
-                    const double2 c = chh[l * (l + 1) / 2 + e.x];
+                    if (slot == 1 && !(dsc.x & 2)) break;
+                    const int m = slot ? (dsc.y & 255) - 64 : ((dsc.x >> 8) & 255) - 64;
+                    const int mp = slot ? ((dsc.y >> 8) & 255) - 64 : ((dsc.x >> 16) & 255) - 64;
+                    const double2 c = chh[l * (l + 1) / 2 + m];
                     const float cr = (float)c.x, ci = (float)-c.y;
-                    const float2 qv = qt[l * l + (e.y + l)];
+                    const float2 qv = qt[l * l + (mp + l)];
                     const float2 wv =
                         make_float2((cr * qv.x - ci * qv.y) * inv_total, (cr * qv.y + ci * qv.x) * inv_total);
                     if (slot) v.z = wv.x, v.w = wv.y;

@@ -76,6 +76,7 @@ BandTablesHost build_band_tables(int L) {
     t.R.assign((size_t)t.rows * 32, 0.0f);
     t.item_of.assign((size_t)(2 * L + 1) * (2 * L + 1), -1);
     t.out_pos.assign((size_t)(2 * L + 1) * (2 * L + 1), 0);
+    t.at_desc.assign((size_t)t.rows * 32, int2{0, 0});
     for (int i = 0; i < t.n_items; ++i) {
         const It& it = items[i];
         const int g = i / 32, j = i % 32;
@@ -97,6 +98,13 @@ BandTablesHost build_band_tables(int L) {
         t.bexp[i] = a | (p << 8);
         t.item_of[(size_t)(m + L) * (2 * L + 1) + (mp + L)] = 2 * i;
         if (!self) t.item_of[(size_t)(pa + L) * (2 * L + 1) + (pb + L)] = 2 * i + 1;
+        for (int st = 0; st <= L - m; ++st) {
+            const int l = m + st;
+            int2 dsc;
+            dsc.x = 1 | (self ? 0 : 2) | (l << 2) | ((m + 64) << 8) | ((mp + 64) << 16);
+            dsc.y = (pa + 64) | ((pb + 64) << 8);
+            t.at_desc[(size_t)(t.row_off[g] + st) * 32 + j] = dsc;
+        }
         {
             const int p0 = 2 * ((t.row_off[g] - m) * 32 + j);
             t.out_pos[(size_t)(m + L) * (2 * L + 1) + (mp + L)] = p0;

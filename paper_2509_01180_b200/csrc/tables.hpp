@@ -26,6 +26,8 @@ struct BandTablesHost {
     std::vector<int> bexp;
     std::vector<float> P, Q, R;
     std::vector<int> item_of;     // [(m+L)(2L+1) + m'+L]: 2 item + slot of half-plane entries, else -1
+    std::vector<int2> at_desc;    // [rows*32] per layout position: x = valid | hasB << 1 | l << 2 | (mA+64) << 8 | (m'A+64) << 16,
+                                  //                               y = (mB+64) | (m'B+64) << 8
     std::vector<int> out_pos;     // [(m+L)(2L+1) + m'+L]: 2 ((row_off[g] - m_item) 32 + lane) + slot; +64 l gives 2 at + slot
 };
 BandTablesHost build_band_tables(int L);
