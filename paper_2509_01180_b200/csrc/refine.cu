@@ -749,15 +749,14 @@ __device__ float2 xi_value(int l, int m, int mp, const float* f, const float* t,
 // band-layout entry (row, lane): (xi_l[A], xi_l[B]) of the lane's item
 __device__ float4 xi_entry(const BandTables& T, const int* row_group, const float* f, const float* t,
                            const int* block_off, const int* radial_count, int row, int lane) {
-    const int g = row_group[row];
-    const int item = g * 32 + lane;
-    const int s = row - T.row_off[g];
-    if (s >= T.item_len[item]) return make_float4(0.f, 0.f, 0.f, 0.f);
-    const char2 mm = T.item_mm[item], pm = T.item_pm[item];
-    const int l = mm.x + s;
-    const float2 xa = xi_value(l, mm.x, mm.y, f, t, block_off, radial_count);
-    const float2 xb = T.item_w[item].y == 0.0f ? make_float2(0.f, 0.f)
-                                               : xi_value(l, pm.x, pm.y, f, t, block_off, radial_count);
+    const int2 dsc = T.at_desc[row * 32 + lane];  // degree and entries of the position
+    if (!(dsc.x & 1)) return make_float4(0.f, 0.f, 0.f, 0.f);
+    const int l = (dsc.x >> 2) & 63;
+    const float2 xa = xi_value(l, ((dsc.x >> 8) & 255) - 64, ((dsc.x >> 16) & 255) - 64, f, t, block_off,
+                               radial_count);
+    const float2 xb = !(dsc.x & 2) ? make_float2(0.f, 0.f)
+                                   : xi_value(l, (dsc.y & 255) - 64, ((dsc.y >> 8) & 255) - 64, f, t, block_off,
+                                              radial_count);
     return make_float4(xa.x, xa.y, xb.x, xb.y);
 }
 
