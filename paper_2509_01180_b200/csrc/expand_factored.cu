@@ -161,10 +161,17 @@ __global__ void __launch_bounds__(kThreads, BMB_EXPAND_MINB) expand_factored_ker
             //    0 < g < n, so truncation = floor.  Item = (ray, radius), radius fastest.
             const int nrc = min(kRC, T.nr - ir);
             const int items = nsamp * kRC;
+            // the footprint of the next item is loaded one iteration ahead
+            auto entry = [&](int it) {
+                const int s = it / kRC, j = it - s * kRC;
+                return (it < items && j < nrc) ? __ldg(T.samp + (size_t)s * T.nr + ir + j) : make_int4(0, 0, 0, 0);
+            };
+            int4 e_next = entry(tid);
             for (int it = tid; it < items; it += kThreads) {
                 const int s = it / kRC, j = it - s * kRC;
+                const int4 e = e_next;
+                e_next = entry(it + kThreads);
                 if (j >= nrc) continue;
-                const int4 e = __ldg(T.samp + (size_t)s * T.nr + ir + j);
                 const int x0 = e.x & 1023, y0 = (e.x >> 10) & 1023, z0 = (e.x >> 20) & 1023;
                 const float fx = __int_as_float(e.y), fy = __int_as_float(e.z), fz = __int_as_float(e.w);
                 const int xs0 = x0 + sx, ys0 = y0 + sy, zs0 = z0 + sz;
