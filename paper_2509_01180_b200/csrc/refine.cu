@@ -479,7 +479,7 @@ __device__ __forceinline__ void group_sync() {
 // scratch layout of one composition (floats): full-plane d table, the m >= 0
 // rows of the phase-folded xi, q~, and the staged FP64 wedge factors
 struct ComposeLayout {
-    int dtab, xd, qt, qh, ch, total;
+    int dtab, xd, qt, tq, qh, ch, total;
 };
 // offset of degree l in the m >= 0 half rows: sum_{j<l} (j+1)(2j+1)
 __host__ __device__ __forceinline__ int xh_off(int l) { return l * (l - 1) * (2 * l - 1) / 3 + 3 * l * (l - 1) / 2 + l; }
@@ -492,6 +492,8 @@ __host__ __device__ inline ComposeLayout compose_layout(int L) {
     c.xd = o;
     o += (2 * xh_off(L + 1) + 3) & ~3;
     c.qt = o;
+    o += (2 * (L + 1) * (L + 1) + 3) & ~3;
+    c.tq = o;  // q_ln e^{-i n g}, per degree (shared by every output m' of the degree)
     o += (2 * (L + 1) * (L + 1) + 3) & ~3;
     c.qh = o;
     o += 4 * ntri;
@@ -515,6 +517,7 @@ __device__ void compose_block(const BandTables& T, const float4* src, const Stag
     float* dtab = scr + lay.dtab;
     float2* xd = reinterpret_cast<float2*>(scr + lay.xd);
     float2* qt = reinterpret_cast<float2*>(scr + lay.qt);
+    float2* tq = reinterpret_cast<float2*>(scr + lay.tq);
     double2* qh = reinterpret_cast<double2*>(scr + lay.qh);
     double2* chh = reinterpret_cast<double2*>(scr + lay.ch);
     const bool wedge = out_w != nullptr;
@@ -628,6 +631,21 @@ __device__ void compose_block(const BandTables& T, const float4* src, const Stag
             }
         }
     }
+    if (wedge) {  // t_l[n] = q_ln e^{-i n g}
+        int l = 0;
+        for (int idx = tid; idx < (L + 1) * (L + 1); idx += nt) {
+            while ((l + 1) * (l + 1) <= idx) ++l;
+            const int n = idx - l * l - l, an = abs(n);
+            double2 qv = qh[l * (l + 1) / 2 + an];
+            if (n < 0) {
+                const double sgn = (an & 1) ? -1.0 : 1.0;
+                qv = make_double2(sgn * qv.x, -sgn * qv.y);
+            }
+            float2 egn = cs.ug[an];
+            if (n < 0) egn.y = -egn.y;
+            tq[idx] = cmul(make_float2((float)qv.x, (float)qv.y), egn);
+        }
+    }
     group_sync<WARP>();
     // q~_l[m'] = e^{-i m' a} sum_n d_{m'n} e^{-i n g} q_ln (rank-one wedge factor)
     if (wedge) {
@@ -637,16 +655,9 @@ __device__ void compose_block(const BandTables& T, const float4* src, const Stag
             const int mp = idx - l * l - l;
             const int w = 2 * l + 1, o = xi_off(l);
             float re = 0.0f, im = 0.0f;
+            const float2* tl = tq + l * l + l;
             for (int n = -l; n <= l; ++n) {
-                const int an = abs(n);
-                double2 qv = qh[l * (l + 1) / 2 + an];
-                if (n < 0) {
-                    const double sgn = (an & 1) ? -1.0 : 1.0;
-                    qv = make_double2(sgn * qv.x, -sgn * qv.y);
-                }
-                float2 egn = cs.ug[an];
-                if (n < 0) egn.y = -egn.y;
-                const float2 t = cmul(make_float2((float)qv.x, (float)qv.y), egn);
+                const float2 t = tl[n];
                 const float dv = dtab[o + (mp + l) * w + (n + l)];
                 re = fmaf(dv, t.x, re);
                 im = fmaf(dv, t.y, im);
