@@ -519,7 +519,7 @@ __device__ void compose_block(const BandTables& T, const float4* src, const Stag
     float2* qt = reinterpret_cast<float2*>(scr + lay.qt);
     float2* tq = reinterpret_cast<float2*>(scr + lay.tq);
     double2* qh = reinterpret_cast<double2*>(scr + lay.qh);
-    double2* chh = reinterpret_cast<double2*>(scr + lay.ch);
+    float2* chf = reinterpret_cast<float2*>(scr + lay.ch);  // conj(chi_lm) as FP32 (cr, ci)
     const bool wedge = out_w != nullptr;
     const int ntri = (L + 1) * (L + 2) / 2;
     if (tid < 32) {
@@ -556,7 +556,8 @@ __device__ void compose_block(const BandTables& T, const float4* src, const Stag
     if (wedge)
         for (int i = (WARP ? tid : tid - 32); i >= 0 && i < ntri; i += (WARP ? 32 : nt - 32)) {
             qh[i] = a.q_hat[i];
-            chh[i] = a.chi_hat[i];
+            const double2 c = a.chi_hat[i];
+            chf[i] = make_float2((float)c.x, (float)-c.y);
         }
     group_sync<WARP>();
     const float cb = (float)cos(cs.eul[1]);
@@ -721,8 +722,8 @@ __device__ void compose_block(const BandTables& T, const float4* src, const Stag
                     if (slot == 1 && !(dsc.x & 2)) break;
                     const int m = slot ? (dsc.y & 255) - 64 : ((dsc.x >> 8) & 255) - 64;
                     const int mp = slot ? ((dsc.y >> 8) & 255) - 64 : ((dsc.x >> 16) & 255) - 64;
-                    const double2 c = chh[l * (l + 1) / 2 + m];
-                    const float cr = (float)c.x, ci = (float)-c.y;
+                    const float2 c = chf[l * (l + 1) / 2 + m];
+                    const float cr = c.x, ci = c.y;
                     const float2 qv = qt[l * l + (mp + l)];
                     const float2 wv =
                         make_float2((cr * qv.x - ci * qv.y) * inv_total, (cr * qv.y + ci * qv.x) * inv_total);
