@@ -575,6 +575,7 @@ __device__ void compose_block(const BandTables& T, const float4* src, const Stag
         const float mir = ((m - mp) & 1) ? -1.0f : 1.0f;
         const float mirp = ((pa - pb) & 1) ? -1.0f : 1.0f;
         const int r0 = T.row_off[item >> 5], lane = item & 31;
+        int ob = xi_off(m), w = 2 * m + 1;  // degree block offset and width, advanced per step
         for (int s0 = 0; s0 < len; s0 += 4) {
             float4 pq[4];
 #pragma unroll
@@ -591,13 +592,15 @@ __device__ void compose_block(const BandTables& T, const float4* src, const Stag
                     d1 = d;
                     d = dn;
                 }
-                const int l = m + st, w = 2 * l + 1, o = xi_off(l);
-                dtab[o + (m + l) * w + (mp + l)] = d;
-                dtab[o + (-m + l) * w + (-mp + l)] = mir * d;
+                const int l = m + st;
+                dtab[ob + (m + l) * w + (mp + l)] = d;
+                dtab[ob + (-m + l) * w + (-mp + l)] = mir * d;
                 if (pair) {
-                    dtab[o + (pa + l) * w + (pb + l)] = sg * d;
-                    dtab[o + (-pa + l) * w + (-pb + l)] = mirp * sg * d;
+                    dtab[ob + (pa + l) * w + (pb + l)] = sg * d;
+                    dtab[ob + (-pa + l) * w + (-pb + l)] = mirp * sg * d;
                 }
+                ob += w * w;  // block of degree l + 1 (xi_off(l + 1))
+                w += 2;
             }
         }
     }
