@@ -1073,10 +1073,12 @@ __global__ void __launch_bounds__(EvalShape<K>::WARPS * 32, BMB_EVAL_MINB(ORDER)
         idx[k] = q0 + k < n ? i : -1;
         const CandWork& wk = a.work[i];
         const int w = i / a.max_cand;
-        const bool chart = wk.status == ST_EVAL2 && a.cand[i].anchored;  // order 0: global angles
+        // order 2 (status EVAL2): chart angles, the chart kernels when anchored; order 0
+        // (trials, final scores): global angles et on the window kernel
+        const bool chart = ORDER == 2 && a.cand[i].anchored;
         job[k].xi = chart ? a.xi_pool + (size_t)wk.slot * len : a.xi_win + (size_t)w * len;
         job[k].wx = !wedge ? nullptr : (chart ? a.w_pool + (size_t)wk.slot * len : a.T.wedge);
-        const double* e = wk.status == ST_EVAL2 ? wk.e : wk.et;
+        const double* e = ORDER == 2 ? wk.e : wk.et;
         job[k].a = e[0], job[k].b = e[1], job[k].g = e[2];
     }
     WarpScratch* ws = wsc + warp * K;
