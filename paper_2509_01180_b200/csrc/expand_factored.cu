@@ -151,6 +151,21 @@ __global__ void __launch_bounds__(kThreads, BMB_EXPAND_MINB) expand_factored_ker
     float acc[RPT];
 #pragma unroll
     for (int q = 0; q < RPT; ++q) acc[q] = 0.0f;
+    // theta role of the specialised kernel (n_theta = NPC, tri(L) <= threads): one
+    // (l, m) per thread, its weights P_l^m(u_t) w_t in registers for all radii
+    float th_w[NPC > 0 ? NPC / 2 : 1];
+    int th_m = 0, th_base = 0;
+    float th_sgn = 1.0f;
+    if constexpr (NPC > 0 && (NPC / 2) * (NPC / 2 + 1) / 2 <= kThreads) {
+        if (tid < T.ntri) {
+            const int2 lm = T.tri_lm[tid];
+            th_m = lm.y;
+            th_base = lm.x * lm.x;
+            th_sgn = ((lm.x + lm.y) & 1) ? -1.0f : 1.0f;
+#pragma unroll
+            for (int t = 0; t < NPC / 2; ++t) th_w[t] = __ldg(T.ptab + (size_t)tid * NPC + t);
+        }
+    }
     __syncthreads();
 
     for (int ir = 0; ir < T.nr; ++ir) {
@@ -220,6 +235,23 @@ __global__ void __launch_bounds__(kThreads, BMB_EXPAND_MINB) expand_factored_ker
         }
         __syncthreads();
         // 3. theta: G[l,m] = sum_t Pbar_l^m(u_t) w_t F[t][m], folded over t <-> nt-1-t
+        if constexpr (NPC > 0 && (NPC / 2) * (NPC / 2 + 1) / 2 <= kThreads) {  // n_theta = n_phi = NPC: the thread's P.w row in registers
+            if (tid < T.ntri) {
+                float re = 0.0f, im = 0.0f;
+#pragma unroll
+                for (int t = 0; t < NPC / 2; ++t) {
+                    const float2 a = F[t * nl + th_m], b = F[(NPC - 1 - t) * nl + th_m];
+                    re = fmaf(th_w[t], fmaf(th_sgn, b.x, a.x), re);
+                    im = fmaf(th_w[t], fmaf(th_sgn, b.y, a.y), im);
+                }
+                if (th_m == 0) {
+                    Gp[th_base] = re;
+                } else {
+                    Gp[th_base + 2 * th_m - 1] = re;
+                    Gp[th_base + 2 * th_m] = im;
+                }
+            }
+        } else
         for (int q = tid; q < T.ntri; q += kThreads) {
             const int2 lm = T.tri_lm[q];
             const float sgn = ((lm.x + lm.y) & 1) ? -1.0f : 1.0f;
