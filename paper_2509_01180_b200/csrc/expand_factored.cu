@@ -93,7 +93,7 @@ struct DftTab {
             }
     }
 };
-template <int NP, int MH>
+template <int NP, int M0, int MH>
 __device__ __forceinline__ void dft_ring(const float* f, float2* Frow) {
     constexpr int H = NP / 2;
     constexpr DftTab<NP> tab{};
@@ -106,7 +106,7 @@ __device__ __forceinline__ void dft_ring(const float* f, float2* Frow) {
     }
     const float f0 = f[0], fh = f[H];
 #pragma unroll
-    for (int m = 0; m < MH; ++m) {
+    for (int m = M0; m < MH; ++m) {
         float re = f0 + ((m & 1) ? -fh : fh);
         float im = 0.0f;
 #pragma unroll
@@ -216,7 +216,15 @@ __global__ void __launch_bounds__(kThreads, BMB_EXPAND_MINB) expand_factored_ker
         __syncthreads();
         // 2. phi-DFT: F[t][m] = sum_p f[t][p] e^{-2 pi i m p / n_phi}, folded
         if constexpr (NPC > 0) {  // one ring per thread, all orders
-            for (int t = tid; t < nt; t += kThreads) dft_ring<NPC, NPC / 2>(samp + rc * nsamp + t * np, F + t * nl);
+            // orders split over two groups of 64 threads (whole warps: no divergence)
+            constexpr int MH = NPC / 2, MS = (MH + 1) / 2;
+            static_assert(NPC <= 64, "one ring per thread of a 64-thread group");
+            for (int it = tid; it < 128; it += kThreads) {
+                const int t = it & 63;
+                if (t >= nt) continue;
+                if (it < 64) dft_ring<NPC, 0, MS>(samp + rc * nsamp + t * np, F + t * nl);
+                else dft_ring<NPC, MS, MH>(samp + rc * nsamp + t * np, F + t * nl);
+            }
         } else if (dtg < TG) {
             for (int t = dtg; t < nt; t += TG) {
                 const float* f = samp + rc * nsamp + t * np;
