@@ -217,14 +217,29 @@ __global__ void __launch_bounds__(kThreads, BMB_EXPAND_MINB) expand_factored_ker
         // 2. phi-DFT: F[t][m] = sum_p f[t][p] e^{-2 pi i m p / n_phi}, folded
         if constexpr (NPC > 0) {  // one ring per thread, all orders
             // orders split over two groups of 64 threads (whole warps: no divergence)
-            constexpr int MH = NPC / 2, MS = (MH + 1) / 2;
+            constexpr int MH = NPC / 2;
             static_assert(NPC <= 64, "one ring per thread of a 64-thread group");
+#if BMB_DFT_GROUPS == 4
+            constexpr int Q = (MH + 3) / 4;
+            {
+                const int it = tid, t = it & 63, g = it >> 6;
+                if (t < nt) {
+                    const float* f = samp + rc * nsamp + t * np;
+                    if (g == 0) dft_ring<NPC, 0, Q>(f, F + t * nl);
+                    else if (g == 1) dft_ring<NPC, Q, 2 * Q>(f, F + t * nl);
+                    else if (g == 2) dft_ring<NPC, 2 * Q, 3 * Q>(f, F + t * nl);
+                    else dft_ring<NPC, 3 * Q, MH>(f, F + t * nl);
+                }
+            }
+#else
+            constexpr int MS = (MH + 1) / 2;
             for (int it = tid; it < 128; it += kThreads) {
                 const int t = it & 63;
                 if (t >= nt) continue;
                 if (it < 64) dft_ring<NPC, 0, MS>(samp + rc * nsamp + t * np, F + t * nl);
                 else dft_ring<NPC, MS, MH>(samp + rc * nsamp + t * np, F + t * nl);
             }
+#endif
         } else if (dtg < TG) {
             for (int t = dtg; t < nt; t += TG) {
                 const float* f = samp + rc * nsamp + t * np;
