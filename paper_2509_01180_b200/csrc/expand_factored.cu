@@ -118,10 +118,18 @@ __device__ __forceinline__ void dft_ring(const float* f, float2* Frow) {
     }
 }
 
+// compile-time knobs (measured defaults): the radial stage's row map in registers,
+// phi-DFT order groups per ring (2 groups of 64 threads)
+#ifndef BMB_RP_REG
+#define BMB_RP_REG 1
+#endif
+#ifndef BMB_DFT_GROUPS
+#define BMB_DFT_GROUPS 2
+#endif
 // HALF: compile-time bound on n_phi / 2 (twiddles in registers); RPT: bound on
 // the real-packed rows per thread (accumulators in registers)
 #ifndef BMB_EXPAND_MINB
-#define BMB_EXPAND_MINB 4
+#define BMB_EXPAND_MINB 3
 #endif
 template <int HALF, int RPT, int NPC>
 __global__ void __launch_bounds__(kThreads, BMB_EXPAND_MINB) expand_factored_kernel(FactoredTables T, const float* __restrict__ vols,
@@ -151,6 +159,11 @@ __global__ void __launch_bounds__(kThreads, BMB_EXPAND_MINB) expand_factored_ker
     float acc[RPT];
 #pragma unroll
     for (int q = 0; q < RPT; ++q) acc[q] = 0.0f;
+#if BMB_RP_REG
+    int rpr[RPT];
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) rpr[q] = tid + q * kThreads < T.coeffs ? T.rowpack[tid + q * kThreads] : 0;
+#endif
     // theta role of the specialised kernel (n_theta = NPC, tri(L) <= threads): one
     // (l, m) per thread, its weights P_l^m(u_t) w_t in registers for all radii
     float th_w[NPC > 0 ? NPC / 2 : 1];
@@ -300,7 +313,11 @@ __global__ void __launch_bounds__(kThreads, BMB_EXPAND_MINB) expand_factored_ker
         for (int q = 0; q < RPT; ++q) {
             const int row = tid + q * kThreads;
             if (row < T.coeffs) {
+#if BMB_RP_REG
+                const int rp = rpr[q];
+#else
                 const int rp = rowpack[row];
+#endif
                 acc[q] = fmaf(rad[rp >> 16], Gp[rp & 0xffff], acc[q]);
             }
         }
