@@ -145,10 +145,13 @@ __global__ void __launch_bounds__(256) seed_kernel(SeedArgs a) {
             const int jj = j + dj;
             if (jj < 0 || jj >= a.nb) continue;
             for (int di = -1; di <= 1 && is_max; ++di) {
-                const int ii = (i + di + a.na) % a.na;
+                int ii = i + di;  // alpha wraps (no integer modulo on the hot path)
+                ii += ii < 0 ? a.na : (ii >= a.na ? -a.na : 0);
+                const int row = (jj * a.na + ii) * a.ng;
                 for (int dk = -1; dk <= 1; ++dk) {
-                    const int kk = (k + dk + a.ng) % a.ng;
-                    const int other = (jj * a.na + ii) * a.ng + kk;
+                    int kk = k + dk;  // gamma wraps
+                    kk += kk < 0 ? a.ng : (kk >= a.ng ? -a.ng : 0);
+                    const int other = row + kk;
                     if (other == idx) continue;
                     const double o = sc[other];
                     if (o > s || (o == s && other < idx)) {
