@@ -1,4 +1,5 @@
 // Context construction and the batched expansion driver.
+#include <cstdlib>
 #include <cstring>
 #include "context.hpp"
 
@@ -213,8 +214,21 @@ void Context::expand_windows(const float* vols, long long vol_stride, int n_vol,
         upload(win_shift, wshift, stream);
         coef.reserve(sizeof(float) * (size_t)nw * geo.m_pad);
         cudaEvent_t f0 = timer.begin(stream);
+        // several windows per volume (the alignment's shift search): gather from an
+        // x-paired copy, one 8-byte load per footprint row (BMB_EXPAND_PAIRS=0: off)
+        static const int pairs_mode = [] {
+            const char* e = std::getenv("BMB_EXPAND_PAIRS");
+            return e ? std::atoi(e) : 1;
+        }();
+        const float2* pairs = nullptr;
+        if (pairs_mode != 0 && nw >= 4 * (long long)n_vol) {
+            vol_pairs.reserve(sizeof(float2) * (size_t)pair_volume_elems(n) * n_vol);
+            launch_pair_volumes(vols, vol_stride, n_vol, n, vol_pairs.as<float2>(), stream);
+            ++timer.launches;
+            pairs = vol_pairs.as<float2>();
+        }
         if (launch_expand_factored(fx, vols, vol_stride, win_vol.as<int>(), win_shift.as<int>(), nw, coef.as<float>(),
-                                   geo.m_pad, stream) != 0)
+                                   geo.m_pad, stream, pairs) != 0)
             throw std::runtime_error("factored expansion launch failed");
         ++timer.launches;
         ++timer.gemm_launches;

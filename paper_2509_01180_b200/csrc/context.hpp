@@ -181,6 +181,7 @@ public:
 
     // work buffers
     DevBuf B_hi, B_lo, col_scale, coef, win_vol, win_shift, vol_scale, norms;
+    DevBuf vol_pairs;  // x-paired particle volumes for the expansion gathers (many windows per volume)
 
     // expansion of `count` windows (volume index + integer shift) of volumes
     // already on the device; real-packed FP32 coefficients into ctx.coef

@@ -17,6 +17,7 @@
 // (DESIGN.md §3 K2f): 16 S + 4 n_phi n_r n_theta (L+1) + 4 n_r tri(L) n_theta +
 // 2 n_r C FLOP, S = n_r n_theta n_phi — 4.47 MFLOP at config 2, about 120x fewer
 // than the dense 2 C V of the pulled-back operator.
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <mutex>
@@ -135,7 +136,7 @@ template <int HALF, int RPT, int NPC>
 __global__ void __launch_bounds__(kThreads, BMB_EXPAND_MINB) expand_factored_kernel(FactoredTables T, const float* __restrict__ vols,
                                                                     long long vol_stride, const int* __restrict__ win_vol,
                                                                     const int* __restrict__ win_shift, float* __restrict__ out,
-                                                                    int ldo) {
+                                                                    int ldo, const float2* __restrict__ pairs) {
     extern __shared__ __align__(16) unsigned char sm[];
     const Smem P = smem_plan(T);
     float* samp = reinterpret_cast<float*>(sm + P.samp);
@@ -148,6 +149,7 @@ __global__ void __launch_bounds__(kThreads, BMB_EXPAND_MINB) expand_factored_ker
     const int n = T.n, L = T.L, nt = T.nt, np = T.np, half = np / 2, nl = L + 1;
     const int nsamp = nt * np;
     const float* __restrict__ v = vols + (long long)win_vol[w] * vol_stride;
+    const float2* __restrict__ vp = pairs ? pairs + win_vol[w] * pair_volume_elems(T.n) : nullptr;
     const int sx = win_shift[3 * w], sy = win_shift[3 * w + 1], sz = win_shift[3 * w + 2];
     for (int i = tid; i < T.coeffs; i += kThreads) rowpack[i] = T.rowpack[i];
     // DFT role: fixed order m, rings t = tg, tg + TG, ...
@@ -209,17 +211,33 @@ __global__ void __launch_bounds__(kThreads, BMB_EXPAND_MINB) expand_factored_ker
                 const bool vy1 = (unsigned)(y0 + 1) < (unsigned)n && (unsigned)(ys0 + 1) < (unsigned)n;
                 const bool vz0 = (unsigned)z0 < (unsigned)n && (unsigned)zs0 < (unsigned)n;
                 const bool vz1 = (unsigned)(z0 + 1) < (unsigned)n && (unsigned)(zs0 + 1) < (unsigned)n;
-                const long long o0 = ((long long)zs0 * n + ys0) * n + xs0;
                 float val = 0.0f;
+                if (vp) {  // x-paired layout: one 8-byte load per (y, z) row; vx0 || vx1 => -1 <= xs0 < n
+                    const long long o0 = ((long long)zs0 * n + ys0) * (n + 1) + xs0 + 1;
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {  // (y, z) rows of the footprint
-                    const int bb = c & 1, aa = c >> 1;
-                    const bool vr = (bb ? vy1 : vy0) && (aa ? vz1 : vz0);
-                    const float* row = v + o0 + (bb ? n : 0) + (aa ? (long long)n * n : 0);
-                    const float v0 = (vr && vx0) ? __ldg(row) : 0.0f;
-                    const float v1 = (vr && vx1) ? __ldg(row + 1) : 0.0f;
-                    const float wyz = (bb ? fy : 1.0f - fy) * (aa ? fz : 1.0f - fz);
-                    val = fmaf(wyz, fmaf(fx, v1 - v0, v0), val);
+                    for (int c = 0; c < 4; ++c) {
+                        const int bb = c & 1, aa = c >> 1;
+                        const bool vr = (bb ? vy1 : vy0) && (aa ? vz1 : vz0);
+                        const float2 pr = (vr && (vx0 || vx1))
+                                              ? __ldg(vp + o0 + (bb ? n + 1 : 0) + (aa ? (long long)n * (n + 1) : 0))
+                                              : make_float2(0.0f, 0.0f);
+                        const float v0 = vx0 ? pr.x : 0.0f;
+                        const float v1 = vx1 ? pr.y : 0.0f;
+                        const float wyz = (bb ? fy : 1.0f - fy) * (aa ? fz : 1.0f - fz);
+                        val = fmaf(wyz, fmaf(fx, v1 - v0, v0), val);
+                    }
+                } else {
+                    const long long o0 = ((long long)zs0 * n + ys0) * n + xs0;
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {  // (y, z) rows of the footprint
+                        const int bb = c & 1, aa = c >> 1;
+                        const bool vr = (bb ? vy1 : vy0) && (aa ? vz1 : vz0);
+                        const float* row = v + o0 + (bb ? n : 0) + (aa ? (long long)n * n : 0);
+                        const float v0 = (vr && vx0) ? __ldg(row) : 0.0f;
+                        const float v1 = (vr && vx1) ? __ldg(row + 1) : 0.0f;
+                        const float wyz = (bb ? fy : 1.0f - fy) * (aa ? fz : 1.0f - fz);
+                        val = fmaf(wyz, fmaf(fx, v1 - v0, v0), val);
+                    }
                 }
                 samp[j * nsamp + s] = val;
             }
@@ -334,10 +352,10 @@ __global__ void __launch_bounds__(kThreads, BMB_EXPAND_MINB) expand_factored_ker
 
 template <int HALF, int RPT, int NPC = 0>
 int launch_t(const FactoredTables& T, size_t smem, const float* vols, long long vol_stride, const int* win_vol,
-             const int* win_shift, int n_win, float* out, int ldo, cudaStream_t s) {
+             const int* win_shift, int n_win, float* out, int ldo, cudaStream_t s, const float2* pairs) {
     ensure_dynamic_smem(expand_factored_kernel<HALF, RPT, NPC>, (int)smem);
     expand_factored_kernel<HALF, RPT, NPC><<<n_win, kThreads, smem, s>>>(T, vols, vol_stride, win_vol, win_shift, out,
-                                                                         ldo);
+                                                                         ldo, pairs);
     return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }
 
@@ -345,8 +363,33 @@ int launch_t(const FactoredTables& T, size_t smem, const float* vols, long long 
 
 size_t factored_smem_bytes(const FactoredTables& T) { return smem_plan(T).total; }
 
+namespace {
+// one thread per output pair; rows of n + 1 pairs (x = -1 .. n-1)
+__global__ void pair_volumes_kernel(const float* __restrict__ vols, long long vol_stride, int n, long long total,
+                                    float2* __restrict__ pairs) {
+    const long long per = pair_volume_elems(n);
+    const int w = n + 1;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long vol = i / per, r = i - vol * per;
+        const long long row = r / w;
+        const int x = (int)(r - row * w) - 1;
+        const float* src = vols + vol * vol_stride + row * n;
+        pairs[i] = make_float2(x >= 0 ? __ldg(src + x) : 0.0f, x + 1 < n ? __ldg(src + x + 1) : 0.0f);
+    }
+}
+}  // namespace
+
+void launch_pair_volumes(const float* vols, long long vol_stride, int n_vol, int n, float2* pairs, cudaStream_t s) {
+    const long long total = pair_volume_elems(n) * n_vol;
+    if (total <= 0) return;
+    const long long blocks = std::min<long long>((total + 255) / 256, 148LL * 16);
+    pair_volumes_kernel<<<(int)blocks, 256, 0, s>>>(vols, vol_stride, n, total, pairs);
+}
+
 int launch_expand_factored(const FactoredTables& T, const float* vols, long long vol_stride, const int* win_vol,
-                           const int* win_shift, int n_win, float* out, int ldo, cudaStream_t s) {
+                           const int* win_shift, int n_win, float* out, int ldo, cudaStream_t s,
+                           const float2* pairs) {
     if (n_win <= 0) return 0;
     const size_t smem = factored_smem_bytes(T);
     if (smem > 220 * 1024) return 1;
@@ -357,16 +400,16 @@ int launch_expand_factored(const FactoredTables& T, const float* vols, long long
         return !(e && std::atoi(e) == 0);
     }();
     if (cdft && T.L + 1 == T.np / 2) {  // n_phi = 2L + 2 with compile-time twiddles
-        if (T.np == 18 && rpt <= 4) return launch_t<9, 4, 18>(T, smem, vols, vol_stride, win_vol, win_shift, n_win, out, ldo, s);
-        if (T.np == 34 && rpt <= 12) return launch_t<17, 12, 34>(T, smem, vols, vol_stride, win_vol, win_shift, n_win, out, ldo, s);
-        if (T.np == 42 && rpt <= 24) return launch_t<21, 24, 42>(T, smem, vols, vol_stride, win_vol, win_shift, n_win, out, ldo, s);
-        if (T.np == 50 && rpt <= 40) return launch_t<25, 40, 50>(T, smem, vols, vol_stride, win_vol, win_shift, n_win, out, ldo, s);
+        if (T.np == 18 && rpt <= 4) return launch_t<9, 4, 18>(T, smem, vols, vol_stride, win_vol, win_shift, n_win, out, ldo, s, pairs);
+        if (T.np == 34 && rpt <= 12) return launch_t<17, 12, 34>(T, smem, vols, vol_stride, win_vol, win_shift, n_win, out, ldo, s, pairs);
+        if (T.np == 42 && rpt <= 24) return launch_t<21, 24, 42>(T, smem, vols, vol_stride, win_vol, win_shift, n_win, out, ldo, s, pairs);
+        if (T.np == 50 && rpt <= 40) return launch_t<25, 40, 50>(T, smem, vols, vol_stride, win_vol, win_shift, n_win, out, ldo, s, pairs);
     }
-    if (half <= 9 && rpt <= 4) return launch_t<9, 4>(T, smem, vols, vol_stride, win_vol, win_shift, n_win, out, ldo, s);
-    if (half <= 17 && rpt <= 12) return launch_t<17, 12>(T, smem, vols, vol_stride, win_vol, win_shift, n_win, out, ldo, s);
-    if (half <= 21 && rpt <= 24) return launch_t<21, 24>(T, smem, vols, vol_stride, win_vol, win_shift, n_win, out, ldo, s);
-    if (half <= 25 && rpt <= 40) return launch_t<25, 40>(T, smem, vols, vol_stride, win_vol, win_shift, n_win, out, ldo, s);
-    if (half <= 33 && rpt <= 72) return launch_t<33, 72>(T, smem, vols, vol_stride, win_vol, win_shift, n_win, out, ldo, s);
+    if (half <= 9 && rpt <= 4) return launch_t<9, 4>(T, smem, vols, vol_stride, win_vol, win_shift, n_win, out, ldo, s, pairs);
+    if (half <= 17 && rpt <= 12) return launch_t<17, 12>(T, smem, vols, vol_stride, win_vol, win_shift, n_win, out, ldo, s, pairs);
+    if (half <= 21 && rpt <= 24) return launch_t<21, 24>(T, smem, vols, vol_stride, win_vol, win_shift, n_win, out, ldo, s, pairs);
+    if (half <= 25 && rpt <= 40) return launch_t<25, 40>(T, smem, vols, vol_stride, win_vol, win_shift, n_win, out, ldo, s, pairs);
+    if (half <= 33 && rpt <= 72) return launch_t<33, 72>(T, smem, vols, vol_stride, win_vol, win_shift, n_win, out, ldo, s, pairs);
     return 1;  // larger bases: use the dense operator path (bm_context_set_expand_mode)
 }
 

@@ -20,7 +20,14 @@ struct FactoredTables {
 size_t factored_smem_bytes(const FactoredTables& T);
 // coefficients of windows (volume win_vol[w] shifted by win_shift[3w..3w+2]) into
 // out[w * ldo + row], real-packed FP32 rows; vols: raster (x fastest), vol_stride apart
+// pairs (optional, else nullptr): the volumes in x-paired layout (launch_pair_volumes)
 int launch_expand_factored(const FactoredTables& T, const float* vols, long long vol_stride, const int* win_vol,
-                           const int* win_shift, int n_win, float* out, int ldo, cudaStream_t s);
+                           const int* win_shift, int n_win, float* out, int ldo, cudaStream_t s,
+                           const float2* pairs = nullptr);
+// x-paired copy of n_vol volumes for the trilinear gathers of the expansion:
+// pairs[v][z][y][x + 1] = (v[x], v[x + 1]) for x = -1 .. n-1, zero outside the row
+// (n * n * (n + 1) float2 per volume), so one 8-byte load serves both x taps
+constexpr long long pair_volume_elems(int n) { return (long long)n * n * (n + 1); }
+void launch_pair_volumes(const float* vols, long long vol_stride, int n_vol, int n, float2* pairs, cudaStream_t s);
 
 }  // namespace bmb
