@@ -67,6 +67,16 @@ int bm_context_set_lanes(bm_context* ctx, int lanes, int min_per_lane);
  * warp iterating its own candidates; measured 4x slower).  Both
  * run the same per-candidate arithmetic; outcomes are bit-identical. */
 int bm_context_set_refine_mode(bm_context* ctx, int mode);
+/* Expansion gathers of the factored mode: 0 = direct loads, 1 = from an
+ * x-paired copy of each volume when it has >= 4 windows (default; the shift
+ * search), 2 = always from the copy.  The coefficients are bit-identical. */
+int bm_context_set_expand_pairs(bm_context* ctx, int mode);
+/* Host-buffer staging: with reuse on, a bm_average_accumulate directly after a
+ * completed bm_align_batch of the same host buffer and count uses the device
+ * copy that bm_align_batch staged (once), instead of copying the buffer again.
+ * The caller promises not to modify the buffer in between.  Default off: every
+ * call stages its host particles. */
+int bm_context_set_stage_reuse(bm_context* ctx, int on);
 /* lambda_cut actually used by the context */
 double bm_context_lambda_cut(const bm_context* ctx);
 /* radial roots / norms of degree l (BasisSpec::root/norm, basis.hpp:40-41); returns count k_l */

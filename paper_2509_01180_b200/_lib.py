@@ -119,6 +119,10 @@ def _declare(L: C.CDLL) -> None:
     L.bm_context_set_refine_mode.restype = I
     L.bm_context_set_expand_mode.argtypes = [P, I]
     L.bm_context_set_expand_mode.restype = I
+    L.bm_context_set_expand_pairs.argtypes = [P, I]
+    L.bm_context_set_expand_pairs.restype = I
+    L.bm_context_set_stage_reuse.argtypes = [P, I]
+    L.bm_context_set_stage_reuse.restype = I
     L.bm_context_eval_stats.argtypes = [P, P, P, I]
     L.bm_context_eval_stats.restype = I
     L.bm_make_template.argtypes = [I, I, I, C.c_ulonglong, P, P]

@@ -317,6 +317,16 @@ class Context:
                    "set_expand_mode")
         self._refresh_info()
 
+    def set_expand_pairs(self, mode: int):
+        """Expansion gathers: 0 direct, 1 x-paired copy when a volume has >= 4 windows
+        (default), 2 always from the copy.  Coefficients are bit-identical."""
+        _lib.check(_lib.lib().bm_context_set_expand_pairs(self._h, int(mode)), "set_expand_pairs")
+
+    def set_stage_reuse(self, on: bool):
+        """Opt in: average_accumulate right after align_batch of the same (unmodified)
+        host buffer reuses the device copy align_batch staged, once."""
+        _lib.check(_lib.lib().bm_context_set_stage_reuse(self._h, 1 if on else 0), "set_stage_reuse")
+
     def eval_stats(self, reset: bool = False):
         """(order-2 evaluations, order-0 evaluations, algorithmic FLOPs) of the refinement."""
         ev = (C.c_longlong * 2)()

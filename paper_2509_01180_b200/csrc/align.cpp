@@ -49,6 +49,8 @@ void AlignConfig::validate(int l_max) const {
     if (max_candidates < 1 || newton_max_iter < 1) throw std::invalid_argument("config: counts must be positive");
     if (max_candidates > 256) throw std::invalid_argument("config: max_candidates above 256 is not supported on the device path");
     if (!(grad_tol > 0.0) || !(step_damping > 0.0)) throw std::invalid_argument("config: tolerances must be positive");
+    if (!std::isfinite(accept_tol) || accept_tol < 0.0)
+        throw std::invalid_argument("config: accept_tol must be finite and non-negative");
     if (shift_radius < 0 || shift_step < 1) throw std::invalid_argument("config: bad shift search parameters");
 }
 
@@ -613,16 +615,33 @@ bool host_pointer(const void* p) {
 const float* Context::device_particles(const float* particles, int count) {
     if (count <= 0 || !host_pointer(particles)) return particles;
     const size_t bytes = sizeof(float) * (size_t)n * n * n * count;
-    if (particles != staged_src_ || count != staged_count_) {
+    // the copy staged by the last bm_align_batch serves this call only when the
+    // caller opted in (bm_context_set_stage_reuse), only for the same buffer and
+    // count, and only once; otherwise the host buffer is staged again
+    const bool reuse = stage_reuse_ && staged_valid_ && particles == staged_src_ && count == staged_count_;
+    staged_valid_ = false;
+    staged_src_ = nullptr;
+    if (!reuse) {
         staged_.reserve(bytes);
         ck(cudaMemcpyAsync(staged_.p, particles, bytes, cudaMemcpyHostToDevice, stream), "stage particles");
-        staged_src_ = particles;
-        staged_count_ = count;
     }
     return staged_.as<float>();
 }
 
 std::vector<ParticleResult> Context::align_batch(const float* particles, int count, const AlignConfig& cfg) {
+    // any earlier staged copy is stale from here on, whatever happens below
+    staged_valid_ = false;
+    staged_src_ = nullptr;
+    std::vector<ParticleResult> out = align_batch_impl(particles, count, cfg);
+    if (count > 0 && host_pointer(particles)) {  // complete: the staged copy holds these bytes
+        staged_src_ = particles;
+        staged_count_ = count;
+        staged_valid_ = true;
+    }
+    return out;
+}
+
+std::vector<ParticleResult> Context::align_batch_impl(const float* particles, int count, const AlignConfig& cfg) {
     if (!has_template) throw std::invalid_argument("align: set_template first");
     cfg.validate(basis.l_max);
     const int k = std::max(1, std::min(lanes, count / std::max(1, lane_min_particles)));
@@ -631,8 +650,6 @@ std::vector<ParticleResult> Context::align_batch(const float* particles, int cou
     if (host) {
         staged_.reserve(sizeof(float) * (size_t)n * n * n * count);
         stage = staged_.as<float>();
-        staged_src_ = particles;
-        staged_count_ = count;
     }
     // slice [o, o + c) of the batch on the device: staged on stream s when host-resident
     auto slice = [&](int o, int c, cudaStream_t s) -> const float* {
@@ -710,6 +727,7 @@ void Context::ensure_lanes() {
     }
     for (auto& c : lane_ctx_) {
         c->expand_mode = expand_mode;
+        c->pairs_mode = pairs_mode;
         c->refine_mode = refine_mode;
         c->pool_budget_ = pool_budget_;  // each lane allocates only what its slice needs
     }
@@ -870,6 +888,12 @@ void Context::align_group(const float* fw, int n_vol, const std::vector<int>& pa
             wv.push_back(p);
             ws.insert(ws.end(), s.begin(), s.end());
         }
+    // the coarse and fine passes read the same volumes: one x-paired copy serves both
+    struct PairHold {
+        Context& c;
+        explicit PairHold(Context& x) : c(x) { c.pairs_hold_ = true; c.pairs_src_ = nullptr; }
+        ~PairHold() { c.pairs_hold_ = false; c.pairs_src_ = nullptr; }
+    } hold(*this);
     std::vector<WindowOutcome> oc = run_windows(fw, n_vol, wv, ws, cfg);
     std::vector<int> best(n_vol, -1);
     std::vector<long long> cand(n_vol, 0), evals(n_vol, 0);

@@ -126,7 +126,8 @@ void launch_average(const float* coef, int ldc, const double* quats, int count, 
     if (count <= 0) return;
     const size_t smem = sizeof(double) * (size_t)(L + 1) * (2 * L + 1) * (2 * L + 3) / 3;
     if (smem > 200 * 1024) throw std::invalid_argument("average: band limit too large for the shared d stack");
-    ensure_dynamic_smem(average_kernel, (int)smem);
+    if (ensure_dynamic_smem(average_kernel, (int)smem) != cudaSuccess)
+        throw std::runtime_error("average: shared-memory opt-in failed");
     average_kernel<<<count, 256, smem, s>>>(coef, ldc, quats, L, block_off, radial_count,
                                             reinterpret_cast<double2*>(sum));
     if (cudaGetLastError() != cudaSuccess) throw std::runtime_error("average kernel launch failed");

@@ -16,6 +16,13 @@
 #include "refine.cuh"
 #include "wedge.hpp"
 
+namespace {
+// FP32 evaluation tolerances (the same values as kFp32AcceptTol / kFp32GradTol
+// of include/ballmatch_b200.hpp and api.FP32_ACCEPT_TOL / FP32_GRAD_TOL)
+constexpr double kFp32AcceptTolC = 1e-6;
+constexpr double kFp32GradTolC = 1e-5;
+}  // namespace
+
 struct bm_context {
     std::unique_ptr<bmb::Context> impl;
 };
@@ -180,11 +187,19 @@ static bmb::AlignConfig cfg_of(const bm_align_config* c) {
     a.seed_grid_step = c->seed_grid_step;
     a.max_candidates = c->max_candidates;
     a.newton_max_iter = c->newton_max_iter;
-    a.grad_tol = c->grad_tol;
     a.step_damping = c->step_damping;
     a.shift_radius = c->shift_radius;
     a.shift_step = c->shift_step;
-    a.accept_tol = c->accept_tol;
+    // accept_tol == 0 (e.g. a zero-initialised struct): the FP32 defaults of the
+    // C++ and Python wrappers (slack 1e-6, gradient floor 1e-5);
+    // negative or non-finite values reach validate() and are rejected there
+    if (c->accept_tol == 0.0) {
+        a.accept_tol = kFp32AcceptTolC;
+        a.grad_tol = std::max(c->grad_tol, kFp32GradTolC);
+    } else {
+        a.accept_tol = c->accept_tol;
+        a.grad_tol = c->grad_tol;
+    }
     return a;
 }
 
@@ -420,6 +435,23 @@ int bm_context_set_expand_mode(bm_context* ctx, int mode) {
         cudaSetDevice(c.device);
         c.expand_mode = mode;
         if (mode == 1) c.ensure_operator();
+        return (int)BM_OK;
+    });
+}
+
+int bm_context_set_expand_pairs(bm_context* ctx, int mode) {
+    return guarded("bm_context_set_expand_pairs", [&] {
+        if (!ctx) return (int)BM_ERR_STATE;
+        if (mode < 0 || mode > 2) throw std::invalid_argument("expand pairs mode must be 0, 1 or 2");
+        ctx->impl->pairs_mode = mode;
+        return (int)BM_OK;
+    });
+}
+
+int bm_context_set_stage_reuse(bm_context* ctx, int on) {
+    return guarded("bm_context_set_stage_reuse", [&] {
+        if (!ctx) return (int)BM_ERR_STATE;
+        ctx->impl->stage_reuse_ = on != 0;
         return (int)BM_OK;
     });
 }

@@ -215,16 +215,23 @@ void Context::expand_windows(const float* vols, long long vol_stride, int n_vol,
         coef.reserve(sizeof(float) * (size_t)nw * geo.m_pad);
         cudaEvent_t f0 = timer.begin(stream);
         // several windows per volume (the alignment's shift search): gather from an
-        // x-paired copy, one 8-byte load per footprint row (BMB_EXPAND_PAIRS=0: off)
-        static const int pairs_mode = [] {
-            const char* e = std::getenv("BMB_EXPAND_PAIRS");
-            return e ? std::atoi(e) : 1;
-        }();
+        // x-paired copy, one 8-byte load per footprint row.  pairs_mode 0: off,
+        // 1: when a volume has >= 4 windows, 2: always (tests).  Same FP32 values
+        // and FMA order either way, so the coefficients are bit-identical.
         const float2* pairs = nullptr;
-        if (pairs_mode != 0 && nw >= 4 * (long long)n_vol) {
-            vol_pairs.reserve(sizeof(float2) * (size_t)pair_volume_elems(n) * n_vol);
-            launch_pair_volumes(vols, vol_stride, n_vol, n, vol_pairs.as<float2>(), stream);
-            ++timer.launches;
+        const size_t pair_bytes = sizeof(float2) * (size_t)pair_volume_elems(n) * n_vol;
+        const bool want = pairs_mode == 2 || (pairs_mode == 1 && nw >= 4 * (long long)n_vol);
+        if (want && pair_bytes <= kMaxPairBytes) {
+            // inside one align_group the coarse and fine passes share the copy
+            const bool have = pairs_hold_ && pairs_src_ == vols && pairs_nvol_ == n_vol && pairs_stride_ == vol_stride;
+            if (!have) {
+                vol_pairs.reserve(pair_bytes);
+                launch_pair_volumes(vols, vol_stride, n_vol, n, vol_pairs.as<float2>(), stream);
+                ++timer.launches;
+                pairs_src_ = pairs_hold_ ? vols : nullptr;
+                pairs_nvol_ = n_vol;
+                pairs_stride_ = vol_stride;
+            }
             pairs = vol_pairs.as<float2>();
         }
         if (launch_expand_factored(fx, vols, vol_stride, win_vol.as<int>(), win_shift.as<int>(), nw, coef.as<float>(),

@@ -182,6 +182,12 @@ public:
     // work buffers
     DevBuf B_hi, B_lo, col_scale, coef, win_vol, win_shift, vol_scale, norms;
     DevBuf vol_pairs;  // x-paired particle volumes for the expansion gathers (many windows per volume)
+    int pairs_mode = 1;                 // 0 off, 1 auto (>= 4 windows per volume), 2 always
+    static constexpr size_t kMaxPairBytes = size_t(8) << 30;  // larger batches gather directly
+    bool pairs_hold_ = false;           // inside align_group: vol_pairs may be reused for pairs_src_
+    const float* pairs_src_ = nullptr;
+    int pairs_nvol_ = 0;
+    long long pairs_stride_ = 0;
 
     // expansion of `count` windows (volume index + integer shift) of volumes
     // already on the device; real-packed FP32 coefficients into ctx.coef
@@ -227,6 +233,9 @@ public:
     DevBuf staged_;
     const float* staged_src_ = nullptr;
     int staged_count_ = 0;
+    bool staged_valid_ = false;  // staged_ holds staged_src_'s bytes (set by a completed align_batch)
+    bool stage_reuse_ = false;   // caller opt-in: bm_context_set_stage_reuse
+    std::vector<ParticleResult> align_batch_impl(const float* particles, int count, const AlignConfig& cfg);
     std::vector<ParticleResult> align_batch_lane(const float* particles, int count, const AlignConfig& cfg);
     // concurrent lanes: sub-contexts with their own stream and buffers that align
     // slices of a large batch from their own host threads (overlapping the

@@ -353,7 +353,7 @@ __global__ void __launch_bounds__(kThreads, BMB_EXPAND_MINB) expand_factored_ker
 template <int HALF, int RPT, int NPC = 0>
 int launch_t(const FactoredTables& T, size_t smem, const float* vols, long long vol_stride, const int* win_vol,
              const int* win_shift, int n_win, float* out, int ldo, cudaStream_t s, const float2* pairs) {
-    ensure_dynamic_smem(expand_factored_kernel<HALF, RPT, NPC>, (int)smem);
+    if (ensure_dynamic_smem(expand_factored_kernel<HALF, RPT, NPC>, (int)smem) != cudaSuccess) return 2;
     expand_factored_kernel<HALF, RPT, NPC><<<n_win, kThreads, smem, s>>>(T, vols, vol_stride, win_vol, win_shift, out,
                                                                          ldo, pairs);
     return cudaGetLastError() == cudaSuccess ? 0 : 2;

@@ -1716,7 +1716,7 @@ int launch_build_xi(const XiArgs& a, cudaStream_t s) {
     if (a.n <= 0) return 0;
     const size_t smem = sizeof(float) * 2 * (size_t)((a.nf + 3) & ~3);
     if (a.nf > 0 && smem <= 200 * 1024) {
-        ensure_dynamic_smem(build_xi_staged_kernel, (int)smem);
+        if (ensure_dynamic_smem(build_xi_staged_kernel, (int)smem) != cudaSuccess) return 2;
         build_xi_staged_kernel<<<a.n, 256, smem, s>>>(a);
         return cudaGetLastError() == cudaSuccess ? 0 : 2;
     }

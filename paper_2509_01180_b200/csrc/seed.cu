@@ -216,7 +216,7 @@ int launch_seed(const SeedArgs& a, int n_win, cudaStream_t s) {
     if (a.ng > 64) return 1;  // b[k][m] staging holds up to 64 gamma points
     const size_t smem = seed_smem_bytes(a);
     if (smem > 200 * 1024) return 1;
-    ensure_dynamic_smem(seed_kernel, (int)smem);
+    if (ensure_dynamic_smem(seed_kernel, (int)smem) != cudaSuccess) return 2;
     if (!seed_needs_scratch(a)) {
         seed_kernel<<<n_win, 256, smem, s>>>(a);
     } else {  // xi in global scratch: a.scratch_windows windows per launch

@@ -246,3 +246,33 @@ def test_host_particles_match_device(cuda_device):
         assert a["shift"] == b["shift"] and list(a["quat"]) == list(b["quat"]) and a["score"] == b["score"]
     # (the FP64 numerator is summed with atomics: order-dependent in the last bits)
     assert torch.allclose(avg_d, avg_h, rtol=1e-12, atol=1e-12)
+
+
+def test_refilled_host_buffer_is_restaged(cuda_device):
+    """A host buffer refilled between align_batch and average_accumulate is staged
+    again (reuse is opt-in and use-once), so the average is built from the new bytes."""
+    import math
+
+    import torch
+
+    n, L = 32, 8
+    tmpl = api.make_template(n, 20, 5)
+    parts, _, _ = api.make_particles(tmpl, 6, 900, 2, 0.5, None)
+    other, _, _ = api.make_particles(tmpl, 6, 950, 2, 0.5, None)
+    cfg = api.make_config(bands=(8,), max_candidates=4, shift_radius=2, shift_step=2)
+    ctx = api.Context(n, L, L * math.pi)
+    ctx.set_template(tmpl, 0.0)
+    ctx.set_lanes(1, 1)
+    host = parts.cpu().pin_memory()
+    res = ctx.align_batch(host, cfg)
+    want = ctx.average_accumulate(other, res)          # device reference on the new bytes
+    host.copy_(other.cpu())                            # refill the same pinned buffer
+    got = ctx.average_accumulate(host, res)
+    assert torch.allclose(got, want, rtol=1e-12, atol=1e-12)
+    # opt-in reuse serves exactly one average of an unmodified buffer
+    ctx.set_stage_reuse(True)
+    host.copy_(parts.cpu())
+    res = ctx.align_batch(host, cfg)
+    a1 = ctx.average_accumulate(host, res)
+    a2 = ctx.average_accumulate(host, res)
+    assert torch.allclose(a1, a2, rtol=1e-12, atol=1e-12)
