@@ -13,7 +13,7 @@
 extern "C" {
 #endif
 
-#define BM_ABI_VERSION 2
+#define BM_ABI_VERSION 3
 
 enum bm_status {
     BM_OK = 0,
@@ -60,13 +60,6 @@ int bm_context_set_expand_mode(bm_context* ctx, int mode);
  * stream with its own buffers and host thread (default 4 lanes, 64 particles per
  * lane).  Results do not depend on the lane count. */
 int bm_context_set_lanes(bm_context* ctx, int lanes, int min_per_lane);
-/* Refinement schedule of bm_align_batch (refine(), src/optimize.cpp:255-357):
- * 0 = list-driven kernels (default: every phase of a Newton iteration is one
- * launch over all candidates of all windows of the stage), 1 = fused per-window
- * kernel (one persistent launch per stage: window kernels in shared memory, each
- * warp iterating its own candidates; measured 4x slower).  Both
- * run the same per-candidate arithmetic; outcomes are bit-identical. */
-int bm_context_set_refine_mode(bm_context* ctx, int mode);
 /* Expansion gathers of the factored mode: 0 = direct loads, 1 = from an
  * x-paired copy of each volume when it has >= 4 windows (default; the shift
  * search), 2 = always from the copy.  The coefficients are bit-identical. */

@@ -115,8 +115,6 @@ def _declare(L: C.CDLL) -> None:
     L.bm_context_eval_counts.restype = I
     L.bm_context_band_timings.argtypes = [P, P]
     L.bm_context_band_timings.restype = I
-    L.bm_context_set_refine_mode.argtypes = [P, I]
-    L.bm_context_set_refine_mode.restype = I
     L.bm_context_set_expand_mode.argtypes = [P, I]
     L.bm_context_set_expand_mode.restype = I
     L.bm_context_set_expand_pairs.argtypes = [P, I]

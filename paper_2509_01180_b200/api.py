@@ -305,12 +305,6 @@ class Context:
         """Concurrent lanes of align_batch (default 4 lanes of >= 64 particles)."""
         _lib.check(_lib.lib().bm_context_set_lanes(self._h, lanes, min_per_lane), "set_lanes")
 
-    def set_refine_mode(self, mode: str):
-        """'lists' (default: list-driven kernels per Newton phase) or 'fused' (one
-        persistent per-window kernel per stage).  Outcomes are bit-identical."""
-        _lib.check(_lib.lib().bm_context_set_refine_mode(self._h, {"lists": 0, "fused": 1}[mode]),
-                   "set_refine_mode")
-
     def set_expand_mode(self, mode: str):
         """'factored' (default) or 'gemm' (dense operator on the tensor cores)."""
         _lib.check(_lib.lib().bm_context_set_expand_mode(self._h, {"factored": 0, "gemm": 1}[mode]),

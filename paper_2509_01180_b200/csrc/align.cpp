@@ -72,6 +72,7 @@ BandTables BandDev::view() const {
     t.out_pos = out_pos.as<int>();
     t.at_desc = at_desc.as<int2>();
     t.wedge = has_wedge ? wedge.as<float4>() : nullptr;
+    t.wedge_side = has_wedge ? wedge_side.as<float4>() : nullptr;
     return t;
 }
 
@@ -82,7 +83,9 @@ BandDev& Context::band(int L) {
         if (wedge_active() && !b.has_wedge) {
             BandTablesHost h = build_band_tables(L);
             upload(b.wedge, wedge_band_entries(h, chi_hat, q_hat, wp_total), stream);
+            upload(b.wedge_side, wedge_band_entries(h, chi_hat, q_side, wp_total), stream);
             b.has_wedge = true;
+            ck(cudaStreamSynchronize(stream), "band wedge tables");
         }
         return b;
     }
@@ -111,6 +114,7 @@ BandDev& Context::band(int L) {
     upload(b->row_group, rg, stream);
     if (wedge_active()) {
         upload(b->wedge, wedge_band_entries(h, chi_hat, q_hat, wp_total), stream);
+        upload(b->wedge_side, wedge_band_entries(h, chi_hat, q_side, wp_total), stream);
         b->has_wedge = true;
     }
     ck(cudaStreamSynchronize(stream), "band tables");
@@ -218,15 +222,8 @@ void Context::set_template(const float* tmpl, double wedge_theta) {
         chi_hat = std::move(f.chi_hat);
         q_hat = std::move(f.q_hat);
         wp_total = f.total;
-        std::vector<double2> cd(chi_hat.size()), qd(q_hat.size());
-        for (size_t i = 0; i < cd.size(); ++i) {
-            cd[i] = double2{chi_hat[i].real(), chi_hat[i].imag()};
-            qd[i] = double2{q_hat[i].real(), q_hat[i].imag()};
-        }
-        upload(chi_dev, cd, stream);
-        upload(q_dev, qd, stream);
-        ck(cudaStreamSynchronize(stream), "wedge factors");
     }
+    build_side_template();
     // band tables carry the wedge entries of this template: rebuild lazily
     bands_.clear();
     seeds_.clear();
@@ -239,194 +236,155 @@ void Context::set_template(const float* tmpl, double wedge_theta) {
     lanes_stale_ = true;
 }
 
+// Template side of the side kernels (refine.cu chart_transform): t' = D(K^-1) t
+// (rotate_expansion) and q' = D(K^-1) q, K = ZYZ(0, pi/2, 0), in FP64 on the host.
+void Context::build_side_template() {
+    const Euler3 e = q_euler(q_inv(q_from_euler(0.0, kPiH / 2.0, 0.0)));
+    const std::vector<std::complex<double>> D = wigner_D_blocks(basis.l_max, e.a, e.b, e.g);
+    std::vector<float> t(geo.m_pad, 0.0f);
+    ck(cudaMemcpyAsync(t.data(), t_hat.p, sizeof(float) * geo.m_pad, cudaMemcpyDeviceToHost, stream), "t_hat");
+    ck(cudaStreamSynchronize(stream), "t_hat");
+    upload(t_side, rotate_real_packed(t, basis, D), stream);
+    q_side.clear();
+    if (!q_hat.empty()) q_side = rotate_tri(q_hat, basis.l_max, D);
+    ck(cudaStreamSynchronize(stream), "side template");
+}
+
 // Bulk-synchronous damped Newton over every candidate of every window
 // (refine(), src/optimize.cpp:255-357), band by band; windows are processed in
-// chunks so the anchored-chart kernel pool stays bounded.
+// chunks so the window + side kernels of a chunk stay within a memory budget.
 void Context::refine_windows(int nw, int maxc, const AlignConfig& cfg, const Quat& koff, long long grid_evals) {
     work_.reserve(sizeof(CandWork) * (size_t)nw * maxc);
     counters_.reserve(sizeof(int) * 8);
-    int* d_counts = counters_.as<int>();  // CNT_L2, CNT_COMP, CNT_T0, CNT_T1
-    int* d_pool = d_counts + 4;
-    int* d_over = d_counts + 5;
+    int* d_counts = counters_.as<int>();  // CNT_L2, -, CNT_T0, CNT_T1, -, -, start counts
     int* h_active = pinned_counts();
     const bool wedge = wedge_active();
-    // window kernels of the largest band plus one anchored-chart slot per seeded
-    // candidate (correlation + wedge kernel) share a memory budget; chunk
-    // boundaries follow the actual per-window candidate counts
     const int Lmax_band = cfg.bands.back();
     BandDev& btop = band(Lmax_band);
     const size_t kernel_bytes = sizeof(float4) * (size_t)btop.rows * 32;
-    const size_t slot_bytes = kernel_bytes * (wedge ? 2 : 1);
-    std::vector<int> ncand(nw);
-    ck(cudaMemcpyAsync(ncand.data(), cand_count_.p, sizeof(int) * nw, cudaMemcpyDeviceToHost, stream), "cand counts");
-    ck(cudaStreamSynchronize(stream), "cand counts");
-    std::vector<std::pair<int, int>> chunks;  // (first window, windows)
-    {
-        int w0 = 0;
-        size_t bytes = 0;
-        for (int w = 0; w < nw; ++w) {
-            const size_t need = kernel_bytes + slot_bytes * (size_t)ncand[w];
-            if (w > w0 && bytes + need > pool_budget_) {
-                chunks.push_back({w0, w - w0});
-                w0 = w;
-                bytes = 0;
-            }
-            bytes += need;
-        }
-        if (nw > w0) chunks.push_back({w0, nw - w0});
-    }
-    for (const auto& ch : chunks) {
-        const long long w0 = ch.first;
-        const int cnt = ch.second;
-        long long chunk_cands = 0;
-        for (int w = 0; w < cnt; ++w) chunk_cands += ncand[w0 + w];
-        {
-            ck(cudaMemsetAsync(d_over, 0, sizeof(int), stream), "overflow");
-            for (size_t bi = 0; bi < cfg.bands.size(); ++bi) {
-                const int L = cfg.bands[bi];
-                BandDev& bd = band(L);
-                const size_t len = (size_t)bd.rows * 32;
-                StageArgs a;
-                a.T = bd.view();
-                a.row_group = bd.row_group.as<int>();
-                // window kernels of this band
-                xi_win_.reserve(sizeof(float4) * len * cnt);
-                XiArgs xa;
-                xa.T = a.T;
-                xa.row_group = a.row_group;
-                xa.f = coef.as<float>() + (size_t)w0 * geo.m_pad;
-                xa.ldf = geo.m_pad;
-                xa.t = t_hat.as<float>();
-                xa.ldt = 0;
-                xa.block_off = geo.block_off;
-                xa.radial_count = geo.radial_count;
-                xa.n = cnt;
-                xa.out = xi_win_.as<float4>();
-                xa.nf = L < basis.l_max ? basis.block_off[L + 1] : geo.coeffs;
-                cudaEvent_t r0 = timer.begin(stream);
-                cudaEvent_t rb = timer.begin(stream);
-                timer.band = (int)bi;
-                cudaEvent_t x0 = timer.begin(stream);
-                if (launch_build_xi(xa, stream) != 0) throw std::runtime_error("build_xi launch failed");
-                timer.end(K_XI, x0, stream);
+    const int per_chunk = (int)std::max<size_t>(1, pool_budget_ / (2 * kernel_bytes));
+    for (int w0 = 0; w0 < nw; w0 += per_chunk) {
+        const int cnt = std::min(per_chunk, nw - w0);
+        for (size_t bi = 0; bi < cfg.bands.size(); ++bi) {
+            const int L = cfg.bands[bi];
+            BandDev& bd = band(L);
+            const size_t len = (size_t)bd.rows * 32;
+            StageArgs a;
+            a.T = bd.view();
+            a.row_group = bd.row_group.as<int>();
+            // window kernels xi(f, t) and side kernels xi(f, D(K^-1) t) of this band
+            xi_win_.reserve(sizeof(float4) * len * cnt);
+            xi_side_.reserve(sizeof(float4) * len * cnt);
+            XiArgs xa;
+            xa.T = a.T;
+            xa.row_group = a.row_group;
+            xa.f = coef.as<float>() + (size_t)w0 * geo.m_pad;
+            xa.ldf = geo.m_pad;
+            xa.t = t_hat.as<float>();
+            xa.ldt = 0;
+            xa.block_off = geo.block_off;
+            xa.radial_count = geo.radial_count;
+            xa.n = cnt;
+            xa.out = xi_win_.as<float4>();
+            xa.nf = L < basis.l_max ? basis.block_off[L + 1] : geo.coeffs;
+            cudaEvent_t r0 = timer.begin(stream);
+            cudaEvent_t rb = timer.begin(stream);
+            timer.band = (int)bi;
+            cudaEvent_t x0 = timer.begin(stream);
+            if (launch_build_xi(xa, stream) != 0) throw std::runtime_error("build_xi launch failed");
+            xa.t = t_side.as<float>();
+            xa.out = xi_side_.as<float4>();
+            if (launch_build_xi(xa, stream) != 0) throw std::runtime_error("build_xi launch failed");
+            timer.end(K_XI, x0, stream);
+            timer.launches += 2;
+            a.xi_win = xi_win_.as<float4>();
+            a.xi_side = xi_side_.as<float4>();
+            a.cand = cand_.as<CandState>() + (size_t)w0 * maxc;
+            a.work = work_.as<CandWork>() + (size_t)w0 * maxc;
+            a.cand_count = cand_count_.as<int>() + w0;
+            a.max_cand = maxc;
+            a.n_win = cnt;
+            a.prm.band = L;
+            a.prm.newton_max_iter = cfg.newton_max_iter;
+            a.prm.grad_tol = cfg.grad_tol;
+            a.prm.accept_tol = cfg.accept_tol;
+            a.prm.step_damping = cfg.step_damping;
+            a.prm.koffset[0] = koff.w;
+            a.prm.koffset[1] = koff.x;
+            a.prm.koffset[2] = koff.y;
+            a.prm.koffset[3] = koff.z;
+            a.prm.max_cand = maxc;
+            a.prm.has_wedge = wedge ? 1 : 0;
+            const long long slots = (long long)cnt * maxc;
+            lists_.reserve(sizeof(int) * 5 * (size_t)slots);
+            a.list2 = lists_.as<int>();
+            int* lt0 = a.list2 + slots;
+            int* lt1 = lt0 + slots;
+            int* ls[2] = {lt1 + slots, lt1 + 2 * slots};  // start lists (this / next iteration)
+            int* d_start = d_counts + 6;                    // their counts
+            a.counts = d_counts;
+            a.eval_stats = eval_stats();
+            ck(cudaMemsetAsync(d_start, 0, sizeof(int) * 2, stream), "start counts");
+            launch_band_begin(a, ls[0], d_start, stream);
+            int cur = 0;
+            long long start_max = slots;
+            ++timer.launches;
+            for (int it = 0; it < cfg.newton_max_iter; ++it) {
+                ck(cudaMemsetAsync(d_counts, 0, sizeof(int) * 4, stream), "counts");
+                cudaEvent_t n2e = timer.begin(stream);
+                ck(cudaMemsetAsync(d_start + (cur ^ 1), 0, sizeof(int), stream), "next start count");
+                launch_iter_begin(a, ls[cur], d_start + cur, (int)std::max<long long>(1, start_max), stream);
+                timer.end(K_NEWTON, n2e, stream);
                 ++timer.launches;
-                a.xi_win = xi_win_.as<float4>();
-                a.pool = (int)std::max<long long>(1, chunk_cands);  // a slot for every candidate: no overflow
-                xi_pool_.reserve(sizeof(float4) * len * a.pool);
-                a.xi_pool = xi_pool_.as<float4>();
-                if (wedge) {
-                    w_pool_.reserve(sizeof(float4) * len * a.pool);
-                    a.w_pool = w_pool_.as<float4>();
-                    a.chi_hat = chi_dev.as<double2>();
-                    a.q_hat = q_dev.as<double2>();
-                    a.wp_total = wp_total;
-                }
-                a.pool_counter = d_pool;
-                a.overflow = d_over;
-                a.cand = cand_.as<CandState>() + (size_t)w0 * maxc;
-                a.work = work_.as<CandWork>() + (size_t)w0 * maxc;
-                a.cand_count = cand_count_.as<int>() + w0;
-                a.max_cand = maxc;
-                a.n_win = cnt;
-                a.prm.band = L;
-                a.prm.newton_max_iter = cfg.newton_max_iter;
-                a.prm.grad_tol = cfg.grad_tol;
-                a.prm.accept_tol = cfg.accept_tol;
-                a.prm.step_damping = cfg.step_damping;
-                a.prm.koffset[0] = koff.w;
-                a.prm.koffset[1] = koff.x;
-                a.prm.koffset[2] = koff.y;
-                a.prm.koffset[3] = koff.z;
-                a.prm.max_cand = maxc;
-                a.prm.has_wedge = wedge ? 1 : 0;
-                a.compose_smem = compose_smem_bytes(L) <= 200 * 1024 ? 1 : 0;
-                a.scratch_per_warp = compose_scratch_floats(L);
-                const long long slots = (long long)cnt * maxc;
-                lists_.reserve(sizeof(int) * 6 * (size_t)slots);
-                a.list2 = lists_.as<int>();
-                a.listc = a.list2 + slots;
-                int* lt0 = a.listc + slots;
-                int* lt1 = lt0 + slots;
-                int* ls[2] = {lt1 + slots, lt1 + 2 * slots};  // start lists (this / next iteration)
-                int* d_start = d_counts + 6;                    // their counts
-                a.counts = d_counts;
-                a.eval_stats = eval_stats();
-                ck(cudaMemsetAsync(d_pool, 0, sizeof(int), stream), "pool");
-                ck(cudaMemsetAsync(d_start, 0, sizeof(int) * 2, stream), "start counts");
-                launch_band_begin(a, ls[0], d_start, stream);
-                int cur = 0;
-                long long start_max = slots;
-                ++timer.launches;
-                for (int it = 0; it < cfg.newton_max_iter; ++it) {
-                    ck(cudaMemsetAsync(d_counts, 0, sizeof(int) * 4, stream), "counts");
-                    cudaEvent_t n2e = timer.begin(stream);
-                    ck(cudaMemsetAsync(d_start + (cur ^ 1), 0, sizeof(int), stream), "next start count");
-                    launch_iter_begin(a, ls[cur], d_start + cur, (int)std::max<long long>(1, start_max), stream);
-                    timer.end(K_NEWTON, n2e, stream);
-                    ++timer.launches;
-                    ck(cudaMemcpyAsync(h_active, d_counts, sizeof(int) * 2, cudaMemcpyDeviceToHost, stream),
-                       "active");
-                    ck(cudaStreamSynchronize(stream), "iteration");
-                    const int n2 = h_active[0], nc = h_active[1];
-                    if (debug_iters_) fprintf(stderr, "[refine] band %d iter %d active %d compose %d\n", L, it, n2, nc);
-                    if (n2 == 0) break;
-                    if (nc > 0) {
-                        if (!a.compose_smem)
-                            scratch_.reserve(sizeof(float) * (size_t)std::min(nc, 4096) * a.scratch_per_warp);
-                        a.scratch = scratch_.as<float>();
-                        cudaEvent_t c0 = timer.begin(stream);
-                        launch_compose(a, a.compose_smem ? nc : std::min(nc, 4096), stream);
-                        timer.end(K_COMPOSE, c0, stream);
-                        ++timer.launches;
-                    }
-                    cudaEvent_t e2 = timer.begin(stream);
-                    launch_eval(a, 2, a.list2, d_counts + CNT_L2, n2, stream);
-                    timer.end(K_EVAL2, e2, stream);
-                    cudaEvent_t n0 = timer.begin(stream);
-                    launch_step(a, lt0, d_counts + CNT_T0, n2, stream);
-                    timer.end(K_NEWTON, n0, stream);
+                ck(cudaMemcpyAsync(h_active, d_counts, sizeof(int), cudaMemcpyDeviceToHost, stream), "active");
+                ck(cudaStreamSynchronize(stream), "iteration");
+                const int n2 = h_active[0];
+                if (debug_iters_) fprintf(stderr, "[refine] band %d iter %d active %d\n", L, it, n2);
+                if (n2 == 0) break;
+                cudaEvent_t e2 = timer.begin(stream);
+                launch_eval(a, 2, a.list2, d_counts + CNT_L2, n2, stream);
+                timer.end(K_EVAL2, e2, stream);
+                cudaEvent_t n0 = timer.begin(stream);
+                launch_step(a, lt0, d_counts + CNT_T0, n2, stream);
+                timer.end(K_NEWTON, n0, stream);
+                timer.launches += 2;
+                for (int r = 0; r < 3; ++r) {
+                    int* src = (r & 1) ? lt1 : lt0;
+                    int* dst = (r & 1) ? lt0 : lt1;
+                    int* csrc = d_counts + ((r & 1) ? CNT_T1 : CNT_T0);
+                    int* cdst = d_counts + ((r & 1) ? CNT_T0 : CNT_T1);
+                    cudaEvent_t e0 = timer.begin(stream);
+                    launch_eval(a, 0, src, csrc, n2, stream);
+                    timer.end(K_EVAL0, e0, stream);
+                    ck(cudaMemsetAsync(cdst, 0, sizeof(int), stream), "retry count");
+                    cudaEvent_t n1 = timer.begin(stream);
+                    launch_accept(a, src, csrc, dst, cdst, ls[cur ^ 1], d_start + (cur ^ 1), n2, stream);
+                    timer.end(K_NEWTON, n1, stream);
                     timer.launches += 2;
-                    for (int r = 0; r < 3; ++r) {
-                        int* src = (r & 1) ? lt1 : lt0;
-                        int* dst = (r & 1) ? lt0 : lt1;
-                        int* csrc = d_counts + ((r & 1) ? CNT_T1 : CNT_T0);
-                        int* cdst = d_counts + ((r & 1) ? CNT_T0 : CNT_T1);
-                        cudaEvent_t e0 = timer.begin(stream);
-                        launch_eval(a, 0, src, csrc, n2, stream);
-                        timer.end(K_EVAL0, e0, stream);
-                        ck(cudaMemsetAsync(cdst, 0, sizeof(int), stream), "retry count");
-                        cudaEvent_t n1 = timer.begin(stream);
-                        launch_accept(a, src, csrc, dst, cdst, ls[cur ^ 1], d_start + (cur ^ 1), n2, stream);
-                        timer.end(K_NEWTON, n1, stream);
-                        timer.launches += 2;
-                    }
-                    cur ^= 1;
-                    start_max = n2;  // accepted trials <= evaluated candidates
                 }
-                const bool prune_now = cfg.prune_after_band && cfg.bands.size() > 1 && bi == 0;
-                if (bi + 1 == cfg.bands.size() || prune_now) {
-                    // final unanchored score at the top band (optimize.cpp:349-352), or at
-                    // the first band before prune_after_band keeps each window's winner
-                    ck(cudaMemsetAsync(d_counts, 0, sizeof(int), stream), "final count");
-                    launch_final_prep(a, stream);
-                    cudaEvent_t ef = timer.begin(stream);
-                    launch_eval(a, 0, a.list2, d_counts + CNT_L2, (int)slots, stream);
-                    timer.end(K_EVAL0, ef, stream);
-                    launch_final_score(a, (int)slots, stream);
-                    timer.launches += 3;
-                    if (prune_now) {
-                        launch_prune(a, stream);
-                        ++timer.launches;
-                    }
-                }
-                ++timer.refine_launches;
-                timer.band = -1;
-                timer.end(K_REFINE, r0, stream);
-                timer.end(K_REFINE_B0 + (int)std::min<size_t>(bi, 3), rb, stream);
+                cur ^= 1;
+                start_max = n2;  // accepted trials <= evaluated candidates
             }
-            ck(cudaMemcpyAsync(h_active + 1, d_over, sizeof(int), cudaMemcpyDeviceToHost, stream), "overflow");
-            ck(cudaStreamSynchronize(stream), "chunk");
-            if (h_active[1] != 0) throw std::logic_error("refine: anchored-chart pool overflow");
+            const bool prune_now = cfg.prune_after_band && cfg.bands.size() > 1 && bi == 0;
+            if (bi + 1 == cfg.bands.size() || prune_now) {
+                // final unanchored score at the top band (optimize.cpp:349-352), or at
+                // the first band before prune_after_band keeps each window's winner
+                ck(cudaMemsetAsync(d_counts, 0, sizeof(int), stream), "final count");
+                launch_final_prep(a, stream);
+                cudaEvent_t ef = timer.begin(stream);
+                launch_eval(a, 0, a.list2, d_counts + CNT_L2, (int)slots, stream);
+                timer.end(K_EVAL0, ef, stream);
+                launch_final_score(a, (int)slots, stream);
+                timer.launches += 3;
+                if (prune_now) {
+                    launch_prune(a, stream);
+                    ++timer.launches;
+                }
+            }
+            ++timer.refine_launches;
+            timer.band = -1;
+            timer.end(K_REFINE, r0, stream);
+            timer.end(K_REFINE_B0 + (int)std::min<size_t>(bi, 3), rb, stream);
         }
         ReduceArgs ra;
         ra.cand = cand_.as<CandState>() + (size_t)w0 * maxc;
@@ -443,90 +401,6 @@ void Context::refine_windows(int nw, int maxc, const AlignConfig& cfg, const Qua
         launch_window_reduce(ra, stream);
         ++timer.launches;
     }
-}
-
-// Fused refinement (refine_fused_kernel): one launch per stage, persistent CTAs
-// pulling windows from a counter; false if the configuration does not fit it.
-bool Context::refine_windows_fused(int nw, int maxc, const AlignConfig& cfg, const Quat& koff, long long grid_evals) {
-    const bool wedge = wedge_active();
-    FusedArgs fa;
-    if ((int)cfg.bands.size() > kFusedMaxBands || maxc > kFusedMaxCand) return false;
-    fa.n_bands = (int)cfg.bands.size();
-    fa.prune_band0 = (cfg.prune_after_band && cfg.bands.size() > 1) ? 1 : 0;
-    int rows_max = 0;
-    work_.reserve(sizeof(CandWork) * (size_t)nw * maxc);
-    for (int bi = 0; bi < fa.n_bands; ++bi) {
-        const int L = cfg.bands[bi];
-        BandDev& bd = band(L);
-        rows_max = std::max(rows_max, bd.rows);
-        StageArgs& a = fa.st[bi];
-        a.T = bd.view();
-        a.row_group = bd.row_group.as<int>();
-        if (wedge) {
-            a.chi_hat = chi_dev.as<double2>();
-            a.q_hat = q_dev.as<double2>();
-            a.wp_total = wp_total;
-        }
-        a.cand = cand_.as<CandState>();
-        a.work = work_.as<CandWork>();
-        a.cand_count = cand_count_.as<int>();
-        a.max_cand = maxc;
-        a.n_win = nw;
-        a.prm.band = L;
-        a.prm.newton_max_iter = cfg.newton_max_iter;
-        a.prm.grad_tol = cfg.grad_tol;
-        a.prm.accept_tol = cfg.accept_tol;
-        a.prm.step_damping = cfg.step_damping;
-        a.prm.koffset[0] = koff.w;
-        a.prm.koffset[1] = koff.x;
-        a.prm.koffset[2] = koff.y;
-        a.prm.koffset[3] = koff.z;
-        a.prm.max_cand = maxc;
-        a.prm.has_wedge = wedge ? 1 : 0;
-        a.eval_stats = eval_stats();
-    }
-    fa.coef = coef.as<float>();
-    fa.ldf = geo.m_pad;
-    fa.t_hat = t_hat.as<float>();
-    fa.block_off = geo.block_off;
-    fa.radial_count = geo.radial_count;
-    fa.slot_len = (long long)rows_max * 32;
-    fa.smem_len = rows_max * 32;
-    fa.scratch_floats = compose_scratch_floats(cfg.bands.back());
-    const int grid = fused_refine_grid(fa, wedge);
-    if (grid <= 0) return false;
-    const size_t slots = (size_t)grid * maxc;
-    xi_pool_.reserve(sizeof(float4) * slots * fa.slot_len);
-    fa.xi_pool = xi_pool_.as<float4>();
-    if (wedge) {
-        w_pool_.reserve(sizeof(float4) * slots * fa.slot_len);
-        fa.w_pool = w_pool_.as<float4>();
-    }
-    scratch_.reserve(sizeof(float) * (size_t)grid * 4 * fa.scratch_floats);  // per warp
-    fa.scratch = scratch_.as<float>();
-    win_counter_.reserve(sizeof(int));
-    fa.win_counter = win_counter_.as<int>();
-    ck(cudaMemsetAsync(fa.win_counter, 0, sizeof(int), stream), "window counter");
-    cudaEvent_t r0 = timer.begin(stream);
-    if (launch_refine_fused(fa, grid, wedge, stream) != 0) throw std::runtime_error("fused refine launch failed");
-    timer.end(K_REFINE, r0, stream);
-    ++timer.launches;
-    ++timer.refine_launches;
-    ReduceArgs ra;
-    ra.cand = cand_.as<CandState>();
-    ra.cand_count = cand_count_.as<int>();
-    ra.max_cand = maxc;
-    ra.n_win = nw;
-    ra.sub_norm = sub_norm_.as<double>();
-    ra.t_norm = t_norm;
-    ra.win_particle = win_vol.as<int>();
-    ra.win_shift = win_shift.as<int>();
-    ra.grid_evals = grid_evals;
-    ra.extra_candidates = fa.prune_band0;
-    ra.out = outcome_.as<WindowOutcome>();
-    launch_window_reduce(ra, stream);
-    ++timer.launches;
-    return true;
 }
 
 std::vector<WindowOutcome> Context::run_windows(const float* vols, int n_vol, const std::vector<int>& wvol,
@@ -581,8 +455,7 @@ std::vector<WindowOutcome> Context::run_windows(const float* vols, int n_vol, co
 
     const Quat koff = q_from_euler(0.0, kPiH / 2.0, 0.0);
     const long long grid_evals = (long long)sd.na * sd.nb * sd.ng;
-    if (refine_mode != 1 || !refine_windows_fused(nw, maxc, cfg, koff, grid_evals))
-        refine_windows(nw, maxc, cfg, koff, grid_evals);
+    refine_windows(nw, maxc, cfg, koff, grid_evals);
     ck(cudaMemcpyAsync(res.data(), outcome_.p, sizeof(WindowOutcome) * nw, cudaMemcpyDeviceToHost, stream),
        "outcomes");
     ck(cudaStreamSynchronize(stream), "run_windows");
@@ -728,7 +601,6 @@ void Context::ensure_lanes() {
     for (auto& c : lane_ctx_) {
         c->expand_mode = expand_mode;
         c->pairs_mode = pairs_mode;
-        c->refine_mode = refine_mode;
         c->pool_budget_ = pool_budget_;  // each lane allocates only what its slice needs
     }
     // lanes created after set_template (a larger set_lanes) adopt it too
@@ -750,17 +622,9 @@ void Context::adopt_template(const Context& src) {
     chi_hat = src.chi_hat;
     q_hat = src.q_hat;
     wp_total = src.wp_total;
-    if (src.wedge) {
-        wedge = std::make_unique<WedgeFilter>(n, wedge_deg, kWedgeTaperDeg);
-        std::vector<double2> cd(chi_hat.size()), qd(q_hat.size());
-        for (size_t i = 0; i < cd.size(); ++i) {
-            cd[i] = double2{chi_hat[i].real(), chi_hat[i].imag()};
-            qd[i] = double2{q_hat[i].real(), q_hat[i].imag()};
-        }
-        upload(chi_dev, cd, stream);
-        upload(q_dev, qd, stream);
-    }
+    if (src.wedge) wedge = std::make_unique<WedgeFilter>(n, wedge_deg, kWedgeTaperDeg);
     ck(cudaStreamSynchronize(stream), "adopt template");
+    build_side_template();
     bands_.clear();
     seeds_.clear();
     has_template = true;

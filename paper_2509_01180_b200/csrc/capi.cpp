@@ -456,15 +456,6 @@ int bm_context_set_stage_reuse(bm_context* ctx, int on) {
     });
 }
 
-int bm_context_set_refine_mode(bm_context* ctx, int mode) {
-    return guarded("bm_context_set_refine_mode", [&] {
-        if (!ctx) return (int)BM_ERR_STATE;
-        if (mode != 0 && mode != 1) throw std::invalid_argument("refine mode must be 0 (list-driven) or 1 (fused)");
-        ctx->impl->refine_mode = mode;
-        return (int)BM_OK;
-    });
-}
-
 int bm_context_eval_stats(bm_context* ctx, long long* evals, double* flops, int reset) {
     return guarded("bm_context_eval_stats", [&] {
         if (!ctx) return (int)BM_ERR_STATE;

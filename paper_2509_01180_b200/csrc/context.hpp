@@ -63,7 +63,8 @@ struct WedgeFilter;
 struct BandDev {
     int L = 0;
     int n_items = 0, n_groups = 0, rows = 0;
-    DevBuf row_off, item_mm, item_pm, item_w, item_len, bfac, bexp, PQR, item_of, out_pos, at_desc, row_group, wedge;
+    DevBuf row_off, item_mm, item_pm, item_w, item_len, bfac, bexp, PQR, item_of, out_pos, at_desc, row_group, wedge,
+        wedge_side;
     bool has_wedge = false;
     BandTables view() const;
 };
@@ -196,7 +197,6 @@ public:
                         const std::vector<int>& wvol, const std::vector<int>& wshift);
 
     int expand_mode = 0;          // 0: factored expansion (K2f), 1: dense operator GEMM (K1 + K2)
-    int refine_mode = 0;          // 0: list-driven kernels, 1: fused per-window refinement kernel
     bool operator_ready = false;
     void ensure_operator();
     void build_factored_tables();
@@ -208,13 +208,15 @@ public:
 
     // ---------------------------------------------------------- template
     DevBuf t_hat;          // real-packed FP32 template coefficients
+    DevBuf t_side;         // D(K^-1) t_hat: template of the side kernels (refine.cu chart_transform)
+    void build_side_template();
     double t_norm = 0.0;
     bool has_template = false;
     double wedge_deg = 0.0;                // <= 0 or >= 90: no wedge
     std::unique_ptr<WedgeFilter> wedge;    // tapered filter for the particles
     std::vector<std::complex<double>> chi_hat, q_hat;  // wedge power factors
+    std::vector<std::complex<double>> q_side;         // D(K^-1) q_hat (side wedge kernel)
     double wp_total = 0.0;
-    DevBuf chi_dev, q_dev;  // device copies of chi_hat / q_hat
     bool wedge_active() const { return wedge_deg > 0.0 && wedge_deg < 90.0 && wp_total > 0.0; }
     void set_template(const float* tmpl, double wedge_deg);
 
@@ -278,7 +280,7 @@ public:
     // evaluations (order 2, order 0) and their algorithmic FLOPs since the last reset
     void read_eval_stats(long long* evals, double* flops, bool reset);
     void eval_counts(int L, long long* out);  // (order 2, order 0) evaluations at band L
-    // bytes for window kernels + anchored-chart pool per chunk (BMB_POOL_GB overrides)
+    // bytes of window + side kernels per refinement chunk (BMB_POOL_GB overrides)
     size_t pool_budget_ = [] {
         const char* e = std::getenv("BMB_POOL_GB");
         return (e && std::atoi(e) > 0) ? (size_t)std::atoi(e) << 30 : 24ull << 30;
@@ -286,11 +288,10 @@ public:
 
 private:
     void refine_windows(int nw, int maxc, const AlignConfig& cfg, const Quat& koff, long long grid_evals);
-    bool refine_windows_fused(int nw, int maxc, const AlignConfig& cfg, const Quat& koff, long long grid_evals);
-    DevBuf work_, counters_, xi_win_, xi_pool_, w_pool_, lists_;
+    DevBuf work_, counters_, xi_win_, xi_side_, lists_;
     std::map<int, std::unique_ptr<BandDev>> bands_;
     std::map<std::pair<int, long long>, std::unique_ptr<SeedDev>> seeds_;
-    DevBuf cand_, cand_count_, outcome_, win_counter_, scratch_, sub_norm_;
+    DevBuf cand_, cand_count_, outcome_, win_counter_, sub_norm_;
 };
 
 }  // namespace bmb

@@ -33,6 +33,7 @@ struct BandTables {
     const int2* at_desc = nullptr;   // [rows*32] layout position descriptors (tables.hpp)
     const int* out_pos = nullptr;    // [(2L+1)^2] 2 ((row_off[g] - m_item) 32 + lane) + slot: + 64 l = 2 at + slot
     const float4* wedge = nullptr;   // [rows*32] wedge-power kernel entries (A, B) (or null)
+    const float4* wedge_side = nullptr;  // [rows*32] the same composed with D(K^-1)^T (side kernels)
 };
 
 // Per-context constants used by the kernels.

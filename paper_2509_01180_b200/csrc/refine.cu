@@ -452,294 +452,6 @@ __device__ __forceinline__ void wappend(bool pred, int v, int* list, int* count)
     if (pred) list[base + __popc(m & lanemask_lt())] = v;
 }
 
-// ---------------------------------------------------------------- composition
-// xi~_l = xi_l D^l(a)^T  (xi_compose_right, src/xcorr.cpp:149-155), with
-// D^l_{m'n}(a) = e^{-i m' a} d^l_{m'n}(b) e^{-i n g}:
-//   xi~_l[m,m'] = e^{-i m' a} sum_n (xi_l[m,n] e^{-i n g}) d^l_{m'n}(b).
-// The full-plane d^l(b) comes from the same band tables as the evaluation
-// (half-plane chains + d_{-m,-m'} = (-1)^{m-m'} d_{m,m'}); the rows m >= 0 of xi
-// (all the product needs) are unpacked into a dense, phase-folded scratch so
-// the n-sum runs over contiguous rows.  The wedge-power kernel is rank one
-// (conj(chi_lm) q_lm' / total), so its composition only rotates q:
-// q~_l = D^l(a) q_l  (O(l^2) per degree).
-struct ComposeScratch {
-    float2 ua[kMaxL + 1];
-    float2 ug[kMaxL + 1];
-    float cp[2 * kMaxL + 3];
-    float sp[2 * kMaxL + 3];
-    double eul[3];
-};
-
-template <bool WARP>
-__device__ __forceinline__ void group_sync() {
-    if (WARP) __syncwarp();
-    else __syncthreads();
-}
-
-// scratch layout of one composition (floats): full-plane d table, the m >= 0
-// rows of the phase-folded xi, q~, and the staged FP64 wedge factors
-struct ComposeLayout {
-    int dtab, xd, qt, tq, qh, ch, total;
-};
-// offset of degree l in the m >= 0 half rows: sum_{j<l} (j+1)(2j+1)
-__host__ __device__ __forceinline__ int xh_off(int l) { return l * (l - 1) * (2 * l - 1) / 3 + 3 * l * (l - 1) / 2 + l; }
-__host__ __device__ inline ComposeLayout compose_layout(int L) {
-    ComposeLayout c;
-    const int nxi = xi_off(L + 1), ntri = (L + 1) * (L + 2) / 2;
-    int o = 0;
-    c.dtab = o;
-    o += (nxi + 3) & ~3;
-    c.xd = o;
-    o += (2 * xh_off(L + 1) + 3) & ~3;
-    c.qt = o;
-    o += (2 * (L + 1) * (L + 1) + 3) & ~3;
-    c.tq = o;  // q_ln e^{-i n g}, per degree (shared by every output m' of the degree)
-    o += (2 * (L + 1) * (L + 1) + 3) & ~3;
-    c.qh = o;
-    o += 4 * ntri;
-    c.ch = o;
-    o += 4 * ntri;
-    c.total = o;
-    return c;
-}
-
-// Cooperative composition of one candidate's chart kernels (WARP: one warp,
-// the fused refinement; else the whole CTA).  scr: compose_layout(T.L) floats
-// (shared memory when it fits).  Four phases: angles and phase tables (warp 0;
-// the other warps stage the wedge factors), d chains + xi unpack, the product
-// and q~, then the wedge kernel written whole (coalesced).
-template <bool WARP = false>
-__device__ void compose_block(const BandTables& T, const float4* src, const StageArgs& a, const Quat& anchor,
-                              float* scr, float4* out, float4* out_w, ComposeScratch& cs) {
-    const int tid = WARP ? (threadIdx.x & 31) : threadIdx.x, nt = WARP ? 32 : blockDim.x;
-    const int L = T.L;
-    const ComposeLayout lay = compose_layout(L);
-    float* dtab = scr + lay.dtab;
-    float2* xd = reinterpret_cast<float2*>(scr + lay.xd);
-    float2* qt = reinterpret_cast<float2*>(scr + lay.qt);
-    float2* tq = reinterpret_cast<float2*>(scr + lay.tq);
-    double2* qh = reinterpret_cast<double2*>(scr + lay.qh);
-    float2* chf = reinterpret_cast<float2*>(scr + lay.ch);  // conj(chi_lm) as FP32 (cr, ci)
-    const bool wedge = out_w != nullptr;
-    const int ntri = (L + 1) * (L + 2) / 2;
-    if (tid < 32) {
-        // every lane of warp 0 converts the anchor (no serial section)
-        const Euler3 e = q_euler(anchor);
-        if (tid == 0) {
-            cs.eul[0] = e.a;
-            cs.eul[1] = e.b;
-            cs.eul[2] = e.g;
-        }
-        for (int m = tid; m <= L; m += 32) {
-            double sn, co;
-            sincos_d(m * e.a, &sn, &co);
-            cs.ua[m] = make_float2((float)co, (float)-sn);
-            sincos_d(m * e.g, &sn, &co);
-            cs.ug[m] = make_float2((float)co, (float)-sn);
-        }
-        double ch, sh;
-        sincos_d(0.5 * e.b, &sh, &ch);
-        for (int j = tid; j <= 2 * L + 2; j += 32) {
-            double pc = 1.0, ps = 1.0, bc = ch, bs = sh;
-            for (int q = j; q; q >>= 1) {
-                if (q & 1) {
-                    pc *= bc;
-                    ps *= bs;
-                }
-                bc *= bc;
-                bs *= bs;
-            }
-            cs.cp[j] = (float)pc;
-            cs.sp[j] = (float)ps;
-        }
-    }
-    if (wedge)
-        for (int i = (WARP ? tid : tid - 32); i >= 0 && i < ntri; i += (WARP ? 32 : nt - 32)) {
-            qh[i] = a.q_hat[i];
-            const double2 c = a.chi_hat[i];
-            chf[i] = make_float2((float)c.x, (float)-c.y);
-        }
-    group_sync<WARP>();
-    const float cb = (float)cos(cs.eul[1]);
-    // full-plane d^l_{m,m'}(b_a): item chains, their partners, and the mirrors
-    // d_{-m,-m'} = (-1)^(m-m') d_{m,m'}; recursion loads issued 4 steps at a time
-    for (int item = tid; item < T.n_groups * 32; item += nt) {
-        const int len = T.item_len[item];
-        const int m = T.item_mm[item].x, mp = T.item_mm[item].y;
-        const int pa = T.item_pm[item].x, pb = T.item_pm[item].y;
-        const float wb = T.item_w[item].y;
-        const float sg = wb < 0.0f ? -1.0f : 1.0f;
-        const bool pair = wb != 0.0f;
-        const int be = T.bexp[item];
-        float d = T.bfac[item] * cs.cp[be & 0xff] * cs.sp[be >> 8], d1 = 0.0f;
-        const float mir = ((m - mp) & 1) ? -1.0f : 1.0f;
-        const float mirp = ((pa - pb) & 1) ? -1.0f : 1.0f;
-        const int r0 = T.row_off[item >> 5], lane = item & 31;
-        int ob = xi_off(m), w = 2 * m + 1;  // degree block offset and width, advanced per step
-        for (int s0 = 0; s0 < len; s0 += 4) {
-            float4 pq[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-                pq[u] = (s0 + u > 0 && s0 + u < len) ? __ldg(T.PQR + (r0 + s0 + u) * 32 + lane)
-                                                     : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int st = s0 + u;
-                if (st >= len) break;
-                if (st > 0) {
-                    const float4 pqr = pq[u];
-                    const float dn = fmaf(pqr.x, cb, pqr.y) * d - pqr.z * d1;
-                    d1 = d;
-                    d = dn;
-                }
-                const int l = m + st;
-                dtab[ob + (m + l) * w + (mp + l)] = d;
-                dtab[ob + (-m + l) * w + (-mp + l)] = mir * d;
-                if (pair) {
-                    dtab[ob + (pa + l) * w + (pb + l)] = sg * d;
-                    dtab[ob + (-pa + l) * w + (-pb + l)] = mirp * sg * d;
-                }
-                ob += w * w;  // block of degree l + 1 (xi_off(l + 1))
-                w += 2;
-            }
-        }
-    }
-    // rows m >= 0 of xi'_l[m,n] = xi_l[m,n] e^{-i n g}: the A and B entries of
-    // every (row, lane) (first index >= 0), and for m = 0 the conjugate mirror
-    // xi_{0,-n} = (-1)^n conj(xi_{0,n})
-    // (the same pass zeroes the output positions no half-plane entry maps to:
-    // padding lanes, steps past an item's chain, B of self-paired items)
-    for (int at = tid; at < T.rows * 32; at += nt) {
-        const int2 dsc = T.at_desc[at];
-        if (!(dsc.x & 1)) {
-            out[at] = make_float4(0.f, 0.f, 0.f, 0.f);
-            continue;
-        }
-        const bool hasB = (dsc.x & 2) != 0;
-        if (!hasB) reinterpret_cast<float2*>(out)[2 * at + 1] = make_float2(0.f, 0.f);
-        const float4 x4 = src[at];
-        const int l = (dsc.x >> 2) & 63, w = 2 * l + 1, o = xh_off(l);
-#pragma unroll
-        for (int slot = 0; slot < 2; ++slot) {
-            if (slot == 1 && !hasB) break;
-            const int m = slot ? (dsc.y & 255) - 64 : ((dsc.x >> 8) & 255) - 64;
-            const int mp = slot ? ((dsc.y >> 8) & 255) - 64 : ((dsc.x >> 16) & 255) - 64;
-            const float2 x = slot ? make_float2(x4.z, x4.w) : make_float2(x4.x, x4.y);
-            float2 egp = cs.ug[abs(mp)];
-            if (mp < 0) egp.y = -egp.y;
-            xd[o + m * w + (mp + l)] = cmul(x, egp);
-            if (m == 0) {
-                const float sgn = (mp & 1) ? -1.0f : 1.0f;
-                const float2 xm = make_float2(sgn * x.x, -sgn * x.y);  // xi[0,-m']
-                xd[o + (-mp + l)] = cmul(xm, make_float2(egp.x, -egp.y));
-            }
-        }
-    }
-    if (wedge) {  // t_l[n] = q_ln e^{-i n g}
-        int l = 0;
-        for (int idx = tid; idx < (L + 1) * (L + 1); idx += nt) {
-            while ((l + 1) * (l + 1) <= idx) ++l;
-            const int n = idx - l * l - l, an = abs(n);
-            double2 qv = qh[l * (l + 1) / 2 + an];
-            if (n < 0) {
-                const double sgn = (an & 1) ? -1.0 : 1.0;
-                qv = make_double2(sgn * qv.x, -sgn * qv.y);
-            }
-            float2 egn = cs.ug[an];
-            if (n < 0) egn.y = -egn.y;
-            tq[idx] = cmul(make_float2((float)qv.x, (float)qv.y), egn);
-        }
-    }
-    group_sync<WARP>();
-    // q~_l[m'] = e^{-i m' a} sum_n d_{m'n} e^{-i n g} q_ln (rank-one wedge factor)
-    if (wedge) {
-        int l = 0;  // idx increases: resume the degree scan
-        for (int idx = tid; idx < (L + 1) * (L + 1); idx += nt) {
-            while ((l + 1) * (l + 1) <= idx) ++l;
-            const int mp = idx - l * l - l;
-            const int w = 2 * l + 1, o = xi_off(l);
-            float re = 0.0f, im = 0.0f;
-            const float2* tl = tq + l * l + l;
-            for (int n = -l; n <= l; ++n) {
-                const float2 t = tl[n];
-                const float dv = dtab[o + (mp + l) * w + (n + l)];
-                re = fmaf(dv, t.x, re);
-                im = fmaf(dv, t.y, im);
-            }
-            float2 eam = cs.ua[abs(mp)];
-            if (mp < 0) eam.y = -eam.y;
-            qt[idx] = cmul(eam, make_float2(re, im));
-        }
-    }
-    // xi~_l[m,m'] = e^{-i m' a} sum_n X_l[m,n] d^l_{m'n} over the half plane m >= 0,
-    // one task per (l, m, quad of 4 consecutive m'): the X row is loaded once per n
-    // for 4 outputs; results scatter to their (item, slot) of the band layout
-    float2* outp = reinterpret_cast<float2*>(out);
-    int total = 0;
-    for (int l = 0; l <= L; ++l) total += (l + 1) * ((2 * l + 4) / 4);
-    int l = 0, base = 0;  // a thread's tasks increase: resume the degree scan
-    for (int wi = tid; wi < total; wi += nt) {
-        for (;; ++l) {
-            const int nb = (l + 1) * ((2 * l + 4) / 4);
-            if (wi < base + nb) break;
-            base += nb;
-        }
-        const int nq = (2 * l + 4) / 4;
-        const int m = (wi - base) / nq, q0 = -l + 4 * ((wi - base) % nq);
-        const int w = 2 * l + 1, o = xi_off(l);
-        const float2* xrow = xd + xh_off(l) + m * w;
-        const float* drow[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) drow[j] = dtab + o + (min(q0 + j, l) + l) * w;
-        float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
-                         make_float2(0.f, 0.f)};
-        for (int n = 0; n < w; ++n) {
-            const float2 x = xrow[n];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const float dv = drow[j][n];
-                acc[j].x = fmaf(x.x, dv, acc[j].x);
-                acc[j].y = fmaf(x.y, dv, acc[j].y);
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int mp = q0 + j;
-            if (mp > l || (m == 0 && mp < 0)) continue;
-            float2 eam = cs.ua[abs(mp)];
-            if (mp < 0) eam.y = -eam.y;
-            outp[T.out_pos[(m + L) * (2 * L + 1) + (mp + L)] + 64 * l] = cmul(eam, acc[j]);
-        }
-    }
-    if (wedge) {
-        group_sync<WARP>();
-        // wedge kernel conj(chi_lm) q~_lm' / total, every layout position (A, B)
-        const float inv_total = (float)(1.0 / a.wp_total);
-        for (int at = tid; at < T.rows * 32; at += nt) {
-            const int2 dsc = T.at_desc[at];
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (dsc.x & 1) {
-                const int l = (dsc.x >> 2) & 63;
-#pragma unroll
-                for (int slot = 0; slot < 2; ++slot) {
-                    if (slot == 1 && !(dsc.x & 2)) break;
-                    const int m = slot ? (dsc.y & 255) - 64 : ((dsc.x >> 8) & 255) - 64;
-                    const int mp = slot ? ((dsc.y >> 8) & 255) - 64 : ((dsc.x >> 16) & 255) - 64;
-                    const float2 c = chf[l * (l + 1) / 2 + m];
-                    const float cr = c.x, ci = c.y;
-                    const float2 qv = qt[l * l + (mp + l)];
-                    const float2 wv =
-                        make_float2((cr * qv.x - ci * qv.y) * inv_total, (cr * qv.y + ci * qv.x) * inv_total);
-                    if (slot) v.z = wv.x, v.w = wv.y;
-                    else v.x = wv.x, v.y = wv.y;
-                }
-            }
-            out_w[at] = v;
-        }
-    }
-    group_sync<WARP>();
-}
-
 // xi_l[m,m'] = sum_k conj(f_klm) t_klm' from real-packed f and t
 __device__ float2 xi_value(int l, int m, int mp, const float* f, const float* t, const int* block_off,
                            const int* radial_count) {
@@ -822,6 +534,83 @@ __device__ void objective(const double* cr, const double* rr, bool wedge, int or
     }
 }
 
+// Chart derivatives of an anchored candidate without a per-candidate kernel.
+// The reference optimizes C~(e) = C(R(e) a) on the composed kernel
+// xi~ = xi D(a)^T (xi_compose_right, src/xcorr.cpp:149-155; refine(),
+// src/optimize.cpp:268-299).  The same function and its e-derivatives follow
+// from the window's own kernels: the objective is evaluated at the global
+// rotation g = R(e) a, either on the window kernel at Euler angles e' = E(g),
+// or — when g itself is near a pole — on the window's side kernel
+// xi' = xi D(K^-1)^T at e' = E(g K) (K = ZYZ(0, pi/2, 0); g and g K are never
+// both within 45 degrees of a pole).  Derivatives then map to the chart by the
+// chain rule through e -> e'.  With W(e) = [z, Rz(a) y, Rz(a) Ry(b) z] (the
+// space-frame angular velocities of the ZYZ angles, dR/de_i = [w_i]x R), both
+// parametrizations move g with the same angular velocity, so
+//   J = de'/de = W(e')^-1 W(e),
+//   d^2 e'_k / de_i de_j = (W(e')^-1 (dW(e)/de_j - sum_k J_kj dW(e')/de'_k J))_ki,
+//   grad = J^T grad',  H = J^T H' J + sum_k grad'_k d^2 e'_k / de de.
+__device__ void euler_frame(double a, double b, double W[9], double dWa[9], double dWb[9]) {
+    double sa, ca, sb, cb;
+    sincos(a, &sa, &ca);
+    sincos(b, &sb, &cb);
+    // columns: w_alpha = z, w_beta = (-sin a, cos a, 0), w_gamma = (cos a sin b, sin a sin b, cos b)
+    W[0] = 0.0, W[1] = -sa, W[2] = ca * sb;
+    W[3] = 0.0, W[4] = ca, W[5] = sa * sb;
+    W[6] = 1.0, W[7] = 0.0, W[8] = cb;
+    dWa[0] = 0.0, dWa[1] = -ca, dWa[2] = -sa * sb;
+    dWa[3] = 0.0, dWa[4] = -sa, dWa[5] = ca * sb;
+    dWa[6] = 0.0, dWa[7] = 0.0, dWa[8] = 0.0;
+    dWb[0] = 0.0, dWb[1] = 0.0, dWb[2] = ca * cb;
+    dWb[3] = 0.0, dWb[4] = 0.0, dWb[5] = sa * cb;
+    dWb[6] = 0.0, dWb[7] = 0.0, dWb[8] = -sb;
+}
+
+__device__ void mat3_mul(const double* A, const double* B, double* C) {
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) C[3 * i + j] = A[3 * i] * B[j] + A[3 * i + 1] * B[3 + j] + A[3 * i + 2] * B[6 + j];
+}
+
+// f: objective at e' (value, gradient, Hessian in e' = ev); rewritten in place
+// as the derivatives with respect to the chart angles e
+__device__ void chart_transform(Derivs& f, const double* e, const double* ev) {
+    double We[9], dWe_a[9], dWe_b[9], Wp[9], dWp_a[9], dWp_b[9];
+    euler_frame(e[0], e[1], We, dWe_a, dWe_b);
+    euler_frame(ev[0], ev[1], Wp, dWp_a, dWp_b);
+    // W(e')^-1 by the adjugate (det = -sin b' != 0: b' is at least 45 degrees from a pole)
+    double Wi[9];
+    Wi[0] = Wp[4] * Wp[8] - Wp[5] * Wp[7];
+    Wi[1] = Wp[2] * Wp[7] - Wp[1] * Wp[8];
+    Wi[2] = Wp[1] * Wp[5] - Wp[2] * Wp[4];
+    Wi[3] = Wp[5] * Wp[6] - Wp[3] * Wp[8];
+    Wi[4] = Wp[0] * Wp[8] - Wp[2] * Wp[6];
+    Wi[5] = Wp[2] * Wp[3] - Wp[0] * Wp[5];
+    Wi[6] = Wp[3] * Wp[7] - Wp[4] * Wp[6];
+    Wi[7] = Wp[1] * Wp[6] - Wp[0] * Wp[7];
+    Wi[8] = Wp[0] * Wp[4] - Wp[1] * Wp[3];
+    const double det = Wp[0] * Wi[0] + Wp[1] * Wi[3] + Wp[2] * Wi[6];
+    for (int i = 0; i < 9; ++i) Wi[i] /= det;
+    double J[9];
+    mat3_mul(Wi, We, J);
+    double g[3], H[9];
+    for (int i = 0; i < 3; ++i) g[i] = J[i] * f.g[0] + J[3 + i] * f.g[1] + J[6 + i] * f.g[2];
+    double HJ[9];
+    mat3_mul(f.h, J, HJ);
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) H[3 * i + j] = J[i] * HJ[j] + J[3 + i] * HJ[3 + j] + J[6 + i] * HJ[6 + j];
+    const double* dWe[3] = {dWe_a, dWe_b, nullptr};
+    for (int j = 0; j < 3; ++j) {
+        // M = dW(e)/de_j - (J_0j dW(e')/da' + J_1j dW(e')/db') J
+        double T[9], TJ[9], M[9], dJ[9];
+        for (int q = 0; q < 9; ++q) T[q] = J[j] * dWp_a[q] + J[3 + j] * dWp_b[q];
+        mat3_mul(T, J, TJ);
+        for (int q = 0; q < 9; ++q) M[q] = (dWe[j] ? dWe[j][q] : 0.0) - TJ[q];
+        mat3_mul(Wi, M, dJ);  // dJ[k][i] = d^2 e'_k / de_i de_j
+        for (int i = 0; i < 3; ++i) H[3 * i + j] += dJ[i] * f.g[0] + dJ[3 + i] * f.g[1] + dJ[6 + i] * f.g[2];
+    }
+    for (int i = 0; i < 3; ++i) f.g[i] = g[i];
+    for (int q = 0; q < 9; ++q) f.h[q] = H[q];
+}
+
 // damped step from wk.f with wk.lam, trial chart rotation (optimize.cpp:313-328)
 // The trial's order-0 evaluation needs only the objective VALUE, which is smooth
 // through the gimbal pole: an anchored candidate is evaluated at the global trial
@@ -869,8 +658,6 @@ __device__ __forceinline__ bool slot_of(const StageArgs& a, long long idx) {
 // band start of candidate i (slot_of(a, i) holds)
 __device__ __forceinline__ void band_begin_one(const StageArgs& a, long long i) {
     CandWork& wk = a.work[i];
-    wk.slot = -1;
-    wk.compose = 0;
     wk.iter = 0;
     wk.retry = 0;
     wk.status = ST_DONE;
@@ -878,11 +665,10 @@ __device__ __forceinline__ void band_begin_one(const StageArgs& a, long long i) 
     if (!st.active || st.diverged) return;
     wk.lambda = a.prm.step_damping;
     st.band_converged = 0;
-    if (st.anchored && a.prm.band > st.anchor_limit) {  // widen the chart kernel
+    if (st.anchored && a.prm.band > st.anchor_limit) {  // re-anchor at the new band (optimize.cpp:289)
         const Quat koff{a.prm.koffset[0], a.prm.koffset[1], a.prm.koffset[2], a.prm.koffset[3]};
         qstore(st.anchor, q_mul(q_inv(koff), qload(st.g)));
         st.anchor_limit = a.prm.band;
-        wk.compose = 1;
     }
     wk.status = ST_START;
 }
@@ -898,8 +684,6 @@ __global__ void band_begin_kernel(StageArgs a, int* start, int* start_count) {
         if (i < n) {
             if (!slot_of(a, i)) {
                 CandWork& wk = a.work[i];
-                wk.slot = -1;
-                wk.compose = 0;
                 wk.iter = 0;
                 wk.retry = 0;
                 wk.status = ST_DONE;
@@ -912,88 +696,51 @@ __global__ void band_begin_kernel(StageArgs a, int* start, int* start_count) {
     }
 }
 
-// chart / re-anchor decision of every candidate still iterating; appends to
-// the order-2 list and the composition list
-// iteration start of candidate i: bit 0 = evaluate at order 2, bit 1 = (re)build
-// the chart kernel first
-__device__ __forceinline__ int iter_begin_one(const StageArgs& a, long long i) {
+// iteration start of candidate i (chart and re-anchor decision,
+// optimize.cpp:292-298): true = evaluate at order 2.  Anchored candidates pick
+// the kernel and angles of their order-2 evaluation (chart_transform).
+__device__ __forceinline__ bool iter_begin_one(const StageArgs& a, long long i) {
     CandWork& wk = a.work[i];
-    if (wk.status != ST_START) return 0;
+    if (wk.status != ST_START) return false;
     if (wk.iter >= a.prm.newton_max_iter) {
         wk.status = ST_DONE;
-        return 0;
+        return false;
     }
     CandState& st = a.cand[i];
     const Quat g = qload(st.g);
+    const Quat koff{a.prm.koffset[0], a.prm.koffset[1], a.prm.koffset[2], a.prm.koffset[3]};
     Euler3 e = q_euler(q_mul(g, q_inv(qload(st.anchor))));
     if (e.b < 0.05 || e.b > kPiD - 0.05) {
-        const Quat koff{a.prm.koffset[0], a.prm.koffset[1], a.prm.koffset[2], a.prm.koffset[3]};
         qstore(st.anchor, q_mul(q_inv(koff), g));
         st.anchor_limit = a.prm.band;
         st.anchored = 1;
-        wk.compose = 1;
         e = q_euler(koff);
     }
     wk.e[0] = e.a, wk.e[1] = e.b, wk.e[2] = e.g;
+    wk.side = 0;
+    if (st.anchored) {
+        // the global rotation g = R(e) a on the window kernel, or g K on the side kernel
+        const Euler3 eg = q_euler(g);
+        const Euler3 ek = q_euler(q_mul(g, koff));
+        const bool side = fabs(sin(ek.b)) > fabs(sin(eg.b));
+        const Euler3& ev = side ? ek : eg;
+        wk.ev[0] = ev.a, wk.ev[1] = ev.b, wk.ev[2] = ev.g;
+        wk.side = side ? 2 : 1;
+    }
     wk.status = ST_EVAL2;
     ++wk.iter;
-    return 1 | (wk.compose ? 2 : 0);
+    return true;
 }
 
 // iteration start of the candidates on the start list (band start, or accepted
-// trials of the previous iteration); appends to the order-2 and composition lists
+// trials of the previous iteration); appends to the order-2 list
 __global__ void iter_begin_kernel(StageArgs a, const int* start, const int* start_count) {
     const int n = *start_count;
     const int n_pad = (n + 31) & ~31;
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_pad; q += gridDim.x * blockDim.x) {
         const int i = q < n ? start[q] : -1;
-        const int f = i >= 0 ? iter_begin_one(a, i) : 0;
-        wappend(f & 1, i, a.list2, a.counts + CNT_L2);
-        wappend((f & 2) != 0, i, a.listc, a.counts + CNT_COMP);
-    }
-}
-
-// one CTA per candidate of the composition list; SMEM: the temporaries live in
-// shared memory (known address space -> LDS/STS), else in global scratch
-template <bool SMEM>
-#ifndef BMB_COMPOSE_THREADS
-#define BMB_COMPOSE_THREADS 256
-#endif
-__global__ void __launch_bounds__(BMB_COMPOSE_THREADS) compose_kernel(StageArgs a) {
-    extern __shared__ __align__(16) unsigned char sm[];
-    __shared__ ComposeScratch cs;
-    __shared__ int s_slot;
-    const int n = a.counts[CNT_COMP];
-    const int len = a.T.rows * 32;
-    const bool wedge = a.prm.has_wedge != 0;
-    float* scr = SMEM ? reinterpret_cast<float*>(sm) : a.scratch + (size_t)blockIdx.x * a.scratch_per_warp;
-    for (int q = blockIdx.x; q < n; q += gridDim.x) {
-        const int i = a.listc[q];
-        CandWork& wk = a.work[i];
-        if (threadIdx.x == 0) {
-            int slot = wk.slot;
-            if (slot < 0) {
-                slot = atomicAdd(a.pool_counter, 1);
-                if (slot >= a.pool) {  // pool exhausted: the host reruns this chunk
-                    *a.overflow = 1;
-                    wk.status = ST_DONE;
-                    slot = -1;
-                }
-            }
-            s_slot = slot;
-        }
-        __syncthreads();
-        const int slot = s_slot;
-        if (slot >= 0) {
-            const int w = i / a.max_cand;
-            compose_block(a.T, a.xi_win + (size_t)w * len, a, qload(a.cand[i].anchor), scr,
-                          a.xi_pool + (size_t)slot * len, wedge ? a.w_pool + (size_t)slot * len : nullptr, cs);
-        }
-        if (threadIdx.x == 0) {
-            wk.slot = slot;
-            wk.compose = 0;
-        }
-        __syncthreads();
+        const bool f = i >= 0 && iter_begin_one(a, i);
+        wappend(f, i, a.list2, a.counts + CNT_L2);
     }
 }
 
@@ -1073,12 +820,13 @@ __global__ void __launch_bounds__(EvalShape<K>::WARPS * 32, BMB_EVAL_MINB(ORDER)
         idx[k] = q0 + k < n ? i : -1;
         const CandWork& wk = a.work[i];
         const int w = i / a.max_cand;
-        // order 2 (status EVAL2): chart angles, the chart kernels when anchored; order 0
-        // (trials, final scores): global angles et on the window kernel
-        const bool chart = ORDER == 2 && a.cand[i].anchored;
-        job[k].xi = chart ? a.xi_pool + (size_t)wk.slot * len : a.xi_win + (size_t)w * len;
-        job[k].wx = !wedge ? nullptr : (chart ? a.w_pool + (size_t)wk.slot * len : a.T.wedge);
-        const double* e = ORDER == 2 ? wk.e : wk.et;
+        // order 2 (status EVAL2): chart angles e, or for an anchored candidate the
+        // angles ev of g (window kernel) or of g K (side kernels); order 0 (trials,
+        // final scores): global angles et on the window kernel
+        const int side = ORDER == 2 ? wk.side : 0;
+        job[k].xi = (side == 2 ? a.xi_side : a.xi_win) + (size_t)w * len;
+        job[k].wx = !wedge ? nullptr : (side == 2 ? a.T.wedge_side : a.T.wedge);
+        const double* e = ORDER == 2 ? (side ? wk.ev : wk.e) : wk.et;
         job[k].a = e[0], job[k].b = e[1], job[k].g = e[2];
     }
     WarpScratch* ws = wsc + warp * K;
@@ -1100,6 +848,7 @@ __device__ __forceinline__ bool step_one(const StageArgs& a, long long i) {
     CandState& st = a.cand[i];
     Derivs f;
     objective(wk.c, wk.r, a.prm.has_wedge != 0, 2, f);
+    if (wk.side) chart_transform(f, wk.e, wk.ev);  // anchored: derivatives in the chart angles
     ++st.evals;
     wk.f[0] = f.v;
     for (int k = 0; k < 3; ++k) wk.f[1 + k] = f.g[k];
@@ -1298,211 +1047,6 @@ __global__ void window_reduce_kernel(ReduceArgs a) {
     a.out[w] = o;
 }
 
-// ---------------------------------------------------------------- fused refinement
-// One persistent CTA of kFW warps per window at a time.  The window kernel of
-// the band is built once into shared memory; the window's candidates are dealt
-// to the warps (candidate c to warp c mod kFW) and every warp then runs its own
-// candidates' damped-Newton loop independently — warp-level lists, K-way
-// evaluations on the shared window kernel (every table and kernel load feeds
-// K rotation chains), chart kernels composed by the warp into its pool slots,
-// thread-per-candidate Newton steps — so a warp in a latency-bound FP64 phase
-// never holds the others.  Block barriers only at band boundaries.
-constexpr int kFW = 4;
-constexpr int kFT = kFW * 32;
-constexpr int kWarpCand = kFusedMaxCand / kFW;  // candidates per warp (<= 32 lanes)
-static_assert(kWarpCand <= 32, "one lane per candidate of a warp");
-
-struct WarpLists {
-    int u[kWarpCand];   // jobs on the window kernel
-    int a[kWarpCand];   // chart jobs
-    int c[kWarpCand];   // compositions
-};
-
-// warp-level append of the predicated lanes' candidate c; returns the new length
-__device__ __forceinline__ int wpush(bool pred, int* list, int n, int c) {
-    const unsigned m = __ballot_sync(0xffffffffu, pred);
-    if (pred) list[n + __popc(m & lanemask_lt())] = c;
-    return n + __popc(m);
-}
-
-// evaluation job of local candidate c of window w
-template <bool WEDGE>
-__device__ __forceinline__ EvalJob fused_job(const StageArgs& a, const FusedArgs& fa, const float4* sxi, int w, int c) {
-    const long long i = (long long)w * a.max_cand + c;
-    const CandWork& wk = a.work[i];
-    const bool chart = wk.status == ST_EVAL2 && a.cand[i].anchored;  // order 0: global angles
-    const size_t slot = (size_t)blockIdx.x * a.max_cand + c;
-    EvalJob j;
-    j.xi = chart ? fa.xi_pool + slot * fa.slot_len : sxi;
-    j.wx = !WEDGE ? nullptr : (chart ? fa.w_pool + slot * fa.slot_len : a.T.wedge);
-    const double* e = wk.status == ST_EVAL2 ? wk.e : wk.et;
-    j.a = e[0], j.b = e[1], j.g = e[2];
-    return j;
-}
-
-template <int ORDER, int K, bool WEDGE>
-__device__ __forceinline__ void fused_eval_group(const StageArgs& a, const FusedArgs& fa, const float4* sxi, int w,
-                                                 const int* cl, WarpScratch* ws) {
-    using O = EvalOpts<ORDER, false>;
-    EvalJob job[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) job[k] = fused_job<WEDGE>(a, fa, sxi, w, cl[k]);
-    warp_eval_k<ORDER, K, WEDGE, O::PF, O::PIPE>(a.T, job, ws);
-    constexpr int NV = ORDER == 0 ? 1 : 10;
-    const int lane = threadIdx.x & 31;
-#pragma unroll
-    for (int k = 0; k < K; ++k)
-        if (lane < NV) {
-            CandWork& wk = a.work[(long long)w * a.max_cand + cl[k]];
-            wk.c[lane] = ws[k].res[lane];
-            wk.r[lane] = ws[k].res[10 + lane];
-        }
-    __syncwarp();
-}
-
-// one warp evaluates its listed candidates of window w: window-kernel jobs in
-// groups of KG (remainder in groups of 2 and 1), then the chart jobs
-template <int ORDER, bool WEDGE>
-__device__ void fused_eval(const StageArgs& a, const FusedArgs& fa, const float4* sxi, int w, const int* lu, int nu,
-                           const int* la, int na, WarpScratch* ws) {
-    constexpr int KG = ORDER == 2 ? 2 : 4;
-    int q = 0;
-    for (; q + KG <= nu; q += KG) fused_eval_group<ORDER, KG, WEDGE>(a, fa, sxi, w, lu + q, ws);
-    if (KG == 4 && q + 2 <= nu) {
-        fused_eval_group<ORDER, 2, WEDGE>(a, fa, sxi, w, lu + q, ws);
-        q += 2;
-    }
-    if (q < nu) fused_eval_group<ORDER, 1, WEDGE>(a, fa, sxi, w, lu + q, ws);
-    for (int j = 0; j < na; ++j) fused_eval_group<ORDER, 1, WEDGE>(a, fa, sxi, w, la + j, ws);
-}
-
-#ifdef BMB_FUSED_PROF
-// per-phase SM cycles of the fused kernel (warp lane 0, summed), debug builds only
-__device__ unsigned long long g_fprof[16];
-#define FP_T0() long long fp_t = clock64()
-#define FP_MARK(k)                                                              \
-    do {                                                                        \
-        __syncwarp();                                                           \
-        const long long fp_n = clock64();                                       \
-        if ((threadIdx.x & 31) == 0) atomicAdd(&g_fprof[k], (unsigned long long)(fp_n - fp_t)); \
-        fp_t = fp_n;                                                            \
-    } while (0)
-#define FP_COUNT(k, v) \
-    do { if ((threadIdx.x & 31) == 0) atomicAdd(&g_fprof[k], (unsigned long long)(v)); } while (0)
-#else
-#define FP_T0() (void)0
-#define FP_MARK(k) (void)0
-#define FP_COUNT(k, v) (void)0
-#endif
-
-template <bool WEDGE>
-__global__ void __launch_bounds__(kFT, 3) refine_fused_kernel(FusedArgs fa) {
-    extern __shared__ __align__(16) unsigned char fsm[];
-    float4* sxi = reinterpret_cast<float4*>(fsm);
-    __shared__ WarpScratch wsc[kFW * 4];
-    __shared__ ComposeScratch csc[kFW];
-    __shared__ WarpLists wl[kFW];
-    __shared__ int s_w;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int maxc = fa.st[0].max_cand;
-    const int n_win = fa.st[0].n_win;
-    WarpScratch* ws = wsc + warp * 4;
-    WarpLists& L_ = wl[warp];
-    float* scr = fa.scratch + ((size_t)blockIdx.x * kFW + warp) * fa.scratch_floats;
-    unsigned long long n_eval[kFusedMaxBands][2];
-    for (int b = 0; b < kFusedMaxBands; ++b) n_eval[b][0] = n_eval[b][1] = 0;
-    FP_T0();
-    for (;;) {
-        if (tid == 0) s_w = atomicAdd(fa.win_counter, 1);
-        __syncthreads();
-        const int w = s_w;
-        if (w >= n_win) break;
-        FP_COUNT(10, 1);
-        const int nc = fa.st[0].cand_count[w];
-        const long long base = (long long)w * maxc;
-        // this lane's candidate (warp-strided deal)
-        const int c = warp + kFW * lane;
-        const bool mine = lane < kWarpCand && c < nc;
-        for (int bi = 0; nc > 0 && bi < fa.n_bands; ++bi) {
-            const StageArgs& a = fa.st[bi];
-            const int len = a.T.rows * 32;
-            // window kernel of this band (build_xi, xi_coefficients) into shared memory
-            const float* f = fa.coef + (size_t)w * fa.ldf;
-            for (int e = tid; e < len; e += kFT)
-                sxi[e] = xi_entry(a.T, a.row_group, f, fa.t_hat, fa.block_off, fa.radial_count, e >> 5, e & 31);
-            if (mine) band_begin_one(a, base + c);
-            FP_MARK(0);
-            __syncthreads();
-            FP_MARK(7);
-            for (;;) {
-                const int fl = mine ? iter_begin_one(a, base + c) : 0;
-                const bool anch = (fl & 1) && a.cand[base + c].anchored;
-                const int n2u = wpush((fl & 1) && !anch, L_.u, 0, c);
-                const int n2a = wpush(anch, L_.a, 0, c);
-                const int ncomp = wpush((fl & 2) != 0, L_.c, 0, c);
-                FP_MARK(8);
-                if (n2u + n2a == 0) break;
-                FP_COUNT(11, 1);
-                FP_COUNT(9, ncomp);
-                // chart kernels xi~ = xi D(a)^T of the (re-)anchored candidates
-                for (int q = 0; q < ncomp; ++q) {
-                    const int cc = L_.c[q];
-                    const size_t slot = (size_t)blockIdx.x * maxc + cc;
-                    compose_block<true>(a.T, sxi, a, qload(a.cand[base + cc].anchor), scr,
-                                        fa.xi_pool + slot * fa.slot_len,
-                                        WEDGE ? fa.w_pool + slot * fa.slot_len : nullptr, csc[warp]);
-                    if (lane == 0) {
-                        a.work[base + cc].slot = (int)slot;
-                        a.work[base + cc].compose = 0;
-                    }
-                }
-                FP_MARK(1);
-                fused_eval<2, WEDGE>(a, fa, sxi, w, L_.u, n2u, L_.a, n2a, ws);
-                n_eval[bi][1] += n2u + n2a;
-                FP_MARK(2);
-                bool tri = (fl & 1) && step_one(a, base + c);
-                FP_MARK(3);
-                for (int r = 0; r < 3; ++r) {
-                    const bool ta = tri && a.cand[base + c].anchored;
-                    const int ntu = wpush(tri && !ta, L_.u, 0, c);
-                    const int nta = wpush(ta, L_.a, 0, c);
-                    __syncwarp();
-                    if (ntu + nta == 0) break;
-                    fused_eval<0, WEDGE>(a, fa, sxi, w, L_.u, ntu, L_.a, nta, ws);
-                    n_eval[bi][0] += ntu + nta;
-                    FP_MARK(4);
-                    tri = tri && accept_one(a, base + c);
-                    FP_MARK(5);
-                }
-                __syncwarp();
-            }
-            const bool prune_now = fa.prune_band0 && bi == 0;
-            if (bi + 1 == fa.n_bands || prune_now) {
-                // final unanchored score (optimize.cpp:349-352) on the window kernel
-                const bool fin = mine && final_prep_one(a, base + c);
-                const int nf = wpush(fin, L_.u, 0, c);
-                __syncwarp();
-                fused_eval<0, WEDGE>(a, fa, sxi, w, L_.u, nf, L_.a, 0, ws);
-                n_eval[bi][0] += nf;
-                if (fin) final_score_one(a, base + c);
-                if (prune_now) {
-                    __syncthreads();
-                    if (tid == 0) prune_window(a, w);
-                }
-                FP_MARK(6);
-            }
-            __syncthreads();  // the next band rebuilds sxi; candidate state settled
-            FP_MARK(7);
-        }
-    }
-    // evaluation counters (one atomic per band and order per warp)
-    if (lane == 0 && fa.st[0].eval_stats)
-        for (int b = 0; b < fa.n_bands; ++b)
-            for (int o = 0; o < 2; ++o)
-                if (n_eval[b][o])
-                    atomicAdd(fa.st[0].eval_stats + ((size_t)fa.st[b].T.L * 2 + o) * 2 + (WEDGE ? 1 : 0), n_eval[b][o]);
-}
-
 // ---------------------------------------------------------------- sweep
 template <int ORDER, int K>
 __global__ void __launch_bounds__(EvalShape<K>::WARPS * 32) eval_sweep_kernel(EvalArgs a) {
@@ -1564,10 +1108,6 @@ __global__ void __launch_bounds__(256) build_xi_staged_kernel(XiArgs a) {
 
 }  // namespace
 
-long long compose_scratch_floats(int L) { return compose_layout(L).total; }
-
-size_t compose_smem_bytes(int L) { return sizeof(float) * (size_t)compose_scratch_floats(L); }
-
 double eval_flops(int L, int order, bool wedge) {
     const double nxi = (L + 1.0) * (2.0 * L + 1.0) * (2.0 * L + 3.0) / 3.0;
     const double plane = (2.0 * L + 1.0) * (2.0 * L + 1.0);
@@ -1593,16 +1133,6 @@ void launch_band_begin(const StageArgs& a, int* start, int* start_count, cudaStr
 }
 void launch_iter_begin(const StageArgs& a, const int* start, const int* start_count, int max_n, cudaStream_t s) {
     iter_begin_kernel<<<thread_grid(max_n), kNB, 0, s>>>(a, start, start_count);
-}
-void launch_compose(const StageArgs& a, int n, cudaStream_t s) {
-    if (n <= 0) return;
-    const size_t smem = a.compose_smem ? compose_smem_bytes(a.T.L) : 0;
-    if (smem) {
-        ensure_dynamic_smem(compose_kernel<true>, (int)smem);
-        compose_kernel<true><<<n, BMB_COMPOSE_THREADS, smem, s>>>(a);
-    } else {
-        compose_kernel<false><<<n, BMB_COMPOSE_THREADS, 0, s>>>(a);
-    }
 }
 // jobs per warp in the refinement: 1 (measured fastest; K-way over runs of
 // same-window candidates in the ordered lists is slower at every order):
@@ -1657,41 +1187,6 @@ void launch_prune(const StageArgs& a, cudaStream_t s) {
 void launch_window_reduce(const ReduceArgs& a, cudaStream_t s) {
     window_reduce_kernel<<<(a.n_win + 127) / 128, 128, 0, s>>>(a);
 }
-
-int fused_refine_grid(const FusedArgs& a, bool wedge) {
-    if (a.n_bands < 1 || a.n_bands > kFusedMaxBands || a.st[0].max_cand > kFusedMaxCand) return 0;
-    const int smem = (int)(sizeof(float4) * (size_t)a.smem_len);
-    if (smem > 160 * 1024) return 0;
-    if (a.st[0].max_cand > kFW * kWarpCand) return 0;
-    const void* fn = wedge ? reinterpret_cast<const void*>(refine_fused_kernel<true>)
-                           : reinterpret_cast<const void*>(refine_fused_kernel<false>);
-    if (ensure_dynamic_smem(fn, smem) != cudaSuccess) return 0;
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kFT, smem) != cudaSuccess || per_sm < 1) return 0;
-    return sms * per_sm;
-}
-
-int launch_refine_fused(const FusedArgs& a, int grid, bool wedge, cudaStream_t s) {
-    if (grid <= 0) return 2;
-    const size_t smem = sizeof(float4) * (size_t)a.smem_len;
-    if (wedge) refine_fused_kernel<true><<<grid, kFT, smem, s>>>(a);
-    else refine_fused_kernel<false><<<grid, kFT, smem, s>>>(a);
-    return cudaGetLastError() == cudaSuccess ? 0 : 2;
-}
-
-#ifdef BMB_FUSED_PROF
-extern "C" int bmb_fused_profile(unsigned long long* out, int reset) {
-    cudaDeviceSynchronize();
-    cudaMemcpyFromSymbol(out, g_fprof, sizeof(unsigned long long) * 16);
-    if (reset) {
-        unsigned long long z[16] = {0};
-        cudaMemcpyToSymbol(g_fprof, z, sizeof(z));
-    }
-    return 0;
-}
-#endif
 
 int launch_eval_sweep(const EvalArgs& a, cudaStream_t s) {
     int sms = 0, dev = 0;

@@ -17,43 +17,32 @@ struct CandWork {
     double c[10];   // raw correlation derivatives (value, grad, hess aa ab ag bb bg gg)
     double r[10];   // raw wedge-power derivatives
     double f[13];   // objective at e: value, grad[3], hess[9]
+    double ev[3];   // anchored: Euler angles of the order-2 evaluation (g, or g K on the side kernels)
     double lambda;  // Levenberg parameter of the iteration
     double lam;     // damping of the current retry
     int status;
     int retry;
     int iter;
-    int compose;    // 1: the chart kernel must be (re)built
-    int slot;       // pool slot of the anchored-chart kernels (-1: none this band)
-    int pad;
+    int side;       // order-2 evaluation: 0 chart angles e on the window kernel (unanchored),
+                    // 1 angles of g on the window kernel, 2 angles of g K on the side kernels
 };
 
 struct StageArgs {
     BandTables T;
     const int* row_group = nullptr;
-    const float4* xi_win = nullptr;  // [n_win][T.rows*32] window kernels (A, B entries)
-    float4* xi_pool = nullptr;       // [pool][T.rows*32] anchored correlation kernels
-    float4* w_pool = nullptr;        // [pool][T.rows*32] anchored wedge kernels
-    int pool = 0;
-    int* pool_counter = nullptr;     // slot allocator (reset per band)
-    int* overflow = nullptr;         // set when the pool is exhausted
+    const float4* xi_win = nullptr;   // [n_win][T.rows*32] window kernels (A, B entries)
+    const float4* xi_side = nullptr;  // [n_win][T.rows*32] side kernels xi D(K^-1)^T (anchored candidates)
     CandState* cand = nullptr;
     CandWork* work = nullptr;
     const int* cand_count = nullptr;
     int max_cand = 0;
     int n_win = 0;
     RefineParams prm;
-    const double2* chi_hat = nullptr;
-    const double2* q_hat = nullptr;
-    double wp_total = 1.0;
-    float* scratch = nullptr;        // compose temporaries per CTA (when not in shared memory)
-    long long scratch_per_warp = 0;  // floats per composing CTA
-    int compose_smem = 0;            // compose temporaries in shared memory
     int* counts = nullptr;           // [CNT_*] list lengths
     int* list2 = nullptr;            // candidates awaiting the order-2 evaluation (or final)
-    int* listc = nullptr;            // candidates whose chart kernel must be (re)built
     unsigned long long* eval_stats = nullptr;  // [kMaxL+1][2][2] evaluations by (L, order, wedge)
 };
-enum { CNT_L2 = 0, CNT_COMP = 1, CNT_T0 = 2, CNT_T1 = 3 };
+enum { CNT_L2 = 0, CNT_T0 = 2, CNT_T1 = 3 };
 
 // one window outcome per window (last band)
 struct ReduceArgs {
@@ -70,13 +59,10 @@ struct ReduceArgs {
     WindowOutcome* out = nullptr;
 };
 
-long long compose_scratch_floats(int L);
-size_t compose_smem_bytes(int L);
 // band start of every candidate; the started ones are appended to start
 void launch_band_begin(const StageArgs& a, int* start, int* start_count, cudaStream_t s);
 // iteration start of the candidates on a start list (max_n bounds its length)
 void launch_iter_begin(const StageArgs& a, const int* start, const int* start_count, int max_n, cudaStream_t s);
-void launch_compose(const StageArgs& a, int n, cudaStream_t s);
 void launch_eval(const StageArgs& a, int order, const int* list, const int* count, int max_n, cudaStream_t s);
 void launch_step(const StageArgs& a, int* list_out, int* count_out, int max_n, cudaStream_t s);
 void launch_accept(const StageArgs& a, const int* list_in, const int* count_in, int* list_out, int* count_out,
@@ -85,36 +71,6 @@ void launch_final_prep(const StageArgs& a, cudaStream_t s);
 void launch_final_score(const StageArgs& a, int max_n, cudaStream_t s);
 void launch_window_reduce(const ReduceArgs& a, cudaStream_t s);
 void launch_prune(const StageArgs& a, cudaStream_t s);
-
-// Fused per-window refinement: one persistent CTA takes a window at a time
-// (atomic window counter) and runs every band of refine() for all of the
-// window's candidates — window kernel built into shared memory, chart kernels
-// composed into the CTA's own pool slots, evaluations, Newton steps and
-// acceptance — with no host round trip.  Same per-candidate arithmetic as the
-// list-driven kernels above, so the outcomes are bit-identical.
-constexpr int kFusedMaxBands = 8;
-constexpr int kFusedMaxCand = 64;
-struct FusedArgs {
-    StageArgs st[kFusedMaxBands];  // per band: tables, parameters (pool/scratch fields unused)
-    int n_bands = 0;
-    int prune_band0 = 0;           // prune_after_band: keep each window's winner after band 0
-    const float* coef = nullptr;   // [n_win][ldf] real-packed window coefficients
-    int ldf = 0;
-    const float* t_hat = nullptr;  // real-packed template coefficients
-    const int* block_off = nullptr;
-    const int* radial_count = nullptr;
-    int* win_counter = nullptr;    // zeroed before the launch
-    float4* xi_pool = nullptr;     // [grid][max_cand][slot_len] chart kernels
-    float4* w_pool = nullptr;      // same, wedge kernels
-    long long slot_len = 0;        // float4 per pool slot (largest band)
-    float* scratch = nullptr;      // [grid][scratch_floats] composition temporaries
-    long long scratch_floats = 0;
-    int smem_len = 0;              // float4 of the shared-memory window kernel (largest band)
-};
-// grid the fused kernel runs with (persistent: resident CTAs on every SM); 0 if
-// the configuration is not supported (too many candidates / bands, kernel too large)
-int fused_refine_grid(const FusedArgs& a, bool wedge);
-int launch_refine_fused(const FusedArgs& a, int grid, bool wedge, cudaStream_t s);
 
 // standalone batched evaluation (rotate-score-gradient sweep, config 4):
 // value + gradient of C(g) = Re sum xi D(g) for n_xi kernels x n_rot angle

@@ -200,4 +200,76 @@ std::vector<double> little_d_full(int L, double beta) {
     return d;
 }
 
+std::vector<std::complex<double>> wigner_D_blocks(int L, double alpha, double beta, double gamma) {
+    const std::vector<double> d = little_d_full(L, beta);
+    std::vector<std::complex<double>> D(d.size());
+    size_t off = 0;
+    for (int l = 0; l <= L; ++l) {
+        const int w = 2 * l + 1;
+        for (int m = -l; m <= l; ++m)
+            for (int mp = -l; mp <= l; ++mp) {
+                const size_t i = off + (size_t)(m + l) * w + (mp + l);
+                D[i] = std::polar(1.0, -(m * alpha + mp * gamma)) * d[i];
+            }
+        off += (size_t)w * w;
+    }
+    return D;
+}
+
+namespace {
+std::complex<double> packed_value(const float* row, int m) {
+    const int am = m < 0 ? -m : m;
+    std::complex<double> z = am == 0 ? std::complex<double>(row[0], 0.0)
+                                     : std::complex<double>(row[2 * am - 1], row[2 * am]);
+    if (m < 0) z = ((am & 1) ? -1.0 : 1.0) * std::conj(z);  // f_{-m} = (-1)^m conj f_m
+    return z;
+}
+}  // namespace
+
+std::vector<float> rotate_real_packed(const std::vector<float>& f, const host::Basis& b,
+                                      const std::vector<std::complex<double>>& D) {
+    std::vector<float> out(f.size(), 0.0f);
+    size_t off = 0;
+    for (int l = 0; l <= b.l_max; ++l) {
+        const int w = 2 * l + 1;
+        for (int k = 0; k < b.radial_count(l); ++k) {
+            const float* row = f.data() + b.block_off[l] + (size_t)k * w;
+            float* o = out.data() + b.block_off[l] + (size_t)k * w;
+            for (int n = 0; n <= l; ++n) {
+                std::complex<double> acc = 0.0;
+                for (int m = -l; m <= l; ++m) acc += D[off + (size_t)(n + l) * w + (m + l)] * packed_value(row, m);
+                if (n == 0) {
+                    o[0] = (float)acc.real();
+                } else {
+                    o[2 * n - 1] = (float)acc.real();
+                    o[2 * n] = (float)acc.imag();
+                }
+            }
+        }
+        off += (size_t)w * w;
+    }
+    return out;
+}
+
+std::vector<std::complex<double>> rotate_tri(const std::vector<std::complex<double>>& q, int L,
+                                             const std::vector<std::complex<double>>& D) {
+    std::vector<std::complex<double>> out(q.size(), 0.0);
+    auto coef = [&](int l, int m) {
+        if (m >= 0) return q[host::tri(l, m)];
+        const std::complex<double> c = std::conj(q[host::tri(l, -m)]);
+        return ((-m) % 2) ? -c : c;
+    };
+    size_t off = 0;
+    for (int l = 0; l <= L; ++l) {
+        const int w = 2 * l + 1;
+        for (int n = 0; n <= l; ++n) {
+            std::complex<double> acc = 0.0;
+            for (int m = -l; m <= l; ++m) acc += D[off + (size_t)(n + l) * w + (m + l)] * coef(l, m);
+            out[host::tri(l, n)] = acc;
+        }
+        off += (size_t)w * w;
+    }
+    return out;
+}
+
 }  // namespace bmb

@@ -43,4 +43,19 @@ std::vector<float4> wedge_band_entries(const BandTablesHost& t,
 // (2l+1)^2 row-major blocks l = 0..L.
 std::vector<double> little_d_full(int L, double beta);
 
+// Side kernels of the anchored-candidate evaluation (refine.cu chart_transform):
+// xi' = xi D(b)^T with b = K^-1 is xi_coefficients(f, D(b) t), so the side
+// kernels only need the rotated template (rotate_expansion, src/steer.cpp:208-223)
+// and, for the wedge-power kernel conj(chi) q^T / total, the rotated q.
+// Wigner D^l_{m,m'}(b) = e^{-i m a} d^l_{m,m'}(beta) e^{-i m' g} (steer.cpp:158-178),
+// packed (2l+1)^2 row-major blocks l = 0..L.
+std::vector<std::complex<double>> wigner_D_blocks(int L, double alpha, double beta, double gamma);
+// f' = D f per (l, k) row of a real-packed FP32 coefficient set (real-volume
+// symmetric in and out), FP64 arithmetic
+std::vector<float> rotate_real_packed(const std::vector<float>& f, const host::Basis& b,
+                                      const std::vector<std::complex<double>>& D);
+// q'_l = D^l q_l for packed m >= 0 factors (tri(l, m)) of a real function
+std::vector<std::complex<double>> rotate_tri(const std::vector<std::complex<double>>& q, int L,
+                                             const std::vector<std::complex<double>>& D);
+
 }  // namespace bmb

@@ -14,7 +14,7 @@ def test_library_exports_every_declared_symbol():
     assert len(syms) >= 15
     for s in syms:
         assert hasattr(L, s), s
-    assert L.bm_abi_version() == 2
+    assert L.bm_abi_version() == 3
 
 
 def test_default_lambda_cut_host_metadata():

@@ -176,34 +176,6 @@ def test_lanes_give_identical_results(cuda_device):
         assert a["evaluations"] == b["evaluations"]
 
 
-@pytest.mark.parametrize("prune", [False, True])
-def test_fused_refine_matches_list_driven(cuda_device, prune):
-    """bm_context_set_refine_mode: the fused per-window refinement kernel and the
-    list-driven kernels run the same per-candidate arithmetic, so every outcome
-    (shift, rotation, score, evaluation count) is bit-identical.  Config-2 shape
-    (64^3, L=16, bands 4-8-16, 24 starts, +-60 deg wedge) on a few particles."""
-    import math
-
-    n, L = 64, 16
-    tmpl = api.make_template(n, 40, 2)
-    parts, _, _ = api.make_particles(tmpl, 4, 900, 3, 0.1, 60.0)
-    cfg = api.make_config(bands=(4, 8, 16), max_candidates=24, prune_after_band=prune)
-    out, stats = {}, {}
-    for mode in ("lists", "fused"):
-        ctx = api.Context(n, L, L * math.pi)
-        ctx.set_template(tmpl, 60.0)
-        ctx.set_refine_mode(mode)
-        ctx.eval_stats(reset=True)
-        out[mode] = ctx.align_batch(parts, cfg)
-        stats[mode] = ctx.eval_stats()[:2]
-    assert stats["lists"] == stats["fused"]
-    for a, b in zip(out["lists"], out["fused"]):
-        assert a["shift"] == b["shift"]
-        assert list(a["quat"]) == list(b["quat"])
-        assert a["score"] == b["score"]
-        assert a["evaluations"] == b["evaluations"]
-
-
 def test_lanes_raised_after_set_template(cuda_device):
     """set_lanes to more lanes after set_template: the new lanes adopt the
     template (regression: they used to raise 'set_template first')."""
