@@ -18,6 +18,8 @@
 #include <stdexcept>
 #include <thread>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "context.hpp"
 #include "refine.cuh"
 #include "rotation.cuh"
@@ -269,6 +271,13 @@ void Context::refine_windows(int nw, int maxc, const AlignConfig& cfg, const Qua
             const int L = cfg.bands[bi];
             BandDev& bd = band(L);
             const size_t len = (size_t)bd.rows * 32;
+            // NVTX range per band ("bmb_band16"): profilers select one band's launches
+            char range[32];
+            snprintf(range, sizeof(range), "bmb_band%d", L);
+            nvtxRangePushA(range);
+            struct RangePop {
+                ~RangePop() { nvtxRangePop(); }
+            } pop_range;
             StageArgs a;
             a.T = bd.view();
             a.row_group = bd.row_group.as<int>();
