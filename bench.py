@@ -46,7 +46,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="product", choices=["product", "reference"])
     ap.add_argument("--particles", type=int, default=CFG["particles"], help="per rank per step")
-    ap.add_argument("--cpu-sample", type=int, default=4, help="particles in the CPU baseline sample")
+    ap.add_argument("--cpu-sample", type=int, default=8,
+                    help="particles in the CPU baseline sample (also the parity sample)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--expand", default="factored", choices=["factored", "gemm"],
                     help="expansion algorithm (K2f factored, or the dense operator on tcgen05)")
@@ -142,14 +143,35 @@ def oracle_config():
                            shift_step=CFG["shift_step"], threads=cpu_cores())
 
 
-def cpu_align_seconds(tmpl, parts):
-    """The CPU restatement of align() (oracle/) on host cores: seconds for `parts`."""
+def cpu_align(tmpl, parts):
+    """The CPU restatement of align() (oracle/) on host cores: (seconds, results) for `parts`."""
     from oracle import bmo
     cfg = oracle_config()
     t0 = time.perf_counter()
-    for p in parts:
-        bmo.align(tmpl, p, cfg, wedge_deg=CFG["wedge"])
-    return time.perf_counter() - t0
+    out = [bmo.align(tmpl, p, cfg, wedge_deg=CFG["wedge"]) for p in parts]
+    return time.perf_counter() - t0, out
+
+
+def cpu_align_seconds(tmpl, parts):
+    return cpu_align(tmpl, parts)[0]
+
+
+def parity_block(dev, ref):
+    """Device align_batch results vs the oracle's align() on the same float32 bytes:
+    the north_star contract is shifts exact, rotations <= 0.5 deg, scores <= 1e-4 rel."""
+    geo, rel, exact = [], [], 0
+    for d, r in zip(dev, ref):
+        exact += tuple(int(x) for x in d["shift"]) == tuple(int(x) for x in r["shift"])
+        c = min(1.0, abs(float(np.dot(np.asarray(d["quat"]), np.asarray(r["quat"])))))
+        geo.append(math.degrees(2.0 * math.acos(c)))
+        rel.append(abs(d["score"] - r["score"]) / max(abs(r["score"]), 1e-300))
+    n = len(ref)
+    return {"n": n, "shift_exact": exact, "max_geodesic_deg": max(geo) if geo else None,
+            "median_geodesic_deg": float(np.median(geo)) if geo else None,
+            "max_score_rel": max(rel) if rel else None,
+            "within_contract": bool(n and exact == n and max(geo) <= 0.5 and max(rel) <= 1e-4),
+            "against": "oracle/ align() (FP64 CPU restatement of the reference) on the first "
+                       f"{n} particles of the timed batch"}
 
 
 def run_reference(args):
@@ -423,6 +445,8 @@ def run_product(args):
                    "note": "evaluations_per_step counts the seed grid too (align() counters)"},
         "e2e": {"value": P * world / (e2e_ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+        "e2e_results_identical": all(a["shift"] == b["shift"] and list(a["quat"]) == list(b["quat"])
+                                     and a["score"] == b["score"] for a, b in zip(res, res_e2e)),
         "gpu_launches": counts_timed["launches"],
         "step_ms": [round(x, 1) for x in step_ms], "host_step_ms": [round(x, 1) for x in host_ms],
         "clocks": clk.summary(),
@@ -437,7 +461,8 @@ def run_product(args):
             k = max(1, args.cpu_sample)
             tmpl_h = tmpl.double().cpu().numpy()
             sample = [p.double().cpu().numpy() for p in parts[:k]]
-            sec = cpu_align_seconds(tmpl_h, sample)
+            sec, ref_res = cpu_align(tmpl_h, sample)
+            line["parity"] = parity_block(res[:k], ref_res)
             line["cpu_baseline"] = {"value": k / sec, "unit": UNIT, "cores": cpu_cores(),
                                     "kind": "port",
                                     "sample": f"first {k} particle(s) of the batch (identical "

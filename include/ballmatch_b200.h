@@ -172,6 +172,39 @@ int bm_search_windows(bm_context* ctx, const float* vols, int n_vol, const int* 
 int bm_eval_sweep(bm_context* ctx, const double* f, int n_f, const double* t, const double* euler,
                   int n_rot, int order, double* out, void* stream);
 
+/* Objective::eval (src/optimize.cpp:102-131) exactly as the refinement evaluates
+ * it: kernels xi = xi_coefficients(f, t) (xcorr.cpp:21-50) of one coefficient set
+ * f (device complex128, reference layout, real-volume symmetric) against t
+ * (device, same layout; NULL = the context's template), with the wedge-power
+ * quotient C / sqrt(clamp(1 - rho, 0.02, 2)) when the template state has a wedge,
+ * at band L for n points.  euler (device double, n x 3) are chart angles e and
+ * anchors (device double, n x 4 quaternions, or NULL) chart anchors a: the
+ * function is C~(e) = C(R(e) a), as on the composed kernel xi D(a)^T of
+ * xi_compose_right (xcorr.cpp:149-155) that refine() uses near the poles
+ * (optimize.cpp:268-299).  order 2: value, gradient, Hessian
+ * (correlation_derivatives order 2, xcorr.cpp:52-105); order 0: value only.
+ * out (device double, n x 13): value, d/d(alpha, beta, gamma), Hessian row-major. */
+int bm_objective_eval(bm_context* ctx, const double* f, const double* t, const double* euler,
+                      const double* anchors, int n, int L, int order, double* out, void* stream);
+
+/* seed_candidates (src/optimize.cpp:197-253, grid_scores 48-97) for n_f
+ * coefficient sets f (device complex128, reference layout) against the context's
+ * template at band L_low on the Euler grid of `step`, with the template's wedge
+ * quotient: quats (host, n_f x max_candidates x 4) in rank order, counts (host,
+ * n_f), scores (host, n_f x max_candidates, may be NULL) the seed grid scores. */
+int bm_seed_candidates(bm_context* ctx, const double* f, int n_f, int L_low, double step,
+                       int max_candidates, double* quats, int* counts, double* scores, void* stream);
+
+/* Template coefficients t_hat (expand of the template, complex128 device,
+ * reference layout) of the current template state. */
+int bm_template_coeffs(bm_context* ctx, double* out, void* stream);
+
+/* Wedge-power kernel of the current template state (wedge_power_kernel,
+ * src/xcorr.cpp:234-357): XiBlocks layout, degree blocks l = 0..l_max of
+ * (2l+1)^2 complex128 entries [m][m'] (host memory, N_xi(l_max) entries).
+ * BM_ERR_STATE without a wedge. */
+int bm_wedge_power_kernel(bm_context* ctx, double* out);
+
 /* Tapered missing-wedge filter of the current template's context on device
  * volumes (apply_wedge_taper, src/xcorr.cpp:210-232). */
 int bm_apply_wedge_taper(bm_context* ctx, const float* in, float* out, int count, void* stream);

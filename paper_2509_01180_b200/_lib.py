@@ -117,6 +117,14 @@ def _declare(L: C.CDLL) -> None:
     L.bm_context_band_timings.restype = I
     L.bm_context_set_expand_mode.argtypes = [P, I]
     L.bm_context_set_expand_mode.restype = I
+    L.bm_objective_eval.argtypes = [P, P, P, P, P, I, I, I, P, P]
+    L.bm_objective_eval.restype = I
+    L.bm_seed_candidates.argtypes = [P, P, I, I, D, I, P, P, P, P]
+    L.bm_seed_candidates.restype = I
+    L.bm_template_coeffs.argtypes = [P, P, P]
+    L.bm_template_coeffs.restype = I
+    L.bm_wedge_power_kernel.argtypes = [P, P]
+    L.bm_wedge_power_kernel.restype = I
     L.bm_context_set_expand_pairs.argtypes = [P, I]
     L.bm_context_set_expand_pairs.restype = I
     L.bm_context_set_stage_reuse.argtypes = [P, I]

@@ -13,6 +13,7 @@ without a CUDA device every call raises.
 from __future__ import annotations
 
 import ctypes as C
+import math
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -256,6 +257,61 @@ class Context:
                                             n_rot, order, C.c_void_p(out.data_ptr()),
                                             self._stream(out)), "eval_sweep")
         return out
+
+    def objective_eval(self, f, euler, anchors=None, L=None, order: int = 2, t=None):
+        """Objective::eval of the refinement (bm_objective_eval) on xi(f, t) (t None:
+        the template) at chart angles euler (n, 3) with chart anchors (n, 4) or None;
+        returns float64 numpy (n, 13): value, gradient, Hessian (row-major)."""
+        torch = _torch()
+        dev = torch.device(f"cuda:{self.device}")
+        fa = torch.view_as_real(torch.as_tensor(f, dtype=torch.complex128)).to(dev).contiguous()
+        ta = None if t is None else torch.view_as_real(torch.as_tensor(t, dtype=torch.complex128)).to(dev).contiguous()
+        ea = torch.as_tensor(np.asarray(euler, dtype=np.float64).reshape(-1, 3)).to(dev).contiguous()
+        aa = None if anchors is None else torch.as_tensor(np.asarray(anchors, dtype=np.float64).reshape(-1, 4)).to(dev).contiguous()
+        n = ea.shape[0]
+        out = torch.empty((n, 13), dtype=torch.float64, device=dev)
+        _lib.check(_lib.lib().bm_objective_eval(
+            self._h, C.c_void_p(fa.data_ptr()), None if ta is None else C.c_void_p(ta.data_ptr()),
+            C.c_void_p(ea.data_ptr()), None if aa is None else C.c_void_p(aa.data_ptr()), n,
+            self.l_max if L is None else int(L), int(order), C.c_void_p(out.data_ptr()), self._stream(out)),
+            "objective_eval")
+        torch.cuda.synchronize(dev)
+        return out.cpu().numpy()
+
+    def seed_candidates(self, f, L_low: int, step: float = math.pi / 8, max_candidates: int = 24):
+        """seed_candidates of coefficient sets f (n_f, coeff_count) against the template:
+        a list of (quaternions (count, 4), grid scores (count,)) in rank order."""
+        torch = _torch()
+        dev = torch.device(f"cuda:{self.device}")
+        fa = torch.view_as_real(torch.as_tensor(f, dtype=torch.complex128)).to(dev).contiguous()
+        if fa.dim() == 2:
+            fa = fa.unsqueeze(0)
+        n_f = fa.shape[0]
+        q = np.zeros((n_f, max_candidates, 4))
+        cnt = np.zeros(n_f, dtype=np.int32)
+        sc = np.zeros((n_f, max_candidates))
+        _lib.check(_lib.lib().bm_seed_candidates(
+            self._h, C.c_void_p(fa.data_ptr()), n_f, int(L_low), float(step), int(max_candidates),
+            q.ctypes.data_as(C.c_void_p), cnt.ctypes.data_as(C.c_void_p), sc.ctypes.data_as(C.c_void_p),
+            self._stream(fa)), "seed_candidates")
+        return [(q[i, :cnt[i]].copy(), sc[i, :cnt[i]].copy()) for i in range(n_f)]
+
+    def template_coeffs(self):
+        """t_hat of the current template (complex128 (coeff_count,), device)."""
+        torch = _torch()
+        out = torch.empty((self.coeff_count, 2), dtype=torch.float64, device=f"cuda:{self.device}")
+        _lib.check(_lib.lib().bm_template_coeffs(self._h, C.c_void_p(out.data_ptr()), self._stream(out)),
+                   "template_coeffs")
+        return torch.view_as_complex(out)
+
+    def wedge_power_kernel(self):
+        """The template's wedge-power kernel in the XiBlocks layout (numpy complex128)."""
+        L = self.l_max
+        nxi = (L + 1) * (2 * L + 1) * (2 * L + 3) // 3
+        out = np.zeros(2 * nxi)
+        _lib.check(_lib.lib().bm_wedge_power_kernel(self._h, out.ctypes.data_as(C.c_void_p)),
+                   "wedge_power_kernel")
+        return out.view(np.complex128)
 
     def apply_wedge_taper(self, vols):
         torch = _torch()

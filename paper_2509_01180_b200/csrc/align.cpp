@@ -412,6 +412,136 @@ void Context::refine_windows(int nw, int maxc, const AlignConfig& cfg, const Qua
     }
 }
 
+// seed_candidates (optimize.cpp:197-253) for n_f device coefficient sets
+// (complex128, reference layout) against the template: candidate rotations
+// (quaternions, rank order) and counts to host
+void Context::seed_candidates(const double* f, int n_f, int L_low, double step, int max_cand, double* quats,
+                              int* counts, double* scores) {
+    if (n_f <= 0) return;
+    if (!has_template) throw std::invalid_argument("seed: set_template first");
+    if (L_low < 0 || L_low > basis.l_max) throw std::invalid_argument("seed: band outside [0, l_max]");
+    if (max_cand < 1 || max_cand > 256) throw std::invalid_argument("seed: max_candidates must be 1..256");
+    if (!(step > 0.0) || step > kPiH) throw std::invalid_argument("seed: grid step must be in (0, pi]");
+    const int ld = geo.m_pad;
+    work_f.reserve(sizeof(float) * (size_t)n_f * ld);
+    launch_from_complex(f, n_f, geo, work_f.as<float>(), ld, stream);
+    SeedDev& sd = seed_tables(L_low, step);
+    SeedArgs sa;
+    sa.coef = work_f.as<float>();
+    sa.ldc = ld;
+    sa.t_hat = t_hat.as<float>();
+    sa.block_off = geo.block_off;
+    sa.radial_count = geo.radial_count;
+    sa.L_low = sd.L_low;
+    sa.rows_low = sd.L_low + 1 <= basis.l_max ? basis.block_off[sd.L_low + 1] : geo.coeffs;
+    sa.nxi = sd.nxi;
+    sa.na = sd.na;
+    sa.nb = sd.nb;
+    sa.ng = sd.ng;
+    sa.dgrid = sd.dgrid.as<double>();
+    sa.ua = sd.ua.as<double2>();
+    sa.ug = sd.ug.as<double2>();
+    sa.wedge_sqrt = sd.has_wedge ? sd.wedge_sqrt.as<double>() : nullptr;
+    sa.max_cand = max_cand;
+    cand_.reserve(sizeof(CandState) * (size_t)n_f * max_cand);
+    cand_count_.reserve(sizeof(int) * n_f);
+    sub_norm_.reserve(sizeof(double) * (size_t)n_f * max_cand);
+    sa.cand = cand_.as<CandState>();
+    sa.cand_count = cand_count_.as<int>();
+    sa.seed_score = scores ? sub_norm_.as<double>() : nullptr;
+    if (seed_needs_scratch(sa)) {
+        sa.scratch_windows = 4096;
+        seed_scratch_.reserve(sizeof(double2) * (size_t)sa.scratch_windows * sa.nxi);
+        sa.xi_scratch = seed_scratch_.as<double2>();
+    }
+    if (launch_seed(sa, n_f, stream) != 0) throw std::runtime_error("seed kernel launch failed");
+    std::vector<CandState> cs((size_t)n_f * max_cand);
+    ck(cudaMemcpyAsync(cs.data(), cand_.p, sizeof(CandState) * cs.size(), cudaMemcpyDeviceToHost, stream), "cands");
+    ck(cudaMemcpyAsync(counts, cand_count_.p, sizeof(int) * n_f, cudaMemcpyDeviceToHost, stream), "counts");
+    if (scores)
+        ck(cudaMemcpyAsync(scores, sub_norm_.p, sizeof(double) * (size_t)n_f * max_cand, cudaMemcpyDeviceToHost,
+                           stream), "scores");
+    ck(cudaStreamSynchronize(stream), "seed");
+    for (size_t i = 0; i < cs.size(); ++i)
+        for (int k = 0; k < 4; ++k) quats[4 * i + k] = cs[i].g[k];
+}
+
+// Objective::eval of the refinement (bm_objective_eval): kernels of one
+// coefficient set f against t (null: the template; its side template is rebuilt
+// for an explicit t), at band L, n chart points
+void Context::objective_eval(const double* f, const double* t, const double* euler, const double* anchors, int n,
+                             int L, int order, double* out) {
+    if (n <= 0) return;
+    if (L < 0 || L > basis.l_max) throw std::invalid_argument("objective: band outside [0, l_max]");
+    if (order != 0 && order != 2) throw std::invalid_argument("objective: order must be 0 or 2");
+    if (!t && !has_template) throw std::invalid_argument("objective: set_template first (or pass t)");
+    const int ld = geo.m_pad;
+    work_f.reserve(sizeof(float) * (size_t)3 * ld);
+    float* fr = work_f.as<float>();
+    const float* tr = t_hat.as<float>();
+    const float* ts = t_side.as<float>();
+    launch_from_complex(f, 1, geo, fr, ld, stream);
+    if (t) {
+        float* tt = fr + ld;
+        cudaMemsetAsync(tt, 0, sizeof(float) * 2 * ld, stream);
+        launch_from_complex(t, 1, geo, tt, ld, stream);
+        std::vector<float> th(ld);
+        ck(cudaMemcpyAsync(th.data(), tt, sizeof(float) * ld, cudaMemcpyDeviceToHost, stream), "t");
+        ck(cudaStreamSynchronize(stream), "t");
+        const Euler3 e = q_euler(q_inv(q_from_euler(0.0, kPiH / 2.0, 0.0)));
+        const std::vector<float> side = rotate_real_packed(th, basis, wigner_D_blocks(basis.l_max, e.a, e.b, e.g));
+        ck(cudaMemcpyAsync(tt + ld, side.data(), sizeof(float) * ld, cudaMemcpyHostToDevice, stream), "t side");
+        tr = tt;
+        ts = tt + ld;
+    }
+    BandDev& bd = band(L);
+    const size_t len = (size_t)bd.rows * 32;
+    xi_win_.reserve(sizeof(float4) * len);
+    xi_side_.reserve(sizeof(float4) * len);
+    XiArgs xa;
+    xa.T = bd.view();
+    xa.row_group = bd.row_group.as<int>();
+    xa.f = fr;
+    xa.ldf = ld;
+    xa.t = tr;
+    xa.ldt = 0;
+    xa.block_off = geo.block_off;
+    xa.radial_count = geo.radial_count;
+    xa.n = 1;
+    xa.out = xi_win_.as<float4>();
+    xa.nf = L < basis.l_max ? basis.block_off[L + 1] : geo.coeffs;
+    if (launch_build_xi(xa, stream) != 0) throw std::runtime_error("build_xi launch failed");
+    xa.t = ts;
+    xa.out = xi_side_.as<float4>();
+    if (launch_build_xi(xa, stream) != 0) throw std::runtime_error("build_xi launch failed");
+    StageArgs a;
+    a.T = bd.view();
+    a.row_group = xa.row_group;
+    a.xi_win = xi_win_.as<float4>();
+    a.xi_side = xi_side_.as<float4>();
+    cand_.reserve(sizeof(CandState) * (size_t)n);
+    work_.reserve(sizeof(CandWork) * (size_t)n);
+    lists_.reserve(sizeof(int) * (size_t)n);
+    counters_.reserve(sizeof(int) * 8);
+    a.cand = cand_.as<CandState>();
+    a.work = work_.as<CandWork>();
+    a.list2 = lists_.as<int>();
+    a.counts = counters_.as<int>();
+    a.max_cand = n;
+    a.n_win = 1;
+    const Quat koff = q_from_euler(0.0, kPiH / 2.0, 0.0);
+    a.prm.band = L;
+    a.prm.koffset[0] = koff.w;
+    a.prm.koffset[1] = koff.x;
+    a.prm.koffset[2] = koff.y;
+    a.prm.koffset[3] = koff.z;
+    a.prm.max_cand = n;
+    a.prm.has_wedge = wedge_active() ? 1 : 0;
+    if (launch_objective_eval(a, euler, anchors, n, order, out, stream) != 0)
+        throw std::runtime_error("objective launch failed");
+    ck(cudaStreamSynchronize(stream), "objective");
+}
+
 std::vector<WindowOutcome> Context::run_windows(const float* vols, int n_vol, const std::vector<int>& wvol,
                                                 const std::vector<int>& wshift, const AlignConfig& cfg) {
     if (!has_template) throw std::invalid_argument("align: set_template first");

@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <complex>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -311,6 +312,71 @@ int bm_eval_sweep(bm_context* ctx, const double* f, int n_f, const double* t, co
         ea.order = order;
         ea.out = out;
         if (bmb::launch_eval_sweep(ea, c.stream) != 0) throw std::runtime_error("eval sweep launch failed");
+        return (int)BM_OK;
+    });
+}
+
+int bm_objective_eval(bm_context* ctx, const double* f, const double* t, const double* euler,
+                      const double* anchors, int n, int L, int order, double* out, void* stream) {
+    return guarded("bm_objective_eval", [&] {
+        if (!ctx) return (int)BM_ERR_STATE;
+        if (n < 0 || (n > 0 && (!f || !euler || !out))) throw std::invalid_argument("bad buffers");
+        if (n == 0) return (int)BM_OK;
+        auto& c = *ctx->impl;
+        cudaSetDevice(c.device);
+        StreamJoin join(ctx, stream);
+        c.objective_eval(f, t, euler, anchors, n, L, order, out);
+        return (int)BM_OK;
+    });
+}
+
+int bm_seed_candidates(bm_context* ctx, const double* f, int n_f, int L_low, double step,
+                       int max_candidates, double* quats, int* counts, double* scores, void* stream) {
+    return guarded("bm_seed_candidates", [&] {
+        if (!ctx) return (int)BM_ERR_STATE;
+        if (n_f < 0 || (n_f > 0 && (!f || !quats || !counts))) throw std::invalid_argument("bad buffers");
+        if (n_f == 0) return (int)BM_OK;
+        auto& c = *ctx->impl;
+        cudaSetDevice(c.device);
+        StreamJoin join(ctx, stream);
+        c.seed_candidates(f, n_f, L_low, step, max_candidates, quats, counts, scores);
+        return (int)BM_OK;
+    });
+}
+
+int bm_template_coeffs(bm_context* ctx, double* out, void* stream) {
+    return guarded("bm_template_coeffs", [&] {
+        if (!ctx) return (int)BM_ERR_STATE;
+        if (!out) throw std::invalid_argument("null output");
+        auto& c = *ctx->impl;
+        if (!c.has_template) return (int)BM_ERR_STATE;
+        cudaSetDevice(c.device);
+        StreamJoin join(ctx, stream);
+        bmb::launch_to_complex(c.t_hat.as<float>(), 1, c.geo.m_pad, c.geo, out, c.stream);
+        return (int)BM_OK;
+    });
+}
+
+int bm_wedge_power_kernel(bm_context* ctx, double* out) {
+    return guarded("bm_wedge_power_kernel", [&] {
+        if (!ctx) return (int)BM_ERR_STATE;
+        if (!out) throw std::invalid_argument("null output");
+        auto& c = *ctx->impl;
+        if (!c.wedge_active()) return (int)BM_ERR_STATE;
+        const int L = c.basis.l_max;
+        auto coef = [&](const std::vector<std::complex<double>>& hat, int l, int m) {
+            if (m >= 0) return hat[bmb::host::tri(l, m)];
+            const std::complex<double> z = std::conj(hat[bmb::host::tri(l, -m)]);
+            return ((-m) % 2) ? -z : z;
+        };
+        size_t o = 0;
+        for (int l = 0; l <= L; ++l)
+            for (int m = -l; m <= l; ++m)
+                for (int mp = -l; mp <= l; ++mp, ++o) {
+                    const std::complex<double> w = std::conj(coef(c.chi_hat, l, m)) * coef(c.q_hat, l, mp) / c.wp_total;
+                    out[2 * o] = w.real();
+                    out[2 * o + 1] = w.imag();
+                }
         return (int)BM_OK;
     });
 }

@@ -223,6 +223,13 @@ public:
     BandDev& band(int L);
     SeedDev& seed_tables(int L_low, double step);
 
+    // seed_candidates for device coefficient sets (bm_seed_candidates)
+    void seed_candidates(const double* f, int n_f, int L_low, double step, int max_cand, double* quats, int* counts,
+                         double* scores);
+    // Objective::eval of the refinement at n chart points (bm_objective_eval)
+    void objective_eval(const double* f, const double* t, const double* euler, const double* anchors, int n, int L,
+                        int order, double* out);
+
     // one window stage: search_one_shift for every (volume, shift) window
     std::vector<WindowOutcome> run_windows(const float* vols, int n_vol, const std::vector<int>& wvol,
                                            const std::vector<int>& wshift, const AlignConfig& cfg);

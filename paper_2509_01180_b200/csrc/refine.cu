@@ -696,6 +696,18 @@ __global__ void band_begin_kernel(StageArgs a, int* start, int* start_count) {
     }
 }
 
+// order-2 evaluation frame of an anchored candidate at global rotation g: the
+// window kernel at E(g), or the side kernels at E(g K), whichever is further from
+// its gimbal pole (chart_transform)
+__device__ __forceinline__ void set_eval_frame(CandWork& wk, const Quat& g, const Quat& koff) {
+    const Euler3 eg = q_euler(g);
+    const Euler3 ek = q_euler(q_mul(g, koff));
+    const bool side = fabs(sin(ek.b)) > fabs(sin(eg.b));
+    const Euler3& ev = side ? ek : eg;
+    wk.ev[0] = ev.a, wk.ev[1] = ev.b, wk.ev[2] = ev.g;
+    wk.side = side ? 2 : 1;
+}
+
 // iteration start of candidate i (chart and re-anchor decision,
 // optimize.cpp:292-298): true = evaluate at order 2.  Anchored candidates pick
 // the kernel and angles of their order-2 evaluation (chart_transform).
@@ -718,15 +730,7 @@ __device__ __forceinline__ bool iter_begin_one(const StageArgs& a, long long i) 
     }
     wk.e[0] = e.a, wk.e[1] = e.b, wk.e[2] = e.g;
     wk.side = 0;
-    if (st.anchored) {
-        // the global rotation g = R(e) a on the window kernel, or g K on the side kernel
-        const Euler3 eg = q_euler(g);
-        const Euler3 ek = q_euler(q_mul(g, koff));
-        const bool side = fabs(sin(ek.b)) > fabs(sin(eg.b));
-        const Euler3& ev = side ? ek : eg;
-        wk.ev[0] = ev.a, wk.ev[1] = ev.b, wk.ev[2] = ev.g;
-        wk.side = side ? 2 : 1;
-    }
+    if (st.anchored) set_eval_frame(wk, g, koff);
     wk.status = ST_EVAL2;
     ++wk.iter;
     return true;
@@ -1047,6 +1051,47 @@ __global__ void window_reduce_kernel(ReduceArgs a) {
     a.out[w] = o;
 }
 
+// ---------------------------------------------------------------- objective probe
+// bm_objective_eval: the refinement's evaluation of Objective::eval
+// (src/optimize.cpp:102-131) at given chart angles and anchors, through the same
+// frame choice, evaluation kernels and chart transform as the Newton loop
+__global__ void objective_setup_kernel(StageArgs a, const double* euler, const double* anchors, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) a.counts[CNT_L2] = n;
+    if (i >= n) return;
+    CandState& st = a.cand[i];
+    CandWork& wk = a.work[i];
+    const Quat koff{a.prm.koffset[0], a.prm.koffset[1], a.prm.koffset[2], a.prm.koffset[3]};
+    const double* e = euler + 3 * i;
+    const Quat anchor = anchors ? qload(anchors + 4 * i) : Quat{1.0, 0.0, 0.0, 0.0};
+    const Quat g = anchors ? q_mul(q_from_euler(e[0], e[1], e[2]), anchor) : q_from_euler(e[0], e[1], e[2]);
+    qstore(st.g, g);
+    qstore(st.anchor, anchor);
+    st.anchored = anchors ? 1 : 0;
+    wk.e[0] = e[0], wk.e[1] = e[1], wk.e[2] = e[2];
+    wk.side = 0;
+    if (anchors) set_eval_frame(wk, g, koff);
+    // order 0: the value at the global rotation on the window kernel (make_trial)
+    const Euler3 eg = q_euler(g);
+    wk.et[0] = anchors ? eg.a : e[0];
+    wk.et[1] = anchors ? eg.b : e[1];
+    wk.et[2] = anchors ? eg.g : e[2];
+    a.list2[i] = i;
+}
+
+__global__ void objective_finalize_kernel(StageArgs a, int n, int order, double* out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    CandWork& wk = a.work[i];
+    Derivs f;
+    objective(wk.c, wk.r, a.prm.has_wedge != 0, order, f);
+    if (order == 2 && wk.side) chart_transform(f, wk.e, wk.ev);
+    double* o = out + 13 * (size_t)i;
+    o[0] = f.v;
+    for (int k = 0; k < 3; ++k) o[1 + k] = order == 2 ? f.g[k] : 0.0;
+    for (int k = 0; k < 9; ++k) o[4 + k] = order == 2 ? f.h[k] : 0.0;
+}
+
 // ---------------------------------------------------------------- sweep
 template <int ORDER, int K>
 __global__ void __launch_bounds__(EvalShape<K>::WARPS * 32) eval_sweep_kernel(EvalArgs a) {
@@ -1186,6 +1231,15 @@ void launch_prune(const StageArgs& a, cudaStream_t s) {
 }
 void launch_window_reduce(const ReduceArgs& a, cudaStream_t s) {
     window_reduce_kernel<<<(a.n_win + 127) / 128, 128, 0, s>>>(a);
+}
+
+int launch_objective_eval(const StageArgs& a, const double* euler, const double* anchors, int n, int order,
+                          double* out, cudaStream_t s) {
+    if (n <= 0) return 0;
+    objective_setup_kernel<<<(n + 127) / 128, 128, 0, s>>>(a, euler, anchors, n);
+    launch_eval(a, order == 2 ? 2 : 0, a.list2, a.counts + CNT_L2, n, s);
+    objective_finalize_kernel<<<(n + 127) / 128, 128, 0, s>>>(a, n, order, out);
+    return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }
 
 int launch_eval_sweep(const EvalArgs& a, cudaStream_t s) {

@@ -72,6 +72,13 @@ void launch_final_score(const StageArgs& a, int max_n, cudaStream_t s);
 void launch_window_reduce(const ReduceArgs& a, cudaStream_t s);
 void launch_prune(const StageArgs& a, cudaStream_t s);
 
+// Objective::eval of the refinement at n chart points (angles euler[3n], anchors
+// [4n] quaternions or null) on the window kernels of a.xi_win / a.xi_side (one
+// window): out[13n] = value, gradient, Hessian (order 2) in the chart angles.
+// a.cand / a.work / a.list2 / a.counts need n slots (a.max_cand = n, a.n_win = 1).
+int launch_objective_eval(const StageArgs& a, const double* euler, const double* anchors, int n, int order,
+                          double* out, cudaStream_t s);
+
 // standalone batched evaluation (rotate-score-gradient sweep, config 4):
 // value + gradient of C(g) = Re sum xi D(g) for n_xi kernels x n_rot angle
 // triples; out[(p*n_rot + g)*4 + {0..3}] = value, dC/dalpha, dC/dbeta, dC/dgamma.

@@ -56,10 +56,12 @@ def test_average_matches_oracle_rotate_expansion(cuda_device):
 
 def test_config2_sized_alignment_parity(cuda_device):
     """64^3, L=16, bands 4-8-16, 24 starts, wedge 60, SNR 0.1, shifts +-3: the
-    metric configuration on two particles, GPU vs oracle align()."""
+    metric configuration (the bench's template and first 16 particles), GPU vs
+    oracle align()."""
     n, L = 64, 16
+    P = 16
     tmpl_d = api.make_template(n, 40, 20250901)
-    parts, q, sh = api.make_particles(tmpl_d, 2, 1000, 3, 0.1, 60.0)
+    parts, q, sh = api.make_particles(tmpl_d, P, 1000, 3, 0.1, 60.0)
     ctx = api.Context(n, L, L * math.pi)
     ctx.set_template(tmpl_d, 60.0)
     cfg = api.make_config(bands=(4, 8, 16), max_candidates=24, shift_radius=4, shift_step=2)
@@ -67,7 +69,7 @@ def test_config2_sized_alignment_parity(cuda_device):
     ocfg = bmo.make_config(l_max=L, lambda_cut=L * math.pi, bands=(4, 8, 16), max_candidates=24,
                            shift_radius=4, shift_step=2)
     tmpl = tmpl_d.cpu().numpy().astype(np.float64)
-    for p in range(2):
+    for p in range(P):
         ref = bmo.align(tmpl, parts[p].cpu().numpy().astype(np.float64), ocfg, wedge_deg=60.0)
         assert got[p]["shift"] == ref["shift"]
         assert bmo.geodesic_degrees(got[p]["quat"], ref["quat"]) < 0.5
@@ -93,10 +95,11 @@ def test_synthesize_matches_oracle(cuda_device, n, L, m_out):
 
 def test_config5_sized_alignment_parity(cuda_device):
     """Config-5 shape: 64^3, L=20, four marching bands 4-8-16-20, 24 starts, 60-blob
-    template, SNR 0.05, shifts +-4, wedge 60; one particle, GPU vs oracle align()."""
+    template, SNR 0.05, shifts +-4, wedge 60; four particles, GPU vs oracle align()."""
     n, L = 64, 20
+    P = 4
     tmpl_d = api.make_template(n, 60, 20250905)
-    parts, q, sh = api.make_particles(tmpl_d, 1, 5000, 4, 0.05, 60.0)
+    parts, q, sh = api.make_particles(tmpl_d, P, 5000, 4, 0.05, 60.0)
     ctx = api.Context(n, L, L * math.pi)
     ctx.set_template(tmpl_d, 60.0)
     cfg = api.make_config(bands=(4, 8, 16, 20), max_candidates=24, shift_radius=4, shift_step=2)
@@ -104,11 +107,12 @@ def test_config5_sized_alignment_parity(cuda_device):
     ocfg = bmo.make_config(l_max=L, lambda_cut=L * math.pi, bands=(4, 8, 16, 20), max_candidates=24,
                            shift_radius=4, shift_step=2)
     tmpl = tmpl_d.cpu().numpy().astype(np.float64)
-    ref = bmo.align(tmpl, parts[0].cpu().numpy().astype(np.float64), ocfg, wedge_deg=60.0)
-    assert got[0]["shift"] == ref["shift"]
-    assert bmo.geodesic_degrees(got[0]["quat"], ref["quat"]) < 0.5
-    assert got[0]["score"] == pytest.approx(ref["score"], rel=1e-4)
-    assert got[0]["bands"] == [4, 8, 16, 20]
+    for p in range(P):
+        ref = bmo.align(tmpl, parts[p].cpu().numpy().astype(np.float64), ocfg, wedge_deg=60.0)
+        assert got[p]["shift"] == ref["shift"]
+        assert bmo.geodesic_degrees(got[p]["quat"], ref["quat"]) < 0.5
+        assert got[p]["score"] == pytest.approx(ref["score"], rel=1e-4)
+        assert got[p]["bands"] == [4, 8, 16, 20]
 
 
 def test_align_batch_edge_counts(cuda_device):
