@@ -153,11 +153,20 @@ def test_wedge_power_kernel_matches_oracle(wedge_ctx):
     assert err < 1e-6, err
 
 
+def _off_pole(q, s):
+    keep = [r for r in range(len(q)) if 1e-6 < bmo.euler_zyz(q[r])[1] < math.pi - 1e-6]
+    return q[keep], s[keep]
+
+
 @pytest.mark.parametrize("wedge", [0.0, 60.0])
 def test_seed_candidates_match_oracle(cuda_device, wedge):
     """Identical FP32 expansions in: the device seed list (FP64 grid scores) equals
-    the oracle's -- same grid rotations in the same rank order -- except where two
-    oracle grid scores tie within 1e-9 relative."""
+    the oracle's -- same grid rotations in the same rank order, scores within 1e-9.
+    Grid points on the gimbal poles (beta = 0 or pi) form plateaus of one rotation
+    whose scores differ only by rounding; which plateau member survives the strict
+    local-maximum test (optimize.cpp:209-237) is decided by that rounding in the
+    reference as well (either side may keep zero, one or two members of a
+    plateau), so only the off-pole candidates are compared."""
     n, L = 64, 16
     tmpl = api.make_template(n, 40, 20250901)
     parts, _, _ = api.make_particles(tmpl, 6, 3000, 3, 0.1, wedge or None)
@@ -174,9 +183,9 @@ def test_seed_candidates_match_oracle(cuda_device, wedge):
         xi = bmo.xi_coefficients(f[p], t, spec)
         q, s, _ = bmo.seed_candidates(xi, L, 4, math.pi / 8, 24, wp, L if wedge else 0)
         gq, gs = got[p]
-        assert len(gq) == len(q), (p, len(gq), len(q))
-        for r in range(len(q)):
-            tie = any(abs(s[r] - s[o]) <= 1e-9 * abs(s[r]) for o in range(len(q)) if o != r)
-            if not tie:
-                assert np.allclose(gq[r], q[r], atol=1e-12) or np.allclose(gq[r], -q[r], atol=1e-12), (p, r)
-            assert abs(gs[r] - s[r]) <= 1e-9 * abs(s[r]) + 1e-12, (p, r, gs[r], s[r])
+        oq, os_ = _off_pole(q, s)
+        dq, ds = _off_pole(gq, gs)
+        assert len(dq) == len(oq), (p, len(dq), len(oq))
+        for r in range(len(oq)):
+            assert np.allclose(dq[r], oq[r], atol=1e-12) or np.allclose(dq[r], -oq[r], atol=1e-12), (p, r)
+            assert abs(ds[r] - os_[r]) <= 1e-9 * abs(os_[r]), (p, r, ds[r], os_[r])
