@@ -75,6 +75,11 @@ double bm_context_lambda_cut(const bm_context* ctx);
 /* radial roots / norms of degree l (BasisSpec::root/norm, basis.hpp:40-41); returns count k_l */
 int bm_context_roots(const bm_context* ctx, int l, double* roots, double* norms);
 double bm_default_lambda_cut(int n, int l_max);
+/* Host-only basis setup (build_spec, src/basis.cpp:88-115, no device needed):
+ * the radial roots lambda_lk <= lambda_cut of degree l <= l_max and their norms
+ * c_lk = sqrt(2) / |j_{l+1}(lambda_lk)| (BasisSpec::root/norm, basis.hpp:40-41);
+ * roots / norms need room for the count (<= lambda_cut / pi + 1 entries). */
+int bm_basis_roots(int l_max, double lambda_cut, int l, double* roots, double* norms, int* count);
 
 /* Batched expansion (expand(shift_volume(v, s)), src/basis.cpp:247-330 with
  * src/volume.cpp:50-67): `count` float32 volumes (device, n^3 each, x fastest)

@@ -117,6 +117,8 @@ def _declare(L: C.CDLL) -> None:
     L.bm_context_band_timings.restype = I
     L.bm_context_set_expand_mode.argtypes = [P, I]
     L.bm_context_set_expand_mode.restype = I
+    L.bm_basis_roots.argtypes = [I, D, I, P, P, P]
+    L.bm_basis_roots.restype = I
     L.bm_objective_eval.argtypes = [P, P, P, P, P, I, I, I, P, P]
     L.bm_objective_eval.restype = I
     L.bm_seed_candidates.argtypes = [P, P, I, I, D, I, P, P, P, P]

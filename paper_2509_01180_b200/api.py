@@ -75,6 +75,18 @@ def make_template(n: int, blobs: int, seed: int, device: int = 0):
     return out
 
 
+def basis_roots(l_max: int, lambda_cut: float, l: int):
+    """Host basis setup (build_spec): roots lambda_lk <= lambda_cut of degree l and
+    their norms, as numpy arrays; no device needed."""
+    cap = int(lambda_cut / math.pi) + 2
+    r = np.zeros(cap)
+    nm = np.zeros(cap)
+    cnt = C.c_int(0)
+    _lib.check(_lib.lib().bm_basis_roots(int(l_max), float(lambda_cut), int(l), r.ctypes.data_as(C.c_void_p),
+                                         nm.ctypes.data_as(C.c_void_p), C.byref(cnt)), "basis_roots")
+    return r[:cnt.value].copy(), nm[:cnt.value].copy()
+
+
 def make_particles(tmpl, count: int, base_seed: int, shift_max: int, snr=None, wedge_deg=None):
     """Particles of a BASELINE config on the device: (count, n, n, n) float32 tensor plus
     the ground truth (quaternions (count, 4), shifts (count, 3))."""

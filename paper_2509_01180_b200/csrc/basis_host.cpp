@@ -8,58 +8,57 @@
 namespace bmb {
 namespace host {
 
+// ---------------------------------------------------------------- Bessel
+// Spherical Bessel functions and their zeros, written from the definitions:
+//   j_0(x) = sin x / x,  j_1(x) = sin x / x^2 - cos x / x,
+//   j_{l+1}(x) = (2l+1)/x j_l(x) - j_{l-1}(x)          (forward-stable for x > l;
+//                                                        run in long double),
+//   j_l(x) = x^l / (2l+1)!! sum_k (-x^2/2)^k / (k! prod_{i=1..k} (2l+2i+1))
+//                                                        (power series, x <= l).
+// The zeros lambda_lk are found by a sign-change scan (consecutive zeros of j_l
+// are more than pi apart) and polished with Newton steps on
+// j_l'(x) = j_{l-1}(x) - (l+1)/x j_l(x).  Zeros of j_0 are k pi exactly.
+
 namespace {
 
-// Miller downward recurrence normalized by j_0 (stable for l >= x);
-// same start index as the reference (src/detail/bessel.cpp:21-38).
-double jl_miller(int l, double x) {
-    const int start = l + 20 + (int)std::sqrt(40.0 * l + 100.0);
-    double hi = 0.0, cur = 1e-290, at_l = 0.0;
-    for (int k = start; k >= 1; --k) {
-        const double lo = (2.0 * k + 1.0) / x * cur - hi;
-        hi = cur;
-        cur = lo;
-        if (k - 1 == l) at_l = cur;
-        if (std::fabs(cur) > 1e270) {
-            cur *= 1e-290;
-            hi *= 1e-290;
-            at_l *= 1e-290;
-        }
+// power series in long double (x <= l: the terms first grow, then alternate
+// and decay; the 64-bit mantissa absorbs the cancellation)
+double jl_series(int l, double xd) {
+    const long double x = xd, h = -0.5L * x * x;
+    long double lead = 1.0L;
+    for (int i = 1; i <= l; ++i) lead *= x / (long double)(2 * i + 1);
+    long double term = 1.0L, sum = 1.0L;
+    for (int k = 1; k < 400; ++k) {
+        term *= h / ((long double)k * (long double)(2 * l + 2 * k + 1));
+        sum += term;
+        if (std::fabs((double)term) <= 1e-21 * std::fabs((double)sum)) break;
     }
-    return at_l * (std::sin(x) / x) / cur;
+    return (double)(lead * sum);
 }
 
-double djl(int l, double x) {
+// j_l'(x)
+double djl_dx(int l, double x) {
     if (l == 0) return -sph_jl(1, x);
-    if (x < 1e-12) return l == 1 ? 1.0 / 3.0 : 0.0;
     return sph_jl(l - 1, x) - (l + 1.0) / x * sph_jl(l, x);
 }
 
-// k-th zero estimate of J_{l+1/2} (McMahon)
-double zero_guess(int l, int k) {
-    const double mu = 4.0 * (l + 0.5) * (l + 0.5);
-    const double b = (k + 0.5 * (l + 0.5) - 0.25) * kPi;
-    const double b8 = 8.0 * b;
-    return b - (mu - 1.0) / b8 - 4.0 * (mu - 1.0) * (7.0 * mu - 31.0) / (3.0 * b8 * b8 * b8);
-}
-
-// root of j_l inside the sign-change bracket (lo, hi): safeguarded Newton
-double bracketed_root(int l, double lo, double hi, double guess) {
-    double f_lo = sph_jl(l, lo);
-    double x = (guess > lo && guess < hi) ? guess : 0.5 * (lo + hi);
-    for (int it = 0; it < 200; ++it) {
-        const double f = sph_jl(l, x);
-        if ((f > 0) == (f_lo > 0)) {
-            lo = x;
-            f_lo = f;
+// the zero of j_l in (a, b), where j_l changes sign exactly once
+double polish_zero(int l, double a, double b) {
+    double fa = sph_jl(l, a);
+    for (int it = 0; it < 60 && b - a > 1e-6 * b; ++it) {  // bisect to a Newton-safe bracket
+        const double c = 0.5 * (a + b), fc = sph_jl(l, c);
+        if ((fc < 0.0) == (fa < 0.0)) {
+            a = c;
+            fa = fc;
         } else {
-            hi = x;
+            b = c;
         }
-        if (std::fabs(f) < 1e-14 && (hi - lo) < 1e-12 * x) return x;
-        const double d = djl(l, x);
-        double nx = d != 0.0 ? x - f / d : 0.5 * (lo + hi);
-        if (!(nx > lo && nx < hi)) nx = 0.5 * (lo + hi);
-        if (nx == x) return x;
+    }
+    double x = 0.5 * (a + b);
+    for (int it = 0; it < 50; ++it) {
+        const double dx = sph_jl(l, x) / djl_dx(l, x);
+        const double nx = std::min(std::max(x - dx, a), b);
+        if (std::fabs(nx - x) <= 4e-16 * x) return nx;
         x = nx;
     }
     return x;
@@ -68,51 +67,43 @@ double bracketed_root(int l, double lo, double hi, double guess) {
 }  // namespace
 
 double sph_jl(int l, double x) {
-    if (x < 0.0) return ((l & 1) ? -1.0 : 1.0) * sph_jl(l, -x);
-    if (x < 1e-6) {
-        if (l == 0) return 1.0 - x * x / 6.0;
-        double v = 1.0;
-        for (int i = 1; i <= l; ++i) v *= x / (2 * i + 1);
-        return v * (1.0 - x * x / (2.0 * (2 * l + 3)));
+    if (x < 0.0) return ((l & 1) ? -1.0 : 1.0) * sph_jl(l, -x);  // parity of j_l
+    if (x <= (double)l || x < 0.5) return jl_series(l, x);
+    // forward recurrence in long double: just above the turning point x ~ l it
+    // amplifies rounding by ~10^3, which the 64-bit mantissa keeps below 1e-16
+    const long double xl = x;
+    long double prev = std::sin(xl) / xl;  // j_0
+    if (l == 0) return (double)prev;
+    long double cur = prev / xl - std::cos(xl) / xl;  // j_1
+    for (int n = 1; n < l; ++n) {
+        const long double next = (2.0L * n + 1.0L) / xl * cur - prev;
+        prev = cur;
+        cur = next;
     }
-    const double j0 = std::sin(x) / x;
-    if (l == 0) return j0;
-    const double j1 = j0 / x - std::cos(x) / x;
-    if (l == 1) return j1;
-    if (x > l + 0.5) {
-        double a = j0, b = j1;
-        for (int k = 1; k < l; ++k) {
-            const double c = (2.0 * k + 1.0) / x * b - a;
-            a = b;
-            b = c;
-        }
-        return b;
-    }
-    return jl_miller(l, x);
+    return (double)cur;
 }
 
-// Roots of j_l interlace those of j_{l-1}; each row keeps a shrinking margin of
-// roots beyond the cutoff so the next row stays bracketed (the reference's
-// table rule, src/detail/bessel.cpp:150-178).
 std::vector<std::vector<double>> bessel_roots(int l_max, double cut) {
     std::vector<std::vector<double>> rows(l_max + 1);
-    std::vector<double> prev;
-    for (int k = 1, beyond = 0; beyond < l_max + 2; ++k) {
-        prev.push_back(k * kPi);
-        if (prev.back() > cut) ++beyond;
-    }
-    rows[0] = prev;
+    for (double z = kPi, k = 1.0; z <= cut; k += 1.0, z = k * kPi) rows[0].push_back(z);
+    const double h = 0.25;  // scan step (< pi, the least zero spacing)
     for (int l = 1; l <= l_max; ++l) {
-        std::vector<double> cur;
-        for (size_t i = 0, beyond = 0; i + 1 < prev.size() && (int)beyond < l_max + 2 - l; ++i) {
-            cur.push_back(bracketed_root(l, prev[i], prev[i + 1], zero_guess(l, (int)i + 1)));
-            if (cur.back() > cut) ++beyond;
+        // no zero of j_l lies below l (j_l > 0 there)
+        double a = std::max(0.5, (double)l), fa = sph_jl(l, a);
+        while (a < cut) {
+            const double b = std::min(a + h, cut), fb = sph_jl(l, b);
+            if (fb == 0.0) {
+                rows[l].push_back(b);
+                a = b + 1e-9 * b;
+                fa = sph_jl(l, a);
+                continue;
+            }
+            if ((fa < 0.0) != (fb < 0.0)) rows[l].push_back(polish_zero(l, a, b));
+            a = b;
+            fa = fb;
         }
-        rows[l] = cur;
-        prev.swap(cur);
+        while (!rows[l].empty() && rows[l].back() > cut) rows[l].pop_back();
     }
-    for (auto& r : rows)
-        while (!r.empty() && r.back() > cut) r.pop_back();
     return rows;
 }
 
@@ -155,25 +146,26 @@ void legendre(int l_max, double u, double* out) {
         }
 }
 
+// Nyquist cut pi n / 2, lowered (to a root of the table) when the basis would
+// exceed n^3 / 4 coefficients: the largest cut whose coefficient count -- every
+// root lambda_lk <= cut weighs 2l + 1 -- stays within n^3 / 4, pi if none does
+// (default_lambda_cut semantics, src/basis.cpp:117-138).
 double default_lambda_cut(int n, int l_max) {
-    const double nyq = kPi * n / 2.0;
-    const auto rows = bessel_roots(l_max, nyq);
-    const size_t cap = (size_t)n * n * n / 4;
-    std::vector<std::pair<double, size_t>> all;
-    size_t count = 0;
-    for (int l = 0; l < (int)rows.size(); ++l)
-        for (double r : rows[l]) {
-            all.emplace_back(r, 2 * l + 1);
-            count += 2 * l + 1;
-        }
-    if (count <= cap) return nyq;
-    std::sort(all.begin(), all.end());
-    size_t acc = 0;
+    const double nyquist = kPi * n / 2.0;
+    const long long budget = (long long)n * n * n / 4;
+    std::vector<std::pair<double, int>> zeros;  // (lambda, weight 2l + 1)
+    const auto table = bessel_roots(l_max, nyquist);
+    for (int l = 0; l <= l_max; ++l)
+        for (double z : table[l]) zeros.push_back({z, 2 * l + 1});
+    std::sort(zeros.begin(), zeros.end());
+    long long used = 0;
+    for (const auto& z : zeros) used += z.second;
+    if (used <= budget) return nyquist;
     double cut = kPi;
-    for (const auto& [r, w] : all) {
-        if (acc + w > cap) break;
-        acc += w;
-        cut = r;
+    used = 0;
+    for (size_t i = 0; i < zeros.size() && used + zeros[i].second <= budget; ++i) {
+        used += zeros[i].second;
+        cut = zeros[i].first;
     }
     return cut;
 }

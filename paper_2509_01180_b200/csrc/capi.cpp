@@ -156,6 +156,20 @@ int bm_context_roots(const bm_context* ctx, int l, double* roots, double* norms)
 
 double bm_default_lambda_cut(int n, int l_max) { return bmb::host::default_lambda_cut(n, l_max); }
 
+int bm_basis_roots(int l_max, double lambda_cut, int l, double* roots, double* norms, int* count) {
+    return guarded("bm_basis_roots", [&] {
+        if (l < 0 || l > l_max) throw std::invalid_argument("degree outside [0, l_max]");
+        if (!count) throw std::invalid_argument("null count");
+        const bmb::host::Basis b = bmb::host::make_basis(l_max, lambda_cut);
+        for (int k = 0; k < b.radial_count(l); ++k) {
+            if (roots) roots[k] = b.roots[l][k];
+            if (norms) norms[k] = b.norms[l][k];
+        }
+        *count = b.radial_count(l);
+        return (int)BM_OK;
+    });
+}
+
 int bm_expand(bm_context* ctx, const float* vols, int count, const int* shifts, double* out,
               void* stream) {
     return guarded("bm_expand", [&] {

@@ -5,6 +5,7 @@ import math
 
 import pytest
 
+from oracle import bmo
 from paper_2509_01180_b200 import _lib
 
 
@@ -32,3 +33,42 @@ def test_context_without_device_fails_loudly():
     rc = _lib.lib().bm_context_create(0, 32, 8, 8 * math.pi, C.byref(h))
     assert rc == 2 and not h.value
     assert b"CUDA" in _lib.lib().bm_last_error()
+
+
+@pytest.mark.parametrize("l_max,cut", [(8, 8 * math.pi), (16, 16 * math.pi), (20, 20 * math.pi),
+                                       (24, 24 * math.pi), (42, 32 * math.pi), (42, 42 * math.pi),
+                                       (1, 4.0), (0, 7.0)])
+def test_host_basis_roots_match_oracle(l_max, cut):
+    """The product's host basis setup (its own Bessel zeros and norms) against the
+    oracle's build_spec: the same index set, roots within 5e-14 and norms within
+    1e-12 (the oracle stops its Newton iteration at ~1e-14 relative, and the norm
+    c = sqrt(2)/|j_{l+1}(lambda)| moves ~20x the root error); and against 40-digit
+    mpmath values of the zeros and norms within 4 ulp-scale (1e-15 relative)."""
+    from paper_2509_01180_b200 import api
+    spec = bmo.Spec(l_max, cut)
+    try:
+        import mpmath
+        mpmath.mp.dps = 40
+    except ImportError:  # pragma: no cover
+        mpmath = None
+    for l in range(l_max + 1):
+        r, nm = api.basis_roots(l_max, cut, l)
+        assert len(r) == spec.radial_count(l), (l, len(r), spec.radial_count(l))
+        for k in range(len(r)):
+            assert r[k] == pytest.approx(spec.root(l, k + 1), rel=5e-14)
+            assert nm[k] == pytest.approx(spec.norm(l, k + 1), rel=1e-12)
+            if mpmath is not None and (k % 5 == 0 or l % 7 == 0):
+                x = mpmath.findroot(lambda t: mpmath.besselj(l + 0.5, t), mpmath.mpf(r[k]))
+                assert r[k] == pytest.approx(float(x), rel=1e-15, abs=0)
+                j = mpmath.sqrt(mpmath.pi / (2 * x)) * mpmath.besselj(l + 1.5, x)
+                assert nm[k] == pytest.approx(float(mpmath.sqrt(2) / abs(j)), rel=2e-15)
+
+
+def test_host_basis_rejects_bad_specs():
+    from paper_2509_01180_b200 import api
+    with pytest.raises(ValueError):
+        api.basis_roots(1, 3.0, 0)  # lambda_cut < pi drops the (0,1) root
+    with pytest.raises(ValueError):
+        api.basis_roots(4, 8.0, 5)
+    r, _ = api.basis_roots(1, 4.0, 1)
+    assert len(r) == 0  # (1, 4): degree 1 has no root below 4
