@@ -102,18 +102,107 @@ void check_cufft(cufftResult r, const char* what) {
 }  // namespace
 
 // smoothstep keep profile (wedge_keep_profile, xcorr.cpp:195-208), tilt axis y, beam z
-double keep_profile(double theta_deg, double nx, double ny, double nz, double taper_deg) {
-    (void)ny;
+__host__ __device__ double keep_profile_hd(double theta_deg, double nx, double nz, double taper_deg) {
+    const double pi = 3.14159265358979323846;
     if (theta_deg >= 90.0) return 1.0;
-    const double along = std::fabs(nz), in_plane = std::fabs(nx);
-    if (taper_deg <= 0.0) return along <= std::tan(theta_deg * kPiH / 180.0) * in_plane ? 1.0 : 0.0;
+    const double along = fabs(nz), in_plane = fabs(nx);
+    if (taper_deg <= 0.0) return along <= tan(theta_deg * pi / 180.0) * in_plane ? 1.0 : 0.0;
     if (along == 0.0 && in_plane == 0.0) return 1.0;
-    const double a = std::atan2(along, in_plane) * 180.0 / kPiH;
+    const double a = atan2(along, in_plane) * 180.0 / pi;
     const double x = (theta_deg - a) / taper_deg;
     if (x >= 1.0) return 1.0;
     if (x <= 0.0) return 0.0;
     return x * x * (3.0 - 2.0 * x);
 }
+double keep_profile(double theta_deg, double nx, double ny, double nz, double taper_deg) {
+    (void)ny;
+    return keep_profile_hd(theta_deg, nx, nz, taper_deg);
+}
+
+namespace {
+// Spherical-harmonic analysis of the directional power q and of the removed
+// fraction chi = 1 - keep on the (Gauss-Legendre u_t, uniform phi_p) sphere grid
+// (the analysis step of wedge_power_kernel, xcorr.cpp:317-341), in FP64 on the
+// device.  Stage 1, one CTA per ring t: the ring's phi-DFT of q and chi for every
+// order m (and the ring's share of the total power).  Stage 2, one thread per
+// packed (l, m): the Gauss-Legendre quadrature over the rings with the
+// fully-normalised P_l^m(u_t), recomputed per thread by its column recurrence.
+__global__ void ring_dft_kernel(const double* __restrict__ q, const double* __restrict__ u, int npf, int L,
+                                double theta_deg, double taper_deg, double2* __restrict__ gq,
+                                double2* __restrict__ gc, double* __restrict__ ring_q) {
+    const int t = blockIdx.x;
+    const double pi = 3.14159265358979323846;
+    const double st = sqrt(fmax(0.0, 1.0 - u[t] * u[t]));
+    const double* qr = q + (size_t)t * npf;
+    for (int m = threadIdx.x; m <= L; m += blockDim.x) {
+        double qr_re = 0.0, qr_im = 0.0, cr = 0.0, ci = 0.0;
+        for (int p = 0; p < npf; ++p) {
+            const double phi = 2.0 * pi * p / npf;
+            double sn, cs;
+            sincos(-m * phi, &sn, &cs);
+            double sp, cp;
+            sincos(phi, &sp, &cp);
+            const double chi = 1.0 - keep_profile_hd(theta_deg, st * cp, u[t], taper_deg);
+            qr_re += qr[p] * cs;
+            qr_im += qr[p] * sn;
+            cr += chi * cs;
+            ci += chi * sn;
+        }
+        gq[(size_t)t * (L + 1) + m] = make_double2(qr_re, qr_im);
+        gc[(size_t)t * (L + 1) + m] = make_double2(cr, ci);
+    }
+    if (threadIdx.x == 0) {
+        double acc = 0.0;
+        for (int p = 0; p < npf; ++p) acc += qr[p];
+        ring_q[t] = acc;
+    }
+}
+
+__global__ void sh_project_kernel(const double2* __restrict__ gq, const double2* __restrict__ gc,
+                                  const double* __restrict__ ring_q, const double* __restrict__ u,
+                                  const double* __restrict__ wu, int nt, int L, double wphi,
+                                  double2* __restrict__ q_hat, double2* __restrict__ chi_hat, double* total) {
+    const int ntri = (L + 1) * (L + 2) / 2;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == ntri) {  // the extra thread: total power sum_t w_t wphi sum_p q
+        double acc = 0.0;
+        for (int t = 0; t < nt; ++t) acc += ring_q[t] * wu[t] * wphi;
+        *total = acc;
+    }
+    if (i >= ntri) return;
+    int l = (int)((sqrt(8.0 * i + 1.0) - 1.0) / 2.0);
+    while ((l + 1) * (l + 2) / 2 <= i) ++l;
+    while (l * (l + 1) / 2 > i) --l;
+    const int m = i - l * (l + 1) / 2;
+    double aq_re = 0.0, aq_im = 0.0, ac_re = 0.0, ac_im = 0.0;
+    for (int t = 0; t < nt; ++t) {
+        // Pbar_l^m(u) by the column recurrence from Pbar_m^m (Condon-Shortley phase)
+        const double x = u[t], s = sqrt(fmax(0.0, 1.0 - x * x));
+        double pmm = 0.28209479177387814;  // 1/sqrt(4 pi)
+        for (int k = 1; k <= m; ++k) pmm = -sqrt((2.0 * k + 1.0) / (2.0 * k)) * s * pmm;
+        double pl = pmm;
+        if (l > m) {
+            double p0 = pmm, p1 = sqrt(2.0 * m + 3.0) * x * pmm;
+            for (int k = m + 2; k <= l; ++k) {
+                const double a = sqrt((4.0 * k * k - 1.0) / ((double)k * k - (double)m * m));
+                const double b = sqrt(((double)(k - 1) * (k - 1) - (double)m * m) / (4.0 * (double)(k - 1) * (k - 1) - 1.0));
+                const double p2 = a * (x * p1 - b * p0);
+                p0 = p1;
+                p1 = p2;
+            }
+            pl = p1;
+        }
+        const double w = pl * wu[t] * wphi;
+        const double2 a = gq[(size_t)t * (L + 1) + m], c = gc[(size_t)t * (L + 1) + m];
+        aq_re += a.x * w;
+        aq_im += a.y * w;
+        ac_re += c.x * w;
+        ac_im += c.y * w;
+    }
+    q_hat[i] = make_double2(aq_re, aq_im);
+    chi_hat[i] = make_double2(ac_re, ac_im);
+}
+}  // namespace
 
 WedgeFilter::WedgeFilter(int n_, double theta, double taper) : n(n_), theta_deg(theta), taper_deg(taper) {
     const int nh = n / 2 + 1;
@@ -225,38 +314,35 @@ WedgePowerFactors wedge_power_factors(const float* tmpl_dev, int n, int l_max, d
     cudaMemcpyAsync(dirs_d, dirs.data(), sizeof(double) * dirs.size(), cudaMemcpyHostToDevice, s);
     cudaMallocAsync(&q_d, sizeof(double) * nt * npf, s);
     power_rays_kernel<<<(nt * npf + 127) / 128, 128, 0, s>>>(pw, np, dirs_d, nt * npf, n_rad, q_d);
-    std::vector<double> q((size_t)nt * npf);
-    cudaMemcpyAsync(q.data(), q_d, sizeof(double) * q.size(), cudaMemcpyDeviceToHost, s);
-    cudaStreamSynchronize(s);
-    cufftDestroy(f);
-    cudaFree(pad);
-    cudaFree(half);
-    cudaFree(pw);
-    cudaFree(dirs_d);
-    cudaFree(q_d);
-    // spherical-harmonic analysis (xcorr.cpp:317-341)
-    std::vector<double> ptab(ntri);
-    const double wphi = 2.0 * kPiH / npf;
-    for (int t = 0; t < nt; ++t) {
-        host::legendre(l_max, u[t], ptab.data());
-        const double wt = wu[t];
-        for (int m = 0; m <= l_max; ++m) {
-            std::complex<double> gq{0, 0}, gc{0, 0};
-            for (int p = 0; p < npf; ++p) {
-                const std::complex<double> e = std::polar(1.0, -m * (2.0 * kPiH * p / npf));
-                const double* d = &dirs[((size_t)t * npf + p) * 3];
-                const double chi = 1.0 - keep_profile(theta_deg, d[0], d[1], d[2], taper_deg);
-                gq += q[(size_t)t * npf + p] * e;
-                gc += chi * e;
-            }
-            for (int l = m; l <= l_max; ++l) {
-                const double pwt = ptab[host::tri(l, m)] * wt * wphi;
-                wf.q_hat[host::tri(l, m)] += gq * pwt;
-                wf.chi_hat[host::tri(l, m)] += gc * pwt;
-            }
-        }
-        for (int p = 0; p < npf; ++p) wf.total += q[(size_t)t * npf + p] * wt * wphi;
+    // spherical-harmonic analysis on the device (ring_dft_kernel, sh_project_kernel)
+    double *u_d = nullptr, *wu_d = nullptr, *ring_d = nullptr, *total_d = nullptr;
+    double2 *gq_d = nullptr, *gc_d = nullptr, *qh_d = nullptr, *ch_d = nullptr;
+    cudaMallocAsync(&u_d, sizeof(double) * nt, s);
+    cudaMallocAsync(&wu_d, sizeof(double) * nt, s);
+    cudaMallocAsync(&ring_d, sizeof(double) * nt, s);
+    cudaMallocAsync(&total_d, sizeof(double), s);
+    cudaMallocAsync(&gq_d, sizeof(double2) * nt * (l_max + 1), s);
+    cudaMallocAsync(&gc_d, sizeof(double2) * nt * (l_max + 1), s);
+    cudaMallocAsync(&qh_d, sizeof(double2) * ntri, s);
+    cudaMallocAsync(&ch_d, sizeof(double2) * ntri, s);
+    cudaMemcpyAsync(u_d, u.data(), sizeof(double) * nt, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(wu_d, wu.data(), sizeof(double) * nt, cudaMemcpyHostToDevice, s);
+    ring_dft_kernel<<<nt, 64, 0, s>>>(q_d, u_d, npf, l_max, theta_deg, taper_deg, gq_d, gc_d, ring_d);
+    sh_project_kernel<<<((int)ntri + 1 + 127) / 128, 128, 0, s>>>(gq_d, gc_d, ring_d, u_d, wu_d, nt, l_max,
+                                                                 2.0 * kPiH / npf, qh_d, ch_d, total_d);
+    std::vector<double2> qh(ntri), ch(ntri);
+    cudaMemcpyAsync(qh.data(), qh_d, sizeof(double2) * ntri, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(ch.data(), ch_d, sizeof(double2) * ntri, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(&wf.total, total_d, sizeof(double), cudaMemcpyDeviceToHost, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess) throw std::runtime_error("wedge power kernel failed");
+    for (size_t i = 0; i < ntri; ++i) {
+        wf.q_hat[i] = {qh[i].x, qh[i].y};
+        wf.chi_hat[i] = {ch[i].x, ch[i].y};
     }
+    cufftDestroy(f);
+    for (void* p : {(void*)pad, (void*)half, (void*)pw, (void*)dirs_d, (void*)q_d, (void*)u_d, (void*)wu_d,
+                    (void*)ring_d, (void*)total_d, (void*)gq_d, (void*)gc_d, (void*)qh_d, (void*)ch_d})
+        cudaFree(p);
     return wf;
 }
 
