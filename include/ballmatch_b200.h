@@ -210,6 +210,29 @@ int bm_template_coeffs(bm_context* ctx, double* out, void* stream);
  * BM_ERR_STATE without a wedge. */
 int bm_wedge_power_kernel(bm_context* ctx, double* out);
 
+/* ------------------------------------------------------------------ reference operators
+ * FP64 device operators on the reference's layouts: coefficient sets complex128
+ * (degree blocks, row k, column m + l: BallExpansion, basis.hpp:67-91), kernels
+ * as XiBlocks (degree blocks l = 0..l_max of (2l+1)^2 entries [m][m'],
+ * xcorr.hpp:22-43).  All pointers are device memory unless noted. */
+/* xi_coefficients (src/xcorr.cpp:21-50): out[p] = xi(f[p], t), f: n sets, t: one set */
+int bm_xi_coefficients(bm_context* ctx, const double* f, int n, const double* t, double* out, void* stream);
+/* xi_compose_right (src/xcorr.cpp:149-155): out = xi D(a)^T for degrees <= l_limit
+ * (l_limit < 0: all), a = quat (host, w x y z) */
+int bm_xi_compose_right(bm_context* ctx, const double* xi, const double* quat, int l_limit, double* out,
+                        void* stream);
+/* rotate_expansion (src/steer.cpp:208-223): out = D(g) f per (k, l) row, g = quat (host) */
+int bm_rotate_expansion(bm_context* ctx, const double* f, const double* quat, double* out, void* stream);
+/* wigner_D (src/steer.cpp:158-178) for degrees <= L (host memory, XiBlocks layout) */
+int bm_wigner_D(int L, const double* quat, double* out);
+/* exhaustive_baseline (src/optimize.cpp:523-539): the first maximum of grid_scores
+ * at band l_cut on the full ZYZ grid of `angular_step` (EulerGrid::with_step) of
+ * one XiBlocks kernel (device); rotation (host quat), score and evaluation count. */
+int bm_exhaustive_baseline(bm_context* ctx, const double* xi, int l_cut, double angular_step, double* quat,
+                           double* score, long long* evaluations, void* stream);
+/* baseline_evaluation_count (src/optimize.cpp:541-544): na * nb * ng of the grid */
+long long bm_baseline_evaluation_count(double angular_step);
+
 /* Tapered missing-wedge filter of the current template's context on device
  * volumes (apply_wedge_taper, src/xcorr.cpp:210-232). */
 int bm_apply_wedge_taper(bm_context* ctx, const float* in, float* out, int count, void* stream);

@@ -1352,6 +1352,23 @@ bool outcome_better(const ShiftOutcome& a, const ShiftOutcome& b) {  // optimize
 }
 }  // namespace
 
+// exhaustive_baseline (optimize.cpp:523-539): first maximum of the full grid
+Baseline exhaustive_baseline(const Xi& xi, int l_cut, double step) {
+    if (!(step > 0.0)) throw std::invalid_argument("baseline: step must be positive");
+    const EulerGrid grid = EulerGrid::with_step(step);
+    const std::vector<double> sc = grid_scores_impl(xi, l_cut, grid);
+    size_t best = 0;
+    for (size_t i = 1; i < sc.size(); ++i)
+        if (sc[i] > sc[best]) best = i;
+    const int k = (int)(best % grid.ng), i = (int)((best / grid.ng) % grid.na), j = (int)(best / ((size_t)grid.ng * grid.na));
+    Baseline b;
+    b.rotation = Rot::from_euler_zyz(grid.alpha(i), grid.beta(j), grid.gamma(k));
+    b.score = sc[best];
+    b.evaluations = grid.size();
+    return b;
+}
+long baseline_evaluation_count(double step) { return EulerGrid::with_step(step).size(); }  // optimize.cpp:541-544
+
 std::vector<double> grid_scores(const Xi& xi, int l_cut, double step) {
     return grid_scores_impl(xi, l_cut, EulerGrid::with_step(step));
 }

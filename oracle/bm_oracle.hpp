@@ -232,6 +232,13 @@ struct Candidate {
     long flat_index = -1;
 };
 std::vector<double> grid_scores(const Xi& xi, int l_cut, double step);
+struct Baseline {  // BaselineResult (optimize.hpp:96-101)
+    Rot rotation;
+    double score = 0;
+    long evaluations = 0;
+};
+Baseline exhaustive_baseline(const Xi& xi, int l_cut, double step);
+long baseline_evaluation_count(double step);
 std::vector<Candidate> seed_candidates(const Xi& xi, int l_low, double step, int max_candidates,
                                        const Xi* wedge_power = nullptr);
 RefineResult refine(const Xi& xi, const Rot& start, const std::vector<int>& bands,

@@ -110,6 +110,8 @@ def lib():
             "bmo_corr_deriv_many": ([I, I, P, I, P, I, I, P, I], I),
             "bmo_xi_compose_right": ([I, P, P, I, P], None),
             "bmo_grid_scores": ([I, P, I, D, P], None),
+            "bmo_exhaustive_baseline": ([I, P, I, D, P, P, P], I),
+            "bmo_baseline_evaluation_count": ([D], LL),
             "bmo_seed_candidates": ([I, P, I, D, I, I, P, P, P, P], I),
             "bmo_refine": ([I, P, P, C.POINTER(Config), I, P, P, P, P, P, I, P, P], I),
             "bmo_energy_ratio": ([I, P, I, P], I),
@@ -563,3 +565,18 @@ def make_particle(tmpl, seed, shift_max, snr=None, wedge=None):
     _chk(lib().bmo_make_particle(t.shape[0], _p(t), seed, shift_max, snr or 0.0, wedge or 0.0,
                                  _p(s), _p(q), _p(sh)), "make_particle")
     return s, q, tuple(int(x) for x in sh)
+
+
+def exhaustive_baseline(xi, L, l_cut, step):
+    """exhaustive_baseline (src/optimize.cpp:523-539): (quat, score, evaluations)."""
+    x = np.ascontiguousarray(xi, dtype=np.complex128)
+    q = np.zeros(4)
+    sc = np.zeros(1)
+    ev = np.zeros(1, dtype=np.int64)
+    _chk(lib().bmo_exhaustive_baseline(L, _p(x), l_cut, step, _p(q), _p(sc), _p(ev)), "baseline")
+    return q, float(sc[0]), int(ev[0])
+
+
+def baseline_evaluation_count(step):
+    """baseline_evaluation_count (src/optimize.cpp:541-544)."""
+    return int(lib().bmo_baseline_evaluation_count(step))

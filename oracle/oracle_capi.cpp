@@ -270,6 +270,20 @@ int bmo_corr_deriv_many(int L, int n_xi, const double* xis, int n_rot, const dou
 void bmo_xi_compose_right(int L, const double* xi, const double* quat, int l_limit, double* out) {
     pack_xi(xi_compose_right(unpack_xi(L, xi), rot_of(quat), l_limit), out);
 }
+int bmo_exhaustive_baseline(int L, const double* xi, int l_cut, double step, double* quat, double* score,
+                            long long* evals) {
+    try {
+        const Baseline b = exhaustive_baseline(unpack_xi(L, xi), l_cut, step);
+        quat[0] = b.rotation.w, quat[1] = b.rotation.x, quat[2] = b.rotation.y, quat[3] = b.rotation.z;
+        *score = b.score;
+        *evals = b.evaluations;
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+long long bmo_baseline_evaluation_count(double step) { return baseline_evaluation_count(step); }
 void bmo_grid_scores(int L, const double* xi, int l_cut, double step, double* out) {
     auto s = grid_scores(unpack_xi(L, xi), l_cut, step);
     std::memcpy(out, s.data(), sizeof(double) * s.size());

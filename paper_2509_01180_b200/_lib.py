@@ -117,6 +117,18 @@ def _declare(L: C.CDLL) -> None:
     L.bm_context_band_timings.restype = I
     L.bm_context_set_expand_mode.argtypes = [P, I]
     L.bm_context_set_expand_mode.restype = I
+    L.bm_xi_coefficients.argtypes = [P, P, I, P, P, P]
+    L.bm_xi_coefficients.restype = I
+    L.bm_xi_compose_right.argtypes = [P, P, P, I, P, P]
+    L.bm_xi_compose_right.restype = I
+    L.bm_rotate_expansion.argtypes = [P, P, P, P, P]
+    L.bm_rotate_expansion.restype = I
+    L.bm_wigner_D.argtypes = [I, P, P]
+    L.bm_wigner_D.restype = I
+    L.bm_exhaustive_baseline.argtypes = [P, P, I, D, P, P, P, P]
+    L.bm_exhaustive_baseline.restype = I
+    L.bm_baseline_evaluation_count.argtypes = [D]
+    L.bm_baseline_evaluation_count.restype = C.c_longlong
     L.bm_basis_roots.argtypes = [I, D, I, P, P, P]
     L.bm_basis_roots.restype = I
     L.bm_objective_eval.argtypes = [P, P, P, P, P, I, I, I, P, P]

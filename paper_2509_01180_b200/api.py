@@ -87,6 +87,24 @@ def basis_roots(l_max: int, lambda_cut: float, l: int):
     return r[:cnt.value].copy(), nm[:cnt.value].copy()
 
 
+def xi_count(L: int) -> int:
+    return (L + 1) * (2 * L + 1) * (2 * L + 3) // 3
+
+
+def wigner_D(L: int, quat):
+    """wigner_D (src/steer.cpp:158-178) for degrees <= L: XiBlocks layout, numpy complex128."""
+    q = np.ascontiguousarray(quat, dtype=np.float64)
+    out = np.zeros(2 * xi_count(L))
+    _lib.check(_lib.lib().bm_wigner_D(int(L), q.ctypes.data_as(C.c_void_p), out.ctypes.data_as(C.c_void_p)),
+               "wigner_D")
+    return out.view(np.complex128)
+
+
+def baseline_evaluation_count(step: float) -> int:
+    """baseline_evaluation_count (src/optimize.cpp:541-544)."""
+    return int(_lib.lib().bm_baseline_evaluation_count(float(step)))
+
+
 def make_particles(tmpl, count: int, base_seed: int, shift_max: int, snr=None, wedge_deg=None):
     """Particles of a BASELINE config on the device: (count, n, n, n) float32 tensor plus
     the ground truth (quaternions (count, 4), shifts (count, 3))."""
@@ -308,6 +326,56 @@ class Context:
             self._stream(fa)), "seed_candidates")
         return [(q[i, :cnt[i]].copy(), sc[i, :cnt[i]].copy()) for i in range(n_f)]
 
+    def _c128(self, x):
+        torch = _torch()
+        return torch.view_as_real(torch.as_tensor(np.asarray(x) if not isinstance(x, torch.Tensor) else x,
+                                                  dtype=torch.complex128)).to(f"cuda:{self.device}").contiguous()
+
+    def xi_coefficients(self, f, t):
+        """xi_coefficients(f[p], t) (src/xcorr.cpp:21-50), FP64: complex (n, N_xi(l_max)) numpy."""
+        torch = _torch()
+        fa = self._c128(f)
+        if fa.dim() == 2:
+            fa = fa.unsqueeze(0)
+        ta = self._c128(t)
+        out = torch.empty((fa.shape[0], xi_count(self.l_max), 2), dtype=torch.float64, device=fa.device)
+        _lib.check(_lib.lib().bm_xi_coefficients(self._h, C.c_void_p(fa.data_ptr()), fa.shape[0],
+                                                 C.c_void_p(ta.data_ptr()), C.c_void_p(out.data_ptr()),
+                                                 self._stream(out)), "xi_coefficients")
+        return torch.view_as_complex(out).cpu().numpy()
+
+    def xi_compose_right(self, xi, quat, l_limit: int = -1):
+        """xi_compose_right (src/xcorr.cpp:149-155), FP64: complex N_xi(l_max) numpy."""
+        torch = _torch()
+        xa = self._c128(xi)
+        q = np.ascontiguousarray(quat, dtype=np.float64)
+        out = torch.empty_like(xa)
+        _lib.check(_lib.lib().bm_xi_compose_right(self._h, C.c_void_p(xa.data_ptr()), q.ctypes.data_as(C.c_void_p),
+                                                  int(l_limit), C.c_void_p(out.data_ptr()), self._stream(out)),
+                   "xi_compose_right")
+        return torch.view_as_complex(out).cpu().numpy()
+
+    def rotate_expansion(self, f, quat):
+        """rotate_expansion (src/steer.cpp:208-223), FP64: complex (coeff_count,) numpy."""
+        torch = _torch()
+        fa = self._c128(f)
+        q = np.ascontiguousarray(quat, dtype=np.float64)
+        out = torch.empty_like(fa)
+        _lib.check(_lib.lib().bm_rotate_expansion(self._h, C.c_void_p(fa.data_ptr()), q.ctypes.data_as(C.c_void_p),
+                                                  C.c_void_p(out.data_ptr()), self._stream(out)), "rotate_expansion")
+        return torch.view_as_complex(out).cpu().numpy()
+
+    def exhaustive_baseline(self, xi, l_cut: int, step: float):
+        """exhaustive_baseline (src/optimize.cpp:523-539) of one kernel: (quat, score, evaluations)."""
+        xa = self._c128(xi)
+        q = np.zeros(4)
+        sc = C.c_double()
+        ev = C.c_longlong()
+        _lib.check(_lib.lib().bm_exhaustive_baseline(self._h, C.c_void_p(xa.data_ptr()), int(l_cut), float(step),
+                                                     q.ctypes.data_as(C.c_void_p), C.byref(sc), C.byref(ev),
+                                                     self._stream(xa)), "exhaustive_baseline")
+        return q, sc.value, ev.value
+
     def template_coeffs(self):
         """t_hat of the current template (complex128 (coeff_count,), device)."""
         torch = _torch()
@@ -406,3 +474,42 @@ class Context:
         return (dict(zip(names, ms[:])),
                 dict(launches=cnt[0], windows_expanded=cnt[1], gemm_launches=cnt[2],
                      refine_launches=cnt[3]))
+
+
+def run_bench(ctx: "Context", subtomo, cfg, true_rotation=None, baseline_step_deg: float = 5.0,
+              baseline_band: int = 0, wedge: bool = False):
+    """run_bench (src/optimize.cpp:546-584): align one subtomogram against the
+    context's template, then the exhaustive grid baseline on the kernel of the
+    winning shift, and the accuracy-matched evaluation ratio
+    align_evaluations / |grid at max(align error, 0.01 deg)|.
+    wedge: the template state has a wedge (the particle is taper-filtered first)."""
+    import time
+    torch = _torch()
+    v = ctx._dev(subtomo)
+    t0 = time.perf_counter()
+    res = ctx.align_batch(v, cfg)[0]
+    torch.cuda.synchronize()
+    rep = {"alignment": res, "align_seconds": time.perf_counter() - t0,
+           "align_evaluations": int(res["evaluations"]), "baseline_step_deg": baseline_step_deg,
+           "baseline_band": baseline_band}
+    fw = ctx.apply_wedge_taper(v) if wedge else v
+    f_hat = ctx.expand(fw, [res["shift"]])
+    xi = ctx.xi_coefficients(f_hat, ctx.template_coeffs())[0]
+    t0 = time.perf_counter()
+    bq, bs, bn = ctx.exhaustive_baseline(xi, baseline_band, baseline_step_deg * math.pi / 180.0)
+    rep["baseline_seconds"] = time.perf_counter() - t0
+    rep["baseline"] = {"quat": bq, "score": bs, "evaluations": bn}
+
+    def geod(a, b):
+        return math.degrees(2.0 * math.acos(min(1.0, abs(float(np.dot(a, b))))))
+    if true_rotation is not None:
+        rep["align_error_deg"] = geod(res["quat"], true_rotation)
+        rep["baseline_error_deg"] = geod(bq, true_rotation)
+        rep["matched_step_deg"] = max(rep["align_error_deg"], 0.01)
+    else:
+        rep["align_error_deg"] = rep["baseline_error_deg"] = -1.0
+        rep["matched_step_deg"] = baseline_step_deg
+    rep["matched_evaluations"] = baseline_evaluation_count(rep["matched_step_deg"] * math.pi / 180.0)
+    rep["evaluation_ratio"] = rep["align_evaluations"] / rep["matched_evaluations"]
+    return rep
+

@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <complex>
 #include <cstring>
 #include <memory>
@@ -14,7 +15,10 @@
 #include "context.hpp"
 #include "average.hpp"
 #include "generate.hpp"
+#include "ops.hpp"
 #include "refine.cuh"
+#include "rotation.cuh"
+#include "tables.hpp"
 #include "wedge.hpp"
 
 namespace {
@@ -391,6 +395,130 @@ int bm_wedge_power_kernel(bm_context* ctx, double* out) {
                     out[2 * o] = w.real();
                     out[2 * o + 1] = w.imag();
                 }
+        return (int)BM_OK;
+    });
+}
+
+namespace {
+bmb::Euler3 euler_of(const double* q) {
+    return bmb::q_euler(bmb::q_normalized(q[0], q[1], q[2], q[3]));
+}
+// D^l(g) blocks on the device (scratch of the context)
+const double* device_wigner(bmb::Context& c, int L, const double* quat) {
+    const bmb::Euler3 e = euler_of(quat);
+    const std::vector<std::complex<double>> D = bmb::wigner_D_blocks(L, e.a, e.b, e.g);
+    c.work_xi.reserve(sizeof(double) * 2 * D.size());
+    cudaMemcpyAsync(c.work_xi.p, D.data(), sizeof(double) * 2 * D.size(), cudaMemcpyHostToDevice, c.stream);
+    return c.work_xi.as<double>();
+}
+long long xi_entries(int L) { return (long long)(L + 1) * (2 * L + 1) * (2 * L + 3) / 3; }
+struct Grid {
+    int na, nb, ng;
+    explicit Grid(double step) {  // EulerGrid::with_step (optimize.cpp:30-36)
+        const double pi = 3.14159265358979323846;
+        na = ng = (int)std::ceil(2.0 * pi / step);
+        nb = (int)std::ceil(pi / step) + 1;
+    }
+    double beta(int j) const { return nb > 1 ? 3.14159265358979323846 * j / (nb - 1) : 0.0; }
+};
+}  // namespace
+
+int bm_xi_coefficients(bm_context* ctx, const double* f, int n, const double* t, double* out, void* stream) {
+    return guarded("bm_xi_coefficients", [&] {
+        if (!ctx) return (int)BM_ERR_STATE;
+        if (n < 0 || (n > 0 && (!f || !t || !out))) throw std::invalid_argument("bad buffers");
+        if (n == 0) return (int)BM_OK;
+        auto& c = *ctx->impl;
+        cudaSetDevice(c.device);
+        StreamJoin join(ctx, stream);
+        if (bmb::launch_xi_coefficients(f, c.geo.coeffs, t, 0, n, c.geo.block_off, c.geo.radial_count,
+                                        c.basis.l_max, out, c.stream) != 0)
+            throw std::runtime_error("xi kernel launch failed");
+        return (int)BM_OK;
+    });
+}
+
+int bm_xi_compose_right(bm_context* ctx, const double* xi, const double* quat, int l_limit, double* out,
+                        void* stream) {
+    return guarded("bm_xi_compose_right", [&] {
+        if (!ctx) return (int)BM_ERR_STATE;
+        if (!xi || !quat || !out) throw std::invalid_argument("bad buffers");
+        auto& c = *ctx->impl;
+        cudaSetDevice(c.device);
+        StreamJoin join(ctx, stream);
+        const int L = c.basis.l_max;
+        const double* D = device_wigner(c, L, quat);
+        if (bmb::launch_xi_compose_right(xi, D, L, l_limit < 0 ? L : l_limit, out, c.stream) != 0)
+            throw std::runtime_error("compose kernel launch failed");
+        cudaStreamSynchronize(c.stream);  // the D scratch is reused by the next call
+        return (int)BM_OK;
+    });
+}
+
+int bm_rotate_expansion(bm_context* ctx, const double* f, const double* quat, double* out, void* stream) {
+    return guarded("bm_rotate_expansion", [&] {
+        if (!ctx) return (int)BM_ERR_STATE;
+        if (!f || !quat || !out) throw std::invalid_argument("bad buffers");
+        auto& c = *ctx->impl;
+        cudaSetDevice(c.device);
+        StreamJoin join(ctx, stream);
+        const int L = c.basis.l_max;
+        const double* D = device_wigner(c, L, quat);
+        if (bmb::launch_rotate_expansion(f, D, c.geo.block_off, c.geo.radial_count, L, c.geo.coeffs, out,
+                                         c.stream) != 0)
+            throw std::runtime_error("rotate kernel launch failed");
+        cudaStreamSynchronize(c.stream);
+        return (int)BM_OK;
+    });
+}
+
+int bm_wigner_D(int L, const double* quat, double* out) {
+    return guarded("bm_wigner_D", [&] {
+        if (L < 0 || L > bmb::kMaxL || !quat || !out) throw std::invalid_argument("bad arguments");
+        const bmb::Euler3 e = euler_of(quat);
+        const std::vector<std::complex<double>> D = bmb::wigner_D_blocks(L, e.a, e.b, e.g);
+        std::memcpy(out, D.data(), sizeof(double) * 2 * D.size());
+        return (int)BM_OK;
+    });
+}
+
+long long bm_baseline_evaluation_count(double angular_step) {
+    if (!(angular_step > 0.0)) return -1;
+    const Grid g(angular_step);
+    return (long long)g.na * g.nb * g.ng;
+}
+
+int bm_exhaustive_baseline(bm_context* ctx, const double* xi, int l_cut, double angular_step, double* quat,
+                           double* score, long long* evaluations, void* stream) {
+    return guarded("bm_exhaustive_baseline", [&] {
+        if (!ctx) return (int)BM_ERR_STATE;
+        if (!xi || !quat || !score) throw std::invalid_argument("bad buffers");
+        if (!(angular_step > 0.0)) throw std::invalid_argument("baseline: step must be positive");
+        auto& c = *ctx->impl;
+        if (l_cut < 0 || l_cut > c.basis.l_max) throw std::invalid_argument("baseline: band outside [0, l_max]");
+        cudaSetDevice(c.device);
+        StreamJoin join(ctx, stream);
+        const Grid g(angular_step);
+        std::vector<double> dgrid;
+        dgrid.reserve((size_t)g.nb * xi_entries(l_cut));
+        for (int j = 0; j < g.nb; ++j) {
+            const std::vector<double> d = bmb::little_d_full(l_cut, g.beta(j));
+            dgrid.insert(dgrid.end(), d.begin(), d.end());
+        }
+        bmb::upload(c.work_f, dgrid, c.stream);
+        c.filtered.reserve(bmb::exhaustive_scratch_bytes(l_cut, g.nb, g.ng));
+        double best = 0.0;
+        long long flat = 0;
+        if (bmb::launch_exhaustive(xi, c.work_f.as<double>(), c.basis.l_max, l_cut, g.na, g.nb, g.ng,
+                                   c.filtered.as<double>(), &best, &flat, c.stream) != 0)
+            throw std::runtime_error("baseline kernel launch failed");
+        if (cudaStreamSynchronize(c.stream) != cudaSuccess) throw std::runtime_error("baseline kernel failed");
+        const double pi = 3.14159265358979323846;
+        const int k = (int)(flat % g.ng), i = (int)((flat / g.ng) % g.na), j = (int)(flat / ((long long)g.ng * g.na));
+        const bmb::Quat q = bmb::q_from_euler(2.0 * pi * i / g.na, g.beta(j), 2.0 * pi * k / g.ng);
+        quat[0] = q.w, quat[1] = q.x, quat[2] = q.y, quat[3] = q.z;
+        *score = best;
+        if (evaluations) *evaluations = (long long)g.na * g.nb * g.ng;
         return (int)BM_OK;
     });
 }

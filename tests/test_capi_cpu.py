@@ -3,6 +3,7 @@ header declares, and refuses to run (loudly) without a CUDA device."""
 import ctypes as C
 import math
 
+import numpy as np
 import pytest
 
 from oracle import bmo
@@ -72,3 +73,18 @@ def test_host_basis_rejects_bad_specs():
         api.basis_roots(4, 8.0, 5)
     r, _ = api.basis_roots(1, 4.0, 1)
     assert len(r) == 0  # (1, 4): degree 1 has no root below 4
+
+
+def test_host_wigner_D_and_grid_count_match_oracle():
+    """wigner_D (steer.cpp:158-178) on the host and the baseline grid count
+    (optimize.cpp:541-544: ceil(2 pi/s)^2 (ceil(pi/s) + 1))."""
+    from paper_2509_01180_b200 import api
+    for s in range(3):
+        q = bmo.haar_rotation(5, s)
+        got = api.wigner_D(12, q)
+        ref = bmo.wigner_D(12, q)
+        assert np.abs(got - ref).max() <= 1e-12
+    for deg in (5.0, 6.0, 22.5, 0.5):
+        st = deg * math.pi / 180.0
+        na, nb = math.ceil(2 * math.pi / st), math.ceil(math.pi / st) + 1
+        assert api.baseline_evaluation_count(st) == na * na * nb == bmo.baseline_evaluation_count(st)

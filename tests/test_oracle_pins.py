@@ -607,3 +607,16 @@ def test_align_auto_bands_and_prune_after_band():
     assert tuple(r["shift"]) == sh and bmo.geodesic_degrees(r["quat"], q) < 0.5
     with pytest.raises(ValueError):
         bmo.align(tmpl, sub, bmo.make_config(l_max=L, bands=(), auto_bands=False))
+
+
+def test_exhaustive_baseline_count_and_self_peak():
+    """test_optimize.cpp:292-301: the grid has ceil(2pi/s)^2 (ceil(pi/s) + 1) points
+    and a template's self-correlation peaks within step * sqrt(3) of the identity."""
+    spec = bmo.Spec(8, 8 * PI)
+    t = bmo.expand(bmo.gaussian_blob_template(32, 10, 3), spec)
+    xi = bmo.xi_coefficients(t, t, spec)
+    step = 5.0 * PI / 180.0
+    q, _, n = bmo.exhaustive_baseline(xi, 8, 4, step)
+    na, nb = math.ceil(2 * PI / step), math.ceil(PI / step) + 1
+    assert n == na * na * nb == bmo.baseline_evaluation_count(step)
+    assert bmo.geodesic_degrees(q, [1.0, 0.0, 0.0, 0.0]) <= 5.0 * math.sqrt(3.0)
