@@ -32,8 +32,11 @@
 #include <optional>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <vector>
+#include <atomic>
+#include <exception>
 
 #include "ballmatch_b200.h"
 
@@ -638,6 +641,118 @@ private:
     detail::DeviceBuffer<double> sum_;
     long long count_ = 0;
 };
+
+#ifdef BALLMATCH_B200_WITH_NCCL
+// Multi-GPU alignment + averaging in ONE process: one
+// Aligner (context, template state) and one host thread per device, NCCL
+// communicators from ncclCommInitAll.  Particles are handed out in chunks from a
+// shared atomic counter (dynamic assignment: a device that draws cheap
+// particles -- fewer fine windows, shorter Newton runs -- simply takes more
+// chunks), each device accumulates the average numerator of its own particles,
+// and the only collective is the allreduce of those numerators and counts.
+class MultiDeviceAligner {
+public:
+    MultiDeviceAligner(const Volume& tmpl, const OptimizerConfig& cfg, const std::vector<int>& devices,
+                       const std::optional<WedgeMask>& wedge = std::nullopt, int chunk = 256)
+        : chunk_(chunk), devices_(devices) {
+        if (devices_.empty()) throw std::invalid_argument("multi-device: no devices");
+        if (chunk_ < 1) throw std::invalid_argument("multi-device: chunk must be >= 1");
+        for (int d : devices_) {
+            OptimizerConfig c = cfg;
+            c.device = d;
+            aligners_.push_back(std::make_unique<Aligner>(tmpl, c, wedge));
+        }
+        comms_.resize(devices_.size());
+        if (ncclCommInitAll(comms_.data(), static_cast<int>(devices_.size()), devices_.data()) != ncclSuccess)
+            throw std::runtime_error("multi-device: ncclCommInitAll failed");
+    }
+    ~MultiDeviceAligner() {
+        for (auto c : comms_)
+            if (c) ncclCommDestroy(c);
+    }
+    MultiDeviceAligner(const MultiDeviceAligner&) = delete;
+    MultiDeviceAligner& operator=(const MultiDeviceAligner&) = delete;
+
+    int devices() const { return static_cast<int>(devices_.size()); }
+    // particles each device aligned in the last call (load-balance evidence)
+    const std::vector<long long>& particles_per_device() const { return per_device_; }
+
+    // align every particle (results in input order) and leave the allreduced
+    // average numerator on every device
+    std::vector<AlignmentResult> align_and_average(const std::vector<Volume>& subtomos) {
+        const size_t total = subtomos.size();
+        std::vector<AlignmentResult> out(total);
+        std::atomic<size_t> next{0};
+        per_device_.assign(devices_.size(), 0);
+        std::vector<std::exception_ptr> err(devices_.size());
+        auto work = [&](size_t i) {
+            try {
+                detail::cuda(cudaSetDevice(devices_[i]), "cudaSetDevice");
+                Aligner& al = *aligners_[i];
+                const int n = subtomos.empty() ? 0 : subtomos[0].n;
+                const size_t vox = static_cast<size_t>(n) * n * n;
+                detail::DeviceBuffer<float> d(vox * static_cast<size_t>(chunk_));
+                std::vector<float> staging;
+                for (size_t p0; (p0 = next.fetch_add(static_cast<size_t>(chunk_))) < total;) {
+                    const size_t cnt = std::min<size_t>(static_cast<size_t>(chunk_), total - p0);
+                    staging.resize(vox * cnt);
+                    for (size_t k = 0; k < cnt; ++k) {
+                        const Volume& v = subtomos[p0 + k];
+                        if (v.n != n) throw std::invalid_argument("align: template and subtomogram grids differ");
+                        for (size_t x = 0; x < vox; ++x) staging[k * vox + x] = static_cast<float>(v.data[x]);
+                    }
+                    detail::cuda(cudaMemcpy(d.get(), staging.data(), staging.size() * sizeof(float),
+                                            cudaMemcpyHostToDevice), "H2D");
+                    auto r = al.align_batch_device(d.get(), static_cast<int>(cnt));
+                    al.accumulate_average_device(d.get(), static_cast<int>(cnt), r);
+                    for (size_t k = 0; k < cnt; ++k) out[p0 + k] = r[k];
+                    per_device_[i] += static_cast<long long>(cnt);
+                }
+                detail::cuda(cudaDeviceSynchronize(), "align");
+            } catch (...) {
+                err[i] = std::current_exception();
+            }
+        };
+        run_all(work);
+        for (auto& e : err)
+            if (e) std::rethrow_exception(e);
+        // the one collective: every device's numerator and count summed over devices
+        auto reduce = [&](size_t i) {
+            try {
+                detail::cuda(cudaSetDevice(devices_[i]), "cudaSetDevice");
+                aligners_[i]->allreduce_average(comms_[i], nullptr);
+            } catch (...) {
+                err[i] = std::current_exception();
+            }
+        };
+        run_all(reduce);
+        for (auto& e : err)
+            if (e) std::rethrow_exception(e);
+        return out;
+    }
+
+    // avg_hat of every particle aligned so far (device 0's allreduced numerator)
+    BallExpansion average() {
+        detail::cuda(cudaSetDevice(devices_[0]), "cudaSetDevice");
+        return aligners_[0]->average();
+    }
+    Aligner& aligner(int i) { return *aligners_.at(static_cast<size_t>(i)); }
+
+private:
+    template <class F>
+    void run_all(F& f) {
+        std::vector<std::thread> th;
+        for (size_t i = 1; i < devices_.size(); ++i) th.emplace_back(f, i);
+        f(0);
+        for (auto& t : th) t.join();
+    }
+    int chunk_;
+    std::vector<int> devices_;
+    std::vector<std::unique_ptr<Aligner>> aligners_;
+    std::vector<ncclComm_t> comms_;
+    std::vector<long long> per_device_;
+};
+#endif
 
 // align (optimize.cpp:423-521): one template, one subtomogram
 inline AlignmentResult align(const Volume& tmpl, const Volume& subtomo, const OptimizerConfig& cfg,

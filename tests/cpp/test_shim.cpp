@@ -11,6 +11,7 @@
 #include <string>
 #include <vector>
 
+#define BALLMATCH_B200_WITH_NCCL
 #include "ballmatch_b200.hpp"
 #include "bm_oracle.hpp"
 
@@ -199,6 +200,57 @@ static void average_matches_oracle() {
     CHECK(dot.real() / (t_hat.norm() * avg.norm()) > 0.5);
 }
 
+// One process, one thread per device, NCCL: the multi-device driver
+// gives the single-device results bit for bit and the same average, and the world-1
+// allreduce of Aligner::allreduce_average leaves the numerator unchanged.
+static void multi_device_matches_single() {
+#ifdef BALLMATCH_B200_WITH_NCCL
+    const auto tmpl = rounded(bmo::gaussian_blob_template(32, 20, 21));
+    bm::OptimizerConfig cfg;
+    cfg.l_max = 8;
+    cfg.lambda_cut = 8 * std::numbers::pi;
+    cfg.fixed_bands = {4, 8};
+    cfg.max_candidates = 8;
+    cfg.shift_radius = 2;
+    std::vector<bm::Volume> subs;
+    for (int p = 0; p < 7; ++p) subs.push_back(to_product(bmo::make_particle(tmpl, 950 + p, 2, 1.0, std::nullopt).sub));
+    bm::Aligner single(to_product(tmpl), cfg);
+    const auto ref = single.align_batch(subs);
+    single.accumulate_average(subs, ref);
+    const auto ref_avg = single.average();
+    // world-1 NCCL allreduce through Aligner::allreduce_average: same numerator and count
+    {
+        ncclComm_t comm;
+        int dev = 0;
+        CHECK(ncclCommInitAll(&comm, 1, &dev) == ncclSuccess);
+        single.allreduce_average(comm, nullptr);
+        CHECK(single.average_count() == 7);
+        CHECK(rel_l2(single.average().coeffs(), ref_avg.coeffs()) == 0.0);
+        ncclCommDestroy(comm);
+    }
+    int n_dev = 0;
+    cudaGetDeviceCount(&n_dev);
+    std::vector<int> devs;
+    for (int d = 0; d < std::min(n_dev, 8); ++d) devs.push_back(d);
+    bm::MultiDeviceAligner multi(to_product(tmpl), cfg, devs, std::nullopt, 2);  // chunks of 2 particles
+    const auto res = multi.align_and_average(subs);
+    for (size_t p = 0; p < subs.size(); ++p) {
+        CHECK(res[p].shift == ref[p].shift);
+        CHECK(res[p].rotation.w() == ref[p].rotation.w() && res[p].rotation.x() == ref[p].rotation.x());
+        CHECK(res[p].score == ref[p].score);
+    }
+    long long total = 0;
+    for (long long c : multi.particles_per_device()) total += c;
+    CHECK(total == 7);
+    const double err = rel_l2(multi.average().coeffs(), ref_avg.coeffs());
+    std::printf("  %d device(s), average rel L2 vs single device %.2e\n", (int)devs.size(), err);
+    CHECK(err < 1e-12);
+#else
+    std::printf("  built without BALLMATCH_B200_WITH_NCCL\n");
+    CHECK(false);
+#endif
+}
+
 // synthesize (basis.cpp:332-419) of the average against the oracle's, FP64 both sides
 static void synthesize_matches_oracle() {
     const auto tmpl = rounded(bmo::gaussian_blob_template(32, 20, 5));
@@ -257,6 +309,7 @@ int main() {
         {"expand_matches_oracle", expand_matches_oracle},
         {"align_matches_oracle", align_matches_oracle},
         {"average_matches_oracle", average_matches_oracle},
+        {"multi_device_matches_single", multi_device_matches_single},
         {"synthesize_matches_oracle", synthesize_matches_oracle},
         {"errors_match_reference", errors_match_reference},
     };
