@@ -54,6 +54,17 @@ def parse():
     return ap.parse_args()
 
 
+def eval_flops(L, order, wedge):
+    """Algorithmic FLOPs of one evaluation at band L (the library's eval_flops,
+    SURVEY.md §8(d) accounting generalised to orders 0/2 and the wedge kernel)."""
+    nxi = (L + 1) * (2 * L + 1) * (2 * L + 3) / 3.0
+    plane = (2 * L + 1) ** 2
+    nd = order + 1
+    nv = 1 if order == 0 else (4 if order == 1 else 10)
+    per_kernel = 4.0 * nd * nxi + 6.0 * nv * plane
+    return 6.0 * nd * nxi + per_kernel * (2.0 if wedge else 1.0)
+
+
 def fp32_simt_peak():
     """FP32 FMA throughput: profiles/fp32_peak.json (tools/probe_fp32_peak.cu measured on
     this pool's B200), else the nominal 148 SM x 128 lanes x 2 x 1.965 GHz."""
@@ -424,6 +435,24 @@ def run_product(args):
                                 "6*nv*(2L+1)^2) per kernel (x2 with the wedge), N_xi=(L+1)(2L+1)(2L+3)/3",
                  "traffic": None}
     roof_eval["frac"] = roof_eval["achieved"] / fp32_peak if roof_eval["achieved"] else None
+    # per-band evaluation counts and FLOPs of the instrumented step: achieved =
+    # flops_per_step / (eval_ms_per_step / 1000) is recomputable from this line
+    per_band, tot = {}, 0.0
+    for L in CFG["bands"]:
+        e2, e0 = ctx.eval_counts(L)
+        f2, f0 = e2 * eval_flops(L, 2, True), e0 * eval_flops(L, 0, True)
+        per_band[str(L)] = {"order2": e2, "order0": e0, "flop_order2": f2, "flop_order0": f0}
+        tot += f2 + f0
+    roof_eval["per_band"] = per_band
+    roof_eval["flops_per_step"] = tot
+    roof_eval["eval_ms_per_step"] = eval_ms
+    tr = ROOT / "profiles" / "round2" / "step_traffic_r2.json"
+    if tr.exists():
+        cls = json.loads(tr.read_text())["classes"]["eval"]
+        roof_eval["traffic"] = cls["dram_bytes"] * P / 1024.0
+        roof_eval["traffic_note"] = ("DRAM bytes (read + write) per step of the evaluation kernels, from "
+                                     "ncu over one config-2 step (profiles/round2/step_traffic_r2.json, "
+                                     "1024 particles, scaled to this batch; cold-cache per launch)")
     dominant = "refine" if refine_ms > gemm_ms else "expand"
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

@@ -85,10 +85,15 @@ def cfg4(n_p=512, n_g=4096, L=24):
     fc, tc = torch.view_as_complex(f), torch.view_as_complex(t)
     ms, _ = timed(lambda: ctx.eval_sweep(fc, tc, e), reps=3)
     nxi = (L + 1) * (2 * L + 1) * (2 * L + 3) // 3
-    flop = n_p * n_g * (20.0 * nxi + 24 * (2 * L + 1) ** 2)
+    # 8 N_xi + 24 (2L+1)^2 per (particle, rotation) unit, plus the
+    # d, d' recursion 12 N_xi once per rotation (amortised over the particles)
+    flop = n_p * n_g * (8.0 * nxi + 24 * (2 * L + 1) ** 2) + n_g * 12.0 * nxi
+    peak = json.loads((Path(__file__).resolve().parent.parent / "profiles" / "fp32_peak.json").read_text())
+    tf = flop / ms / 1e9
     print(json.dumps({"config": 4, "L": L, "particles": n_p, "rotations": n_g, "ms": ms,
-                      "evaluations_per_s": n_p * n_g / ms * 1e3, "algorithmic_tflops": flop / ms / 1e9,
-                      "flop_per_eval": "20 N_xi + 24 (2L+1)^2 (order 1: d, d' recursion + contraction + phases)"}),
+                      "evaluations_per_s": n_p * n_g / ms * 1e3, "algorithmic_tflops": tf,
+                      "frac_fp32_peak": tf / float(peak["fp32_fma_tflops"]),
+                      "flop_accounting": "SURVEY.md §8(d): n_p n_g (8 N_xi + 24 (2L+1)^2) + n_g 12 N_xi"}),
           flush=True)
 
 
