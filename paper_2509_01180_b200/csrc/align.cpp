@@ -300,12 +300,11 @@ void Context::refine_windows(int nw, int maxc, const AlignConfig& cfg, const Qua
             cudaEvent_t rb = timer.begin(stream);
             timer.band = (int)bi;
             cudaEvent_t x0 = timer.begin(stream);
-            if (launch_build_xi(xa, stream) != 0) throw std::runtime_error("build_xi launch failed");
-            xa.t = t_side.as<float>();
-            xa.out = xi_side_.as<float4>();
+            xa.t2 = t_side.as<float>();
+            xa.out2 = xi_side_.as<float4>();
             if (launch_build_xi(xa, stream) != 0) throw std::runtime_error("build_xi launch failed");
             timer.end(K_XI, x0, stream);
-            timer.launches += 2;
+            timer.launches += 1;
             a.xi_win = xi_win_.as<float4>();
             a.xi_side = xi_side_.as<float4>();
             a.cand = cand_.as<CandState>() + (size_t)w0 * maxc;

@@ -1151,6 +1151,72 @@ __global__ void __launch_bounds__(256) build_xi_staged_kernel(XiArgs a) {
         out[e] = xi_entry(a.T, a.row_group, fs, ts, a.block_off, a.radial_count, e >> 5, e & 31);
 }
 
+// xi_l[m,m'] against two templates (t and the side template u) at once: the
+// f loads are shared and the sign/conjugation of negative orders is applied to
+// the four raw k-sums after the loop:
+//   f_m = s_m (fr + i c_m fi), t_m' = s_m' (tr + i c_m' ti)  (s = (-1)^|m| for m < 0, c = -1 for m < 0)
+//   conj(f) t = s_m s_m' [(S_rr + c_m c_m' S_ii) + i (c_m' S_ri - c_m S_ir)]
+__device__ __forceinline__ void xi_value2(int l, int m, int mp, const float* f, const float* t, const float* u,
+                                          const int* block_off, const int* radial_count, float2& xt, float2& xu) {
+    const int nk = radial_count[l], base = block_off[l], w = 2 * l + 1;
+    const int am = abs(m), amp = abs(mp);
+    const int fo = base + (am ? 2 * am - 1 : 0), to = base + (amp ? 2 * amp - 1 : 0);
+    float rr = 0.f, ii = 0.f, ri = 0.f, ir = 0.f, urr = 0.f, uii = 0.f, uri = 0.f, uir = 0.f;
+    for (int k = 0; k < nk; ++k) {
+        const float fr = f[fo + k * w], fi = am ? f[fo + 1 + k * w] : 0.f;
+        const float tr = t[to + k * w], ti = amp ? t[to + 1 + k * w] : 0.f;
+        const float vr = u[to + k * w], vi = amp ? u[to + 1 + k * w] : 0.f;
+        rr = fmaf(fr, tr, rr);
+        ii = fmaf(fi, ti, ii);
+        ri = fmaf(fr, ti, ri);
+        ir = fmaf(fi, tr, ir);
+        urr = fmaf(fr, vr, urr);
+        uii = fmaf(fi, vi, uii);
+        uri = fmaf(fr, vi, uri);
+        uir = fmaf(fi, vr, uir);
+    }
+    const float sg = ((m < 0 && (am & 1)) ? -1.f : 1.f) * ((mp < 0 && (amp & 1)) ? -1.f : 1.f);
+    const float cm = m < 0 ? -1.f : 1.f, cp = mp < 0 ? -1.f : 1.f;
+    xt = make_float2(sg * fmaf(cm * cp, ii, rr), sg * (cp * ri - cm * ir));
+    xu = make_float2(sg * fmaf(cm * cp, uii, urr), sg * (cp * uri - cm * uir));
+}
+
+// window and side kernels of one coefficient set per CTA (f, t and the side
+// template staged in shared memory), written to out and out2
+__global__ void __launch_bounds__(256) build_xi_pair_kernel(XiArgs a) {
+    extern __shared__ __align__(16) float xs[];
+    const int np = (a.nf + 3) & ~3;
+    float* fs = xs;
+    float* ts = xs + np;
+    float* us = ts + np;
+    const float* f = a.f + (long long)blockIdx.x * a.ldf;
+    for (int i = threadIdx.x; i < a.nf; i += blockDim.x) {
+        fs[i] = f[i];
+        ts[i] = a.t[i];
+        us[i] = a.t2[i];
+    }
+    __syncthreads();
+    const size_t off = (size_t)blockIdx.x * a.T.rows * 32;
+    for (int e = threadIdx.x; e < a.T.rows * 32; e += blockDim.x) {
+        const int2 dsc = a.T.at_desc[e];
+        float4 o1 = make_float4(0.f, 0.f, 0.f, 0.f), o2 = o1;
+        if (dsc.x & 1) {
+            const int l = (dsc.x >> 2) & 63;
+            float2 x, y;
+            xi_value2(l, ((dsc.x >> 8) & 255) - 64, ((dsc.x >> 16) & 255) - 64, fs, ts, us, a.block_off,
+                      a.radial_count, x, y);
+            o1.x = x.x, o1.y = x.y, o2.x = y.x, o2.y = y.y;
+            if (dsc.x & 2) {
+                xi_value2(l, (dsc.y & 255) - 64, ((dsc.y >> 8) & 255) - 64, fs, ts, us, a.block_off, a.radial_count,
+                          x, y);
+                o1.z = x.x, o1.w = x.y, o2.z = y.x, o2.w = y.y;
+            }
+        }
+        a.out[off + e] = o1;
+        a.out2[off + e] = o2;
+    }
+}
+
 }  // namespace
 
 double eval_flops(int L, int order, bool wedge) {
@@ -1263,6 +1329,13 @@ int launch_eval_sweep(const EvalArgs& a, cudaStream_t s) {
 
 int launch_build_xi(const XiArgs& a, cudaStream_t s) {
     if (a.n <= 0) return 0;
+    if (a.t2) {  // window + side kernels in one pass
+        const size_t smem = sizeof(float) * 3 * (size_t)((a.nf + 3) & ~3);
+        if (a.ldt != 0 || a.nf <= 0 || smem > 200 * 1024 || !a.out2) return 1;
+        if (ensure_dynamic_smem(build_xi_pair_kernel, (int)smem) != cudaSuccess) return 2;
+        build_xi_pair_kernel<<<a.n, 256, smem, s>>>(a);
+        return cudaGetLastError() == cudaSuccess ? 0 : 2;
+    }
     const size_t smem = sizeof(float) * 2 * (size_t)((a.nf + 3) & ~3);
     if (a.nf > 0 && smem <= 200 * 1024) {
         if (ensure_dynamic_smem(build_xi_staged_kernel, (int)smem) != cudaSuccess) return 2;

@@ -110,6 +110,8 @@ struct XiArgs {
     const int* radial_count = nullptr;
     int n = 0;
     float4* out = nullptr;      // [n][T.rows*32]
+    const float* t2 = nullptr;  // optional second (shared) template: kernels of (f, t2) into out2
+    float4* out2 = nullptr;
     int nf = 0;                 // real-packed floats of degrees <= T.L (> 0: one CTA per set, rows staged in smem)
 };
 int launch_build_xi(const XiArgs& a, cudaStream_t s);
