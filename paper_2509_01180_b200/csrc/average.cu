@@ -34,15 +34,16 @@ __device__ __forceinline__ int dxi_off(int l) { return l * (2 * l - 1) * (2 * l 
 
 __global__ void average_kernel(const float* __restrict__ coef, int ldc, const double* __restrict__ quats,
                                int L, const int* __restrict__ block_off, const int* __restrict__ radial_count,
-                               double2* __restrict__ sum) {
+                               double2* __restrict__ sum, int count, double* __restrict__ dglob) {
     extern __shared__ double dsm[];
-    const int p = blockIdx.x;
+    // large L: the d stack in a per-CTA global scratch slice, CTAs loop over particles
+    for (int p = blockIdx.x; p < count; p += gridDim.x) {
     // rotation g^-1 and its ZYZ angles
     const Quat g{quats[4 * p], quats[4 * p + 1], quats[4 * p + 2], quats[4 * p + 3]};
     const Euler3 e = q_euler(q_inv(g));
     const double cb = cos(e.b), ch = cos(0.5 * e.b), sh = sin(0.5 * e.b);
     const int W = 2 * L + 1;
-    double* d = dsm;  // N_xi(L) full-plane little-d
+    double* d = dglob ? dglob + (size_t)blockIdx.x * dxi_off(L + 1) : dsm;  // N_xi(L) full-plane little-d
     for (int idx = threadIdx.x; idx < W * W; idx += blockDim.x) {
         const int m = idx / W - L, n = idx % W - L;
         const int l0 = max(abs(m), abs(n));
@@ -117,6 +118,8 @@ __global__ void average_kernel(const float* __restrict__ coef, int ldc, const do
         atomicAdd(&sum[o].x, ca * re + sa * im);
         atomicAdd(&sum[o].y, ca * im - sa * re);
     }
+    __syncthreads();  // d is rebuilt for the next particle
+    }
 }
 
 }  // namespace
@@ -125,11 +128,19 @@ void launch_average(const float* coef, int ldc, const double* quats, int count, 
                     const int* radial_count, double* sum, cudaStream_t s) {
     if (count <= 0) return;
     const size_t smem = sizeof(double) * (size_t)(L + 1) * (2 * L + 1) * (2 * L + 3) / 3;
-    if (smem > 200 * 1024) throw std::invalid_argument("average: band limit too large for the shared d stack");
-    if (ensure_dynamic_smem(average_kernel, (int)smem) != cudaSuccess)
-        throw std::runtime_error("average: shared-memory opt-in failed");
-    average_kernel<<<count, 256, smem, s>>>(coef, ldc, quats, L, block_off, radial_count,
-                                            reinterpret_cast<double2*>(sum));
+    if (smem <= 200 * 1024) {
+        if (ensure_dynamic_smem(average_kernel, (int)smem) != cudaSuccess)
+            throw std::runtime_error("average: shared-memory opt-in failed");
+        average_kernel<<<count, 256, smem, s>>>(coef, ldc, quats, L, block_off, radial_count,
+                                                reinterpret_cast<double2*>(sum), count, nullptr);
+    } else {  // large bases: d stacks in global scratch, 1024 CTAs
+        const int grid = count < 1024 ? count : 1024;
+        double* scratch = nullptr;
+        if (cudaMallocAsync(&scratch, smem * grid, s) != cudaSuccess) throw std::bad_alloc();
+        average_kernel<<<grid, 256, 0, s>>>(coef, ldc, quats, L, block_off, radial_count,
+                                            reinterpret_cast<double2*>(sum), count, scratch);
+        cudaFreeAsync(scratch, s);
+    }
     if (cudaGetLastError() != cudaSuccess) throw std::runtime_error("average kernel launch failed");
 }
 

@@ -350,6 +350,127 @@ __global__ void __launch_bounds__(kThreads, BMB_EXPAND_MINB) expand_factored_ker
     }
 }
 
+// ---------------------------------------------------------------- large bases
+// Bases beyond the register-resident specialisations (the paper's L = 42,
+// C = 34,949 at 64^3): stages 1-3 per radius write the packed theta output
+// G[w][i][(L+1)^2] to global memory (kernel A), then the radial contraction
+// out[w][row] = sum_i radial[i][pair(row)] G[w][i][lm(row)] runs as its own
+// kernel (B) with one thread per (window, row) -- no per-thread accumulator bound.
+__global__ void __launch_bounds__(kThreads) expand_theta_kernel(FactoredTables T, const float* __restrict__ vols,
+                                                                long long vol_stride, const int* __restrict__ win_vol,
+                                                                const int* __restrict__ win_shift, int w0,
+                                                                float* __restrict__ G, const float2* __restrict__ pairs) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const int n = T.n, L = T.L, nt = T.nt, np = T.np, half = np / 2, nl = L + 1, nsamp = nt * np;
+    float* samp = reinterpret_cast<float*>(sm);
+    float2* F = reinterpret_cast<float2*>(sm + al16(sizeof(float) * (size_t)nsamp));
+    const int w = w0 + blockIdx.x, tid = threadIdx.x;
+    const float* __restrict__ v = vols + (long long)win_vol[w] * vol_stride;
+    const float2* __restrict__ vp = pairs ? pairs + win_vol[w] * pair_volume_elems(n) : nullptr;
+    const int sx = win_shift[3 * w], sy = win_shift[3 * w + 1], sz = win_shift[3 * w + 2];
+    float* Gw = G + (size_t)blockIdx.x * T.nr * nl * nl;
+    for (int ir = 0; ir < T.nr; ++ir) {
+        for (int s = tid; s < nsamp; s += kThreads) {  // 1. trilinear samples of radius ir
+            const int4 e = __ldg(T.samp + (size_t)s * T.nr + ir);
+            const int x0 = e.x & 1023, y0 = (e.x >> 10) & 1023, z0 = (e.x >> 20) & 1023;
+            const float fx = __int_as_float(e.y), fy = __int_as_float(e.z), fz = __int_as_float(e.w);
+            const int xs0 = x0 + sx, ys0 = y0 + sy, zs0 = z0 + sz;
+            const bool vx0 = (unsigned)x0 < (unsigned)n && (unsigned)xs0 < (unsigned)n;
+            const bool vx1 = (unsigned)(x0 + 1) < (unsigned)n && (unsigned)(xs0 + 1) < (unsigned)n;
+            const bool vy0 = (unsigned)y0 < (unsigned)n && (unsigned)ys0 < (unsigned)n;
+            const bool vy1 = (unsigned)(y0 + 1) < (unsigned)n && (unsigned)(ys0 + 1) < (unsigned)n;
+            const bool vz0 = (unsigned)z0 < (unsigned)n && (unsigned)zs0 < (unsigned)n;
+            const bool vz1 = (unsigned)(z0 + 1) < (unsigned)n && (unsigned)(zs0 + 1) < (unsigned)n;
+            float val = 0.0f;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int bb = c & 1, aa = c >> 1;
+                const bool vr = (bb ? vy1 : vy0) && (aa ? vz1 : vz0);
+                float v0 = 0.0f, v1 = 0.0f;
+                if (vp) {
+                    const long long o = ((long long)(zs0 + aa) * n + ys0 + bb) * (n + 1) + xs0 + 1;
+                    const float2 pr = (vr && (vx0 || vx1)) ? __ldg(vp + o) : make_float2(0.0f, 0.0f);
+                    v0 = vx0 ? pr.x : 0.0f;
+                    v1 = vx1 ? pr.y : 0.0f;
+                } else {
+                    const float* row = v + ((long long)(zs0 + aa) * n + ys0 + bb) * n + xs0;
+                    v0 = (vr && vx0) ? __ldg(row) : 0.0f;
+                    v1 = (vr && vx1) ? __ldg(row + 1) : 0.0f;
+                }
+                const float wyz = (bb ? fy : 1.0f - fy) * (aa ? fz : 1.0f - fz);
+                val = fmaf(wyz, fmaf(fx, v1 - v0, v0), val);
+            }
+            samp[s] = val;
+        }
+        __syncthreads();
+        for (int q = tid; q < nt * nl; q += kThreads) {  // 2. folded phi-DFT per (ring, order)
+            const int t = q / nl, m = q - t * nl;
+            const float* f = samp + t * np;
+            float re = f[0] + ((m & 1) ? -f[half] : f[half]);
+            float im = 0.0f;
+            for (int p = 1; p < half; ++p) {
+                const float2 tw = __ldg(T.tw + p * nl + m);
+                const float a = f[p], b = f[np - p];
+                re = fmaf(a + b, tw.x, re);
+                im = fmaf(a - b, tw.y, im);
+            }
+            F[q] = make_float2(re, im);
+        }
+        __syncthreads();
+        float* Gr = Gw + (size_t)ir * nl * nl;
+        for (int q = tid; q < T.ntri; q += kThreads) {  // 3. folded theta contraction
+            const int2 lm = T.tri_lm[q];
+            const float sgn = ((lm.x + lm.y) & 1) ? -1.0f : 1.0f;
+            const float* pt = T.ptab + (size_t)q * nt;
+            float re = 0.0f, im = 0.0f;
+            for (int t = 0; t < nt / 2; ++t) {
+                const float2 a = F[t * nl + lm.y], b = F[(nt - 1 - t) * nl + lm.y];
+                const float wgt = __ldg(pt + t);
+                re = fmaf(wgt, fmaf(sgn, b.x, a.x), re);
+                im = fmaf(wgt, fmaf(sgn, b.y, a.y), im);
+            }
+            const int base = lm.x * lm.x;
+            if (lm.y == 0) {
+                Gr[base] = re;
+            } else {
+                Gr[base + 2 * lm.y - 1] = re;
+                Gr[base + 2 * lm.y] = im;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void expand_radial_kernel(FactoredTables T, const float* __restrict__ G, int w0, float* __restrict__ out,
+                                     int ldo) {
+    const int row = blockIdx.x * blockDim.x + threadIdx.x;
+    if (row >= T.coeffs) return;
+    const int nl2 = (T.L + 1) * (T.L + 1);
+    const int rp = __ldg(T.rowpack + row), pr = rp >> 16;
+    const float* g = G + (size_t)blockIdx.y * T.nr * nl2 + (rp & 0xffff);
+    float acc = 0.0f;
+    for (int i = 0; i < T.nr; ++i) acc = fmaf(__ldg(T.radial_t + (size_t)i * T.pairs + pr), g[(size_t)i * nl2], acc);
+    out[(long long)(w0 + blockIdx.y) * ldo + row] = acc;
+}
+
+int launch_split(const FactoredTables& T, const float* vols, long long vol_stride, const int* win_vol,
+                 const int* win_shift, int n_win, float* out, int ldo, cudaStream_t s, const float2* pairs) {
+    const size_t smem = al16(sizeof(float) * (size_t)T.nt * T.np) + sizeof(float2) * (size_t)T.nt * (T.L + 1);
+    if (smem > 220 * 1024) return 1;
+    if (ensure_dynamic_smem(expand_theta_kernel, (int)smem) != cudaSuccess) return 2;
+    const size_t per = sizeof(float) * (size_t)T.nr * (T.L + 1) * (T.L + 1);
+    const int chunk = (int)std::max<size_t>(1, std::min<size_t>((size_t)n_win, (size_t(2) << 30) / per));
+    float* G = nullptr;
+    if (cudaMallocAsync(&G, per * chunk, s) != cudaSuccess) return 2;
+    for (int w0 = 0; w0 < n_win; w0 += chunk) {
+        const int cnt = std::min(chunk, n_win - w0);
+        expand_theta_kernel<<<cnt, kThreads, smem, s>>>(T, vols, vol_stride, win_vol, win_shift, w0, G, pairs);
+        expand_radial_kernel<<<dim3((T.coeffs + 255) / 256, cnt), 256, 0, s>>>(T, G, w0, out, ldo);
+    }
+    cudaFreeAsync(G, s);
+    return cudaGetLastError() == cudaSuccess ? 0 : 2;
+}
+
 template <int HALF, int RPT, int NPC = 0>
 int launch_t(const FactoredTables& T, size_t smem, const float* vols, long long vol_stride, const int* win_vol,
              const int* win_shift, int n_win, float* out, int ldo, cudaStream_t s, const float2* pairs) {
@@ -392,7 +513,9 @@ int launch_expand_factored(const FactoredTables& T, const float* vols, long long
                            const float2* pairs) {
     if (n_win <= 0) return 0;
     const size_t smem = factored_smem_bytes(T);
-    if (smem > 220 * 1024) return 1;
+    const char* force = std::getenv("BMB_EXPAND_SPLIT");  // tests: the large-basis path at any size
+    if (smem > 220 * 1024 || T.L + 1 > kThreads || (force && std::atoi(force) != 0))
+        return launch_split(T, vols, vol_stride, win_vol, win_shift, n_win, out, ldo, s, pairs);
     const int half = T.np / 2, rpt = (T.coeffs + kThreads - 1) / kThreads;
     if (T.L + 1 > kThreads) return 1;
     static const bool cdft = [] {
@@ -410,7 +533,7 @@ int launch_expand_factored(const FactoredTables& T, const float* vols, long long
     if (half <= 21 && rpt <= 24) return launch_t<21, 24>(T, smem, vols, vol_stride, win_vol, win_shift, n_win, out, ldo, s, pairs);
     if (half <= 25 && rpt <= 40) return launch_t<25, 40>(T, smem, vols, vol_stride, win_vol, win_shift, n_win, out, ldo, s, pairs);
     if (half <= 33 && rpt <= 72) return launch_t<33, 72>(T, smem, vols, vol_stride, win_vol, win_shift, n_win, out, ldo, s, pairs);
-    return 1;  // larger bases: use the dense operator path (bm_context_set_expand_mode)
+    return launch_split(T, vols, vol_stride, win_vol, win_shift, n_win, out, ldo, s, pairs);
 }
 
 }  // namespace bmb

@@ -1183,19 +1183,27 @@ __device__ __forceinline__ void xi_value2(int l, int m, int mp, const float* f, 
 
 // window and side kernels of one coefficient set per CTA (f, t and the side
 // template staged in shared memory), written to out and out2
+// (STAGED false: large bases read f and the templates from global memory)
+template <bool STAGED>
 __global__ void __launch_bounds__(256) build_xi_pair_kernel(XiArgs a) {
     extern __shared__ __align__(16) float xs[];
     const int np = (a.nf + 3) & ~3;
-    float* fs = xs;
-    float* ts = xs + np;
-    float* us = ts + np;
     const float* f = a.f + (long long)blockIdx.x * a.ldf;
-    for (int i = threadIdx.x; i < a.nf; i += blockDim.x) {
-        fs[i] = f[i];
-        ts[i] = a.t[i];
-        us[i] = a.t2[i];
+    const float* fs = f;
+    const float* ts = a.t;
+    const float* us = a.t2;
+    if constexpr (STAGED) {
+        float* fw = xs;
+        float* tw = xs + np;
+        float* uw = tw + np;
+        for (int i = threadIdx.x; i < a.nf; i += blockDim.x) {
+            fw[i] = f[i];
+            tw[i] = a.t[i];
+            uw[i] = a.t2[i];
+        }
+        fs = fw, ts = tw, us = uw;
+        __syncthreads();
     }
-    __syncthreads();
     const size_t off = (size_t)blockIdx.x * a.T.rows * 32;
     for (int e = threadIdx.x; e < a.T.rows * 32; e += blockDim.x) {
         const int2 dsc = a.T.at_desc[e];
@@ -1331,9 +1339,13 @@ int launch_build_xi(const XiArgs& a, cudaStream_t s) {
     if (a.n <= 0) return 0;
     if (a.t2) {  // window + side kernels in one pass
         const size_t smem = sizeof(float) * 3 * (size_t)((a.nf + 3) & ~3);
-        if (a.ldt != 0 || a.nf <= 0 || smem > 200 * 1024 || !a.out2) return 1;
-        if (ensure_dynamic_smem(build_xi_pair_kernel, (int)smem) != cudaSuccess) return 2;
-        build_xi_pair_kernel<<<a.n, 256, smem, s>>>(a);
+        if (a.ldt != 0 || a.nf <= 0 || !a.out2) return 1;
+        if (smem <= 200 * 1024) {
+            if (ensure_dynamic_smem(build_xi_pair_kernel<true>, (int)smem) != cudaSuccess) return 2;
+            build_xi_pair_kernel<true><<<a.n, 256, smem, s>>>(a);
+        } else {
+            build_xi_pair_kernel<false><<<a.n, 256, 0, s>>>(a);
+        }
         return cudaGetLastError() == cudaSuccess ? 0 : 2;
     }
     const size_t smem = sizeof(float) * 2 * (size_t)((a.nf + 3) & ~3);

@@ -22,7 +22,8 @@ def main():
     parts, q, sh = api.make_particles(tmpl, P, 1000, 3, 0.1, 60.0)
     cfg = api.make_config(bands=(4, 8, 16), max_candidates=24, shift_radius=4, shift_step=2)
     ctx.set_lanes(lanes, 64)
-    ctx.align_batch(parts[:8], cfg)
+    if not os.environ.get("BMB_NO_WARMUP"):
+        ctx.align_batch(parts[:8], cfg)
     torch.cuda.synchronize()
     t0 = time.time()
     ctx.align_batch(parts, cfg)
