@@ -324,8 +324,9 @@ void Context::refine_windows(int nw, int maxc, const AlignConfig& cfg, const Qua
             a.prm.max_cand = maxc;
             a.prm.has_wedge = wedge ? 1 : 0;
             const long long slots = (long long)cnt * maxc;
-            lists_.reserve(sizeof(int) * 5 * (size_t)slots);
+            lists_.reserve(sizeof(int) * 6 * (size_t)slots);
             a.list2 = lists_.as<int>();
+            a.lists = a.list2 + 5 * slots;
             int* lt0 = a.list2 + slots;
             int* lt1 = lt0 + slots;
             int* ls[2] = {lt1 + slots, lt1 + 2 * slots};  // start lists (this / next iteration)
@@ -344,34 +345,44 @@ void Context::refine_windows(int nw, int maxc, const AlignConfig& cfg, const Qua
                 launch_iter_begin(a, ls[cur], d_start + cur, (int)std::max<long long>(1, start_max), stream);
                 timer.end(K_NEWTON, n2e, stream);
                 ++timer.launches;
-                ck(cudaMemcpyAsync(h_active, d_counts, sizeof(int), cudaMemcpyDeviceToHost, stream), "active");
+                ck(cudaMemcpyAsync(h_active, d_counts, sizeof(int) * 2, cudaMemcpyDeviceToHost, stream), "active");
                 ck(cudaStreamSynchronize(stream), "iteration");
-                const int n2 = h_active[0];
-                if (debug_iters_) fprintf(stderr, "[refine] band %d iter %d active %d\n", L, it, n2);
-                if (n2 == 0) break;
-                cudaEvent_t e2 = timer.begin(stream);
-                launch_eval(a, 2, a.list2, d_counts + CNT_L2, n2, stream);
-                timer.end(K_EVAL2, e2, stream);
+                const int n2 = h_active[CNT_L2], ns = h_active[CNT_STEP];
+                if (debug_iters_) fprintf(stderr, "[refine] band %d iter %d active %d evaluated %d\n", L, it, ns, n2);
+                if (ns == 0) break;
+                if (n2 > 0) {  // candidates without the order-2 results of an accepted trial
+                    cudaEvent_t e2 = timer.begin(stream);
+                    launch_eval(a, 2, a.list2, d_counts + CNT_L2, n2, stream);
+                    timer.end(K_EVAL2, e2, stream);
+                    ++timer.launches;
+                }
                 cudaEvent_t n0 = timer.begin(stream);
-                launch_step(a, lt0, d_counts + CNT_T0, n2, stream);
+                launch_step(a, lt0, d_counts + CNT_T0, ns, stream);
                 timer.end(K_NEWTON, n0, stream);
-                timer.launches += 2;
+                ++timer.launches;
                 for (int r = 0; r < 3; ++r) {
                     int* src = (r & 1) ? lt1 : lt0;
                     int* dst = (r & 1) ? lt0 : lt1;
                     int* csrc = d_counts + ((r & 1) ? CNT_T1 : CNT_T0);
                     int* cdst = d_counts + ((r & 1) ? CNT_T0 : CNT_T1);
+                    // trials at order 2: an accepted trial's derivatives serve the next iteration
                     cudaEvent_t e0 = timer.begin(stream);
-                    launch_eval(a, 0, src, csrc, n2, stream);
+                    launch_eval(a, 2, src, csrc, ns, stream, true);
                     timer.end(K_EVAL0, e0, stream);
                     ck(cudaMemsetAsync(cdst, 0, sizeof(int), stream), "retry count");
                     cudaEvent_t n1 = timer.begin(stream);
-                    launch_accept(a, src, csrc, dst, cdst, ls[cur ^ 1], d_start + (cur ^ 1), n2, stream);
+                    launch_accept(a, src, csrc, dst, cdst, ls[cur ^ 1], d_start + (cur ^ 1), ns, stream);
                     timer.end(K_NEWTON, n1, stream);
                     timer.launches += 2;
                 }
+                if (debug_iters_) {  // accepted trials of this iteration (next start list)
+                    int acc = 0;
+                    ck(cudaMemcpyAsync(&acc, d_start + (cur ^ 1), sizeof(int), cudaMemcpyDeviceToHost, stream), "dbg");
+                    ck(cudaStreamSynchronize(stream), "dbg");
+                    fprintf(stderr, "[refine] band %d iter %d accepted %d\n", L, it, acc);
+                }
                 cur ^= 1;
-                start_max = n2;  // accepted trials <= evaluated candidates
+                start_max = ns;  // accepted trials <= stepped candidates
             }
             const bool prune_now = cfg.prune_after_band && cfg.bands.size() > 1 && bi == 0;
             if (bi + 1 == cfg.bands.size() || prune_now) {

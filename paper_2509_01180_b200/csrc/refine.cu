@@ -617,7 +617,8 @@ __device__ void chart_transform(Derivs& f, const double* e, const double* ev) {
 // rotation h_try * a on the window kernel (C~(h) = C(h a), xcorr.cpp:149-155)
 // instead of streaming its private chart kernels; et holds those angles.
 __device__ __forceinline__ Quat qload(const double* q);
-__device__ void make_trial(CandWork& wk, const CandState& st) {
+__device__ __forceinline__ void choose_frame(const Quat& g, const Quat& koff, double* ev, int& side);
+__device__ void make_trial(CandWork& wk, const CandState& st, const Quat& koff) {
     double m[9];
     for (int i = 0; i < 9; ++i) m[i] = wk.f[4 + i];
     m[0] -= wk.lam;
@@ -641,8 +642,18 @@ __device__ void make_trial(CandWork& wk, const CandState& st) {
     }
     const Quat h = q_from_euler(wk.e[0] + p[0], wk.e[1] + p[1], wk.e[2] + p[2]);
     wk.gt[0] = h.w, wk.gt[1] = h.x, wk.gt[2] = h.y, wk.gt[3] = h.z;
-    const Euler3 et = q_euler(st.anchored ? q_mul(h, qload(st.anchor)) : h);
+    const Quat gt = st.anchored ? q_mul(h, qload(st.anchor)) : h;
+    const Euler3 et = q_euler(gt);
     wk.et[0] = et.a, wk.et[1] = et.b, wk.et[2] = et.g;
+    // frame of the trial's order-2 evaluation: the global angles (unanchored: the
+    // next iteration's chart angles exactly), or for an anchored candidate the
+    // better-conditioned of g and g K
+    if (st.anchored) {
+        choose_frame(gt, koff, wk.evt, wk.sidet);
+    } else {
+        wk.evt[0] = et.a, wk.evt[1] = et.b, wk.evt[2] = et.g;
+        wk.sidet = 0;
+    }
 }
 
 __device__ __forceinline__ Quat qload(const double* q) { return Quat{q[0], q[1], q[2], q[3]}; }
@@ -660,6 +671,7 @@ __device__ __forceinline__ void band_begin_one(const StageArgs& a, long long i) 
     CandWork& wk = a.work[i];
     wk.iter = 0;
     wk.retry = 0;
+    wk.fresh = 0;
     wk.status = ST_DONE;
     CandState& st = a.cand[i];
     if (!st.active || st.diverged) return;
@@ -686,6 +698,7 @@ __global__ void band_begin_kernel(StageArgs a, int* start, int* start_count) {
                 CandWork& wk = a.work[i];
                 wk.iter = 0;
                 wk.retry = 0;
+                wk.fresh = 0;
                 wk.status = ST_DONE;
             } else {
                 band_begin_one(a, i);
@@ -699,52 +712,69 @@ __global__ void band_begin_kernel(StageArgs a, int* start, int* start_count) {
 // order-2 evaluation frame of an anchored candidate at global rotation g: the
 // window kernel at E(g), or the side kernels at E(g K), whichever is further from
 // its gimbal pole (chart_transform)
-__device__ __forceinline__ void set_eval_frame(CandWork& wk, const Quat& g, const Quat& koff) {
+__device__ __forceinline__ void choose_frame(const Quat& g, const Quat& koff, double* ev, int& side) {
     const Euler3 eg = q_euler(g);
     const Euler3 ek = q_euler(q_mul(g, koff));
-    const bool side = fabs(sin(ek.b)) > fabs(sin(eg.b));
-    const Euler3& ev = side ? ek : eg;
-    wk.ev[0] = ev.a, wk.ev[1] = ev.b, wk.ev[2] = ev.g;
-    wk.side = side ? 2 : 1;
+    const bool use_side = fabs(sin(ek.b)) > fabs(sin(eg.b));
+    const Euler3& e = use_side ? ek : eg;
+    ev[0] = e.a, ev[1] = e.b, ev[2] = e.g;
+    side = use_side ? 2 : 1;
+}
+__device__ __forceinline__ void set_eval_frame(CandWork& wk, const Quat& g, const Quat& koff) {
+    choose_frame(g, koff, wk.ev, wk.side);
 }
 
 // iteration start of candidate i (chart and re-anchor decision,
-// optimize.cpp:292-298): true = evaluate at order 2.  Anchored candidates pick
-// the kernel and angles of their order-2 evaluation (chart_transform).
-__device__ __forceinline__ bool iter_begin_one(const StageArgs& a, long long i) {
+// optimize.cpp:292-298): 0 = no step, 1 = evaluate at order 2 first, 2 = step on
+// the order-2 results of the accepted trial (already at g).  Anchored candidates
+// pick the kernel and angles of their order-2 evaluation (chart_transform).
+__device__ __forceinline__ int iter_begin_one(const StageArgs& a, long long i) {
     CandWork& wk = a.work[i];
-    if (wk.status != ST_START) return false;
+    if (wk.status != ST_START) return 0;
     if (wk.iter >= a.prm.newton_max_iter) {
         wk.status = ST_DONE;
-        return false;
+        return 0;
     }
     CandState& st = a.cand[i];
     const Quat g = qload(st.g);
     const Quat koff{a.prm.koffset[0], a.prm.koffset[1], a.prm.koffset[2], a.prm.koffset[3]};
+    const bool was_anchored = st.anchored != 0;
     Euler3 e = q_euler(q_mul(g, q_inv(qload(st.anchor))));
+    bool reanchored = false;
     if (e.b < 0.05 || e.b > kPiD - 0.05) {
         qstore(st.anchor, q_mul(q_inv(koff), g));
         st.anchor_limit = a.prm.band;
         st.anchored = 1;
+        reanchored = true;
         e = q_euler(koff);
     }
     wk.e[0] = e.a, wk.e[1] = e.b, wk.e[2] = e.g;
-    wk.side = 0;
-    if (st.anchored) set_eval_frame(wk, g, koff);
     wk.status = ST_EVAL2;
     ++wk.iter;
-    return true;
+    // the accepted trial's derivatives are in its own frame: the global angles of g
+    // (unanchored -- exactly this iteration's chart angles unless the candidate
+    // anchors right now, when that frame sits at a pole) or a well-conditioned
+    // anchored frame (any chart of g follows by chart_transform)
+    if (wk.fresh && (was_anchored || !reanchored)) {
+        wk.fresh = 0;
+        return 2;
+    }
+    wk.fresh = 0;
+    wk.side = 0;
+    if (st.anchored) set_eval_frame(wk, g, koff);
+    return 1;
 }
 
 // iteration start of the candidates on the start list (band start, or accepted
-// trials of the previous iteration); appends to the order-2 list
+// trials of the previous iteration); appends to the order-2 list and the step list
 __global__ void iter_begin_kernel(StageArgs a, const int* start, const int* start_count) {
     const int n = *start_count;
     const int n_pad = (n + 31) & ~31;
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_pad; q += gridDim.x * blockDim.x) {
         const int i = q < n ? start[q] : -1;
-        const bool f = i >= 0 && iter_begin_one(a, i);
-        wappend(f, i, a.list2, a.counts + CNT_L2);
+        const int f = i >= 0 ? iter_begin_one(a, i) : 0;
+        wappend(f == 1, i, a.list2, a.counts + CNT_L2);
+        wappend(f != 0, i, a.lists, a.counts + CNT_STEP);
     }
 }
 
@@ -802,7 +832,7 @@ __device__ __forceinline__ void eval_group(const BandTables& T, const EvalJob (&
 #define BMB_EVAL_MINB2 4
 #endif
 #define BMB_EVAL_MINB(order) ((order) == 2 ? BMB_EVAL_MINB2 : BMB_EVAL_MINB0)
-template <int ORDER, int K>
+template <int ORDER, int K, bool TRIAL = false>
 __global__ void __launch_bounds__(EvalShape<K>::WARPS * 32, BMB_EVAL_MINB(ORDER)) eval_kernel(StageArgs a, const int* list,
                                                                                        const int* count) {
     constexpr int WARPS = EvalShape<K>::WARPS;
@@ -827,10 +857,11 @@ __global__ void __launch_bounds__(EvalShape<K>::WARPS * 32, BMB_EVAL_MINB(ORDER)
         // order 2 (status EVAL2): chart angles e, or for an anchored candidate the
         // angles ev of g (window kernel) or of g K (side kernels); order 0 (trials,
         // final scores): global angles et on the window kernel
-        const int side = ORDER == 2 ? wk.side : 0;
+        // (TRIAL: order 2 at the trial point in its frame evt / sidet)
+        const int side = ORDER == 2 ? (TRIAL ? wk.sidet : wk.side) : 0;
         job[k].xi = (side == 2 ? a.xi_side : a.xi_win) + (size_t)w * len;
         job[k].wx = !wedge ? nullptr : (side == 2 ? a.T.wedge_side : a.T.wedge);
-        const double* e = ORDER == 2 ? (side ? wk.ev : wk.e) : wk.et;
+        const double* e = ORDER == 2 ? (TRIAL ? (side ? wk.evt : wk.et) : (side ? wk.ev : wk.e)) : wk.et;
         job[k].a = e[0], job[k].b = e[1], job[k].g = e[2];
     }
     WarpScratch* ws = wsc + warp * K;
@@ -870,17 +901,17 @@ __device__ __forceinline__ bool step_one(const StageArgs& a, long long i) {
     }
     wk.lam = wk.lambda;
     wk.retry = 0;
-    make_trial(wk, st);
+    make_trial(wk, st, Quat{a.prm.koffset[0], a.prm.koffset[1], a.prm.koffset[2], a.prm.koffset[3]});
     wk.status = ST_EVAL0;
     return true;
 }
 
 // Newton step of every order-2 evaluated candidate; appends trials to list_out
 __global__ void step_kernel(StageArgs a, int* list_out, int* count_out) {
-    const int n = a.counts[CNT_L2];
+    const int n = a.counts[CNT_STEP];
     const int n_pad = (n + 31) & ~31;
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_pad; q += gridDim.x * blockDim.x) {
-        const int i = q < n ? a.list2[q] : -1;
+        const int i = q < n ? a.lists[q] : -1;
         const bool t = i >= 0 && step_one(a, i);
         wappend(t, i, list_out, count_out);
     }
@@ -891,13 +922,17 @@ __device__ __forceinline__ bool accept_one(const StageArgs& a, long long i) {
     CandWork& wk = a.work[i];
     CandState& st = a.cand[i];
     Derivs t;
-    objective(wk.c, wk.r, a.prm.has_wedge != 0, 0, t);
+    objective(wk.c, wk.r, a.prm.has_wedge != 0, 0, t);  // the value (the trial ran at order 2)
     ++st.evals;
     const double scale = fmax(fabs(wk.f[0]), 1e-300);
     // tolerant acceptance (optimize.cpp:330-341)
     if (t.v > wk.f[0] - a.prm.accept_tol * scale) {
         qstore(st.g, q_mul(qload(wk.gt), qload(st.anchor)));
         wk.lambda = fmax(wk.lam / 10.0, 1e-12);
+        // the trial's order-2 results are the next iteration's evaluation at g
+        wk.ev[0] = wk.evt[0], wk.ev[1] = wk.evt[1], wk.ev[2] = wk.evt[2];
+        wk.side = wk.sidet;
+        wk.fresh = 1;
         if (t.v > st.best_score) {
             st.best_score = t.v;
             for (int k = 0; k < 4; ++k) st.best_g[k] = st.g[k];
@@ -912,7 +947,7 @@ __device__ __forceinline__ bool accept_one(const StageArgs& a, long long i) {
         wk.status = ST_DONE;
         return false;
     }
-    make_trial(wk, st);
+    make_trial(wk, st, Quat{a.prm.koffset[0], a.prm.koffset[1], a.prm.koffset[2], a.prm.koffset[3]});
     return true;
 }
 
@@ -1268,16 +1303,19 @@ static int eval_k_for(int order, int /*max_n*/) {
     return order == 2 ? k2 : k0;
 }
 
-template <int ORDER, int K>
+template <int ORDER, int K, bool TRIAL = false>
 static void launch_eval_k(const StageArgs& a, const int* list, const int* count, int max_n, cudaStream_t s) {
     constexpr int per = K * EvalShape<K>::WARPS;
-    eval_kernel<ORDER, K><<<(max_n + per - 1) / per, EvalShape<K>::WARPS * 32, 0, s>>>(a, list, count);
+    eval_kernel<ORDER, K, TRIAL><<<(max_n + per - 1) / per, EvalShape<K>::WARPS * 32, 0, s>>>(a, list, count);
 }
 
-void launch_eval(const StageArgs& a, int order, const int* list, const int* count, int max_n, cudaStream_t s) {
+void launch_eval(const StageArgs& a, int order, const int* list, const int* count, int max_n, cudaStream_t s,
+                 bool trial) {
     if (max_n <= 0) return;
     const int k = eval_k_for(order, max_n);
-    if (order == 2) {
+    if (order == 2 && trial) {
+        launch_eval_k<2, 1, true>(a, list, count, max_n, s);
+    } else if (order == 2) {
         if (k >= 2) launch_eval_k<2, 2>(a, list, count, max_n, s);
         else launch_eval_k<2, 1>(a, list, count, max_n, s);
     } else {

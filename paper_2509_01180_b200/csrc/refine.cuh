@@ -25,6 +25,9 @@ struct CandWork {
     int iter;
     int side;       // order-2 evaluation: 0 chart angles e on the window kernel (unanchored),
                     // 1 angles of g on the window kernel, 2 angles of g K on the side kernels
+    double evt[3];  // frame of the trial's order-2 evaluation (same convention, sidet)
+    int sidet;
+    int fresh;      // c / r hold the order-2 results of the accepted trial at g (frame ev, side)
 };
 
 struct StageArgs {
@@ -40,9 +43,10 @@ struct StageArgs {
     RefineParams prm;
     int* counts = nullptr;           // [CNT_*] list lengths
     int* list2 = nullptr;            // candidates awaiting the order-2 evaluation (or final)
+    int* lists = nullptr;            // candidates taking a Newton step this iteration (list2 + reused)
     unsigned long long* eval_stats = nullptr;  // [kMaxL+1][2][2] evaluations by (L, order, wedge)
 };
-enum { CNT_L2 = 0, CNT_T0 = 2, CNT_T1 = 3 };
+enum { CNT_L2 = 0, CNT_STEP = 1, CNT_T0 = 2, CNT_T1 = 3 };
 
 // one window outcome per window (last band)
 struct ReduceArgs {
@@ -63,7 +67,11 @@ struct ReduceArgs {
 void launch_band_begin(const StageArgs& a, int* start, int* start_count, cudaStream_t s);
 // iteration start of the candidates on a start list (max_n bounds its length)
 void launch_iter_begin(const StageArgs& a, const int* start, const int* start_count, int max_n, cudaStream_t s);
-void launch_eval(const StageArgs& a, int order, const int* list, const int* count, int max_n, cudaStream_t s);
+// order 2 at the iteration point (trial = false) or at the trial point (trial = true,
+// the refinement's trials: their derivatives serve the next iteration when accepted);
+// order 0 at the global angles et (final scores)
+void launch_eval(const StageArgs& a, int order, const int* list, const int* count, int max_n, cudaStream_t s,
+                 bool trial = false);
 void launch_step(const StageArgs& a, int* list_out, int* count_out, int max_n, cudaStream_t s);
 void launch_accept(const StageArgs& a, const int* list_in, const int* count_in, int* list_out, int* count_out,
                    int* start_out, int* start_count, int max_n, cudaStream_t s);
