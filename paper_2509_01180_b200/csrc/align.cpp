@@ -324,70 +324,65 @@ void Context::refine_windows(int nw, int maxc, const AlignConfig& cfg, const Qua
             a.prm.max_cand = maxc;
             a.prm.has_wedge = wedge ? 1 : 0;
             const long long slots = (long long)cnt * maxc;
-            lists_.reserve(sizeof(int) * 6 * (size_t)slots);
-            a.list2 = lists_.as<int>();
-            a.lists = a.list2 + 5 * slots;
-            int* lt0 = a.list2 + slots;
-            int* lt1 = lt0 + slots;
-            int* ls[2] = {lt1 + slots, lt1 + 2 * slots};  // start lists (this / next iteration)
-            int* d_start = d_counts + 6;                    // their counts
+            // lists: fresh[2] (candidates whose iteration needs an order-2 evaluation at g),
+            // trial[2] (pending trials), start (band start); counts d_counts[0..1] fresh,
+            // [2..3] trial, [4] start
+            lists_.reserve(sizeof(int) * 5 * (size_t)slots);
+            int* lbase = lists_.as<int>();
+            int* fresh[2] = {lbase, lbase + slots};
+            int* trial[2] = {lbase + 2 * slots, lbase + 3 * slots};
+            int* start = lbase + 4 * slots;
+            int* c_fresh[2] = {d_counts, d_counts + 1};
+            int* c_trial[2] = {d_counts + 2, d_counts + 3};
+            int* c_start = d_counts + 4;
+            a.list2 = fresh[0];  // iter_begin / final_prep append to list2 with count CNT_L2 = c_fresh[0]
             a.counts = d_counts;
             a.eval_stats = eval_stats();
-            ck(cudaMemsetAsync(d_start, 0, sizeof(int) * 2, stream), "start counts");
-            launch_band_begin(a, ls[0], d_start, stream);
+            ck(cudaMemsetAsync(d_counts, 0, sizeof(int) * 5, stream), "counts");
+            cudaEvent_t b0 = timer.begin(stream);
+            launch_band_begin(a, start, c_start, stream);
+            launch_iter_begin(a, start, c_start, (int)slots, stream);  // band start: all need an evaluation
+            timer.end(K_NEWTON, b0, stream);
+            timer.launches += 2;
+            // rounds: evaluate and step the fresh candidates, evaluate every pending trial
+            // at order 2, then accept / retry / advance each to its next iteration
             int cur = 0;
-            long long start_max = slots;
-            ++timer.launches;
-            for (int it = 0; it < cfg.newton_max_iter; ++it) {
-                ck(cudaMemsetAsync(d_counts, 0, sizeof(int) * 4, stream), "counts");
-                cudaEvent_t n2e = timer.begin(stream);
-                ck(cudaMemsetAsync(d_start + (cur ^ 1), 0, sizeof(int), stream), "next start count");
-                launch_iter_begin(a, ls[cur], d_start + cur, (int)std::max<long long>(1, start_max), stream);
-                timer.end(K_NEWTON, n2e, stream);
-                ++timer.launches;
-                ck(cudaMemcpyAsync(h_active, d_counts, sizeof(int) * 2, cudaMemcpyDeviceToHost, stream), "active");
-                ck(cudaStreamSynchronize(stream), "iteration");
-                const int n2 = h_active[CNT_L2], ns = h_active[CNT_STEP];
-                if (debug_iters_) fprintf(stderr, "[refine] band %d iter %d active %d evaluated %d\n", L, it, ns, n2);
-                if (ns == 0) break;
-                if (n2 > 0) {  // candidates without the order-2 results of an accepted trial
+            const int max_rounds = 4 * cfg.newton_max_iter + 8;
+            for (int round = 0; round < max_rounds; ++round) {
+                ck(cudaMemcpyAsync(h_active, d_counts, sizeof(int) * 4, cudaMemcpyDeviceToHost, stream), "active");
+                ck(cudaStreamSynchronize(stream), "round");
+                const int nf = h_active[cur], nt = h_active[2 + cur];
+                if (debug_iters_) fprintf(stderr, "[refine] band %d round %d fresh %d trials %d\n", L, round, nf, nt);
+                if (nf == 0 && nt == 0) break;
+                ck(cudaMemsetAsync(c_fresh[cur ^ 1], 0, sizeof(int), stream), "next fresh count");
+                ck(cudaMemsetAsync(c_trial[cur ^ 1], 0, sizeof(int), stream), "next trial count");
+                if (nf > 0) {
                     cudaEvent_t e2 = timer.begin(stream);
-                    launch_eval(a, 2, a.list2, d_counts + CNT_L2, n2, stream);
+                    launch_eval(a, 2, fresh[cur], c_fresh[cur], nf, stream);
                     timer.end(K_EVAL2, e2, stream);
-                    ++timer.launches;
+                    cudaEvent_t n0 = timer.begin(stream);
+                    launch_step(a, fresh[cur], c_fresh[cur], trial[cur], c_trial[cur], nf, stream);
+                    timer.end(K_NEWTON, n0, stream);
+                    timer.launches += 2;
                 }
-                cudaEvent_t n0 = timer.begin(stream);
-                launch_step(a, lt0, d_counts + CNT_T0, ns, stream);
-                timer.end(K_NEWTON, n0, stream);
-                ++timer.launches;
-                for (int r = 0; r < 3; ++r) {
-                    int* src = (r & 1) ? lt1 : lt0;
-                    int* dst = (r & 1) ? lt0 : lt1;
-                    int* csrc = d_counts + ((r & 1) ? CNT_T1 : CNT_T0);
-                    int* cdst = d_counts + ((r & 1) ? CNT_T0 : CNT_T1);
-                    // trials at order 2: an accepted trial's derivatives serve the next iteration
+                const int nt_max = nt + nf;
+                if (nt_max > 0) {
                     cudaEvent_t e0 = timer.begin(stream);
-                    launch_eval(a, 2, src, csrc, ns, stream, true);
+                    launch_eval(a, 2, trial[cur], c_trial[cur], nt_max, stream, true);
                     timer.end(K_EVAL0, e0, stream);
-                    ck(cudaMemsetAsync(cdst, 0, sizeof(int), stream), "retry count");
                     cudaEvent_t n1 = timer.begin(stream);
-                    launch_accept(a, src, csrc, dst, cdst, ls[cur ^ 1], d_start + (cur ^ 1), ns, stream);
+                    launch_advance(a, trial[cur], c_trial[cur], trial[cur ^ 1], c_trial[cur ^ 1], fresh[cur ^ 1],
+                                   c_fresh[cur ^ 1], nt_max, stream);
                     timer.end(K_NEWTON, n1, stream);
                     timer.launches += 2;
                 }
-                if (debug_iters_) {  // accepted trials of this iteration (next start list)
-                    int acc = 0;
-                    ck(cudaMemcpyAsync(&acc, d_start + (cur ^ 1), sizeof(int), cudaMemcpyDeviceToHost, stream), "dbg");
-                    ck(cudaStreamSynchronize(stream), "dbg");
-                    fprintf(stderr, "[refine] band %d iter %d accepted %d\n", L, it, acc);
-                }
                 cur ^= 1;
-                start_max = ns;  // accepted trials <= stepped candidates
             }
             const bool prune_now = cfg.prune_after_band && cfg.bands.size() > 1 && bi == 0;
             if (bi + 1 == cfg.bands.size() || prune_now) {
                 // final unanchored score at the top band (optimize.cpp:349-352), or at
                 // the first band before prune_after_band keeps each window's winner
+                a.list2 = fresh[0];
                 ck(cudaMemsetAsync(d_counts, 0, sizeof(int), stream), "final count");
                 launch_final_prep(a, stream);
                 cudaEvent_t ef = timer.begin(stream);

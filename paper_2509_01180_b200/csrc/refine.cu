@@ -774,7 +774,6 @@ __global__ void iter_begin_kernel(StageArgs a, const int* start, const int* star
         const int i = q < n ? start[q] : -1;
         const int f = i >= 0 ? iter_begin_one(a, i) : 0;
         wappend(f == 1, i, a.list2, a.counts + CNT_L2);
-        wappend(f != 0, i, a.lists, a.counts + CNT_STEP);
     }
 }
 
@@ -907,11 +906,24 @@ __device__ __forceinline__ bool step_one(const StageArgs& a, long long i) {
 }
 
 // Newton step of every order-2 evaluated candidate; appends trials to list_out
-__global__ void step_kernel(StageArgs a, int* list_out, int* count_out) {
-    const int n = a.counts[CNT_STEP];
+// resident CTAs per SM the thread-per-candidate Newton kernels are compiled for
+// (0: no register cap; their FP64 chains are latency-bound)
+#ifndef BMB_NEWTON_MINB
+#define BMB_NEWTON_MINB 0
+#endif
+#if BMB_NEWTON_MINB > 0
+#define BMB_NEWTON_BOUNDS __launch_bounds__(BMB_NEWTON_BLOCK_SIZE, BMB_NEWTON_MINB)
+#else
+#define BMB_NEWTON_BOUNDS
+#endif
+#ifndef BMB_NEWTON_BLOCK_SIZE
+#define BMB_NEWTON_BLOCK_SIZE 32
+#endif
+__global__ void BMB_NEWTON_BOUNDS step_kernel(StageArgs a, const int* list_in, const int* count_in, int* list_out, int* count_out) {
+    const int n = *count_in;
     const int n_pad = (n + 31) & ~31;
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_pad; q += gridDim.x * blockDim.x) {
-        const int i = q < n ? a.lists[q] : -1;
+        const int i = q < n ? list_in[q] : -1;
         const bool t = i >= 0 && step_one(a, i);
         wappend(t, i, list_out, count_out);
     }
@@ -951,19 +963,32 @@ __device__ __forceinline__ bool accept_one(const StageArgs& a, long long i) {
     return true;
 }
 
-// acceptance test of every trial in list_in; failed trials with retries left
-// are re-queued in list_out
-// acceptance test of every trial in list_in; failed trials with retries left
-// are re-queued in list_out, accepted ones join the next iteration's start list
-__global__ void accept_kernel(StageArgs a, const int* list_in, const int* count_in, int* list_out,
-                              int* count_out, int* start_out, int* start_count) {
+// One Newton round of every pending trial: the acceptance test; an accepted
+// trial starts the candidate's next iteration right away (iter_begin_one) and,
+// with the trial's own order-2 results, takes its Newton step (step_one) -- the
+// new trial joins trial_out; a candidate whose iteration needs a fresh order-2
+// evaluation (it just anchored) joins fresh_out; a rejected trial with retries
+// left is re-queued with its damped retry.  The per-candidate sequence is the
+// reference's (optimize.cpp:291-346); only the interleaving across candidates
+// differs from a lock-step iteration.
+__global__ void BMB_NEWTON_BOUNDS advance_kernel(StageArgs a, const int* list_in, const int* count_in, int* trial_out, int* trial_count,
+                               int* fresh_out, int* fresh_count) {
     const int n = *count_in;
     const int n_pad = (n + 31) & ~31;
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_pad; q += gridDim.x * blockDim.x) {
         const int i = q < n ? list_in[q] : -1;
-        const bool rq = i >= 0 && accept_one(a, i);
-        wappend(rq, i, list_out, count_out);
-        wappend(i >= 0 && !rq && a.work[i].status == ST_START, i, start_out, start_count);
+        bool trial = false, fresh = false;
+        if (i >= 0) {
+            if (accept_one(a, i)) {
+                trial = true;  // damped retry
+            } else if (a.work[i].status == ST_START) {
+                const int f = iter_begin_one(a, i);
+                if (f == 2) trial = step_one(a, i);
+                else fresh = f == 1;
+            }
+        }
+        wappend(trial, i, trial_out, trial_count);
+        wappend(fresh, i, fresh_out, fresh_count);
     }
 }
 
@@ -1273,10 +1298,7 @@ double eval_flops(int L, int order, bool wedge) {
 
 // thread-per-candidate bookkeeping kernels: small CTAs so that a few thousand
 // candidates still spread over every SM (these kernels are latency-bound)
-#ifndef BMB_NEWTON_BLOCK
-#define BMB_NEWTON_BLOCK 32
-#endif
-constexpr int kNB = BMB_NEWTON_BLOCK;
+constexpr int kNB = BMB_NEWTON_BLOCK_SIZE;
 static int thread_grid(long long n) {
     long long b = (n + kNB - 1) / kNB;
     return (int)(b < 1 ? 1 : (b > 16384 ? 16384 : b));
@@ -1324,13 +1346,14 @@ void launch_eval(const StageArgs& a, int order, const int* list, const int* coun
         else launch_eval_k<0, 1>(a, list, count, max_n, s);
     }
 }
-void launch_step(const StageArgs& a, int* list_out, int* count_out, int max_n, cudaStream_t s) {
-    step_kernel<<<thread_grid(max_n), kNB, 0, s>>>(a, list_out, count_out);
+void launch_step(const StageArgs& a, const int* list_in, const int* count_in, int* list_out, int* count_out,
+                 int max_n, cudaStream_t s) {
+    step_kernel<<<thread_grid(max_n), kNB, 0, s>>>(a, list_in, count_in, list_out, count_out);
 }
-void launch_accept(const StageArgs& a, const int* list_in, const int* count_in, int* list_out, int* count_out,
-                   int* start_out, int* start_count, int max_n, cudaStream_t s) {
-    accept_kernel<<<thread_grid(max_n), kNB, 0, s>>>(a, list_in, count_in, list_out, count_out, start_out,
-                                                     start_count);
+void launch_advance(const StageArgs& a, const int* list_in, const int* count_in, int* trial_out, int* trial_count,
+                    int* fresh_out, int* fresh_count, int max_n, cudaStream_t s) {
+    advance_kernel<<<thread_grid(max_n), kNB, 0, s>>>(a, list_in, count_in, trial_out, trial_count, fresh_out,
+                                                      fresh_count);
 }
 void launch_final_prep(const StageArgs& a, cudaStream_t s) {
     final_prep_kernel<<<thread_grid((long long)a.n_win * a.max_cand), kNB, 0, s>>>(a);

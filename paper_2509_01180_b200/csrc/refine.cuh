@@ -43,7 +43,6 @@ struct StageArgs {
     RefineParams prm;
     int* counts = nullptr;           // [CNT_*] list lengths
     int* list2 = nullptr;            // candidates awaiting the order-2 evaluation (or final)
-    int* lists = nullptr;            // candidates taking a Newton step this iteration (list2 + reused)
     unsigned long long* eval_stats = nullptr;  // [kMaxL+1][2][2] evaluations by (L, order, wedge)
 };
 enum { CNT_L2 = 0, CNT_STEP = 1, CNT_T0 = 2, CNT_T1 = 3 };
@@ -72,9 +71,13 @@ void launch_iter_begin(const StageArgs& a, const int* start, const int* start_co
 // order 0 at the global angles et (final scores)
 void launch_eval(const StageArgs& a, int order, const int* list, const int* count, int max_n, cudaStream_t s,
                  bool trial = false);
-void launch_step(const StageArgs& a, int* list_out, int* count_out, int max_n, cudaStream_t s);
-void launch_accept(const StageArgs& a, const int* list_in, const int* count_in, int* list_out, int* count_out,
-                   int* start_out, int* start_count, int max_n, cudaStream_t s);
+// Newton step of the candidates on list_in (order-2 results in c / r); trials to list_out
+void launch_step(const StageArgs& a, const int* list_in, const int* count_in, int* list_out, int* count_out,
+                 int max_n, cudaStream_t s);
+// one round over pending trials (order-2 evaluated): accept / retry, and for accepted
+// trials the next iteration's start and step (advance_kernel)
+void launch_advance(const StageArgs& a, const int* list_in, const int* count_in, int* trial_out, int* trial_count,
+                    int* fresh_out, int* fresh_count, int max_n, cudaStream_t s);
 void launch_final_prep(const StageArgs& a, cudaStream_t s);
 void launch_final_score(const StageArgs& a, int max_n, cudaStream_t s);
 void launch_window_reduce(const ReduceArgs& a, cudaStream_t s);
