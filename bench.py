@@ -435,6 +435,13 @@ def run_product(args):
                                 "6*nv*(2L+1)^2) per kernel (x2 with the wedge), N_xi=(L+1)(2L+1)(2L+3)/3",
                  "traffic": None}
     roof_eval["frac"] = roof_eval["achieved"] / fp32_peak if roof_eval["achieved"] else None
+    forms = ROOT / "profiles" / "round2" / "fp32_forms.json"
+    if forms.exists() and roof_eval["achieved"]:
+        reg = float(json.loads(forms.read_text())["ffma_reg_tflops"])
+        roof_eval["peak_register_operand"] = reg
+        roof_eval["frac_register_operand"] = roof_eval["achieved"] / reg
+        roof_eval["peak_register_operand_note"] = ("FFMA with three register operands, measured "
+                                                   "(tools/probe_ffma2.cu, profiles/round2/fp32_forms.json)")
     # per-band evaluation counts and FLOPs of the instrumented step: achieved =
     # flops_per_step / (eval_ms_per_step / 1000) is recomputable from this line
     per_band, tot = {}, 0.0
