@@ -233,6 +233,15 @@ int bm_exhaustive_baseline(bm_context* ctx, const double* xi, int l_cut, double 
 /* baseline_evaluation_count (src/optimize.cpp:541-544): na * nb * ng of the grid */
 long long bm_baseline_evaluation_count(double angular_step);
 
+/* The same sweep (order 1: value and Euler gradient) as two tensor-core GEMMs:
+ * per-particle rows of xi (value, -i m, -i m' weighted, half plane folded by the
+ * real-volume symmetry) against per-rotation rows of D^l(g) and D'^l(g), FP16
+ * three-pass split on tcgen05 (FP32-accurate).  Same inputs and output layout as
+ * bm_eval_sweep.  timing (host, may be NULL, 4 doubles): tables ms, GEMM ms,
+ * gather ms, tensor-pipe FLOPs of the GEMMs (synchronizes when given). */
+int bm_eval_sweep_tc(bm_context* ctx, const double* f, int n_f, const double* t, const double* euler, int n_rot,
+                     double* out, double* timing, void* stream);
+
 /* Tapered missing-wedge filter of the current template's context on device
  * volumes (apply_wedge_taper, src/xcorr.cpp:210-232). */
 int bm_apply_wedge_taper(bm_context* ctx, const float* in, float* out, int count, void* stream);

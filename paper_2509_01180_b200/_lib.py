@@ -117,6 +117,8 @@ def _declare(L: C.CDLL) -> None:
     L.bm_context_band_timings.restype = I
     L.bm_context_set_expand_mode.argtypes = [P, I]
     L.bm_context_set_expand_mode.restype = I
+    L.bm_eval_sweep_tc.argtypes = [P, P, I, P, P, I, P, P, P]
+    L.bm_eval_sweep_tc.restype = I
     L.bm_xi_coefficients.argtypes = [P, P, I, P, P, P]
     L.bm_xi_coefficients.restype = I
     L.bm_xi_compose_right.argtypes = [P, P, P, I, P, P]

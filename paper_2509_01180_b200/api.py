@@ -393,6 +393,23 @@ class Context:
                    "wedge_power_kernel")
         return out.view(np.complex128)
 
+    def eval_sweep_tc(self, f, t, euler, timing: bool = False):
+        """The config-4 sweep as two tensor-core GEMMs (bm_eval_sweep_tc): same output
+        as eval_sweep(order=1); with timing, also (tables ms, GEMM ms, gather ms, GEMM FLOPs)."""
+        torch = _torch()
+        dev = torch.device(f"cuda:{self.device}")
+        fa = torch.view_as_real(torch.as_tensor(f, dtype=torch.complex128)).to(dev).contiguous()
+        ta = torch.view_as_real(torch.as_tensor(t, dtype=torch.complex128)).to(dev).contiguous()
+        ea = torch.as_tensor(euler, dtype=torch.float64).to(dev).contiguous()
+        n_f, n_rot = fa.shape[0], ea.shape[0]
+        out = torch.empty((n_f, n_rot, 4), dtype=torch.float64, device=dev)
+        tm = np.zeros(4)
+        _lib.check(_lib.lib().bm_eval_sweep_tc(self._h, C.c_void_p(fa.data_ptr()), n_f, C.c_void_p(ta.data_ptr()),
+                                               C.c_void_p(ea.data_ptr()), n_rot, C.c_void_p(out.data_ptr()),
+                                               tm.ctypes.data_as(C.c_void_p) if timing else None,
+                                               self._stream(out)), "eval_sweep_tc")
+        return (out, tuple(tm)) if timing else out
+
     def apply_wedge_taper(self, vols):
         torch = _torch()
         v = self._dev(vols)

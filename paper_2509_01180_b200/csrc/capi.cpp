@@ -16,6 +16,7 @@
 #include "average.hpp"
 #include "generate.hpp"
 #include "ops.hpp"
+#include "sweep_tc.hpp"
 #include "refine.cuh"
 #include "rotation.cuh"
 #include "tables.hpp"
@@ -519,6 +520,35 @@ int bm_exhaustive_baseline(bm_context* ctx, const double* xi, int l_cut, double 
         quat[0] = q.w, quat[1] = q.x, quat[2] = q.y, quat[3] = q.z;
         *score = best;
         if (evaluations) *evaluations = (long long)g.na * g.nb * g.ng;
+        return (int)BM_OK;
+    });
+}
+
+int bm_eval_sweep_tc(bm_context* ctx, const double* f, int n_f, const double* t, const double* euler, int n_rot,
+                     double* out, double* timing, void* stream) {
+    return guarded("bm_eval_sweep_tc", [&] {
+        if (!ctx) return (int)BM_ERR_STATE;
+        if (n_f < 0 || n_rot < 0) throw std::invalid_argument("bad sizes");
+        if (n_f == 0 || n_rot == 0) return (int)BM_OK;
+        if (!f || !t || !euler || !out) throw std::invalid_argument("bad buffers");
+        auto& c = *ctx->impl;
+        cudaSetDevice(c.device);
+        StreamJoin join(ctx, stream);
+        const int L = c.basis.l_max;
+        const long long nxi = xi_entries(L);
+        c.work_xi.reserve(sizeof(double) * 2 * (size_t)nxi * n_f);
+        if (bmb::launch_xi_coefficients(f, c.geo.coeffs, t, 0, n_f, c.geo.block_off, c.geo.radial_count, L,
+                                        c.work_xi.as<double>(), c.stream) != 0)
+            throw std::runtime_error("xi kernel launch failed");
+        bmb::SweepTcTimes tm;
+        if (bmb::sweep_tc(c.work_xi.as<double>(), n_f, L, euler, n_rot, out, c.stream, timing ? &tm : nullptr) != 0)
+            throw std::runtime_error("tensor-core sweep failed");
+        if (timing) {
+            timing[0] = tm.tables_ms;
+            timing[1] = tm.gemm_ms;
+            timing[2] = tm.gather_ms;
+            timing[3] = tm.gemm_flops;
+        }
         return (int)BM_OK;
     });
 }

@@ -29,8 +29,9 @@ def random_coeffs(spec, rng, count):
     return out
 
 
+@pytest.mark.parametrize("path", ["simt", "tensor"])
 @pytest.mark.parametrize("L", [4, 8, 16, 24])
-def test_eval_sweep_matches_oracle(cuda_device, L):
+def test_eval_sweep_matches_oracle(cuda_device, L, path):
     rng = np.random.default_rng(L)
     spec = bmo.Spec(L, L * math.pi)
     ctx = api.Context(0, L, L * math.pi)  # basis-only context (no expansion operator)
@@ -42,7 +43,7 @@ def test_eval_sweep_matches_oracle(cuda_device, L):
         e[1] = min(max(e[1], 0.02), math.pi - 0.02)
         eul.append(e)
     eul = np.array(eul)
-    got = ctx.eval_sweep(f, t, eul, order=1).cpu().numpy()
+    got = (ctx.eval_sweep(f, t, eul, order=1) if path == "simt" else ctx.eval_sweep_tc(f, t, eul)).cpu().numpy()
     for p in range(len(f)):
         xi = bmo.xi_coefficients(f[p], t, spec)
         for g in range(len(eul)):

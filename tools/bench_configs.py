@@ -90,7 +90,19 @@ def cfg4(n_p=512, n_g=4096, L=24):
     flop = n_p * n_g * (8.0 * nxi + 24 * (2 * L + 1) ** 2) + n_g * 12.0 * nxi
     peak = json.loads((Path(__file__).resolve().parent.parent / "profiles" / "fp32_peak.json").read_text())
     tf = flop / ms / 1e9
-    print(json.dumps({"config": 4, "L": L, "particles": n_p, "rotations": n_g, "ms": ms,
+    ms_tc, _ = timed(lambda: ctx.eval_sweep_tc(fc, tc, e), reps=3)
+    _, tm = ctx.eval_sweep_tc(fc, tc, e, timing=True)
+    peaks = json.loads((Path(__file__).resolve().parent.parent / "MEASURED_PEAKS.json").read_text()) \
+        if (Path(__file__).resolve().parent.parent / "MEASURED_PEAKS.json").exists() else {"bf16_tflops": 1590.0}
+    tensor_tf = tm[3] / (tm[1] / 1e3) / 1e12
+    print(json.dumps({"config": 4, "path": "tensor (bm_eval_sweep_tc)", "L": L, "particles": n_p, "rotations": n_g,
+                      "ms": ms_tc, "evaluations_per_s": n_p * n_g / ms_tc * 1e3,
+                      "algorithmic_tflops": flop / ms_tc / 1e9, "phases_ms": {"tables": tm[0], "gemm": tm[1],
+                                                                             "gather": tm[2]},
+                      "gemm_tensor_tflops": tensor_tf, "tensor_frac_of_bf16_peak": tensor_tf / peaks["bf16_tflops"],
+                      "flop_accounting": "algorithmic as the SIMT line; GEMM: 2 K N (3P + P) x 3 FP16 passes"}),
+          flush=True)
+    print(json.dumps({"config": 4, "path": "simt (bm_eval_sweep)", "L": L, "particles": n_p, "rotations": n_g, "ms": ms,
                       "evaluations_per_s": n_p * n_g / ms * 1e3, "algorithmic_tflops": tf,
                       "frac_fp32_peak": tf / float(peak["fp32_fma_tflops"]),
                       "flop_accounting": "SURVEY.md §8(d): n_p n_g (8 N_xi + 24 (2L+1)^2) + n_g 12 N_xi"}),
