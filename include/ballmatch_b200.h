@@ -130,6 +130,10 @@ typedef struct bm_align_result {
     int windows;
     int n_bands;   /* the band schedule used (auto_bands: per particle) */
     int bands[16];
+    long long evaluations_per_band[16];  /* aligned with bands; the seed grid counts at bands[0] */
+    double expand_template_s;  /* phase timings (optimize.hpp:83-86), of the batch call: */
+    double coarse_search_s;    /* the particles are aligned together, so these are shared */
+    double fine_search_s;
 } bm_align_result;
 
 /* One window outcome (search_one_shift, src/optimize.cpp:361-419). */

@@ -477,6 +477,10 @@ struct AlignmentResult {
     double subtomo_norm = 0.0;
     double wall_time_s = 0.0;  // of the whole batch call
     int windows = 0;
+    std::map<int, long> evaluations_per_band;  // band -> evaluations (the seed grid counts at the first band)
+    double expand_template_s = 0.0;  // phase timings of the batch call (the particles share them)
+    double coarse_search_s = 0.0;
+    double fine_search_s = 0.0;
 };
 
 // Batched alignment against one template (the reference's align() semantics per
@@ -523,6 +527,10 @@ public:
             o.score = r.score;
             o.converged = r.converged != 0;
             o.candidates_evaluated = static_cast<long>(r.candidates);
+            for (int j = 0; j < r.n_bands && j < 16; ++j) o.evaluations_per_band[r.bands[j]] = static_cast<long>(r.evaluations_per_band[j]);
+            o.expand_template_s = r.expand_template_s;
+            o.coarse_search_s = r.coarse_search_s;
+            o.fine_search_s = r.fine_search_s;
             o.evaluations = static_cast<long>(r.evaluations);
             o.bands.assign(r.bands, r.bands + r.n_bands);
             o.template_norm = template_norm();

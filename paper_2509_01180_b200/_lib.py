@@ -59,7 +59,9 @@ class AlignResult(C.Structure):
     _fields_ = [("shift", C.c_int * 3), ("quat", C.c_double * 4), ("score", C.c_double),
                 ("converged", C.c_int), ("candidates", C.c_longlong),
                 ("evaluations", C.c_longlong), ("subtomo_norm", C.c_double),
-                ("windows", C.c_int), ("n_bands", C.c_int), ("bands", C.c_int * 16)]
+                ("windows", C.c_int), ("n_bands", C.c_int), ("bands", C.c_int * 16),
+                ("evaluations_per_band", C.c_longlong * 16), ("expand_template_s", C.c_double),
+                ("coarse_search_s", C.c_double), ("fine_search_s", C.c_double)]
 
 
 class WindowResult(C.Structure):

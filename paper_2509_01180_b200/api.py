@@ -231,7 +231,11 @@ class Context:
         return [dict(shift=tuple(r.shift), quat=np.array(r.quat[:]), score=r.score,
                      converged=bool(r.converged), candidates=r.candidates,
                      evaluations=r.evaluations, subtomo_norm=r.subtomo_norm, windows=r.windows,
-                     bands=[int(b) for b in r.bands[:r.n_bands]])
+                     bands=[int(b) for b in r.bands[:r.n_bands]],
+                     evaluations_per_band={int(r.bands[j]): int(r.evaluations_per_band[j])
+                                           for j in range(r.n_bands)},
+                     expand_template_s=r.expand_template_s, coarse_search_s=r.coarse_search_s,
+                     fine_search_s=r.fine_search_s)
                 for r in out[:count]]
 
     def average_accumulate(self, particles, results, out=None):

@@ -214,6 +214,8 @@ std::string config_json(const bm::OptimizerConfig& c, double wedge, double cut_e
 }
 
 std::string result_json(const bm::AlignmentResult& r, int indent) {
+    Obj per_band;
+    for (const auto& [band, n] : r.evaluations_per_band) per_band.num(std::to_string(band), static_cast<double>(n));
     return Obj()
         .add("shift_voxels", Json::arr(std::vector<int>{r.shift[0], r.shift[1], r.shift[2]}))
         .add("rotation", rotation_json(r.rotation))
@@ -221,11 +223,17 @@ std::string result_json(const bm::AlignmentResult& r, int indent) {
         .flag("converged", r.converged)
         .num("candidates_evaluated", static_cast<double>(r.candidates_evaluated))
         .num("evaluations", static_cast<double>(r.evaluations))
+        .add("evaluations_per_band", per_band.dump(indent + 2))
         .add("bands", Json::arr(r.bands))
         .num("template_norm", r.template_norm)
         .num("subtomo_norm", r.subtomo_norm)
         .num("windows", r.windows)
-        .add("timings", Obj().num("wall_s", r.wall_time_s).dump(indent + 2))
+        .add("timings", Obj()
+                            .num("expand_template_s", r.expand_template_s)
+                            .num("coarse_search_s", r.coarse_search_s)
+                            .num("fine_search_s", r.fine_search_s)
+                            .num("wall_s", r.wall_time_s)
+                            .dump(indent + 2))
         .dump(indent);
 }
 

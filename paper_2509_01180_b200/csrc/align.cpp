@@ -17,6 +17,7 @@
 #include <map>
 #include <stdexcept>
 #include <thread>
+#include <chrono>
 
 #include <nvtx3/nvToolsExt.h>
 
@@ -203,6 +204,12 @@ SeedDev& Context::seed_tables(int L, double step) {
 
 void Context::set_template(const float* tmpl, double wedge_theta) {
     if (geo.support == 0) throw std::invalid_argument("set_template: context has no operator (n = 0)");
+    const auto t0 = std::chrono::steady_clock::now();
+    struct Stamp {
+        double& out;
+        std::chrono::steady_clock::time_point t0;
+        ~Stamp() { out = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); }
+    } stamp{template_s_, t0};
     // template expansion through the same tensor-core path (align: t_hat = expand(tmpl))
     std::vector<int> wv{0}, ws{0, 0, 0};
     expand_windows(tmpl, (long long)n * n * n, 1, wv, ws);
@@ -313,6 +320,7 @@ void Context::refine_windows(int nw, int maxc, const AlignConfig& cfg, const Qua
             a.max_cand = maxc;
             a.n_win = cnt;
             a.prm.band = L;
+            a.prm.band_index = (int)bi;
             a.prm.newton_max_iter = cfg.newton_max_iter;
             a.prm.grad_tol = cfg.grad_tol;
             a.prm.accept_tol = cfg.accept_tol;
@@ -536,6 +544,7 @@ void Context::objective_eval(const double* f, const double* t, const double* eul
     a.n_win = 1;
     const Quat koff = q_from_euler(0.0, kPiH / 2.0, 0.0);
     a.prm.band = L;
+    a.prm.band_index = 0;
     a.prm.koffset[0] = koff.w;
     a.prm.koffset[1] = koff.x;
     a.prm.koffset[2] = koff.y;
@@ -902,14 +911,19 @@ void Context::align_group(const float* fw, int n_vol, const std::vector<int>& pa
         explicit PairHold(Context& x) : c(x) { c.pairs_hold_ = true; c.pairs_src_ = nullptr; }
         ~PairHold() { c.pairs_hold_ = false; c.pairs_src_ = nullptr; }
     } hold(*this);
+    const auto t_coarse = std::chrono::steady_clock::now();
     std::vector<WindowOutcome> oc = run_windows(fw, n_vol, wv, ws, cfg);
+    const double coarse_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_coarse).count();
     std::vector<int> best(n_vol, -1);
     std::vector<long long> cand(n_vol, 0), evals(n_vol, 0);
+    std::vector<std::array<long long, kMaxBands>> band_evals(n_vol);
+    for (auto& b : band_evals) b.fill(0);
     std::vector<int> nwin(n_vol, 0);
     for (size_t i = 0; i < oc.size(); ++i) {
         const int p = oc[i].particle;
         cand[p] += oc[i].n_cand;
         evals[p] += oc[i].evals;
+        for (int b = 0; b < kMaxBands; ++b) band_evals[p][b] += oc[i].band_evals[b];
         ++nwin[p];
         if (oc[i].valid && (best[p] < 0 || better(oc[i], oc[best[p]]))) best[p] = (int)i;
     }
@@ -928,13 +942,16 @@ void Context::align_group(const float* fw, int n_vol, const std::vector<int>& pa
                     fs.insert(fs.end(), s.begin(), s.end());
                 }
     }
+    const auto t_fine = std::chrono::steady_clock::now();
     std::vector<WindowOutcome> fo = run_windows(fw, n_vol, fv, fs, cfg);
+    const double fine_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_fine).count();
     std::vector<WindowOutcome> bestw(n_vol);
     for (int p : parts) bestw[p] = oc[best[p]];
     for (const auto& o : fo) {
         const int p = o.particle;
         cand[p] += o.n_cand;
         evals[p] += o.evals;
+        for (int b = 0; b < kMaxBands; ++b) band_evals[p][b] += o.band_evals[b];
         ++nwin[p];
         if (o.valid && better(o, bestw[p])) bestw[p] = o;
     }
@@ -949,6 +966,10 @@ void Context::align_group(const float* fw, int n_vol, const std::vector<int>& pa
         r.subtomo_norm = bestw[p].sub_norm;
         r.windows = nwin[p];
         r.bands = cfg.bands;
+        r.evaluations_per_band.assign(band_evals[p].begin(), band_evals[p].begin() + cfg.bands.size());
+        r.coarse_search_s = coarse_s;  // of the whole group (the stages run batched)
+        r.fine_search_s = fine_s;
+        r.expand_template_s = template_s_;
     }
 }
 

@@ -257,6 +257,11 @@ int bm_align_batch(bm_context* ctx, const float* particles, int count, const bm_
             o.windows = r.windows;
             o.n_bands = (int)std::min<size_t>(r.bands.size(), 16);
             for (int j = 0; j < o.n_bands; ++j) o.bands[j] = r.bands[j];
+            for (int j = 0; j < 16; ++j)
+                o.evaluations_per_band[j] = j < (int)r.evaluations_per_band.size() ? r.evaluations_per_band[j] : 0;
+            o.expand_template_s = r.expand_template_s;
+            o.coarse_search_s = r.coarse_search_s;
+            o.fine_search_s = r.fine_search_s;
         }
         return (int)BM_OK;
     });

@@ -103,6 +103,8 @@ struct ParticleResult {
     double subtomo_norm;
     int windows;
     std::vector<int> bands;
+    std::vector<long long> evaluations_per_band;  // aligned with bands (AlignmentResult, optimize.hpp:83)
+    double expand_template_s = 0.0, coarse_search_s = 0.0, fine_search_s = 0.0;  // phase timings (batch level)
 };
 
 // Per-kernel-class CUDA-event timing on the context stream (bench evidence).
@@ -212,6 +214,7 @@ public:
     void build_side_template();
     double t_norm = 0.0;
     bool has_template = false;
+    double template_s_ = 0.0;  // wall time of the last set_template
     double wedge_deg = 0.0;                // <= 0 or >= 90: no wedge
     std::unique_ptr<WedgeFilter> wedge;    // tapered filter for the particles
     std::vector<std::complex<double>> chi_hat, q_hat;  // wedge power factors

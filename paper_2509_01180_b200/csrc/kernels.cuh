@@ -9,6 +9,7 @@
 namespace bmb {
 
 constexpr int kMaxL = 48;  // largest band limit the device tables support
+constexpr int kMaxBands = 16;  // bands of one marching schedule (bm_align_config.bands)
 
 // Per-band evaluation tables (host-built, device-resident).  The half-plane
 // items (m,m') of degree <= L (m > 0, or m = 0 and m' >= 0) are sorted by
@@ -62,6 +63,7 @@ struct CandState {
     int band_converged;
     int evals;
     int active;         // 0 for empty candidate slots
+    int band_evals[kMaxBands];  // evaluations by band index (evaluations_per_band, optimize.hpp:83)
 };
 
 struct WindowOutcome {
@@ -76,6 +78,7 @@ struct WindowOutcome {
     double sub_norm;
     double quat[4];
     long long evals;
+    long long band_evals[kMaxBands];  // by band index; the seed grid counts at band 0
 };
 
 struct RefineParams {
@@ -88,6 +91,7 @@ struct RefineParams {
     int max_cand;
     int has_wedge;
     int first_band;
+    int band_index;       // position of band in the schedule (per-band counters)
 };
 
 // ---- launchers (stream-ordered, no host sync)

@@ -884,6 +884,7 @@ __device__ __forceinline__ bool step_one(const StageArgs& a, long long i) {
     objective(wk.c, wk.r, a.prm.has_wedge != 0, 2, f);
     if (wk.side) chart_transform(f, wk.e, wk.ev);  // anchored: derivatives in the chart angles
     ++st.evals;
+    ++st.band_evals[a.prm.band_index];
     wk.f[0] = f.v;
     for (int k = 0; k < 3; ++k) wk.f[1 + k] = f.g[k];
     for (int k = 0; k < 9; ++k) wk.f[4 + k] = f.h[k];
@@ -936,6 +937,7 @@ __device__ __forceinline__ bool accept_one(const StageArgs& a, long long i) {
     Derivs t;
     objective(wk.c, wk.r, a.prm.has_wedge != 0, 0, t);  // the value (the trial ran at order 2)
     ++st.evals;
+    ++st.band_evals[a.prm.band_index];
     const double scale = fmax(fabs(wk.f[0]), 1e-300);
     // tolerant acceptance (optimize.cpp:330-341)
     if (t.v > wk.f[0] - a.prm.accept_tol * scale) {
@@ -1010,6 +1012,7 @@ __device__ __forceinline__ void final_score_one(const StageArgs& a, long long i)
     objective(wk.c, wk.r, a.prm.has_wedge != 0, 0, t);
     a.cand[i].score = t.v;
     ++a.cand[i].evals;
+    ++a.cand[i].band_evals[a.prm.band_index];
     wk.status = ST_DONE;
 }
 
@@ -1080,11 +1083,13 @@ __global__ void window_reduce_kernel(ReduceArgs a) {
     o.sub_norm = a.sub_norm[w];
     o.valid = (nc > 0 && o.sub_norm > 0.0) ? 1 : 0;
     o.evals = a.grid_evals;
+    for (int b = 0; b < kMaxBands; ++b) o.band_evals[b] = b == 0 ? a.grid_evals : 0;
     int best = -1;
     double bs = 0.0, ba = 0.0;
     for (int c = 0; c < nc; ++c) {
         const CandState& st = cs[c];
         o.evals += st.evals;
+        for (int b = 0; b < kMaxBands; ++b) o.band_evals[b] += st.band_evals[b];
         if (!st.active) continue;  // pruned after the first band
         const double ang = q_angle(qload(st.diverged ? st.best_g : st.g));
         // search_one_shift tie rule (optimize.cpp:405-412)

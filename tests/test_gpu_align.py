@@ -248,3 +248,24 @@ def test_refilled_host_buffer_is_restaged(cuda_device):
     a1 = ctx.average_accumulate(host, res)
     a2 = ctx.average_accumulate(host, res)
     assert torch.allclose(a1, a2, rtol=1e-12, atol=1e-12)
+
+
+def test_evaluations_per_band_and_phase_timings(cuda_device):
+    """AlignmentResult's evaluations_per_band (optimize.hpp:83; optimize.cpp:507-511):
+    per band of the schedule, summing to the total; the seed grid is counted at the
+    first band; phase timings are filled."""
+    import math
+
+    n, L = 32, 8
+    tmpl = api.make_template(n, 20, 5)
+    parts, _, _ = api.make_particles(tmpl, 4, 1200, 2, 0.5, 60.0)
+    cfg = api.make_config(bands=(4, 8), max_candidates=8, shift_radius=2, shift_step=2)
+    ctx = api.Context(n, L, L * math.pi)
+    ctx.set_template(tmpl, 60.0)
+    for r in ctx.align_batch(parts, cfg):
+        epb = r["evaluations_per_band"]
+        assert set(epb) == {4, 8}
+        assert sum(epb.values()) == r["evaluations"]
+        assert epb[4] >= r["windows"] * 16 * 9 * 16  # the 16 x 9 x 16 seed grid of every window
+        assert epb[8] > 0
+        assert r["coarse_search_s"] > 0 and r["fine_search_s"] > 0 and r["expand_template_s"] > 0
