@@ -63,7 +63,7 @@ struct CandState {
     int band_converged;
     int evals;
     int active;         // 0 for empty candidate slots
-    int band_evals[kMaxBands];  // evaluations by band index (evaluations_per_band, optimize.hpp:83)
+    unsigned short band_evals[kMaxBands];  // evaluations by band index (evaluations_per_band, optimize.hpp:83)
 };
 
 struct WindowOutcome {
