@@ -546,7 +546,9 @@ int bm_eval_sweep_tc(bm_context* ctx, const double* f, int n_f, const double* t,
                                         c.work_xi.as<double>(), c.stream) != 0)
             throw std::runtime_error("xi kernel launch failed");
         bmb::SweepTcTimes tm;
-        if (bmb::sweep_tc(c.work_xi.as<double>(), n_f, L, euler, n_rot, out, c.stream, timing ? &tm : nullptr) != 0)
+        c.filtered.reserve(bmb::sweep_tc_bytes(n_f, L, n_rot));  // grow-only scratch
+        if (bmb::sweep_tc(c.work_xi.as<double>(), n_f, L, euler, n_rot, out, c.filtered.p, c.stream,
+                          timing ? &tm : nullptr) != 0)
             throw std::runtime_error("tensor-core sweep failed");
         if (timing) {
             timing[0] = tm.tables_ms;

@@ -24,6 +24,14 @@ Context::Context(int dev, int n_, int l_max, double lambda_cut) : device(dev), n
     if (l_max > kMaxL) throw std::invalid_argument("context: l_max exceeds the device tables (48)");
     BMB_CUDA(cudaSetDevice(device));
     BMB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    {  // stream-ordered scratch (large-basis expansion, average): keep freed blocks in
+       // the device pool instead of returning them to the driver at every sync
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            unsigned long long keep = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+    }
     basis = host::make_basis(l_max, lambda_cut);
     if (const char* e = std::getenv("BMB_EXPAND")) expand_mode = std::string(e) == "gemm" ? 1 : 0;
     geo.n = n;

@@ -303,20 +303,25 @@ const ChainTablesDev& chain_tables(int L) {
 
 long long sweep_tc_k(int L) { return 2 * hp_offset(L + 1); }
 
-int sweep_tc(const double* xi, int P, int L, const double* euler, int G, double* out, cudaStream_t s,
+size_t sweep_tc_bytes(int P, int L, int G) {
+    const long long k_pad = round_up(sweep_tc_k(L), 64);
+    const long long m1 = round_up(3LL * P, 128), m2 = round_up(P, 128), n_pad = round_up(G, 128);
+    const size_t b_rows = sizeof(__half) * (size_t)n_pad * k_pad;
+    const size_t a_rows = sizeof(__half) * (size_t)m1 * k_pad;
+    return 4 * b_rows + 2 * a_rows + sizeof(float) * (m1 + n_pad * 2) + sizeof(float) * (size_t)n_pad * (m1 + m2);
+}
+
+int sweep_tc(const double* xi, int P, int L, const double* euler, int G, double* out, void* scratch, cudaStream_t s,
              SweepTcTimes* times) {
     if (P <= 0 || G <= 0) return 0;
-    if (L < 0 || L > kMaxSweepL) return 1;
+    if (L < 0 || L > kMaxSweepL || !scratch) return 1;
     const long long nxi = (long long)(L + 1) * (2 * L + 1) * (2 * L + 3) / 3;
     const long long k_pad = round_up(sweep_tc_k(L), 64);
     const long long m1 = round_up(3LL * P, 128), m2 = round_up(P, 128), n_pad = round_up(G, 128);
     const float dp_scale = exp2f(ceilf(log2f((float)(L > 0 ? L : 1))));
-    char* buf = nullptr;
+    char* buf = static_cast<char*>(scratch);
     const size_t b_rows = sizeof(__half) * (size_t)n_pad * k_pad;  // one of hi / lo
     const size_t a_rows = sizeof(__half) * (size_t)m1 * k_pad;
-    const size_t bytes = 4 * b_rows + 2 * a_rows + sizeof(float) * (m1 + n_pad * 2) +
-                         sizeof(float) * (size_t)n_pad * (m1 + m2);
-    if (cudaMallocAsync(&buf, bytes, s) != cudaSuccess) return 2;
     cudaMemsetAsync(buf, 0, 4 * b_rows + 2 * a_rows, s);  // K and row padding must be zero
     __half* d_hi = reinterpret_cast<__half*>(buf);
     __half* d_lo = d_hi + (size_t)n_pad * k_pad;
@@ -389,7 +394,6 @@ int sweep_tc(const double* xi, int P, int L, const double* euler, int G, double*
         times->gemm_flops = 2.0 * (double)k_pad * n_pad * (m1 + m2) * 3.0;  // three FP16 passes
         for (auto& e : ev) cudaEventDestroy(e);
     }
-    cudaFreeAsync(buf, s);
     if (rc != 0 || cudaGetLastError() != cudaSuccess) return 2;
     return 0;
 }
