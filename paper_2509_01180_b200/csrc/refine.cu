@@ -549,10 +549,20 @@ __device__ void objective(const double* cr, const double* rr, bool wedge, int or
 //   J = de'/de = W(e')^-1 W(e),
 //   d^2 e'_k / de_i de_j = (W(e')^-1 (dW(e)/de_j - sum_k J_kj dW(e')/de'_k J))_ki,
 //   grad = J^T grad',  H = J^T H' J + sum_k grad'_k d^2 e'_k / de de.
-__device__ void euler_frame(double a, double b, double W[9], double dWa[9], double dWb[9]) {
-    double sa, ca, sb, cb;
-    sincos(a, &sa, &ca);
-    sincos(b, &sb, &cb);
+// cs = (cos a, sin a, cos b, sin b) of the ZYZ angles of q (rotation.cpp:77-93:
+// a = atan2(m12, m02), b = atan2(hypot(m02, m12), m22)), from the matrix entries
+__device__ __forceinline__ void frame_trig(const Quat& q, double cs[4]) {
+    const double m02 = 2 * (q.x * q.z + q.w * q.y), m12 = 2 * (q.y * q.z - q.w * q.x);
+    const double m22 = 1 - 2 * (q.x * q.x + q.y * q.y);
+    const double sb = hypot(m02, m12);
+    cs[0] = m02 / sb, cs[1] = m12 / sb;
+    cs[2] = m22, cs[3] = sb;
+    const double rb = rhypot(m22, sb);  // the matrix of a unit quaternion has m22^2 + sb^2 = 1 up to rounding
+    cs[2] *= rb, cs[3] *= rb;
+}
+
+__device__ void euler_frame(const double cs[4], double W[9], double dWa[9], double dWb[9]) {
+    const double ca = cs[0], sa = cs[1], cb = cs[2], sb = cs[3];
     // columns: w_alpha = z, w_beta = (-sin a, cos a, 0), w_gamma = (cos a sin b, sin a sin b, cos b)
     W[0] = 0.0, W[1] = -sa, W[2] = ca * sb;
     W[3] = 0.0, W[4] = ca, W[5] = sa * sb;
@@ -571,11 +581,11 @@ __device__ void mat3_mul(const double* A, const double* B, double* C) {
 }
 
 // f: objective at e' (value, gradient, Hessian in e' = ev); rewritten in place
-// as the derivatives with respect to the chart angles e
-__device__ void chart_transform(Derivs& f, const double* e, const double* ev) {
+// as the derivatives with respect to the chart angles e (te, tv: the frames' trig)
+__device__ void chart_transform(Derivs& f, const double* te, const double* tv) {
     double We[9], dWe_a[9], dWe_b[9], Wp[9], dWp_a[9], dWp_b[9];
-    euler_frame(e[0], e[1], We, dWe_a, dWe_b);
-    euler_frame(ev[0], ev[1], Wp, dWp_a, dWp_b);
+    euler_frame(te, We, dWe_a, dWe_b);
+    euler_frame(tv, Wp, dWp_a, dWp_b);
     // W(e')^-1 by the adjugate (det = -sin b' != 0: b' is at least 45 degrees from a pole)
     double Wi[9];
     Wi[0] = Wp[4] * Wp[8] - Wp[5] * Wp[7];
@@ -617,7 +627,7 @@ __device__ void chart_transform(Derivs& f, const double* e, const double* ev) {
 // rotation h_try * a on the window kernel (C~(h) = C(h a), xcorr.cpp:149-155)
 // instead of streaming its private chart kernels; et holds those angles.
 __device__ __forceinline__ Quat qload(const double* q);
-__device__ __forceinline__ void choose_frame(const Quat& g, const Quat& koff, double* ev, int& side);
+__device__ __forceinline__ void choose_frame(const Quat& g, const Quat& koff, double* ev, int& side, double* tv);
 __device__ void make_trial(CandWork& wk, const CandState& st, const Quat& koff) {
     double m[9];
     for (int i = 0; i < 9; ++i) m[i] = wk.f[4 + i];
@@ -649,7 +659,7 @@ __device__ void make_trial(CandWork& wk, const CandState& st, const Quat& koff) 
     // next iteration's chart angles exactly), or for an anchored candidate the
     // better-conditioned of g and g K
     if (st.anchored) {
-        choose_frame(gt, koff, wk.evt, wk.sidet);
+        choose_frame(gt, koff, wk.evt, wk.sidet, wk.tvt);
     } else {
         wk.evt[0] = et.a, wk.evt[1] = et.b, wk.evt[2] = et.g;
         wk.sidet = 0;
@@ -672,6 +682,7 @@ __device__ __forceinline__ void band_begin_one(const StageArgs& a, long long i) 
     wk.iter = 0;
     wk.retry = 0;
     wk.fresh = 0;
+    if (a.prm.band_index == 0) wk.val_band = -1;  // the work slots are reused across stages
     wk.status = ST_DONE;
     CandState& st = a.cand[i];
     if (!st.active || st.diverged) return;
@@ -712,16 +723,20 @@ __global__ void band_begin_kernel(StageArgs a, int* start, int* start_count) {
 // order-2 evaluation frame of an anchored candidate at global rotation g: the
 // window kernel at E(g), or the side kernels at E(g K), whichever is further from
 // its gimbal pole (chart_transform)
-__device__ __forceinline__ void choose_frame(const Quat& g, const Quat& koff, double* ev, int& side) {
-    const Euler3 eg = q_euler(g);
-    const Euler3 ek = q_euler(q_mul(g, koff));
-    const bool use_side = fabs(sin(ek.b)) > fabs(sin(eg.b));
-    const Euler3& e = use_side ? ek : eg;
+__device__ __forceinline__ void choose_frame(const Quat& g, const Quat& koff, double* ev, int& side, double* tv) {
+    // sin b of g and of g K straight from the matrices; only the chosen frame's angles are computed
+    const Quat gk = q_mul(g, koff);
+    const double sg = hypot(2 * (g.x * g.z + g.w * g.y), 2 * (g.y * g.z - g.w * g.x));
+    const double sk = hypot(2 * (gk.x * gk.z + gk.w * gk.y), 2 * (gk.y * gk.z - gk.w * gk.x));
+    const bool use_side = sk > sg;
+    const Quat& q = use_side ? gk : g;
+    const Euler3 e = q_euler(q);
     ev[0] = e.a, ev[1] = e.b, ev[2] = e.g;
     side = use_side ? 2 : 1;
+    frame_trig(q, tv);
 }
 __device__ __forceinline__ void set_eval_frame(CandWork& wk, const Quat& g, const Quat& koff) {
-    choose_frame(g, koff, wk.ev, wk.side);
+    choose_frame(g, koff, wk.ev, wk.side, wk.tv);
 }
 
 // iteration start of candidate i (chart and re-anchor decision,
@@ -739,16 +754,19 @@ __device__ __forceinline__ int iter_begin_one(const StageArgs& a, long long i) {
     const Quat g = qload(st.g);
     const Quat koff{a.prm.koffset[0], a.prm.koffset[1], a.prm.koffset[2], a.prm.koffset[3]};
     const bool was_anchored = st.anchored != 0;
-    Euler3 e = q_euler(q_mul(g, q_inv(qload(st.anchor))));
+    Quat h = q_mul(g, q_inv(qload(st.anchor)));
+    Euler3 e = q_euler(h);
     bool reanchored = false;
     if (e.b < 0.05 || e.b > kPiD - 0.05) {
         qstore(st.anchor, q_mul(q_inv(koff), g));
         st.anchor_limit = a.prm.band;
         st.anchored = 1;
         reanchored = true;
+        h = koff;
         e = q_euler(koff);
     }
     wk.e[0] = e.a, wk.e[1] = e.b, wk.e[2] = e.g;
+    if (st.anchored) frame_trig(h, wk.te);  // the chart side of chart_transform
     wk.status = ST_EVAL2;
     ++wk.iter;
     // the accepted trial's derivatives are in its own frame: the global angles of g
@@ -882,7 +900,9 @@ __device__ __forceinline__ bool step_one(const StageArgs& a, long long i) {
     CandState& st = a.cand[i];
     Derivs f;
     objective(wk.c, wk.r, a.prm.has_wedge != 0, 2, f);
-    if (wk.side) chart_transform(f, wk.e, wk.ev);  // anchored: derivatives in the chart angles
+    if (wk.side) chart_transform(f, wk.te, wk.tv);  // anchored: derivatives in the chart angles
+    wk.val = f.v;  // the objective at g (any chart: the same function value)
+    wk.val_band = a.prm.band_index;
     ++st.evals;
     ++st.band_evals[a.prm.band_index];
     wk.f[0] = f.v;
@@ -942,9 +962,12 @@ __device__ __forceinline__ bool accept_one(const StageArgs& a, long long i) {
     // tolerant acceptance (optimize.cpp:330-341)
     if (t.v > wk.f[0] - a.prm.accept_tol * scale) {
         qstore(st.g, q_mul(qload(wk.gt), qload(st.anchor)));
+        wk.val = t.v;  // the trial point is the new g
+        wk.val_band = a.prm.band_index;
         wk.lambda = fmax(wk.lam / 10.0, 1e-12);
         // the trial's order-2 results are the next iteration's evaluation at g
         wk.ev[0] = wk.evt[0], wk.ev[1] = wk.evt[1], wk.ev[2] = wk.evt[2];
+        for (int k = 0; k < 4; ++k) wk.tv[k] = wk.tvt[k];
         wk.side = wk.sidet;
         wk.fresh = 1;
         if (t.v > st.best_score) {
@@ -999,7 +1022,16 @@ __device__ __forceinline__ bool final_prep_one(const StageArgs& a, long long i) 
     CandWork& wk = a.work[i];
     wk.status = ST_DONE;
     if (!a.cand[i].active) return false;
-    const CandState& st = a.cand[i];
+    CandState& st = a.cand[i];
+    // the final score is Objective::eval at g at this band (optimize.cpp:349-352): a
+    // candidate whose last evaluation at g ran at this band already has that value
+    // (the evaluation is still counted, as in the reference)
+    if (!st.diverged && wk.val_band == a.prm.band_index) {
+        st.score = wk.val;
+        ++st.evals;
+        ++st.band_evals[a.prm.band_index];
+        return false;
+    }
     const Euler3 e = q_euler(qload(st.diverged ? st.best_g : st.g));
     wk.et[0] = e.a, wk.et[1] = e.b, wk.et[2] = e.g;
     wk.status = ST_FINAL;
@@ -1061,6 +1093,7 @@ __device__ void prune_window(const StageArgs& a, int w) {
     st.anchor_limit = -1;
     st.diverged = 0;
     st.band_converged = 0;
+    a.work[(size_t)w * a.max_cand + best].val_band = -1;
     st.best_score = -DBL_MAX * 2.0;  // -inf
 }
 
@@ -1134,6 +1167,7 @@ __global__ void objective_setup_kernel(StageArgs a, const double* euler, const d
     qstore(st.anchor, anchor);
     st.anchored = anchors ? 1 : 0;
     wk.e[0] = e[0], wk.e[1] = e[1], wk.e[2] = e[2];
+    frame_trig(q_from_euler(e[0], e[1], e[2]), wk.te);
     wk.side = 0;
     if (anchors) set_eval_frame(wk, g, koff);
     // order 0: the value at the global rotation on the window kernel (make_trial)
@@ -1150,7 +1184,7 @@ __global__ void objective_finalize_kernel(StageArgs a, int n, int order, double*
     CandWork& wk = a.work[i];
     Derivs f;
     objective(wk.c, wk.r, a.prm.has_wedge != 0, order, f);
-    if (order == 2 && wk.side) chart_transform(f, wk.e, wk.ev);
+    if (order == 2 && wk.side) chart_transform(f, wk.te, wk.tv);
     double* o = out + 13 * (size_t)i;
     o[0] = f.v;
     for (int k = 0; k < 3; ++k) o[1 + k] = order == 2 ? f.g[k] : 0.0;

@@ -28,6 +28,11 @@ struct CandWork {
     double evt[3];  // frame of the trial's order-2 evaluation (same convention, sidet)
     int sidet;
     int fresh;      // c / r hold the order-2 results of the accepted trial at g (frame ev, side)
+    // (cos a, sin a, cos b, sin b) of the chart angles e, of the evaluation frame ev and of
+    // the trial frame evt, taken from the rotation matrices (chart_transform needs no sincos)
+    double te[4], tv[4], tvt[4];
+    double val;     // objective value at g of the last evaluation there ...
+    int val_band;   // ... and its band index (-1: none); serves the final score
 };
 
 struct StageArgs {
