@@ -410,6 +410,7 @@ void Context::refine_windows(int nw, int maxc, const AlignConfig& cfg, const Qua
         }
         ReduceArgs ra;
         ra.cand = cand_.as<CandState>() + (size_t)w0 * maxc;
+        ra.work = work_.as<CandWork>() + (size_t)w0 * maxc;
         ra.cand_count = cand_count_.as<int>() + w0;
         ra.max_cand = maxc;
         ra.n_win = cnt;

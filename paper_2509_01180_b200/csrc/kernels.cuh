@@ -63,7 +63,6 @@ struct CandState {
     int band_converged;
     int evals;
     int active;         // 0 for empty candidate slots
-    unsigned short band_evals[kMaxBands];  // evaluations by band index (evaluations_per_band, optimize.hpp:83)
 };
 
 struct WindowOutcome {

@@ -682,7 +682,10 @@ __device__ __forceinline__ void band_begin_one(const StageArgs& a, long long i) 
     wk.iter = 0;
     wk.retry = 0;
     wk.fresh = 0;
-    if (a.prm.band_index == 0) wk.val_band = -1;  // the work slots are reused across stages
+    if (a.prm.band_index == 0) {  // the work slots are reused across stages
+        wk.val_band = -1;
+        for (int b = 0; b < kMaxBands; ++b) wk.band_evals[b] = 0;
+    }
     wk.status = ST_DONE;
     CandState& st = a.cand[i];
     if (!st.active || st.diverged) return;
@@ -904,7 +907,7 @@ __device__ __forceinline__ bool step_one(const StageArgs& a, long long i) {
     wk.val = f.v;  // the objective at g (any chart: the same function value)
     wk.val_band = a.prm.band_index;
     ++st.evals;
-    ++st.band_evals[a.prm.band_index];
+    ++wk.band_evals[a.prm.band_index];
     wk.f[0] = f.v;
     for (int k = 0; k < 3; ++k) wk.f[1 + k] = f.g[k];
     for (int k = 0; k < 9; ++k) wk.f[4 + k] = f.h[k];
@@ -957,7 +960,7 @@ __device__ __forceinline__ bool accept_one(const StageArgs& a, long long i) {
     Derivs t;
     objective(wk.c, wk.r, a.prm.has_wedge != 0, 0, t);  // the value (the trial ran at order 2)
     ++st.evals;
-    ++st.band_evals[a.prm.band_index];
+    ++wk.band_evals[a.prm.band_index];
     const double scale = fmax(fabs(wk.f[0]), 1e-300);
     // tolerant acceptance (optimize.cpp:330-341)
     if (t.v > wk.f[0] - a.prm.accept_tol * scale) {
@@ -1029,7 +1032,7 @@ __device__ __forceinline__ bool final_prep_one(const StageArgs& a, long long i) 
     if (!st.diverged && wk.val_band == a.prm.band_index) {
         st.score = wk.val;
         ++st.evals;
-        ++st.band_evals[a.prm.band_index];
+        ++wk.band_evals[a.prm.band_index];
         return false;
     }
     const Euler3 e = q_euler(qload(st.diverged ? st.best_g : st.g));
@@ -1044,7 +1047,7 @@ __device__ __forceinline__ void final_score_one(const StageArgs& a, long long i)
     objective(wk.c, wk.r, a.prm.has_wedge != 0, 0, t);
     a.cand[i].score = t.v;
     ++a.cand[i].evals;
-    ++a.cand[i].band_evals[a.prm.band_index];
+    ++wk.band_evals[a.prm.band_index];
     wk.status = ST_DONE;
 }
 
@@ -1122,7 +1125,8 @@ __global__ void window_reduce_kernel(ReduceArgs a) {
     for (int c = 0; c < nc; ++c) {
         const CandState& st = cs[c];
         o.evals += st.evals;
-        for (int b = 0; b < kMaxBands; ++b) o.band_evals[b] += st.band_evals[b];
+        const CandWork& wk = a.work[(size_t)w * a.max_cand + c];
+        for (int b = 0; b < kMaxBands; ++b) o.band_evals[b] += wk.band_evals[b];
         if (!st.active) continue;  // pruned after the first band
         const double ang = q_angle(qload(st.diverged ? st.best_g : st.g));
         // search_one_shift tie rule (optimize.cpp:405-412)

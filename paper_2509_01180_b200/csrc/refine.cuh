@@ -33,6 +33,7 @@ struct CandWork {
     double te[4], tv[4], tvt[4];
     double val;     // objective value at g of the last evaluation there ...
     int val_band;   // ... and its band index (-1: none); serves the final score
+    unsigned short band_evals[kMaxBands];  // evaluations by band index (evaluations_per_band, optimize.hpp:83)
 };
 
 struct StageArgs {
@@ -55,6 +56,7 @@ enum { CNT_L2 = 0, CNT_STEP = 1, CNT_T0 = 2, CNT_T1 = 3 };
 // one window outcome per window (last band)
 struct ReduceArgs {
     const CandState* cand = nullptr;
+    const CandWork* work = nullptr;  // per-band evaluation counters
     const int* cand_count = nullptr;
     int max_cand = 0;
     int n_win = 0;

@@ -197,7 +197,6 @@ __global__ void __launch_bounds__(256) seed_kernel(SeedArgs a) {
             c.diverged = 0;
             c.band_converged = 0;
             c.evals = 0;
-            for (int b = 0; b < kMaxBands; ++b) c.band_evals[b] = 0;
             c.active = 1;
             if (a.seed_score) a.seed_score[(size_t)w * a.max_cand + rank] = s;
         }
