@@ -471,6 +471,206 @@ int launch_split(const FactoredTables& T, const float* vols, long long vol_strid
     return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }
 
+// ---------------------------------------------------------------- window pairs
+// Two windows per CTA (consecutive windows of the alignment's shift lists: the
+// same particle, shifts a voxel or two apart).  Each sample's footprint is
+// loaded and decoded once for both windows and the second window's gathers
+// mostly hit the L1 lines the first one pulled in; the phi-DFT of the pair keeps
+// all 256 threads busy (2 windows x 2 order groups x 64 rings) and the theta
+// threads reuse their register weights for both.  Same FP32 values and FMA order
+// per window as expand_factored_kernel (bit-identical coefficients).
+#ifndef BMB_EXPAND_PAIR_MINB
+#define BMB_EXPAND_PAIR_MINB 2
+#endif
+struct SmemPair {
+    size_t samp, F, G, rad, total;
+};
+__host__ __device__ inline SmemPair smem_plan_pair(const FactoredTables& T) {
+    SmemPair s;
+    size_t o = 0;
+    s.samp = o;
+    o = al16(o + 2 * sizeof(float) * (size_t)kRC * T.nt * T.np);
+    s.F = o;
+    o = al16(o + 2 * sizeof(float2) * (size_t)T.nt * (T.L + 1));
+    s.G = o;
+    o = al16(o + 2 * sizeof(float) * (size_t)(T.L + 1) * (T.L + 1));
+    s.rad = o;
+    o = al16(o + sizeof(float) * (size_t)T.pairs);
+    s.total = o;
+    return s;
+}
+
+template <int RPT, int NPC>
+__global__ void __launch_bounds__(kThreads, BMB_EXPAND_PAIR_MINB)
+    expand_pair_kernel(FactoredTables T, const float* __restrict__ vols, long long vol_stride,
+                       const int* __restrict__ win_vol, const int* __restrict__ win_shift, int n_win,
+                       float* __restrict__ out, int ldo, const float2* __restrict__ pairs) {
+    static_assert(NPC > 0 && NPC <= 64 && (NPC / 2) * (NPC / 2 + 1) / 2 <= kThreads, "specialised shapes only");
+    extern __shared__ __align__(16) unsigned char sm[];
+    const SmemPair P = smem_plan_pair(T);
+    const int n = T.n, nt = T.nt, np = NPC, nl = T.L + 1, nsamp = nt * np;
+    float* samp = reinterpret_cast<float*>(sm + P.samp);          // [2][kRC][nsamp]
+    float2* F = reinterpret_cast<float2*>(sm + P.F);              // [2][nt][nl]
+    float* Gp = reinterpret_cast<float*>(sm + P.G);               // [2][nl^2]
+    float* rad = reinterpret_cast<float*>(sm + P.rad);
+    const int tid = threadIdx.x;
+    const int wa = 2 * blockIdx.x;
+    const bool two = wa + 1 < n_win;
+    const int wb = two ? wa + 1 : wa;
+    const float* __restrict__ v[2] = {vols + (long long)win_vol[wa] * vol_stride,
+                                      vols + (long long)win_vol[wb] * vol_stride};
+    const float2* __restrict__ vp[2] = {pairs ? pairs + win_vol[wa] * pair_volume_elems(n) : nullptr,
+                                        pairs ? pairs + win_vol[wb] * pair_volume_elems(n) : nullptr};
+    int sh[2][3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) sh[0][q] = win_shift[3 * wa + q], sh[1][q] = win_shift[3 * wb + q];
+    float acc[2][RPT];
+    int rpr[RPT];
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+        acc[0][q] = acc[1][q] = 0.0f;
+        rpr[q] = tid + q * kThreads < T.coeffs ? T.rowpack[tid + q * kThreads] : 0;
+    }
+    float th_w[NPC / 2];
+    int th_m = 0, th_base = 0;
+    float th_sgn = 1.0f;
+    if (tid < T.ntri) {
+        const int2 lm = T.tri_lm[tid];
+        th_m = lm.y;
+        th_base = lm.x * lm.x;
+        th_sgn = ((lm.x + lm.y) & 1) ? -1.0f : 1.0f;
+#pragma unroll
+        for (int t = 0; t < NPC / 2; ++t) th_w[t] = __ldg(T.ptab + (size_t)tid * NPC + t);
+    }
+    __syncthreads();
+    for (int ir = 0; ir < T.nr; ++ir) {
+        const int rc = ir % kRC;
+        if (rc == 0) {
+            const int nrc = min(kRC, T.nr - ir);
+            const int items = nsamp * kRC;
+            auto entry = [&](int it) {
+                const int s = it / kRC, j = it - s * kRC;
+                return (it < items && j < nrc) ? __ldg(T.samp + (size_t)s * T.nr + ir + j) : make_int4(0, 0, 0, 0);
+            };
+            int4 e_next = entry(tid);
+            for (int it = tid; it < items; it += kThreads) {
+                const int s = it / kRC, j = it - s * kRC;
+                const int4 e = e_next;
+                e_next = entry(it + kThreads);
+                if (j >= nrc) continue;
+                const int x0 = e.x & 1023, y0 = (e.x >> 10) & 1023, z0 = (e.x >> 20) & 1023;
+                const float fx = __int_as_float(e.y), fy = __int_as_float(e.z), fz = __int_as_float(e.w);
+                const bool gx0 = (unsigned)x0 < (unsigned)n, gx1 = (unsigned)(x0 + 1) < (unsigned)n;
+                const bool gy0 = (unsigned)y0 < (unsigned)n, gy1 = (unsigned)(y0 + 1) < (unsigned)n;
+                const bool gz0 = (unsigned)z0 < (unsigned)n, gz1 = (unsigned)(z0 + 1) < (unsigned)n;
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const int xs0 = x0 + sh[q][0], ys0 = y0 + sh[q][1], zs0 = z0 + sh[q][2];
+                    const bool vx0 = gx0 && (unsigned)xs0 < (unsigned)n;
+                    const bool vx1 = gx1 && (unsigned)(xs0 + 1) < (unsigned)n;
+                    const bool vy0 = gy0 && (unsigned)ys0 < (unsigned)n;
+                    const bool vy1 = gy1 && (unsigned)(ys0 + 1) < (unsigned)n;
+                    const bool vz0 = gz0 && (unsigned)zs0 < (unsigned)n;
+                    const bool vz1 = gz1 && (unsigned)(zs0 + 1) < (unsigned)n;
+                    float val = 0.0f;
+                    if (vp[q]) {
+                        const long long o0 = ((long long)zs0 * n + ys0) * (n + 1) + xs0 + 1;
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            const int bb = c & 1, aa = c >> 1;
+                            const bool vr = (bb ? vy1 : vy0) && (aa ? vz1 : vz0);
+                            const float2 pr = (vr && (vx0 || vx1))
+                                                  ? __ldg(vp[q] + o0 + (bb ? n + 1 : 0) + (aa ? (long long)n * (n + 1) : 0))
+                                                  : make_float2(0.0f, 0.0f);
+                            const float v0 = vx0 ? pr.x : 0.0f;
+                            const float v1 = vx1 ? pr.y : 0.0f;
+                            const float wyz = (bb ? fy : 1.0f - fy) * (aa ? fz : 1.0f - fz);
+                            val = fmaf(wyz, fmaf(fx, v1 - v0, v0), val);
+                        }
+                    } else {
+                        const long long o0 = ((long long)zs0 * n + ys0) * n + xs0;
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            const int bb = c & 1, aa = c >> 1;
+                            const bool vr = (bb ? vy1 : vy0) && (aa ? vz1 : vz0);
+                            const float* row = v[q] + o0 + (bb ? n : 0) + (aa ? (long long)n * n : 0);
+                            const float v0 = (vr && vx0) ? __ldg(row) : 0.0f;
+                            const float v1 = (vr && vx1) ? __ldg(row + 1) : 0.0f;
+                            const float wyz = (bb ? fy : 1.0f - fy) * (aa ? fz : 1.0f - fz);
+                            val = fmaf(wyz, fmaf(fx, v1 - v0, v0), val);
+                        }
+                    }
+                    samp[(q * kRC + j) * nsamp + s] = val;
+                }
+            }
+        }
+        for (int i = tid; i < T.pairs; i += kThreads) rad[i] = T.radial_t[(size_t)ir * T.pairs + i];
+        __syncthreads();
+        {  // 2. phi-DFT: thread = (window, order group, ring)
+            constexpr int MH = NPC / 2, MS = (MH + 1) / 2;
+            const int q = tid >> 7, g = (tid >> 6) & 1, t = tid & 63;
+            if (t < nt) {
+                const float* f = samp + (q * kRC + rc) * nsamp + t * np;
+                float2* Fr = F + (q * nt + t) * nl;
+                if (g == 0) dft_ring<NPC, 0, MS>(f, Fr);
+                else dft_ring<NPC, MS, MH>(f, Fr);
+            }
+        }
+        __syncthreads();
+        if (tid < T.ntri) {  // 3. theta, both windows with the same register weights
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const float2* Fq = F + q * nt * nl;
+                float re = 0.0f, im = 0.0f;
+#pragma unroll
+                for (int t = 0; t < NPC / 2; ++t) {
+                    const float2 a = Fq[t * nl + th_m], b = Fq[(NPC - 1 - t) * nl + th_m];
+                    re = fmaf(th_w[t], fmaf(th_sgn, b.x, a.x), re);
+                    im = fmaf(th_w[t], fmaf(th_sgn, b.y, a.y), im);
+                }
+                float* G = Gp + q * nl * nl;
+                if (th_m == 0) {
+                    G[th_base] = re;
+                } else {
+                    G[th_base + 2 * th_m - 1] = re;
+                    G[th_base + 2 * th_m] = im;
+                }
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int qq = 0; qq < RPT; ++qq) {  // 4. radial
+            const int row = tid + qq * kThreads;
+            if (row < T.coeffs) {
+                const int rp = rpr[qq];
+                const float rv = rad[rp >> 16];
+                acc[0][qq] = fmaf(rv, Gp[rp & 0xffff], acc[0][qq]);
+                acc[1][qq] = fmaf(rv, Gp[nl * nl + (rp & 0xffff)], acc[1][qq]);
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int qq = 0; qq < RPT; ++qq) {
+        const int row = tid + qq * kThreads;
+        if (row < T.coeffs) {
+            out[(long long)wa * ldo + row] = acc[0][qq];
+            if (two) out[(long long)wb * ldo + row] = acc[1][qq];
+        }
+    }
+}
+
+template <int RPT, int NPC>
+int launch_pair(const FactoredTables& T, const float* vols, long long vol_stride, const int* win_vol,
+                const int* win_shift, int n_win, float* out, int ldo, cudaStream_t s, const float2* pairs) {
+    const size_t smem = smem_plan_pair(T).total;
+    if (smem > 220 * 1024) return 1;
+    if (ensure_dynamic_smem(expand_pair_kernel<RPT, NPC>, (int)smem) != cudaSuccess) return 2;
+    expand_pair_kernel<RPT, NPC><<<(n_win + 1) / 2, kThreads, smem, s>>>(T, vols, vol_stride, win_vol, win_shift,
+                                                                           n_win, out, ldo, pairs);
+    return cudaGetLastError() == cudaSuccess ? 0 : 2;
+}
+
 template <int HALF, int RPT, int NPC = 0>
 int launch_t(const FactoredTables& T, size_t smem, const float* vols, long long vol_stride, const int* win_vol,
              const int* win_shift, int n_win, float* out, int ldo, cudaStream_t s, const float2* pairs) {
@@ -522,6 +722,14 @@ int launch_expand_factored(const FactoredTables& T, const float* vols, long long
         const char* e = std::getenv("BMB_EXPAND_CDFT");
         return !(e && std::atoi(e) == 0);
     }();
+    static const bool pair_windows = [] {
+        const char* e = std::getenv("BMB_EXPAND_PAIRWIN");
+        return !(e && std::atoi(e) == 0);
+    }();
+    if (cdft && pair_windows && n_win >= 2 && T.L + 1 == T.np / 2 && T.ntri <= kThreads) {
+        if (T.np == 18 && rpt <= 4) return launch_pair<4, 18>(T, vols, vol_stride, win_vol, win_shift, n_win, out, ldo, s, pairs);
+        if (T.np == 34 && rpt <= 12) return launch_pair<12, 34>(T, vols, vol_stride, win_vol, win_shift, n_win, out, ldo, s, pairs);
+    }
     if (cdft && T.L + 1 == T.np / 2) {  // n_phi = 2L + 2 with compile-time twiddles
         if (T.np == 18 && rpt <= 4) return launch_t<9, 4, 18>(T, smem, vols, vol_stride, win_vol, win_shift, n_win, out, ldo, s, pairs);
         if (T.np == 34 && rpt <= 12) return launch_t<17, 12, 34>(T, smem, vols, vol_stride, win_vol, win_shift, n_win, out, ldo, s, pairs);

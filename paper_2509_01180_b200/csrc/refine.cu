@@ -144,6 +144,9 @@ __device__ __forceinline__ float2 phase_of(const WarpScratch& w, int m, int mp) 
 #ifndef BMB_PIPE_MASK
 #define BMB_PIPE_MASK 0
 #endif
+#ifndef BMB_PF_MIN_GROUPS
+#define BMB_PF_MIN_GROUPS 4
+#endif
 template <int ORDER, bool SWEEP>
 struct EvalOpts {
     static constexpr int bit = SWEEP ? 4 : (ORDER == 2 ? 2 : 1);
@@ -200,8 +203,9 @@ __device__ __forceinline__ void warp_eval_k(const BandTables& T, const EvalJob (
     // the kernels are streamed once per evaluation: group g+1's rows are pulled
     // into L1 while group g runs (L2 latency off the recursion's critical path)
     // (kernels staged in shared memory by the fused refinement are not prefetched)
-    const bool pf_x = PF && __isGlobal(xi);
-    const bool pf_w = PF && WEDGE && __isGlobal(wx);
+    // (low bands: a group or two of short rows, nothing to hide the prefetch behind)
+    const bool pf_x = PF && T.n_groups > BMB_PF_MIN_GROUPS && __isGlobal(xi);
+    const bool pf_w = PF && WEDGE && T.n_groups > BMB_PF_MIN_GROUPS && __isGlobal(wx);
     if (T.n_groups > 0) {
         if (pf_x) prefetch_rows(xi, T.row_off[0], T.row_off[1], lane);
         if (pf_w) prefetch_rows(wx, T.row_off[0], T.row_off[1], lane);
