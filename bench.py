@@ -229,7 +229,9 @@ def config_block(batch):
 
 
 # kernel classes of the CUPTI breakdown (name prefix -> class)
-KCLASS = (("expand_factored", "expand"), ("split3_gemm", "expand"), ("gather_windows", "expand"),
+KCLASS = (("expand_factored", "expand"), ("expand_pair", "expand"), ("expand_theta", "expand"),
+          ("expand_radial", "expand"), ("pair_volumes", "expand"), ("split3_gemm", "expand"),
+          ("gather_windows", "expand"), ("advance_kernel", "newton"),
           ("eval_kernel<2", "eval_order2"), ("eval_kernel<0", "eval_order0"), ("compose_kernel", "compose"),
           ("iter_begin", "newton"), ("step_kernel", "newton"), ("accept_kernel", "newton"),
           ("band_begin", "newton"), ("final_", "newton"), ("prune", "newton"), ("seed_kernel", "seed"),
@@ -416,7 +418,8 @@ def run_product(args):
                    + 4.0 * ctx.n_r * ntri * ctx.n_theta + 2.0 * ctx.n_r * C)
         gemm_flops = per_win * windows_per_step
         peak_x = fp32_peak
-        roof_gemm = {"kernel": "expand_factored_kernel (trilinear samples, phi-DFT, theta + radial contractions)",
+        roof_gemm = {"kernel": "expand_pair_kernel / expand_factored_kernel (trilinear samples, phi-DFT, theta + "
+                               "radial contractions; two windows per CTA)",
                      "bound": "fp32_simt", "peak": peak_x, "peak_note": fp32_kind,
                      "algorithmic": "per window 16 S taps + 4 n_phi n_r n_theta (L+1) + 4 n_r tri(L) n_theta + "
                                     "2 n_r C, S=%d C=%d (%.2f MFLOP)" % (S, C, per_win / 1e6)}
