@@ -656,15 +656,14 @@ __device__ void make_trial(CandWork& wk, const CandState& st, const Quat& koff) 
     }
     const Quat h = q_from_euler(wk.e[0] + p[0], wk.e[1] + p[1], wk.e[2] + p[2]);
     wk.gt[0] = h.w, wk.gt[1] = h.x, wk.gt[2] = h.y, wk.gt[3] = h.z;
-    const Quat gt = st.anchored ? q_mul(h, qload(st.anchor)) : h;
-    const Euler3 et = q_euler(gt);
-    wk.et[0] = et.a, wk.et[1] = et.b, wk.et[2] = et.g;
     // frame of the trial's order-2 evaluation: the global angles (unanchored: the
     // next iteration's chart angles exactly), or for an anchored candidate the
-    // better-conditioned of g and g K
+    // better-conditioned of g and g K (its global angles et are not needed)
     if (st.anchored) {
-        choose_frame(gt, koff, wk.evt, wk.sidet, wk.tvt);
+        choose_frame(q_mul(h, qload(st.anchor)), koff, wk.evt, wk.sidet, wk.tvt);
     } else {
+        const Euler3 et = q_euler(h);
+        wk.et[0] = et.a, wk.et[1] = et.b, wk.et[2] = et.g;
         wk.evt[0] = et.a, wk.evt[1] = et.b, wk.evt[2] = et.g;
         wk.sidet = 0;
     }
