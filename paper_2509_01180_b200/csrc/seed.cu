@@ -15,7 +15,7 @@ namespace bmb {
 // shared-memory plan: [f | t] (later reused for one beta slice A_j), xi (or
 // the global scratch when it does not fit), scores, maxima
 struct SeedSmem {
-    size_t region0, xi, sc, maxima, bk, total;
+    size_t region0, xi, sc, maxima, bk, cands, total;
     bool xi_in_smem;
 };
 __host__ __device__ inline SeedSmem seed_smem_plan(int rows_low, int L, int nxi, int npt) {
@@ -27,13 +27,21 @@ __host__ __device__ inline SeedSmem seed_smem_plan(int rows_low, int L, int nxi,
     p.region0 = (p.region0 + 15) / 16 * 16;
     const size_t xib = sizeof(double2) * (size_t)nxi;
     const size_t bkb = sizeof(double2) * (size_t)wd * 64;  // b[k][m] for up to 64 gamma points
-    const size_t rest = sizeof(double) * npt + sizeof(int) * npt + bkb;
+    const bool cands_extra = sizeof(int) * (size_t)npt > bkb;
+    const size_t rest = sizeof(double) * npt + sizeof(int) * npt + bkb + (cands_extra ? sizeof(int) * npt : 0);
     p.xi_in_smem = p.region0 + xib + rest <= 200 * 1024;
     p.xi = p.region0;
     p.sc = p.xi + (p.xi_in_smem ? xib : 0);
     p.maxima = p.sc + sizeof(double) * npt;
     p.bk = (p.maxima + sizeof(int) * npt + 15) / 16 * 16;
     p.total = p.bk + bkb;
+    // axis-neighbour survivors: in the b[k][m] staging once the scores are done
+    if (!cands_extra) {
+        p.cands = p.bk;
+    } else {
+        p.cands = p.total;
+        p.total += sizeof(int) * (size_t)npt;
+    }
     return p;
 }
 
@@ -52,14 +60,14 @@ __global__ void __launch_bounds__(256) seed_kernel(SeedArgs a) {
     double* sc = reinterpret_cast<double*>(sm + plan.sc);
     double2* Bk = reinterpret_cast<double2*>(sm + plan.bk);
     int* maxima = reinterpret_cast<int*>(sm + plan.maxima);
-    __shared__ int n_max;
+    __shared__ int n_max, n_cand;
 
     const float* cw = a.coef + (long long)w * a.ldc;
     for (int r = threadIdx.x; r < nrow; r += blockDim.x) {
         f[r] = cw[r];
         t[r] = a.t_hat[r];
     }
-    if (threadIdx.x == 0) n_max = 0;
+    if (threadIdx.x == 0) n_max = n_cand = 0;
     __syncthreads();
 
     // xi_l[m,m'] = sum_k conj(f_klm) t_klm'  (xi_coefficients(f_hat, t_hat), xcorr.cpp:34-50)
@@ -136,9 +144,35 @@ __global__ void __launch_bounds__(256) seed_kernel(SeedArgs a) {
     }
 
     // strict local maxima over the 26-neighbourhood (alpha/gamma wrap, beta clamps);
-    // a plateau keeps its lowest flat index
+    // a plateau keeps its lowest flat index.  Two passes: the six axis neighbours
+    // reject most points with cheap index arithmetic, and only the survivors,
+    // compacted, run the full test (a warp no longer waits on its one survivor).
+    int* cands = reinterpret_cast<int*>(sm + plan.cands);
+    const int plane = a.na * a.ng;
     for (int idx = threadIdx.x; idx < npt; idx += blockDim.x) {
-        const int k = idx % a.ng, i = (idx / a.ng) % a.na, j = idx / (a.ng * a.na);
+        const int k = idx % a.ng, i = (idx / a.ng) % a.na, j = idx / plane;
+        const double s = sc[idx];
+        const int km = k == 0 ? idx + a.ng - 1 : idx - 1;
+        const int kp = k == a.ng - 1 ? idx - (a.ng - 1) : idx + 1;
+        const int im = i == 0 ? idx + (a.na - 1) * a.ng : idx - a.ng;
+        const int ip = i == a.na - 1 ? idx - (a.na - 1) * a.ng : idx + a.ng;
+        const int jm = j == 0 ? idx : idx - plane;
+        const int jp = j == a.nb - 1 ? idx : idx + plane;
+        const int nb6[6] = {km, kp, im, ip, jm, jp};
+        bool keep_pt = true;
+#pragma unroll
+        for (int u = 0; u < 6; ++u) {
+            const int other = nb6[u];
+            const double o = sc[other];
+            keep_pt = keep_pt && (other == idx || !(o > s || (o == s && other < idx)));
+        }
+        if (keep_pt) cands[atomicAdd(&n_cand, 1)] = idx;
+    }
+    __syncthreads();
+    const int nc = n_cand;
+    for (int q = threadIdx.x; q < nc; q += blockDim.x) {
+        const int idx = cands[q];
+        const int k = idx % a.ng, i = (idx / a.ng) % a.na, j = idx / plane;
         const double s = sc[idx];
         bool is_max = true;
         for (int dj = -1; dj <= 1 && is_max; ++dj) {
