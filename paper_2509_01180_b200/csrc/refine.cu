@@ -900,6 +900,19 @@ __global__ void __launch_bounds__(EvalShape<K>::WARPS * 32, BMB_EVAL_MINB(ORDER)
         }
 }
 
+// The Newton kernels are latency-bound dependent FP64 chains over one
+// candidate's CandWork (about 580 bytes) and CandState: requesting all of their
+// cache lines up front turns the chain's serialized DRAM round trips into one.
+__device__ __forceinline__ void prefetch_span(const void* p, size_t bytes) {
+    const size_t b = reinterpret_cast<size_t>(p);
+    for (size_t o = b & ~size_t(127); o < b + bytes; o += 128)
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(o));
+}
+__device__ __forceinline__ void prefetch_cand(const StageArgs& a, long long i) {
+    prefetch_span(a.work + i, sizeof(CandWork));
+    prefetch_span(a.cand + i, sizeof(CandState));
+}
+
 // Newton step of an order-2 evaluated candidate; true: a trial was made
 __device__ __forceinline__ bool step_one(const StageArgs& a, long long i) {
     CandWork& wk = a.work[i];
@@ -951,6 +964,7 @@ __global__ void BMB_NEWTON_BOUNDS step_kernel(StageArgs a, const int* list_in, c
     const int n_pad = (n + 31) & ~31;
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_pad; q += gridDim.x * blockDim.x) {
         const int i = q < n ? list_in[q] : -1;
+        if (i >= 0) prefetch_cand(a, i);
         const bool t = i >= 0 && step_one(a, i);
         wappend(t, i, list_out, count_out);
     }
@@ -1010,6 +1024,7 @@ __global__ void BMB_NEWTON_BOUNDS advance_kernel(StageArgs a, const int* list_in
         const int i = q < n ? list_in[q] : -1;
         bool trial = false, fresh = false;
         if (i >= 0) {
+            prefetch_cand(a, i);
             if (accept_one(a, i)) {
                 trial = true;  // damped retry
             } else if (a.work[i].status == ST_START) {
