@@ -789,6 +789,19 @@ __device__ __forceinline__ int iter_begin_one(const StageArgs& a, long long i) {
     return 1;
 }
 
+// The Newton kernels are latency-bound dependent FP64 chains over one
+// candidate's CandWork (about 580 bytes) and CandState: requesting all of their
+// cache lines up front turns the chain's serialized DRAM round trips into one.
+__device__ __forceinline__ void prefetch_span(const void* p, size_t bytes) {
+    const size_t b = reinterpret_cast<size_t>(p);
+    for (size_t o = b & ~size_t(127); o < b + bytes; o += 128)
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(o));
+}
+__device__ __forceinline__ void prefetch_cand(const StageArgs& a, long long i) {
+    prefetch_span(a.work + i, sizeof(CandWork));
+    prefetch_span(a.cand + i, sizeof(CandState));
+}
+
 // iteration start of the candidates on the start list (band start, or accepted
 // trials of the previous iteration); appends to the order-2 list and the step list
 __global__ void iter_begin_kernel(StageArgs a, const int* start, const int* start_count) {
@@ -796,6 +809,7 @@ __global__ void iter_begin_kernel(StageArgs a, const int* start, const int* star
     const int n_pad = (n + 31) & ~31;
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_pad; q += gridDim.x * blockDim.x) {
         const int i = q < n ? start[q] : -1;
+        if (i >= 0) prefetch_cand(a, i);
         const int f = i >= 0 ? iter_begin_one(a, i) : 0;
         wappend(f == 1, i, a.list2, a.counts + CNT_L2);
     }
@@ -900,20 +914,9 @@ __global__ void __launch_bounds__(EvalShape<K>::WARPS * 32, BMB_EVAL_MINB(ORDER)
         }
 }
 
-// The Newton kernels are latency-bound dependent FP64 chains over one
-// candidate's CandWork (about 580 bytes) and CandState: requesting all of their
-// cache lines up front turns the chain's serialized DRAM round trips into one.
-__device__ __forceinline__ void prefetch_span(const void* p, size_t bytes) {
-    const size_t b = reinterpret_cast<size_t>(p);
-    for (size_t o = b & ~size_t(127); o < b + bytes; o += 128)
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(o));
-}
-__device__ __forceinline__ void prefetch_cand(const StageArgs& a, long long i) {
-    prefetch_span(a.work + i, sizeof(CandWork));
-    prefetch_span(a.cand + i, sizeof(CandState));
-}
-
-// Newton step of an order-2 evaluated candidate; true: a trial was made
+// Newton step of an order-2 evaluated candidate; true: a trial is due (made here
+// unless the caller makes it: one inlined copy of make_trial per kernel)
+template <bool MAKE = true>
 __device__ __forceinline__ bool step_one(const StageArgs& a, long long i) {
     CandWork& wk = a.work[i];
     CandState& st = a.cand[i];
@@ -940,7 +943,7 @@ __device__ __forceinline__ bool step_one(const StageArgs& a, long long i) {
     }
     wk.lam = wk.lambda;
     wk.retry = 0;
-    make_trial(wk, st, Quat{a.prm.koffset[0], a.prm.koffset[1], a.prm.koffset[2], a.prm.koffset[3]});
+    if (MAKE) make_trial(wk, st, Quat{a.prm.koffset[0], a.prm.koffset[1], a.prm.koffset[2], a.prm.koffset[3]});
     wk.status = ST_EVAL0;
     return true;
 }
@@ -970,7 +973,8 @@ __global__ void BMB_NEWTON_BOUNDS step_kernel(StageArgs a, const int* list_in, c
     }
 }
 
-// acceptance test of a trial; true: it failed with retries left (re-queue)
+// acceptance test of a trial; true: it failed with retries left (re-queue after
+// the caller makes the damped trial)
 __device__ __forceinline__ bool accept_one(const StageArgs& a, long long i) {
     CandWork& wk = a.work[i];
     CandState& st = a.cand[i];
@@ -1004,7 +1008,6 @@ __device__ __forceinline__ bool accept_one(const StageArgs& a, long long i) {
         wk.status = ST_DONE;
         return false;
     }
-    make_trial(wk, st, Quat{a.prm.koffset[0], a.prm.koffset[1], a.prm.koffset[2], a.prm.koffset[3]});
     return true;
 }
 
@@ -1029,9 +1032,12 @@ __global__ void BMB_NEWTON_BOUNDS advance_kernel(StageArgs a, const int* list_in
                 trial = true;  // damped retry
             } else if (a.work[i].status == ST_START) {
                 const int f = iter_begin_one(a, i);
-                if (f == 2) trial = step_one(a, i);
+                if (f == 2) trial = step_one<false>(a, i);
                 else fresh = f == 1;
             }
+            if (trial)
+                make_trial(a.work[i], a.cand[i],
+                           Quat{a.prm.koffset[0], a.prm.koffset[1], a.prm.koffset[2], a.prm.koffset[3]});
         }
         wappend(trial, i, trial_out, trial_count);
         wappend(fresh, i, fresh_out, fresh_count);
@@ -1085,8 +1091,11 @@ __global__ void final_prep_kernel(StageArgs a) {
 
 __global__ void final_score_kernel(StageArgs a) {
     const int n = a.counts[CNT_L2];
-    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x)
-        final_score_one(a, a.list2[q]);
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+        const int i = a.list2[q];
+        prefetch_cand(a, i);
+        final_score_one(a, i);
+    }
 }
 
 // prune_after_band (optimize.cpp:391-403): after the first band every candidate

@@ -51,16 +51,14 @@ BMB_HD Euler3 q_euler(const Quat& q) {
     Euler3 e;
     const double sb = hypot(m02, m12);
     e.b = atan2(sb, m22);
-    if (sb > 1e-12) {
-        e.a = atan2(m12, m02);
-        e.g = atan2(m21, -m20);
-    } else if (m22 > 0.0) {
-        e.a = atan2(m10, m00);
-        e.g = 0.0;
-    } else {
-        e.a = atan2(-m10, -m00);
-        e.g = 0.0;
+    // one atan2 per angle (the branches pick its arguments; atan2(0, 1) = +0)
+    double ya = m12, xa = m02, yg = m21, xg = -m20;
+    if (!(sb > 1e-12)) {
+        const double s = m22 > 0.0 ? 1.0 : -1.0;
+        ya = s * m10, xa = s * m00, yg = 0.0, xg = 1.0;
     }
+    e.a = atan2(ya, xa);
+    e.g = atan2(yg, xg);
     return e;
 }
 // geodesic angle to the identity, radians (angle_to, rotation.cpp:102-107)
@@ -73,19 +71,36 @@ BMB_HD double q_angle(const Quat& q) {
 // (src/optimize.cpp:316-323): full pivoting in column-major search order,
 // rank threshold = eps * 3 * |largest pivot|.
 struct LU3 {
+    // every index below is a compile-time constant after unrolling (the pivot
+    // swaps are predicated), so the factors stay in registers
     double a[3][3];
     int rp[3], cp[3];
     int nz;
     double maxpiv;
+    static BMB_HD void swap_(double& x, double& y) {
+        const double t = x;
+        x = y;
+        y = t;
+    }
     BMB_HD void factor(const double m[9]) {
+#pragma unroll
         for (int i = 0; i < 3; ++i)
+#pragma unroll
             for (int j = 0; j < 3; ++j) a[i][j] = m[i * 3 + j];
         nz = 3;
         maxpiv = 0.0;
+        bool stop = false;
+#pragma unroll
         for (int k = 0; k < 3; ++k) {
+            if (stop) {
+                rp[k] = cp[k] = k;
+                continue;
+            }
             int br = k, bc = k;
             double big = -1.0;
+#pragma unroll
             for (int j = k; j < 3; ++j)
+#pragma unroll
                 for (int i = k; i < 3; ++i) {
                     const double v = fabs(a[i][j]);
                     if (v > big) {
@@ -96,27 +111,29 @@ struct LU3 {
                 }
             if (big == 0.0) {
                 nz = k;
-                for (int i = k; i < 3; ++i) rp[i] = cp[i] = i;
-                break;
+                stop = true;
+                rp[k] = cp[k] = k;
+                continue;
             }
             if (big > maxpiv) maxpiv = big;
             rp[k] = br;
             cp[k] = bc;
-            if (br != k)
-                for (int j = 0; j < 3; ++j) {
-                    const double t = a[k][j];
-                    a[k][j] = a[br][j];
-                    a[br][j] = t;
-                }
-            if (bc != k)
-                for (int i = 0; i < 3; ++i) {
-                    const double t = a[i][k];
-                    a[i][k] = a[i][bc];
-                    a[i][bc] = t;
-                }
+#pragma unroll
+            for (int i = k + 1; i < 3; ++i)
+                if (br == i)
+#pragma unroll
+                    for (int j = 0; j < 3; ++j) swap_(a[k][j], a[i][j]);
+#pragma unroll
+            for (int j = k + 1; j < 3; ++j)
+                if (bc == j)
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) swap_(a[i][k], a[i][j]);
             if (k < 2) {
+#pragma unroll
                 for (int i = k + 1; i < 3; ++i) a[i][k] /= a[k][k];
+#pragma unroll
                 for (int i = k + 1; i < 3; ++i)
+#pragma unroll
                     for (int j = k + 1; j < 3; ++j) a[i][j] -= a[i][k] * a[k][j];
             }
         }
@@ -124,33 +141,33 @@ struct LU3 {
     BMB_HD bool invertible() const {
         const double thr = 2.220446049250313e-16 * 3.0 * fabs(maxpiv);
         int rank = 0;
-        for (int i = 0; i < nz; ++i)
-            if (fabs(a[i][i]) > thr) ++rank;
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+            if (i < nz && fabs(a[i][i]) > thr) ++rank;
         return rank == 3;
     }
     BMB_HD void solve(const double b[3], double x[3]) const {
-        double c[3] = {b[0], b[1], b[2]};
-        for (int k = 0; k < 3; ++k)
-            if (rp[k] != k) {
-                const double t = c[k];
-                c[k] = c[rp[k]];
-                c[rp[k]] = t;
-            }
-        for (int i = 1; i < 3; ++i)
-            for (int j = 0; j < i; ++j) c[i] -= a[i][j] * c[j];
-        for (int i = 2; i >= 0; --i) {
-            for (int j = i + 1; j < 3; ++j) c[i] -= a[i][j] * c[j];
-            c[i] /= a[i][i];
-        }
-        for (int k = 2; k >= 0; --k)
-            if (cp[k] != k) {
-                const double t = c[k];
-                c[k] = c[cp[k]];
-                c[cp[k]] = t;
-            }
-        x[0] = c[0];
-        x[1] = c[1];
-        x[2] = c[2];
+        // P^T b (rows), L and U substitutions, then Q (columns) -- written out in
+        // scalars so that nothing is addressed dynamically
+        double c0 = b[0], c1 = b[1], c2 = b[2], t;
+        if (rp[0] == 1) t = c0, c0 = c1, c1 = t;
+        else if (rp[0] == 2) t = c0, c0 = c2, c2 = t;
+        if (rp[1] == 2) t = c1, c1 = c2, c2 = t;
+        c1 -= a[1][0] * c0;
+        c2 -= a[2][0] * c0;
+        c2 -= a[2][1] * c1;
+        c2 /= a[2][2];
+        c1 -= a[1][2] * c2;
+        c1 /= a[1][1];
+        c0 -= a[0][1] * c1;
+        c0 -= a[0][2] * c2;
+        c0 /= a[0][0];
+        if (cp[1] == 2) t = c1, c1 = c2, c2 = t;
+        if (cp[0] == 1) t = c0, c0 = c1, c1 = t;
+        else if (cp[0] == 2) t = c0, c0 = c2, c2 = t;
+        x[0] = c0;
+        x[1] = c1;
+        x[2] = c2;
     }
 };
 
