@@ -602,7 +602,8 @@ __device__ void chart_transform(Derivs& f, const double* te, const double* tv) {
     Wi[7] = Wp[1] * Wp[6] - Wp[0] * Wp[7];
     Wi[8] = Wp[0] * Wp[4] - Wp[1] * Wp[3];
     const double det = Wp[0] * Wi[0] + Wp[1] * Wi[3] + Wp[2] * Wi[6];
-    for (int i = 0; i < 9; ++i) Wi[i] /= det;
+    const double rdet = 1.0 / det;
+    for (int i = 0; i < 9; ++i) Wi[i] *= rdet;
     double J[9];
     mat3_mul(Wi, We, J);
     double g[3], H[9];
@@ -760,8 +761,16 @@ __device__ __forceinline__ int iter_begin_one(const StageArgs& a, long long i) {
     const Quat g = qload(st.g);
     const Quat koff{a.prm.koffset[0], a.prm.koffset[1], a.prm.koffset[2], a.prm.koffset[3]};
     const bool was_anchored = st.anchored != 0;
-    Quat h = q_mul(g, q_inv(qload(st.anchor)));
-    Euler3 e = q_euler(h);
+    // an unanchored candidate that just accepted its trial sits at the trial's
+    // global angles (g = h_try exactly: the anchor is the identity)
+    Quat h = g;
+    Euler3 e;
+    if (wk.fresh && !was_anchored) {
+        e.a = wk.et[0], e.b = wk.et[1], e.g = wk.et[2];
+    } else {
+        h = q_mul(g, q_inv(qload(st.anchor)));
+        e = q_euler(h);
+    }
     bool reanchored = false;
     if (e.b < 0.05 || e.b > kPiD - 0.05) {
         qstore(st.anchor, q_mul(q_inv(koff), g));
