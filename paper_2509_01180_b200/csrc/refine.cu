@@ -801,10 +801,15 @@ __device__ __forceinline__ int iter_begin_one(const StageArgs& a, long long i) {
 // The Newton kernels are latency-bound dependent FP64 chains over one
 // candidate's CandWork (about 580 bytes) and CandState: requesting all of their
 // cache lines up front turns the chain's serialized DRAM round trips into one.
+#ifndef BMB_PF_LEVEL
+#define BMB_PF_LEVEL 1
+#endif
 __device__ __forceinline__ void prefetch_span(const void* p, size_t bytes) {
     const size_t b = reinterpret_cast<size_t>(p);
-    for (size_t o = b & ~size_t(127); o < b + bytes; o += 128)
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(o));
+    for (size_t o = b & ~size_t(127); o < b + bytes; o += 128) {
+        if (BMB_PF_LEVEL == 1) asm volatile("prefetch.global.L1 [%0];" ::"l"(o));
+        if (BMB_PF_LEVEL == 2) asm volatile("prefetch.global.L2 [%0];" ::"l"(o));
+    }
 }
 __device__ __forceinline__ void prefetch_cand(const StageArgs& a, long long i) {
     prefetch_span(a.work + i, sizeof(CandWork));
