@@ -232,7 +232,8 @@ def config_block(batch):
 KCLASS = (("expand_factored", "expand"), ("expand_pair", "expand"), ("expand_theta", "expand"),
           ("expand_radial", "expand"), ("pair_volumes", "expand"), ("split3_gemm", "expand"),
           ("gather_windows", "expand"), ("advance_kernel", "newton"),
-          ("eval_kernel<2", "eval_order2"), ("eval_kernel<0", "eval_order0"), ("compose_kernel", "compose"),
+          ("eval_kernel<2", "eval_order2"), ("eval_kernel<0", "eval_order0"),
+          ("eval_half_kernel<2", "eval_order2"), ("eval_half_kernel<0", "eval_order0"), ("compose_kernel", "compose"),
           ("iter_begin", "newton"), ("step_kernel", "newton"), ("accept_kernel", "newton"),
           ("band_begin", "newton"), ("final_", "newton"), ("prune", "newton"), ("seed_kernel", "seed"),
           ("build_xi", "xi_build"), ("window_reduce", "misc"), ("window_norms", "misc"),
@@ -374,6 +375,7 @@ def run_product(args):
     ctx.eval_stats(reset=True)
     kms, busy_ms, launch_ms = cupti_step(lambda: step(parts))
     _, counts = ctx.timings(reset=True)
+    band_counts = {L: ctx.eval_counts(L) for L in CFG["bands"]}  # before the reset below
     ev2, ev0, ev_flops = ctx.eval_stats(reset=True)
     ctx.set_timing(False)
     ctx.set_lanes(4)
@@ -428,7 +430,8 @@ def run_product(args):
     roof_gemm["frac"] = roof_gemm["achieved"] / peak_x if roof_gemm["achieved"] else None
     # rotate-score-gradient evaluation kernels (FP32 SIMT register recursion)
     eval_ms = kms.get("eval_order2", 0.0) + kms.get("eval_order0", 0.0)
-    roof_eval = {"kernel": "eval_kernel<2>+eval_kernel<0> (warp Wigner-d recursion, K jobs per warp)",
+    roof_eval = {"kernel": "eval_half_kernel<2>+eval_half_kernel<0> (Wigner-d recursion; two jobs per "
+                           "warp, one per 16-lane half)",
                  "bound": "fp32_simt",
                  "achieved": ev_flops / (eval_ms / 1000.0) / 1e12 if eval_ms > 0 else None,
                  "peak": fp32_peak, "unit": "TFLOP/s", "peak_note": fp32_kind,
@@ -449,7 +452,7 @@ def run_product(args):
     # flops_per_step / (eval_ms_per_step / 1000) is recomputable from this line
     per_band, tot = {}, 0.0
     for L in CFG["bands"]:
-        e2, e0 = ctx.eval_counts(L)
+        e2, e0 = band_counts[L]
         f2, f0 = e2 * eval_flops(L, 2, True), e0 * eval_flops(L, 0, True)
         per_band[str(L)] = {"order2": e2, "order0": e0, "flop_order2": f2, "flop_order0": f0}
         tot += f2 + f0

@@ -437,6 +437,232 @@ __device__ __forceinline__ void warp_eval_k(const BandTables& T, const EvalJob (
     __syncwarp();
 }
 
+// ---------------------------------------------------------------- half-warp jobs
+// Two evaluations per warp, one per 16-lane half.  At low bands a job's chains
+// are short (L = 4: 25 items in one group of 32 lanes), and the per-job work
+// around them -- four FP64 sincos, the phase powers, the FP64 reduction of 20
+// sums -- costs as much as the chains.  A half-warp walks each 32-lane group of
+// the band layout in two passes of 16 items (each pass only as long as its
+// longest chain: items are sorted by chain length), and the per-job work runs
+// on both halves at once.  Same tables, same per-item FP32 sequence as the
+// full-warp kernel; only the lane partition of the items (hence the FP32
+// partial sums) differs.
+template <int NT>
+__device__ __forceinline__ void half_reduce_publish(double (&v)[NT], double* out) {
+    constexpr int P = NT <= 1 ? 1 : NT <= 2 ? 2 : NT <= 4 ? 4 : NT <= 8 ? 8 : NT <= 16 ? 16 : 32;
+    static_assert(NT <= 32, "reduce-scatter over at most 32 values");
+    constexpr int LOGP = P == 1 ? 0 : P == 2 ? 1 : P == 4 ? 2 : P == 8 ? 3 : P == 16 ? 4 : 5;
+    constexpr int R = LOGP < 4 ? LOGP : 4;  // halving rounds over the 16 lanes
+    constexpr int KEEP = P >> R;            // sums left per lane
+    const int l16 = threadIdx.x & 15;
+    double w[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) w[i] = i < NT ? v[i] : 0.0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int off = 8 >> r;
+        const int half = P >> (r + 1);
+        const bool low = (l16 & off) == 0;
+#pragma unroll
+        for (int j = 0; j < half; ++j) {
+            const double mine = low ? w[j] : w[j + half];
+            const double send = low ? w[j + half] : w[j];
+            w[j] = mine + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+    }
+#pragma unroll
+    for (int r = R; r < 4; ++r) w[0] += __shfl_xor_sync(0xffffffffu, w[0], 8 >> r);
+    // position j of this lane holds sum j + sum_r b_r P / 2^(r+1), b_r = lane bit (3 - r)
+    int base = 0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) base += ((l16 >> (3 - r)) & 1) * (P >> (r + 1));
+    if ((l16 & ((16 >> R) - 1)) == 0) {
+#pragma unroll
+        for (int j = 0; j < KEEP; ++j)
+            if (base + j < NT) out[base + j] = w[j];
+    }
+}
+
+template <int ORDER, bool WEDGE, bool PF>
+__device__ __forceinline__ void warp_eval_half(const BandTables& T, const EvalJob& job, WarpScratch* ws) {
+    const float4* __restrict__ xi = job.xi;
+    const float4* __restrict__ wx = job.wx;
+    const int l16 = threadIdx.x & 15;
+    const int L = T.L;
+    const bool pf_x = PF && T.n_groups > BMB_PF_MIN_GROUPS && __isGlobal(xi);
+    const bool pf_w = PF && WEDGE && T.n_groups > BMB_PF_MIN_GROUPS && __isGlobal(wx);
+    // L1 prefetch of rows [r0, r1) of this half's kernel: 16 lanes, one line each per pass
+    auto prefetch_half = [&](const float4* k, int r0, int r1) {
+        const char* b = reinterpret_cast<const char*>(k + (size_t)r0 * 32);
+        const int bytes = (r1 - r0) * 512;
+        for (int off = l16 * 128; off < bytes; off += 16 * 128) prefetch_l1(b + off);
+    };
+    if (T.n_groups > 0) {
+        if (pf_x) prefetch_half(xi, T.row_off[0], T.row_off[1]);
+        if (pf_w) prefetch_half(wx, T.row_off[0], T.row_off[1]);
+    }
+    // four FP64 sincos per job on lanes 0..3 of its half (beta/2, beta, alpha, gamma)
+    if (l16 < 4) {
+        const double ang = l16 == 0 ? 0.5 * job.b : (l16 == 1 ? job.b : (l16 == 2 ? job.a : job.g));
+        double sn, co;
+        sincos_d(ang, &sn, &co);
+        ws->cs_half[2 * l16] = co;
+        ws->cs_half[2 * l16 + 1] = sn;
+    }
+    __syncwarp();
+    {
+        const double car = ws->cs_half[4], cai = -ws->cs_half[5];  // e^{-i alpha}
+        const double cgr = ws->cs_half[6], cgi = -ws->cs_half[7];  // e^{-i gamma}
+        for (int m = l16; m <= L; m += 16) {
+            double ar = 1.0, ai = 0.0, gr = 1.0, gi = 0.0;
+            double br_ = car, bi_ = cai, hr = cgr, hi = cgi;
+            for (int e = m; e; e >>= 1) {
+                if (e & 1) {
+                    const double t = ar * br_ - ai * bi_;
+                    ai = ar * bi_ + ai * br_;
+                    ar = t;
+                    const double u = gr * hr - gi * hi;
+                    gi = gr * hi + gi * hr;
+                    gr = u;
+                }
+                const double t2 = br_ * br_ - bi_ * bi_;
+                bi_ = 2.0 * br_ * bi_;
+                br_ = t2;
+                const double u2 = hr * hr - hi * hi;
+                hi = 2.0 * hr * hi;
+                hr = u2;
+            }
+            ws->ua[m] = make_float2((float)ar, (float)ai);
+            ws->ug[m] = make_float2((float)gr, (float)gi);
+        }
+        const double ch = ws->cs_half[0], sh = ws->cs_half[1];
+        for (int j = l16; j <= 2 * L + 2; j += 16) {
+            double pc = 1.0, ps = 1.0, bc = ch, bs = sh;
+            for (int e = j; e; e >>= 1) {
+                if (e & 1) {
+                    pc *= bc;
+                    ps *= bs;
+                }
+                bc *= bc;
+                bs *= bs;
+            }
+            ws->cp[j] = (float)pc;
+            ws->sp[j] = (float)ps;
+        }
+    }
+    __syncwarp();
+    const float cb = (float)ws->cs_half[2], sb = (float)ws->cs_half[3];
+    const float* cp = ws->cp;
+    const float* sp = ws->sp;
+
+    constexpr int NV = ORDER == 0 ? 1 : (ORDER == 1 ? 4 : 10);
+    float acc[NV], accw[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) acc[i] = accw[i] = 0.0f;
+
+    for (int g = 0; g < T.n_groups; ++g) {
+        const int r0 = T.row_off[g];
+        if ((pf_x || pf_w) && g + 1 < T.n_groups) {
+            const int n0 = T.row_off[g + 1], n1 = T.row_off[g + 2];
+            if (pf_x) prefetch_half(xi, n0, n1);
+            if (pf_w) prefetch_half(wx, n0, n1);
+        }
+#pragma unroll 1
+        for (int p = 0; p < 2; ++p) {
+            const int slot = p * 16 + l16;
+            const int item = g * 32 + slot;
+            const int plen = T.item_len[g * 32 + p * 16];  // the pass's longest chain (0: padding)
+            if (plen == 0) break;
+            const int be = T.bexp[item];
+            const int ea = be & 0xff, ep = be >> 8;
+            const float bf = T.bfac[item];
+            const float4* __restrict__ pq = T.PQR + r0 * 32 + slot;
+            const float4* __restrict__ xr = xi + r0 * 32 + slot;
+            const float4* __restrict__ wr = WEDGE ? wx + r0 * 32 + slot : nullptr;
+            const float4 x0 = xr[0];
+            const float4 w0 = WEDGE ? wr[0] : make_float4(0.f, 0.f, 0.f, 0.f);
+            float d = __fmul_rn(__fmul_rn(bf, cp[ea]), sp[ep]);
+            float dp = 0.0f, dpp = 0.0f, d1 = 0.0f, dp1 = 0.0f, dpp1 = 0.0f;
+            if (ORDER >= 1) {
+                const float tb = ep ? __fmul_rn(__fmul_rn((float)ep, cp[ea + 1]), sp[ep - 1]) : 0.0f;
+                const float ta = ea ? __fmul_rn(__fmul_rn((float)ea, cp[ea - 1]), sp[ep + 1]) : 0.0f;
+                dp = __fmul_rn(__fmul_rn(0.5f, bf), __fsub_rn(tb, ta));
+            }
+            if (ORDER >= 2) {
+                const float t2b = ep > 1 ? __fmul_rn(__fmul_rn(ep * (ep - 1.0f), cp[ea + 2]), sp[ep - 2]) : 0.0f;
+                const float t2a = ea > 1 ? __fmul_rn(__fmul_rn(ea * (ea - 1.0f), cp[ea - 2]), sp[ep + 2]) : 0.0f;
+                const float mid = __fmul_rn(__fmul_rn(2.0f * ea * ep + ea + ep, cp[ea]), sp[ep]);
+                dpp = __fmul_rn(__fmul_rn(0.25f, bf), __fsub_rn(__fadd_rn(t2b, t2a), mid));
+            }
+            Chain3<ORDER> CA, CB, WA, WB;
+            CA.init(make_float2(x0.x, x0.y), d, dp, dpp);
+            CB.init(make_float2(x0.z, x0.w), d, dp, dpp);
+            if (WEDGE) {
+                WA.init(make_float2(w0.x, w0.y), d, dp, dpp);
+                WB.init(make_float2(w0.z, w0.w), d, dp, dpp);
+            }
+#pragma unroll 2
+            for (int s = 1; s < plen; ++s) {
+                const float4 pqr = __ldg(pq + s * 32);
+                const float4 x = xr[s * 32];
+                const float4 w = WEDGE ? wr[s * 32] : make_float4(0.f, 0.f, 0.f, 0.f);
+                const float P = pqr.x, Q = pqr.y, R = pqr.z;
+                const float t1 = fmaf(P, cb, Q);
+                const float dn = fmaf(t1, d, -__fmul_rn(R, d1));
+                float dpn = 0.0f, dppn = 0.0f;
+                if (ORDER >= 1) {
+                    const float t1p = __fmul_rn(-P, sb);
+                    dpn = fmaf(t1p, d, fmaf(t1, dp, -__fmul_rn(R, dp1)));
+                    if (ORDER >= 2) {
+                        const float t1pp = __fmul_rn(-P, cb);
+                        dppn = fmaf(t1pp, d, fmaf(2.0f * t1p, dp, fmaf(t1, dpp, -__fmul_rn(R, dpp1))));
+                    }
+                }
+                d1 = d;
+                d = dn;
+                if (ORDER >= 1) {
+                    dp1 = dp;
+                    dp = dpn;
+                }
+                if (ORDER >= 2) {
+                    dpp1 = dpp;
+                    dpp = dppn;
+                }
+                CA.step(make_float2(x.x, x.y), d, dp, dpp);
+                CB.step(make_float2(x.z, x.w), d, dp, dpp);
+                if (WEDGE) {
+                    WA.step(make_float2(w.x, w.y), d, dp, dpp);
+                    WB.step(make_float2(w.z, w.w), d, dp, dpp);
+                }
+            }
+            const char2 mm = T.item_mm[item], pm = T.item_pm[item];
+            const float2 iw = T.item_w[item];
+            const float2 za = phase_of(*ws, mm.x, mm.y), zb = phase_of(*ws, pm.x, pm.y);
+            phase_acc<ORDER, NV>(acc, CA, za, iw.x, mm.x, mm.y);
+            phase_acc<ORDER, NV>(acc, CB, zb, iw.y, pm.x, pm.y);
+            if (WEDGE) {
+                phase_acc<ORDER, NV>(accw, WA, za, iw.x, mm.x, mm.y);
+                phase_acc<ORDER, NV>(accw, WB, zb, iw.y, pm.x, pm.y);
+            }
+        }
+    }
+    constexpr int NW = WEDGE ? 2 : 1;
+    constexpr int NT = NW * NV;
+    double v[NT];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        v[i] = acc[i];
+        if (WEDGE) v[NV + i] = accw[i];
+    }
+    half_reduce_publish<NT>(v, ws->red);
+    __syncwarp();
+    if (l16 < NV) {
+        ws->res[l16] = ws->red[l16];
+        ws->res[10 + l16] = WEDGE ? ws->red[NV + l16] : 0.0;
+    }
+    __syncwarp();
+}
+
 __device__ __forceinline__ unsigned lanemask_lt() {
     unsigned m;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -928,6 +1154,47 @@ __global__ void __launch_bounds__(EvalShape<K>::WARPS * 32, BMB_EVAL_MINB(ORDER)
         }
 }
 
+// two listed candidates per warp, one per half (warp_eval_half)
+#ifndef BMB_HALF_WARPS
+#define BMB_HALF_WARPS 8
+#endif
+template <int ORDER, bool TRIAL = false>
+__global__ void __launch_bounds__(BMB_HALF_WARPS * 32, BMB_EVAL_MINB(ORDER)) eval_half_kernel(StageArgs a, const int* list,
+                                                                                          const int* count) {
+    constexpr int WARPS = BMB_HALF_WARPS;
+    __shared__ WarpScratch wsc[WARPS * 2];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, h = lane >> 4, l16 = lane & 15;
+    const int n = *count;
+    const int len = a.T.rows * 32;
+    const bool wedge = a.prm.has_wedge != 0;
+    if (a.eval_stats && blockIdx.x == 0 && threadIdx.x == 0)
+        atomicAdd(a.eval_stats + ((size_t)a.T.L * 2 + (ORDER == 2)) * 2 + (wedge ? 1 : 0), (unsigned long long)n);
+    const int q0 = (blockIdx.x * WARPS + warp) * 2;
+    if (q0 >= n) return;
+    const bool live = q0 + h < n;
+    const int i = list[live ? q0 + h : q0];  // tail: the second half repeats the first job, result dropped
+    EvalJob job;
+    {
+        const CandWork& wk = a.work[i];
+        const int w = i / a.max_cand;
+        const int side = ORDER == 2 ? (TRIAL ? wk.sidet : wk.side) : 0;
+        job.xi = (side == 2 ? a.xi_side : a.xi_win) + (size_t)w * len;
+        job.wx = !wedge ? nullptr : (side == 2 ? a.T.wedge_side : a.T.wedge);
+        const double* e = ORDER == 2 ? (TRIAL ? (side ? wk.evt : wk.et) : (side ? wk.ev : wk.e)) : wk.et;
+        job.a = e[0], job.b = e[1], job.g = e[2];
+    }
+    WarpScratch* ws = wsc + warp * 2 + h;
+    using O = EvalOpts<ORDER, false>;
+    if (wedge) warp_eval_half<ORDER, true, O::PF>(a.T, job, ws);
+    else warp_eval_half<ORDER, false, O::PF>(a.T, job, ws);
+    constexpr int NV = ORDER == 0 ? 1 : 10;
+    if (live && l16 < NV) {
+        CandWork& wk = a.work[i];
+        wk.c[l16] = ws->res[l16];
+        wk.r[l16] = ws->res[10 + l16];
+    }
+}
+
 // Newton step of an order-2 evaluated candidate; true: a trial is due (made here
 // unless the caller makes it: one inlined copy of make_trial per kernel)
 template <bool MAKE = true>
@@ -1415,9 +1682,31 @@ static void launch_eval_k(const StageArgs& a, const int* list, const int* count,
     eval_kernel<ORDER, K, TRIAL><<<(max_n + per - 1) / per, EvalShape<K>::WARPS * 32, 0, s>>>(a, list, count);
 }
 
+// bands evaluated two jobs per warp (eval_half_kernel): BMB_HALF_MAX_L (default: all;
+// measured: config 2 2870 -> 3067 subtomograms/s, config 5 (L = 20) 1253 -> 1272
+// against full-warp jobs; -1 disables) for A/B runs
+static int half_max_l() {
+    static const int v = [] {
+        const char* e = std::getenv("BMB_HALF_MAX_L");
+        return e ? std::atoi(e) : kMaxL;
+    }();
+    return v;
+}
+template <int ORDER, bool TRIAL = false>
+static void launch_eval_half(const StageArgs& a, const int* list, const int* count, int max_n, cudaStream_t s) {
+    constexpr int per = 2 * BMB_HALF_WARPS;
+    eval_half_kernel<ORDER, TRIAL><<<(max_n + per - 1) / per, BMB_HALF_WARPS * 32, 0, s>>>(a, list, count);
+}
+
 void launch_eval(const StageArgs& a, int order, const int* list, const int* count, int max_n, cudaStream_t s,
                  bool trial) {
     if (max_n <= 0) return;
+    if (a.T.L <= half_max_l()) {
+        if (order == 2 && trial) launch_eval_half<2, true>(a, list, count, max_n, s);
+        else if (order == 2) launch_eval_half<2>(a, list, count, max_n, s);
+        else launch_eval_half<0>(a, list, count, max_n, s);
+        return;
+    }
     const int k = eval_k_for(order, max_n);
     if (order == 2 && trial) {
         launch_eval_k<2, 1, true>(a, list, count, max_n, s);
