@@ -233,7 +233,7 @@ KCLASS = (("expand_factored", "expand"), ("expand_pair", "expand"), ("expand_the
           ("expand_radial", "expand"), ("pair_volumes", "expand"), ("split3_gemm", "expand"),
           ("gather_windows", "expand"), ("advance_kernel", "newton"),
           ("eval_kernel<2", "eval_order2"), ("eval_kernel<0", "eval_order0"),
-          ("eval_half_kernel<2", "eval_order2"), ("eval_half_kernel<0", "eval_order0"), ("compose_kernel", "compose"),
+          ("eval_sub_kernel<2", "eval_order2"), ("eval_sub_kernel<0", "eval_order0"), ("compose_kernel", "compose"),
           ("iter_begin", "newton"), ("step_kernel", "newton"), ("accept_kernel", "newton"),
           ("band_begin", "newton"), ("final_", "newton"), ("prune", "newton"), ("seed_kernel", "seed"),
           ("build_xi", "xi_build"), ("window_reduce", "misc"), ("window_norms", "misc"),
@@ -430,8 +430,8 @@ def run_product(args):
     roof_gemm["frac"] = roof_gemm["achieved"] / peak_x if roof_gemm["achieved"] else None
     # rotate-score-gradient evaluation kernels (FP32 SIMT register recursion)
     eval_ms = kms.get("eval_order2", 0.0) + kms.get("eval_order0", 0.0)
-    roof_eval = {"kernel": "eval_half_kernel<2>+eval_half_kernel<0> (Wigner-d recursion; two jobs per "
-                           "warp, one per 16-lane half)",
+    roof_eval = {"kernel": "eval_sub_kernel<2>+eval_sub_kernel<0> (Wigner-d recursion; 16 lanes per job, "
+                           "8 at L=4)",
                  "bound": "fp32_simt",
                  "achieved": ev_flops / (eval_ms / 1000.0) / 1e12 if eval_ms > 0 else None,
                  "peak": fp32_peak, "unit": "TFLOP/s", "peak_note": fp32_kind,

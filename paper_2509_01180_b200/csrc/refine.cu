@@ -37,15 +37,17 @@ namespace {
 
 constexpr double kPiD = 3.14159265358979323846;
 
-struct WarpScratch {
-    float2 ua[kMaxL + 1];
-    float2 ug[kMaxL + 1];
-    float cp[2 * kMaxL + 3];
-    float sp[2 * kMaxL + 3];
+template <int ML>
+struct WarpScratchT {
+    float2 ua[ML + 1];
+    float2 ug[ML + 1];
+    float cp[2 * ML + 3];
+    float sp[2 * ML + 3];
     double res[20];     // reduced (value, grad[3], hess aa ab ag bb bg gg) x (corr, wedge)
     double red[32];     // reduce-scatter staging (first scratch set of a warp)
     double cs_half[8];  // cos, sin of beta/2, beta, alpha, gamma
 };
+using WarpScratch = WarpScratchT<kMaxL>;
 
 // single out-of-line copies of the FP64 math-library routines
 __device__ __noinline__ void sincos_d(double x, double* s, double* c) { sincos(x, s, c); }
@@ -128,7 +130,8 @@ __device__ __forceinline__ void phase_acc(float* ac, const Chain3<ORDER>& ch, fl
     }
 }
 
-__device__ __forceinline__ float2 phase_of(const WarpScratch& w, int m, int mp) {
+template <class WS>
+__device__ __forceinline__ float2 phase_of(const WS& w, int m, int mp) {
     float2 pa = w.ua[abs(m)], pg = w.ug[abs(mp)];
     if (m < 0) pa.y = -pa.y;
     if (mp < 0) pg.y = -pg.y;
@@ -447,22 +450,24 @@ __device__ __forceinline__ void warp_eval_k(const BandTables& T, const EvalJob (
 // on both halves at once.  Same tables, same per-item FP32 sequence as the
 // full-warp kernel; only the lane partition of the items (hence the FP32
 // partial sums) differs.
-template <int NT>
-__device__ __forceinline__ void half_reduce_publish(double (&v)[NT], double* out) {
+template <int NT, int LANES>
+__device__ __forceinline__ void sub_reduce_publish(double (&v)[NT], double* out) {
     constexpr int P = NT <= 1 ? 1 : NT <= 2 ? 2 : NT <= 4 ? 4 : NT <= 8 ? 8 : NT <= 16 ? 16 : 32;
     static_assert(NT <= 32, "reduce-scatter over at most 32 values");
+    static_assert(LANES == 8 || LANES == 16, "8- or 16-lane jobs");
     constexpr int LOGP = P == 1 ? 0 : P == 2 ? 1 : P == 4 ? 2 : P == 8 ? 3 : P == 16 ? 4 : 5;
-    constexpr int R = LOGP < 4 ? LOGP : 4;  // halving rounds over the 16 lanes
-    constexpr int KEEP = P >> R;            // sums left per lane
-    const int l16 = threadIdx.x & 15;
+    constexpr int LB = LANES == 16 ? 4 : 3;  // lane bits of a job
+    constexpr int R = LOGP < LB ? LOGP : LB;  // halving rounds over the job's lanes
+    constexpr int KEEP = P >> R;              // sums left per lane
+    const int ls = threadIdx.x & (LANES - 1);
     double w[P];
 #pragma unroll
     for (int i = 0; i < P; ++i) w[i] = i < NT ? v[i] : 0.0;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-        const int off = 8 >> r;
+        const int off = (LANES / 2) >> r;
         const int half = P >> (r + 1);
-        const bool low = (l16 & off) == 0;
+        const bool low = (ls & off) == 0;
 #pragma unroll
         for (int j = 0; j < half; ++j) {
             const double mine = low ? w[j] : w[j + half];
@@ -471,23 +476,24 @@ __device__ __forceinline__ void half_reduce_publish(double (&v)[NT], double* out
         }
     }
 #pragma unroll
-    for (int r = R; r < 4; ++r) w[0] += __shfl_xor_sync(0xffffffffu, w[0], 8 >> r);
-    // position j of this lane holds sum j + sum_r b_r P / 2^(r+1), b_r = lane bit (3 - r)
+    for (int r = R; r < LB; ++r) w[0] += __shfl_xor_sync(0xffffffffu, w[0], (LANES / 2) >> r);
+    // position j of this lane holds sum j + sum_r b_r P / 2^(r+1), b_r = lane bit (LB - 1 - r)
     int base = 0;
 #pragma unroll
-    for (int r = 0; r < R; ++r) base += ((l16 >> (3 - r)) & 1) * (P >> (r + 1));
-    if ((l16 & ((16 >> R) - 1)) == 0) {
+    for (int r = 0; r < R; ++r) base += ((ls >> (LB - 1 - r)) & 1) * (P >> (r + 1));
+    if ((ls & ((LANES >> R) - 1)) == 0) {
 #pragma unroll
         for (int j = 0; j < KEEP; ++j)
             if (base + j < NT) out[base + j] = w[j];
     }
 }
 
-template <int ORDER, bool WEDGE, bool PF>
-__device__ __forceinline__ void warp_eval_half(const BandTables& T, const EvalJob& job, WarpScratch* ws) {
+template <int ORDER, bool WEDGE, bool PF, int LANES, class WS>
+__device__ __forceinline__ void warp_eval_sub(const BandTables& T, const EvalJob& job, WS* ws) {
+    constexpr int PASSES = 32 / LANES;
     const float4* __restrict__ xi = job.xi;
     const float4* __restrict__ wx = job.wx;
-    const int l16 = threadIdx.x & 15;
+    const int l16 = threadIdx.x & (LANES - 1);
     const int L = T.L;
     const bool pf_x = PF && T.n_groups > BMB_PF_MIN_GROUPS && __isGlobal(xi);
     const bool pf_w = PF && WEDGE && T.n_groups > BMB_PF_MIN_GROUPS && __isGlobal(wx);
@@ -495,7 +501,7 @@ __device__ __forceinline__ void warp_eval_half(const BandTables& T, const EvalJo
     auto prefetch_half = [&](const float4* k, int r0, int r1) {
         const char* b = reinterpret_cast<const char*>(k + (size_t)r0 * 32);
         const int bytes = (r1 - r0) * 512;
-        for (int off = l16 * 128; off < bytes; off += 16 * 128) prefetch_l1(b + off);
+        for (int off = l16 * 128; off < bytes; off += LANES * 128) prefetch_l1(b + off);
     };
     if (T.n_groups > 0) {
         if (pf_x) prefetch_half(xi, T.row_off[0], T.row_off[1]);
@@ -513,7 +519,7 @@ __device__ __forceinline__ void warp_eval_half(const BandTables& T, const EvalJo
     {
         const double car = ws->cs_half[4], cai = -ws->cs_half[5];  // e^{-i alpha}
         const double cgr = ws->cs_half[6], cgi = -ws->cs_half[7];  // e^{-i gamma}
-        for (int m = l16; m <= L; m += 16) {
+        for (int m = l16; m <= L; m += LANES) {
             double ar = 1.0, ai = 0.0, gr = 1.0, gi = 0.0;
             double br_ = car, bi_ = cai, hr = cgr, hi = cgi;
             for (int e = m; e; e >>= 1) {
@@ -536,7 +542,7 @@ __device__ __forceinline__ void warp_eval_half(const BandTables& T, const EvalJo
             ws->ug[m] = make_float2((float)gr, (float)gi);
         }
         const double ch = ws->cs_half[0], sh = ws->cs_half[1];
-        for (int j = l16; j <= 2 * L + 2; j += 16) {
+        for (int j = l16; j <= 2 * L + 2; j += LANES) {
             double pc = 1.0, ps = 1.0, bc = ch, bs = sh;
             for (int e = j; e; e >>= 1) {
                 if (e & 1) {
@@ -568,10 +574,10 @@ __device__ __forceinline__ void warp_eval_half(const BandTables& T, const EvalJo
             if (pf_w) prefetch_half(wx, n0, n1);
         }
 #pragma unroll 1
-        for (int p = 0; p < 2; ++p) {
-            const int slot = p * 16 + l16;
+        for (int p = 0; p < PASSES; ++p) {
+            const int slot = p * LANES + l16;
             const int item = g * 32 + slot;
-            const int plen = T.item_len[g * 32 + p * 16];  // the pass's longest chain (0: padding)
+            const int plen = T.item_len[g * 32 + p * LANES];  // the pass's longest chain (0: padding)
             if (plen == 0) break;
             const int be = T.bexp[item];
             const int ea = be & 0xff, ep = be >> 8;
@@ -654,11 +660,11 @@ __device__ __forceinline__ void warp_eval_half(const BandTables& T, const EvalJo
         v[i] = acc[i];
         if (WEDGE) v[NV + i] = accw[i];
     }
-    half_reduce_publish<NT>(v, ws->red);
+    sub_reduce_publish<NT, LANES>(v, ws->red);
     __syncwarp();
-    if (l16 < NV) {
-        ws->res[l16] = ws->red[l16];
-        ws->res[10 + l16] = WEDGE ? ws->red[NV + l16] : 0.0;
+    for (int i = l16; i < NV; i += LANES) {
+        ws->res[i] = ws->red[i];
+        ws->res[10 + i] = WEDGE ? ws->red[NV + i] : 0.0;
     }
     __syncwarp();
 }
@@ -1154,25 +1160,32 @@ __global__ void __launch_bounds__(EvalShape<K>::WARPS * 32, BMB_EVAL_MINB(ORDER)
         }
 }
 
-// two listed candidates per warp, one per half (warp_eval_half)
+// 32 / LANES listed candidates per warp, one per LANES-lane slice (warp_eval_sub);
+// the scratch sets are sized for the bands the slice width serves
 #ifndef BMB_HALF_WARPS
 #define BMB_HALF_WARPS 8
 #endif
-template <int ORDER, bool TRIAL = false>
-__global__ void __launch_bounds__(BMB_HALF_WARPS * 32, BMB_EVAL_MINB(ORDER)) eval_half_kernel(StageArgs a, const int* list,
-                                                                                          const int* count) {
-    constexpr int WARPS = BMB_HALF_WARPS;
-    __shared__ WarpScratch wsc[WARPS * 2];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, h = lane >> 4, l16 = lane & 15;
+template <int LANES>
+struct SubShape {
+    static constexpr int ML = LANES == 8 ? 8 : kMaxL;  // 8-lane jobs serve L <= 8
+    using WS = WarpScratchT<ML>;
+};
+template <int ORDER, bool TRIAL, int LANES>
+__global__ void __launch_bounds__(BMB_HALF_WARPS * 32, BMB_EVAL_MINB(ORDER)) eval_sub_kernel(StageArgs a, const int* list,
+                                                                                         const int* count) {
+    constexpr int WARPS = BMB_HALF_WARPS, JOBS = 32 / LANES;
+    using WS = typename SubShape<LANES>::WS;
+    __shared__ WS wsc[WARPS * JOBS];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, h = lane / LANES, l16 = lane & (LANES - 1);
     const int n = *count;
     const int len = a.T.rows * 32;
     const bool wedge = a.prm.has_wedge != 0;
     if (a.eval_stats && blockIdx.x == 0 && threadIdx.x == 0)
         atomicAdd(a.eval_stats + ((size_t)a.T.L * 2 + (ORDER == 2)) * 2 + (wedge ? 1 : 0), (unsigned long long)n);
-    const int q0 = (blockIdx.x * WARPS + warp) * 2;
+    const int q0 = (blockIdx.x * WARPS + warp) * JOBS;
     if (q0 >= n) return;
     const bool live = q0 + h < n;
-    const int i = list[live ? q0 + h : q0];  // tail: the second half repeats the first job, result dropped
+    const int i = list[live ? q0 + h : q0];  // tail: idle slices repeat the first job, results dropped
     EvalJob job;
     {
         const CandWork& wk = a.work[i];
@@ -1183,16 +1196,17 @@ __global__ void __launch_bounds__(BMB_HALF_WARPS * 32, BMB_EVAL_MINB(ORDER)) eva
         const double* e = ORDER == 2 ? (TRIAL ? (side ? wk.evt : wk.et) : (side ? wk.ev : wk.e)) : wk.et;
         job.a = e[0], job.b = e[1], job.g = e[2];
     }
-    WarpScratch* ws = wsc + warp * 2 + h;
+    WS* ws = wsc + warp * JOBS + h;
     using O = EvalOpts<ORDER, false>;
-    if (wedge) warp_eval_half<ORDER, true, O::PF>(a.T, job, ws);
-    else warp_eval_half<ORDER, false, O::PF>(a.T, job, ws);
+    if (wedge) warp_eval_sub<ORDER, true, O::PF, LANES>(a.T, job, ws);
+    else warp_eval_sub<ORDER, false, O::PF, LANES>(a.T, job, ws);
     constexpr int NV = ORDER == 0 ? 1 : 10;
-    if (live && l16 < NV) {
-        CandWork& wk = a.work[i];
-        wk.c[l16] = ws->res[l16];
-        wk.r[l16] = ws->res[10 + l16];
-    }
+    for (int v = l16; v < NV; v += LANES)
+        if (live) {
+            CandWork& wk = a.work[i];
+            wk.c[v] = ws->res[v];
+            wk.r[v] = ws->res[10 + v];
+        }
 }
 
 // Newton step of an order-2 evaluated candidate; true: a trial is due (made here
@@ -1682,7 +1696,7 @@ static void launch_eval_k(const StageArgs& a, const int* list, const int* count,
     eval_kernel<ORDER, K, TRIAL><<<(max_n + per - 1) / per, EvalShape<K>::WARPS * 32, 0, s>>>(a, list, count);
 }
 
-// bands evaluated two jobs per warp (eval_half_kernel): BMB_HALF_MAX_L (default: all;
+// bands evaluated two or four jobs per warp (eval_sub_kernel): BMB_HALF_MAX_L (default: all;
 // measured: config 2 2870 -> 3067 subtomograms/s, config 5 (L = 20) 1253 -> 1272
 // against full-warp jobs; -1 disables) for A/B runs
 static int half_max_l() {
@@ -1692,10 +1706,26 @@ static int half_max_l() {
     }();
     return v;
 }
+// bands evaluated 8 lanes per job, four jobs per warp: BMB_QUARTER_MAX_L (default
+// 8, measured: config 2 3067 -> 3120 subtomograms/s against 16-lane jobs at L = 4, 8,
+// and 8-lane jobs at L = 16 were slower (3050); at most 8, the scratch size; -1 disables)
+static int quarter_max_l() {
+    static const int v = [] {
+        const char* e = std::getenv("BMB_QUARTER_MAX_L");
+        const int q = e ? std::atoi(e) : 8;
+        return q > 8 ? 8 : q;
+    }();
+    return v;
+}
+template <int ORDER, bool TRIAL, int LANES>
+static void launch_eval_sub_w(const StageArgs& a, const int* list, const int* count, int max_n, cudaStream_t s) {
+    constexpr int per = (32 / LANES) * BMB_HALF_WARPS;
+    eval_sub_kernel<ORDER, TRIAL, LANES><<<(max_n + per - 1) / per, BMB_HALF_WARPS * 32, 0, s>>>(a, list, count);
+}
 template <int ORDER, bool TRIAL = false>
 static void launch_eval_half(const StageArgs& a, const int* list, const int* count, int max_n, cudaStream_t s) {
-    constexpr int per = 2 * BMB_HALF_WARPS;
-    eval_half_kernel<ORDER, TRIAL><<<(max_n + per - 1) / per, BMB_HALF_WARPS * 32, 0, s>>>(a, list, count);
+    if (a.T.L <= quarter_max_l()) launch_eval_sub_w<ORDER, TRIAL, 8>(a, list, count, max_n, s);
+    else launch_eval_sub_w<ORDER, TRIAL, 16>(a, list, count, max_n, s);
 }
 
 void launch_eval(const StageArgs& a, int order, const int* list, const int* count, int max_n, cudaStream_t s,
