@@ -488,9 +488,13 @@ __device__ __forceinline__ void sub_reduce_publish(double (&v)[NT], double* out)
     }
 }
 
+#ifndef BMB_SUB_PIPE
+#define BMB_SUB_PIPE 0
+#endif
 template <int ORDER, bool WEDGE, bool PF, int LANES, class WS>
 __device__ __forceinline__ void warp_eval_sub(const BandTables& T, const EvalJob& job, WS* ws) {
     constexpr int PASSES = 32 / LANES;
+    constexpr bool SUB_PIPE = BMB_SUB_PIPE != 0;
     const float4* __restrict__ xi = job.xi;
     const float4* __restrict__ wx = job.wx;
     const int l16 = threadIdx.x & (LANES - 1);
@@ -607,11 +611,26 @@ __device__ __forceinline__ void warp_eval_sub(const BandTables& T, const EvalJob
                 WA.init(make_float2(w0.x, w0.y), d, dp, dpp);
                 WB.init(make_float2(w0.z, w0.w), d, dp, dpp);
             }
+            float4 pqn = (SUB_PIPE && plen > 1) ? __ldg(pq + 32) : make_float4(0.f, 0.f, 0.f, 0.f);
+            float4 xn = (SUB_PIPE && plen > 1) ? xr[32] : make_float4(0.f, 0.f, 0.f, 0.f);
+            float4 wn = (SUB_PIPE && WEDGE && plen > 1) ? wr[32] : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 2
             for (int s = 1; s < plen; ++s) {
-                const float4 pqr = __ldg(pq + s * 32);
-                const float4 x = xr[s * 32];
-                const float4 w = WEDGE ? wr[s * 32] : make_float4(0.f, 0.f, 0.f, 0.f);
+                float4 pqr, x, w;
+                if (SUB_PIPE) {
+                    pqr = pqn;
+                    x = xn;
+                    w = wn;
+                    if (s + 1 < plen) {
+                        pqn = __ldg(pq + (s + 1) * 32);
+                        xn = xr[(s + 1) * 32];
+                        if (WEDGE) wn = wr[(s + 1) * 32];
+                    }
+                } else {
+                    pqr = __ldg(pq + s * 32);
+                    x = xr[s * 32];
+                    w = WEDGE ? wr[s * 32] : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
                 const float P = pqr.x, Q = pqr.y, R = pqr.z;
                 const float t1 = fmaf(P, cb, Q);
                 const float dn = fmaf(t1, d, -__fmul_rn(R, d1));
