@@ -13,11 +13,11 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
   python bench.py --particles 64 --steps 1 --warmup 3 --no-cpu-baseline > $O/ncu_launch.log 2>&1; echo "launches=$?" >> $O/status.txt
 export BMB_NO_WARMUP=1
 timeout 900 ncu --set full --import-source on --clock-control none --nvtx --nvtx-include "bmb_band16/" \
-  -k regex:eval_kernel --launch-count 2 -o $O/eval_l16 python tools/probe_bands.py 64 > $O/ncu_eval.log 2>&1; echo "ncu_eval=$?" >> $O/status.txt
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:expand_factored --launch-skip 1 \
+  -k regex:"eval_kernel|eval_sub_kernel" --launch-count 2 -o $O/eval_l16 python tools/probe_bands.py 64 > $O/ncu_eval.log 2>&1; echo "ncu_eval=$?" >> $O/status.txt
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"expand_factored|expand_pair" --launch-skip 1 \
   --launch-count 1 -o $O/expand python tools/probe_bands.py 64 > $O/ncu_exp.log 2>&1; echo "ncu_exp=$?" >> $O/status.txt
-timeout 900 ncu --set full --import-source on --clock-control none --nvtx --nvtx-include "bmb_band16/" \
-  -k regex:advance_kernel --launch-count 1 -o $O/advance python tools/probe_bands.py 64 > $O/ncu_adv.log 2>&1; echo "ncu_adv=$?" >> $O/status.txt
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:advance_kernel \
+  --launch-skip 3 --launch-count 1 -o $O/advance python tools/probe_bands.py 1024 > $O/ncu_adv.log 2>&1; echo "ncu_adv=$?" >> $O/status.txt
 unset BMB_NO_WARMUP
 timeout 900 ncu --set full --clock-control none -k regex:split3_gemm --launch-count 1 -o $O/sweep_gemm \
   python tools/bench_configs.py 4 > $O/ncu_gemm.log 2>&1; echo "ncu_gemm=$?" >> $O/status.txt
