@@ -243,7 +243,7 @@ void Context::expand_windows(const float* vols, long long vol_stride, int n_vol,
             pairs = vol_pairs.as<float2>();
         }
         if (launch_expand_factored(fx, vols, vol_stride, win_vol.as<int>(), win_shift.as<int>(), nw, coef.as<float>(),
-                                   geo.m_pad, stream, pairs) != 0)
+                                   geo.m_pad, stream, pairs, nw >= 2LL * n_vol) != 0)
             throw std::runtime_error("factored expansion launch failed");
         ++timer.launches;
         ++timer.gemm_launches;

@@ -710,7 +710,7 @@ void launch_pair_volumes(const float* vols, long long vol_stride, int n_vol, int
 
 int launch_expand_factored(const FactoredTables& T, const float* vols, long long vol_stride, const int* win_vol,
                            const int* win_shift, int n_win, float* out, int ldo, cudaStream_t s,
-                           const float2* pairs) {
+                           const float2* pairs, bool same_volume_pairs) {
     if (n_win <= 0) return 0;
     const size_t smem = factored_smem_bytes(T);
     const char* force = std::getenv("BMB_EXPAND_SPLIT");  // tests: the large-basis path at any size
@@ -722,10 +722,11 @@ int launch_expand_factored(const FactoredTables& T, const float* vols, long long
         const char* e = std::getenv("BMB_EXPAND_CDFT");
         return !(e && std::atoi(e) == 0);
     }();
-    static const bool pair_windows = [] {
-        const char* e = std::getenv("BMB_EXPAND_PAIRWIN");
-        return !(e && std::atoi(e) == 0);
-    }();
+    // BMB_EXPAND_PAIRWIN: 0 off, 1 (default) when consecutive windows share volumes,
+    // 2 always (tests: bit-identity of the two kernels); read per launch
+    const char* pw = std::getenv("BMB_EXPAND_PAIRWIN");
+    const int pair_mode = pw ? std::atoi(pw) : 1;
+    const bool pair_windows = pair_mode == 2 || (pair_mode == 1 && same_volume_pairs);
     if (cdft && pair_windows && n_win >= 2 && T.L + 1 == T.np / 2 && T.ntri <= kThreads) {
         if (T.np == 18 && rpt <= 4) return launch_pair<4, 18>(T, vols, vol_stride, win_vol, win_shift, n_win, out, ldo, s, pairs);
         if (T.np == 34 && rpt <= 12) return launch_pair<12, 34>(T, vols, vol_stride, win_vol, win_shift, n_win, out, ldo, s, pairs);

@@ -21,9 +21,12 @@ size_t factored_smem_bytes(const FactoredTables& T);
 // coefficients of windows (volume win_vol[w] shifted by win_shift[3w..3w+2]) into
 // out[w * ldo + row], real-packed FP32 rows; vols: raster (x fastest), vol_stride apart
 // pairs (optional, else nullptr): the volumes in x-paired layout (launch_pair_volumes)
+// same_volume_pairs: consecutive windows mostly come from one volume (the shift
+// search), so the two-window kernel shares their footprints; false for one window
+// per volume, where it would only cost occupancy
 int launch_expand_factored(const FactoredTables& T, const float* vols, long long vol_stride, const int* win_vol,
                            const int* win_shift, int n_win, float* out, int ldo, cudaStream_t s,
-                           const float2* pairs = nullptr);
+                           const float2* pairs = nullptr, bool same_volume_pairs = true);
 // x-paired copy of n_vol volumes for the trilinear gathers of the expansion:
 // pairs[v][z][y][x + 1] = (v[x], v[x + 1]) for x = -1 .. n-1, zero outside the row
 // (n * n * (n + 1) float2 per volume), so one 8-byte load serves both x taps

@@ -80,3 +80,24 @@ def test_expand_pairs_bit_identical(cuda_device, n, L):
         assert _rel_l2(paired[i], ref) < 1e-5
     with pytest.raises(ValueError):
         ctx.set_expand_pairs(3)
+
+
+@pytest.mark.parametrize("n,L", [(32, 8), (64, 16)])
+def test_expand_window_pairs_bit_identical(cuda_device, n, L, monkeypatch):
+    """The two-windows-per-CTA kernel (used for the shift search, where consecutive
+    windows share a particle) gives the same bits as one window per CTA, including
+    an odd window count and pairs that straddle two volumes."""
+    ctx = api.Context(n, L, L * math.pi)
+    spec = bmo.Spec(L, L * math.pi)
+    t = bmo.gaussian_blob_template(n, 20, 13)
+    rng = np.random.default_rng(8)
+    shifts = [(0, 0, 0), (1, 0, 0), (-2, 3, 1), (4, -4, 2), (-1, -1, -1), (3, 2, -3), (0, 2, 0)]
+    vols = np.stack([(t + 0.2 * rng.standard_normal(t.shape)).astype(np.float32) for _ in shifts])
+    monkeypatch.setenv("BMB_EXPAND_PAIRWIN", "0")
+    single = ctx.expand(vols, shifts).cpu().numpy()
+    monkeypatch.setenv("BMB_EXPAND_PAIRWIN", "2")
+    paired = ctx.expand(vols, shifts).cpu().numpy()
+    assert np.array_equal(single, paired)
+    for i, s in enumerate(shifts):
+        ref = bmo.expand(bmo.shift_volume(vols[i].astype(np.float64), s), spec)
+        assert _rel_l2(paired[i], ref) < 1e-5
