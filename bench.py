@@ -459,12 +459,12 @@ def run_product(args):
     roof_eval["per_band"] = per_band
     roof_eval["flops_per_step"] = tot
     roof_eval["eval_ms_per_step"] = eval_ms
-    tr = ROOT / "profiles" / "round2" / "step_traffic_r2.json"
+    tr = ROOT / "profiles" / "round2" / "step_traffic_r2b.json"
     if tr.exists():
         cls = json.loads(tr.read_text())["classes"]["eval"]
         roof_eval["traffic"] = cls["dram_bytes"] * P / 1024.0
         roof_eval["traffic_note"] = ("DRAM bytes (read + write) per step of the evaluation kernels, from "
-                                     "ncu over one config-2 step (profiles/round2/step_traffic_r2.json, "
+                                     "ncu over one config-2 step (profiles/round2/step_traffic_r2b.json, "
                                      "1024 particles, scaled to this batch; cold-cache per launch)")
     dominant = "refine" if refine_ms > gemm_ms else "expand"
     line = {
