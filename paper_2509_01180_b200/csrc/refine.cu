@@ -37,7 +37,14 @@ namespace {
 
 constexpr double kPiD = 3.14159265358979323846;
 
-template <int ML>
+// STEP: shared-memory bank offset (4-byte words mod 32) between consecutive
+// scratch sets.  The slices of a warp look up the same item positions in their
+// own sets, so sets STEP banks apart keep those lookups conflict-free
+// (16 for two 16-lane slices, 8 for four 8-lane slices).
+#ifndef BMB_WS_BANK_PAD
+#define BMB_WS_BANK_PAD 1
+#endif
+template <int ML, int STEP>
 struct WarpScratchT {
     float2 ua[ML + 1];
     float2 ug[ML + 1];
@@ -46,8 +53,11 @@ struct WarpScratchT {
     double res[20];     // reduced (value, grad[3], hess aa ab ag bb bg gg) x (corr, wedge)
     double red[32];     // reduce-scatter staging (first scratch set of a warp)
     double cs_half[8];  // cos, sin of beta/2, beta, alpha, gamma
+    static constexpr int kWords = 4 * (ML + 1) + 2 * (2 * ML + 3) + 2 * (20 + 32 + 8);
+    static constexpr int kPad = BMB_WS_BANK_PAD ? ((STEP - kWords % 32 + 31) % 32) + 1 : 2;
+    float pad[kPad];
 };
-using WarpScratch = WarpScratchT<kMaxL>;
+using WarpScratch = WarpScratchT<kMaxL, 16>;
 
 // single out-of-line copies of the FP64 math-library routines
 __device__ __noinline__ void sincos_d(double x, double* s, double* c) { sincos(x, s, c); }
@@ -1187,7 +1197,7 @@ __global__ void __launch_bounds__(EvalShape<K>::WARPS * 32, BMB_EVAL_MINB(ORDER)
 template <int LANES>
 struct SubShape {
     static constexpr int ML = LANES == 8 ? 8 : kMaxL;  // 8-lane jobs serve L <= 8
-    using WS = WarpScratchT<ML>;
+    using WS = WarpScratchT<ML, LANES == 8 ? 8 : 16>;
 };
 template <int ORDER, bool TRIAL, int LANES>
 __global__ void __launch_bounds__(BMB_HALF_WARPS * 32, BMB_EVAL_MINB(ORDER)) eval_sub_kernel(StageArgs a, const int* list,
