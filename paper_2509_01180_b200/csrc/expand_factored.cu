@@ -213,13 +213,13 @@ __global__ void __launch_bounds__(kThreads, BMB_EXPAND_MINB) expand_factored_ker
                 const bool vz1 = (unsigned)(z0 + 1) < (unsigned)n && (unsigned)(zs0 + 1) < (unsigned)n;
                 float val = 0.0f;
                 if (vp) {  // x-paired layout: one 8-byte load per (y, z) row; vx0 || vx1 => -1 <= xs0 < n
-                    const long long o0 = ((long long)zs0 * n + ys0) * (n + 1) + xs0 + 1;
+                    const int o0 = (zs0 * n + ys0) * (n + 1) + xs0 + 1;  // within one volume: 32-bit
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {
                         const int bb = c & 1, aa = c >> 1;
                         const bool vr = (bb ? vy1 : vy0) && (aa ? vz1 : vz0);
                         const float2 pr = (vr && (vx0 || vx1))
-                                              ? __ldg(vp + o0 + (bb ? n + 1 : 0) + (aa ? (long long)n * (n + 1) : 0))
+                                              ? __ldg(vp + o0 + (bb ? n + 1 : 0) + (aa ? n * (n + 1) : 0))
                                               : make_float2(0.0f, 0.0f);
                         const float v0 = vx0 ? pr.x : 0.0f;
                         const float v1 = vx1 ? pr.y : 0.0f;
@@ -227,12 +227,12 @@ __global__ void __launch_bounds__(kThreads, BMB_EXPAND_MINB) expand_factored_ker
                         val = fmaf(wyz, fmaf(fx, v1 - v0, v0), val);
                     }
                 } else {
-                    const long long o0 = ((long long)zs0 * n + ys0) * n + xs0;
+                    const int o0 = (zs0 * n + ys0) * n + xs0;
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {  // (y, z) rows of the footprint
                         const int bb = c & 1, aa = c >> 1;
                         const bool vr = (bb ? vy1 : vy0) && (aa ? vz1 : vz0);
-                        const float* row = v + o0 + (bb ? n : 0) + (aa ? (long long)n * n : 0);
+                        const float* row = v + o0 + (bb ? n : 0) + (aa ? n * n : 0);
                         const float v0 = (vr && vx0) ? __ldg(row) : 0.0f;
                         const float v1 = (vr && vx1) ? __ldg(row + 1) : 0.0f;
                         const float wyz = (bb ? fy : 1.0f - fy) * (aa ? fz : 1.0f - fz);
@@ -574,13 +574,13 @@ __global__ void __launch_bounds__(kThreads, BMB_EXPAND_PAIR_MINB)
                     const bool vz1 = gz1 && (unsigned)(zs0 + 1) < (unsigned)n;
                     float val = 0.0f;
                     if (vp[q]) {
-                        const long long o0 = ((long long)zs0 * n + ys0) * (n + 1) + xs0 + 1;
+                        const int o0 = (zs0 * n + ys0) * (n + 1) + xs0 + 1;  // within one volume: 32-bit
 #pragma unroll
                         for (int c = 0; c < 4; ++c) {
                             const int bb = c & 1, aa = c >> 1;
                             const bool vr = (bb ? vy1 : vy0) && (aa ? vz1 : vz0);
                             const float2 pr = (vr && (vx0 || vx1))
-                                                  ? __ldg(vp[q] + o0 + (bb ? n + 1 : 0) + (aa ? (long long)n * (n + 1) : 0))
+                                                  ? __ldg(vp[q] + o0 + (bb ? n + 1 : 0) + (aa ? n * (n + 1) : 0))
                                                   : make_float2(0.0f, 0.0f);
                             const float v0 = vx0 ? pr.x : 0.0f;
                             const float v1 = vx1 ? pr.y : 0.0f;
@@ -588,12 +588,12 @@ __global__ void __launch_bounds__(kThreads, BMB_EXPAND_PAIR_MINB)
                             val = fmaf(wyz, fmaf(fx, v1 - v0, v0), val);
                         }
                     } else {
-                        const long long o0 = ((long long)zs0 * n + ys0) * n + xs0;
+                        const int o0 = (zs0 * n + ys0) * n + xs0;
 #pragma unroll
                         for (int c = 0; c < 4; ++c) {
                             const int bb = c & 1, aa = c >> 1;
                             const bool vr = (bb ? vy1 : vy0) && (aa ? vz1 : vz0);
-                            const float* row = v[q] + o0 + (bb ? n : 0) + (aa ? (long long)n * n : 0);
+                            const float* row = v[q] + o0 + (bb ? n : 0) + (aa ? n * n : 0);
                             const float v0 = (vr && vx0) ? __ldg(row) : 0.0f;
                             const float v1 = (vr && vx1) ? __ldg(row + 1) : 0.0f;
                             const float wyz = (bb ? fy : 1.0f - fy) * (aa ? fz : 1.0f - fz);
