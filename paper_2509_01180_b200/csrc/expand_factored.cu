@@ -573,7 +573,16 @@ __global__ void __launch_bounds__(kThreads, BMB_EXPAND_PAIR_MINB)
                     const bool vz0 = gz0 && (unsigned)zs0 < (unsigned)n;
                     const bool vz1 = gz1 && (unsigned)(zs0 + 1) < (unsigned)n;
                     float val = 0.0f;
-                    if (vp[q]) {
+                    const bool inside = vx0 && vx1 && vy0 && vy1 && vz0 && vz1;
+                    if (vp[q] && inside) {  // every tap inside both grids: no masks (same values and order)
+                        const float2* b = vp[q] + ((zs0 * n + ys0) * (n + 1) + xs0 + 1);
+                        const int rowp = n + 1, slab = n * (n + 1);
+                        const float2 p0 = __ldg(b), p1 = __ldg(b + rowp), p2 = __ldg(b + slab), p3 = __ldg(b + slab + rowp);
+                        val = fmaf((1.0f - fy) * (1.0f - fz), fmaf(fx, p0.y - p0.x, p0.x), val);
+                        val = fmaf(fy * (1.0f - fz), fmaf(fx, p1.y - p1.x, p1.x), val);
+                        val = fmaf((1.0f - fy) * fz, fmaf(fx, p2.y - p2.x, p2.x), val);
+                        val = fmaf(fy * fz, fmaf(fx, p3.y - p3.x, p3.x), val);
+                    } else if (vp[q]) {
                         const int o0 = (zs0 * n + ys0) * (n + 1) + xs0 + 1;  // within one volume: 32-bit
 #pragma unroll
                         for (int c = 0; c < 4; ++c) {
