@@ -229,7 +229,7 @@ def config_block(batch):
 
 
 # kernel classes of the CUPTI breakdown (name prefix -> class)
-KCLASS = (("expand_factored", "expand"), ("expand_pair", "expand"), ("expand_theta", "expand"),
+KCLASS = (("expand_factored", "expand"), ("expand_pair", "expand"), ("expand_tc", "expand"), ("expand_quad", "expand"), ("quad_volumes", "expand"), ("expand_theta", "expand"),
           ("expand_radial", "expand"), ("pair_volumes", "expand"), ("split3_gemm", "expand"),
           ("gather_windows", "expand"), ("advance_kernel", "newton"),
           ("eval_kernel<2", "eval_order2"), ("eval_kernel<0", "eval_order0"),

@@ -60,9 +60,11 @@ int bm_context_set_expand_mode(bm_context* ctx, int mode);
  * stream with its own buffers and host thread (default 4 lanes, 64 particles per
  * lane).  Results do not depend on the lane count. */
 int bm_context_set_lanes(bm_context* ctx, int lanes, int min_per_lane);
-/* Expansion gathers of the factored mode: 0 = direct loads, 1 = from an
- * x-paired copy of each volume when it has >= 4 windows (default; the shift
- * search), 2 = always from the copy.  The coefficients are bit-identical. */
+/* Expansion gathers of the factored mode: 0 = direct loads, 1 = from a copy of
+ * each volume when it has >= 4 windows (default; the shift search: the
+ * zero-padded quad copy when every |shift| <= 6, else the x-paired copy),
+ * 2 = always from the x-paired copy, 3 = always from the quad copy when the
+ * shifts allow it.  The coefficients are bit-identical. */
 int bm_context_set_expand_pairs(bm_context* ctx, int mode);
 /* Host-buffer staging: with reuse on, a bm_average_accumulate directly after a
  * completed bm_align_batch of the same host buffer and count uses the device
@@ -90,6 +92,13 @@ int bm_basis_roots(int l_max, double lambda_cut, int l, double* roots, double* n
  * legacy default stream) and later work on `stream` is ordered after it. */
 int bm_expand(bm_context* ctx, const float* vols, int count, const int* shifts, double* out,
               void* stream);
+/* The same for shift windows that share volumes (the shift search of
+ * search_one_shift, src/optimize.cpp:361-419: expand(shift_volume(f, s)) for
+ * many s of one subtomogram): window w reads volume win_vol[w] (host int[n_win],
+ * 0 <= win_vol[w] < n_vol) shifted by win_shift[3w..3w+2] (host); out is
+ * n_win x coeff_count complex128 on the device. */
+int bm_expand_windows(bm_context* ctx, const float* vols, int n_vol, const int* win_vol, const int* win_shift,
+                      int n_win, double* out, void* stream);
 
 /* ------------------------------------------------------------------ alignment
  * Mirrors OptimizerConfig (include/ballmatch/optimize.hpp:15-32); l_max and

@@ -90,6 +90,8 @@ def _declare(L: C.CDLL) -> None:
     L.bm_default_lambda_cut.restype = D
     L.bm_expand.argtypes = [P, P, I, P, P, P]
     L.bm_expand.restype = I
+    L.bm_expand_windows.argtypes = [P, P, I, P, P, I, P, P]
+    L.bm_expand_windows.restype = I
     L.bm_set_template.argtypes = [P, P, D, P]
     L.bm_set_template.restype = I
     L.bm_template_norm.argtypes = [P]

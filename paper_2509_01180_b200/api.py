@@ -188,6 +188,20 @@ class Context:
                                         C.c_void_p(out.data_ptr()), C.c_void_p(stream)), "expand")
         return torch.view_as_complex(out)
 
+    def expand_windows(self, vols, win_vol, shifts):
+        """expand(shift_volume(vols[win_vol[w]], shifts[w])) for every window w (the
+        shift search's expansions: many windows per volume) -> complex128
+        (n_win, coeff_count) on the device."""
+        torch = _torch()
+        v = self._dev(vols)
+        wv = np.ascontiguousarray(np.asarray(win_vol, dtype=np.int32))
+        s = np.ascontiguousarray(np.asarray(shifts, dtype=np.int32).reshape(len(wv), 3))
+        out = torch.empty((len(wv), self.coeff_count, 2), dtype=torch.float64, device=v.device)
+        _lib.check(_lib.lib().bm_expand_windows(self._h, C.c_void_p(v.data_ptr()), v.shape[0],
+                                                wv.ctypes.data_as(C.c_void_p), s.ctypes.data_as(C.c_void_p), len(wv),
+                                                C.c_void_p(out.data_ptr()), self._stream(v)), "expand_windows")
+        return torch.view_as_complex(out)
+
     # ------------------------------------------------------------------ align
     def _dev(self, vols):
         torch = _torch()
@@ -469,8 +483,9 @@ class Context:
         self._refresh_info()
 
     def set_expand_pairs(self, mode: int):
-        """Expansion gathers: 0 direct, 1 x-paired copy when a volume has >= 4 windows
-        (default), 2 always from the copy.  Coefficients are bit-identical."""
+        """Expansion gathers: 0 direct, 1 from a copy when a volume has >= 4 windows
+        (default: zero-padded quad copy for |shift| <= 6, else x-paired copy), 2 always
+        x-paired copy, 3 always quad copy.  Coefficients are bit-identical."""
         _lib.check(_lib.lib().bm_context_set_expand_pairs(self._h, int(mode)), "set_expand_pairs")
 
     def set_stage_reuse(self, on: bool):

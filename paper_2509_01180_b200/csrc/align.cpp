@@ -909,8 +909,8 @@ void Context::align_group(const float* fw, int n_vol, const std::vector<int>& pa
     // the coarse and fine passes read the same volumes: one x-paired copy serves both
     struct PairHold {
         Context& c;
-        explicit PairHold(Context& x) : c(x) { c.pairs_hold_ = true; c.pairs_src_ = nullptr; }
-        ~PairHold() { c.pairs_hold_ = false; c.pairs_src_ = nullptr; }
+        explicit PairHold(Context& x) : c(x) { c.pairs_hold_ = true; c.pairs_src_ = nullptr; c.quads_src_ = nullptr; }
+        ~PairHold() { c.pairs_hold_ = c.quads_hold_ = false; c.pairs_src_ = c.quads_src_ = nullptr; }
     } hold(*this);
     const auto t_coarse = std::chrono::steady_clock::now();
     std::vector<WindowOutcome> oc = run_windows(fw, n_vol, wv, ws, cfg);

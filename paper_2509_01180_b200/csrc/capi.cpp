@@ -195,6 +195,26 @@ int bm_expand(bm_context* ctx, const float* vols, int count, const int* shifts, 
 }
 
 
+int bm_expand_windows(bm_context* ctx, const float* vols, int n_vol, const int* win_vol, const int* win_shift,
+                      int n_win, double* out, void* stream) {
+    return guarded("bm_expand_windows", [&] {
+        if (!ctx) return (int)BM_ERR_STATE;
+        if (n_vol < 0 || n_win < 0 || (n_win > 0 && (!vols || !out || !win_vol || !win_shift)))
+            throw std::invalid_argument("bad buffers");
+        for (int i = 0; i < n_win; ++i)
+            if (win_vol[i] < 0 || win_vol[i] >= n_vol) throw std::invalid_argument("window volume index out of range");
+        auto& c = *ctx->impl;
+        cudaSetDevice(c.device);
+        const std::vector<int> wv(win_vol, win_vol + n_win), ws(win_shift, win_shift + 3 * (size_t)n_win);
+        StreamJoin join(ctx, stream);
+        const long long stride = (long long)c.n * c.n * c.n;
+        c.expand_windows(vols, stride, n_vol, wv, ws);
+        bmb::launch_to_complex(c.coef.as<float>(), n_win, c.geo.m_pad, c.geo, out, c.stream);
+        if (cudaGetLastError() != cudaSuccess) throw std::runtime_error("kernel launch failed");
+        return (int)BM_OK;
+    });
+}
+
 static bmb::AlignConfig cfg_of(const bm_align_config* c) {
     if (!c) throw std::invalid_argument("null config");
     if (c->n_bands < 0 || c->n_bands > 16) throw std::invalid_argument("config: at most 16 bands");
@@ -687,7 +707,7 @@ int bm_context_set_expand_mode(bm_context* ctx, int mode) {
 int bm_context_set_expand_pairs(bm_context* ctx, int mode) {
     return guarded("bm_context_set_expand_pairs", [&] {
         if (!ctx) return (int)BM_ERR_STATE;
-        if (mode < 0 || mode > 2) throw std::invalid_argument("expand pairs mode must be 0, 1 or 2");
+        if (mode < 0 || mode > 3) throw std::invalid_argument("expand pairs mode must be 0, 1, 2 or 3");
         ctx->impl->pairs_mode = mode;
         return (int)BM_OK;
     });

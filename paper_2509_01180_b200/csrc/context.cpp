@@ -135,6 +135,8 @@ void Context::build_factored_tables() {
             const float fx = (float)(gx - (double)x0), fy = (float)(gy - (double)y0), fz = (float)(gz - (double)z0);
             int4 e;
             e.x = (x0 & 1023) | ((y0 & 1023) << 10) | ((z0 & 1023) << 20);
+            // bit 30: the footprint leaves the window grid (0 <= g, so only on the high side)
+            if (x0 + 1 >= n || y0 + 1 >= n || z0 + 1 >= n) e.x |= 1 << 30;
             std::memcpy(&e.y, &fx, 4);
             std::memcpy(&e.z, &fy, 4);
             std::memcpy(&e.w, &fz, 4);
@@ -229,6 +231,56 @@ void Context::expand_windows(const float* vols, long long vol_stride, int n_vol,
         const float2* pairs = nullptr;
         const size_t pair_bytes = sizeof(float2) * (size_t)pair_volume_elems(n) * n_vol;
         const bool want = pairs_mode == 2 || (pairs_mode == 1 && nw >= 4 * (long long)n_vol);
+        // pairs_mode 1 (when a volume has >= 4 windows) or 3 (always, tests): the
+        // zero-padded quad copy and the pair-list kernel (K2q) when every shift fits
+        // the padding and the basis has a specialised kernel
+        if (pairs_mode == 3 || want) {
+            static const bool quad_on = [] {
+                const char* e = std::getenv("BMB_EXPAND_QUAD");
+                return !(e && std::atoi(e) == 0);
+            }();
+            int smax = 0;
+            for (int v : wshift) smax = std::max(smax, std::abs(v));
+            const size_t quad_bytes = sizeof(float4) * (size_t)quad_volume_elems(n) * n_vol;
+            if ((quad_on || pairs_mode == 3) && pairs_mode != 2 && smax <= kQuadPad && quad_bytes <= kMaxPairBytes) {
+                // pair list: x-neighbours (same volume, y and z shift; x apart by 1 or 2) share their loads
+                std::vector<int4> pl;
+                std::vector<int> singles;
+                for (int i = 0; i < nw;) {
+                    const int dx = i + 1 < nw ? wshift[3 * i + 3] - wshift[3 * i] : 0;
+                    if (i + 1 < nw && wvol[i] == wvol[i + 1] && wshift[3 * i + 1] == wshift[3 * i + 4] &&
+                        wshift[3 * i + 2] == wshift[3 * i + 5] && (dx == 1 || dx == 2)) {
+                        pl.push_back(make_int4(i, i + 1, dx, 0));
+                        i += 2;
+                    } else {
+                        singles.push_back(i++);
+                    }
+                }
+                for (size_t k = 0; k < singles.size(); k += 2)
+                    pl.push_back(make_int4(singles[k], k + 1 < singles.size() ? singles[k + 1] : singles[k], 0, 0));
+                const bool have = quads_hold_ && quads_src_ == vols && quads_nvol_ == n_vol && quads_stride_ == vol_stride;
+                if (!have) {
+                    vol_quads.reserve(quad_bytes);
+                    launch_quad_volumes(vols, vol_stride, n_vol, n, vol_quads.as<float4>(), stream);
+                    ++timer.launches;
+                    quads_src_ = pairs_hold_ ? vols : nullptr;
+                    quads_hold_ = pairs_hold_;
+                    quads_nvol_ = n_vol;
+                    quads_stride_ = vol_stride;
+                }
+                upload(win_pairs, pl, stream);
+                const int rc = launch_expand_quads(fx, vol_quads.as<float4>(), win_vol.as<int>(), win_shift.as<int>(),
+                                                   win_pairs.as<int4>(), (int)pl.size(), coef.as<float>(), geo.m_pad, stream);
+                if (rc == 0) {
+                    ++timer.launches;
+                    ++timer.gemm_launches;
+                    timer.windows_expanded += nw;
+                    timer.end(K_GEMM, f0, stream);
+                    return;
+                }
+                if (rc != 1) throw std::runtime_error("quad expansion launch failed");
+            }
+        }
         if (want && pair_bytes <= kMaxPairBytes) {
             // inside one align_group the coarse and fine passes share the copy
             const bool have = pairs_hold_ && pairs_src_ == vols && pairs_nvol_ == n_vol && pairs_stride_ == vol_stride;

@@ -185,7 +185,13 @@ public:
     // work buffers
     DevBuf B_hi, B_lo, col_scale, coef, win_vol, win_shift, vol_scale, norms;
     DevBuf vol_pairs;  // x-paired particle volumes for the expansion gathers (many windows per volume)
-    int pairs_mode = 1;                 // 0 off, 1 auto (>= 4 windows per volume), 2 always
+    DevBuf vol_quads;  // zero-padded quad copy (kernel K2q) and its CTA pair list
+    DevBuf win_pairs;
+    bool quads_hold_ = false;
+    const float* quads_src_ = nullptr;
+    int quads_nvol_ = 0;
+    long long quads_stride_ = 0;
+    int pairs_mode = 1;                 // 0 off, 1 auto (>= 4 windows per volume), 2 always x-pairs, 3 always quads
     static constexpr size_t kMaxPairBytes = size_t(8) << 30;  // larger batches gather directly
     bool pairs_hold_ = false;           // inside align_group: vol_pairs may be reused for pairs_src_
     const float* pairs_src_ = nullptr;

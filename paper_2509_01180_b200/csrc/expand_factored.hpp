@@ -33,4 +33,18 @@ int launch_expand_factored(const FactoredTables& T, const float* vols, long long
 constexpr long long pair_volume_elems(int n) { return (long long)n * n * (n + 1); }
 void launch_pair_volumes(const float* vols, long long vol_stride, int n_vol, int n, float2* pairs, cudaStream_t s);
 
+// zero-padded quad copy for the shift search (kernel K2q):
+// quads[v][z + M][y + M][x + M] = (v[x], v[x+1], v[x+2], v[x+3]), zero outside the
+// grid, M = kQuadPad, (n + 2M)^3 float4 per volume.  Valid for |shift| <= kQuadPad.
+constexpr int kQuadPad = 6;
+constexpr long long quad_volume_elems(int n) { return (long long)(n + 2 * kQuadPad) * (n + 2 * kQuadPad) * (n + 2 * kQuadPad); }
+void launch_quad_volumes(const float* vols, long long vol_stride, int n_vol, int n, float4* quads, cudaStream_t s);
+// one CTA per pair_list entry (window a, window b, mode, 0): mode 1 / 2 = windows of
+// one volume whose shifts differ by that much in x only (one 16-byte load per
+// footprint row serves both), mode 0 = any two windows; b == a for a single window.
+// The footprint table must flag entries that leave the window grid in bit 30.
+// Returns 1 when the basis has no specialised kernel (the caller falls back).
+int launch_expand_quads(const FactoredTables& T, const float4* quads, const int* win_vol, const int* win_shift,
+                        const int4* pair_list, int n_pairs, float* out, int ldo, cudaStream_t s);
+
 }  // namespace bmb

@@ -79,7 +79,45 @@ def test_expand_pairs_bit_identical(cuda_device, n, L):
         ref = bmo.expand(bmo.shift_volume(vols[i].astype(np.float64), s), spec)
         assert _rel_l2(paired[i], ref) < 1e-5
     with pytest.raises(ValueError):
-        ctx.set_expand_pairs(3)
+        ctx.set_expand_pairs(4)
+
+
+@pytest.mark.parametrize("n,L", [(32, 8), (64, 16), (48, 16)])
+def test_expand_quads_bit_identical(cuda_device, n, L):
+    """The pair-list kernel on the zero-padded quad copy (x-neighbour windows share
+    one 16-byte load per footprint row) gives the same bits as direct loads: x
+    pairs 1 and 2 apart, unrelated pairs, an odd count, the largest shifts the
+    padding allows, and a shift beyond it (falls back to the x-paired copy)."""
+    ctx = api.Context(n, L, L * math.pi)
+    spec = bmo.Spec(L, L * math.pi)
+    t = bmo.gaussian_blob_template(n, 20, 21)
+    rng = np.random.default_rng(3)
+    base = [(t + 0.2 * rng.standard_normal(t.shape)).astype(np.float32) for _ in range(3)]
+    shifts = [(-4, 0, 2), (-2, 0, 2), (0, 0, 2), (1, 0, 2), (3, -1, -1), (5, -1, -1), (6, 6, -6), (-6, -6, 6),
+              (0, 0, 0), (0, 0, 0), (2, 1, 0)]
+    which = [0, 0, 0, 0, 1, 1, 1, 1, 2, 0, 2]
+    vols = np.stack(base)
+    ctx.set_expand_pairs(0)
+    direct = ctx.expand_windows(vols, which, shifts).cpu().numpy()
+    ctx.set_expand_pairs(3)
+    quad = ctx.expand_windows(vols, which, shifts).cpu().numpy()
+    assert np.array_equal(direct, quad)
+    for i in (0, 3, 6, 7):
+        ref = bmo.expand(bmo.shift_volume(base[which[i]].astype(np.float64), shifts[i]), spec)
+        assert _rel_l2(quad[i], ref) < 1e-5
+    far = shifts[:-1] + [(7, 0, 0)]
+    ctx.set_expand_pairs(0)
+    d2 = ctx.expand_windows(vols, which, far).cpu().numpy()
+    ctx.set_expand_pairs(3)
+    q2 = ctx.expand_windows(vols, which, far).cpu().numpy()
+    assert np.array_equal(d2, q2)
+    # a whole coarse shift grid of one volume (the alignment's lists: x fastest)
+    grid = [(x, y, z) for z in (-4, -2, 0, 2, 4) for y in (-4, -2, 0, 2, 4) for x in (-4, -2, 0, 2, 4)]
+    ctx.set_expand_pairs(0)
+    d3 = ctx.expand_windows(vols[:1], [0] * len(grid), grid).cpu().numpy()
+    ctx.set_expand_pairs(1)
+    q3 = ctx.expand_windows(vols[:1], [0] * len(grid), grid).cpu().numpy()
+    assert np.array_equal(d3, q3)
 
 
 @pytest.mark.parametrize("n,L", [(32, 8), (64, 16)])
@@ -93,6 +131,7 @@ def test_expand_window_pairs_bit_identical(cuda_device, n, L, monkeypatch):
     rng = np.random.default_rng(8)
     shifts = [(0, 0, 0), (1, 0, 0), (-2, 3, 1), (4, -4, 2), (-1, -1, -1), (3, 2, -3), (0, 2, 0)]
     vols = np.stack([(t + 0.2 * rng.standard_normal(t.shape)).astype(np.float32) for _ in shifts])
+    monkeypatch.setenv("BMB_EXPAND_TC", "0")
     monkeypatch.setenv("BMB_EXPAND_PAIRWIN", "0")
     single = ctx.expand(vols, shifts).cpu().numpy()
     monkeypatch.setenv("BMB_EXPAND_PAIRWIN", "2")
@@ -101,3 +140,31 @@ def test_expand_window_pairs_bit_identical(cuda_device, n, L, monkeypatch):
     for i, s in enumerate(shifts):
         ref = bmo.expand(bmo.shift_volume(vols[i].astype(np.float64), s), spec)
         assert _rel_l2(paired[i], ref) < 1e-5
+
+
+@pytest.mark.parametrize("pairs", [0, 2])
+@pytest.mark.parametrize("n,L", [(32, 8), (64, 16), (48, 16)])
+def test_expand_tensor_dft_matches(cuda_device, n, L, pairs, monkeypatch):
+    """The two-window kernel with its phi-DFT on the tensor cores (tcgen05 kind::tf32,
+    3xTF32 split, FP32 side samples) against the FP32-pipe kernel and the oracle:
+    same samples, so only the DFT's rounding differs (bar here 2e-6 relative L2
+    between the two device paths; 1e-5 against the oracle as everywhere)."""
+    ctx = api.Context(n, L, L * math.pi)
+    spec = bmo.Spec(L, L * math.pi)
+    t = bmo.gaussian_blob_template(n, 20, 17)
+    rng = np.random.default_rng(9)
+    shifts = [(0, 0, 0), (1, 0, 0), (-2, 3, 1), (4, -4, 2), (-1, -1, -1), (3, 2, -3), (0, 2, 0)]
+    vols = np.stack([(t + 0.2 * rng.standard_normal(t.shape)).astype(np.float32) for _ in shifts])
+    ctx.set_expand_pairs(pairs)
+    monkeypatch.setenv("BMB_EXPAND_PAIRWIN", "2")
+    monkeypatch.setenv("BMB_EXPAND_TC", "0")
+    simt = ctx.expand(vols, shifts).cpu().numpy()
+    monkeypatch.setenv("BMB_EXPAND_TC", "1")
+    tc = ctx.expand(vols, shifts).cpu().numpy()
+    assert not np.array_equal(simt, tc)  # the tensor path really ran
+    for i, s in enumerate(shifts):
+        assert _rel_l2(tc[i], simt[i]) < 2e-6
+        ref = bmo.expand(bmo.shift_volume(vols[i].astype(np.float64), s), spec)
+        assert _rel_l2(tc[i], ref) < 1e-5
+    many = ctx.expand(np.concatenate([vols] * 40), shifts * 40).cpu().numpy()
+    assert np.array_equal(many[:7], tc) and np.array_equal(many[-7:], tc)  # deterministic across CTAs

@@ -7,7 +7,7 @@ from collections import defaultdict
 
 CLASSES = (("eval_kernel<2", "eval_order2"), ("eval_kernel<0", "eval_order0"),
            ("eval_sub_kernel<2", "eval_order2"), ("eval_sub_kernel<0", "eval_order0"), ("expand_factored", "expand"),
-           ("expand_pair", "expand"), ("advance_kernel", "newton"), ("step_kernel", "newton"),
+           ("expand_pair", "expand"), ("expand_tc", "expand"), ("expand_quad", "expand"), ("quad_volumes", "expand"), ("advance_kernel", "newton"), ("step_kernel", "newton"),
            ("build_xi", "xi_build"), ("seed_kernel", "seed"))
 
 
