@@ -242,7 +242,8 @@ void Context::expand_windows(const float* vols, long long vol_stride, int n_vol,
             int smax = 0;
             for (int v : wshift) smax = std::max(smax, std::abs(v));
             const size_t quad_bytes = sizeof(float4) * (size_t)quad_volume_elems(n) * n_vol;
-            if ((quad_on || pairs_mode == 3) && pairs_mode != 2 && smax <= kQuadPad && quad_bytes <= kMaxPairBytes) {
+            if ((quad_on || pairs_mode == 3) && pairs_mode != 2 && smax <= kQuadPad && quad_bytes <= kMaxPairBytes &&
+                expand_quads_supported(fx)) {
                 // pair list: x-neighbours (same volume, y and z shift; x apart by 1 or 2) share their loads
                 std::vector<int4> pl;
                 std::vector<int> singles;

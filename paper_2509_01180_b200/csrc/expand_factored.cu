@@ -1074,12 +1074,14 @@ __global__ void __launch_bounds__(kThreads, BMB_EXPAND_PAIR_MINB)
         const int w = q ? wb : wa;
         cb[q] = ((win_shift[3 * w + 2] + kQuadPad) * ROW + win_shift[3 * w + 1] + kQuadPad) * ROW + win_shift[3 * w] + kQuadPad;
     }
+    // the row map of the radial stage: in registers while the accumulators leave room
+    constexpr bool RP_REG = RPT <= 12;
     float acc[2][RPT];
-    int rpr[RPT];
+    int rpr[RP_REG ? RPT : 1];
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
         acc[0][q] = acc[1][q] = 0.0f;
-        rpr[q] = tid + q * kThreads < T.coeffs ? T.rowpack[tid + q * kThreads] : 0;
+        if constexpr (RP_REG) rpr[q] = tid + q * kThreads < T.coeffs ? T.rowpack[tid + q * kThreads] : 0;
     }
     float th_w[NPC / 2];
     int th_m = 0, th_base = 0;
@@ -1214,7 +1216,9 @@ __global__ void __launch_bounds__(kThreads, BMB_EXPAND_PAIR_MINB)
         for (int qq = 0; qq < RPT; ++qq) {  // 4. radial
             const int row = tid + qq * kThreads;
             if (row < T.coeffs) {
-                const int rp = rpr[qq];
+                int rp;
+                if constexpr (RP_REG) rp = rpr[qq];
+                else rp = __ldg(T.rowpack + row);
                 const float rv = rad[rp >> 16];
                 acc[0][qq] = fmaf(rv, Gp[rp & 0xffff], acc[0][qq]);
                 acc[1][qq] = fmaf(rv, Gp[nl * nl + (rp & 0xffff)], acc[1][qq]);
@@ -1308,14 +1312,19 @@ void launch_quad_volumes(const float* vols, long long vol_stride, int n_vol, int
     quad_volumes_kernel<<<(int)blocks, 256, 0, s>>>(vols, vol_stride, n, total, quads);
 }
 
+bool expand_quads_supported(const FactoredTables& T) {
+    const int rpt = (T.coeffs + kThreads - 1) / kThreads;
+    if (!(T.L + 1 == T.np / 2 && T.nt == T.np && T.ntri <= kThreads)) return false;
+    return (T.np == 18 && rpt <= 4) || (T.np == 34 && rpt <= 12) || (T.np == 42 && rpt <= 24);
+}
+
 int launch_expand_quads(const FactoredTables& T, const float4* quads, const int* win_vol, const int* win_shift,
                         const int4* pair_list, int n_pairs, float* out, int ldo, cudaStream_t s) {
     if (n_pairs <= 0) return 0;
-    const int rpt = (T.coeffs + kThreads - 1) / kThreads;
-    if (!(T.L + 1 == T.np / 2 && T.ntri <= kThreads)) return 1;
-    if (T.np == 18 && rpt <= 4) return launch_quad<4, 18>(T, quads, win_vol, win_shift, pair_list, n_pairs, out, ldo, s);
-    if (T.np == 34 && rpt <= 12) return launch_quad<12, 34>(T, quads, win_vol, win_shift, pair_list, n_pairs, out, ldo, s);
-    return 1;
+    if (!expand_quads_supported(T)) return 1;
+    if (T.np == 18) return launch_quad<4, 18>(T, quads, win_vol, win_shift, pair_list, n_pairs, out, ldo, s);
+    if (T.np == 34) return launch_quad<12, 34>(T, quads, win_vol, win_shift, pair_list, n_pairs, out, ldo, s);
+    return launch_quad<24, 42>(T, quads, win_vol, win_shift, pair_list, n_pairs, out, ldo, s);
 }
 
 void launch_pair_volumes(const float* vols, long long vol_stride, int n_vol, int n, float2* pairs, cudaStream_t s) {

@@ -43,7 +43,9 @@ void launch_quad_volumes(const float* vols, long long vol_stride, int n_vol, int
 // one volume whose shifts differ by that much in x only (one 16-byte load per
 // footprint row serves both), mode 0 = any two windows; b == a for a single window.
 // The footprint table must flag entries that leave the window grid in bit 30.
-// Returns 1 when the basis has no specialised kernel (the caller falls back).
+// Returns 1 when the basis has no specialised kernel (the caller falls back;
+// expand_quads_supported tells beforehand).
+bool expand_quads_supported(const FactoredTables& T);
 int launch_expand_quads(const FactoredTables& T, const float4* quads, const int* win_vol, const int* win_shift,
                         const int4* pair_list, int n_pairs, float* out, int ldo, cudaStream_t s);
 

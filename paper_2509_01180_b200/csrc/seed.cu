@@ -17,16 +17,28 @@ namespace bmb {
 struct SeedSmem {
     size_t region0, xi, sc, maxima, bk, cands, total;
     bool xi_in_smem;
+    int sb;  // beta slices collapsed per batch (A_j and b[k][m] of sb slices live at once)
 };
-__host__ __device__ inline SeedSmem seed_smem_plan(int rows_low, int L, int nxi, int npt) {
+__host__ __device__ inline SeedSmem seed_smem_plan(int rows_low, int L, int nxi, int npt, int nb, int ng) {
     const int wd = 2 * L + 1;
     SeedSmem p;
     const size_t ft = sizeof(double) * 2 * (size_t)rows_low;
     const size_t aj = sizeof(double2) * (size_t)wd * wd;
-    p.region0 = (ft > aj ? ft : aj + 0);
-    p.region0 = (p.region0 + 15) / 16 * 16;
     const size_t xib = sizeof(double2) * (size_t)nxi;
-    const size_t bkb = sizeof(double2) * (size_t)wd * 64;  // b[k][m] for up to 64 gamma points
+    const size_t fixed = sizeof(double) * npt + 2 * sizeof(int) * (size_t)npt + 64;
+    // as many slices per batch as keep the CTA near 64 KB (three CTAs per SM): the
+    // three phases of a batch then run on sb times the threads between barriers
+    p.sb = 1;
+    for (int sb = nb; sb > 1; --sb) {
+        const size_t r0 = ft > aj * sb ? ft : aj * sb;
+        if (r0 + xib + fixed + sizeof(double2) * (size_t)wd * ng * sb <= 72 * 1024) {
+            p.sb = sb;
+            break;
+        }
+    }
+    p.region0 = ft > aj * p.sb ? ft : aj * p.sb;
+    p.region0 = (p.region0 + 15) / 16 * 16;
+    const size_t bkb = sizeof(double2) * (size_t)wd * ng * p.sb;  // b[j][k][m] of one batch
     const bool cands_extra = sizeof(int) * (size_t)npt > bkb;
     const size_t rest = sizeof(double) * npt + sizeof(int) * npt + bkb + (cands_extra ? sizeof(int) * npt : 0);
     p.xi_in_smem = p.region0 + xib + rest <= 200 * 1024;
@@ -51,7 +63,7 @@ __global__ void __launch_bounds__(256) seed_kernel(SeedArgs a) {
     const int L = a.L_low, wd = 2 * L + 1;
     const int npt = a.na * a.nb * a.ng;
     const int nrow = a.rows_low;  // real-packed rows of degrees <= L
-    const SeedSmem plan = seed_smem_plan(nrow, L, a.nxi, npt);
+    const SeedSmem plan = seed_smem_plan(nrow, L, a.nxi, npt, a.nb, a.ng);
     double* f = reinterpret_cast<double*>(sm);
     double* t = f + nrow;
     double2* Aj = reinterpret_cast<double2*>(sm);  // overlays f, t once xi is built
@@ -102,39 +114,47 @@ __global__ void __launch_bounds__(256) seed_kernel(SeedArgs a) {
     __syncthreads();
 
     // per beta slice j: A_j[m][m'] = sum_l xi_l[m,m'] d^l_{m,m'}(beta_j), then
-    // score(i,j,k) = Re sum_m ua_i[m] sum_m' A_j[m][m'] ug_k[m']
-    for (int j = 0; j < a.nb; ++j) {
-        for (int e = threadIdx.x; e < wd * wd; e += blockDim.x) {
+    // score(i,j,k) = Re sum_m ua_i[m] sum_m' A_j[m][m'] ug_k[m'].  plan.sb slices go
+    // through each phase together (three barriers per batch instead of per slice);
+    // every output keeps its own summation order.
+    const int wd2 = wd * wd, gw = a.ng * wd, ag = a.na * a.ng;
+    for (int j0 = 0; j0 < a.nb; j0 += plan.sb) {
+        const int nj = min(plan.sb, a.nb - j0);
+        for (int q = threadIdx.x; q < nj * wd2; q += blockDim.x) {
+            const int dj = q / wd2, e = q - dj * wd2;
             const int m = e / wd - L, mp = e % wd - L;
             double re = 0.0, im = 0.0;
             for (int l = max(abs(m), abs(mp)); l <= L; ++l) {
                 const int o = l * (2 * l - 1) * (2 * l + 1) / 3 + (m + l) * (2 * l + 1) + (mp + l);
-                const double d = a.dgrid[(size_t)j * a.nxi + o];
+                const double d = a.dgrid[(size_t)(j0 + dj) * a.nxi + o];
                 re += xi[o].x * d;
                 im += xi[o].y * d;
             }
-            Aj[e] = make_double2(re, im);
+            Aj[q] = make_double2(re, im);
         }
         __syncthreads();
         // b[k][m] = sum_m' A_j[m][m'] ug_k[m'], then score = Re sum_m ua_i[m] b[k][m]
         // (the reference's collapse and sweep order, optimize.cpp:79-93)
-        for (int q = threadIdx.x; q < a.ng * wd; q += blockDim.x) {
-            const int k = q / wd, m = q % wd;
+        for (int q = threadIdx.x; q < nj * gw; q += blockDim.x) {
+            const int dj = q / gw, r = q - dj * gw;
+            const int k = r / wd, m = r % wd;
             const double2* pg = a.ug + (size_t)k * wd;
+            const double2* Ar = Aj + dj * wd2 + m * wd;
             double bre = 0.0, bim = 0.0;
             for (int mp = 0; mp < wd; ++mp) {
-                const double2 x = Aj[m * wd + mp], y = pg[mp];
+                const double2 x = Ar[mp], y = pg[mp];
                 bre += x.x * y.x - x.y * y.y;
                 bim += x.x * y.y + x.y * y.x;
             }
             Bk[q] = make_double2(bre, bim);
         }
         __syncthreads();
-        for (int q = threadIdx.x; q < a.na * a.ng; q += blockDim.x) {
-            const int k = q % a.ng, i = q / a.ng;
-            const int idx = (j * a.na + i) * a.ng + k;
+        for (int q = threadIdx.x; q < nj * ag; q += blockDim.x) {
+            const int dj = q / ag, r = q - dj * ag;
+            const int k = r % a.ng, i = r / a.ng;
+            const int idx = ((j0 + dj) * a.na + i) * a.ng + k;
             const double2* pa = a.ua + (size_t)i * wd;
-            const double2* bk = Bk + (size_t)k * wd;
+            const double2* bk = Bk + (size_t)dj * gw + (size_t)k * wd;
             double acc = 0.0;
             for (int m = 0; m < wd; ++m) acc += pa[m].x * bk[m].x - pa[m].y * bk[m].y;
             if (a.wedge_sqrt) acc /= a.wedge_sqrt[idx];
@@ -239,15 +259,14 @@ __global__ void __launch_bounds__(256) seed_kernel(SeedArgs a) {
 }
 
 size_t seed_smem_bytes(const SeedArgs& a) {
-    return seed_smem_plan(a.rows_low, a.L_low, a.nxi, a.na * a.nb * a.ng).total;
+    return seed_smem_plan(a.rows_low, a.L_low, a.nxi, a.na * a.nb * a.ng, a.nb, a.ng).total;
 }
 bool seed_needs_scratch(const SeedArgs& a) {
-    return !seed_smem_plan(a.rows_low, a.L_low, a.nxi, a.na * a.nb * a.ng).xi_in_smem;
+    return !seed_smem_plan(a.rows_low, a.L_low, a.nxi, a.na * a.nb * a.ng, a.nb, a.ng).xi_in_smem;
 }
 
 int launch_seed(const SeedArgs& a, int n_win, cudaStream_t s) {
     if (n_win <= 0) return 0;
-    if (a.ng > 64) return 1;  // b[k][m] staging holds up to 64 gamma points
     const size_t smem = seed_smem_bytes(a);
     if (smem > 200 * 1024) return 1;
     if (ensure_dynamic_smem(seed_kernel, (int)smem) != cudaSuccess) return 2;

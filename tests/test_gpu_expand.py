@@ -82,7 +82,7 @@ def test_expand_pairs_bit_identical(cuda_device, n, L):
         ctx.set_expand_pairs(4)
 
 
-@pytest.mark.parametrize("n,L", [(32, 8), (64, 16), (48, 16)])
+@pytest.mark.parametrize("n,L", [(32, 8), (64, 16), (48, 16), (64, 20)])
 def test_expand_quads_bit_identical(cuda_device, n, L):
     """The pair-list kernel on the zero-padded quad copy (x-neighbour windows share
     one 16-byte load per footprint row) gives the same bits as direct loads: x

@@ -18,11 +18,19 @@ from paper_2509_01180_b200 import api
 def main():
     P = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
     lanes = int(sys.argv[2]) if len(sys.argv) > 2 else 3
-    ctx = api.Context(64, 16, 16 * math.pi)
-    tmpl = api.make_template(64, 40, 7)
-    ctx.set_template(tmpl, 60.0)
-    parts, q, sh = api.make_particles(tmpl, P, 1000, 3, 0.1, 60.0)
-    cfg = api.make_config(bands=(4, 8, 16), max_candidates=24, shift_radius=4, shift_step=2)
+    import os
+    if os.environ.get("CONFIG") == "5":  # BASELINE config 5: L = 20, bands 4-8-16-20, shifts +-4, SNR 0.05
+        ctx = api.Context(64, 20, 20 * math.pi)
+        tmpl = api.make_template(64, 60, 20250905)
+        ctx.set_template(tmpl, 60.0)
+        parts, q, sh = api.make_particles(tmpl, P, 5000, 4, 0.05, 60.0)
+        cfg = api.make_config(bands=(4, 8, 16, 20), max_candidates=24, shift_radius=4, shift_step=2)
+    else:
+        ctx = api.Context(64, 16, 16 * math.pi)
+        tmpl = api.make_template(64, 40, 7)
+        ctx.set_template(tmpl, 60.0)
+        parts, q, sh = api.make_particles(tmpl, P, 1000, 3, 0.1, 60.0)
+        cfg = api.make_config(bands=(4, 8, 16), max_candidates=24, shift_radius=4, shift_step=2)
     ctx.set_lanes(lanes, 64)
     ctx.align_batch(parts, cfg)
     torch.cuda.synchronize()
