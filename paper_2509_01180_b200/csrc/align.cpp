@@ -303,6 +303,7 @@ void Context::refine_windows(int nw, int maxc, const AlignConfig& cfg, const Qua
             xa.n = cnt;
             xa.out = xi_win_.as<float4>();
             xa.nf = L < basis.l_max ? basis.block_off[L + 1] : geo.coeffs;
+            for (int l = 0; l <= L; ++l) xa.npairs += basis.radial_count(l) * (l + 1);
             cudaEvent_t r0 = timer.begin(stream);
             cudaEvent_t rb = timer.begin(stream);
             timer.band = (int)bi;

@@ -1635,47 +1635,104 @@ __device__ __forceinline__ void xi_value2(int l, int m, int mp, const float* f, 
     xu = make_float2(sg * fmaf(cm * cp, uii, urr), sg * (cp * uri - cm * uir));
 }
 
-// window and side kernels of one coefficient set per CTA (f, t and the side
-// template staged in shared memory), written to out and out2
-// (STAGED false: large bases read f and the templates from global memory)
+// the same on staged complex pairs: fp[pair] = (Re, Im) of f and tu[pair] = (Re t,
+// Im t, Re u, Im u), a row (l, k) holding its l + 1 orders (order 0 with a zero
+// imaginary part), so one 8-byte and one 16-byte load feed the eight FMAs of a k
+// step.  Same products and order as xi_value2.
+__device__ __forceinline__ void xi_value2s(int l, int m, int mp, const float2* fp, const float4* tu, int nk,
+                                           float2& xt, float2& xu) {
+    const int am = abs(m), amp = abs(mp), st = l + 1;
+    const float2* pf = fp + am;
+    const float4* pt = tu + amp;
+    float rr = 0.f, ii = 0.f, ri = 0.f, ir = 0.f, urr = 0.f, uii = 0.f, uri = 0.f, uir = 0.f;
+#pragma unroll 4
+    for (int k = 0; k < nk; ++k) {
+        const float2 fv = pf[k * st];
+        const float4 tv = pt[k * st];
+        rr = fmaf(fv.x, tv.x, rr);
+        ii = fmaf(fv.y, tv.y, ii);
+        ri = fmaf(fv.x, tv.y, ri);
+        ir = fmaf(fv.y, tv.x, ir);
+        urr = fmaf(fv.x, tv.z, urr);
+        uii = fmaf(fv.y, tv.w, uii);
+        uri = fmaf(fv.x, tv.w, uri);
+        uir = fmaf(fv.y, tv.z, uir);
+    }
+    const float sg = ((m < 0 && (am & 1)) ? -1.f : 1.f) * ((mp < 0 && (amp & 1)) ? -1.f : 1.f);
+    const float cm = m < 0 ? -1.f : 1.f, cp = mp < 0 ? -1.f : 1.f;
+    xt = make_float2(sg * fmaf(cm * cp, ii, rr), sg * (cp * ri - cm * ir));
+    xu = make_float2(sg * fmaf(cm * cp, uii, urr), sg * (cp * uri - cm * uir));
+}
+
+// window and side kernels of one coefficient set per CTA, written to out and out2.
+// STAGED: f, t and the side template staged in shared memory as complex pairs
+// (a.npairs of them); false: large bases read f and the templates from global memory
 template <bool STAGED>
 __global__ void __launch_bounds__(256) build_xi_pair_kernel(XiArgs a) {
     extern __shared__ __align__(16) float xs[];
-    const int np = (a.nf + 3) & ~3;
     const float* f = a.f + (long long)blockIdx.x * a.ldf;
-    const float* fs = f;
-    const float* ts = a.t;
-    const float* us = a.t2;
-    if constexpr (STAGED) {
-        float* fw = xs;
-        float* tw = xs + np;
-        float* uw = tw + np;
-        for (int i = threadIdx.x; i < a.nf; i += blockDim.x) {
-            fw[i] = f[i];
-            tw[i] = a.t[i];
-            uw[i] = a.t2[i];
-        }
-        fs = fw, ts = tw, us = uw;
-        __syncthreads();
-    }
     const size_t off = (size_t)blockIdx.x * a.T.rows * 32;
-    for (int e = threadIdx.x; e < a.T.rows * 32; e += blockDim.x) {
-        const int2 dsc = a.T.at_desc[e];
-        float4 o1 = make_float4(0.f, 0.f, 0.f, 0.f), o2 = o1;
-        if (dsc.x & 1) {
-            const int l = (dsc.x >> 2) & 63;
-            float2 x, y;
-            xi_value2(l, ((dsc.x >> 8) & 255) - 64, ((dsc.x >> 16) & 255) - 64, fs, ts, us, a.block_off,
-                      a.radial_count, x, y);
-            o1.x = x.x, o1.y = x.y, o2.x = y.x, o2.y = y.y;
-            if (dsc.x & 2) {
-                xi_value2(l, (dsc.y & 255) - 64, ((dsc.y >> 8) & 255) - 64, fs, ts, us, a.block_off, a.radial_count,
-                          x, y);
-                o1.z = x.x, o1.w = x.y, o2.z = y.x, o2.w = y.y;
-            }
+    if constexpr (STAGED) {
+        const int np2 = (a.npairs + 1) & ~1;
+        float2* fp = reinterpret_cast<float2*>(xs);
+        float4* tu = reinterpret_cast<float4*>(xs + 2 * np2);
+        int* poff = reinterpret_cast<int*>(tu + np2);  // [L + 1] first pair of degree l
+        int* nks = poff + a.T.L + 1;                   // [L + 1] radial count of degree l
+        if (threadIdx.x <= a.T.L) {
+            int sum = 0;
+            for (int l = 0; l < threadIdx.x; ++l) sum += a.radial_count[l] * (l + 1);
+            poff[threadIdx.x] = sum;
+            nks[threadIdx.x] = a.radial_count[threadIdx.x];
         }
-        a.out[off + e] = o1;
-        a.out2[off + e] = o2;
+        __syncthreads();
+        int l = 0;  // degree of pair p: monotone in p, so the scan resumes where it stopped
+        for (int p = threadIdx.x; p < a.npairs; p += blockDim.x) {  // independent loads: one latency for all
+            while (l < a.T.L && poff[l + 1] <= p) ++l;
+            const int st = l + 1, q = p - poff[l];
+            const int k = q / st, am = q - k * st;
+            const int src = a.block_off[l] + k * (2 * l + 1) + (am ? 2 * am - 1 : 0);
+            fp[p] = make_float2(f[src], am ? f[src + 1] : 0.f);
+            tu[p] = make_float4(a.t[src], am ? a.t[src + 1] : 0.f, a.t2[src], am ? a.t2[src + 1] : 0.f);
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < a.T.rows * 32; e += blockDim.x) {
+            const int2 dsc = a.T.at_desc[e];
+            float4 o1 = make_float4(0.f, 0.f, 0.f, 0.f), o2 = o1;
+            if (dsc.x & 1) {
+                const int l = (dsc.x >> 2) & 63;
+                const float2* fl = fp + poff[l];
+                const float4* tl = tu + poff[l];
+                const int nk = nks[l];
+                float2 x, y;
+                xi_value2s(l, ((dsc.x >> 8) & 255) - 64, ((dsc.x >> 16) & 255) - 64, fl, tl, nk, x, y);
+                o1.x = x.x, o1.y = x.y, o2.x = y.x, o2.y = y.y;
+                if (dsc.x & 2) {
+                    xi_value2s(l, (dsc.y & 255) - 64, ((dsc.y >> 8) & 255) - 64, fl, tl, nk, x, y);
+                    o1.z = x.x, o1.w = x.y, o2.z = y.x, o2.w = y.y;
+                }
+            }
+            a.out[off + e] = o1;
+            a.out2[off + e] = o2;
+        }
+    } else {
+        for (int e = threadIdx.x; e < a.T.rows * 32; e += blockDim.x) {
+            const int2 dsc = a.T.at_desc[e];
+            float4 o1 = make_float4(0.f, 0.f, 0.f, 0.f), o2 = o1;
+            if (dsc.x & 1) {
+                const int l = (dsc.x >> 2) & 63;
+                float2 x, y;
+                xi_value2(l, ((dsc.x >> 8) & 255) - 64, ((dsc.x >> 16) & 255) - 64, f, a.t, a.t2, a.block_off,
+                          a.radial_count, x, y);
+                o1.x = x.x, o1.y = x.y, o2.x = y.x, o2.y = y.y;
+                if (dsc.x & 2) {
+                    xi_value2(l, (dsc.y & 255) - 64, ((dsc.y >> 8) & 255) - 64, f, a.t, a.t2, a.block_off,
+                              a.radial_count, x, y);
+                    o1.z = x.x, o1.w = x.y, o2.z = y.x, o2.w = y.y;
+                }
+            }
+            a.out[off + e] = o1;
+            a.out2[off + e] = o2;
+        }
     }
 }
 
@@ -1831,9 +1888,10 @@ int launch_eval_sweep(const EvalArgs& a, cudaStream_t s) {
 int launch_build_xi(const XiArgs& a, cudaStream_t s) {
     if (a.n <= 0) return 0;
     if (a.t2) {  // window + side kernels in one pass
-        const size_t smem = sizeof(float) * 3 * (size_t)((a.nf + 3) & ~3);
+        // staged complex pairs: 8 B of f and 16 B of (t, u) per pair, + per-degree offsets and counts
+        const size_t smem = 24 * (size_t)((a.npairs + 1) & ~1) + 2 * sizeof(int) * (size_t)(a.T.L + 1);
         if (a.ldt != 0 || a.nf <= 0 || !a.out2) return 1;
-        if (smem <= 200 * 1024) {
+        if (a.npairs > 0 && a.T.L < 256 && smem <= 200 * 1024) {
             if (ensure_dynamic_smem(build_xi_pair_kernel<true>, (int)smem) != cudaSuccess) return 2;
             build_xi_pair_kernel<true><<<a.n, 256, smem, s>>>(a);
         } else {

@@ -131,6 +131,7 @@ struct XiArgs {
     const float* t2 = nullptr;  // optional second (shared) template: kernels of (f, t2) into out2
     float4* out2 = nullptr;
     int nf = 0;                 // real-packed floats of degrees <= T.L (> 0: one CTA per set, rows staged in smem)
+    int npairs = 0;             // complex (order >= 0) entries of degrees <= T.L: sum_l n_k(l) (l + 1) (staged pair kernel)
 };
 int launch_build_xi(const XiArgs& a, cudaStream_t s);
 

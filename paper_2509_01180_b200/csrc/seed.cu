@@ -57,6 +57,14 @@ __host__ __device__ inline SeedSmem seed_smem_plan(int rows_low, int L, int nxi,
     return p;
 }
 
+// floor(x / d) for x < 2^32 / d by one multiply-high (the index arithmetic of the
+// grid phases divides by run-time extents)
+struct FastDiv {
+    unsigned d, magic;
+    __device__ __forceinline__ explicit FastDiv(int dd) : d((unsigned)dd), magic(0xFFFFFFFFu / (unsigned)dd + 1u) {}
+    __device__ __forceinline__ int div(int x) const { return d == 1 ? x : (int)__umulhi((unsigned)x, magic); }
+};
+
 __global__ void __launch_bounds__(256) seed_kernel(SeedArgs a) {
     extern __shared__ __align__(16) unsigned char sm[];
     const int w = blockIdx.x;
@@ -118,11 +126,13 @@ __global__ void __launch_bounds__(256) seed_kernel(SeedArgs a) {
     // through each phase together (three barriers per batch instead of per slice);
     // every output keeps its own summation order.
     const int wd2 = wd * wd, gw = a.ng * wd, ag = a.na * a.ng;
+    const FastDiv d_wd(wd), d_wd2(wd2), d_gw(gw), d_ag(ag), d_ng(a.ng), d_plane(ag);
     for (int j0 = 0; j0 < a.nb; j0 += plan.sb) {
         const int nj = min(plan.sb, a.nb - j0);
         for (int q = threadIdx.x; q < nj * wd2; q += blockDim.x) {
-            const int dj = q / wd2, e = q - dj * wd2;
-            const int m = e / wd - L, mp = e % wd - L;
+            const int dj = d_wd2.div(q), e = q - dj * wd2;
+            const int mr = d_wd.div(e);
+            const int m = mr - L, mp = e - mr * wd - L;
             double re = 0.0, im = 0.0;
             for (int l = max(abs(m), abs(mp)); l <= L; ++l) {
                 const int o = l * (2 * l - 1) * (2 * l + 1) / 3 + (m + l) * (2 * l + 1) + (mp + l);
@@ -136,8 +146,8 @@ __global__ void __launch_bounds__(256) seed_kernel(SeedArgs a) {
         // b[k][m] = sum_m' A_j[m][m'] ug_k[m'], then score = Re sum_m ua_i[m] b[k][m]
         // (the reference's collapse and sweep order, optimize.cpp:79-93)
         for (int q = threadIdx.x; q < nj * gw; q += blockDim.x) {
-            const int dj = q / gw, r = q - dj * gw;
-            const int k = r / wd, m = r % wd;
+            const int dj = d_gw.div(q), r = q - dj * gw;
+            const int k = d_wd.div(r), m = r - k * wd;
             const double2* pg = a.ug + (size_t)k * wd;
             const double2* Ar = Aj + dj * wd2 + m * wd;
             double bre = 0.0, bim = 0.0;
@@ -150,8 +160,8 @@ __global__ void __launch_bounds__(256) seed_kernel(SeedArgs a) {
         }
         __syncthreads();
         for (int q = threadIdx.x; q < nj * ag; q += blockDim.x) {
-            const int dj = q / ag, r = q - dj * ag;
-            const int k = r % a.ng, i = r / a.ng;
+            const int dj = d_ag.div(q), r = q - dj * ag;
+            const int i = d_ng.div(r), k = r - i * a.ng;
             const int idx = ((j0 + dj) * a.na + i) * a.ng + k;
             const double2* pa = a.ua + (size_t)i * wd;
             const double2* bk = Bk + (size_t)dj * gw + (size_t)k * wd;
@@ -170,7 +180,7 @@ __global__ void __launch_bounds__(256) seed_kernel(SeedArgs a) {
     int* cands = reinterpret_cast<int*>(sm + plan.cands);
     const int plane = a.na * a.ng;
     for (int idx = threadIdx.x; idx < npt; idx += blockDim.x) {
-        const int k = idx % a.ng, i = (idx / a.ng) % a.na, j = idx / plane;
+        const int j = d_plane.div(idx), ik = idx - j * plane, i = d_ng.div(ik), k = ik - i * a.ng;
         const double s = sc[idx];
         const int km = k == 0 ? idx + a.ng - 1 : idx - 1;
         const int kp = k == a.ng - 1 ? idx - (a.ng - 1) : idx + 1;
@@ -192,7 +202,7 @@ __global__ void __launch_bounds__(256) seed_kernel(SeedArgs a) {
     const int nc = n_cand;
     for (int q = threadIdx.x; q < nc; q += blockDim.x) {
         const int idx = cands[q];
-        const int k = idx % a.ng, i = (idx / a.ng) % a.na, j = idx / plane;
+        const int j = d_plane.div(idx), ik = idx - j * plane, i = d_ng.div(ik), k = ik - i * a.ng;
         const double s = sc[idx];
         bool is_max = true;
         for (int dj = -1; dj <= 1 && is_max; ++dj) {
@@ -232,7 +242,7 @@ __global__ void __launch_bounds__(256) seed_kernel(SeedArgs a) {
             rank += (t2 > s || (t2 == s && jdx < idx)) ? 1 : 0;
         }
         if (rank < keep) {
-            const int k = idx % a.ng, i = (idx / a.ng) % a.na, j = idx / (a.ng * a.na);
+            const int j = d_plane.div(idx), ik = idx - j * plane, i = d_ng.div(ik), k = ik - i * a.ng;
             const double alpha = 2.0 * 3.14159265358979323846 * i / a.na;
             const double beta = a.nb > 1 ? 3.14159265358979323846 * j / (a.nb - 1) : 0.0;
             const double gamma = 2.0 * 3.14159265358979323846 * k / a.ng;
