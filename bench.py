@@ -422,8 +422,8 @@ def run_product(args):
                    + 4.0 * ctx.n_r * ntri * ctx.n_theta + 2.0 * ctx.n_r * C)
         gemm_flops = per_win * windows_per_step
         peak_x = fp32_peak
-        roof_gemm = {"kernel": "expand_pair_kernel / expand_factored_kernel (trilinear samples, phi-DFT, theta + "
-                               "radial contractions; two windows per CTA)",
+        roof_gemm = {"kernel": "expand_quad_kernel (quad-copy gathers, phi-DFT, theta + radial contractions; two "
+                               "windows per CTA, x-neighbours share their loads)",
                      "bound": "fp32_simt", "peak": peak_x, "peak_note": fp32_kind,
                      "algorithmic": "per window 16 S taps + 4 n_phi n_r n_theta (L+1) + 4 n_r tri(L) n_theta + "
                                     "2 n_r C, S=%d C=%d (%.2f MFLOP)" % (S, C, per_win / 1e6)}
@@ -461,12 +461,16 @@ def run_product(args):
     roof_eval["per_band"] = per_band
     roof_eval["flops_per_step"] = tot
     roof_eval["eval_ms_per_step"] = eval_ms
-    tr = ROOT / "profiles" / "round2" / "step_traffic_r2b.json"
+    tr = ROOT / "profiles" / "round2" / "step_traffic_r2c.json"
     if tr.exists():
-        cls = json.loads(tr.read_text())["classes"]["eval"]
+        classes = json.loads(tr.read_text())["classes"]
+        cls = classes["eval"]
         roof_eval["traffic"] = cls["dram_bytes"] * P / 1024.0
+        if args.expand == "factored" and "expand" in classes:
+            roof_gemm["traffic"] = classes["expand"]["dram_bytes"] * P / 1024.0
+            roof_gemm["traffic_note"] = "DRAM bytes per step of the expansion kernels (quad copy + gathers), same ncu pass"
         roof_eval["traffic_note"] = ("DRAM bytes (read + write) per step of the evaluation kernels, from "
-                                     "ncu over one config-2 step (profiles/round2/step_traffic_r2b.json, "
+                                     "ncu over one config-2 step (profiles/round2/step_traffic_r2c.json, "
                                      "1024 particles, scaled to this batch; cold-cache per launch)")
     dominant = "refine" if refine_ms > gemm_ms else "expand"
     line = {
