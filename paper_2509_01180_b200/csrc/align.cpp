@@ -357,12 +357,30 @@ void Context::refine_windows(int nw, int maxc, const AlignConfig& cfg, const Qua
             // at order 2, then accept / retry / advance each to its next iteration
             int cur = 0;
             const int max_rounds = 4 * cfg.newton_max_iter + 8;
+            // The list lengths come back to the host to size the launches and to stop.
+            // Candidates only ever leave the lists, so once few are left (the long
+            // tail: after ~20 of ~60 rounds under 2% remain) the host reads the counts
+            // every round_check_-th round only and sizes the rounds in between by the
+            // last sum (an upper bound); the kernels take the true lengths from device
+            // memory, and a round on empty lists is a few empty launches.
+            int bound = (int)slots, since_check = 0;
+            int nf = 0, nt = 0;
             for (int round = 0; round < max_rounds; ++round) {
-                ck(cudaMemcpyAsync(h_active, d_counts, sizeof(int) * 4, cudaMemcpyDeviceToHost, stream), "active");
-                ck(cudaStreamSynchronize(stream), "round");
-                const int nf = h_active[cur], nt = h_active[2 + cur];
-                if (debug_iters_) fprintf(stderr, "[refine] band %d round %d fresh %d trials %d\n", L, round, nf, nt);
-                if (nf == 0 && nt == 0) break;
+                const bool check = debug_iters_ || round_check_ <= 1 || bound > kTailCandidates ||
+                                   since_check + 1 >= round_check_;
+                if (check) {
+                    ck(cudaMemcpyAsync(h_active, d_counts, sizeof(int) * 4, cudaMemcpyDeviceToHost, stream), "active");
+                    ck(cudaStreamSynchronize(stream), "round");
+                    nf = h_active[cur], nt = h_active[2 + cur];
+                    if (debug_iters_)
+                        fprintf(stderr, "[refine] band %d round %d fresh %d trials %d\n", L, round, nf, nt);
+                    if (nf == 0 && nt == 0) break;
+                    bound = nf + nt;
+                    since_check = 0;
+                } else {
+                    nf = bound, nt = 0;  // launch bounds only (nt_max below = bound)
+                    ++since_check;
+                }
                 ck(cudaMemsetAsync(c_fresh[cur ^ 1], 0, sizeof(int), stream), "next fresh count");
                 ck(cudaMemsetAsync(c_trial[cur ^ 1], 0, sizeof(int), stream), "next trial count");
                 if (nf > 0) {

@@ -273,6 +273,12 @@ public:
     DevBuf work_f, work_xi, filtered;
 
     bool debug_iters_ = std::getenv("BMB_DEBUG_ITERS") != nullptr;
+    // Newton rounds: host reads of the list lengths in the tail (align.cpp run_windows)
+    static constexpr int kTailCandidates = 8192;
+    int round_check_ = [] {
+        const char* e = std::getenv("BMB_ROUND_CHECK");
+        return e ? std::atoi(e) : 4;
+    }();
     // pinned host words for the per-iteration list counts (allocated once:
     // cudaMallocHost / cudaFreeHost per call stall the host unpredictably)
     int* pinned_ = nullptr;
