@@ -1011,14 +1011,12 @@ __device__ __forceinline__ void set_eval_frame(CandWork& wk, const Quat& g, cons
 // optimize.cpp:292-298): 0 = no step, 1 = evaluate at order 2 first, 2 = step on
 // the order-2 results of the accepted trial (already at g).  Anchored candidates
 // pick the kernel and angles of their order-2 evaluation (chart_transform).
-__device__ __forceinline__ int iter_begin_one(const StageArgs& a, long long i) {
-    CandWork& wk = a.work[i];
+__device__ __forceinline__ int iter_begin_one(const StageArgs& a, CandWork& wk, CandState& st) {
     if (wk.status != ST_START) return 0;
     if (wk.iter >= a.prm.newton_max_iter) {
         wk.status = ST_DONE;
         return 0;
     }
-    CandState& st = a.cand[i];
     const Quat g = qload(st.g);
     const Quat koff{a.prm.koffset[0], a.prm.koffset[1], a.prm.koffset[2], a.prm.koffset[3]};
     const bool was_anchored = st.anchored != 0;
@@ -1057,6 +1055,10 @@ __device__ __forceinline__ int iter_begin_one(const StageArgs& a, long long i) {
     wk.side = 0;
     if (st.anchored) set_eval_frame(wk, g, koff);
     return 1;
+}
+
+__device__ __forceinline__ int iter_begin_one(const StageArgs& a, long long i) {
+    return iter_begin_one(a, a.work[i], a.cand[i]);
 }
 
 // The Newton kernels are latency-bound dependent FP64 chains over one
@@ -1241,9 +1243,7 @@ __global__ void __launch_bounds__(BMB_HALF_WARPS * 32, BMB_EVAL_MINB(ORDER)) eva
 // Newton step of an order-2 evaluated candidate; true: a trial is due (made here
 // unless the caller makes it: one inlined copy of make_trial per kernel)
 template <bool MAKE = true>
-__device__ __forceinline__ bool step_one(const StageArgs& a, long long i) {
-    CandWork& wk = a.work[i];
-    CandState& st = a.cand[i];
+__device__ __forceinline__ bool step_one(const StageArgs& a, CandWork& wk, CandState& st) {
     Derivs f;
     objective(wk.c, wk.r, a.prm.has_wedge != 0, 2, f);
     if (wk.side) chart_transform(f, wk.te, wk.tv);  // anchored: derivatives in the chart angles
@@ -1286,22 +1286,73 @@ __device__ __forceinline__ bool step_one(const StageArgs& a, long long i) {
 #ifndef BMB_NEWTON_BLOCK_SIZE
 #define BMB_NEWTON_BLOCK_SIZE 32
 #endif
+// A warp's candidates staged in shared memory for the Newton kernels: the
+// thread-per-candidate chains read and update most of CandWork / CandState field
+// by field, and every such access was a dependent global round trip (ncu: 78% of
+// the stalls on long scoreboards, 13% issue).  The warp copies its 32 records in
+// with coalesced, independent 8-byte loads (one memory latency for all of them),
+// runs the chain on the shared copies and writes the records back.  Strides of
+// an odd number of 8-byte words keep the per-lane records on distinct banks.
+constexpr int kWorkWords = (int)(sizeof(CandWork) / 8), kCandWords = (int)(sizeof(CandState) / 8);
+constexpr int kWorkStride = kWorkWords | 1, kCandStride = kCandWords | 1;  // in 8-byte words
+static_assert(sizeof(CandWork) % 8 == 0 && sizeof(CandState) % 8 == 0, "records are copied in 8-byte words");
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(gmem)
+                 : "memory");
+}
+struct NewtonStage {
+    unsigned long long work[32 * kWorkStride];
+    unsigned long long cand[32 * kCandStride];
+};
+__device__ __forceinline__ void stage_in(const StageArgs& a, int i, NewtonStage& sm) {
+    const int lane = threadIdx.x & 31;
+    for (int c = 0; c < 32; ++c) {
+        const int ic = __shfl_sync(0xffffffffu, i, c);
+        if (ic < 0) continue;
+        const unsigned long long* gw = reinterpret_cast<const unsigned long long*>(a.work + ic);
+        const unsigned long long* gc = reinterpret_cast<const unsigned long long*>(a.cand + ic);
+        // asynchronous copies (no register staging): every record's loads are in flight at once
+        for (int k = lane; k < kWorkWords; k += 32) cp_async8(sm.work + c * kWorkStride + k, gw + k);
+        if (lane < kCandWords) cp_async8(sm.cand + c * kCandStride + lane, gc + lane);
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncwarp();
+}
+__device__ __forceinline__ void stage_out(const StageArgs& a, int i, const NewtonStage& sm) {
+    const int lane = threadIdx.x & 31;
+    __syncwarp();
+    for (int c = 0; c < 32; ++c) {
+        const int ic = __shfl_sync(0xffffffffu, i, c);
+        if (ic < 0) continue;
+        unsigned long long* gw = reinterpret_cast<unsigned long long*>(a.work + ic);
+        unsigned long long* gc = reinterpret_cast<unsigned long long*>(a.cand + ic);
+        for (int k = lane; k < kWorkWords; k += 32) gw[k] = sm.work[c * kWorkStride + k];
+        if (lane < kCandWords) gc[lane] = sm.cand[c * kCandStride + lane];
+    }
+    __syncwarp();
+}
+static_assert(kCandWords <= 32, "one pass of the warp copies a CandState");
+
 __global__ void BMB_NEWTON_BOUNDS step_kernel(StageArgs a, const int* list_in, const int* count_in, int* list_out, int* count_out) {
+    extern __shared__ __align__(16) unsigned char newton_smem[];
+    NewtonStage& sm = reinterpret_cast<NewtonStage*>(newton_smem)[threadIdx.x >> 5];
+    const int lane = threadIdx.x & 31;
     const int n = *count_in;
     const int n_pad = (n + 31) & ~31;
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_pad; q += gridDim.x * blockDim.x) {
         const int i = q < n ? list_in[q] : -1;
-        if (i >= 0) prefetch_cand(a, i);
-        const bool t = i >= 0 && step_one(a, i);
+        stage_in(a, i, sm);
+        CandWork& wk = *reinterpret_cast<CandWork*>(sm.work + lane * kWorkStride);
+        CandState& st = *reinterpret_cast<CandState*>(sm.cand + lane * kCandStride);
+        const bool t = i >= 0 && step_one(a, wk, st);
+        stage_out(a, i, sm);
         wappend(t, i, list_out, count_out);
     }
 }
 
 // acceptance test of a trial; true: it failed with retries left (re-queue after
 // the caller makes the damped trial)
-__device__ __forceinline__ bool accept_one(const StageArgs& a, long long i) {
-    CandWork& wk = a.work[i];
-    CandState& st = a.cand[i];
+__device__ __forceinline__ bool accept_one(const StageArgs& a, CandWork& wk, CandState& st) {
     Derivs t;
     objective(wk.c, wk.r, a.prm.has_wedge != 0, 0, t);  // the value (the trial ran at order 2)
     ++st.evals;
@@ -1345,24 +1396,29 @@ __device__ __forceinline__ bool accept_one(const StageArgs& a, long long i) {
 // differs from a lock-step iteration.
 __global__ void BMB_NEWTON_BOUNDS advance_kernel(StageArgs a, const int* list_in, const int* count_in, int* trial_out, int* trial_count,
                                int* fresh_out, int* fresh_count) {
+    extern __shared__ __align__(16) unsigned char newton_smem[];
+    NewtonStage& sm = reinterpret_cast<NewtonStage*>(newton_smem)[threadIdx.x >> 5];
+    const int lane = threadIdx.x & 31;
     const int n = *count_in;
     const int n_pad = (n + 31) & ~31;
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_pad; q += gridDim.x * blockDim.x) {
         const int i = q < n ? list_in[q] : -1;
         bool trial = false, fresh = false;
+        stage_in(a, i, sm);
         if (i >= 0) {
-            prefetch_cand(a, i);
-            if (accept_one(a, i)) {
+            CandWork& wk = *reinterpret_cast<CandWork*>(sm.work + lane * kWorkStride);
+            CandState& st = *reinterpret_cast<CandState*>(sm.cand + lane * kCandStride);
+            if (accept_one(a, wk, st)) {
                 trial = true;  // damped retry
-            } else if (a.work[i].status == ST_START) {
-                const int f = iter_begin_one(a, i);
-                if (f == 2) trial = step_one<false>(a, i);
+            } else if (wk.status == ST_START) {
+                const int f = iter_begin_one(a, wk, st);
+                if (f == 2) trial = step_one<false>(a, wk, st);
                 else fresh = f == 1;
             }
             if (trial)
-                make_trial(a.work[i], a.cand[i],
-                           Quat{a.prm.koffset[0], a.prm.koffset[1], a.prm.koffset[2], a.prm.koffset[3]});
+                make_trial(wk, st, Quat{a.prm.koffset[0], a.prm.koffset[1], a.prm.koffset[2], a.prm.koffset[3]});
         }
+        stage_out(a, i, sm);
         wappend(trial, i, trial_out, trial_count);
         wappend(fresh, i, fresh_out, fresh_count);
     }
@@ -1837,12 +1893,16 @@ void launch_eval(const StageArgs& a, int order, const int* list, const int* coun
 }
 void launch_step(const StageArgs& a, const int* list_in, const int* count_in, int* list_out, int* count_out,
                  int max_n, cudaStream_t s) {
-    step_kernel<<<thread_grid(max_n), kNB, 0, s>>>(a, list_in, count_in, list_out, count_out);
+    constexpr int smem = (kNB / 32) * (int)sizeof(NewtonStage);
+    if (smem > 48 * 1024) ensure_dynamic_smem(step_kernel, smem);
+    step_kernel<<<thread_grid(max_n), kNB, smem, s>>>(a, list_in, count_in, list_out, count_out);
 }
 void launch_advance(const StageArgs& a, const int* list_in, const int* count_in, int* trial_out, int* trial_count,
                     int* fresh_out, int* fresh_count, int max_n, cudaStream_t s) {
-    advance_kernel<<<thread_grid(max_n), kNB, 0, s>>>(a, list_in, count_in, trial_out, trial_count, fresh_out,
-                                                      fresh_count);
+    constexpr int smem = (kNB / 32) * (int)sizeof(NewtonStage);
+    if (smem > 48 * 1024) ensure_dynamic_smem(advance_kernel, smem);
+    advance_kernel<<<thread_grid(max_n), kNB, smem, s>>>(a, list_in, count_in, trial_out, trial_count, fresh_out,
+                                                         fresh_count);
 }
 void launch_final_prep(const StageArgs& a, cudaStream_t s) {
     final_prep_kernel<<<thread_grid((long long)a.n_win * a.max_cand), kNB, 0, s>>>(a);
