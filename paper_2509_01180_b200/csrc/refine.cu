@@ -157,6 +157,9 @@ __device__ __forceinline__ float2 phase_of(const WS& w, int m, int mp) {
 #ifndef BMB_PIPE_MASK
 #define BMB_PIPE_MASK 0
 #endif
+#ifndef BMB_PF_SMALL
+#define BMB_PF_SMALL 1
+#endif
 #ifndef BMB_PF_MIN_GROUPS
 #define BMB_PF_MIN_GROUPS 4
 #endif
@@ -520,6 +523,9 @@ __device__ __forceinline__ void warp_eval_sub(const BandTables& T, const EvalJob
     if (T.n_groups > 0) {
         if (pf_x) prefetch_half(xi, T.row_off[0], T.row_off[1]);
         if (pf_w) prefetch_half(wx, T.row_off[0], T.row_off[1]);
+        // low bands: the job's whole window kernel is a few KB; request it now so that
+        // it arrives behind the sincos and the phase powers (BMB_PF_SMALL=0: off)
+        if (BMB_PF_SMALL && PF && !pf_x && __isGlobal(xi)) prefetch_half(xi, T.row_off[0], T.row_off[T.n_groups]);
     }
     // four FP64 sincos per job on lanes 0..3 of its half (beta/2, beta, alpha, gamma)
     if (l16 < 4) {
@@ -1293,27 +1299,40 @@ __device__ __forceinline__ bool step_one(const StageArgs& a, CandWork& wk, CandS
 // with coalesced, independent 8-byte loads (one memory latency for all of them),
 // runs the chain on the shared copies and writes the records back.  Strides of
 // an odd number of 8-byte words keep the per-lane records on distinct banks.
-constexpr int kWorkWords = (int)(sizeof(CandWork) / 8), kCandWords = (int)(sizeof(CandState) / 8);
-constexpr int kWorkStride = kWorkWords | 1, kCandStride = kCandWords | 1;  // in 8-byte words
-static_assert(sizeof(CandWork) % 8 == 0 && sizeof(CandState) % 8 == 0, "records are copied in 8-byte words");
+// CandWork in 16-byte chunks at a stride of an odd number of chunks, CandState in
+// 8-byte words at an odd stride: the lanes' records fall on different banks.
+constexpr int kWorkChunks = (int)(sizeof(CandWork) / 16), kCandWords = (int)(sizeof(CandState) / 8);
+constexpr int kWorkStride = (kWorkChunks | 1) * 2, kCandStride = kCandWords | 1;  // in 8-byte words
+static_assert(sizeof(CandWork) % 16 == 0 && sizeof(CandState) % 8 == 0, "record sizes the copies assume");
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(gmem)
                  : "memory");
 }
-struct NewtonStage {
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(gmem)
+                 : "memory");
+}
+struct __align__(16) NewtonStage {
     unsigned long long work[32 * kWorkStride];
     unsigned long long cand[32 * kCandStride];
 };
+// the warp's 32 * kWorkChunks chunks (and 32 * kCandWords words) dealt round-robin to
+// the lanes: every copy instruction moves 512 (256) contiguous-by-record bytes
 __device__ __forceinline__ void stage_in(const StageArgs& a, int i, NewtonStage& sm) {
     const int lane = threadIdx.x & 31;
-    for (int c = 0; c < 32; ++c) {
+#pragma unroll 5
+    for (int j = 0; j < kWorkChunks; ++j) {
+        const int f = lane + 32 * j, c = f / kWorkChunks, k = f - c * kWorkChunks;
         const int ic = __shfl_sync(0xffffffffu, i, c);
-        if (ic < 0) continue;
-        const unsigned long long* gw = reinterpret_cast<const unsigned long long*>(a.work + ic);
-        const unsigned long long* gc = reinterpret_cast<const unsigned long long*>(a.cand + ic);
-        // asynchronous copies (no register staging): every record's loads are in flight at once
-        for (int k = lane; k < kWorkWords; k += 32) cp_async8(sm.work + c * kWorkStride + k, gw + k);
-        if (lane < kCandWords) cp_async8(sm.cand + c * kCandStride + lane, gc + lane);
+        if (ic >= 0)
+            cp_async16(sm.work + c * kWorkStride + 2 * k, reinterpret_cast<const uint4*>(a.work + ic) + k);
+    }
+#pragma unroll
+    for (int j = 0; j < kCandWords; ++j) {
+        const int f = lane + 32 * j, c = f / kCandWords, k = f - c * kCandWords;
+        const int ic = __shfl_sync(0xffffffffu, i, c);
+        if (ic >= 0)
+            cp_async8(sm.cand + c * kCandStride + k, reinterpret_cast<const unsigned long long*>(a.cand + ic) + k);
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncwarp();
@@ -1321,17 +1340,21 @@ __device__ __forceinline__ void stage_in(const StageArgs& a, int i, NewtonStage&
 __device__ __forceinline__ void stage_out(const StageArgs& a, int i, const NewtonStage& sm) {
     const int lane = threadIdx.x & 31;
     __syncwarp();
-    for (int c = 0; c < 32; ++c) {
+#pragma unroll 5
+    for (int j = 0; j < kWorkChunks; ++j) {
+        const int f = lane + 32 * j, c = f / kWorkChunks, k = f - c * kWorkChunks;
         const int ic = __shfl_sync(0xffffffffu, i, c);
-        if (ic < 0) continue;
-        unsigned long long* gw = reinterpret_cast<unsigned long long*>(a.work + ic);
-        unsigned long long* gc = reinterpret_cast<unsigned long long*>(a.cand + ic);
-        for (int k = lane; k < kWorkWords; k += 32) gw[k] = sm.work[c * kWorkStride + k];
-        if (lane < kCandWords) gc[lane] = sm.cand[c * kCandStride + lane];
+        if (ic >= 0)
+            reinterpret_cast<uint4*>(a.work + ic)[k] = *reinterpret_cast<const uint4*>(sm.work + c * kWorkStride + 2 * k);
+    }
+#pragma unroll
+    for (int j = 0; j < kCandWords; ++j) {
+        const int f = lane + 32 * j, c = f / kCandWords, k = f - c * kCandWords;
+        const int ic = __shfl_sync(0xffffffffu, i, c);
+        if (ic >= 0) reinterpret_cast<unsigned long long*>(a.cand + ic)[k] = sm.cand[c * kCandStride + k];
     }
     __syncwarp();
 }
-static_assert(kCandWords <= 32, "one pass of the warp copies a CandState");
 
 __global__ void BMB_NEWTON_BOUNDS step_kernel(StageArgs a, const int* list_in, const int* count_in, int* list_out, int* count_out) {
     extern __shared__ __align__(16) unsigned char newton_smem[];
