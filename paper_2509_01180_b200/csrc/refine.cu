@@ -1151,6 +1151,9 @@ __device__ __forceinline__ void eval_group(const BandTables& T, const EvalJob (&
 #ifndef BMB_EVAL_MINB2
 #define BMB_EVAL_MINB2 4
 #endif
+#ifndef BMB_EVAL_MINB2_L8
+#define BMB_EVAL_MINB2_L8 3
+#endif
 #define BMB_EVAL_MINB(order) ((order) == 2 ? BMB_EVAL_MINB2 : BMB_EVAL_MINB0)
 template <int ORDER, int K, bool TRIAL = false>
 __global__ void __launch_bounds__(EvalShape<K>::WARPS * 32, BMB_EVAL_MINB(ORDER)) eval_kernel(StageArgs a, const int* list,
@@ -1207,8 +1210,9 @@ struct SubShape {
     static constexpr int ML = LANES == 8 ? 8 : kMaxL;  // 8-lane jobs serve L <= 8
     using WS = WarpScratchT<ML, LANES == 8 ? 8 : 16>;
 };
+// (8-lane jobs at order 2: three CTAs per SM, 85 registers, measured 3% faster than four)
 template <int ORDER, bool TRIAL, int LANES>
-__global__ void __launch_bounds__(BMB_HALF_WARPS * 32, BMB_EVAL_MINB(ORDER)) eval_sub_kernel(StageArgs a, const int* list,
+__global__ void __launch_bounds__(BMB_HALF_WARPS * 32, (ORDER == 2 && LANES == 8) ? BMB_EVAL_MINB2_L8 : BMB_EVAL_MINB(ORDER)) eval_sub_kernel(StageArgs a, const int* list,
                                                                                          const int* count) {
     constexpr int WARPS = BMB_HALF_WARPS, JOBS = 32 / LANES;
     using WS = typename SubShape<LANES>::WS;

@@ -14,6 +14,13 @@ namespace bmb {
 
 // shared-memory plan: [f | t] (later reused for one beta slice A_j), xi (or
 // the global scratch when it does not fit), scores, maxima
+// shared-memory budget of a CTA (sets the beta slices per batch) and resident CTAs per SM
+#ifndef BMB_SEED_SMEM_KB
+#define BMB_SEED_SMEM_KB 52
+#endif
+#ifndef BMB_SEED_MINB
+#define BMB_SEED_MINB 4
+#endif
 struct SeedSmem {
     size_t region0, xi, sc, maxima, bk, cands, total;
     bool xi_in_smem;
@@ -26,12 +33,12 @@ __host__ __device__ inline SeedSmem seed_smem_plan(int rows_low, int L, int nxi,
     const size_t aj = sizeof(double2) * (size_t)wd * wd;
     const size_t xib = sizeof(double2) * (size_t)nxi;
     const size_t fixed = sizeof(double) * npt + 2 * sizeof(int) * (size_t)npt + 64;
-    // as many slices per batch as keep the CTA near 64 KB (three CTAs per SM): the
+    // as many slices per batch as keep the CTA near 52 KB (four CTAs per SM, measured best): the
     // three phases of a batch then run on sb times the threads between barriers
     p.sb = 1;
     for (int sb = nb; sb > 1; --sb) {
         const size_t r0 = ft > aj * sb ? ft : aj * sb;
-        if (r0 + xib + fixed + sizeof(double2) * (size_t)wd * ng * sb <= 72 * 1024) {
+        if (r0 + xib + fixed + sizeof(double2) * (size_t)wd * ng * sb <= BMB_SEED_SMEM_KB * 1024) {
             p.sb = sb;
             break;
         }
@@ -65,7 +72,7 @@ struct FastDiv {
     __device__ __forceinline__ int div(int x) const { return d == 1 ? x : (int)__umulhi((unsigned)x, magic); }
 };
 
-__global__ void __launch_bounds__(256) seed_kernel(SeedArgs a) {
+__global__ void __launch_bounds__(256, BMB_SEED_MINB) seed_kernel(SeedArgs a) {
     extern __shared__ __align__(16) unsigned char sm[];
     const int w = blockIdx.x;
     const int L = a.L_low, wd = 2 * L + 1;

@@ -10,7 +10,7 @@ sys.path.insert(0, str(ROOT))
 from paper_2509_01180_b200 import build as B  # noqa: E402
 
 
-VARIANT_SOURCES = ("refine.cu", "expand_factored.cu")
+VARIANT_SOURCES = ("refine.cu", "expand_factored.cu", "seed.cu")
 
 
 def main():
