@@ -1151,9 +1151,6 @@ __device__ __forceinline__ void eval_group(const BandTables& T, const EvalJob (&
 #ifndef BMB_EVAL_MINB2
 #define BMB_EVAL_MINB2 4
 #endif
-#ifndef BMB_EVAL_MINB2_L8
-#define BMB_EVAL_MINB2_L8 3
-#endif
 #define BMB_EVAL_MINB(order) ((order) == 2 ? BMB_EVAL_MINB2 : BMB_EVAL_MINB0)
 template <int ORDER, int K, bool TRIAL = false>
 __global__ void __launch_bounds__(EvalShape<K>::WARPS * 32, BMB_EVAL_MINB(ORDER)) eval_kernel(StageArgs a, const int* list,
@@ -1203,16 +1200,26 @@ __global__ void __launch_bounds__(EvalShape<K>::WARPS * 32, BMB_EVAL_MINB(ORDER)
 // 32 / LANES listed candidates per warp, one per LANES-lane slice (warp_eval_sub);
 // the scratch sets are sized for the bands the slice width serves
 #ifndef BMB_HALF_WARPS
-#define BMB_HALF_WARPS 8
+#define BMB_HALF_WARPS 4
+#endif
+#ifndef BMB_SUB_WARPS_O2
+#define BMB_SUB_WARPS_O2 32
+#endif
+#ifndef BMB_SUB_WARPS_OTHER
+#define BMB_SUB_WARPS_OTHER 24
 #endif
 template <int LANES>
 struct SubShape {
     static constexpr int ML = LANES == 8 ? 8 : kMaxL;  // 8-lane jobs serve L <= 8
     using WS = WarpScratchT<ML, LANES == 8 ? 8 : 16>;
 };
-// (8-lane jobs at order 2: three CTAs per SM, 85 registers, measured 3% faster than four)
+// CTAs of four warps (measured 2.6% faster than eight: finer tail); resident warps per SM
+// by register cap: 32 at order 2 with 16-lane jobs (64 registers), 24 with 8-lane jobs and
+// at order 0 (85 registers; 8-lane order 2 measured 3% faster than at 64 registers)
+#define BMB_SUB_MINB(order, lanes) \
+    (((order) == 2 && (lanes) == 16 ? BMB_SUB_WARPS_O2 : BMB_SUB_WARPS_OTHER) / BMB_HALF_WARPS)
 template <int ORDER, bool TRIAL, int LANES>
-__global__ void __launch_bounds__(BMB_HALF_WARPS * 32, (ORDER == 2 && LANES == 8) ? BMB_EVAL_MINB2_L8 : BMB_EVAL_MINB(ORDER)) eval_sub_kernel(StageArgs a, const int* list,
+__global__ void __launch_bounds__(BMB_HALF_WARPS * 32, BMB_SUB_MINB(ORDER, LANES)) eval_sub_kernel(StageArgs a, const int* list,
                                                                                          const int* count) {
     constexpr int WARPS = BMB_HALF_WARPS, JOBS = 32 / LANES;
     using WS = typename SubShape<LANES>::WS;
