@@ -1203,7 +1203,7 @@ __global__ void __launch_bounds__(EvalShape<K>::WARPS * 32, BMB_EVAL_MINB(ORDER)
 #define BMB_HALF_WARPS 4
 #endif
 #ifndef BMB_SUB_WARPS_O2
-#define BMB_SUB_WARPS_O2 32
+#define BMB_SUB_WARPS_O2 28
 #endif
 #ifndef BMB_SUB_WARPS_OTHER
 #define BMB_SUB_WARPS_OTHER 24
@@ -1214,8 +1214,9 @@ struct SubShape {
     using WS = WarpScratchT<ML, LANES == 8 ? 8 : 16>;
 };
 // CTAs of four warps (measured 2.6% faster than eight: finer tail); resident warps per SM
-// by register cap: 32 at order 2 with 16-lane jobs (64 registers), 24 with 8-lane jobs and
-// at order 0 (85 registers; 8-lane order 2 measured 3% faster than at 64 registers)
+// by register cap: 28 at order 2 with 16-lane jobs (72 registers: 4.6% faster than 32 warps
+// at 64 registers with their spills, 24 warps slower again), 24 with 8-lane jobs and at
+// order 0 (85 registers; 8-lane order 2 measured 3% faster than at 64 registers)
 #define BMB_SUB_MINB(order, lanes) \
     (((order) == 2 && (lanes) == 16 ? BMB_SUB_WARPS_O2 : BMB_SUB_WARPS_OTHER) / BMB_HALF_WARPS)
 template <int ORDER, bool TRIAL, int LANES>
