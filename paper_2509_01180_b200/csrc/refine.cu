@@ -1301,6 +1301,9 @@ __device__ __forceinline__ bool step_one(const StageArgs& a, CandWork& wk, CandS
 #else
 #define BMB_NEWTON_BOUNDS
 #endif
+#ifndef BMB_NEWTON_PAD_BYTES
+#define BMB_NEWTON_PAD_BYTES 0  // occupancy experiments: extra dynamic shared memory per CTA
+#endif
 #ifndef BMB_NEWTON_BLOCK_SIZE
 #define BMB_NEWTON_BLOCK_SIZE 32
 #endif
@@ -1928,13 +1931,13 @@ void launch_eval(const StageArgs& a, int order, const int* list, const int* coun
 }
 void launch_step(const StageArgs& a, const int* list_in, const int* count_in, int* list_out, int* count_out,
                  int max_n, cudaStream_t s) {
-    constexpr int smem = (kNB / 32) * (int)sizeof(NewtonStage);
+    constexpr int smem = (kNB / 32) * (int)sizeof(NewtonStage) + BMB_NEWTON_PAD_BYTES;
     if (smem > 48 * 1024) ensure_dynamic_smem(step_kernel, smem);
     step_kernel<<<thread_grid(max_n), kNB, smem, s>>>(a, list_in, count_in, list_out, count_out);
 }
 void launch_advance(const StageArgs& a, const int* list_in, const int* count_in, int* trial_out, int* trial_count,
                     int* fresh_out, int* fresh_count, int max_n, cudaStream_t s) {
-    constexpr int smem = (kNB / 32) * (int)sizeof(NewtonStage);
+    constexpr int smem = (kNB / 32) * (int)sizeof(NewtonStage) + BMB_NEWTON_PAD_BYTES;
     if (smem > 48 * 1024) ensure_dynamic_smem(advance_kernel, smem);
     advance_kernel<<<thread_grid(max_n), kNB, smem, s>>>(a, list_in, count_in, trial_out, trial_count, fresh_out,
                                                          fresh_count);
