@@ -465,7 +465,7 @@ def run_product(args):
     roof_eval["per_band"] = per_band
     roof_eval["flops_per_step"] = tot
     roof_eval["eval_ms_per_step"] = eval_ms
-    tr = ROOT / "profiles" / "round2" / "step_traffic_r2c.json"
+    tr = ROOT / "profiles" / "round2" / "step_traffic_r2e.json"
     if tr.exists():
         classes = json.loads(tr.read_text())["classes"]
         cls = classes["eval"]
@@ -474,7 +474,7 @@ def run_product(args):
             roof_gemm["traffic"] = classes["expand"]["dram_bytes"] * P / 1024.0
             roof_gemm["traffic_note"] = "DRAM bytes per step of the expansion kernels (quad copy + gathers), same ncu pass"
         roof_eval["traffic_note"] = ("DRAM bytes (read + write) per step of the evaluation kernels, from "
-                                     "ncu over one config-2 step (profiles/round2/step_traffic_r2c.json, "
+                                     "ncu over one config-2 step (profiles/round2/step_traffic_r2e.json, "
                                      "1024 particles, scaled to this batch; cold-cache per launch)")
     dominant = "refine" if refine_ms > gemm_ms else "expand"
     line = {

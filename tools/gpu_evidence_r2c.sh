@@ -1,7 +1,7 @@
-# Round-2 end-of-round evidence (quad expansion kernel) in one box session (writes gpurun_out/ev3/*):
+# Round-2 end-of-round evidence (quad expansion kernel) in one box session (writes gpurun_out/ev4/*):
 #   gpurun --timeout 3000 -- 'bash tools/gpu_evidence_r2c.sh'
 set -u
-O=gpurun_out/ev3
+O=gpurun_out/ev4
 mkdir -p $O
 timeout 1200 python -m pytest -q -m gpu tests > $O/gpu_tests.log 2>&1; echo "tests=$?" > $O/status.txt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke=$?" >> $O/status.txt
