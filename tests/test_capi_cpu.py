@@ -88,3 +88,11 @@ def test_host_wigner_D_and_grid_count_match_oracle():
         st = deg * math.pi / 180.0
         na, nb = math.ceil(2 * math.pi / st), math.ceil(math.pi / st) + 1
         assert api.baseline_evaluation_count(st) == na * na * nb == bmo.baseline_evaluation_count(st)
+
+
+def test_expand_entry_points_reject_a_null_context():
+    """bm_expand / bm_expand_windows without a context: an error code, no crash
+    (the argument checks run before any device call)."""
+    L = _lib.lib()
+    assert L.bm_expand(None, None, 0, None, None, None) != 0
+    assert L.bm_expand_windows(None, None, 0, None, None, 0, None, None) != 0
