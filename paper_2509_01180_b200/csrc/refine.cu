@@ -27,6 +27,8 @@
 #include <cfloat>
 #include <cstdlib>
 
+#include <cstddef>
+
 #include "smem_attr.hpp"
 #include "refine.cuh"
 #include "rotation.cuh"
@@ -1352,12 +1354,21 @@ __device__ __forceinline__ void stage_in(const StageArgs& a, int i, NewtonStage&
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncwarp();
 }
+// the raw derivatives c / r are inputs of the Newton kernels only (the evaluation kernels
+// write them): their chunks are not written back
+constexpr int kRawChunk0 = (int)(offsetof(CandWork, c) / 16);
+constexpr int kRawChunk1 = (int)((offsetof(CandWork, r) + sizeof(double) * 10) / 16);
+static_assert(offsetof(CandWork, c) % 16 == 0 && (offsetof(CandWork, r) + sizeof(double) * 10) % 16 == 0 &&
+                  offsetof(CandWork, r) == offsetof(CandWork, c) + sizeof(double) * 10,
+              "c and r form one 16-byte aligned span of CandWork");
 __device__ __forceinline__ void stage_out(const StageArgs& a, int i, const NewtonStage& sm) {
     const int lane = threadIdx.x & 31;
     __syncwarp();
+    constexpr int kBack = kWorkChunks - (kRawChunk1 - kRawChunk0);  // chunks written back per record
 #pragma unroll 5
-    for (int j = 0; j < kWorkChunks; ++j) {
-        const int f = lane + 32 * j, c = f / kWorkChunks, k = f - c * kWorkChunks;
+    for (int j = 0; j < kBack; ++j) {
+        const int f = lane + 32 * j, c = f / kBack, kk = f - c * kBack;
+        const int k = kk < kRawChunk0 ? kk : kk + (kRawChunk1 - kRawChunk0);
         const int ic = __shfl_sync(0xffffffffu, i, c);
         if (ic >= 0)
             reinterpret_cast<uint4*>(a.work + ic)[k] = *reinterpret_cast<const uint4*>(sm.work + c * kWorkStride + 2 * k);
