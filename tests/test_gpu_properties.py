@@ -1,0 +1,101 @@
+"""Size-independent properties at BASELINE.json's full sizes, where the CPU oracle
+is too slow to run the whole case (it checks small samples of the same
+configurations elsewhere): linearity and shift covariance of the expansion on
+the alignment's whole shift grids, and the generate -> align -> recover round
+trip on the full 1024-particle batch of the metric configuration."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2509_01180_b200 import api
+
+pytestmark = pytest.mark.gpu
+
+
+def _shifted(v, s):
+    """shift_volume (src/volume.cpp:50-67) on the device: out[z, y, x] = v[z+sz, y+sy, x+sx],
+    zero where the source leaves the grid."""
+    n = v.shape[-1]
+    out = torch.zeros_like(v)
+    sx, sy, sz = s
+
+    def rng(d):
+        return (max(0, -d), min(n, n - d))
+
+    (x0, x1), (y0, y1), (z0, z1) = rng(sx), rng(sy), rng(sz)
+    out[z0:z1, y0:y1, x0:x1] = v[z0 + sz:z1 + sz, y0 + sy:y1 + sy, x0 + sx:x1 + sx]
+    return out
+
+
+def test_expansion_is_linear_on_a_config3_batch(cuda_device):
+    """expand(a u + b v) = a expand(u) + b expand(v) on 2048 volumes of config 3's
+    64^3 / L = 16 case (i.i.d. N(0,1) voxels): FP32 rounding only."""
+    n, L, count = 64, 16, 2048
+    ctx = api.Context(n, L, L * math.pi)
+    g = torch.Generator(device=cuda_device).manual_seed(31)
+    u = torch.randn((count, n, n, n), generator=g, device=cuda_device)
+    v = torch.randn((count, n, n, n), generator=g, device=cuda_device)
+    a, b = 0.75, -1.5
+    eu, ev = ctx.expand(u), ctx.expand(v)
+    ew = ctx.expand(a * u + b * v)
+    ref = a * eu + b * ev
+    err = torch.linalg.norm(ew - ref, dim=1) / torch.linalg.norm(ref, dim=1)
+    assert float(err.max()) < 5e-6, float(err.max())
+    assert float(torch.linalg.norm(eu, dim=1).min()) > 0  # non-trivial expansions
+
+
+@pytest.mark.parametrize("L", [16, 20])
+def test_window_expansions_equal_expansions_of_shifted_volumes(cuda_device, L):
+    """The shift search expands windows of a volume in place (padded quad copy,
+    x-neighbour windows sharing their loads).  Every window of the coarse grid
+    (radius 4, step 2) and of a fine cube must give exactly the bits of the plain
+    expansion of the explicitly shifted volume (same taps, same FP32 order), for
+    configs 2 (L = 16) and 5 (L = 20)."""
+    n = 64
+    ctx = api.Context(n, L, L * math.pi)
+    tmpl = api.make_template(n, 40, 7)
+    parts, _, _ = api.make_particles(tmpl, 2, 4100, 3, 0.1, 60.0)
+    coarse = [(x, y, z) for z in range(-4, 5, 2) for y in range(-4, 5, 2) for x in range(-4, 5, 2)]
+    fine = [(2 + x, -2 + y, 0 + z) for z in range(-2, 3) for y in range(-2, 3) for x in range(-2, 3)
+            if (x % 2, y % 2, z % 2) != (0, 0, 0)]
+    shifts = coarse + fine
+    win_vol = [0] * len(shifts) + [1] * len(shifts)
+    got = ctx.expand_windows(parts, win_vol, shifts + shifts)
+    ctx.set_expand_pairs(0)
+    for p in range(2):
+        vols = torch.stack([_shifted(parts[p], s) for s in shifts])
+        ref = ctx.expand(vols)
+        assert torch.equal(got[p * len(shifts):(p + 1) * len(shifts)], ref)
+
+
+def test_config2_round_trip_on_the_full_batch(cuda_device):
+    """Generate the metric configuration's 1024 particles from the template with known
+    rotations and shifts (SNR 0.1, +-60 degree wedge, shifts +-3), align them, and
+    recover the truth: the reference's acceptance criteria are statistical at this
+    noise level (tests/acceptance.cpp), so the bars are >= 90% exact shifts and a
+    median rotation error below 1 degree; every result must be finite and every
+    particle must have searched its 125 coarse and 98 to 117 fine windows."""
+    n, L, count = 64, 16, 1024
+    ctx = api.Context(n, L, L * math.pi)
+    tmpl = api.make_template(n, 40, 7)
+    ctx.set_template(tmpl, 60.0)
+    parts, q, sh = api.make_particles(tmpl, count, 1000, 3, 0.1, 60.0)
+    cfg = api.make_config(bands=(4, 8, 16), max_candidates=24, shift_radius=4, shift_step=2)
+    res = ctx.align_batch(parts, cfg)
+    assert len(res) == count
+    exact = sum(tuple(r["shift"]) == tuple(int(x) for x in sh[i]) for i, r in enumerate(res))
+    errs = []
+    for i, r in enumerate(res):
+        assert all(math.isfinite(x) for x in r["quat"]) and math.isfinite(r["score"])
+        assert abs(sum(x * x for x in r["quat"]) - 1.0) < 1e-9
+        assert 125 + 98 <= r["windows"] <= 125 + 117  # the fine cube minus the 8 to 27 coarse points inside it
+        d = min(1.0, abs(float(np.dot(r["quat"], q[i]))))
+        errs.append(math.degrees(2 * math.acos(d)))
+    assert exact >= 0.9 * count, exact
+    assert float(np.median(errs)) < 1.0, float(np.median(errs))
+    # the batch is deterministic: a second pass gives the same bits
+    again = ctx.align_batch(parts, cfg)
+    assert all(a["shift"] == b["shift"] and list(a["quat"]) == list(b["quat"]) and a["score"] == b["score"]
+               for a, b in zip(res, again))
