@@ -151,3 +151,31 @@ def test_config4_sweep_gradient_and_tensor_path_at_full_size(cuda_device):
         gscale = float(g.abs().max())
         # truncation h^2 |C'''| / 6 ~ 1e-6 L^2 relative, FP32 score noise / h ~ 1e-3 relative
         assert float((fd - g).abs().max()) <= 5e-3 * gscale, (axis, float((fd - g).abs().max()), gscale)
+
+
+def test_config5_average_is_additive_over_shards(cuda_device):
+    """Config 5's averaging step shards the particles over the GPUs and combines the
+    partial averages with one allreduce (a sum).  On one device: the FP64 average of a
+    batch equals the sum of the averages of its shards (the alignment of a particle
+    does not depend on the batch it is in), and it correlates with the template's own
+    expansion (the aligned particles add up coherently)."""
+    n, L, count = 64, 20, 96
+    ctx = api.Context(n, L, L * math.pi)
+    tmpl = api.make_template(n, 60, 20250905)
+    ctx.set_template(tmpl, 60.0)
+    parts, _, _ = api.make_particles(tmpl, count, 5000, 4, 0.05, 60.0)
+    cfg = api.make_config(bands=(4, 8, 16, 20), max_candidates=24, shift_radius=4, shift_step=2)
+    res = ctx.align_batch(parts, cfg)
+    whole = ctx.average_accumulate(parts, res)
+    shards = [(0, 40), (40, 41), (41, 96)]
+    total = torch.zeros_like(whole)
+    for a, b in shards:
+        r = ctx.align_batch(parts[a:b], cfg)
+        assert all(x["shift"] == y["shift"] and list(x["quat"]) == list(y["quat"]) for x, y in zip(r, res[a:b]))
+        total += ctx.average_accumulate(parts[a:b], r)
+    assert float(torch.linalg.norm(total - whole)) <= 1e-12 * float(torch.linalg.norm(whole))
+    t_hat = ctx.expand(tmpl[None])[0]
+    avg = torch.view_as_complex(whole.contiguous()) if whole.shape[-1] == 2 and not whole.is_complex() else whole
+    corr = abs(complex(torch.vdot(t_hat, avg.to(t_hat.dtype)))) / (
+        float(torch.linalg.norm(t_hat)) * float(torch.linalg.norm(avg)))
+    assert corr > 0.5, corr
