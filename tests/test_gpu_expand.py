@@ -168,3 +168,24 @@ def test_expand_tensor_dft_matches(cuda_device, n, L, pairs, monkeypatch):
         assert _rel_l2(tc[i], ref) < 1e-5
     many = ctx.expand(np.concatenate([vols] * 40), shifts * 40).cpu().numpy()
     assert np.array_equal(many[:7], tc) and np.array_equal(many[-7:], tc)  # deterministic across CTAs
+
+
+def test_expand_windows_edge_cases(cuda_device):
+    """bm_expand_windows: no windows, one window, a volume index out of range, and a
+    window list that skips a volume."""
+    n, L = 32, 8
+    ctx = api.Context(n, L, L * math.pi)
+    spec = bmo.Spec(L, L * math.pi)
+    t = bmo.gaussian_blob_template(n, 20, 5).astype(np.float32)
+    vols = np.stack([t, 2.0 * t, -t])
+    assert ctx.expand_windows(vols, [], np.zeros((0, 3), np.int32)).shape == (0, ctx.coeff_count)
+    one = ctx.expand_windows(vols, [1], [(1, -2, 0)]).cpu().numpy()
+    ref = bmo.expand(bmo.shift_volume(vols[1].astype(np.float64), (1, -2, 0)), spec)
+    assert _rel_l2(one[0], ref) < 1e-5
+    with pytest.raises(ValueError):
+        ctx.expand_windows(vols, [0, 3], [(0, 0, 0), (0, 0, 0)])
+    with pytest.raises(ValueError):
+        ctx.expand_windows(vols, [-1], [(0, 0, 0)])
+    skip = ctx.expand_windows(vols, [0, 0, 2, 2, 2], [(0, 0, 0), (2, 0, 0), (0, 0, 0), (1, 0, 0), (2, 0, 0)]).cpu().numpy()
+    assert np.array_equal(skip[2], -skip[0])  # linear in the volume, bit for bit for a sign flip
+    assert np.array_equal(skip[4], -skip[1])
